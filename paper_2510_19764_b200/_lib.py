@@ -1,0 +1,109 @@
+"""ctypes binding of the sm_100a C-ABI library (``include/sparsewire_b200.h``).
+
+There is no CPU fallback: importing the device layer without the built
+library, or calling it without a CUDA device, raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsparsewire_b200.so")
+MAX_PLANES = 8
+
+
+class Ragged(C.Structure):
+    """sw_ragged_t"""
+    _fields_ = [("num_pre", C.c_int32), ("num_post", C.c_int32),
+                ("max_row_length", C.c_int32), ("stride", C.c_int32),
+                ("row_length", C.c_void_p), ("target", C.c_void_p),
+                ("n_planes", C.c_int32), ("plane_bytes", C.c_int32 * MAX_PLANES),
+                ("planes", C.c_void_p * MAX_PLANES)]
+
+
+class BitfieldDesc(C.Structure):
+    """sw_bitfield_t"""
+    _fields_ = [("words", C.c_void_p), ("num_pre", C.c_int32), ("num_post", C.c_int32),
+                ("words_per_row", C.c_int32)]
+
+
+P = C.c_void_p
+I32 = C.c_int32
+I64 = C.c_int64
+U64 = C.c_uint64
+F64 = C.c_double
+F32 = C.c_float
+RP = C.POINTER(Ragged)
+BP = C.POINTER(BitfieldDesc)
+
+# name -> argtypes (restype is int status for all but sw_last_error)
+SIGNATURES: dict[str, list] = {
+    "sw_abi_version": [],
+    "sw_rng_selftest": [P, P],
+    "sw_rng_u64": [U64, U64, I64, P, P],
+    "sw_rng_uniform01": [U64, U64, I64, P, P],
+    "sw_rng_uniform_int_seq": [U64, U64, I64, P, P],
+    "sw_rng_child_keys": [U64, I64, P, P],
+    "sw_bitfield_randomize": [BP, U64, P],
+    "sw_ragged_remove_marked": [RP, P, P, P],
+    "sw_init_bernoulli_count": [I64, I32, U64, U64, I32, F64, P, I32, P, P, P],
+    "sw_init_bernoulli_fill": [I64, I32, U64, U64, I32, F64, P, I32, P, P, I32, P],
+    "sw_deepr_init_bitfields": [RP, I32, BP, BP, U64, P],
+    "sw_deepr_l1": [RP, I32, BP, F64, P],
+    "sw_deepr_eliminate": [RP, I32, BP, BP, P, P],
+    "sw_deepr_form_pass": [RP, BP, I32, P, U64, U64, P, P, P, P],
+    "sw_adam_f64": [P, P, P, P, I64, F64, F64, F64, F64, F64, F64, F64, F64, P],
+}
+
+_lib = None
+
+
+def lib():
+    """Load the library once; fail loudly when it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise errors.ExtensionMissing(
+            f"{LIB_PATH} not built: run `python -m paper_2510_19764_b200.build` "
+            "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    for name, argtypes in SIGNATURES.items():
+        fn = getattr(L, name)
+        fn.argtypes = argtypes
+        fn.restype = C.c_int
+    L.sw_last_error.argtypes = []
+    L.sw_last_error.restype = C.c_char_p
+    _lib = L
+    return L
+
+
+def require_cuda(t: torch.Tensor | None = None) -> None:
+    if not torch.cuda.is_available():
+        raise errors.DeviceUnavailable("a CUDA device is required (no CPU fallback)")
+    if t is not None and not t.is_cuda:
+        raise errors.DeviceUnavailable("tensor must live on the CUDA device")
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def call(name: str, *args) -> None:
+    """Invoke one entry point; map its status onto the reference exceptions."""
+    L = lib()
+    st = getattr(L, name)(*args)
+    if st != 0:
+        msg = (L.sw_last_error() or b"").decode(errors="replace")
+        raise errors.from_status(st, f"{name}: {msg}")
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()

@@ -1,0 +1,182 @@
+"""Device-resident padded ragged connectivity (the reference's
+``sparsewire/connectivity.py`` API, storage in HBM).
+
+``RaggedMatrix`` keeps ``row_length`` int32 [P] and ``target`` int32
+[P, max(cap, 1)] as CUDA tensors (connectivity.py:24-40); ``SynVarMatrix``
+keeps named slot-aligned planes, float64 by default (:65-88).  Structural
+changes happen inside the sm_100a kernels; ``version`` is bumped by the
+host layer after every mutating call (:38-40).
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Iterable
+
+import numpy as np
+import torch
+
+from . import _lib
+from .rng import CounterRng
+
+DEV = "cuda"
+
+
+class RaggedMatrix:
+    __slots__ = ("num_pre", "num_post", "max_row_length", "row_length", "target",
+                 "multapse_free", "version")
+
+    def __init__(self, num_pre: int, num_post: int, max_row_length: int,
+                 multapse_free: bool = True, device=DEV):
+        _lib.require_cuda()
+        self.num_pre = num_pre
+        self.num_post = num_post
+        self.max_row_length = max_row_length
+        self.row_length = torch.zeros(num_pre, dtype=torch.int32, device=device)
+        self.target = torch.zeros((num_pre, max(max_row_length, 1)), dtype=torch.int32,
+                                  device=device)
+        self.multapse_free = multapse_free
+        self.version = 0
+
+    @property
+    def stride(self) -> int:
+        return self.target.shape[1]
+
+    def edge_count(self) -> int:
+        return int(self.row_length.sum().item())
+
+    def row_targets(self, i: int) -> torch.Tensor:
+        return self.target[i, : int(self.row_length[i].item())]
+
+    def slot_mask(self) -> torch.Tensor:
+        return (torch.arange(self.stride, device=self.target.device)[None, :]
+                < self.row_length[:, None])
+
+    def contains(self, pre: int, post: int) -> bool:
+        return bool((self.row_targets(pre) == post).any().item())
+
+    def edge_list(self) -> tuple[np.ndarray, np.ndarray]:
+        lens = self.row_length.cpu().numpy().astype(np.int64)
+        pre = np.repeat(np.arange(self.num_pre, dtype=np.int64), lens)
+        post = self.target[self.slot_mask()].cpu().numpy().astype(np.int64)
+        return pre, post
+
+    # -- state transfer (reference-layout numpy arrays) ------------------------
+    def load_state(self, row_length: np.ndarray, target: np.ndarray) -> None:
+        """Inject host state (e.g. from a reference object) into HBM."""
+        self.row_length.copy_(torch.from_numpy(np.ascontiguousarray(row_length, dtype=np.int32)))
+        self.target.copy_(torch.from_numpy(np.ascontiguousarray(target, dtype=np.int32)))
+        self.version += 1
+
+    def host_state(self) -> dict[str, np.ndarray]:
+        return {"row_length": self.row_length.cpu().numpy(), "target": self.target.cpu().numpy()}
+
+
+class SynVarMatrix:
+    __slots__ = ("matrix", "planes")
+
+    def __init__(self, matrix: RaggedMatrix, names: Iterable[str] = ()):
+        self.matrix = matrix
+        self.planes: dict[str, torch.Tensor] = {}
+        for n in names:
+            self.add_plane(n)
+
+    def add_plane(self, name: str, dtype=torch.float64) -> torch.Tensor:
+        if name in self.planes:
+            raise KeyError(f"plane {name!r} already exists")
+        if len(self.planes) >= _lib.MAX_PLANES:
+            raise ValueError(f"at most {_lib.MAX_PLANES} planes per matrix")
+        if dtype not in (torch.float64, torch.float32, torch.int32, torch.int64):
+            raise TypeError("planes must be 4- or 8-byte types")
+        t = torch.zeros(self.matrix.target.shape, dtype=dtype, device=self.matrix.target.device)
+        self.planes[name] = t
+        return t
+
+    def plane(self, name: str) -> torch.Tensor:
+        return self.planes[name]
+
+    def row(self, name: str, i: int) -> torch.Tensor:
+        return self.planes[name][i, : int(self.matrix.row_length[i].item())]
+
+    def plane_index(self, name: str) -> int:
+        return list(self.planes).index(name)
+
+
+def descriptor(m: RaggedMatrix, syn: SynVarMatrix | None) -> _lib.Ragged:
+    d = _lib.Ragged()
+    d.num_pre, d.num_post = m.num_pre, m.num_post
+    d.max_row_length, d.stride = m.max_row_length, m.stride
+    d.row_length, d.target = m.row_length.data_ptr(), m.target.data_ptr()
+    planes = list(syn.planes.values()) if syn is not None else []
+    d.n_planes = len(planes)
+    for k, t in enumerate(planes):
+        if not t.is_contiguous() or t.shape != m.target.shape:
+            raise ValueError("planes must be contiguous [num_pre, stride]")
+        d.plane_bytes[k] = t.element_size()
+        d.planes[k] = t.data_ptr()
+    return d
+
+
+def remove_marked(m: RaggedMatrix, syn: SynVarMatrix | None, marked: torch.Tensor,
+                  removed: torch.Tensor | None = None) -> None:
+    """Remove every marked slot of every row with the exact ``remove_slots``
+    order (connectivity.py:130-136), all rows in one launch."""
+    if marked.dtype != torch.uint8 or marked.shape != m.target.shape:
+        raise ValueError("marked must be uint8 [num_pre, stride]")
+    d = descriptor(m, syn)
+    _lib.call("sw_ragged_remove_marked", C_ref(d), marked.data_ptr(), _lib.ptr(removed),
+              _lib.stream_ptr())
+    m.version += 1
+
+
+def C_ref(d):
+    import ctypes
+    return ctypes.byref(d)
+
+
+def _init_rows(num_pre, num_post, key, counter0, mode, density, lut, side, headroom,
+               multapse_free, names, cap=None):
+    _lib.require_cuda()
+    st = _lib.stream_ptr()
+    rl = torch.zeros(num_pre, dtype=torch.int32, device=DEV)
+    mx = torch.zeros(1, dtype=torch.int32, device=DEV)
+    lut_t = None if lut is None else torch.as_tensor(np.ascontiguousarray(lut, dtype=np.float64),
+                                                     device=DEV)
+    _lib.call("sw_init_bernoulli_count", num_pre, num_post, key, counter0, mode, float(density),
+              _lib.ptr(lut_t), side, rl.data_ptr(), mx.data_ptr(), st)
+    if cap is None:
+        cap = math.ceil(headroom * int(mx.item()))
+        if multapse_free:
+            cap = min(cap, num_post)
+    m = RaggedMatrix(num_pre, num_post, cap, multapse_free)
+    _lib.call("sw_init_bernoulli_fill", num_pre, num_post, key, counter0, mode, float(density),
+              _lib.ptr(lut_t), side, m.row_length.data_ptr(), m.target.data_ptr(), m.stride, st)
+    m.version += 1
+    return m, SynVarMatrix(m, names)
+
+
+def init_pairwise_bernoulli_density(num_pre: int, num_post: int, density: float,
+                                    capacity_headroom: float, rng: CounterRng,
+                                    var_names=(), exclude_diagonal: bool = False,
+                                    multapse_free: bool = True, capacity: int | None = None):
+    """``init_pairwise_bernoulli`` with p(i, j) = density (0 on the diagonal
+    when excluded), drawn on the device with the reference's counters
+    (connectivity.py:231-236).  Advances ``rng`` past the P*N draws."""
+    if capacity_headroom < 1.0:
+        raise ValueError("capacity_headroom must be >= 1")
+    out = _init_rows(num_pre, num_post, rng.key, rng.counter, 1 if exclude_diagonal else 0,
+                     density, None, 1, capacity_headroom, multapse_free, var_names, capacity)
+    rng.counter += num_pre * num_post
+    return out
+
+
+def init_pairwise_bernoulli_torus(side: int, offset_prob: np.ndarray, capacity_headroom: float,
+                                  rng: CounterRng, var_names=(), multapse_free: bool = True):
+    """``init_pairwise_bernoulli`` on a side x side torus where p depends on
+    the wrapped offset only (topomap.py:376-388).  ``offset_prob[dx + side*dy]``
+    must be computed by host numpy (exp/hypot)."""
+    n = side * side
+    out = _init_rows(n, n, rng.key, rng.counter, 2, 0.0, offset_prob, side, capacity_headroom,
+                     multapse_free, var_names)
+    rng.counter += n * n
+    return out

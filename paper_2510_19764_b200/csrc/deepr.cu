@@ -1,0 +1,410 @@
+// DEEP R on the padded ragged layout: bitfield init, L1 nudge, eliminate,
+// form (device histogram of the host draws + warp-batched row placement).
+// Reference: sparsewire/deep_r.py:23-177, bitfield.py:19-96,
+// connectivity.py:91-136, updates.py:309-372.
+#include "common.cuh"
+#include "ragged.cuh"
+
+namespace {
+
+constexpr int kWarps = 8;            // warps per block for warp-per-row kernels
+constexpr int kThreads = kWarps * 32;
+
+int rows_grid(int64_t rows) {
+  int64_t g = (rows + kWarps - 1) / kWarps;
+  const int64_t cap = 148 * 64;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+int flat_grid(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  const int64_t cap = 148 * 32;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+__device__ __forceinline__ bool bit_of(const uint64_t* row, int j) {
+  return (row[j >> 6] >> (j & 63)) & 1ull;
+}
+
+// ---- Bitfield.randomize (bitfield.py:92-96) ----------------------------------
+__global__ void k_bf_randomize(sw_bitfield_t bf, uint64_t key, uint64_t tail_mask) {
+  const int64_t total = (int64_t)bf.num_pre * bf.words_per_row;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t v = sw::draw(key, (uint64_t)x);
+    if ((int)(x % bf.words_per_row) == bf.words_per_row - 1) v &= tail_mask;
+    bf.words[x] = v;
+  }
+}
+
+// conn bits := edges; sign bit set for w > 0, cleared for w < 0 (deep_r.py:56-64)
+__global__ void k_deepr_init_bits(sw_ragged_t m, int wp, sw_bitfield_t sign, sw_bitfield_t conn) {
+  const int64_t total = (int64_t)m.num_pre * m.stride;
+  const double* w = (const double*)m.planes[wp];
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = x / m.stride;
+    const int s = (int)(x - i * m.stride);
+    if (s >= m.row_length[i]) continue;
+    const int j = m.target[x];
+    const uint64_t bit = 1ull << (j & 63);
+    atomicOr((unsigned long long*)&conn.words[i * conn.words_per_row + (j >> 6)], bit);
+    const double wv = w[x];
+    if (wv > 0.0)
+      atomicOr((unsigned long long*)&sign.words[i * sign.words_per_row + (j >> 6)], bit);
+    else if (wv < 0.0)
+      atomicAnd((unsigned long long*)&sign.words[i * sign.words_per_row + (j >> 6)], ~bit);
+  }
+}
+
+// ---- l1_step (deep_r.py:68-77) -------------------------------------------------
+__global__ void k_deepr_l1(sw_ragged_t m, int gp, sw_bitfield_t sign, double l1) {
+  const int64_t total = (int64_t)m.num_pre * m.stride;
+  double* g = (double*)m.planes[gp];
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = x / m.stride;
+    const int s = (int)(x - i * m.stride);
+    if (s >= m.row_length[i]) continue;   // padding gets +-0.0 in the reference: no-op
+    const int j = m.target[x];
+    const bool pos = bit_of(sign.words + i * sign.words_per_row, j);
+    g[x] = __dadd_rn(g[x], pos ? l1 : -l1);
+  }
+}
+
+// ---- eliminate (deep_r.py:81-99) --------------------------------------------------
+// Warp per row.  Mismatch scan (4x unrolled for memory-level parallelism),
+// ascending marked-slot list in shared memory, conn-bit clears, then the exact
+// chained-removal gather.
+__global__ void __launch_bounds__(kThreads)
+k_deepr_eliminate(sw_ragged_t m, int wp, sw_bitfield_t sign, sw_bitfield_t conn, int64_t* dormant) {
+  extern __shared__ int s_lists[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* list = s_lists + warp * m.stride;
+  const double* w = (const double*)m.planes[wp];
+  const unsigned lt = sw::lanemask_lt();
+  for (int64_t i = (int64_t)blockIdx.x * kWarps + warp; i < m.num_pre;
+       i += (int64_t)gridDim.x * kWarps) {
+    const int n = m.row_length[i];
+    const int64_t off = i * (int64_t)m.stride;
+    const uint64_t* srow = sign.words + i * sign.words_per_row;
+    uint64_t* crow = conn.words + i * conn.words_per_row;
+    int k = 0;
+    for (int base = 0; base < n; base += 128) {
+      int t[4];
+      double wv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int s = base + u * 32 + lane;
+        t[u] = 0;
+        wv[u] = 0.0;
+        if (s < n) { t[u] = __ldg(m.target + off + s); wv[u] = __ldg(w + off + s); }
+      }
+      uint64_t sw_[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int s = base + u * 32 + lane;
+        sw_[u] = (s < n && wv[u] != 0.0) ? __ldg(srow + (t[u] >> 6)) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int s = base + u * 32 + lane;
+        const bool bit = (sw_[u] >> (t[u] & 63)) & 1ull;
+        const bool mis = (s < n) && ((wv[u] < 0.0 && bit) || (wv[u] > 0.0 && !bit));
+        if (mis)
+          atomicAnd((unsigned long long*)&crow[t[u] >> 6], ~(1ull << (t[u] & 63)));
+        const unsigned b = __ballot_sync(SW_FULL_MASK, mis);
+        if (mis) list[k + __popc(b & lt)] = s;
+        k += __popc(b);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) dormant[i] = k;
+    if (k > 0) {
+      sw::warp_apply_removal(m, off, list, n, k);
+      if (lane == 0) m.row_length[i] = n - k;
+    }
+    __syncwarp();
+  }
+}
+
+// generic removal of caller-marked slots (remove_slots semantics)
+__global__ void __launch_bounds__(kThreads)
+k_remove_marked(sw_ragged_t m, const uint8_t* marked, int64_t* removed) {
+  extern __shared__ int s_lists[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* list = s_lists + warp * m.stride;
+  const unsigned lt = sw::lanemask_lt();
+  for (int64_t i = (int64_t)blockIdx.x * kWarps + warp; i < m.num_pre;
+       i += (int64_t)gridDim.x * kWarps) {
+    const int n = m.row_length[i];
+    const int64_t off = i * (int64_t)m.stride;
+    int k = 0;
+    for (int base = 0; base < n; base += 32) {
+      const int s = base + lane;
+      const bool mk = s < n && marked[off + s];
+      const unsigned b = __ballot_sync(SW_FULL_MASK, mk);
+      if (mk) list[k + __popc(b & lt)] = s;
+      k += __popc(b);
+    }
+    __syncwarp();
+    if (removed && lane == 0) removed[i] = k;
+    if (k > 0) {
+      sw::warp_apply_removal(m, off, list, n, k);
+      if (lane == 0) m.row_length[i] = n - k;
+    }
+    __syncwarp();
+  }
+}
+
+// ---- form: host-phase draws as a device histogram (deep_r.py:110-121) --------------
+__global__ void k_sum_i64(const int64_t* x, int64_t n, int64_t* out) {
+  int64_t acc = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc += x[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(SW_FULL_MASK, acc, o);
+  __shared__ int64_t part[32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = (threadIdx.x < (blockDim.x >> 5)) ? part[threadIdx.x] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(SW_FULL_MASK, acc, o);
+    if (threadIdx.x == 0 && acc) atomicAdd((unsigned long long*)out, (unsigned long long)acc);
+  }
+}
+
+// D draws of uniform_int(num_pre) on the host stream: draw c lands in row
+// h mod P when valid.  Invalid (rejected) counters are counted; the serial
+// fix-up kernel then continues from counter D until D valid draws exist.
+__global__ void k_form_hist(int64_t* counters, uint64_t key, uint64_t P, uint64_t rem,
+                            int32_t* act) {
+  const int64_t D = counters[0];
+  const bool pow2 = (P & (P - 1)) == 0;
+  int64_t rej = 0;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < D;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = sw::draw(key, (uint64_t)c);
+    if (sw::draw_valid(h, rem)) {
+      const uint64_t r = pow2 ? (h & (P - 1)) : (h % P);
+      atomicAdd(act + r, 1);
+    } else {
+      ++rej;
+    }
+  }
+  if (rej) atomicAdd((unsigned long long*)&counters[2], (unsigned long long)rej);
+}
+
+__global__ void k_form_hist_fix(int64_t* counters, uint64_t key, uint64_t P, uint64_t rem,
+                                int32_t* act) {
+  int64_t need = counters[2];
+  uint64_t c = (uint64_t)counters[0];
+  while (need > 0) {
+    const uint64_t h = sw::draw(key, c++);
+    if (sw::draw_valid(h, rem)) { act[h % P] += 1; --need; }
+  }
+}
+
+// ---- form: row phase (deep_r.py:126-145) ------------------------------
+// Warp per row.  Lane l evaluates draw #(ctr + l) of the row stream; the
+// reference's sequential inner loop is replayed exactly over the 32 lanes:
+// valid draws are iterations, a candidate is placed unless an earlier lane
+// of the batch already placed the same post (match_any), the failure streak
+// resets per activation and ends it after num_post misses, a full row stops
+// all remaining activations without consuming draws.
+__global__ void __launch_bounds__(kThreads)
+k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row_base,
+                  const int32_t* act, int64_t* unplaced, int64_t* counters) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = sw::lanemask_lt();
+  const int N = m.num_post;
+  const uint64_t rem = sw::reject_rem((uint64_t)N);
+  const bool pow2 = (N & (N - 1)) == 0;
+  const int cap = m.max_row_length;
+  for (int64_t i = (int64_t)blockIdx.x * kWarps + warp; i < m.num_pre;
+       i += (int64_t)gridDim.x * kWarps) {
+    const int acts = act[i];
+    if (acts == 0) {
+      if (lane == 0) unplaced[i] = 0;
+      continue;
+    }
+    const int64_t off = i * (int64_t)m.stride;
+    uint64_t* crow = conn.words + i * conn.words_per_row;
+    const uint64_t key = sw::child_key(row_base, (uint64_t)i);
+    uint64_t ctr = 0;
+    int len = m.row_length[i];
+    int a = 0, streak = 0, unpl = 0;
+    while (a < acts) {
+      if (len >= cap) { unpl += acts - a; break; }
+      const uint64_t h = sw::draw(key, ctr + lane);
+      const bool valid = sw::draw_valid(h, rem);
+      const int j = (int)(pow2 ? (h & (uint64_t)(N - 1)) : (h % (uint64_t)N));
+      bool cand = valid && !(excl_diag && j == (int)i);
+      if (cand) cand = !((__ldcg(crow + (j >> 6)) >> (j & 63)) & 1ull);
+      const unsigned peers = __match_any_sync(SW_FULL_MASK, cand ? j : (N + lane));
+      const bool first = cand && !(peers & lt);
+      const unsigned vmask = __ballot_sync(SW_FULL_MASK, valid);
+      const unsigned fmask = __ballot_sync(SW_FULL_MASK, first);
+      unsigned placed;
+      int consumed;   // lanes (counters) consumed by this batch
+      if (streak + 32 < N) {
+        // fast path: no activation can exhaust its num_post iterations here
+        const int need = min(acts - a, cap - len);
+        const int nf = __popc(fmask);
+        if (nf <= need) {
+          placed = fmask;
+          consumed = 32;
+          a += nf;
+          len += nf;
+          if (fmask) {
+            const int hi = 31 - __clz(fmask);
+            const unsigned above = (hi == 31) ? 0u : (~0u << (hi + 1));
+            streak = __popc(vmask & ~fmask & above);
+          } else {
+            streak += __popc(vmask);
+          }
+        } else {
+          // lane of the need-th placement
+          unsigned f = fmask;
+          for (int q = 1; q < need; ++q) f &= f - 1;
+          const int L = __ffs(f) - 1;
+          placed = fmask & ((L == 31) ? ~0u : ((2u << L) - 1u));
+          consumed = L + 1;
+          a += need;
+          len += need;
+          streak = 0;
+        }
+      } else {
+        // exact serial walk over the lanes (small num_post)
+        placed = 0u;
+        consumed = 32;
+        unsigned vm = vmask;
+        while (vm) {
+          const int l = __ffs(vm) - 1;
+          vm &= vm - 1;
+          if ((fmask >> l) & 1u) {
+            placed |= 1u << l;
+            ++a; ++len; streak = 0;
+            if (a == acts || len == cap) { consumed = l + 1; break; }
+          } else {
+            if (++streak == N) {
+              ++unpl; ++a; streak = 0;
+              if (a == acts) { consumed = l + 1; break; }
+            }
+          }
+        }
+      }
+      if ((placed >> lane) & 1u) {
+        const int slot = len - __popc(placed) + __popc(placed & lt);
+        m.target[off + slot] = j;
+        sw::zero_slot(m, off, slot);
+        atomicOr((unsigned long long*)(crow + (j >> 6)), 1ull << (j & 63));
+      }
+      ctr += (uint64_t)consumed;
+      __syncwarp();
+    }
+    if (lane == 0) {
+      m.row_length[i] = len;
+      unplaced[i] = unpl;
+      if (unpl) atomicAdd((unsigned long long*)&counters[1], (unsigned long long)unpl);
+    }
+  }
+}
+
+int elim_smem(const sw_ragged_t* m) { return kWarps * m->stride * (int)sizeof(int); }
+
+int check_ragged(const sw_ragged_t* m, const char* where) {
+  if (!m || m->num_pre < 0 || m->stride < 1 || m->n_planes < 0 || m->n_planes > SW_MAX_PLANES) {
+    sw::set_last_error(where);
+    return SW_ERR_INVALID_ARG;
+  }
+  return SW_OK;
+}
+
+}  // namespace
+
+extern "C" int sw_bitfield_randomize(const sw_bitfield_t* bf, uint64_t key, void* stream) {
+  const int tail = bf->num_post - (bf->words_per_row - 1) * 64;
+  const uint64_t mask = tail >= 64 ? ~0ull : ((1ull << tail) - 1ull);
+  const int64_t total = (int64_t)bf->num_pre * bf->words_per_row;
+  if (total == 0) return SW_OK;
+  k_bf_randomize<<<flat_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(*bf, key, mask);
+  SW_CHECK_LAUNCH("sw_bitfield_randomize");
+  return SW_OK;
+}
+
+extern "C" int sw_deepr_init_bitfields(const sw_ragged_t* m, int32_t wp, const sw_bitfield_t* sign,
+                                       const sw_bitfield_t* conn, uint64_t sign_key, void* stream) {
+  if (int s = check_ragged(m, "sw_deepr_init_bitfields: bad matrix")) return s;
+  int s = sw_bitfield_randomize(sign, sign_key, stream);
+  if (s) return s;
+  cudaMemsetAsync(conn->words, 0, (size_t)conn->num_pre * conn->words_per_row * 8, (cudaStream_t)stream);
+  const int64_t total = (int64_t)m->num_pre * m->stride;
+  if (total == 0) return SW_OK;
+  k_deepr_init_bits<<<flat_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(*m, wp, *sign, *conn);
+  SW_CHECK_LAUNCH("sw_deepr_init_bitfields");
+  return SW_OK;
+}
+
+extern "C" int sw_deepr_l1(const sw_ragged_t* m, int32_t gp, const sw_bitfield_t* sign, double l1,
+                           void* stream) {
+  if (int s = check_ragged(m, "sw_deepr_l1: bad matrix")) return s;
+  if (l1 == 0.0) return SW_OK;   // deep_r.py:74-75
+  const int64_t total = (int64_t)m->num_pre * m->stride;
+  if (total == 0) return SW_OK;
+  k_deepr_l1<<<flat_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(*m, gp, *sign, l1);
+  SW_CHECK_LAUNCH("sw_deepr_l1");
+  return SW_OK;
+}
+
+static int set_smem(const void* fn, int bytes) {
+  if (bytes > 48 * 1024) {
+    if (bytes > 227 * 1024) { sw::set_last_error("row capacity too large for shared-memory slot lists"); return SW_ERR_INVALID_ARG; }
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  }
+  return SW_OK;
+}
+
+extern "C" int sw_deepr_eliminate(const sw_ragged_t* m, int32_t wp, const sw_bitfield_t* sign,
+                                  const sw_bitfield_t* conn, int64_t* dormant, void* stream) {
+  if (int s = check_ragged(m, "sw_deepr_eliminate: bad matrix")) return s;
+  if (m->num_pre == 0) return SW_OK;
+  const int smem = elim_smem(m);
+  if (int s = set_smem((const void*)k_deepr_eliminate, smem)) return s;
+  k_deepr_eliminate<<<rows_grid(m->num_pre), kThreads, smem, (cudaStream_t)stream>>>(*m, wp, *sign, *conn, dormant);
+  SW_CHECK_LAUNCH("sw_deepr_eliminate");
+  return SW_OK;
+}
+
+extern "C" int sw_ragged_remove_marked(const sw_ragged_t* m, const uint8_t* marked, int64_t* removed,
+                                       void* stream) {
+  if (int s = check_ragged(m, "sw_ragged_remove_marked: bad matrix")) return s;
+  if (m->num_pre == 0) return SW_OK;
+  const int smem = elim_smem(m);
+  if (int s = set_smem((const void*)k_remove_marked, smem)) return s;
+  k_remove_marked<<<rows_grid(m->num_pre), kThreads, smem, (cudaStream_t)stream>>>(*m, marked, removed);
+  SW_CHECK_LAUNCH("sw_ragged_remove_marked");
+  return SW_OK;
+}
+
+extern "C" int sw_deepr_form_pass(const sw_ragged_t* m, const sw_bitfield_t* conn, int32_t excl_diag,
+                                  const int64_t* pending_src, uint64_t host_key, uint64_t row_base,
+                                  int32_t* act, int64_t* unplaced, int64_t* counters, void* stream) {
+  if (int s = check_ragged(m, "sw_deepr_form_pass: bad matrix")) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t P = m->num_pre;
+  cudaMemsetAsync(counters, 0, 4 * sizeof(int64_t), st);
+  if (P == 0) return SW_OK;
+  cudaMemsetAsync(act, 0, (size_t)P * sizeof(int32_t), st);
+  k_sum_i64<<<flat_grid(P, 256), 256, 0, st>>>(pending_src, P, counters);
+  const uint64_t rem = sw::reject_rem((uint64_t)P);
+  k_form_hist<<<148 * 8, 256, 0, st>>>(counters, host_key, (uint64_t)P, rem, act);
+  if (rem != 0) k_form_hist_fix<<<1, 1, 0, st>>>(counters, host_key, (uint64_t)P, rem, act);
+  k_deepr_form_rows<<<rows_grid(P), kThreads, 0, st>>>(*m, *conn, excl_diag, row_base, act, unplaced, counters);
+  SW_CHECK_LAUNCH("sw_deepr_form_pass");
+  return SW_OK;
+}

@@ -1,0 +1,71 @@
+// Warp-per-row helpers on the padded ragged layout (connectivity.py:24-136).
+#pragma once
+#include "common.cuh"
+
+namespace sw {
+
+struct RowView {
+  int32_t* target;   // target + i*stride
+  int64_t off;       // i*stride, for the planes
+};
+
+// Move slot src -> dst in target and every plane (connectivity.py:121-125).
+__device__ __forceinline__ void move_slot(const sw_ragged_t& m, int64_t off, int dst, int src) {
+  m.target[off + dst] = m.target[off + src];
+#pragma unroll 1
+  for (int p = 0; p < m.n_planes; ++p) {
+    if (m.plane_bytes[p] == 8) {
+      uint64_t* pl = (uint64_t*)m.planes[p];
+      pl[off + dst] = pl[off + src];
+    } else {
+      uint32_t* pl = (uint32_t*)m.planes[p];
+      pl[off + dst] = pl[off + src];
+    }
+  }
+}
+
+// Zero every plane at one slot (add_synapse, connectivity.py:103-105).
+__device__ __forceinline__ void zero_slot(const sw_ragged_t& m, int64_t off, int s) {
+#pragma unroll 1
+  for (int p = 0; p < m.n_planes; ++p) {
+    if (m.plane_bytes[p] == 8) ((uint64_t*)m.planes[p])[off + s] = 0ull;
+    else ((uint32_t*)m.planes[p])[off + s] = 0u;
+  }
+}
+
+// Exact remove_slots permutation (connectivity.py:130-136).
+// list[0..k) holds the marked slots of a row of length n in ASCENDING order.
+// The t-th largest marked slot m_t (t = 1..k) that lies below n2 = n - k
+// receives the content of resolve(n - t), where resolve(p) follows
+// p -> n - rank(p) while p is itself marked.  All sources are >= n2 and all
+// destinations < n2, so the gathers are independent and run lane-parallel.
+// Padding beyond n2 is left unspecified (the reference leaves stale values).
+__device__ __forceinline__ void warp_apply_removal(const sw_ragged_t& m, int64_t off,
+                                                   const int* list, int n, int k) {
+  const int lane = threadIdx.x & 31;
+  const int n2 = n - k;
+  for (int t0 = 1; t0 <= k; t0 += 32) {
+    const int t = t0 + lane;
+    if (t <= k) {
+      const int mt = list[k - t];
+      if (mt < n2) {
+        int p = n - t;
+        while (true) {
+          // binary search p among marked slots (list ascending)
+          int lo = 0, hi = k - 1, q = -1;
+          while (lo <= hi) {
+            int mid = (lo + hi) >> 1;
+            int v = list[mid];
+            if (v == p) { q = mid; break; }
+            if (v < p) lo = mid + 1; else hi = mid - 1;
+          }
+          if (q < 0) break;
+          p = n - (k - q);   // rank(list[q]) = k - q
+        }
+        move_slot(m, off, mt, p);
+      }
+    }
+  }
+}
+
+}  // namespace sw

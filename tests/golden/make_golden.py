@@ -1,0 +1,240 @@
+"""Generate golden vectors by running the REAL reference (sparsewire 0.1.0).
+
+Run in the build container only (the reference is not on the GPU box):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONPATH=/root/reference/pkg/src \
+        python tests/golden/make_golden.py
+
+Writes small ``*.npz`` fixtures next to this script.  The oracle
+(``oracle/``) is checked against them by ``tests/test_oracle_golden.py`` and
+the CUDA path by ``tests/test_gpu_*.py``.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+
+from sparsewire import rng as R  # noqa: E402
+from sparsewire.connectivity import (RaggedMatrix, SynVarMatrix,  # noqa: E402
+                                     init_pairwise_bernoulli, remove_slots,
+                                     TransposeMap, propagate_spikes)
+from sparsewire.deep_r import DeepR  # noqa: E402
+from sparsewire.updates import Model  # noqa: E402
+from sparsewire.plasticity import Adam  # noqa: E402
+from sparsewire.neurons import AlifLayer, AlifParams  # noqa: E402
+from sparsewire._kernels import eprop_accumulate_batch  # noqa: E402
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from golden_cases import DEEPR_CASES  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PLANES = ("w", "grad", "adam_m", "adam_v")
+
+
+def save(name, **arrays):
+    np.savez_compressed(os.path.join(HERE, name), **arrays)
+    print("wrote", name, sum(a.nbytes for a in arrays.values()), "bytes")
+
+
+def gen_rng():
+    keys_parts = [(0,), (1,), (1, "host", 3, 7, 0), (42, "row", 0, 0, 1),
+                  ("task", "example", 5), (2**64 - 1, -1, "päß-unicode-longer-than-8"),
+                  (7, "init", "ff")]
+    fold = np.array([R.fold_key(*p) for p in keys_parts], dtype=np.uint64)
+    mix_in = np.array([0, 1, 0x9E3779B97F4A7C15, 12345, 2**63, 2**64 - 1], dtype=np.uint64)
+    mix_out = np.array([R.mix64(int(x)) for x in mix_in], dtype=np.uint64)
+    key = R.fold_key(9, "golden")
+    rng = R.CounterRng(9, "golden")
+    draws = rng.u64_array(4096)
+    u01 = R.CounterRng(9, "golden").uniform01_array(4096)
+    # uniform_int sequences for several n, including non powers of two
+    ns = np.array([1, 2, 3, 7, 256, 700, 1000, 65536, 2**20, 3 * 2**40 + 1], dtype=np.uint64)
+    ui = []
+    for n in ns:
+        r = R.CounterRng(9, "uint", int(n))
+        ui.append([r.uniform_int(int(n)) for _ in range(512)] + [r.counter])
+    ui = np.array(ui, dtype=np.uint64)
+    child = np.array([R.CounterRng.from_key(key).child_key(i) for i in range(300)], dtype=np.uint64)
+    # sample_k_distinct: rejection and Fisher-Yates branches
+    skd_cases = [(3, 100), (10, 256), (5, 8), (8, 8), (40, 64), (1, 1), (0, 5)]
+    skd = []
+    for (k, n) in skd_cases:
+        r = R.CounterRng(9, "skd", k, n)
+        out = r.sample_k_distinct(k, n)
+        skd.append(np.concatenate([out, [r.counter]]).astype(np.int64))
+    save("rng.npz", fold=fold, mix_in=mix_in, mix_out=mix_out, key=np.uint64(key),
+         draws=draws, u01=u01, ns=ns, ui=ui, child=child,
+         skd_cases=np.array(skd_cases, dtype=np.int64),
+         skd=np.array([np.pad(s, (0, 64 - s.size), constant_values=-1) for s in skd]))
+
+
+def gen_remove():
+    rng = np.random.default_rng(5)
+    rows = []
+    for _ in range(400):
+        n = int(rng.integers(1, 90))
+        k = int(rng.integers(0, n + 1))
+        marked = np.sort(rng.choice(n, size=k, replace=False))
+        m = RaggedMatrix(1, 10_000, 96)
+        syn = SynVarMatrix(m, ("w",))
+        m.target[0, :n] = np.arange(n) + 1000
+        syn.planes["w"][0, :n] = np.arange(n) * 0.5
+        m.row_length[0] = n
+        remove_slots(m, syn, 0, marked)
+        out = np.full(96, -1, dtype=np.int32)
+        out[: m.row_length[0]] = m.target[0, : m.row_length[0]] - 1000
+        mk = np.full(96, -1, dtype=np.int32)
+        mk[:k] = marked
+        rows.append((n, k, mk, out))
+    save("remove.npz", n=np.array([r[0] for r in rows]), k=np.array([r[1] for r in rows]),
+         marked=np.stack([r[2] for r in rows]), result=np.stack([r[3] for r in rows]))
+
+
+def deep_r_build(num_pre, num_post, density, seed, l1, exclude_diagonal, headroom):
+    """Mirrors pkg/tests/test_deep_r.py:16-37."""
+    model = Model(seed)
+    rng = R.CounterRng(seed, "init")
+
+    def prob(i, cols):
+        p = np.full(cols.size, density)
+        if exclude_diagonal:
+            p[i] = 0.0
+        return p
+
+    m, syn = init_pairwise_bernoulli(num_pre, num_post, prob, headroom, rng, var_names=PLANES)
+    mask = m.slot_mask()
+    w = syn.planes["w"]
+    w[mask] = rng.normal_array(w.size).reshape(w.shape)[mask] * 0.1
+    model.add_matrix("sg", m, syn)
+    dr = DeepR(m, syn, "sg", l1_strength=l1, exclude_diagonal=exclude_diagonal)
+    dr.init_bitfields(R.CounterRng(seed, "bits"))
+    dr.register(model, "deep_r", "sg")
+    return model, m, syn, dr
+
+
+def snap(m, syn, dr):
+    return dict(row_length=m.row_length.copy(), target=m.target.copy(),
+                w=syn.planes["w"].copy(), grad=syn.planes["grad"].copy(),
+                adam_m=syn.planes["adam_m"].copy(), adam_v=syn.planes["adam_v"].copy(),
+                sign=dr.sign_bits.words.copy(), conn=dr.conn_bits.words.copy(),
+                dormant=dr.dormant.copy(), last_removed=np.int64(dr.last_removed))
+
+
+
+
+def gen_deep_r():
+    """Per case: initial state; then per cycle: new weights (flip injection),
+    l1 + group run, post state.  Mirrors test_deep_r.py:178-197."""
+    for (name, P, N, dens, seed, diag, head, cycles) in DEEPR_CASES:
+        model, m, syn, dr = deep_r_build(P, N, dens, seed, 0.005, diag, head)
+        out = {f"init_{k}": v for k, v in snap(m, syn, dr).items()}
+        out["meta"] = np.array([P, N, m.max_row_length, int(diag), cycles, seed], dtype=np.int64)
+        flip = R.CounterRng(99, name)
+        for c in range(cycles):
+            w = syn.planes["w"]
+            mask = m.slot_mask()
+            scale = 0.1 if c % 2 == 0 else 1.0
+            w[mask] = flip.normal_array(w.size).reshape(w.shape)[mask] * scale
+            syn.planes["grad"][mask] = flip.normal_array(w.size).reshape(w.shape)[mask] * 0.01
+            out[f"c{c}_w_in"] = w.copy()
+            out[f"c{c}_grad_in"] = syn.planes["grad"].copy()
+            dr.l1_step()
+            out[f"c{c}_grad_l1"] = syn.planes["grad"].copy()
+            model.run_update_group("deep_r")
+            for k, v in snap(m, syn, dr).items():
+                out[f"c{c}_{k}"] = v
+        save(f"deepr_{name}.npz", **out)
+
+
+def gen_adam():
+    rng = R.CounterRng(5, "adam")
+    shape = (37, 19)
+    p = rng.normal_array(37 * 19).reshape(shape)
+    m = np.zeros(shape)
+    v = np.zeros(shape)
+    out = {"p0": p.copy()}
+    adam = Adam(1e-3, m=m, v=v)
+    for t in range(5):
+        g = rng.normal_array(37 * 19).reshape(shape) * (10.0 ** (-t))
+        out[f"g{t}"] = g.copy()
+        adam.apply(p, g)
+        out[f"p{t + 1}"] = p.copy()
+        out[f"m{t + 1}"] = m.copy()
+        out[f"v{t + 1}"] = v.copy()
+    save("adam.npz", **out)
+
+
+def gen_alif_eprop():
+    """ALIF step/surrogate (float32, neurons.py:60-73) and the numba e-prop
+    kernel (_kernels.py:15-39) over several steps with ragged rows."""
+    prm = AlifParams()
+    rng = R.CounterRng(6, "alif")
+    B, H = 8, 48
+    layer = AlifLayer(H, prm, batch=B, dtype=np.float32)
+    out = {}
+    for t in range(6):
+        rec = (rng.normal_array(B * H).reshape(B, H) * 0.4).astype(np.float32)
+        ext = (rng.normal_array(B * H).reshape(B, H) * 0.4).astype(np.float32)
+        out[f"rec{t}"], out[f"ext{t}"] = rec, ext
+        out[f"psi{t}"] = layer.surrogate()
+        layer.step(rec, ext)
+        out[f"v{t}"], out[f"a{t}"], out[f"z{t}"] = layer.v.copy(), layer.a.copy(), layer.z.copy()
+    # e-prop
+    P, cap = 30, 12
+    m = RaggedMatrix(P, H, cap)
+    er = R.CounterRng(6, "eprop")
+    for i in range(P):
+        k = er.uniform_int(cap + 1)
+        m.target[i, :k] = er.sample_k_distinct(k, H)
+        m.row_length[i] = k
+    eps = np.zeros((B, P, cap), dtype=np.float32)
+    ebar = np.zeros_like(eps)
+    grad = np.zeros((P, cap))
+    a, b_, r_ = np.float32(prm.alpha), np.float32(prm.beta), np.float32(prm.rho)
+    out["target"], out["row_length"] = m.target.copy(), m.row_length.copy()
+    trace = np.zeros((B, P), dtype=np.float32)
+    for t in range(25):
+        x = (er.uniform01_array(B * P).reshape(B, P) < 0.2).astype(np.float32)
+        trace *= a
+        trace += x
+        psi = (er.uniform01_array(B * H).reshape(B, H) * 0.5).astype(np.float32)
+        lsig = er.normal_array(B * H).reshape(B, H).astype(np.float32)
+        out[f"trace{t}"], out[f"psi_e{t}"], out[f"lsig{t}"] = trace.copy(), psi, lsig
+        eprop_accumulate_batch(m.target, m.row_length, trace, psi, lsig, eps, ebar, grad, b_, r_, a)
+    out["eps"], out["ebar"], out["grad"] = eps, ebar, grad
+    save("alif_eprop.npz", **out)
+
+
+def gen_transpose_prop():
+    rng = R.CounterRng(8, "tp")
+    P, N, cap = 50, 40, 16
+    m = RaggedMatrix(P, N, cap)
+    syn = SynVarMatrix(m, ("g",))
+    for i in range(P):
+        k = rng.uniform_int(cap + 1)
+        m.target[i, :k] = rng.sample_k_distinct(k, N)
+        m.row_length[i] = k
+        syn.planes["g"][i, :k] = rng.uniform01_array(k) * 0.2
+    tm = TransposeMap(m)
+    tm.rebuild()
+    spikes = np.flatnonzero(rng.uniform01_array(P) < 0.3)
+    out_v = np.zeros(N)
+    propagate_spikes(m, syn.planes["g"], spikes, out_v)
+    save("transpose_prop.npz", target=m.target, row_length=m.row_length, g=syn.planes["g"],
+         col_length=tm.col_length, source_pre=tm.source_pre, source_slot=tm.source_slot,
+         spikes=spikes, out=out_v)
+
+
+if __name__ == "__main__":
+    gen_rng()
+    gen_remove()
+    gen_deep_r()
+    gen_adam()
+    gen_alif_eprop()
+    gen_transpose_prop()

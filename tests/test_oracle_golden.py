@@ -1,0 +1,98 @@
+"""Pin the CPU oracle against golden vectors produced by the real reference
+(tests/golden/make_golden.py) and the reference's own known answers."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import rng as O
+from oracle.deep_r import AdamOracle
+from oracle.ragged import Ragged, removal_permutation
+from oracle_helpers import PLANES, oracle_deepr_from_fixture, valid_equal
+
+from golden_cases import DEEPR_CASES
+
+
+def test_mix64_known_answers():
+    # pkg/tests/test_rng.py:118-123
+    assert O.mix64(0) == 0
+    assert O.mix64(1) == 6238072747940578789
+    assert O.mix64(0x9E3779B97F4A7C15) == 16294208416658607535
+
+
+def test_rng_golden():
+    g = golden("rng.npz")
+    parts = [(0,), (1,), (1, "host", 3, 7, 0), (42, "row", 0, 0, 1),
+             ("task", "example", 5), (2**64 - 1, -1, "päß-unicode-longer-than-8"),
+             (7, "init", "ff")]
+    assert [O.fold_key(*p) for p in parts] == [int(x) for x in g["fold"]]
+    assert [O.mix64(int(x)) for x in g["mix_in"]] == [int(x) for x in g["mix_out"]]
+    key = O.fold_key(9, "golden")
+    assert key == int(g["key"])
+    assert np.array_equal(O.Stream(key).u64_array(4096), g["draws"])
+    assert np.array_equal(O.Stream(key).uniform01_array(4096), g["u01"])
+    for n, row in zip(g["ns"], g["ui"]):
+        s = O.Stream.of(9, "uint", int(n))
+        vals = [s.uniform_int(int(n)) for _ in range(512)]
+        assert vals == [int(x) for x in row[:512]]
+        assert s.counter == int(row[512])
+    assert [O.child_key(key, i) for i in range(300)] == [int(x) for x in g["child"]]
+    assert np.array_equal(O.child_keys_np(key, np.arange(300)), g["child"])
+    for (k, n), ref in zip(g["skd_cases"], g["skd"]):
+        s = O.Stream.of(9, "skd", int(k), int(n))
+        out = s.sample_k_distinct(int(k), int(n))
+        ref = ref[ref >= 0]
+        assert list(out) == list(ref[:-1])
+        assert s.counter == ref[-1]
+
+
+def test_remove_slots_golden_and_closed_form():
+    g = golden("remove.npz")
+    for n, k, marked, result in zip(g["n"], g["k"], g["marked"], g["result"]):
+        n, k = int(n), int(k)
+        mk = marked[:k]
+        # serial replay
+        m = Ragged(1, 10_000, 96, ("w",))
+        m.target[0, :n] = np.arange(n)
+        m.row_length[0] = n
+        m.remove_slots(0, mk)
+        assert list(m.target[0, : n - k]) == list(result[: n - k])
+        # closed form used by the CUDA kernel
+        row = list(range(n))
+        for dst, src in removal_permutation(n, mk):
+            row[dst] = src
+        assert row[: n - k] == list(result[: n - k])
+
+
+@pytest.mark.parametrize("case", [c[0] for c in DEEPR_CASES])
+def test_deep_r_group_golden(case):
+    fx = golden(f"deepr_{case}.npz")
+    model, m, dr, cycles = oracle_deepr_from_fixture(fx)
+    for c in range(cycles):
+        m.planes["w"][:] = fx[f"c{c}_w_in"]
+        m.planes["grad"][:] = fx[f"c{c}_grad_in"]
+        dr.l1_step()
+        assert np.array_equal(m.planes["grad"], fx[f"c{c}_grad_l1"])
+        model.run_update_group("deep_r")
+        rl = fx[f"c{c}_row_length"]
+        assert np.array_equal(m.row_length, rl)
+        assert valid_equal(rl, m.target, fx[f"c{c}_target"])
+        for p in PLANES:
+            assert valid_equal(rl, m.planes[p], fx[f"c{c}_{p}"]), p
+        assert np.array_equal(dr.conn, fx[f"c{c}_conn"])
+        assert np.array_equal(dr.sign, fx[f"c{c}_sign"])
+        assert np.array_equal(dr.dormant, fx[f"c{c}_dormant"])
+        assert dr.last_removed == int(fx[f"c{c}_last_removed"])
+
+
+def test_adam_golden():
+    g = golden("adam.npz")
+    p = g["p0"].copy()
+    a = AdamOracle(shape=p.shape)
+    for t in range(5):
+        gr = g[f"g{t}"].copy()
+        a.apply(p, gr)
+        assert np.array_equal(p, g[f"p{t + 1}"])
+        assert np.array_equal(a.m, g[f"m{t + 1}"])
+        assert np.array_equal(a.v, g[f"v{t + 1}"])
+        assert not gr.any()
