@@ -146,6 +146,91 @@ SW_API int sw_adam_f64(double* p, double* g, double* m, double* v, int64_t n,
                 double b1, double one_minus_b1, double b2, double one_minus_b2,
                 double c1, double c2, double lr, double eps, void* stream);
 
+/* ---- e-prop (_kernels.py:15-39) ------------------------------------------- */
+/* Drop-in for eprop_accumulate_batch: reference layout eps/ebar [B,P,S] f32,
+ * grad [P,S] f64, pre_trace [B,P], psi/lsig [B,num_post]; thread per
+ * synapse, replicas ascending, float32 ops separately rounded (bit-exact). */
+SW_API int sw_eprop_accumulate_batch(const int32_t* targets, const int32_t* row_length,
+                                     int32_t num_pre, int32_t stride, const float* pre_trace,
+                                     const float* psi, const float* lsig, int32_t batch,
+                                     int32_t num_post, float* eps, float* ebar, double* grad,
+                                     float beta, float rho, float alpha, void* stream);
+/* Per-batch compact synapse order for the fused step: synapses bucketed by
+ * (target >> shift, pre, slot).  scratch: 2*G*num_pre int32 with
+ * G = ((num_post-1) >> shift) + 1.  out_* have e_pad entries (multiple of
+ * 32); entries past *total are padding (out_off = -1). */
+SW_API int sw_eprop_plan(const int32_t* row_length, const int32_t* target, int32_t num_pre,
+                         int32_t stride, int32_t num_post, int32_t shift, int32_t* scratch,
+                         int32_t* out_pre, int32_t* out_post, int32_t* out_off,
+                         int32_t e_pad, int32_t* total, void* stream);
+/* out[e] = plane[off[e]] (0 for off < 0) / plane[off[e]] = in[e] */
+SW_API int sw_gather_f64(const double* plane, const int32_t* off, int32_t n, double* out, void* stream);
+SW_API int sw_scatter_f64(double* plane, const int32_t* off, int32_t n, const double* in, void* stream);
+
+/* One projection onto the hidden layer in compact plan order. */
+typedef struct sw_eprop_seg {
+  const int32_t* pre;       /* [e_pad] presynaptic index   */
+  const int32_t* post;      /* [e_pad] postsynaptic index  */
+  const float* pre_trace;   /* [B, num_pre] xbar or zbar   */
+  float* eps;               /* [B, e_pad]                  */
+  float* ebar;              /* [B, e_pad]                  */
+  double* grad;             /* [e_pad] compact gradient    */
+  int32_t num_pre;
+  int32_t e_pad;            /* multiple of 32              */
+} sw_eprop_seg_t;
+
+/* Fused hot-path step: both projections' eligibility recursion and
+ * gradient accumulation (bit-identical to eprop_accumulate_batch on the
+ * same synapses) plus, when d != NULL, the readout gradients
+ * g_w_out[C,H] += d^T zbar and g_b_out[C] += sum_b d (classifier.py:221-222). */
+SW_API int sw_eprop_fused_step(const sw_eprop_seg_t* segs, int32_t n_segs, const float* psi,
+                               const float* lsig, int32_t batch, int32_t hidden, float beta,
+                               float rho, float alpha, const double* d, const float* zbar,
+                               double* g_w_out, double* g_b_out, int32_t num_classes,
+                               void* stream);
+
+/* ---- neurons (neurons.py) --------------------------------------------------- */
+/* AlifLayer.step (neurons.py:60-67), float32, n = batch*hidden elements. */
+SW_API int sw_alif_step(float* v, float* a, float* z, const float* rec, const float* ext,
+                        int64_t n, float alpha, float rho, float beta, float v_thr, void* stream);
+/* AlifLayer.surrogate (neurons.py:69-73). */
+SW_API int sw_alif_surrogate(const float* v, const float* a, float* psi, int64_t n, float beta,
+                             float v_thr, void* stream);
+/* LifCondLayer.step (neurons.py:137-148); spike_bits[ceil(n/32)] (LSB = lowest id). */
+SW_API int sw_lif_cond_step(double* V, double* g, int64_t* ref_until, const double* incoming,
+                            int32_t n, int64_t step_index, double decay_s, double g_leak,
+                            double v_rest, double e_exc, double v_theta, double v_reset,
+                            double h, double tau_m, int64_t ref_steps, uint32_t* spike_bits,
+                            void* stream);
+/* PoissonSource.poisson_step (neurons.py:189-195): u = uniform01 #(counter0 + node) < p. */
+SW_API int sw_poisson_step(uint64_t key, int64_t counter0, const double* p, int32_t n,
+                           uint32_t* spike_bits, void* stream);
+
+/* ---- classifier timestep (classifier.py:188-234) ----------------------------- */
+typedef struct sw_clf_step {
+  const int32_t* in_row_length;  const int32_t* in_target;  const float* in_w32;
+  int32_t in_stride;  int32_t num_inputs;
+  const int32_t* rec_row_length; const int32_t* rec_target; const float* rec_w32;
+  int32_t rec_stride; int32_t hidden;
+  const double* w_out; const double* b_out; int32_t num_classes;
+  const double* p_in;      /* [B, num_inputs] per-example spike probability  */
+  const uint64_t* ex_key;  /* [B] fold_key(seed,"task","example",e)          */
+  const int32_t* labels;   /* [B]                                            */
+  int32_t t;               /* timestep                                       */
+  int32_t batch;
+  float* v; float* a; float* z; float* zbar; float* xbar;     /* [B,H] / [B,NI] */
+  double* y; double* pi_sum; double* loss; double* d;         /* [B,C] / [B]    */
+  float* psi; float* lsig;                                    /* [B,H]          */
+  float alpha; float rho; float beta; float v_thr; double alpha64;
+} sw_clf_step_t;
+/* One fused forward timestep for all replicas (block per replica). */
+SW_API int sw_clf_step(const sw_clf_step_t* params, void* stream);
+/* out2[0] = sum of per-replica cross-entropy, out2[1] = #correct (argmax pi_sum). */
+SW_API int sw_clf_batch_stats(const double* loss, const double* pi_sum, const int32_t* labels,
+                              int32_t batch, int32_t num_classes, double* out2, void* stream);
+SW_API int sw_f64_to_f32(const double* in, float* out, int64_t n, void* stream);
+SW_API int sw_scale_f64(double* x, int64_t n, double s, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

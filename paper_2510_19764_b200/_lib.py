@@ -40,6 +40,23 @@ U64 = C.c_uint64
 F64 = C.c_double
 F32 = C.c_float
 RP = C.POINTER(Ragged)
+
+
+class EpropSeg(C.Structure):
+    """sw_eprop_seg_t"""
+    _fields_ = [("pre", P), ("post", P), ("pre_trace", P), ("eps", P), ("ebar", P),
+                ("grad", P), ("num_pre", I32), ("e_pad", I32)]
+
+
+class ClfStep(C.Structure):
+    """sw_clf_step_t"""
+    _fields_ = [("in_row_length", P), ("in_target", P), ("in_w32", P), ("in_stride", I32),
+                ("num_inputs", I32), ("rec_row_length", P), ("rec_target", P), ("rec_w32", P),
+                ("rec_stride", I32), ("hidden", I32), ("w_out", P), ("b_out", P),
+                ("num_classes", I32), ("p_in", P), ("ex_key", P), ("labels", P), ("t", I32),
+                ("batch", I32), ("v", P), ("a", P), ("z", P), ("zbar", P), ("xbar", P),
+                ("y", P), ("pi_sum", P), ("loss", P), ("d", P), ("psi", P), ("lsig", P),
+                ("alpha", F32), ("rho", F32), ("beta", F32), ("v_thr", F32), ("alpha64", F64)]
 BP = C.POINTER(BitfieldDesc)
 
 # name -> argtypes (restype is int status for all but sw_last_error)
@@ -58,6 +75,19 @@ SIGNATURES: dict[str, list] = {
     "sw_deepr_l1": [RP, I32, BP, F64, P],
     "sw_deepr_eliminate": [RP, I32, BP, BP, P, P],
     "sw_deepr_form_pass": [RP, BP, I32, P, U64, U64, P, P, P, P],
+    "sw_eprop_accumulate_batch": [P, P, I32, I32, P, P, P, I32, I32, P, P, P, F32, F32, F32, P],
+    "sw_eprop_plan": [P, P, I32, I32, I32, I32, P, P, P, P, I32, P, P],
+    "sw_gather_f64": [P, P, I32, P, P],
+    "sw_scatter_f64": [P, P, I32, P, P],
+    "sw_eprop_fused_step": [C.c_void_p, I32, P, P, I32, I32, F32, F32, F32, P, P, P, P, I32, P],
+    "sw_alif_step": [P, P, P, P, P, I64, F32, F32, F32, F32, P],
+    "sw_alif_surrogate": [P, P, P, I64, F32, F32, P],
+    "sw_lif_cond_step": [P, P, P, P, I32, I64, F64, F64, F64, F64, F64, F64, F64, F64, I64, P, P],
+    "sw_poisson_step": [U64, I64, P, I32, P, P],
+    "sw_clf_step": [C.c_void_p, P],
+    "sw_clf_batch_stats": [P, P, P, I32, I32, P, P],
+    "sw_f64_to_f32": [P, P, I64, P],
+    "sw_scale_f64": [P, I64, F64, P],
     "sw_adam_f64": [P, P, P, P, I64, F64, F64, F64, F64, F64, F64, F64, F64, P],
 }
 

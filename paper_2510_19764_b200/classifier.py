@@ -1,0 +1,427 @@
+"""Recurrent ALIF classifier trained with e-prop + DEEP R on the device
+(``sparsewire/classifier.py`` API).
+
+Per timestep two sm_100a launches (``sw_clf_step``: fused per-replica
+forward; ``sw_eprop_fused_step``: eligibility/gradient update of both
+projections + readout gradients); the whole 1000-step trial is captured
+once as a CUDA graph and replayed every batch.  Per batch: gradient scale,
+L1 nudge, Adam, DEEP R (classifier.py:236-263).  With ``process_group``
+set, replicas are sharded across ranks and the raw gradient sums are
+all-reduced (NCCL) before the update, so every rank applies the same
+update and replays the same rewiring streams.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .connectivity import init_pairwise_bernoulli_density
+from .deep_r import DeepR
+from .neurons import AlifParams
+from .plasticity import Adam
+from .rng import CounterRng, fold_key
+from .updates import Model
+
+
+@dataclass
+class SyntheticTask:
+    """classifier.py:28-79: class rate templates; per-example lognormal
+    jitter (host numpy Box-Muller/exp); Poisson spikes drawn on the device
+    from the example's counter stream."""
+
+    num_classes: int = 3
+    num_inputs: int = 20
+    example_steps: int = 200
+    seed: int = 0
+    rate_lo: float = 5.0
+    rate_hi: float = 80.0
+    dt: float = 1.0
+    num_train: int = 320
+    num_test: int = 96
+    jitter: float = 0.8
+
+    def __post_init__(self):
+        rng = CounterRng(self.seed, "task", "templates")
+        rates = self.rate_lo + rng.uniform01_array(self.num_classes * self.num_inputs) * (
+            self.rate_hi - self.rate_lo)
+        self.rates = rates.reshape(self.num_classes, self.num_inputs)
+
+    def label(self, example: int) -> int:
+        return example % self.num_classes
+
+    def example_rates(self, example: int) -> np.ndarray:
+        rates = self.rates[self.label(example)]
+        if self.jitter:
+            noise = CounterRng(self.seed, "task", "jitter", example).normal_array(self.num_inputs)
+            rates = rates * np.exp(self.jitter * noise)
+        return rates
+
+    def example_prob(self, example: int) -> np.ndarray:
+        return 1.0 - np.exp(-self.example_rates(example) * self.dt * 1e-3)
+
+    def example_key(self, example: int) -> int:
+        return fold_key(self.seed, "task", "example", example)
+
+    def batch_inputs(self, example_ids):
+        """Host-side per-example inputs of one batch: spike probabilities
+        [B, NI] float64, stream keys [B] and labels [B]."""
+        p = np.stack([self.example_prob(e) for e in example_ids])
+        keys = np.array([self.example_key(e) for e in example_ids], dtype=np.uint64)
+        labels = np.array([self.label(e) for e in example_ids], dtype=np.int32)
+        return p, keys, labels
+
+    def example_spikes(self, example: int) -> torch.Tensor:
+        """[example_steps, num_inputs] bool spikes, drawn on the device."""
+        n = self.example_steps * self.num_inputs
+        u = torch.empty(n, dtype=torch.float64, device="cuda")
+        _lib.call("sw_rng_uniform01", self.example_key(example), 0, n, u.data_ptr(),
+                  _lib.stream_ptr())
+        p = torch.from_numpy(self.example_prob(example)).cuda()
+        return u.view(self.example_steps, self.num_inputs) < p[None, :]
+
+    def batch(self, example_ids):
+        spikes = torch.stack([self.example_spikes(e) for e in example_ids])
+        labels = np.array([self.label(e) for e in example_ids])
+        return spikes, labels
+
+    def train_ids(self, batch_index: int, batch_size: int) -> list[int]:
+        start = batch_index * batch_size
+        return [(start + r) % self.num_train for r in range(batch_size)]
+
+    def test_ids(self) -> list[int]:
+        return [self.num_train + r for r in range(self.num_test)]
+
+
+class _Plan:
+    """Compact per-batch synapse order of one projection (sw_eprop_plan)."""
+
+    def __init__(self, m, batch, shift=5):
+        self.m = m
+        self.shift = shift
+        self.e_pad = 0
+        self.batch = batch
+        G = ((m.num_post - 1) >> shift) + 1
+        self.scratch = torch.zeros(2 * G * m.num_pre, dtype=torch.int32, device="cuda")
+        self.total = torch.zeros(1, dtype=torch.int32, device="cuda")
+
+    def ensure(self, edges: int) -> None:
+        e_pad = max(32, (edges + 31) // 32 * 32)
+        if e_pad == self.e_pad:
+            return
+        self.e_pad = e_pad
+        dev = "cuda"
+        self.pre = torch.zeros(e_pad, dtype=torch.int32, device=dev)
+        self.post = torch.zeros(e_pad, dtype=torch.int32, device=dev)
+        self.off = torch.zeros(e_pad, dtype=torch.int32, device=dev)
+        self.grad = torch.zeros(e_pad, dtype=torch.float64, device=dev)
+        self.eps = torch.zeros((self.batch, e_pad), dtype=torch.float32, device=dev)
+        self.ebar = torch.zeros_like(self.eps)
+
+    def build(self) -> None:
+        m = self.m
+        _lib.call("sw_eprop_plan", m.row_length.data_ptr(), m.target.data_ptr(), m.num_pre,
+                  m.stride, m.num_post, self.shift, self.scratch.data_ptr(), self.pre.data_ptr(),
+                  self.post.data_ptr(), self.off.data_ptr(), self.e_pad, self.total.data_ptr(),
+                  _lib.stream_ptr())
+
+    def seg(self, trace: torch.Tensor) -> _lib.EpropSeg:
+        s = _lib.EpropSeg()
+        s.pre, s.post, s.pre_trace = self.pre.data_ptr(), self.post.data_ptr(), trace.data_ptr()
+        s.eps, s.ebar, s.grad = self.eps.data_ptr(), self.ebar.data_ptr(), self.grad.data_ptr()
+        s.num_pre, s.e_pad = self.m.num_pre, self.e_pad
+        return s
+
+
+class EpropClassifierTrainer:
+    """classifier.py:82-293 on the device."""
+
+    def __init__(self, task: SyntheticTask, hidden: int = 128, input_density: float = 0.1,
+                 recurrent_density: float = 0.1, deep_r: bool = True, l1_strength: float = 0.005,
+                 learning_rate: float = 1e-3, batch_size: int = 32, seed: int = 0,
+                 workers: int = 1, dtype=np.float32, input_gain: float = 0.5,
+                 recurrent_gain: float = 0.15, use_graph: bool = True, process_group=None,
+                 local_batch: slice | None = None):
+        _lib.require_cuda()
+        if np.dtype(dtype) != np.float32:
+            raise TypeError("the device trainer computes the forward pass in float32")
+        self.task = task
+        self.hidden = hidden
+        self.batch_size = batch_size
+        self.seed = seed
+        self.deep_r_enabled = deep_r
+        self.params = AlifParams()
+        self.use_graph = use_graph
+        self.pg = process_group
+        # replicas handled by this rank (batch-DP); default: all of them
+        self.local = local_batch if local_batch is not None else slice(0, batch_size)
+        self.local_b = self.local.stop - self.local.start
+
+        headroom = 2.0 if deep_r else 1.0
+        self.net = Model(seed, workers=workers)
+        self.m_in, self.s_in = self._make_matrix(
+            "in", task.num_inputs, hidden, input_density, headroom,
+            input_gain / math.sqrt(max(1.0, input_density * task.num_inputs)), False)
+        self.m_rec, self.s_rec = self._make_matrix(
+            "rec", hidden, hidden, recurrent_density, headroom,
+            recurrent_gain / math.sqrt(max(1.0, recurrent_density * hidden)), True)
+        out_rng = CounterRng(seed, "init", "out")
+        C = task.num_classes
+        self.w_out = torch.from_numpy(out_rng.normal_array(
+            C * hidden, std=1.0 / math.sqrt(hidden)).reshape(C, hidden)).cuda()
+        self.b_out = torch.zeros(C, dtype=torch.float64, device="cuda")
+        self.g_w_out = torch.zeros_like(self.w_out)
+        self.g_b_out = torch.zeros_like(self.b_out)
+        self.adam_in = Adam(learning_rate, m=self.s_in.planes["adam_m"], v=self.s_in.planes["adam_v"])
+        self.adam_rec = Adam(learning_rate, m=self.s_rec.planes["adam_m"], v=self.s_rec.planes["adam_v"])
+        self.adam_out = Adam(learning_rate, shape=self.w_out.shape)
+        self.adam_b = Adam(learning_rate, shape=self.b_out.shape)
+        if deep_r:
+            self.deep_r_in = DeepR(self.m_in, self.s_in, "in", l1_strength=l1_strength)
+            self.deep_r_rec = DeepR(self.m_rec, self.s_rec, "rec", l1_strength=l1_strength,
+                                    exclude_diagonal=True)
+            self.deep_r_in.init_bitfields(CounterRng(seed, "deep_r", "in"))
+            self.deep_r_rec.init_bitfields(CounterRng(seed, "deep_r", "rec"))
+            self.deep_r_in.register(self.net, "deep_r", "in")
+            self.deep_r_rec.register(self.net, "deep_r", "rec")
+        self._alloc_state()
+        self.history: list[dict] = []
+        self._graph = None
+        self._graph_learn = None
+        self.steps_launched = 0
+
+    # -- construction ------------------------------------------------------------
+    def _make_matrix(self, name, num_pre, num_post, density, headroom, w_std, exclude_diagonal):
+        rng = CounterRng(self.seed, "init", name)
+        m, syn = init_pairwise_bernoulli_density(num_pre, num_post, density, headroom, rng,
+                                                 var_names=("w", "grad", "adam_m", "adam_v"),
+                                                 exclude_diagonal=exclude_diagonal)
+        draws = rng.normal_array(m.num_pre * m.stride, std=w_std).reshape(m.num_pre, m.stride)
+        mask = m.slot_mask()
+        w = syn.planes["w"]
+        w.copy_(torch.where(mask, torch.from_numpy(draws).cuda(), w))
+        self.net.add_matrix(name, m, syn)
+        return m, syn
+
+    def _alloc_state(self):
+        B, H, NI, C = self.local_b, self.hidden, self.task.num_inputs, self.task.num_classes
+        f32 = dict(dtype=torch.float32, device="cuda")
+        f64 = dict(dtype=torch.float64, device="cuda")
+        self.v = torch.zeros((B, H), **f32)
+        self.a = torch.zeros((B, H), **f32)
+        self.z = torch.zeros((B, H), **f32)
+        self.zbar = torch.zeros((B, H), **f32)
+        self.xbar = torch.zeros((B, NI), **f32)
+        self.psi = torch.zeros((B, H), **f32)
+        self.lsig = torch.zeros((B, H), **f32)
+        self.y = torch.zeros((B, C), **f64)
+        self.pi_sum = torch.zeros((B, C), **f64)
+        self.loss_b = torch.zeros(B, **f64)
+        self.d = torch.zeros((B, C), **f64)
+        self.p_in = torch.zeros((B, NI), **f64)
+        self.keys = torch.zeros(B, dtype=torch.int64, device="cuda")
+        self.labels = torch.zeros(B, dtype=torch.int32, device="cuda")
+        self.w32_in = torch.zeros(self.m_in.target.shape, **f32)
+        self.w32_rec = torch.zeros(self.m_rec.target.shape, **f32)
+        self.stats = torch.zeros(2, **f64)
+        self.stats_host = torch.zeros(2, dtype=torch.float64, pin_memory=True)
+        self.pin_p = torch.zeros((B, NI), dtype=torch.float64, pin_memory=True)
+        self.pin_keys = torch.zeros(B, dtype=torch.int64, pin_memory=True)
+        self.pin_labels = torch.zeros(B, dtype=torch.int32, pin_memory=True)
+        self.plan_in = _Plan(self.m_in, B)
+        self.plan_rec = _Plan(self.m_rec, B)
+        self._segs = (_lib.EpropSeg * 2)()
+
+    # -- per-step launches ------------------------------------------------------------
+    def _step_params(self, t: int) -> _lib.ClfStep:
+        p = self.params
+        s = _lib.ClfStep()
+        mi, mr = self.m_in, self.m_rec
+        s.in_row_length, s.in_target, s.in_w32 = mi.row_length.data_ptr(), mi.target.data_ptr(), self.w32_in.data_ptr()
+        s.in_stride, s.num_inputs = mi.stride, self.task.num_inputs
+        s.rec_row_length, s.rec_target, s.rec_w32 = mr.row_length.data_ptr(), mr.target.data_ptr(), self.w32_rec.data_ptr()
+        s.rec_stride, s.hidden = mr.stride, self.hidden
+        s.w_out, s.b_out, s.num_classes = self.w_out.data_ptr(), self.b_out.data_ptr(), self.task.num_classes
+        s.p_in, s.ex_key, s.labels = self.p_in.data_ptr(), self.keys.data_ptr(), self.labels.data_ptr()
+        s.t, s.batch = t, self.local_b
+        s.v, s.a, s.z, s.zbar, s.xbar = (x.data_ptr() for x in (self.v, self.a, self.z, self.zbar, self.xbar))
+        s.y, s.pi_sum, s.loss, s.d = (x.data_ptr() for x in (self.y, self.pi_sum, self.loss_b, self.d))
+        s.psi, s.lsig = self.psi.data_ptr(), self.lsig.data_ptr()
+        s.alpha, s.rho = float(np.float32(p.alpha)), float(np.float32(p.rho))
+        s.beta, s.v_thr = float(np.float32(p.beta)), float(np.float32(p.v_thr))
+        s.alpha64 = p.alpha
+        return s
+
+    def _launch_steps(self, learn: bool) -> None:
+        st = _lib.stream_ptr()
+        p = self.params
+        a32, r32, b32 = float(np.float32(p.alpha)), float(np.float32(p.rho)), float(np.float32(p.beta))
+        self._segs[0] = self.plan_in.seg(self.xbar)
+        self._segs[1] = self.plan_rec.seg(self.zbar)
+        for t in range(self.task.example_steps):
+            prm = self._step_params(t)
+            _lib.call("sw_clf_step", ctypes.byref(prm), st)
+            if learn:
+                _lib.call("sw_eprop_fused_step", ctypes.cast(self._segs, ctypes.c_void_p), 2,
+                          self.psi.data_ptr(), self.lsig.data_ptr(), self.local_b, self.hidden,
+                          b32, r32, a32, self.d.data_ptr(), self.zbar.data_ptr(),
+                          self.g_w_out.data_ptr(), self.g_b_out.data_ptr(),
+                          self.task.num_classes, st)
+        self.steps_launched += self.task.example_steps
+
+    def _run_trial(self, learn: bool) -> None:
+        if not self.use_graph:
+            self._launch_steps(learn)
+            return
+        if self._graph is None or self._graph_learn != learn or self._graph_key != self._buffers_key():
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    self._launch_steps(learn)
+            torch.cuda.current_stream().wait_stream(s)
+            self._graph, self._graph_learn, self._graph_key = g, learn, self._buffers_key()
+            self.steps_launched -= self.task.example_steps   # capture is not execution
+        self._graph.replay()
+        self.steps_launched += self.task.example_steps
+
+    def _buffers_key(self):
+        return (self.plan_in.e_pad, self.plan_rec.e_pad, self.plan_in.pre.data_ptr(),
+                self.plan_rec.pre.data_ptr())
+
+    # -- batch ------------------------------------------------------------------------
+    def _upload_batch(self, ids) -> None:
+        p, keys, labels = self.task.batch_inputs(ids)
+        self.pin_p.copy_(torch.from_numpy(p[self.local]))
+        self.pin_keys.copy_(torch.from_numpy(keys[self.local].view(np.int64)))
+        self.pin_labels.copy_(torch.from_numpy(labels[self.local]))
+        self.p_in.copy_(self.pin_p, non_blocking=True)
+        self.keys.copy_(self.pin_keys, non_blocking=True)
+        self.labels.copy_(self.pin_labels, non_blocking=True)
+        self.h2d_bytes = p[self.local].nbytes + keys[self.local].nbytes + labels[self.local].nbytes
+
+    def _prepare(self, learn: bool) -> None:
+        st = _lib.stream_ptr()
+        _lib.call("sw_f64_to_f32", self.s_in.planes["w"].data_ptr(), self.w32_in.data_ptr(),
+                  self.w32_in.numel(), st)
+        _lib.call("sw_f64_to_f32", self.s_rec.planes["w"].data_ptr(), self.w32_rec.data_ptr(),
+                  self.w32_rec.numel(), st)
+        for x in (self.v, self.a, self.z, self.zbar, self.xbar, self.y, self.pi_sum, self.loss_b):
+            x.zero_()
+        if learn:
+            for plan, syn in ((self.plan_in, self.s_in), (self.plan_rec, self.s_rec)):
+                plan.ensure(plan.m.edge_count())
+                plan.build()
+                plan.eps.zero_()
+                plan.ebar.zero_()
+                _lib.call("sw_gather_f64", syn.planes["grad"].data_ptr(), plan.off.data_ptr(),
+                          plan.e_pad, plan.grad.data_ptr(), st)
+
+    def _finish(self, learn: bool):
+        st = _lib.stream_ptr()
+        if learn:
+            for plan, syn in ((self.plan_in, self.s_in), (self.plan_rec, self.s_rec)):
+                _lib.call("sw_scatter_f64", syn.planes["grad"].data_ptr(), plan.off.data_ptr(),
+                          plan.e_pad, plan.grad.data_ptr(), st)
+        _lib.call("sw_clf_batch_stats", self.loss_b.data_ptr(), self.pi_sum.data_ptr(),
+                  self.labels.data_ptr(), self.local_b, self.task.num_classes,
+                  self.stats.data_ptr(), st)
+
+    def _forward_batch(self, ids, learn: bool):
+        self._upload_batch(ids)
+        self._prepare(learn)
+        self._run_trial(learn)
+        self._finish(learn)
+
+    def _allreduce_grads(self) -> None:
+        """Batch-DP: sum raw gradients and batch statistics over ranks
+        (classifier.py:242-246 order: reduce, then scale)."""
+        import torch.distributed as dist
+        flat = torch.cat([self.s_in.planes["grad"].flatten(), self.s_rec.planes["grad"].flatten(),
+                          self.g_w_out.flatten(), self.g_b_out, self.stats])
+        dist.all_reduce(flat, group=self.pg)
+        o = 0
+        for t in (self.s_in.planes["grad"], self.s_rec.planes["grad"], self.g_w_out, self.g_b_out,
+                  self.stats):
+            n = t.numel()
+            t.copy_(flat[o:o + n].view_as(t))
+            o += n
+
+    def gradient_phase(self, batch_index: int) -> tuple[float, float]:
+        """Forward + e-prop over one batch, gradient scaling, L1 and Adam
+        (classifier.py:236-253)."""
+        ids = self.task.train_ids(batch_index, self.batch_size)
+        self._forward_batch(ids, learn=True)
+        if self.pg is not None:
+            self._allreduce_grads()
+        self.stats_host.copy_(self.stats, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        loss = float(self.stats_host[0]) / (self.batch_size * self.task.example_steps)
+        accuracy = float(self.stats_host[1]) / self.batch_size
+        if not math.isfinite(loss):
+            raise FloatingPointError(f"loss diverged at batch {batch_index}")
+        st = _lib.stream_ptr()
+        inv_b = 1.0 / self.batch_size
+        for t in (self.s_in.planes["grad"], self.s_rec.planes["grad"], self.g_w_out, self.g_b_out):
+            _lib.call("sw_scale_f64", t.data_ptr(), t.numel(), inv_b, st)
+        if self.deep_r_enabled:
+            self.deep_r_in.l1_step()
+            self.deep_r_rec.l1_step()
+        self.adam_in.apply(self.s_in.planes["w"], self.s_in.planes["grad"])
+        self.adam_rec.apply(self.s_rec.planes["w"], self.s_rec.planes["grad"])
+        self.adam_out.apply(self.w_out, self.g_w_out)
+        self.adam_b.apply(self.b_out, self.g_b_out)
+        return loss, accuracy
+
+    def rewire_phase(self) -> int:
+        if not self.deep_r_enabled:
+            return 0
+        self.net.run_update_group("deep_r")
+        return self.deep_r_in.last_removed + self.deep_r_rec.last_removed
+
+    def train_batch(self, batch_index: int) -> dict:
+        loss, accuracy = self.gradient_phase(batch_index)
+        removed = self.rewire_phase()
+        total = self.m_in.edge_count() + self.m_rec.edge_count()
+        metrics = {"batch": batch_index, "loss": loss, "accuracy": accuracy,
+                   "removed": removed, "total": total,
+                   "fraction_rewired": removed / total if total else 0.0}
+        self.history.append(metrics)
+        return metrics
+
+    def evaluate(self, example_ids) -> float:
+        correct = count = 0
+        for start in range(0, len(example_ids), self.batch_size):
+            ids = list(example_ids[start:start + self.batch_size])
+            real = len(ids)
+            if real < self.batch_size:
+                ids += [ids[-1]] * (self.batch_size - real)
+            self._forward_batch(ids, learn=False)
+            pred = self.pi_sum.argmax(dim=1).cpu().numpy()
+            labels = np.array([self.task.label(e) for e in ids])[self.local]
+            lo = self.local.start
+            keep = min(max(real - lo, 0), self.local_b)
+            correct += int((pred[:keep] == labels[:keep]).sum())
+            count += keep
+        return correct / count if count else 0.0
+
+    def run(self, num_batches: int, stop_at_accuracy: float | None = None) -> list[dict]:
+        for b in range(num_batches):
+            m = self.train_batch(b)
+            if stop_at_accuracy is not None and m["accuracy"] >= stop_at_accuracy:
+                break
+        return self.history
+
+    def connectivity_fingerprint(self) -> bytes:
+        parts = []
+        for m in (self.m_in, self.m_rec):
+            parts.append(m.row_length.cpu().numpy().tobytes())
+            parts.append((m.target * m.slot_mask()).cpu().numpy().tobytes())
+        return b"".join(parts)

@@ -1,0 +1,322 @@
+// e-prop eligibility recursion + gradient accumulation (sparsewire/_kernels.py:15-39).
+//
+// Per (replica b, synapse i->j):
+//   e    = psi[b,j] * (zb - beta*eps)        (float32, separately rounded)
+//   ebar = alpha*ebar + e
+//   grad += (double)(lsig[b,j] * ebar)      (float64, replicas ascending)
+//   eps  = rho*eps + e
+//
+// Two entry points:
+//  * sw_eprop_accumulate_batch: the reference layout ([B,P,S] eps/ebar,
+//    [P,S] grad), thread per synapse, replicas ascending — the drop-in.
+//  * sw_eprop_fused_step: the hot path.  Synapses are stored compactly in a
+//    per-batch "plan" order: bucketed by 32-post group, then by pre, then
+//    slot (sw_eprop_plan_*), so a warp's 32 synapses touch one 128-byte line
+//    of psi/lsig and one or two sectors of the pre trace per replica, and
+//    eps/ebar[b, e] are perfectly coalesced.  A block owns 32 synapses and
+//    all replicas: warps compute the float32 terms for disjoint replica
+//    chunks into shared memory, warp 0 folds them into the float64 gradient
+//    in ascending replica order (bit-identical to the reference's loop).
+//    Extra blocks of the same launch reduce the readout gradients
+//    g_w_out += d^T zbar, g_b_out += sum_b d (classifier.py:221-222).
+#include "common.cuh"
+
+namespace {
+
+__global__ void k_eprop_ref(const int32_t* targets, const int32_t* row_length, int P, int S,
+                            const float* pre_trace, const float* psi, const float* lsig, int B,
+                            int H, float* eps, float* ebar, double* grad, float beta, float rho,
+                            float alpha) {
+  const int64_t total = (int64_t)P * S;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(x / S), s = (int)(x - (int64_t)i * S);
+    if (s >= row_length[i]) continue;
+    const int j = targets[x];
+    double g = grad[x];
+    for (int b = 0; b < B; ++b) {
+      const int64_t q = (int64_t)b * total + x;
+      const float zb = pre_trace[(int64_t)b * P + i];
+      const float ep = eps[q];
+      const float e = __fmul_rn(psi[(int64_t)b * H + j], __fsub_rn(zb, __fmul_rn(beta, ep)));
+      const float eb = __fadd_rn(__fmul_rn(alpha, ebar[q]), e);
+      ebar[q] = eb;
+      g = __dadd_rn(g, (double)__fmul_rn(lsig[(int64_t)b * H + j], eb));
+      eps[q] = __fadd_rn(__fmul_rn(rho, ep), e);
+    }
+    grad[x] = g;
+  }
+}
+
+// ---- plan: bucket synapses by (target >> shift, pre, slot) ----------------------------
+__global__ void k_bucket_count(const int32_t* row_length, const int32_t* target, int P, int S,
+                               int shift, int32_t* counts /* [G*P] */) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+    const int n = row_length[i];
+    for (int s = 0; s < n; ++s) atomicAdd(&counts[(target[(int64_t)i * S + s] >> shift) * P + i], 1);
+  }
+}
+
+// single-block exclusive scan (in place), n up to a few million
+__global__ void k_scan_excl(int32_t* a, int n, int32_t* total) {
+  __shared__ int32_t warp_sums[32];
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int x = base + threadIdx.x;
+    const int v = x < n ? a[x] : 0;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(SW_FULL_MASK, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) warp_sums[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      int w = lane < (blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(SW_FULL_MASK, w, o);
+        if (lane >= o) w += t;
+      }
+      warp_sums[lane] = w;   // inclusive
+    }
+    __syncthreads();
+    const int before = carry + (warp ? warp_sums[warp - 1] : 0);
+    if (x < n) a[x] = before + inc - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = before + inc;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && total) *total = carry;
+}
+
+__global__ void k_bucket_fill(const int32_t* row_length, const int32_t* target, int P, int S,
+                              int shift, int32_t* cursor /* [G*P], starts as offsets */,
+                              int32_t* out_pre, int32_t* out_post, int32_t* out_off) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+    const int n = row_length[i];
+    for (int s = 0; s < n; ++s) {
+      const int j = target[(int64_t)i * S + s];
+      const int pos = atomicAdd(&cursor[(j >> shift) * P + i], 1);   // only this thread touches it
+      out_pre[pos] = i;
+      out_post[pos] = j;
+      out_off[pos] = i * S + s;
+    }
+  }
+}
+
+__global__ void k_plan_pad(int32_t* pre, int32_t* post, int32_t* off, const int32_t* total, int e_pad) {
+  const int e0 = *total;
+  for (int e = e0 + blockIdx.x * blockDim.x + threadIdx.x; e < e_pad; e += gridDim.x * blockDim.x) {
+    pre[e] = 0;
+    post[e] = 0;
+    off[e] = -1;
+  }
+}
+
+__global__ void k_gather_f64(const double* plane, const int32_t* off, int n, double* out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
+    out[e] = off[e] >= 0 ? plane[off[e]] : 0.0;
+}
+
+__global__ void k_scatter_f64(double* plane, const int32_t* off, int n, const double* in) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
+    if (off[e] >= 0) plane[off[e]] = in[e];
+}
+
+// ---- fused hot-path step ----------------------------------------------------------------
+struct Seg {
+  const int32_t* pre;
+  const int32_t* post;
+  const float* trace;   // [B, P]
+  float* eps;           // [B, E_pad]
+  float* ebar;
+  double* grad;         // [E_pad]
+  int P;
+  int e_pad;
+  int tiles;
+};
+
+struct ReadoutArgs {
+  const double* d;      // [B, C]
+  const float* zbar;    // [B, H]
+  double* g_w_out;      // [C, H]
+  double* g_b_out;      // [C]
+  int C;
+};
+
+constexpr int kNW = 8;     // warps per block
+constexpr int kBPW = 8;    // replicas per warp per chunk
+constexpr int kChunk = kNW * kBPW;
+
+__global__ void __launch_bounds__(kNW * 32)
+k_eprop_fused(Seg s0, Seg s1, const float* __restrict__ psi, const float* __restrict__ lsig,
+              int B, int H, float beta, float rho, float alpha, ReadoutArgs ro) {
+  __shared__ float terms[kChunk][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int tile = blockIdx.x;
+  if (tile >= s0.tiles + s1.tiles) {
+    // readout-gradient blocks: block r covers classes x 32-post tile
+    const int r = tile - s0.tiles - s1.tiles;
+    const int htiles = (H + 31) / 32;
+    const int c = r / htiles, h = (r % htiles) * 32 + lane;
+    __shared__ double part[kNW][33];
+    double acc = 0.0, accb = 0.0;
+    if (h < H) {
+      for (int b = warp; b < B; b += kNW) {
+        const double dv = ro.d[(int64_t)b * ro.C + c];
+        acc += dv * (double)ro.zbar[(int64_t)b * H + h];
+        accb += dv;
+      }
+    }
+    part[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && h < H) {
+      double t = 0.0;
+      for (int w = 0; w < kNW; ++w) t += part[w][lane];
+      ro.g_w_out[(int64_t)c * H + h] += t;
+    }
+    __syncthreads();
+    if ((r % htiles) == 0) {
+      part[warp][lane] = accb;   // same for all lanes (h-independent); lane 0 carries it
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kNW; ++w) t += part[w][0];
+        ro.g_b_out[c] += t;
+      }
+    }
+    return;
+  }
+  const Seg& sg = (tile < s0.tiles) ? s0 : s1;
+  if (tile >= s0.tiles) tile -= s0.tiles;
+  const int e = tile * 32 + lane;
+  const int pre = sg.pre[e];
+  const int post = sg.post[e];
+  const float* trace = sg.trace + pre;
+  const float* ps = psi + post;
+  const float* ls = lsig + post;
+  float* eps = sg.eps + e;
+  float* ebar = sg.ebar + e;
+  const int64_t ES = sg.e_pad;
+  double g = (warp == 0) ? sg.grad[e] : 0.0;
+  for (int b0 = 0; b0 < B; b0 += kChunk) {
+    float zb[kBPW], p[kBPW], l[kBPW], ep[kBPW], eb[kBPW];
+#pragma unroll
+    for (int q = 0; q < kBPW; ++q) {
+      const int b = b0 + warp * kBPW + q;
+      if (b < B) {
+        zb[q] = __ldg(trace + (int64_t)b * sg.P);
+        p[q] = __ldg(ps + (int64_t)b * H);
+        l[q] = __ldg(ls + (int64_t)b * H);
+        ep[q] = __ldcs(eps + b * ES);
+        eb[q] = __ldcs(ebar + b * ES);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kBPW; ++q) {
+      const int b = b0 + warp * kBPW + q;
+      if (b < B) {
+        const float ee = __fmul_rn(p[q], __fsub_rn(zb[q], __fmul_rn(beta, ep[q])));
+        const float ebn = __fadd_rn(__fmul_rn(alpha, eb[q]), ee);
+        __stcs(ebar + b * ES, ebn);
+        __stcs(eps + b * ES, __fadd_rn(__fmul_rn(rho, ep[q]), ee));
+        terms[warp * kBPW + q][lane] = __fmul_rn(l[q], ebn);
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const int nb = min(kChunk, B - b0);
+      for (int r = 0; r < nb; ++r) g = __dadd_rn(g, (double)terms[r][lane]);
+    }
+    __syncthreads();
+  }
+  if (warp == 0) sg.grad[e] = g;
+}
+
+int grid1(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+extern "C" int sw_eprop_accumulate_batch(const int32_t* targets, const int32_t* row_length,
+                                         int32_t num_pre, int32_t stride, const float* pre_trace,
+                                         const float* psi, const float* lsig, int32_t batch,
+                                         int32_t num_post, float* eps, float* ebar, double* grad,
+                                         float beta, float rho, float alpha, void* stream) {
+  const int64_t total = (int64_t)num_pre * stride;
+  if (total == 0) return SW_OK;
+  k_eprop_ref<<<grid1(total), 256, 0, (cudaStream_t)stream>>>(targets, row_length, num_pre, stride,
+                                                              pre_trace, psi, lsig, batch, num_post,
+                                                              eps, ebar, grad, beta, rho, alpha);
+  SW_CHECK_LAUNCH("sw_eprop_accumulate_batch");
+  return SW_OK;
+}
+
+extern "C" int sw_eprop_plan(const int32_t* row_length, const int32_t* target, int32_t num_pre,
+                             int32_t stride, int32_t num_post, int32_t shift, int32_t* scratch,
+                             int32_t* out_pre, int32_t* out_post, int32_t* out_off,
+                             int32_t e_pad, int32_t* total, void* stream) {
+  // scratch: 2 * G * num_pre int32 (counts/offsets, cursor)
+  cudaStream_t st = (cudaStream_t)stream;
+  const int G = ((num_post - 1) >> shift) + 1;
+  const int n = G * num_pre;
+  int32_t* counts = scratch;
+  int32_t* cursor = scratch + n;
+  cudaMemsetAsync(counts, 0, (size_t)n * 4, st);
+  if (num_pre > 0) {
+    k_bucket_count<<<grid1(num_pre), 256, 0, st>>>(row_length, target, num_pre, stride, shift, counts);
+    k_scan_excl<<<1, 1024, 0, st>>>(counts, n, total);
+    cudaMemcpyAsync(cursor, counts, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
+    k_bucket_fill<<<grid1(num_pre), 256, 0, st>>>(row_length, target, num_pre, stride, shift, cursor,
+                                                  out_pre, out_post, out_off);
+  } else {
+    cudaMemsetAsync(total, 0, 4, st);
+  }
+  k_plan_pad<<<grid1(e_pad), 256, 0, st>>>(out_pre, out_post, out_off, total, e_pad);
+  SW_CHECK_LAUNCH("sw_eprop_plan");
+  return SW_OK;
+}
+
+extern "C" int sw_gather_f64(const double* plane, const int32_t* off, int32_t n, double* out, void* stream) {
+  if (n <= 0) return SW_OK;
+  k_gather_f64<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(plane, off, n, out);
+  SW_CHECK_LAUNCH("sw_gather_f64");
+  return SW_OK;
+}
+
+extern "C" int sw_scatter_f64(double* plane, const int32_t* off, int32_t n, const double* in, void* stream) {
+  if (n <= 0) return SW_OK;
+  k_scatter_f64<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(plane, off, n, in);
+  SW_CHECK_LAUNCH("sw_scatter_f64");
+  return SW_OK;
+}
+
+extern "C" int sw_eprop_fused_step(const sw_eprop_seg_t* segs, int32_t n_segs, const float* psi,
+                                   const float* lsig, int32_t batch, int32_t hidden, float beta,
+                                   float rho, float alpha, const double* d, const float* zbar,
+                                   double* g_w_out, double* g_b_out, int32_t num_classes,
+                                   void* stream) {
+  if (n_segs < 1 || n_segs > 2) { sw::set_last_error("eprop: 1 or 2 segments"); return SW_ERR_INVALID_ARG; }
+  Seg s[2] = {};
+  for (int k = 0; k < n_segs; ++k) {
+    const sw_eprop_seg_t& q = segs[k];
+    if (q.e_pad % 32) { sw::set_last_error("eprop: e_pad must be a multiple of 32"); return SW_ERR_INVALID_ARG; }
+    s[k] = Seg{q.pre, q.post, q.pre_trace, q.eps, q.ebar, q.grad, q.num_pre, q.e_pad, q.e_pad / 32};
+  }
+  ReadoutArgs ro{d, zbar, g_w_out, g_b_out, num_classes};
+  const int ro_blocks = (d && num_classes > 0) ? num_classes * ((hidden + 31) / 32) : 0;
+  const int grid = s[0].tiles + s[1].tiles + ro_blocks;
+  if (grid == 0) return SW_OK;
+  k_eprop_fused<<<grid, kNW * 32, 0, (cudaStream_t)stream>>>(s[0], s[1], psi, lsig, batch, hidden,
+                                                             beta, rho, alpha, ro);
+  SW_CHECK_LAUNCH("sw_eprop_fused_step");
+  return SW_OK;
+}

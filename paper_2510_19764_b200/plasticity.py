@@ -40,3 +40,24 @@ class Adam:
         _lib.call("sw_adam_f64", params.data_ptr(), grads.data_ptr(), self.m.data_ptr(),
                   self.v.data_ptr(), n, self.beta1, 1.0 - self.beta1, self.beta2,
                   1.0 - self.beta2, c1, c2, self.lr, self.eps, _lib.stream_ptr())
+
+
+def eprop_accumulate_batch(targets, row_length, pre_trace, psi, lsig, eps, ebar, grad,
+                           beta, rho, alpha) -> None:
+    """Drop-in for ``sparsewire._kernels.eprop_accumulate_batch`` (:15-39) on
+    CUDA tensors in the reference layout: targets [P,S] int32, row_length [P]
+    int32, pre_trace [B,P] / psi, lsig [B,H] float32, eps, ebar [B,P,S]
+    float32 (updated in place), grad [P,S] float64 (accumulated).  One thread
+    per synapse, replicas ascending: bit-identical to the numba kernel."""
+    for t, dt in ((targets, torch.int32), (row_length, torch.int32), (pre_trace, torch.float32),
+                  (psi, torch.float32), (lsig, torch.float32), (eps, torch.float32),
+                  (ebar, torch.float32), (grad, torch.float64)):
+        if t.dtype != dt or not t.is_cuda or not t.is_contiguous():
+            raise TypeError("eprop_accumulate_batch: wrong dtype/device/layout")
+    P, S = targets.shape
+    B = pre_trace.shape[0]
+    H = psi.shape[1]
+    _lib.call("sw_eprop_accumulate_batch", targets.data_ptr(), row_length.data_ptr(), P, S,
+              pre_trace.data_ptr(), psi.data_ptr(), lsig.data_ptr(), B, H, eps.data_ptr(),
+              ebar.data_ptr(), grad.data_ptr(), float(beta), float(rho), float(alpha),
+              _lib.stream_ptr())

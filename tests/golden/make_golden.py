@@ -231,7 +231,30 @@ def gen_transpose_prop():
          spikes=spikes, out=out_v)
 
 
+def gen_trainer():
+    """Small e-prop + DEEP R training run (classifier.py:82-263)."""
+    from sparsewire.classifier import EpropClassifierTrainer, SyntheticTask
+    task = SyntheticTask(num_classes=3, num_inputs=20, example_steps=60, seed=4)
+    tr = EpropClassifierTrainer(task, hidden=24, batch_size=8, seed=4, deep_r=True,
+                                input_density=0.3, recurrent_density=0.2)
+    out = {}
+    for b in range(3):
+        h = tr.train_batch(b)
+        out[f"b{b}_loss"] = np.float64(h["loss"])
+        out[f"b{b}_acc"] = np.float64(h["accuracy"])
+        out[f"b{b}_removed"] = np.int64(h["removed"])
+    for name, m, syn in (("in", tr.m_in, tr.s_in), ("rec", tr.m_rec, tr.s_rec)):
+        out[f"{name}_row_length"] = m.row_length.copy()
+        out[f"{name}_target"] = m.target.copy()
+        for pl in PLANES:
+            out[f"{name}_{pl}"] = syn.planes[pl].copy()
+    out["w_out"] = tr.w_out.copy()
+    out["b_out"] = tr.b_out.copy()
+    save("trainer.npz", **out)
+
+
 if __name__ == "__main__":
+    gen_trainer()
     gen_rng()
     gen_remove()
     gen_deep_r()

@@ -1,0 +1,166 @@
+"""Device e-prop / ALIF kernels and the device trainer vs the reference
+golden vectors and the oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+from oracle_helpers import valid_equal
+
+pytestmark = pytest.mark.gpu
+
+
+def test_alif_kernels_bit_exact(dev_lib):
+    from paper_2510_19764_b200.neurons import AlifLayer, AlifParams
+    g = golden("alif_eprop.npz")
+    layer = AlifLayer(48, AlifParams(), batch=8)
+    for t in range(6):
+        assert np.array_equal(layer.surrogate().cpu().numpy(), g[f"psi{t}"])
+        layer.step(torch.from_numpy(g[f"rec{t}"]).cuda(), torch.from_numpy(g[f"ext{t}"]).cuda())
+        assert np.array_equal(layer.v.cpu().numpy(), g[f"v{t}"])
+        assert np.array_equal(layer.a.cpu().numpy(), g[f"a{t}"])
+        assert np.array_equal(layer.z.cpu().numpy(), g[f"z{t}"])
+
+
+def test_eprop_dropin_bit_exact(dev_lib):
+    from paper_2510_19764_b200.neurons import AlifParams
+    from paper_2510_19764_b200.plasticity import eprop_accumulate_batch
+    g = golden("alif_eprop.npz")
+    p = AlifParams()
+    tg = torch.from_numpy(g["target"]).cuda()
+    rl = torch.from_numpy(g["row_length"]).cuda()
+    eps = torch.zeros((8,) + tuple(tg.shape), dtype=torch.float32, device="cuda")
+    ebar = torch.zeros_like(eps)
+    grad = torch.zeros(tuple(tg.shape), dtype=torch.float64, device="cuda")
+    for t in range(25):
+        eprop_accumulate_batch(tg, rl, torch.from_numpy(g[f"trace{t}"]).cuda(),
+                               torch.from_numpy(g[f"psi_e{t}"]).cuda(),
+                               torch.from_numpy(g[f"lsig{t}"]).cuda(), eps, ebar, grad,
+                               np.float32(p.beta), np.float32(p.rho), np.float32(p.alpha))
+    assert np.array_equal(eps.cpu().numpy(), g["eps"])
+    assert np.array_equal(ebar.cpu().numpy(), g["ebar"])
+    assert np.array_equal(grad.cpu().numpy(), g["grad"])
+
+
+@pytest.mark.parametrize("B,P,H,cap,R", [(8, 30, 48, 12, 6), (64, 700, 256, 82, 26),
+                                         (37, 100, 1024, 40, 10)])
+def test_fused_eprop_equals_reference_layout(dev_lib, B, P, H, cap, R):
+    """The compact-plan fused kernel reproduces the reference-layout kernel
+    bit-for-bit (eps, ebar per synapse and the float64 gradient)."""
+    from paper_2510_19764_b200 import _lib
+    from paper_2510_19764_b200.classifier import _Plan
+    from paper_2510_19764_b200.connectivity import RaggedMatrix
+    from paper_2510_19764_b200.plasticity import eprop_accumulate_batch
+    import ctypes
+    rs = np.random.default_rng(P)
+    tg = np.zeros((P, cap), np.int32)
+    rl = np.zeros(P, np.int32)
+    for i in range(P):
+        k = int(min(cap, rs.poisson(R)))
+        tg[i, :k] = rs.choice(H, size=k, replace=False)
+        rl[i] = k
+    m = RaggedMatrix(P, H, cap)
+    m.load_state(rl, tg)
+    plan = _Plan(m, B)
+    plan.ensure(int(rl.sum()))
+    plan.build()
+    grad0 = rs.standard_normal((P, cap))
+    gplane = torch.from_numpy(grad0).cuda()
+    _lib.call("sw_gather_f64", gplane.data_ptr(), plan.off.data_ptr(), plan.e_pad,
+              plan.grad.data_ptr(), _lib.stream_ptr())
+    ref_eps = torch.zeros((B, P, cap), dtype=torch.float32, device="cuda")
+    ref_ebar = torch.zeros_like(ref_eps)
+    ref_grad = torch.from_numpy(grad0.copy()).cuda()
+    segs = (_lib.EpropSeg * 1)()
+    for t in range(7):
+        trace = torch.from_numpy((rs.random((B, P)) * 2).astype(np.float32)).cuda()
+        psi = torch.from_numpy((rs.random((B, H)) * 0.5).astype(np.float32)).cuda()
+        lsig = torch.from_numpy(rs.standard_normal((B, H)).astype(np.float32)).cuda()
+        eprop_accumulate_batch(m.target, m.row_length, trace, psi, lsig, ref_eps, ref_ebar,
+                               ref_grad, 0.0174, 0.9995, 0.95)
+        segs[0] = plan.seg(trace)
+        _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 1, psi.data_ptr(),
+                  lsig.data_ptr(), B, H, float(np.float32(0.0174)), float(np.float32(0.9995)),
+                  float(np.float32(0.95)), None, None, None, None, 0, _lib.stream_ptr())
+    _lib.call("sw_scatter_f64", gplane.data_ptr(), plan.off.data_ptr(), plan.e_pad,
+              plan.grad.data_ptr(), _lib.stream_ptr())
+    assert valid_equal(rl, gplane.cpu().numpy(), ref_grad.cpu().numpy())
+    off = plan.off.cpu().numpy()
+    E = int(rl.sum())
+    re = ref_eps.reshape(B, -1).cpu().numpy()[:, off[:E]]
+    assert np.array_equal(plan.eps.cpu().numpy()[:, :E], re)
+    rb = ref_ebar.reshape(B, -1).cpu().numpy()[:, off[:E]]
+    assert np.array_equal(plan.ebar.cpu().numpy()[:, :E], rb)
+
+
+def _small_trainer(use_graph=True):
+    from paper_2510_19764_b200.classifier import EpropClassifierTrainer, SyntheticTask
+    task = SyntheticTask(num_classes=3, num_inputs=20, example_steps=60, seed=4)
+    return EpropClassifierTrainer(task, hidden=24, batch_size=8, seed=4, deep_r=True,
+                                  input_density=0.3, recurrent_density=0.2, use_graph=use_graph)
+
+
+def test_trainer_init_matches_reference_exactly(dev_lib):
+    from oracle.classifier import TaskOracle, TrainerOracle
+    tr = _small_trainer()
+    ot = TrainerOracle(TaskOracle(num_classes=3, num_inputs=20, example_steps=60, seed=4),
+                       hidden=24, batch_size=8, seed=4, input_density=0.3, recurrent_density=0.2)
+    for dm, ds, om, dr, odr in ((tr.m_in, tr.s_in, ot.m_in, tr.deep_r_in, ot.dr_in),
+                                (tr.m_rec, tr.s_rec, ot.m_rec, tr.deep_r_rec, ot.dr_rec)):
+        assert np.array_equal(dm.row_length.cpu().numpy(), om.row_length)
+        assert np.array_equal(dm.target.cpu().numpy(), om.target)
+        assert np.array_equal(ds.planes["w"].cpu().numpy(), om.planes["w"])
+        assert np.array_equal(dr.sign_bits.host_words(), odr.sign)
+        assert np.array_equal(dr.conn_bits.host_words(), odr.conn)
+    assert np.array_equal(tr.w_out.cpu().numpy(), ot.w_out)
+
+
+def test_trainer_matches_reference_run_and_rewires_exactly(dev_lib):
+    """Three batches vs the golden reference run: loss/weights to float
+    tolerance; each DEEP R step state-injected into the oracle and compared
+    bit-exactly (row lengths, targets, planes, bits)."""
+    from oracle.deep_r import DeepROracle
+    from oracle.ragged import Ragged
+    from oracle.updates import OracleModel
+    g = golden("trainer.npz")
+    for use_graph in (True, False):
+        tr = _small_trainer(use_graph)
+        for b in range(3):
+            loss, acc = tr.gradient_phase(b)
+            assert abs(loss - float(g[f"b{b}_loss"])) <= 1e-6 * abs(loss), (b, loss)
+            # state injection: oracle DEEP R on the device's post-Adam state
+            om = OracleModel(4)
+            objs = []
+            for name, m, s, d in (("in", tr.m_in, tr.s_in, tr.deep_r_in),
+                                  ("rec", tr.m_rec, tr.s_rec, tr.deep_r_rec)):
+                o = Ragged(m.num_pre, m.num_post, m.max_row_length, ("w", "grad", "adam_m", "adam_v"))
+                o.row_length[:] = m.row_length.cpu().numpy()
+                o.target[:] = m.target.cpu().numpy()
+                for p in o.planes:
+                    o.planes[p][:] = s.planes[p].cpu().numpy()
+                od = DeepROracle(o, l1=0.005, exclude_diagonal=(name == "rec"))
+                od.sign[:] = d.sign_bits.host_words()
+                od.conn[:] = d.conn_bits.host_words()
+                om.add_matrix(name, o)
+                od.register(om, "deep_r", name)
+                objs.append((o, od, m, s, d))
+            for bnd in om.groups["deep_r"]:
+                bnd.update_count = b
+            om.run_update_group("deep_r")
+            removed = tr.rewire_phase()
+            assert removed == sum(od.last_removed for _, od, _, _, _ in objs)
+            for o, od, m, s, d in objs:
+                rl = o.row_length
+                assert np.array_equal(m.row_length.cpu().numpy(), rl)
+                assert valid_equal(rl, m.target.cpu().numpy(), o.target)
+                for p in o.planes:
+                    assert valid_equal(rl, s.planes[p].cpu().numpy(), o.planes[p])
+                assert np.array_equal(d.conn_bits.host_words(), od.conn)
+        for name, m, s in (("in", tr.m_in, tr.s_in), ("rec", tr.m_rec, tr.s_rec)):
+            rl = g[f"{name}_row_length"]
+            assert np.array_equal(m.row_length.cpu().numpy(), rl)
+            assert valid_equal(rl, m.target.cpu().numpy(), g[f"{name}_target"])
+            mask = np.arange(rl.size and m.stride)[None, :] < rl[:, None]
+            assert np.allclose(s.planes["w"].cpu().numpy()[mask], g[f"{name}_w"][mask],
+                               rtol=1e-6, atol=1e-9)

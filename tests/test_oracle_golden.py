@@ -96,3 +96,48 @@ def test_adam_golden():
         assert np.array_equal(a.m, g[f"m{t + 1}"])
         assert np.array_equal(a.v, g[f"v{t + 1}"])
         assert not gr.any()
+
+
+def test_alif_and_eprop_golden():
+    from oracle.classifier import AlifP, alif_step, alif_surrogate, eprop_accumulate
+    g = golden("alif_eprop.npz")
+    B, H = 8, 48
+    v = np.zeros((B, H), np.float32)
+    a = np.zeros_like(v)
+    z = np.zeros_like(v)
+    for t in range(6):
+        assert np.array_equal(alif_surrogate(v, a), g[f"psi{t}"])
+        v, a, z = alif_step(v, a, z, g[f"rec{t}"], g[f"ext{t}"])
+        assert np.array_equal(v, g[f"v{t}"]) and np.array_equal(a, g[f"a{t}"])
+        assert np.array_equal(z, g[f"z{t}"])
+    p = AlifP()
+    tg, rl = g["target"], g["row_length"]
+    eps = np.zeros((B,) + tg.shape, np.float32)
+    ebar = np.zeros_like(eps)
+    grad = np.zeros(tg.shape)
+    for t in range(25):
+        eprop_accumulate(tg, rl, g[f"trace{t}"], g[f"psi_e{t}"], g[f"lsig{t}"], eps, ebar, grad,
+                         np.float32(p.beta), np.float32(p.rho), np.float32(p.alpha))
+    assert np.array_equal(eps, g["eps"]) and np.array_equal(ebar, g["ebar"])
+    assert np.array_equal(grad, g["grad"])
+
+
+def test_trainer_oracle_matches_reference_run():
+    """The oracle trainer reproduces a 3-batch reference training run
+    bit-for-bit on this host (same numpy/OpenBLAS)."""
+    from oracle.classifier import TaskOracle, TrainerOracle
+    g = golden("trainer.npz")
+    task = TaskOracle(num_classes=3, num_inputs=20, example_steps=60, seed=4)
+    tr = TrainerOracle(task, hidden=24, batch_size=8, seed=4, input_density=0.3,
+                       recurrent_density=0.2)
+    for b in range(3):
+        loss, acc = tr.gradient_phase(b)
+        removed = tr.rewire_phase()
+        assert abs(loss - float(g[f"b{b}_loss"])) <= 1e-12 * abs(loss)
+        assert acc == float(g[f"b{b}_acc"])
+        assert removed == int(g[f"b{b}_removed"])
+    for name, m in (("in", tr.m_in), ("rec", tr.m_rec)):
+        rl = g[f"{name}_row_length"]
+        assert np.array_equal(m.row_length, rl)
+        assert valid_equal(rl, m.target, g[f"{name}_target"])
+        assert np.allclose(m.planes["w"], g[f"{name}_w"], rtol=1e-9, atol=1e-12)
