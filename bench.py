@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark of the structural-plasticity hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload clf-c1|clf-c2]
+
+Headline (BASELINE.json metric, configs[1]): e-prop + DEEP R training time
+per epoch of the recurrent ALIF classifier 700 -> 256 hidden, 10% sparse
+input/recurrent connectivity with DEEP R, 20 classes, batch 512, 1000-step
+SHD-shaped synthetic trials (8156 training examples -> 16 batches/epoch).
+A step = one training batch (1000 timesteps of forward + e-prop, gradient
+scaling, L1, Adam x4, DEEP R group).  s/epoch = 16 x ms/step / 1000.
+
+N > 1 (torchrun): the 512 replicas are sharded across ranks (batch-DP,
+strong scaling) with one NCCL all-reduce of the raw gradients per batch.
+
+--impl reference times the reference CPU path (the oracle port in
+``oracle/``, single-threaded) on a bounded sample of the same workload and
+extrapolates to s/epoch; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (num_inputs, hidden, density_in, density_rec, classes, batch, steps)
+    "clf-c1": dict(num_inputs=700, hidden=256, density=0.10, classes=20, batch=512, steps=1000),
+    "clf-c2": dict(num_inputs=700, hidden=1024, density=0.01, classes=20, batch=512, steps=1000),
+}
+NUM_TRAIN = 8156
+EPOCH_BATCHES = -(-NUM_TRAIN // 512)   # 16
+
+
+def measured_peak():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
+        if os.path.exists(p):
+            d = json.load(open(p))
+            return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sms.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def dist_setup(n_gpus):
+    import torch
+    import torch.distributed as dist
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1:
+        lr = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(lr)
+        dist.init_process_group("nccl")
+        return dist.get_rank(), ws, lr
+    return 0, 1, 0
+
+
+def flush_l2(buf):
+    buf.add_(1)   # 256 MiB write > 126 MB L2
+
+
+# ------------------------------------------------------------------ reference arm
+def cpu_reference_sample(w, sample_steps=None):
+    """Time the oracle port of the classifier step on the host CPU over a
+    bounded number of timesteps of one batch (+ one DEEP R group) and
+    extrapolate to s/epoch.  Single-threaded."""
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        return _cpu_reference_sample(w, sample_steps)
+
+
+def _cpu_reference_sample(w, sample_steps):
+    from oracle.classifier import TaskOracle, TrainerOracle
+    task = TaskOracle(num_classes=w["classes"], num_inputs=w["num_inputs"],
+                      example_steps=sample_steps or 4, seed=1, num_train=NUM_TRAIN)
+    t0 = time.perf_counter()
+    tr = TrainerOracle(task, hidden=w["hidden"], input_density=w["density"],
+                       recurrent_density=w["density"], batch_size=w["batch"], seed=1)
+    build_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    tr.forward(task.train_ids(0, w["batch"]), learn=True)
+    fwd = time.perf_counter() - t0
+    per_step = fwd / task.example_steps
+    t0 = time.perf_counter()
+    inv = 1.0 / w["batch"]
+    for t in (tr.m_in.planes["grad"], tr.m_rec.planes["grad"]):
+        t *= inv
+    tr.dr_in.l1_step()
+    tr.dr_rec.l1_step()
+    tr.adam_in.apply(tr.m_in.planes["w"], tr.m_in.planes["grad"])
+    tr.adam_rec.apply(tr.m_rec.planes["w"], tr.m_rec.planes["grad"])
+    tr.rewire_phase()
+    upd = time.perf_counter() - t0
+    batch_s = per_step * w["steps"] + upd
+    return {"s_per_epoch": batch_s * EPOCH_BATCHES, "batch_s": batch_s, "per_step_s": per_step,
+            "update_s": upd, "build_s": build_s, "sample_steps": task.example_steps}
+
+
+def run_reference(args, w):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    vals = []
+    for _ in range(args.steps):
+        r = cpu_reference_sample(w, sample_steps=args.ref_sample_steps)
+        vals.append(r["s_per_epoch"])
+    v = statistics.median(vals)
+    sample = (f"{r['sample_steps']} of {w['steps']} timesteps of one {w['batch']}-replica batch "
+              f"+ one full update/DEEP R group, extrapolated x{w['steps']} steps x{EPOCH_BATCHES} batches")
+    line = {"impl": "reference", "metric": "e-prop+DEEP R training time per epoch",
+            "value": round(v, 3), "unit": "s/epoch", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: e-prop ALIF classifier {w['num_inputs']}->{w['hidden']}, "
+                                   f"{int(w['density'] * 100)}% + DEEP R, batch {w['batch']}, SHD-shaped synthetic"},
+            "cpu_baseline": {"value": round(v, 3), "unit": "s/epoch", "cores": 1, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": round(v, 3), "unit": "s/epoch", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ device arm
+def run_device(args, w):
+    import torch
+    import torch.distributed as dist
+    rank, ws, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", local)
+    from paper_2510_19764_b200 import _lib
+    from paper_2510_19764_b200.classifier import EpropClassifierTrainer, SyntheticTask
+
+    B = w["batch"]
+    per = B // ws
+    local_slice = slice(rank * per, (rank + 1) * per if rank < ws - 1 else B)
+    task = SyntheticTask(num_classes=w["classes"], num_inputs=w["num_inputs"],
+                         example_steps=w["steps"], seed=1, num_train=NUM_TRAIN, num_test=2264)
+    tr = EpropClassifierTrainer(task, hidden=w["hidden"], input_density=w["density"],
+                                recurrent_density=w["density"], deep_r=True, batch_size=B,
+                                seed=1, process_group=dist.group.WORLD if ws > 1 else None,
+                                local_batch=local_slice)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    n_batches = args.warmup + args.steps
+    # host inputs of every batch (numpy), prepared outside the timed regions
+    host = [tr.host_inputs(b) for b in range(n_batches)]
+    dev_inputs = [(torch.from_numpy(h[0]).to(dev), torch.from_numpy(h[1].view(np.int64)).to(dev),
+                   torch.from_numpy(h[2]).to(dev)) for h in host]
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(run_one, label):
+        times = []
+        for b in range(args.warmup):
+            run_one(b)
+        l0 = _lib.launch_count()
+        g0 = tr.steps_launched
+        barrier()
+        with ClockSampler(local) as clk:
+            for k in range(args.steps):
+                b = args.warmup + k
+                flush_l2(flush)
+                barrier()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                run_one(b)
+                e1.record()
+                e1.synchronize()
+                times.append(e0.elapsed_time(e1))
+            barrier()
+        ms = sum(times) / len(times)
+        if ws > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        eager = _lib.launch_count() - l0
+        return ms, eager, tr.steps_launched - g0, clk.summary()
+
+    # kernels per captured trial (graph): count one eager capture-equivalent launch set
+    def run_resident(b):
+        tr.set_inputs_device(*dev_inputs[b])
+        tr.train_batch(b, resident=True)
+
+    def run_e2e(b):
+        tr.train_batch(b, host=host[b])
+
+    ms_dev, eager_dev, steps_dev, clocks = timed(run_resident, "resident")
+    ms_e2e, _, _, clocks_e2e = timed(run_e2e, "e2e")
+    # graph kernels per trial: 2 per timestep (clf_step + fused e-prop)
+    graph_kernels = 2 * steps_dev
+    launches_per_step = (eager_dev + graph_kernels) / args.steps
+
+    # ---- roofline of the dominant kernel (fused e-prop step), timed live
+    import ctypes
+    p = tr.params
+    a32, r32, b32 = (float(np.float32(x)) for x in (p.alpha, p.rho, p.beta))
+    segs = (_lib.EpropSeg * 2)()
+    segs[0] = tr.plan_in.seg(tr.xbar)
+    segs[1] = tr.plan_rec.seg(tr.zbar)
+    st = torch.cuda.current_stream()
+    reps = 50
+    for _ in range(3):
+        _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 2, tr.psi.data_ptr(),
+                  tr.lsig.data_ptr(), tr.local_b, tr.hidden, b32, r32, a32, tr.d.data_ptr(),
+                  tr.zbar.data_ptr(), tr.g_w_out.data_ptr(), tr.g_b_out.data_ptr(),
+                  w["classes"], st.cuda_stream)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 2, tr.psi.data_ptr(),
+                  tr.lsig.data_ptr(), tr.local_b, tr.hidden, b32, r32, a32, tr.d.data_ptr(),
+                  tr.zbar.data_ptr(), tr.g_w_out.data_ptr(), tr.g_b_out.data_ptr(),
+                  w["classes"], st.cuda_stream)
+    e1.record(st)
+    e1.synchronize()
+    k_ms = e0.elapsed_time(e1) / reps
+    E = tr.m_in.edge_count() + tr.m_rec.edge_count()
+    Bl = tr.local_b
+    alg_bytes = Bl * E * 16 + E * (16 + 4) + Bl * (w["num_inputs"] + w["hidden"] + 2 * w["hidden"]) * 4
+    achieved = alg_bytes / (k_ms * 1e-3) / 1e9
+    peak, peak_kind = measured_peak()
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "eprop_ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(args.workload)
+        except Exception:
+            traffic = None
+
+    s_epoch = ms_dev * EPOCH_BATCHES / 1000.0
+    s_epoch_e2e = ms_e2e * EPOCH_BATCHES / 1000.0
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        r = cpu_reference_sample(w, sample_steps=args.ref_sample_steps)
+        cpu = {"value": round(r["s_per_epoch"], 3), "unit": "s/epoch", "cores": 1, "kind": "port",
+               "sample": f"{r['sample_steps']} timesteps of one {w['batch']}-replica batch + one "
+                         f"update/DEEP R group (oracle port, 1 thread), extrapolated to "
+                         f"{w['steps']} steps x {EPOCH_BATCHES} batches"}
+    h2d = sum(x.nbytes for x in host[0]) // ws
+    if rank == 0:
+        line = {
+            "metric": "e-prop+DEEP R training time per epoch", "value": round(s_epoch, 4),
+            "unit": "s/epoch", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_dev, 3), "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: e-prop ALIF classifier {w['num_inputs']}->{w['hidden']}, "
+                                   f"{int(w['density'] * 100)}% in/rec + DEEP R, 20 classes, batch {B}, "
+                                   f"{w['steps']}-step SHD-shaped synthetic trials, {EPOCH_BATCHES} batches/epoch",
+                       "global_batch": B, "seq_len": w["steps"], "parallelism": f"dp{ws}",
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       "edges": E},
+            "e2e": {"value": round(s_epoch_e2e, 4), "unit": "s/epoch",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16 + 8 * 4},
+            "gpu_launches": int(round(launches_per_step * args.steps)),
+            "gpu_launches_per_step": round(launches_per_step, 1),
+            "roofline": {"kernel": "k_eprop_fused (sw_eprop_fused_step)", "bound": "hbm",
+                         "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "alg_bytes_per_launch": int(alg_bytes), "kernel_us": round(k_ms * 1e3, 2),
+                         "share_of_step": round(k_ms * w["steps"] / ms_dev, 3)},
+            "clocks": clocks,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="clf-c1", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-sample-steps", type=int, default=4)
+    args = ap.parse_args()
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, w)
+    else:
+        run_device(args, w)
+
+
+if __name__ == "__main__":
+    main()

@@ -69,6 +69,8 @@ typedef struct sw_bitfield {
 /* ---- library ---------------------------------------------------------- */
 SW_API int sw_abi_version(void);
 SW_API const char* sw_last_error(void);
+/* Number of kernels this library has enqueued so far (graph capture counts once). */
+SW_API long long sw_launch_count(void);
 /* Device self-test of the SplitMix64 golden vectors (test_rng.py:118-123);
  * writes mix64(0), mix64(1), mix64(G) into out[3] (device pointer). */
 SW_API int sw_rng_selftest(uint64_t* out3, void* stream);

@@ -108,6 +108,8 @@ def lib():
         fn = getattr(L, name)
         fn.argtypes = argtypes
         fn.restype = C.c_int
+    L.sw_launch_count.argtypes = []
+    L.sw_launch_count.restype = C.c_longlong
     L.sw_last_error.argtypes = []
     L.sw_last_error.restype = C.c_char_p
     _lib = L
@@ -133,6 +135,10 @@ def call(name: str, *args) -> None:
     if st != 0:
         msg = (L.sw_last_error() or b"").decode(errors="replace")
         raise errors.from_status(st, f"{name}: {msg}")
+
+
+def launch_count() -> int:
+    return int(lib().sw_launch_count())
 
 
 def ptr(t: torch.Tensor | None) -> int | None:

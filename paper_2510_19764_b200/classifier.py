@@ -297,8 +297,12 @@ class EpropClassifierTrainer:
                 self.plan_rec.pre.data_ptr())
 
     # -- batch ------------------------------------------------------------------------
-    def _upload_batch(self, ids) -> None:
-        p, keys, labels = self.task.batch_inputs(ids)
+    def host_inputs(self, batch_index: int):
+        """Host-side inputs of a training batch (numpy): p [B,NI], keys, labels."""
+        return self.task.batch_inputs(self.task.train_ids(batch_index, self.batch_size))
+
+    def _upload_batch(self, ids, host=None) -> None:
+        p, keys, labels = host if host is not None else self.task.batch_inputs(ids)
         self.pin_p.copy_(torch.from_numpy(p[self.local]))
         self.pin_keys.copy_(torch.from_numpy(keys[self.local].view(np.int64)))
         self.pin_labels.copy_(torch.from_numpy(labels[self.local]))
@@ -306,6 +310,12 @@ class EpropClassifierTrainer:
         self.keys.copy_(self.pin_keys, non_blocking=True)
         self.labels.copy_(self.pin_labels, non_blocking=True)
         self.h2d_bytes = p[self.local].nbytes + keys[self.local].nbytes + labels[self.local].nbytes
+
+    def set_inputs_device(self, p: torch.Tensor, keys: torch.Tensor, labels: torch.Tensor) -> None:
+        """Batch inputs already resident in HBM (device-to-device copy)."""
+        self.p_in.copy_(p[self.local])
+        self.keys.copy_(keys[self.local])
+        self.labels.copy_(labels[self.local])
 
     def _prepare(self, learn: bool) -> None:
         st = _lib.stream_ptr()
@@ -334,8 +344,9 @@ class EpropClassifierTrainer:
                   self.labels.data_ptr(), self.local_b, self.task.num_classes,
                   self.stats.data_ptr(), st)
 
-    def _forward_batch(self, ids, learn: bool):
-        self._upload_batch(ids)
+    def _forward_batch(self, ids, learn: bool, host=None, resident: bool = False):
+        if not resident:
+            self._upload_batch(ids, host)
         self._prepare(learn)
         self._run_trial(learn)
         self._finish(learn)
@@ -354,11 +365,13 @@ class EpropClassifierTrainer:
             t.copy_(flat[o:o + n].view_as(t))
             o += n
 
-    def gradient_phase(self, batch_index: int) -> tuple[float, float]:
+    def gradient_phase(self, batch_index: int, host=None, resident: bool = False
+                       ) -> tuple[float, float]:
         """Forward + e-prop over one batch, gradient scaling, L1 and Adam
-        (classifier.py:236-253)."""
+        (classifier.py:236-253).  ``host`` = precomputed host inputs;
+        ``resident`` = the batch inputs are already in HBM (benchmarking)."""
         ids = self.task.train_ids(batch_index, self.batch_size)
-        self._forward_batch(ids, learn=True)
+        self._forward_batch(ids, learn=True, host=host, resident=resident)
         if self.pg is not None:
             self._allreduce_grads()
         self.stats_host.copy_(self.stats, non_blocking=True)
@@ -386,8 +399,8 @@ class EpropClassifierTrainer:
         self.net.run_update_group("deep_r")
         return self.deep_r_in.last_removed + self.deep_r_rec.last_removed
 
-    def train_batch(self, batch_index: int) -> dict:
-        loss, accuracy = self.gradient_phase(batch_index)
+    def train_batch(self, batch_index: int, host=None, resident: bool = False) -> dict:
+        loss, accuracy = self.gradient_phase(batch_index, host, resident)
         removed = self.rewire_phase()
         total = self.m_in.edge_count() + self.m_rec.edge_count()
         metrics = {"batch": batch_index, "loss": loss, "accuracy": accuracy,

@@ -28,7 +28,7 @@ extern "C" int sw_adam_f64(double* p, double* g, double* m, double* v, int64_t n
   int64_t grid = (n + 255) / 256;
   if (grid > 148 * 16) grid = 148 * 16;
   k_adam_f64<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(p, g, m, v, n, b1, one_minus_b1, b2,
-                                                           one_minus_b2, c1, c2, lr, eps);
+                                                           one_minus_b2, c1, c2, lr, eps); sw::count_launch();
   SW_CHECK_LAUNCH("sw_adam_f64");
   return SW_OK;
 }

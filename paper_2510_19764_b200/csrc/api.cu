@@ -1,11 +1,14 @@
 // Library plumbing (error string, ABI version) and the counter-RNG entry points.
 #include <cstdio>
 #include <cstring>
-#include <mutex>
+#include <atomic>
 #include "common.cuh"
 
 namespace sw {
 static thread_local char g_last_error[512] = "";
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_last_error(const char* msg) {
   std::snprintf(g_last_error, sizeof(g_last_error), "%s", msg);
@@ -25,6 +28,7 @@ int check_launch(const char* where) {
 
 extern "C" int sw_abi_version(void) { return SW_ABI_VERSION; }
 extern "C" const char* sw_last_error(void) { return sw::g_last_error; }
+extern "C" long long sw_launch_count(void) { return sw::g_launches.load(); }
 
 __global__ void k_rng_selftest(uint64_t* out) {
   out[0] = sw::mix64(0);
@@ -33,7 +37,7 @@ __global__ void k_rng_selftest(uint64_t* out) {
 }
 
 extern "C" int sw_rng_selftest(uint64_t* out3, void* stream) {
-  k_rng_selftest<<<1, 1, 0, (cudaStream_t)stream>>>(out3);
+  k_rng_selftest<<<1, 1, 0, (cudaStream_t)stream>>>(out3); sw::count_launch();
   SW_CHECK_LAUNCH("sw_rng_selftest");
   return SW_OK;
 }
@@ -70,28 +74,28 @@ static int grid_for(int64_t n, int block) {
 
 extern "C" int sw_rng_u64(uint64_t key, uint64_t counter0, int64_t n, uint64_t* out, void* stream) {
   if (n <= 0) return SW_OK;
-  k_rng_u64<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(key, counter0, n, out);
+  k_rng_u64<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(key, counter0, n, out); sw::count_launch();
   SW_CHECK_LAUNCH("sw_rng_u64");
   return SW_OK;
 }
 
 extern "C" int sw_rng_uniform01(uint64_t key, uint64_t counter0, int64_t n, double* out, void* stream) {
   if (n <= 0) return SW_OK;
-  k_rng_u01<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(key, counter0, n, out);
+  k_rng_u01<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(key, counter0, n, out); sw::count_launch();
   SW_CHECK_LAUNCH("sw_rng_uniform01");
   return SW_OK;
 }
 
 extern "C" int sw_rng_child_keys(uint64_t key, int64_t n, uint64_t* out, void* stream) {
   if (n <= 0) return SW_OK;
-  k_rng_child<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(key, n, out);
+  k_rng_child<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(key, n, out); sw::count_launch();
   SW_CHECK_LAUNCH("sw_rng_child_keys");
   return SW_OK;
 }
 
 extern "C" int sw_rng_uniform_int_seq(uint64_t key, uint64_t n, int64_t count, uint64_t* out, void* stream) {
   if (n == 0 || count < 0) { sw::set_last_error("uniform_int: n must be positive"); return SW_ERR_INVALID_ARG; }
-  k_rng_uint_seq<<<1, 1, 0, (cudaStream_t)stream>>>(key, n, count, out);
+  k_rng_uint_seq<<<1, 1, 0, (cudaStream_t)stream>>>(key, n, count, out); sw::count_launch();
   SW_CHECK_LAUNCH("sw_rng_uniform_int_seq");
   return SW_OK;
 }

@@ -225,28 +225,28 @@ extern "C" int sw_clf_step(const sw_clf_step_t* p, void* stream) {
     if (smem > 227 * 1024) { sw::set_last_error("clf_step: layer too large"); return SW_ERR_INVALID_ARG; }
     cudaFuncSetAttribute((const void*)k_clf_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
-  k_clf_step<<<p->batch, kThreads, smem, (cudaStream_t)stream>>>(*p);
+  k_clf_step<<<p->batch, kThreads, smem, (cudaStream_t)stream>>>(*p); sw::count_launch();
   SW_CHECK_LAUNCH("sw_clf_step");
   return SW_OK;
 }
 
 extern "C" int sw_clf_batch_stats(const double* loss, const double* pi_sum, const int32_t* labels,
                                   int32_t batch, int32_t num_classes, double* out2, void* stream) {
-  k_clf_batch_stats<<<1, kThreads, 0, (cudaStream_t)stream>>>(loss, pi_sum, labels, batch, num_classes, out2);
+  k_clf_batch_stats<<<1, kThreads, 0, (cudaStream_t)stream>>>(loss, pi_sum, labels, batch, num_classes, out2); sw::count_launch();
   SW_CHECK_LAUNCH("sw_clf_batch_stats");
   return SW_OK;
 }
 
 extern "C" int sw_f64_to_f32(const double* in, float* out, int64_t n, void* stream) {
   if (n <= 0) return SW_OK;
-  k_f64_to_f32<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(in, out, n);
+  k_f64_to_f32<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(in, out, n); sw::count_launch();
   SW_CHECK_LAUNCH("sw_f64_to_f32");
   return SW_OK;
 }
 
 extern "C" int sw_scale_f64(double* x, int64_t n, double s, void* stream) {
   if (n <= 0) return SW_OK;
-  k_scale_f64<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(x, n, s);
+  k_scale_f64<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(x, n, s); sw::count_launch();
   SW_CHECK_LAUNCH("sw_scale_f64");
   return SW_OK;
 }

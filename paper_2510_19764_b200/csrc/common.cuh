@@ -73,6 +73,7 @@ __device__ __forceinline__ void raise_flag(int* flag, int code) {
 namespace sw {
 void set_last_error(const char* msg);
 int check_launch(const char* where);
+void count_launch();
 }  // namespace sw
 
 #define SW_CHECK_LAUNCH(name) do { int _s = sw::check_launch(name); if (_s) return _s; } while (0)

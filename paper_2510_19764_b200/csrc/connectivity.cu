@@ -76,7 +76,7 @@ extern "C" int sw_init_bernoulli_count(int64_t num_pre, int32_t num_post, uint64
   }
   k_bernoulli<false><<<grid_rows(num_pre), 256, 0, st>>>(num_pre, num_post, key, counter0, mode,
                                                          density, lut, side, row_length, nullptr,
-                                                         1, max_len);
+                                                         1, max_len); sw::count_launch();
   SW_CHECK_LAUNCH("sw_init_bernoulli_count");
   return SW_OK;
 }
@@ -89,7 +89,7 @@ extern "C" int sw_init_bernoulli_fill(int64_t num_pre, int32_t num_post, uint64_
   if (num_pre == 0 || num_post == 0) return SW_OK;
   k_bernoulli<true><<<grid_rows(num_pre), 256, 0, st>>>(num_pre, num_post, key, counter0, mode,
                                                         density, lut, side, row_length, target,
-                                                        stride, nullptr);
+                                                        stride, nullptr); sw::count_launch();
   SW_CHECK_LAUNCH("sw_init_bernoulli_fill");
   return SW_OK;
 }

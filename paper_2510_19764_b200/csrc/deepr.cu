@@ -332,7 +332,7 @@ extern "C" int sw_bitfield_randomize(const sw_bitfield_t* bf, uint64_t key, void
   const uint64_t mask = tail >= 64 ? ~0ull : ((1ull << tail) - 1ull);
   const int64_t total = (int64_t)bf->num_pre * bf->words_per_row;
   if (total == 0) return SW_OK;
-  k_bf_randomize<<<flat_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(*bf, key, mask);
+  k_bf_randomize<<<flat_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(*bf, key, mask); sw::count_launch();
   SW_CHECK_LAUNCH("sw_bitfield_randomize");
   return SW_OK;
 }
@@ -345,7 +345,7 @@ extern "C" int sw_deepr_init_bitfields(const sw_ragged_t* m, int32_t wp, const s
   cudaMemsetAsync(conn->words, 0, (size_t)conn->num_pre * conn->words_per_row * 8, (cudaStream_t)stream);
   const int64_t total = (int64_t)m->num_pre * m->stride;
   if (total == 0) return SW_OK;
-  k_deepr_init_bits<<<flat_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(*m, wp, *sign, *conn);
+  k_deepr_init_bits<<<flat_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(*m, wp, *sign, *conn); sw::count_launch();
   SW_CHECK_LAUNCH("sw_deepr_init_bitfields");
   return SW_OK;
 }
@@ -356,7 +356,7 @@ extern "C" int sw_deepr_l1(const sw_ragged_t* m, int32_t gp, const sw_bitfield_t
   if (l1 == 0.0) return SW_OK;   // deep_r.py:74-75
   const int64_t total = (int64_t)m->num_pre * m->stride;
   if (total == 0) return SW_OK;
-  k_deepr_l1<<<flat_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(*m, gp, *sign, l1);
+  k_deepr_l1<<<flat_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(*m, gp, *sign, l1); sw::count_launch();
   SW_CHECK_LAUNCH("sw_deepr_l1");
   return SW_OK;
 }
@@ -375,7 +375,7 @@ extern "C" int sw_deepr_eliminate(const sw_ragged_t* m, int32_t wp, const sw_bit
   if (m->num_pre == 0) return SW_OK;
   const int smem = elim_smem(m);
   if (int s = set_smem((const void*)k_deepr_eliminate, smem)) return s;
-  k_deepr_eliminate<<<rows_grid(m->num_pre), kThreads, smem, (cudaStream_t)stream>>>(*m, wp, *sign, *conn, dormant);
+  k_deepr_eliminate<<<rows_grid(m->num_pre), kThreads, smem, (cudaStream_t)stream>>>(*m, wp, *sign, *conn, dormant); sw::count_launch();
   SW_CHECK_LAUNCH("sw_deepr_eliminate");
   return SW_OK;
 }
@@ -386,7 +386,7 @@ extern "C" int sw_ragged_remove_marked(const sw_ragged_t* m, const uint8_t* mark
   if (m->num_pre == 0) return SW_OK;
   const int smem = elim_smem(m);
   if (int s = set_smem((const void*)k_remove_marked, smem)) return s;
-  k_remove_marked<<<rows_grid(m->num_pre), kThreads, smem, (cudaStream_t)stream>>>(*m, marked, removed);
+  k_remove_marked<<<rows_grid(m->num_pre), kThreads, smem, (cudaStream_t)stream>>>(*m, marked, removed); sw::count_launch();
   SW_CHECK_LAUNCH("sw_ragged_remove_marked");
   return SW_OK;
 }
@@ -400,11 +400,11 @@ extern "C" int sw_deepr_form_pass(const sw_ragged_t* m, const sw_bitfield_t* con
   cudaMemsetAsync(counters, 0, 4 * sizeof(int64_t), st);
   if (P == 0) return SW_OK;
   cudaMemsetAsync(act, 0, (size_t)P * sizeof(int32_t), st);
-  k_sum_i64<<<flat_grid(P, 256), 256, 0, st>>>(pending_src, P, counters);
+  k_sum_i64<<<flat_grid(P, 256), 256, 0, st>>>(pending_src, P, counters); sw::count_launch();
   const uint64_t rem = sw::reject_rem((uint64_t)P);
-  k_form_hist<<<148 * 8, 256, 0, st>>>(counters, host_key, (uint64_t)P, rem, act);
-  if (rem != 0) k_form_hist_fix<<<1, 1, 0, st>>>(counters, host_key, (uint64_t)P, rem, act);
-  k_deepr_form_rows<<<rows_grid(P), kThreads, 0, st>>>(*m, *conn, excl_diag, row_base, act, unplaced, counters);
+  k_form_hist<<<148 * 8, 256, 0, st>>>(counters, host_key, (uint64_t)P, rem, act); sw::count_launch();
+  if (rem != 0) { k_form_hist_fix<<<1, 1, 0, st>>>(counters, host_key, (uint64_t)P, rem, act); sw::count_launch(); }
+  k_deepr_form_rows<<<rows_grid(P), kThreads, 0, st>>>(*m, *conn, excl_diag, row_base, act, unplaced, counters); sw::count_launch();
   SW_CHECK_LAUNCH("sw_deepr_form_pass");
   return SW_OK;
 }

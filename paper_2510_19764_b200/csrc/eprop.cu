@@ -255,7 +255,7 @@ extern "C" int sw_eprop_accumulate_batch(const int32_t* targets, const int32_t* 
   if (total == 0) return SW_OK;
   k_eprop_ref<<<grid1(total), 256, 0, (cudaStream_t)stream>>>(targets, row_length, num_pre, stride,
                                                               pre_trace, psi, lsig, batch, num_post,
-                                                              eps, ebar, grad, beta, rho, alpha);
+                                                              eps, ebar, grad, beta, rho, alpha); sw::count_launch();
   SW_CHECK_LAUNCH("sw_eprop_accumulate_batch");
   return SW_OK;
 }
@@ -272,29 +272,29 @@ extern "C" int sw_eprop_plan(const int32_t* row_length, const int32_t* target, i
   int32_t* cursor = scratch + n;
   cudaMemsetAsync(counts, 0, (size_t)n * 4, st);
   if (num_pre > 0) {
-    k_bucket_count<<<grid1(num_pre), 256, 0, st>>>(row_length, target, num_pre, stride, shift, counts);
-    k_scan_excl<<<1, 1024, 0, st>>>(counts, n, total);
+    k_bucket_count<<<grid1(num_pre), 256, 0, st>>>(row_length, target, num_pre, stride, shift, counts); sw::count_launch();
+    k_scan_excl<<<1, 1024, 0, st>>>(counts, n, total); sw::count_launch();
     cudaMemcpyAsync(cursor, counts, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
     k_bucket_fill<<<grid1(num_pre), 256, 0, st>>>(row_length, target, num_pre, stride, shift, cursor,
-                                                  out_pre, out_post, out_off);
+                                                  out_pre, out_post, out_off); sw::count_launch();
   } else {
     cudaMemsetAsync(total, 0, 4, st);
   }
-  k_plan_pad<<<grid1(e_pad), 256, 0, st>>>(out_pre, out_post, out_off, total, e_pad);
+  k_plan_pad<<<grid1(e_pad), 256, 0, st>>>(out_pre, out_post, out_off, total, e_pad); sw::count_launch();
   SW_CHECK_LAUNCH("sw_eprop_plan");
   return SW_OK;
 }
 
 extern "C" int sw_gather_f64(const double* plane, const int32_t* off, int32_t n, double* out, void* stream) {
   if (n <= 0) return SW_OK;
-  k_gather_f64<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(plane, off, n, out);
+  k_gather_f64<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(plane, off, n, out); sw::count_launch();
   SW_CHECK_LAUNCH("sw_gather_f64");
   return SW_OK;
 }
 
 extern "C" int sw_scatter_f64(double* plane, const int32_t* off, int32_t n, const double* in, void* stream) {
   if (n <= 0) return SW_OK;
-  k_scatter_f64<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(plane, off, n, in);
+  k_scatter_f64<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(plane, off, n, in); sw::count_launch();
   SW_CHECK_LAUNCH("sw_scatter_f64");
   return SW_OK;
 }
@@ -316,7 +316,7 @@ extern "C" int sw_eprop_fused_step(const sw_eprop_seg_t* segs, int32_t n_segs, c
   const int grid = s[0].tiles + s[1].tiles + ro_blocks;
   if (grid == 0) return SW_OK;
   k_eprop_fused<<<grid, kNW * 32, 0, (cudaStream_t)stream>>>(s[0], s[1], psi, lsig, batch, hidden,
-                                                             beta, rho, alpha, ro);
+                                                             beta, rho, alpha, ro); sw::count_launch();
   SW_CHECK_LAUNCH("sw_eprop_fused_step");
   return SW_OK;
 }

@@ -99,7 +99,7 @@ int grid1(int64_t n) {
 extern "C" int sw_alif_step(float* v, float* a, float* z, const float* rec, const float* ext,
                             int64_t n, float alpha, float rho, float beta, float v_thr, void* stream) {
   if (n <= 0) return SW_OK;
-  k_alif_step<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(v, a, z, rec, ext, n, alpha, rho, beta, v_thr);
+  k_alif_step<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(v, a, z, rec, ext, n, alpha, rho, beta, v_thr); sw::count_launch();
   SW_CHECK_LAUNCH("sw_alif_step");
   return SW_OK;
 }
@@ -107,7 +107,7 @@ extern "C" int sw_alif_step(float* v, float* a, float* z, const float* rec, cons
 extern "C" int sw_alif_surrogate(const float* v, const float* a, float* psi, int64_t n, float beta,
                                  float v_thr, void* stream) {
   if (n <= 0) return SW_OK;
-  k_alif_surrogate<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(v, a, psi, n, beta, v_thr);
+  k_alif_surrogate<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(v, a, psi, n, beta, v_thr); sw::count_launch();
   SW_CHECK_LAUNCH("sw_alif_surrogate");
   return SW_OK;
 }
@@ -120,7 +120,7 @@ extern "C" int sw_lif_cond_step(double* V, double* g, int64_t* ref_until, const 
   if (n <= 0) return SW_OK;
   k_lif_cond_step<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(
       V, g, ref_until, incoming, n, step_index, decay_s, g_leak, v_rest, e_exc, v_theta, v_reset, h,
-      tau_m, ref_steps, spike_bits, nullptr, nullptr);
+      tau_m, ref_steps, spike_bits, nullptr, nullptr); sw::count_launch();
   SW_CHECK_LAUNCH("sw_lif_cond_step");
   return SW_OK;
 }
@@ -128,7 +128,7 @@ extern "C" int sw_lif_cond_step(double* V, double* g, int64_t* ref_until, const 
 extern "C" int sw_poisson_step(uint64_t key, int64_t counter0, const double* p, int32_t n,
                                uint32_t* spike_bits, void* stream) {
   if (n <= 0) return SW_OK;
-  k_poisson_step<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(key, counter0, p, n, spike_bits);
+  k_poisson_step<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(key, counter0, p, n, spike_bits); sw::count_launch();
   SW_CHECK_LAUNCH("sw_poisson_step");
   return SW_OK;
 }
