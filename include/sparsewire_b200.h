@@ -174,8 +174,8 @@ typedef struct sw_eprop_seg {
   const int32_t* pre;       /* [e_pad] presynaptic index   */
   const int32_t* post;      /* [e_pad] postsynaptic index  */
   const float* pre_trace;   /* [B, num_pre] xbar or zbar   */
-  float* eps;               /* [B, e_pad]                  */
-  float* ebar;              /* [B, e_pad]                  */
+  float* eps;               /* [e_pad/32, B, 32] tile-major */
+  float* ebar;              /* [e_pad/32, B, 32]            */
   double* grad;             /* [e_pad] compact gradient    */
   int32_t num_pre;
   int32_t e_pad;            /* multiple of 32              */
@@ -184,12 +184,14 @@ typedef struct sw_eprop_seg {
 /* Fused hot-path step: both projections' eligibility recursion and
  * gradient accumulation (bit-identical to eprop_accumulate_batch on the
  * same synapses) plus, when d != NULL, the readout gradients
- * g_w_out[C,H] += d^T zbar and g_b_out[C] += sum_b d (classifier.py:221-222). */
+ * g_w_out[C,H] += d^T zbar and g_b_out[C] += sum_b d (classifier.py:221-222).
+ * workspace: 2 uint32 zeroed once by the caller (tile tickets; the kernel
+ * leaves them zeroed, so the launch can be captured in a CUDA graph). */
 SW_API int sw_eprop_fused_step(const sw_eprop_seg_t* segs, int32_t n_segs, const float* psi,
                                const float* lsig, int32_t batch, int32_t hidden, float beta,
                                float rho, float alpha, const double* d, const float* zbar,
                                double* g_w_out, double* g_b_out, int32_t num_classes,
-                               void* stream);
+                               uint32_t* workspace, void* stream);
 
 /* ---- neurons (neurons.py) --------------------------------------------------- */
 /* AlifLayer.step (neurons.py:60-67), float32, n = batch*hidden elements. */

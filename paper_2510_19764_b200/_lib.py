@@ -79,7 +79,7 @@ SIGNATURES: dict[str, list] = {
     "sw_eprop_plan": [P, P, I32, I32, I32, I32, P, P, P, P, I32, P, P],
     "sw_gather_f64": [P, P, I32, P, P],
     "sw_scatter_f64": [P, P, I32, P, P],
-    "sw_eprop_fused_step": [C.c_void_p, I32, P, P, I32, I32, F32, F32, F32, P, P, P, P, I32, P],
+    "sw_eprop_fused_step": [C.c_void_p, I32, P, P, I32, I32, F32, F32, F32, P, P, P, P, I32, P, P],
     "sw_alif_step": [P, P, P, P, P, I64, F32, F32, F32, F32, P],
     "sw_alif_surrogate": [P, P, P, I64, F32, F32, P],
     "sw_lif_cond_step": [P, P, P, P, I32, I64, F64, F64, F64, F64, F64, F64, F64, F64, I64, P, P],
@@ -135,6 +135,19 @@ def call(name: str, *args) -> None:
     if st != 0:
         msg = (L.sw_last_error() or b"").decode(errors="replace")
         raise errors.from_status(st, f"{name}: {msg}")
+
+
+_ws = {}
+
+
+def workspace(device=None) -> int:
+    """Per-device zeroed scratch words for the kernels' tile tickets."""
+    dev = torch.cuda.current_device() if device is None else device
+    t = _ws.get(dev)
+    if t is None:
+        t = torch.zeros(64, dtype=torch.int32, device=f"cuda:{dev}")
+        _ws[dev] = t
+    return t.data_ptr()
 
 
 def launch_count() -> int:

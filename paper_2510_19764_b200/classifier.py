@@ -120,7 +120,8 @@ class _Plan:
         self.post = torch.zeros(e_pad, dtype=torch.int32, device=dev)
         self.off = torch.zeros(e_pad, dtype=torch.int32, device=dev)
         self.grad = torch.zeros(e_pad, dtype=torch.float64, device=dev)
-        self.eps = torch.zeros((self.batch, e_pad), dtype=torch.float32, device=dev)
+        # tile-major eligibility state [tile, replica, lane] (sw_eprop_fused_step)
+        self.eps = torch.zeros((e_pad // 32, self.batch, 32), dtype=torch.float32, device=dev)
         self.ebar = torch.zeros_like(self.eps)
 
     def build(self) -> None:
@@ -236,6 +237,7 @@ class EpropClassifierTrainer:
         self.plan_in = _Plan(self.m_in, B)
         self.plan_rec = _Plan(self.m_rec, B)
         self._segs = (_lib.EpropSeg * 2)()
+        _lib.workspace()   # allocate the ticket words outside any graph capture
 
     # -- per-step launches ------------------------------------------------------------
     def _step_params(self, t: int) -> _lib.ClfStep:
@@ -271,7 +273,7 @@ class EpropClassifierTrainer:
                           self.psi.data_ptr(), self.lsig.data_ptr(), self.local_b, self.hidden,
                           b32, r32, a32, self.d.data_ptr(), self.zbar.data_ptr(),
                           self.g_w_out.data_ptr(), self.g_b_out.data_ptr(),
-                          self.task.num_classes, st)
+                          self.task.num_classes, _lib.workspace(), st)
         self.steps_launched += self.task.example_steps
 
     def _run_trial(self, learn: bool) -> None:

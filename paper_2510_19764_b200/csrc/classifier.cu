@@ -83,6 +83,19 @@ __device__ void warp_accumulate_rows(const int* list, int n, const int32_t* __re
   }
 }
 
+constexpr int kStageCap = 4096;   // staged (target, w) entries of the spiking rows
+
+// Ordered adds of staged rows: rows r0..r1-1 of the staged list, each row's
+// entries [off[r], off[r+1]) added by the lanes; rows strictly in order.
+__device__ __forceinline__ void warp_add_staged(const int* off, int r0, int r1, const int* st_t,
+                                                const float* st_w, float* acc) {
+  const int lane = threadIdx.x & 31;
+  for (int r = r0; r < r1; ++r) {
+    for (int q = off[r] + lane; q < off[r + 1]; q += 32) acc[st_t[q]] = __fadd_rn(acc[st_t[q]], st_w[q]);
+    __syncwarp();
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_clf_step(sw_clf_step_t P) {
   extern __shared__ unsigned char smem_raw[];
   const int H = P.hidden, NI = P.num_inputs, C = P.num_classes;
@@ -90,7 +103,10 @@ __global__ void __launch_bounds__(kThreads) k_clf_step(sw_clf_step_t P) {
   float* acc_rec = acc_ext + H;
   int* xlist = (int*)(acc_rec + H);
   int* zlist = xlist + NI;
-  double* yv = (double*)(((uintptr_t)(zlist + H) + 15) & ~(uintptr_t)15);
+  int* roff = zlist + H;                    // [NI + H + 1] staged row offsets
+  int* st_t = roff + NI + H + 1;            // [kStageCap]
+  float* st_w = (float*)(st_t + kStageCap); // [kStageCap]
+  double* yv = (double*)(((uintptr_t)(st_w + kStageCap) + 15) & ~(uintptr_t)15);
   double* dv = yv + C;
   __shared__ int warp_cnt[kWarps];
   __shared__ int nx, nz;
@@ -98,35 +114,79 @@ __global__ void __launch_bounds__(kThreads) k_clf_step(sw_clf_step_t P) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t bH = (int64_t)b * H, bI = (int64_t)b * NI, bC = (int64_t)b * C;
 
-  // 1. input spikes + xbar (classifier.py:63-67, 212-213)
+  // 1. input spikes (classifier.py:63-67) + xbar (:212-213), one draw per input
   const uint64_t key = P.ex_key[b];
   const uint64_t c0 = (uint64_t)P.t * (uint64_t)NI;
   const double* pin = P.p_in + bI;
-  auto xspk = [&](int k) { return sw::u01(sw::draw(key, c0 + (uint64_t)k)) < pin[k]; };
+  auto xspk = [&](int k) {
+    const bool f = sw::u01(sw::draw(key, c0 + (uint64_t)k)) < pin[k];
+    P.xbar[bI + k] = __fadd_rn(__fmul_rn(P.xbar[bI + k], P.alpha), f ? 1.0f : 0.0f);
+    return f;
+  };
   block_compact(NI, xspk, xlist, &nx, warp_cnt);
-  for (int k = threadIdx.x; k < NI; k += kThreads) {
-    const float x = xspk(k) ? 1.0f : 0.0f;
-    P.xbar[bI + k] = __fadd_rn(__fmul_rn(P.xbar[bI + k], P.alpha), x);
-  }
   // 2. hidden spike list (old z) + zbar (classifier.py:207, 210-211)
   const float* z = P.z + bH;
-  block_compact(H, [&](int h) { return z[h] != 0.0f; }, zlist, &nz, warp_cnt);
-  for (int h = threadIdx.x; h < H; h += kThreads) {
-    P.zbar[bH + h] = __fadd_rn(__fmul_rn(P.zbar[bH + h], P.alpha), z[h]);
+  block_compact(H, [&](int h) {
+    const float zh = z[h];
+    P.zbar[bH + h] = __fadd_rn(__fmul_rn(P.zbar[bH + h], P.alpha), zh);
     acc_ext[h] = 0.0f;
     acc_rec[h] = 0.0f;
+    return zh != 0.0f;
+  }, zlist, &nz, warp_cnt);
+  // 3a. lengths of the spiking rows -> staged offsets (warp 0 scan)
+  const int nrows = nx + nz;
+  for (int r = threadIdx.x; r < nrows; r += kThreads)
+    roff[r + 1] = (r < nx) ? __ldg(P.in_row_length + xlist[r]) : __ldg(P.rec_row_length + zlist[r - nx]);
+  __syncthreads();
+  if (warp == 0) {
+    int carry = 0;
+    for (int base = 0; base < nrows; base += 32) {
+      const int r = base + lane;
+      int v = r < nrows ? roff[r + 1] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(SW_FULL_MASK, v, o);
+        if (lane >= o) v += t;
+      }
+      if (r < nrows) roff[r + 1] = carry + v;
+      carry += __shfl_sync(SW_FULL_MASK, v, 31);
+    }
+    if (lane == 0) roff[0] = 0;
   }
   __syncthreads();
-  // 3. event-driven propagation
-  if (warp == 0) warp_accumulate_rows(xlist, nx, P.in_row_length, P.in_target, P.in_w32, P.in_stride, acc_ext);
-  else if (warp == 1) warp_accumulate_rows(zlist, nz, P.rec_row_length, P.rec_target, P.rec_w32, P.rec_stride, acc_rec);
-  // 5a. readout y = alpha*y + z @ W_out^T + b (classifier.py:215), warps over classes
-  for (int c = warp; c < C; c += kWarps) {
-    double s = 0.0;
-    for (int q = lane; q < nz; q += 32) s += P.w_out[(int64_t)c * H + zlist[q]];
+  const bool staged = roff[nrows] <= kStageCap;
+  // 3b. stage every spiking row's (target, w) with coalesced loads, all warps
+  if (staged) {
+    for (int r = warp; r < nrows; r += kWarps) {
+      const bool in = r < nx;
+      const int i = in ? xlist[r] : zlist[r - nx];
+      const int64_t o = (int64_t)i * (in ? P.in_stride : P.rec_stride);
+      const int32_t* tg = (in ? P.in_target : P.rec_target) + o;
+      const float* wv = (in ? P.in_w32 : P.rec_w32) + o;
+      const int q0 = roff[r], len = roff[r + 1] - q0;
+      for (int c = lane; c < len; c += 32) {
+        st_t[q0 + c] = __ldg(tg + c);
+        st_w[q0 + c] = __ldg(wv + c);
+      }
+    }
+  }
+  __syncthreads();
+  // 3c. ordered event-driven accumulation (warp 0: input rows, warp 1: hidden rows)
+  if (warp == 0) {
+    if (staged) warp_add_staged(roff, 0, nx, st_t, st_w, acc_ext);
+    else warp_accumulate_rows(xlist, nx, P.in_row_length, P.in_target, P.in_w32, P.in_stride, acc_ext);
+  } else if (warp == 1) {
+    if (staged) warp_add_staged(roff, nx, nrows, st_t, st_w, acc_rec);
+    else warp_accumulate_rows(zlist, nz, P.rec_row_length, P.rec_target, P.rec_w32, P.rec_stride, acc_rec);
+  } else {
+    // 5a. readout y = alpha*y + z @ W_out^T + b (classifier.py:215), warps 2.. over classes
+    for (int c = warp - 2; c < C; c += kWarps - 2) {
+      double s = 0.0;
+      for (int q = lane; q < nz; q += 32) s += __ldg(P.w_out + (int64_t)c * H + zlist[q]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(SW_FULL_MASK, s, o);
-    if (lane == 0) yv[c] = __dadd_rn(__dadd_rn(__dmul_rn(P.alpha64, P.y[bC + c]), s), P.b_out[c]);
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(SW_FULL_MASK, s, o);
+      if (lane == 0) yv[c] = __dadd_rn(__dadd_rn(__dmul_rn(P.alpha64, P.y[bC + c]), s), P.b_out[c]);
+    }
   }
   __syncthreads();
   // 5b. softmax / cross-entropy / d (plasticity.py:156-165, classifier.py:216-219)
@@ -159,7 +219,7 @@ __global__ void __launch_bounds__(kThreads) k_clf_step(sw_clf_step_t P) {
     const float r = __fsub_rn(1.0f, fabsf(cc));
     P.psi[bH + h] = __fmul_rn(0.5f, (r > 0.0f || r != r) ? r : 0.0f);
     double ls = 0.0;
-    for (int c = 0; c < C; ++c) ls = __dadd_rn(ls, __dmul_rn(dv[c], P.w_out[(int64_t)c * H + h]));
+    for (int c = 0; c < C; ++c) ls = __dadd_rn(ls, __dmul_rn(dv[c], __ldg(P.w_out + (int64_t)c * H + h)));
     P.lsig[bH + h] = __double2float_rn(ls);
     float vv = __fmul_rn(P.alpha, __fsub_rn(vo, __fmul_rn(zo, P.v_thr)));
     vv = __fadd_rn(__fadd_rn(vv, acc_rec[h]), acc_ext[h]);
@@ -220,7 +280,8 @@ int grid1(int64_t n) {
 extern "C" int sw_clf_step(const sw_clf_step_t* p, void* stream) {
   const int H = p->hidden, NI = p->num_inputs, C = p->num_classes;
   if (p->batch <= 0) return SW_OK;
-  const size_t smem = (size_t)(2 * H) * 4 + (size_t)(NI + H) * 4 + 16 + (size_t)2 * C * 8;
+  const size_t smem = (size_t)(2 * H) * 4 + (size_t)(NI + H) * 4 + (size_t)(NI + H + 1) * 4 +
+                      (size_t)kStageCap * 8 + 16 + (size_t)2 * C * 8;
   if (smem > 48 * 1024) {
     if (smem > 227 * 1024) { sw::set_last_error("clf_step: layer too large"); return SW_ERR_INVALID_ARG; }
     cudaFuncSetAttribute((const void*)k_clf_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -21,6 +21,7 @@
 //    g_w_out += d^T zbar, g_b_out += sum_b d (classifier.py:221-222).
 #include "common.cuh"
 
+
 namespace {
 
 __global__ void k_eprop_ref(const int32_t* targets, const int32_t* row_length, int P, int S,
@@ -128,116 +129,6 @@ __global__ void k_scatter_f64(double* plane, const int32_t* off, int n, const do
     if (off[e] >= 0) plane[off[e]] = in[e];
 }
 
-// ---- fused hot-path step ----------------------------------------------------------------
-struct Seg {
-  const int32_t* pre;
-  const int32_t* post;
-  const float* trace;   // [B, P]
-  float* eps;           // [B, E_pad]
-  float* ebar;
-  double* grad;         // [E_pad]
-  int P;
-  int e_pad;
-  int tiles;
-};
-
-struct ReadoutArgs {
-  const double* d;      // [B, C]
-  const float* zbar;    // [B, H]
-  double* g_w_out;      // [C, H]
-  double* g_b_out;      // [C]
-  int C;
-};
-
-constexpr int kNW = 8;     // warps per block
-constexpr int kBPW = 8;    // replicas per warp per chunk
-constexpr int kChunk = kNW * kBPW;
-
-__global__ void __launch_bounds__(kNW * 32)
-k_eprop_fused(Seg s0, Seg s1, const float* __restrict__ psi, const float* __restrict__ lsig,
-              int B, int H, float beta, float rho, float alpha, ReadoutArgs ro) {
-  __shared__ float terms[kChunk][33];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int tile = blockIdx.x;
-  if (tile >= s0.tiles + s1.tiles) {
-    // readout-gradient blocks: block r covers classes x 32-post tile
-    const int r = tile - s0.tiles - s1.tiles;
-    const int htiles = (H + 31) / 32;
-    const int c = r / htiles, h = (r % htiles) * 32 + lane;
-    __shared__ double part[kNW][33];
-    double acc = 0.0, accb = 0.0;
-    if (h < H) {
-      for (int b = warp; b < B; b += kNW) {
-        const double dv = ro.d[(int64_t)b * ro.C + c];
-        acc += dv * (double)ro.zbar[(int64_t)b * H + h];
-        accb += dv;
-      }
-    }
-    part[warp][lane] = acc;
-    __syncthreads();
-    if (warp == 0 && h < H) {
-      double t = 0.0;
-      for (int w = 0; w < kNW; ++w) t += part[w][lane];
-      ro.g_w_out[(int64_t)c * H + h] += t;
-    }
-    __syncthreads();
-    if ((r % htiles) == 0) {
-      part[warp][lane] = accb;   // same for all lanes (h-independent); lane 0 carries it
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < kNW; ++w) t += part[w][0];
-        ro.g_b_out[c] += t;
-      }
-    }
-    return;
-  }
-  const Seg& sg = (tile < s0.tiles) ? s0 : s1;
-  if (tile >= s0.tiles) tile -= s0.tiles;
-  const int e = tile * 32 + lane;
-  const int pre = sg.pre[e];
-  const int post = sg.post[e];
-  const float* trace = sg.trace + pre;
-  const float* ps = psi + post;
-  const float* ls = lsig + post;
-  float* eps = sg.eps + e;
-  float* ebar = sg.ebar + e;
-  const int64_t ES = sg.e_pad;
-  double g = (warp == 0) ? sg.grad[e] : 0.0;
-  for (int b0 = 0; b0 < B; b0 += kChunk) {
-    float zb[kBPW], p[kBPW], l[kBPW], ep[kBPW], eb[kBPW];
-#pragma unroll
-    for (int q = 0; q < kBPW; ++q) {
-      const int b = b0 + warp * kBPW + q;
-      if (b < B) {
-        zb[q] = __ldg(trace + (int64_t)b * sg.P);
-        p[q] = __ldg(ps + (int64_t)b * H);
-        l[q] = __ldg(ls + (int64_t)b * H);
-        ep[q] = __ldcs(eps + b * ES);
-        eb[q] = __ldcs(ebar + b * ES);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < kBPW; ++q) {
-      const int b = b0 + warp * kBPW + q;
-      if (b < B) {
-        const float ee = __fmul_rn(p[q], __fsub_rn(zb[q], __fmul_rn(beta, ep[q])));
-        const float ebn = __fadd_rn(__fmul_rn(alpha, eb[q]), ee);
-        __stcs(ebar + b * ES, ebn);
-        __stcs(eps + b * ES, __fadd_rn(__fmul_rn(rho, ep[q]), ee));
-        terms[warp * kBPW + q][lane] = __fmul_rn(l[q], ebn);
-      }
-    }
-    __syncthreads();
-    if (warp == 0) {
-      const int nb = min(kChunk, B - b0);
-      for (int r = 0; r < nb; ++r) g = __dadd_rn(g, (double)terms[r][lane]);
-    }
-    __syncthreads();
-  }
-  if (warp == 0) sg.grad[e] = g;
-}
-
 int grid1(int64_t n) {
   int64_t g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
@@ -299,24 +190,3 @@ extern "C" int sw_scatter_f64(double* plane, const int32_t* off, int32_t n, cons
   return SW_OK;
 }
 
-extern "C" int sw_eprop_fused_step(const sw_eprop_seg_t* segs, int32_t n_segs, const float* psi,
-                                   const float* lsig, int32_t batch, int32_t hidden, float beta,
-                                   float rho, float alpha, const double* d, const float* zbar,
-                                   double* g_w_out, double* g_b_out, int32_t num_classes,
-                                   void* stream) {
-  if (n_segs < 1 || n_segs > 2) { sw::set_last_error("eprop: 1 or 2 segments"); return SW_ERR_INVALID_ARG; }
-  Seg s[2] = {};
-  for (int k = 0; k < n_segs; ++k) {
-    const sw_eprop_seg_t& q = segs[k];
-    if (q.e_pad % 32) { sw::set_last_error("eprop: e_pad must be a multiple of 32"); return SW_ERR_INVALID_ARG; }
-    s[k] = Seg{q.pre, q.post, q.pre_trace, q.eps, q.ebar, q.grad, q.num_pre, q.e_pad, q.e_pad / 32};
-  }
-  ReadoutArgs ro{d, zbar, g_w_out, g_b_out, num_classes};
-  const int ro_blocks = (d && num_classes > 0) ? num_classes * ((hidden + 31) / 32) : 0;
-  const int grid = s[0].tiles + s[1].tiles + ro_blocks;
-  if (grid == 0) return SW_OK;
-  k_eprop_fused<<<grid, kNW * 32, 0, (cudaStream_t)stream>>>(s[0], s[1], psi, lsig, batch, hidden,
-                                                             beta, rho, alpha, ro); sw::count_launch();
-  SW_CHECK_LAUNCH("sw_eprop_fused_step");
-  return SW_OK;
-}

@@ -82,16 +82,19 @@ def test_fused_eprop_equals_reference_layout(dev_lib, B, P, H, cap, R):
         segs[0] = plan.seg(trace)
         _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 1, psi.data_ptr(),
                   lsig.data_ptr(), B, H, float(np.float32(0.0174)), float(np.float32(0.9995)),
-                  float(np.float32(0.95)), None, None, None, None, 0, _lib.stream_ptr())
+                  float(np.float32(0.95)), None, None, None, None, 0, _lib.workspace(),
+                  _lib.stream_ptr())
     _lib.call("sw_scatter_f64", gplane.data_ptr(), plan.off.data_ptr(), plan.e_pad,
               plan.grad.data_ptr(), _lib.stream_ptr())
     assert valid_equal(rl, gplane.cpu().numpy(), ref_grad.cpu().numpy())
     off = plan.off.cpu().numpy()
     E = int(rl.sum())
+    def flat(t):   # [tile, B, 32] -> [B, e_pad]
+        return t.permute(1, 0, 2).reshape(B, -1).cpu().numpy()
     re = ref_eps.reshape(B, -1).cpu().numpy()[:, off[:E]]
-    assert np.array_equal(plan.eps.cpu().numpy()[:, :E], re)
+    assert np.array_equal(flat(plan.eps)[:, :E], re)
     rb = ref_ebar.reshape(B, -1).cpu().numpy()[:, off[:E]]
-    assert np.array_equal(plan.ebar.cpu().numpy()[:, :E], rb)
+    assert np.array_equal(flat(plan.ebar)[:, :E], rb)
 
 
 def _small_trainer(use_graph=True):
