@@ -20,188 +20,320 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-// Block-wide ascending compaction of flags over [0, n): list gets the
-// indices with flag set, *count the number.  flag_fn(k) -> bool.
-template <typename F>
-__device__ void block_compact(int n, F flag_fn, int* list, int* count, int* warp_cnt) {
+constexpr int kStageCap = 2048;   // staged (target, w) entries of the spiking rows
+constexpr int kPerThread = 8;     // (NI + H) <= kThreads * kPerThread
+
+// Block-wide exclusive scan of two ints (count, length-sum); returns the
+// exclusive prefixes for this thread and the totals.
+__device__ __forceinline__ void block_scan2(int a, int b, int& ea, int& eb, int& ta, int& tb,
+                                            int2* wsum) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) *count = 0;
+  int ia = a, ib = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int xa = __shfl_up_sync(SW_FULL_MASK, ia, o);
+    const int xb = __shfl_up_sync(SW_FULL_MASK, ib, o);
+    if (lane >= o) { ia += xa; ib += xb; }
+  }
+  if (lane == 31) wsum[warp] = make_int2(ia, ib);
   __syncthreads();
-  for (int base = 0; base < n; base += kThreads) {
-    const int k = base + threadIdx.x;
-    const bool f = (k < n) && flag_fn(k);
-    const unsigned b = __ballot_sync(SW_FULL_MASK, f);
-    if (lane == 0) warp_cnt[warp] = __popc(b);
-    __syncthreads();
-    int before = *count;
-    for (int w = 0; w < warp; ++w) before += warp_cnt[w];
-    if (f) list[before + __popc(b & sw::lanemask_lt())] = k;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int tot = 0;
-      for (int w = 0; w < kWarps; ++w) tot += warp_cnt[w];
-      *count += tot;
-    }
-    __syncthreads();
-  }
-}
-
-// Warp-serial ascending-row accumulation into shared memory.
-__device__ void warp_accumulate_rows(const int* list, int n, const int32_t* __restrict__ row_length,
-                                     const int32_t* __restrict__ target, const float* __restrict__ w32,
-                                     int stride, float* acc) {
-  const int lane = threadIdx.x & 31;
-  for (int r0 = 0; r0 < n; r0 += 4) {
-    int len[4], t[4];
-    float w[4];
-    int64_t off[4];
+  int pa = 0, pb = 0;
+  ta = 0;
+  tb = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      len[u] = 0;
-      t[u] = 0;
-      w[u] = 0.f;
-      off[u] = 0;
-      if (r0 + u < n) {
-        const int i = list[r0 + u];
-        off[u] = (int64_t)i * stride;
-        len[u] = __ldg(row_length + i);
-        if (lane < len[u]) {
-          t[u] = __ldg(target + off[u] + lane);
-          w[u] = __ldg(w32 + off[u] + lane);
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (lane < len[u]) acc[t[u]] = __fadd_rn(acc[t[u]], w[u]);
-      for (int c = 32 + lane; c < len[u]; c += 32) {
-        const int tt = __ldg(target + off[u] + c);
-        acc[tt] = __fadd_rn(acc[tt], __ldg(w32 + off[u] + c));
-      }
-      __syncwarp();
-    }
+  for (int w = 0; w < kWarps; ++w) {
+    const int2 v = wsum[w];
+    if (w < warp) { pa += v.x; pb += v.y; }
+    ta += v.x;
+    tb += v.y;
   }
+  ea = pa + ia - a;
+  eb = pb + ib - b;
 }
 
-constexpr int kStageCap = 4096;   // staged (target, w) entries of the spiking rows
-
-// Ordered adds of staged rows: rows r0..r1-1 of the staged list, each row's
-// entries [off[r], off[r+1]) added by the lanes; rows strictly in order.
-__device__ __forceinline__ void warp_add_staged(const int* off, int r0, int r1, const int* st_t,
-                                                const float* st_w, float* acc) {
-  const int lane = threadIdx.x & 31;
-  for (int r = r0; r < r1; ++r) {
-    for (int q = off[r] + lane; q < off[r + 1]; q += 32) acc[st_t[q]] = __fadd_rn(acc[st_t[q]], st_w[q]);
-    __syncwarp();
-  }
-}
+// Phase timestamps of one block (clock64), compiled in with -DSW_CLF_PROF;
+// read back with sw_debug_clf_prof (tools/timing_breakdown.py).
+__device__ long long g_clf_prof[16];
+#ifdef SW_CLF_PROF
+#define PROF(i) do { if (blockIdx.x == 7 && threadIdx.x == 0) g_clf_prof[i] = clock64(); } while (0)
+#else
+#define PROF(i) do { } while (0)
+#endif
 
 __global__ void __launch_bounds__(kThreads) k_clf_step(sw_clf_step_t P) {
   extern __shared__ unsigned char smem_raw[];
   const int H = P.hidden, NI = P.num_inputs, C = P.num_classes;
+  const int NT = NI + H;
   float* acc_ext = (float*)smem_raw;
   float* acc_rec = acc_ext + H;
-  int* xlist = (int*)(acc_rec + H);
-  int* zlist = xlist + NI;
-  int* roff = zlist + H;                    // [NI + H + 1] staged row offsets
-  int* st_t = roff + NI + H + 1;            // [kStageCap]
-  float* st_w = (float*)(st_t + kStageCap); // [kStageCap]
-  double* yv = (double*)(((uintptr_t)(st_w + kStageCap) + 15) & ~(uintptr_t)15);
+  int* rlen = (int*)(acc_rec + H);          // [NT] row lengths (inputs | hidden)
+  int* list = rlen + NT;                    // [NT] spiking rows, ascending (inputs | hidden)
+  int* roff = list + NT;                    // [NT + 1]
+  int* st_kr = roff + NT + 1;               // [kStageCap] key | row << 16
+  float* st_w = (float*)(st_kr + kStageCap); // [kStageCap]
+  int* srow = (int*)(st_w + kStageCap);      // [kStageCap] sorted by key
+  float* sw_ = (float*)(srow + kStageCap);   // [kStageCap]
+  int* koff = (int*)(sw_ + kStageCap);       // [2H + 1] key offsets
+  int* kcur = koff + 2 * H + 1;              // [2H] counts, then cursors
+  double* yv = (double*)(((uintptr_t)(kcur + 2 * H) + 15) & ~(uintptr_t)15);
   double* dv = yv + C;
-  __shared__ int warp_cnt[kWarps];
-  __shared__ int nx, nz;
+  __shared__ int2 wsum[kWarps];
+  __shared__ int s_nx, s_nrows, s_total;
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t bH = (int64_t)b * H, bI = (int64_t)b * NI, bC = (int64_t)b * C;
 
-  // 1. input spikes (classifier.py:63-67) + xbar (:212-213), one draw per input
-  const uint64_t key = P.ex_key[b];
-  const uint64_t c0 = (uint64_t)P.t * (uint64_t)NI;
-  const double* pin = P.p_in + bI;
-  auto xspk = [&](int k) {
-    const bool f = sw::u01(sw::draw(key, c0 + (uint64_t)k)) < pin[k];
-    P.xbar[bI + k] = __fadd_rn(__fmul_rn(P.xbar[bI + k], P.alpha), f ? 1.0f : 0.0f);
-    return f;
-  };
-  block_compact(NI, xspk, xlist, &nx, warp_cnt);
-  // 2. hidden spike list (old z) + zbar (classifier.py:207, 210-211)
-  const float* z = P.z + bH;
-  block_compact(H, [&](int h) {
-    const float zh = z[h];
-    P.zbar[bH + h] = __fadd_rn(__fmul_rn(P.zbar[bH + h], P.alpha), zh);
+  PROF(0);
+  // P0: row lengths to shared memory; zero the current accumulators
+  for (int x = threadIdx.x; x < NT; x += kThreads)
+    rlen[x] = (x < NI) ? __ldg(P.in_row_length + x) : __ldg(P.rec_row_length + (x - NI));
+  for (int h = threadIdx.x; h < H; h += kThreads) {
     acc_ext[h] = 0.0f;
     acc_rec[h] = 0.0f;
-    return zh != 0.0f;
-  }, zlist, &nz, warp_cnt);
-  // 3a. lengths of the spiking rows -> staged offsets (warp 0 scan)
-  const int nrows = nx + nz;
-  for (int r = threadIdx.x; r < nrows; r += kThreads)
-    roff[r + 1] = (r < nx) ? __ldg(P.in_row_length + xlist[r]) : __ldg(P.rec_row_length + zlist[r - nx]);
-  __syncthreads();
-  if (warp == 0) {
-    int carry = 0;
-    for (int base = 0; base < nrows; base += 32) {
-      const int r = base + lane;
-      int v = r < nrows ? roff[r + 1] : 0;
+  }
+  // P1: this thread's contiguous chunk of [inputs | hidden]: spike flags,
+  // xbar/zbar updates (classifier.py:63-67, 207-213)
+  const int per = (NT + kThreads - 1) / kThreads;
+  const int x0 = threadIdx.x * per;
+  const uint64_t key = P.ex_key[b];
+  const uint64_t c0 = (uint64_t)P.t * (uint64_t)NI;
+  unsigned flags = 0;
+  float tr[kPerThread], zv[kPerThread];
+  double pv[kPerThread];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(SW_FULL_MASK, v, o);
-        if (lane >= o) v += t;
+  for (int j = 0; j < kPerThread; ++j) {   // all loads first
+    const int x = x0 + j;
+    tr[j] = 0.f;
+    zv[j] = 0.f;
+    pv[j] = 0.0;
+    if (j < per && x < NT) {
+      if (x < NI) {
+        pv[j] = P.p_in[bI + x];
+        tr[j] = P.xbar[bI + x];
+      } else {
+        zv[j] = P.z[bH + x - NI];
+        tr[j] = P.zbar[bH + x - NI];
       }
-      if (r < nrows) roff[r + 1] = carry + v;
-      carry += __shfl_sync(SW_FULL_MASK, v, 31);
     }
-    if (lane == 0) roff[0] = 0;
+  }
+  PROF(12);
+#pragma unroll
+  for (int j = 0; j < kPerThread; ++j) {
+    const int x = x0 + j;
+    if (j < per && x < NT) {
+      bool f;
+      if (x < NI) {
+        f = sw::u01(sw::draw(key, c0 + (uint64_t)x)) < pv[j];
+        P.xbar[bI + x] = __fadd_rn(__fmul_rn(tr[j], P.alpha), f ? 1.0f : 0.0f);
+      } else {
+        f = zv[j] != 0.0f;
+        P.zbar[bH + x - NI] = __fadd_rn(__fmul_rn(tr[j], P.alpha), zv[j]);
+      }
+      if (f) flags |= 1u << j;
+    }
+  }
+  PROF(1);
+  __syncthreads();   // rlen ready
+  PROF(2);
+  // P2: one block scan -> ascending spike list + staged row offsets
+  int cnt = 0, lsum = 0;
+  for (int j = 0; j < per; ++j)
+    if ((flags >> j) & 1u) { ++cnt; lsum += rlen[x0 + j]; }
+  int ec, el, tc, tl;
+  block_scan2(cnt, lsum, ec, el, tc, tl, wsum);
+  for (int j = 0; j < per; ++j) {
+    if ((flags >> j) & 1u) {
+      list[ec] = x0 + j;
+      roff[ec] = el;
+      el += rlen[x0 + j];
+      ++ec;
+    }
+  }
+  if (threadIdx.x == 0) {
+    roff[tc] = tl;
+    s_nrows = tc;
+    s_total = tl;
+  }
+  // number of spiking inputs = count of flags with x < NI
+  int cin = 0;
+  for (int j = 0; j < per; ++j)
+    if (((flags >> j) & 1u) && x0 + j < NI) ++cin;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cin += __shfl_xor_sync(SW_FULL_MASK, cin, o);
+  __syncthreads();
+  if (lane == 0) wsum[warp].x = cin;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < kWarps; ++w) t += wsum[w].x;
+    s_nx = t;
   }
   __syncthreads();
-  const bool staged = roff[nrows] <= kStageCap;
-  // 3b. stage every spiking row's (target, w) with coalesced loads, all warps
+  PROF(3);
+  const int nrows = s_nrows, nx = s_nx, nz = nrows - nx;
+  
+  const int* zl = list + nx;   // hidden entries are NI + h
+  const bool staged = s_total <= kStageCap;
+  // P3: stage every spiking row's (target, w) with coalesced loads; the
+  // readout warps also issue their W_out gathers here
+  // P3: stage every spiking row's (key = [in|rec] post, row, w) with
+  // independent loads (flattened, owning row by binary search) and count
+  // entries per key.  P4 turns this into a counting sort by key that is
+  // stable in row order, and each thread sums its posts' entries in
+  // ascending row (= ascending pre) order: the same float32 sequential sum
+  // per post as the reference, without a serial walk over the rows.
+  for (int k = threadIdx.x; k < 2 * H; k += kThreads) kcur[k] = 0;
+  __syncthreads();
+  const int T = s_total;
   if (staged) {
-    for (int r = warp; r < nrows; r += kWarps) {
-      const bool in = r < nx;
-      const int i = in ? xlist[r] : zlist[r - nx];
-      const int64_t o = (int64_t)i * (in ? P.in_stride : P.rec_stride);
-      const int32_t* tg = (in ? P.in_target : P.rec_target) + o;
-      const float* wv = (in ? P.in_w32 : P.rec_w32) + o;
-      const int q0 = roff[r], len = roff[r + 1] - q0;
-      for (int c = lane; c < len; c += 32) {
-        st_t[q0 + c] = __ldg(tg + c);
-        st_w[q0 + c] = __ldg(wv + c);
+    for (int q0 = threadIdx.x; q0 < T; q0 += 4 * kThreads) {
+      int tv[4], rv[4];
+      float wv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * kThreads;
+        tv[u] = 0;
+        rv[u] = 0;
+        wv[u] = 0.f;
+        if (q < T) {
+          int lo = 0, hi = nrows - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (roff[mid] <= q) lo = mid; else hi = mid - 1;
+          }
+          const int x = list[lo];
+          const bool in = x < NI;
+          const int64_t o = (int64_t)(in ? x : x - NI) * (in ? P.in_stride : P.rec_stride) + (q - roff[lo]);
+          tv[u] = __ldg((in ? P.in_target : P.rec_target) + o) + (in ? 0 : H);
+          wv[u] = __ldg((in ? P.in_w32 : P.rec_w32) + o);
+          rv[u] = lo;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * kThreads;
+        if (q < T) {
+          st_kr[q] = tv[u] | (rv[u] << 16);
+          st_w[q] = wv[u];
+          atomicAdd(&kcur[tv[u]], 1);
+        }
       }
     }
   }
+  PROF(4);
   __syncthreads();
-  // 3c. ordered event-driven accumulation (warp 0: input rows, warp 1: hidden rows)
-  if (warp == 0) {
-    if (staged) warp_add_staged(roff, 0, nx, st_t, st_w, acc_ext);
-    else warp_accumulate_rows(xlist, nx, P.in_row_length, P.in_target, P.in_w32, P.in_stride, acc_ext);
-  } else if (warp == 1) {
-    if (staged) warp_add_staged(roff, nx, nrows, st_t, st_w, acc_rec);
-    else warp_accumulate_rows(zlist, nz, P.rec_row_length, P.rec_target, P.rec_w32, P.rec_stride, acc_rec);
+  PROF(5);
+  if (staged) {
+    // exclusive scan of the 2H key counts (contiguous chunk per thread)
+    const int NK = 2 * H;
+    const int kper = (NK + kThreads - 1) / kThreads;
+    const int k0 = threadIdx.x * kper;
+    int loc = 0;
+    for (int j = 0; j < kper; ++j) if (k0 + j < NK) loc += kcur[k0 + j];
+    int ex, dummy_e, tot, dummy_t;
+    block_scan2(loc, 0, ex, dummy_e, tot, dummy_t, wsum);
+    for (int j = 0; j < kper; ++j) {
+      if (k0 + j < NK) {
+        const int c = kcur[k0 + j];
+        koff[k0 + j] = ex;
+        kcur[k0 + j] = ex;
+        ex += c;
+      }
+    }
+    if (threadIdx.x == 0) koff[NK] = tot;
+    PROF(10);
+    __syncthreads();
+    for (int q = threadIdx.x; q < T; q += kThreads) {
+      const int kr = st_kr[q];
+      const int dst = atomicAdd(&kcur[kr & 0xFFFF], 1);
+      srow[dst] = kr >> 16;
+      sw_[dst] = st_w[q];
+    }
+    PROF(11);
+    __syncthreads();
+    for (int k = threadIdx.x; k < NK; k += kThreads) {
+      const int a = koff[k], e = koff[k + 1];
+      // insertion sort of the (few) entries by row, then the ordered sum
+      for (int i = a + 1; i < e; ++i) {
+        const int r = srow[i];
+        const float w = sw_[i];
+        int j = i - 1;
+        while (j >= a && srow[j] > r) { srow[j + 1] = srow[j]; sw_[j + 1] = sw_[j]; --j; }
+        srow[j + 1] = r;
+        sw_[j + 1] = w;
+      }
+      float acc = 0.0f;
+      for (int i = a; i < e; ++i) acc = __fadd_rn(acc, sw_[i]);
+      if (k < H) acc_ext[k] = acc; else acc_rec[k - H] = acc;
+    }
+    PROF(15);
   } else {
-    // 5a. readout y = alpha*y + z @ W_out^T + b (classifier.py:215), warps 2.. over classes
-    for (int c = warp - 2; c < C; c += kWarps - 2) {
-      double s = 0.0;
-      for (int q = lane; q < nz; q += 32) s += __ldg(P.w_out + (int64_t)c * H + zlist[q]);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(SW_FULL_MASK, s, o);
-      if (lane == 0) yv[c] = __dadd_rn(__dadd_rn(__dmul_rn(P.alpha64, P.y[bC + c]), s), P.b_out[c]);
+    // fallback (very many spiking synapses): warp-serial ordered walk
+    if (warp == 0) {
+      for (int r = 0; r < nx; ++r) {
+        const int64_t o = (int64_t)list[r] * P.in_stride;
+        for (int c = lane; c < rlen[list[r]]; c += 32) {
+          const int t = __ldg(P.in_target + o + c);
+          acc_ext[t] = __fadd_rn(acc_ext[t], __ldg(P.in_w32 + o + c));
+        }
+        __syncwarp();
+      }
+    } else if (warp == 1) {
+      for (int r = nx; r < nrows; ++r) {
+        const int64_t o = (int64_t)(list[r] - NI) * P.rec_stride;
+        for (int c = lane; c < rlen[list[r]]; c += 32) {
+          const int t = __ldg(P.rec_target + o + c);
+          acc_rec[t] = __fadd_rn(acc_rec[t], __ldg(P.rec_w32 + o + c));
+        }
+        __syncwarp();
+      }
     }
   }
+  // readout y = alpha*y + z @ W_out^T + b (classifier.py:215): up to 4
+  // classes per warp, their gathers issued together
+  for (int c0 = warp; c0 < C; c0 += 4 * kWarps) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int q = lane; q < nz; q += 32) {
+      const int h = zl[q] - NI;
+      double w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * kWarps;
+        w[u] = c < C ? __ldg(P.w_out + (int64_t)c * H + h) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s[u] += w[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + u * kWarps;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s[u] += __shfl_xor_sync(SW_FULL_MASK, s[u], o);
+      if (lane == 0 && c < C)
+        yv[c] = __dadd_rn(__dadd_rn(__dmul_rn(P.alpha64, P.y[bC + c]), s[u]), P.b_out[c]);
+    }
+  }
+  PROF(6);
   __syncthreads();
-  // 5b. softmax / cross-entropy / d (plasticity.py:156-165, classifier.py:216-219)
+  PROF(7);
+  // P5: softmax / cross-entropy / d (plasticity.py:156-165, classifier.py:216-219)
   if (warp == 0) {
     double mx = -INFINITY;
     for (int c = lane; c < C; c += 32) mx = fmax(mx, yv[c]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(SW_FULL_MASK, mx, o));
     double se = 0.0;
-    for (int c = lane; c < C; c += 32) se += exp(yv[c] - mx);
+    double ex[2] = {0.0, 0.0};
+    for (int c = lane, u = 0; c < C; c += 32, ++u) {
+      const double e = exp(yv[c] - mx);
+      if (u < 2) ex[u] = e;
+      se += e;
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(SW_FULL_MASK, se, o);
     const int label = P.labels[b];
-    for (int c = lane; c < C; c += 32) {
-      const double pi = exp(yv[c] - mx) / se;
+    for (int c = lane, u = 0; c < C; c += 32, ++u) {
+      const double pi = (u < 2 ? ex[u] : exp(yv[c] - mx)) / se;
       P.y[bC + c] = yv[c];
       P.pi_sum[bC + c] += pi;
       const double dd = pi - (c == label ? 1.0 : 0.0);
@@ -210,10 +342,12 @@ __global__ void __launch_bounds__(kThreads) k_clf_step(sw_clf_step_t P) {
       if (c == label) P.loss[b] += -log(pi);
     }
   }
+  PROF(8);
   __syncthreads();
-  // 4 + 5c + 6: per hidden neuron
+  PROF(9);
+  // P6: surrogate (pre-step state), learning signal, ALIF step
   for (int h = threadIdx.x; h < H; h += kThreads) {
-    const float vo = P.v[bH + h], ao = P.a[bH + h], zo = z[h];
+    const float vo = P.v[bH + h], ao = P.a[bH + h], zo = P.z[bH + h];
     const float thr_o = __fadd_rn(P.v_thr, __fmul_rn(P.beta, ao));
     const float cc = __fdiv_rn(__fsub_rn(vo, thr_o), P.v_thr);
     const float r = __fsub_rn(1.0f, fabsf(cc));
@@ -277,11 +411,19 @@ int grid1(int64_t n) {
 
 }  // namespace
 
+extern "C" __attribute__((visibility("default"))) int sw_debug_clf_prof(long long* out16) {
+  return cudaMemcpyFromSymbol(out16, g_clf_prof, 16 * sizeof(long long)) == cudaSuccess ? 0 : SW_ERR_CUDA;
+}
+
 extern "C" int sw_clf_step(const sw_clf_step_t* p, void* stream) {
   const int H = p->hidden, NI = p->num_inputs, C = p->num_classes;
   if (p->batch <= 0) return SW_OK;
-  const size_t smem = (size_t)(2 * H) * 4 + (size_t)(NI + H) * 4 + (size_t)(NI + H + 1) * 4 +
-                      (size_t)kStageCap * 8 + 16 + (size_t)2 * C * 8;
+  if (NI + H > kThreads * kPerThread) {
+    sw::set_last_error("clf_step: num_inputs + hidden must be <= 2048");
+    return SW_ERR_INVALID_ARG;
+  }
+  const size_t smem = (size_t)(2 * H) * 4 + (size_t)(NI + H) * 8 + (size_t)(NI + H + 1) * 4 +
+                      (size_t)kStageCap * 16 + (size_t)(4 * H + 1) * 4 + 16 + (size_t)2 * C * 8;
   if (smem > 48 * 1024) {
     if (smem > 227 * 1024) { sw::set_last_error("clf_step: layer too large"); return SW_ERR_INVALID_ARG; }
     cudaFuncSetAttribute((const void*)k_clf_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -9,7 +9,10 @@
 // shared-memory ring:
 //   warp 0      loader:  takes tiles from an atomic ticket, issues
 //                        cp.async.bulk global->shared for eps and ebar of
-//                        each 32-replica chunk (mbarrier complete_tx);
+//                        each 32-replica chunk (mbarrier complete_tx) with an
+//                        L2 evict-first policy, so the 200 MB/step stream does
+//                        not evict the small per-replica state of the forward
+//                        kernel;
 //   warps 2..9  compute: 4 replicas each per stage — gathers zb/psi/lsig
 //                        (L2-resident, 128-byte lines thanks to the plan
 //                        order), updates eps/ebar in place in shared memory,
@@ -136,6 +139,7 @@ k_eprop_fused(Seg s0, Seg s1, const float* __restrict__ psi, const float* __rest
     if (warp == 0) {
       // ---------------- loader ----------------
       if (lane == 0) {
+        const uint64_t pol = sw::policy_evict_first();
         uint32_t k = 0;
         while (true) {
           const int tile = (int)atomicAdd(&tickets[0], 1u);
@@ -157,14 +161,15 @@ k_eprop_fused(Seg s0, Seg s1, const float* __restrict__ psi, const float* __rest
             const uint32_t bytes = (uint32_t)nb * kRowBytes;
             const int64_t off = ((int64_t)lt * B + (int64_t)ch * kCB) * 32;
             sw::mbar_arrive_expect_tx(&S.full[slot], 2 * bytes);
-            sw::bulk_g2s(&S.st[slot].eps[0][0], sg.eps + off, bytes, &S.full[slot]);
-            sw::bulk_g2s(&S.st[slot].ebar[0][0], sg.ebar + off, bytes, &S.full[slot]);
+            sw::bulk_g2s_hint(&S.st[slot].eps[0][0], sg.eps + off, bytes, &S.full[slot], pol);
+            sw::bulk_g2s_hint(&S.st[slot].ebar[0][0], sg.ebar + off, bytes, &S.full[slot], pol);
           }
         }
       }
     } else if (warp == 1) {
       // ---------------- ordered float64 sum + bulk store ----------------
       double g = 0.0;
+      const uint64_t pol = sw::policy_evict_first();
       for (uint32_t k = 0;; ++k) {
         const int slot = k % kStages;
         const uint32_t par = (k / kStages) & 1;
@@ -178,8 +183,8 @@ k_eprop_fused(Seg s0, Seg s1, const float* __restrict__ psi, const float* __rest
         const int nb = min(kCB, B - ch * kCB);
         if (lane == 0) {
           const int64_t off = ((int64_t)lt * B + (int64_t)ch * kCB) * 32;
-          sw::bulk_s2g(sg.eps + off, &S.st[slot].eps[0][0], (uint32_t)nb * kRowBytes);
-          sw::bulk_s2g(sg.ebar + off, &S.st[slot].ebar[0][0], (uint32_t)nb * kRowBytes);
+          sw::bulk_s2g_hint(sg.eps + off, &S.st[slot].eps[0][0], (uint32_t)nb * kRowBytes, pol);
+          sw::bulk_s2g_hint(sg.ebar + off, &S.st[slot].ebar[0][0], (uint32_t)nb * kRowBytes, pol);
           sw::bulk_commit();
         }
         const int e = lt * 32 + lane;
