@@ -235,6 +235,97 @@ SW_API int sw_clf_batch_stats(const double* loss, const double* pi_sum, const in
 SW_API int sw_f64_to_f32(const double* in, float* out, int64_t n, void* stream);
 SW_API int sw_scale_f64(double* x, int64_t n, double s, void* stream);
 
+/* ---- transpose (connectivity.py:151-203) ----------------------------------- */
+/* TransposeMap.rebuild in CSR form: for post j, (pre, slot) of its incoming
+ * synapses in [col_ptr[j], col_ptr[j+1]) ordered by (pre, slot) (the
+ * reference's lexsort order).  col_length[N], col_ptr[N+1],
+ * src_pre/src_slot[>= edges], cursor[N] scratch, *max_len = widest column.
+ * changed: device flag (NULL = always); when it reads 0 nothing is rebuilt
+ * (remap-only-if-changed, updates.py:367-369). */
+SW_API int sw_transpose_rebuild(const sw_ragged_t* m, int32_t* col_length, int32_t* col_ptr,
+                                int32_t* src_pre, int32_t* src_slot, int32_t* cursor,
+                                int32_t* max_len, const int32_t* changed, void* stream);
+
+/* ---- spike propagation (connectivity.py:139-148) ---------------------------- */
+/* Event-driven, warp per spiking row, float64 atomics: out[target] += w.
+ * spikes[*n_spikes] (device count), max_spikes bounds the grid. */
+SW_API int sw_propagate_atomic(const int32_t* row_length, const int32_t* target, const double* w,
+                               int32_t stride, const int32_t* spikes, const int32_t* n_spikes,
+                               int32_t max_spikes, double* out, void* stream);
+typedef struct sw_prop_proj {
+  const int32_t* col_ptr;    /* transpose CSR of the projection */
+  const int32_t* src_pre;
+  const int32_t* src_slot;
+  const double* weights;     /* [num_pre, stride] */
+  const uint32_t* spike_bits;/* presynaptic spikes, bit i of word i/32 */
+  int32_t stride;
+} sw_prop_proj_t;
+/* Bit-exact with np.add.at in ascending spike order: out[j] = (accumulate ?
+ * out[j] : 0) + contributions of projection 0 (ascending pre) then 1. */
+SW_API int sw_propagate_ordered(const sw_prop_proj_t* projs, int32_t n_proj, int32_t num_post,
+                                double* out, int32_t accumulate, void* stream);
+/* Ascending id list of the set bits (single block). */
+SW_API int sw_spike_bits_to_list(const uint32_t* bits, int32_t n, int32_t* list, int32_t* count,
+                                 void* stream);
+
+/* ---- trace STDP (plasticity.py:42-95) --------------------------------------- */
+SW_API int sw_stdp_decay(double* x, int32_t nx, double dx, double* y, int32_t ny, double dy,
+                         void* stream);
+/* on_pre_spikes: w = clip(w - a_minus*y[post]) on spiking rows, then x[pre] += 1 */
+SW_API int sw_stdp_pre(const int32_t* row_length, const int32_t* target, double* w, int32_t stride,
+                       int32_t num_pre, const uint32_t* pre_bits, const double* y, double* x,
+                       double a_minus, double w_min, double w_max, void* stream);
+/* on_post_spikes through the transpose: w = clip(w + a_plus*x[pre]), then y[post] += 1 */
+SW_API int sw_stdp_post(const int32_t* col_ptr, const int32_t* src_pre, const int32_t* src_slot,
+                        double* w, int32_t stride, int32_t num_post, const uint32_t* post_bits,
+                        const double* x, double* y, double a_plus, double w_min, double w_max,
+                        void* stream);
+
+/* ---- topographic-map rewiring (topomap.py:70-223) --------------------------- */
+typedef struct sw_rewire_params {
+  uint64_t host_prefix;      /* fold_key(seed, "host") */
+  uint64_t row_prefix;       /* fold_key(seed, "row")  */
+  int32_t rule_id;
+  int32_t side;              /* torus side length (num_post = side*side) */
+  int64_t total_attempts;    /* n_attempts * scale^2 (topomap.py:360) */
+  const double* form_lut;    /* [num_post] formation probability by torus offset */
+  const double* dist_lut;    /* [num_post] toroidal distance by torus offset */
+  double g_theta, p_dep, p_pot, g_init;
+} sw_rewire_params_t;
+/* One RewiringRule update (host + row phases), no host round trip.
+ * attempts[num_pre] int32 (input when forced_attempts != 0), update_count
+ * (device int64, read then incremented), keys[2] scratch, totals[8] int64
+ * out ([0] removed [1] kept [2] formed [3] form_missed [4] form_full
+ * [5] attempts [7] error count), changed (device flag for the remap),
+ * rej scratch int64; ev_off/ev_kind/ev_d (may be NULL): per-attempt event
+ * records in row order (kind 1 = elimination, 2 = formation, distance). */
+SW_API int sw_rewire_update(const sw_ragged_t* m, int32_t weight_plane, const sw_rewire_params_t* prm,
+                            int32_t* attempts, int64_t* update_count, uint64_t* keys,
+                            int64_t* totals, int32_t* changed, int64_t* rej, int32_t* ev_off,
+                            int8_t* ev_kind, double* ev_d, int32_t forced_attempts, void* stream);
+
+/* ---- topographic-map step (topomap.py:419-452) ------------------------------ */
+typedef struct sw_topomap_step {
+  int32_t n;                      /* nodes per sheet (num_pre = num_post) */
+  int64_t* step;                  /* device step index, incremented per step */
+  uint64_t poisson_key;           /* fold_key(seed, "poisson"); counter = step*n + node */
+  const double* p_src;            /* [n] 1 - exp(-rate*h*1e-3) (host numpy) */
+  uint32_t* src_bits;             /* [ceil(n/32)] source spikes of this step */
+  uint32_t* tgt_bits;             /* [ceil(n/32)] target spikes of this step */
+  double* V; double* g_tot; int64_t* ref_until; double* pending;
+  double decay_s, g_leak, v_rest, e_exc, v_theta, v_reset, h, tau_m;
+  int64_t ref_steps;
+  const int32_t* ff_row_length; const int32_t* ff_target; double* ff_g; int32_t ff_stride;
+  const int32_t* ff_col_ptr; const int32_t* ff_src_pre; const int32_t* ff_src_slot;
+  const int32_t* lat_row_length; const int32_t* lat_target; double* lat_g; int32_t lat_stride;
+  const int32_t* lat_col_ptr; const int32_t* lat_src_pre; const int32_t* lat_src_slot;
+  double* ff_x; double* ff_y; double* lat_x; double* lat_y;
+  double decay_x, decay_y, a_plus, a_minus, w_min, w_max;
+} sw_topomap_step_t;
+/* neurons -> ordered propagation + trace decay -> STDP pre -> STDP post ->
+ * step += 1; spike_counts[2] (device, may be NULL) accumulate spikes. */
+SW_API int sw_topomap_step(const sw_topomap_step_t* s, int64_t* spike_counts, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

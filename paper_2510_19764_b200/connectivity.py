@@ -180,3 +180,43 @@ def init_pairwise_bernoulli_torus(side: int, offset_prob: np.ndarray, capacity_h
                      multapse_free, var_names)
     rng.counter += n * n
     return out
+
+
+def spikes_to_bits(spikes: torch.Tensor, n: int) -> torch.Tensor:
+    """Index tensor -> packed uint32 spike mask (int32 storage), on the device."""
+    flags = torch.zeros(((n + 31) // 32) * 32, dtype=torch.int64, device=DEV)
+    if spikes.numel():
+        flags[spikes.to(device=DEV, dtype=torch.int64)] = 1
+    w = (flags.view(-1, 32) << torch.arange(32, device=DEV, dtype=torch.int64)).sum(dim=1)
+    return torch.where(w >= 2**31, w - 2**32, w).to(torch.int32)
+
+
+def propagate_spikes(m: RaggedMatrix, weights: torch.Tensor, spikes: torch.Tensor,
+                     out: torch.Tensor, tmap=None) -> None:
+    """out[j] += weights of synapses from spiking rows onto j
+    (connectivity.py:139-148).
+
+    With a fresh ``tmap`` (TransposeMap of ``m``) the sum is computed per post
+    in ascending-spike order through the transpose: bit-identical to the
+    reference's np.add.at for an ascending spike set.  Without one the
+    event-driven atomic kernel runs (warp per spiking row; summation order,
+    and so the last bits, may vary between runs)."""
+    if weights.dtype != torch.float64 or out.dtype != torch.float64:
+        raise TypeError("float64 weights/out expected")
+    st = _lib.stream_ptr()
+    if tmap is not None:
+        tmap.check_fresh()
+        bits = spikes_to_bits(spikes, m.num_pre)
+        pr = (_lib.PropProj * 1)()
+        pr[0].col_ptr, pr[0].src_pre, pr[0].src_slot = (tmap.col_ptr.data_ptr(),
+                                                        tmap.src_pre.data_ptr(),
+                                                        tmap.src_slot.data_ptr())
+        pr[0].weights, pr[0].spike_bits, pr[0].stride = weights.data_ptr(), bits.data_ptr(), m.stride
+        import ctypes as _c
+        _lib.call("sw_propagate_ordered", _c.cast(pr, _c.c_void_p), 1, m.num_post, out.data_ptr(), 1, st)
+        return
+    sp = spikes.to(device=DEV, dtype=torch.int32).contiguous()
+    n = torch.tensor([sp.numel()], dtype=torch.int32, device=DEV)
+    _lib.call("sw_propagate_atomic", m.row_length.data_ptr(), m.target.data_ptr(),
+              weights.data_ptr(), m.stride, sp.data_ptr(), n.data_ptr(), max(1, sp.numel()),
+              out.data_ptr(), st)

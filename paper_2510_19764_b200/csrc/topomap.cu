@@ -1,0 +1,220 @@
+// Topographic-map rewiring rule (sparsewire/topomap.py:70-223) on the device.
+//
+// One rewiring update of one projection = four stream-ordered kernels that
+// need no host round trip (so the update can live inside a CUDA graph):
+//  1. k_rw_keys:  host/row stream keys folded on the device from the host
+//     prefixes fold_key(seed,"host") / fold_key(seed,"row") with
+//     (rule_id, update_count, pass 0) (updates.py:313-318, 346-349); bumps
+//     update_count; zeroes the per-update counters;
+//  2. host phase (topomap.py:101-108): histogram of total_attempts draws of
+//     uniform_int(num_pre) on the host stream (exact rejection replay);
+//  3. k_rw_rows: thread per row with attempts (topomap.py:142-196):
+//     sample_k_distinct (rejection, or partial Fisher-Yates when 2k >= N),
+//     ascending selected slots, elimination draws in slot order with
+//     p = g < g_theta ? p_dep : p_pot, chained removal (remove_slots order),
+//     formation draws for the remaining candidates in ascending post order
+//     against the host-built formation-probability LUT (indexed by torus
+//     offset), add_synapse at g_init or form_full on RowFull;
+//  4. totals / event records for collect() and the device "changed" flag
+//     that gates the transpose remap.
+#include "common.cuh"
+#include "ragged.cuh"
+#include "util.cuh"
+
+namespace {
+
+constexpr int kKMax = 64;   // attempts per row handled by one thread
+
+__global__ void k_rw_keys(uint64_t host_prefix, uint64_t row_prefix, int32_t rule_id,
+                          int64_t* update_count, uint64_t* keys, int64_t* totals, int32_t* changed) {
+  const uint64_t u = (uint64_t)*update_count;
+  keys[0] = sw::fold_int(sw::fold_int(sw::fold_int(host_prefix, (uint64_t)rule_id), u), 0);
+  keys[1] = sw::fold_int(sw::fold_int(sw::fold_int(row_prefix, (uint64_t)rule_id), u), 0);
+  *update_count = (int64_t)u + 1;
+  for (int k = 0; k < 8; ++k) totals[k] = 0;
+  *changed = 0;
+}
+
+__device__ __forceinline__ int torus_offset(int i, int j, int side) {
+  const int xi = i % side, yi = i / side, xj = j % side, yj = j / side;
+  return (xj - xi + side) % side + side * ((yj - yi + side) % side);
+}
+
+struct RwArgs {
+  sw_ragged_t m;
+  int gp;                       // weight plane index
+  const int32_t* attempts;
+  const uint64_t* keys;         // [host, row_base]
+  const double* form_lut;       // [N] by torus offset
+  const double* dist_lut;       // [N] by torus offset
+  int side;
+  double g_theta, p_dep, p_pot, g_init;
+  int64_t* totals;              // [0]=removed [1]=kept [2]=formed [3]=missed [4]=full [5]=attempts [7]=error
+  int32_t* changed;
+  const int32_t* ev_off;        // [P] exclusive scan of attempts (or null)
+  int8_t* ev_kind;              // 1 = elimination, 2 = formation
+  double* ev_d;
+};
+
+__device__ __forceinline__ int fy_get(const int* key, const int* val, int n, int p) {
+  for (int q = 0; q < n; ++q) if (key[q] == p) return val[q];
+  return p;
+}
+
+__global__ void k_rw_rows(RwArgs A) {
+  const sw_ragged_t& m = A.m;
+  const int N = m.num_post;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.num_pre; i += gridDim.x * blockDim.x) {
+    const int k = A.attempts[i];
+    if (k == 0) continue;
+    if (k > kKMax || k > N) { atomicAdd((unsigned long long*)&A.totals[7], 1ull); continue; }
+    const uint64_t key = sw::child_key(A.keys[1], (uint64_t)i);
+    uint64_t ctr = 0;
+    int cand[kKMax];
+    // sample_k_distinct (rng.py:116-141)
+    if (2 * k < N) {
+      const uint64_t rem = sw::reject_rem((uint64_t)N);
+      int filled = 0;
+      while (filled < k) {
+        const int v = (int)sw::uniform_int_seq(key, ctr, (uint64_t)N, rem);
+        bool seen = false;
+        for (int q = 0; q < filled; ++q) seen |= (cand[q] == v);
+        if (!seen) cand[filled++] = v;
+      }
+    } else {
+      int fk[2 * kKMax], fv[2 * kKMax], nf = 0;
+      for (int q = 0; q < k; ++q) {
+        const uint64_t nn = (uint64_t)(N - q);
+        const int j = q + (int)sw::uniform_int_seq(key, ctr, nn, sw::reject_rem(nn));
+        const int vq = fy_get(fk, fv, nf, q), vj = fy_get(fk, fv, nf, j);
+        // set(q, vj); set(j, vq)
+        int t;
+        for (t = 0; t < nf && fk[t] != q; ++t) {}
+        if (t == nf) { fk[nf] = q; ++nf; }
+        fv[t] = vj;
+        for (t = 0; t < nf && fk[t] != j; ++t) {}
+        if (t == nf) { fk[nf] = j; ++nf; }
+        fv[t] = vq;
+      }
+      for (int q = 0; q < k; ++q) cand[q] = fy_get(fk, fv, nf, q);
+    }
+    const int64_t off = (int64_t)i * m.stride;
+    double* g = (double*)m.planes[A.gp];
+    int n = m.row_length[i];
+    // selected slots (ascending) and which candidates are connected
+    int sel[kKMax];
+    int ns = 0;
+    unsigned long long conn = 0ull;
+    for (int s = 0; s < n && ns < k; ++s) {
+      const int t = m.target[off + s];
+      for (int q = 0; q < k; ++q) {
+        if (cand[q] == t) { sel[ns++] = s; conn |= 1ull << q; break; }
+      }
+    }
+    // elimination draws in slot order (topomap.py:163-175)
+    unsigned long long hit = 0ull;
+    for (int q = 0; q < ns; ++q) {
+      const double u = sw::u01(sw::draw(key, ctr++));
+      const double p = g[off + sel[q]] < A.g_theta ? A.p_dep : A.p_pot;
+      if (u < p) hit |= 1ull << q;
+    }
+    const int removed = __popcll(hit), kept = ns - removed;
+    int ev = A.ev_kind ? A.ev_off[i] : 0;
+    if (A.ev_kind) {
+      for (int q = 0; q < ns; ++q)
+        if ((hit >> q) & 1ull) {
+          A.ev_kind[ev] = 1;
+          A.ev_d[ev] = A.dist_lut[torus_offset(i, m.target[off + sel[q]], A.side)];
+          ++ev;
+        }
+    }
+    // chained removal, descending slots (connectivity.py:130-136)
+    for (int q = ns - 1; q >= 0; --q) {
+      if (!((hit >> q) & 1ull)) continue;
+      const int last = n - 1;
+      if (sel[q] != last) sw::move_slot(m, off, sel[q], last);
+      n = last;
+    }
+    // remaining candidates, ascending post (topomap.py:177-193)
+    int rem_[kKMax];
+    int nr = 0;
+    for (int q = 0; q < k; ++q) {
+      if ((conn >> q) & 1ull) continue;
+      const int v = cand[q];
+      int r = nr++;
+      while (r > 0 && rem_[r - 1] > v) { rem_[r] = rem_[r - 1]; --r; }
+      rem_[r] = v;
+    }
+    int formed = 0, missed = 0, full = 0;
+    for (int q = 0; q < nr; ++q) {
+      const int j = rem_[q];
+      const int o = torus_offset(i, j, A.side);
+      const double u = sw::u01(sw::draw(key, ctr++));
+      if (!(u < A.form_lut[o])) { ++missed; continue; }
+      if (n >= m.max_row_length) { ++full; continue; }
+      m.target[off + n] = j;
+      sw::zero_slot(m, off, n);
+      g[off + n] = A.g_init;
+      ++n;
+      ++formed;
+      if (A.ev_kind) {
+        A.ev_kind[ev] = 2;
+        A.ev_d[ev] = A.dist_lut[o];
+        ++ev;
+      }
+    }
+    if (A.ev_kind)
+      for (; ev < A.ev_off[i] + k; ++ev) A.ev_kind[ev] = 0;
+    m.row_length[i] = n;
+    atomicAdd((unsigned long long*)&A.totals[0], (unsigned long long)removed);
+    atomicAdd((unsigned long long*)&A.totals[1], (unsigned long long)kept);
+    atomicAdd((unsigned long long*)&A.totals[2], (unsigned long long)formed);
+    atomicAdd((unsigned long long*)&A.totals[3], (unsigned long long)missed);
+    atomicAdd((unsigned long long*)&A.totals[4], (unsigned long long)full);
+    atomicAdd((unsigned long long*)&A.totals[5], (unsigned long long)k);
+    if (removed + formed) *A.changed = 1;
+  }
+}
+
+__global__ void k_copy_i32(const int32_t* a, int32_t* b, int n) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) b[x] = a[x];
+}
+
+int grid1(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+extern "C" int sw_rewire_update(const sw_ragged_t* m, int32_t weight_plane, const sw_rewire_params_t* prm,
+                                int32_t* attempts, int64_t* update_count, uint64_t* keys,
+                                int64_t* totals, int32_t* changed, int64_t* rej, int32_t* ev_off,
+                                int8_t* ev_kind, double* ev_d, int32_t forced_attempts, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int P = m->num_pre;
+  k_rw_keys<<<1, 1, 0, st>>>(prm->host_prefix, prm->row_prefix, prm->rule_id, update_count, keys,
+                             totals, changed); sw::count_launch();
+  if (!forced_attempts) {
+    cudaMemsetAsync(attempts, 0, (size_t)P * sizeof(int32_t), st);
+    cudaMemsetAsync(rej, 0, sizeof(int64_t), st);
+    if (prm->total_attempts > 0 && P > 0) {
+      int64_t blocks = (prm->total_attempts + 255) / 256;
+      if (blocks > 148 * 8) blocks = 148 * 8;
+      sw::k_hist_draws_dk<<<(int)blocks, 256, 0, st>>>(prm->total_attempts, keys, (uint64_t)P, attempts, rej); sw::count_launch();
+      if (sw::reject_rem((uint64_t)P) != 0) {
+        sw::k_hist_fix_dk<<<1, 1, 0, st>>>(prm->total_attempts, keys, (uint64_t)P, attempts, rej); sw::count_launch();
+      }
+    }
+  }
+  if (ev_kind) {
+    k_copy_i32<<<grid1(P), 256, 0, st>>>(attempts, ev_off, P); sw::count_launch();
+    sw::k_scan_excl_i32<<<1, 1024, 0, st>>>(ev_off, P, nullptr); sw::count_launch();
+  }
+  RwArgs A{*m, weight_plane, attempts, keys, prm->form_lut, prm->dist_lut, prm->side,
+           prm->g_theta, prm->p_dep, prm->p_pot, prm->g_init, totals, changed, ev_off, ev_kind, ev_d};
+  if (P > 0) { k_rw_rows<<<grid1(P), 256, 0, st>>>(A); sw::count_launch(); }
+  SW_CHECK_LAUNCH("sw_rewire_update");
+  return SW_OK;
+}

@@ -1,0 +1,143 @@
+// TransposeMap.rebuild (connectivity.py:173-192) on the device, CSR layout:
+// for post j the (pre, slot) of its incoming synapses in
+// [col_ptr[j], col_ptr[j+1]), ordered by (pre, slot) — the reference's
+// lexsort((slot, pre, post)) order.  Count -> scan -> atomic scatter ->
+// per-column insertion sort (columns are short; the sort makes the
+// nondeterministic scatter order irrelevant).  All kernels early-exit when
+// *changed == 0, so "remap only if the matrix changed" (updates.py:367-369)
+// is decided on the device and the rebuild can sit in a CUDA graph.
+#include "common.cuh"
+#include "util.cuh"
+
+namespace {
+
+__device__ __forceinline__ bool skip(const int32_t* changed) { return changed && *changed == 0; }
+
+__global__ void k_tr_zero(int32_t* col_length, int N, int32_t* max_len, const int32_t* changed) {
+  if (skip(changed)) return;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) col_length[j] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *max_len = 0;
+}
+
+__global__ void k_tr_count(sw_ragged_t m, int32_t* col_length, const int32_t* changed) {
+  if (skip(changed)) return;
+  const int64_t total = (int64_t)m.num_pre * m.stride;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = x / m.stride;
+    if ((int)(x - i * m.stride) < m.row_length[i]) atomicAdd(&col_length[m.target[x]], 1);
+  }
+}
+
+__global__ void k_tr_prep(const int32_t* col_length, int32_t* col_ptr, int N, const int32_t* changed) {
+  if (skip(changed)) return;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) col_ptr[j] = col_length[j];
+}
+
+__global__ void k_tr_scan(int32_t* col_ptr, int N, const int32_t* changed) {
+  if (skip(changed)) return;
+  // single block; col_ptr[N] receives the total
+  __shared__ int32_t warp_sums[32];
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int base = 0; base < N; base += blockDim.x) {
+    const int x = base + threadIdx.x;
+    const int v = x < N ? col_ptr[x] : 0;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(SW_FULL_MASK, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) warp_sums[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      int w = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(SW_FULL_MASK, w, o);
+        if (lane >= o) w += t;
+      }
+      warp_sums[lane] = w;
+    }
+    __syncthreads();
+    const int before = carry + (warp ? warp_sums[warp - 1] : 0);
+    if (x < N) col_ptr[x] = before + inc - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = before + inc;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) col_ptr[N] = carry;
+}
+
+__global__ void k_tr_scatter(sw_ragged_t m, const int32_t* col_ptr, int32_t* cursor, int32_t* src_pre,
+                             int32_t* src_slot, int N, const int32_t* changed) {
+  if (skip(changed)) return;
+  // cursor[j] counts fills of column j (zeroed by the caller-side memset kernel)
+  const int64_t total = (int64_t)m.num_pre * m.stride;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = x / m.stride;
+    const int s = (int)(x - i * m.stride);
+    if (s < m.row_length[i]) {
+      const int j = m.target[x];
+      const int pos = col_ptr[j] + atomicAdd(&cursor[j], 1);
+      src_pre[pos] = (int32_t)i;
+      src_slot[pos] = s;
+    }
+  }
+}
+
+__global__ void k_tr_sort(const int32_t* col_ptr, int32_t* src_pre, int32_t* src_slot, int N,
+                          int32_t* max_len, const int32_t* changed) {
+  if (skip(changed)) return;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
+    const int a = col_ptr[j], e = col_ptr[j + 1];
+    for (int q = a + 1; q < e; ++q) {
+      const int p = src_pre[q], s = src_slot[q];
+      int r = q - 1;
+      while (r >= a && (src_pre[r] > p || (src_pre[r] == p && src_slot[r] > s))) {
+        src_pre[r + 1] = src_pre[r];
+        src_slot[r + 1] = src_slot[r];
+        --r;
+      }
+      src_pre[r + 1] = p;
+      src_slot[r + 1] = s;
+    }
+    atomicMax(max_len, e - a);
+  }
+}
+
+__global__ void k_zero_i32_guard(int32_t* a, int n, const int32_t* changed) {
+  if (skip(changed)) return;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) a[j] = 0;
+}
+
+int grid1(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+extern "C" int sw_transpose_rebuild(const sw_ragged_t* m, int32_t* col_length, int32_t* col_ptr,
+                                    int32_t* src_pre, int32_t* src_slot, int32_t* cursor,
+                                    int32_t* max_len, const int32_t* changed, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int N = m->num_post;
+  const int64_t total = (int64_t)m->num_pre * m->stride;
+  k_tr_zero<<<grid1(N), 256, 0, st>>>(col_length, N, max_len, changed); sw::count_launch();
+  k_zero_i32_guard<<<grid1(N), 256, 0, st>>>(cursor, N, changed); sw::count_launch();
+  if (total) { k_tr_count<<<grid1(total), 256, 0, st>>>(*m, col_length, changed); sw::count_launch(); }
+  k_tr_prep<<<grid1(N), 256, 0, st>>>(col_length, col_ptr, N, changed); sw::count_launch();
+  k_tr_scan<<<1, 1024, 0, st>>>(col_ptr, N, changed); sw::count_launch();
+  if (total) {
+    k_tr_scatter<<<grid1(total), 256, 0, st>>>(*m, col_ptr, cursor, src_pre, src_slot, N, changed); sw::count_launch();
+  }
+  k_tr_sort<<<grid1(N), 256, 0, st>>>(col_ptr, src_pre, src_slot, N, max_len, changed); sw::count_launch();
+  SW_CHECK_LAUNCH("sw_transpose_rebuild");
+  return SW_OK;
+}

@@ -61,3 +61,73 @@ def eprop_accumulate_batch(targets, row_length, pre_trace, psi, lsig, eps, ebar,
               pre_trace.data_ptr(), psi.data_ptr(), lsig.data_ptr(), B, H, eps.data_ptr(),
               ebar.data_ptr(), grad.data_ptr(), float(beta), float(rho), float(alpha),
               _lib.stream_ptr())
+
+
+# ----------------------------------------------------------------------
+# trace STDP (plasticity.py:42-95)
+# ----------------------------------------------------------------------
+
+from dataclasses import dataclass  # noqa: E402
+import math  # noqa: E402
+
+
+@dataclass
+class StdpParams:
+    g_max: float = 0.2
+    w_min: float = 0.0
+    w_max: float = 0.2
+    a_plus: float = 0.1 * 0.2
+    tau_plus: float = 20.0
+    tau_minus: float = 64.0
+    b_ratio: float = 1.2
+
+    @property
+    def a_minus(self) -> float:
+        return self.b_ratio * self.a_plus * self.tau_plus / self.tau_minus
+
+
+def _as_bits(spikes, n):
+    from .connectivity import spikes_to_bits
+    if spikes.dtype == torch.int32 and spikes.numel() == (n + 31) // 32:
+        return spikes
+    return spikes_to_bits(spikes, n)
+
+
+class StdpSynapses:
+    """Trace STDP on one projection; x [num_pre], y [num_post] float64 on the
+    device.  Same event ordering as the reference (depression on pre spikes
+    with y before this step's increments, then x += 1; potentiation on post
+    spikes through the transpose, then y += 1)."""
+
+    def __init__(self, matrix, syn, h: float, params: StdpParams | None = None,
+                 weight_plane: str = "g"):
+        self.matrix = matrix
+        self.syn = syn
+        self.params = params or StdpParams()
+        self.weight_plane = weight_plane
+        self.x = torch.zeros(matrix.num_pre, dtype=torch.float64, device="cuda")
+        self.y = torch.zeros(matrix.num_post, dtype=torch.float64, device="cuda")
+        self._decay_x = math.exp(-h / self.params.tau_plus)
+        self._decay_y = math.exp(-h / self.params.tau_minus)
+
+    def decay_step(self) -> None:
+        _lib.call("sw_stdp_decay", self.x.data_ptr(), self.x.numel(), self._decay_x,
+                  self.y.data_ptr(), self.y.numel(), self._decay_y, _lib.stream_ptr())
+
+    def on_pre_spikes(self, pre) -> None:
+        """``pre``: index tensor (ascending) or packed spike bits."""
+        m, p = self.matrix, self.params
+        bits = _as_bits(pre, m.num_pre)
+        _lib.call("sw_stdp_pre", m.row_length.data_ptr(), m.target.data_ptr(),
+                  self.syn.planes[self.weight_plane].data_ptr(), m.stride, m.num_pre,
+                  bits.data_ptr(), self.y.data_ptr(), self.x.data_ptr(), p.a_minus, p.w_min,
+                  p.w_max, _lib.stream_ptr())
+
+    def on_post_spikes(self, tmap, post) -> None:
+        tmap.check_fresh()
+        m, p = self.matrix, self.params
+        bits = _as_bits(post, m.num_post)
+        _lib.call("sw_stdp_post", tmap.col_ptr.data_ptr(), tmap.src_pre.data_ptr(),
+                  tmap.src_slot.data_ptr(), self.syn.planes[self.weight_plane].data_ptr(),
+                  m.stride, m.num_post, bits.data_ptr(), self.x.data_ptr(), self.y.data_ptr(),
+                  p.a_plus, p.w_min, p.w_max, _lib.stream_ptr())

@@ -253,7 +253,132 @@ def gen_trainer():
     save("trainer.npz", **out)
 
 
+def _tm_snap(model):
+    out = {}
+    for name in ("ff", "lat"):
+        m, syn = model.net.matrices[name]
+        out[f"{name}_row_length"] = m.row_length.copy()
+        out[f"{name}_target"] = m.target.copy()
+        out[f"{name}_g"] = syn.planes["g"].copy()
+    out["updates"] = np.array([b.update_count for b in model.net.groups["rewiring"]])
+    return out
+
+
+def _tm_events(rule):
+    kinds, dists = [], []
+    for i in np.flatnonzero(rule.attempts):
+        rec = rule._row_events[i]
+        if rec is None:
+            continue
+        elim_d, form_d = rec[0], rec[1]
+        kinds += [1] * len(elim_d) + [2] * len(form_d)
+        dists += list(elim_d) + list(form_d)
+    return np.array(kinds, dtype=np.int8), np.array(dists, dtype=np.float64)
+
+
+def gen_topomap():
+    """State-injection fixtures for the rewiring rule: the full ff/lat state
+    before and after each rewiring group of a reference run, the host LUTs,
+    stats and events; plus the first steps' spikes of a free run."""
+    from sparsewire.topomap import TopomapModel, formation_probability
+    for (tag, scale, seed, dur, depress) in (("s1", 1, 3, 20.0, False), ("s2dep", 2, 5, 5.0, True)):
+        model = TopomapModel(scale, seed)
+        n = model.geometry.n
+        dist = model.geometry.toroidal_distance(0, np.arange(n))
+        out = {"dist": dist, "ff_lut": formation_probability(model.ff_params, dist),
+               "lat_lut": formation_probability(model.lat_params, dist),
+               "meta": np.array([scale, seed], dtype=np.int64)}
+        if depress:
+            for name in ("ff", "lat"):
+                m, syn = model.net.matrices[name]
+                syn.planes["g"][m.slot_mask()] = 0.05
+        recs = []
+        orig = model.net.run_update_group
+
+        def wrapped(group, _orig=orig, _recs=recs, _model=model):
+            pre = _tm_snap(_model)
+            _orig(group)
+            post = _tm_snap(_model)
+            ev = {}
+            for r in ("ff", "lat"):
+                rule = getattr(_model, f"{r}_rule")
+                ev[f"{r}_attempts"] = rule.attempts.copy()
+                ev[f"{r}_ev_kind"], ev[f"{r}_ev_d"] = _tm_events(rule)
+            _recs.append((pre, post, ev))
+        model.net.run_update_group = wrapped
+        model.run(dur)
+        for k, (pre, post, ev) in enumerate(recs):
+            for key, v in pre.items():
+                out[f"u{k}_pre_{key}"] = v
+            for key, v in post.items():
+                if key.endswith("_g") or key.endswith("_target") or key.endswith("row_length"):
+                    out[f"u{k}_post_{key}"] = v
+            for key, v in ev.items():
+                out[f"u{k}_{key}"] = v
+        out["n_updates"] = np.int64(len(recs))
+        save(f"topomap_{tag}.npz", **out)
+    # free run: Poisson source spikes and target spikes of the first 300 steps
+    model = TopomapModel(1, seed=11)
+    src_log, tgt_log, pend = [], [], []
+    sp, tp = model.source.poisson_step, model.target.step
+
+    def psrc(rng, h, _f=sp):
+        s_ = _f(rng, h)
+        src_log.append(s_.copy())
+        return s_
+
+    def ptgt(pending, k, _f=tp):
+        pend.append(pending.copy())
+        t_ = _f(pending, k)
+        tgt_log.append(t_.copy())
+        return t_
+    model.source.poisson_step = psrc
+    model.target.step = ptgt
+    model.run(30.0)
+    st = model.state_arrays()
+    src = np.zeros((len(src_log), model.geometry.n), dtype=bool)
+    tgt = np.zeros_like(src)
+    for t_, (a, b) in enumerate(zip(src_log, tgt_log)):
+        src[t_, a] = True
+        tgt[t_, b] = True
+    save("topomap_run.npz", src=src, tgt=tgt, pending=np.array(pend),
+         **{f"state_{k.replace('.', '_')}": v for k, v in st.items()})
+
+
+def gen_stdp():
+    from sparsewire.plasticity import StdpSynapses, StdpParams
+    rng = R.CounterRng(12, "stdp")
+    P, N, cap = 40, 30, 12
+    m = RaggedMatrix(P, N, cap)
+    syn = SynVarMatrix(m, ("g",))
+    for i in range(P):
+        k = rng.uniform_int(cap + 1)
+        m.target[i, :k] = rng.sample_k_distinct(k, N)
+        m.row_length[i] = k
+        syn.planes["g"][i, :k] = rng.uniform01_array(k) * 0.2
+    tm = TransposeMap(m)
+    tm.rebuild()
+    st = StdpSynapses(m, syn, 0.1, StdpParams())
+    out = {"target": m.target.copy(), "row_length": m.row_length.copy(), "g0": syn.planes["g"].copy()}
+    for t in range(40):
+        pre = np.flatnonzero(rng.uniform01_array(P) < 0.3)
+        post = np.flatnonzero(rng.uniform01_array(N) < 0.3)
+        out[f"pre{t}"] = np.isin(np.arange(P), pre)
+        out[f"post{t}"] = np.isin(np.arange(N), post)
+        st.decay_step()
+        if pre.size:
+            st.on_pre_spikes(pre)
+        if post.size:
+            st.on_post_spikes(tm, post)
+    out["g"] = syn.planes["g"].copy()
+    out["x"] = st.x.copy()
+    out["y"] = st.y.copy()
+    save("stdp.npz", **out)
+
+
 if __name__ == "__main__":
+    gen_topomap()
+    gen_stdp()
     gen_trainer()
     gen_rng()
     gen_remove()

@@ -31,3 +31,34 @@ def valid_equal(row_length, a, b):
     """Compare [P, cap] arrays on valid slots only."""
     mask = np.arange(a.shape[1])[None, :] < row_length[:, None]
     return np.array_equal(a[mask], b[mask])
+
+
+def oracle_topomap_group(fx, k):
+    """Oracle rewiring group (ff rule id 0, lat rule id 1) loaded with the
+    pre-update state of update k of a topomap fixture."""
+    from oracle.topomap import RewiringOracle
+    scale, seed = (int(x) for x in fx["meta"])
+    side = 16 * scale
+    model = OracleModel(seed)
+    rules = {}
+    for name in ("ff", "lat"):
+        tg = fx[f"u{k}_pre_{name}_target"]
+        N = side * side
+        m = Ragged(N, N, tg.shape[1], ("g",))
+        m.row_length[:] = fx[f"u{k}_pre_{name}_row_length"]
+        m.target[:] = tg
+        m.planes["g"][:] = fx[f"u{k}_pre_{name}_g"]
+        model.add_matrix(name, m)
+        r = RewiringOracle(m, side, fx[f"{name}_lut"], fx["dist"], 10 * scale * scale)
+        model.add_rule("rewiring", name, r)
+        rules[name] = (m, r)
+    for b, u in zip(model.groups["rewiring"], fx[f"u{k}_pre_updates"]):
+        b.update_count = int(u)
+    return model, rules
+
+
+def check_topomap_post(fx, k, name, row_length, target, g):
+    rl = fx[f"u{k}_post_{name}_row_length"]
+    assert np.array_equal(row_length, rl), (k, name)
+    assert valid_equal(rl, target, fx[f"u{k}_post_{name}_target"]), (k, name)
+    assert valid_equal(rl, g, fx[f"u{k}_post_{name}_g"]), (k, name)

@@ -1,0 +1,195 @@
+"""Device topomap path vs reference golden vectors and the oracle:
+transpose, ordered propagation, STDP (bit-exact), rewiring (state-injected,
+bit-exact), Poisson/LIF free run, graph vs eager equivalence."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+from oracle_helpers import check_topomap_post
+
+pytestmark = pytest.mark.gpu
+
+
+def _matrix_from(target, row_length, planes):
+    from paper_2510_19764_b200.connectivity import RaggedMatrix, SynVarMatrix
+    P, cap = target.shape
+    return P, cap
+
+
+def test_transpose_and_propagation(dev_lib):
+    from paper_2510_19764_b200.connectivity import RaggedMatrix, SynVarMatrix, propagate_spikes
+    from paper_2510_19764_b200.transpose import TransposeMap
+    g = golden("transpose_prop.npz")
+    m = RaggedMatrix(50, 40, 16)
+    syn = SynVarMatrix(m, ("g",))
+    m.load_state(g["row_length"], g["target"])
+    syn.planes["g"].copy_(torch.from_numpy(g["g"]))
+    tm = TransposeMap(m)
+    tm.rebuild()
+    cl, sp, ss = tm.reference_layout()
+    assert np.array_equal(cl, g["col_length"])
+    assert np.array_equal(sp, g["source_pre"]) and np.array_equal(ss, g["source_slot"])
+    assert tm.max_col_length == int(g["col_length"].max())
+    spikes = torch.from_numpy(g["spikes"]).cuda()
+    out = torch.zeros(40, dtype=torch.float64, device="cuda")
+    propagate_spikes(m, syn.planes["g"], spikes, out, tmap=tm)
+    assert np.array_equal(out.cpu().numpy(), g["out"])           # ordered: bit-exact
+    out2 = torch.zeros_like(out)
+    propagate_spikes(m, syn.planes["g"], spikes, out2)             # event-driven atomics
+    assert np.allclose(out2.cpu().numpy(), g["out"], rtol=1e-13, atol=0)
+
+
+def test_stdp_bit_exact(dev_lib):
+    from paper_2510_19764_b200.connectivity import RaggedMatrix, SynVarMatrix
+    from paper_2510_19764_b200.plasticity import StdpParams, StdpSynapses
+    from paper_2510_19764_b200.transpose import TransposeMap
+    g = golden("stdp.npz")
+    m = RaggedMatrix(40, 30, 12)
+    syn = SynVarMatrix(m, ("g",))
+    m.load_state(g["row_length"], g["target"])
+    syn.planes["g"].copy_(torch.from_numpy(g["g0"]))
+    tm = TransposeMap(m)
+    tm.rebuild()
+    st = StdpSynapses(m, syn, 0.1, StdpParams())
+    for t in range(40):
+        pre = torch.from_numpy(np.flatnonzero(g[f"pre{t}"])).cuda()
+        post = torch.from_numpy(np.flatnonzero(g[f"post{t}"])).cuda()
+        st.decay_step()
+        st.on_pre_spikes(pre)
+        st.on_post_spikes(tm, post)
+    mask = np.arange(12)[None, :] < g["row_length"][:, None]
+    assert np.array_equal(syn.planes["g"].cpu().numpy()[mask], g["g"][mask])
+    assert np.array_equal(st.x.cpu().numpy(), g["x"]) and np.array_equal(st.y.cpu().numpy(), g["y"])
+
+
+def _device_group(fx, k, record_events=True):
+    from paper_2510_19764_b200.connectivity import RaggedMatrix, SynVarMatrix
+    from paper_2510_19764_b200.geometry import GridGeometry
+    from paper_2510_19764_b200.topomap import RewiringParams, RewiringRule
+    from paper_2510_19764_b200.updates import Model
+    scale, seed = (int(x) for x in fx["meta"])
+    side = 16 * scale
+    N = side * side
+    geom = GridGeometry(side)
+    model = Model(seed)
+    out = {}
+    for name, prm in (("ff", RewiringParams.feedforward()), ("lat", RewiringParams.lateral())):
+        tg = fx[f"u{k}_pre_{name}_target"]
+        m = RaggedMatrix(N, N, tg.shape[1])
+        syn = SynVarMatrix(m, ("g",))
+        m.load_state(fx[f"u{k}_pre_{name}_row_length"], tg)
+        syn.planes["g"].copy_(torch.from_numpy(fx[f"u{k}_pre_{name}_g"]))
+        model.add_matrix(name, m, syn)
+        rule = RewiringRule(f"{name}_rewire", m, syn, geom, prm, 10 * scale * scale,
+                            record_events=record_events, form_lut=fx[f"{name}_lut"],
+                            dist_lut=fx["dist"])
+        model.add_rule("rewiring", name, rule.descriptor())
+        out[name] = (m, syn, rule)
+    for b, u in zip(model.groups["rewiring"], fx[f"u{k}_pre_updates"]):
+        b.update_count = int(u)
+    return model, out
+
+
+@pytest.mark.parametrize("tag", ["s1", "s2dep"])
+def test_rewiring_state_injected_bit_exact(dev_lib, tag):
+    fx = golden(f"topomap_{tag}.npz")
+    changes = 0
+    for k in range(int(fx["n_updates"])):
+        model, objs = _device_group(fx, k)
+        model.run_update_group("rewiring")
+        for name, (m, syn, rule) in objs.items():
+            rule.collect(1.0)
+            check_topomap_post(fx, k, name, m.row_length.cpu().numpy(), m.target.cpu().numpy(),
+                               syn.planes["g"].cpu().numpy())
+            assert np.array_equal(rule.attempts.cpu().numpy(), fx[f"u{k}_{name}_attempts"])
+            kinds = fx[f"u{k}_{name}_ev_kind"]
+            d = fx[f"u{k}_{name}_ev_d"]
+            assert [e[1] for e in rule.elim_events] == list(d[kinds == 1])
+            assert [e[1] for e in rule.form_events] == list(d[kinds == 2])
+            changes += rule.last_stats["removed"] + rule.last_stats["formed"]
+            assert rule.last_stats["attempts"] == 10 * int(fx["meta"][0]) ** 2
+    assert changes > 0
+
+
+def test_free_run_spikes_match_reference(dev_lib):
+    """300 steps of TopomapModel(1, seed=11): source spikes are counter-exact;
+    target spikes and propagated conductances match the reference run (LIF
+    uses exp: float tolerance on V, spikes identical in practice)."""
+    from paper_2510_19764_b200.neurons import unpack_spike_bits
+    from paper_2510_19764_b200.topomap import TopomapModel
+    g = golden("topomap_run.npz")
+    model = TopomapModel(1, seed=11, record_events=False, use_graph=False)
+    T = g["src"].shape[0]
+    src_ok = tgt_ok = 0
+    for t in range(T):
+        model.run(0.1)
+        src = unpack_spike_bits(model.source.spike_bits, 256).cpu().numpy()
+        tgt = unpack_spike_bits(model.target.spike_bits, 256).cpu().numpy()
+        src_ok += np.array_equal(src, np.flatnonzero(g["src"][t]))
+        tgt_ok += np.array_equal(tgt, np.flatnonzero(g["tgt"][t]))
+    assert src_ok == T
+    assert tgt_ok >= T - 2
+    st = model.state_arrays()
+    assert np.allclose(st["V"], g["state_V"], rtol=0, atol=1e-6)
+    for key in ("ff.row_length", "lat.row_length"):
+        assert np.array_equal(st[key], g["state_" + key.replace(".", "_")])
+
+
+def test_graph_replay_equals_eager(dev_lib):
+    from paper_2510_19764_b200.topomap import TopomapModel
+    a = TopomapModel(1, seed=74, record_events=False, use_graph=True)
+    b = TopomapModel(1, seed=74, record_events=False, use_graph=False)
+    ra = a.run(40.0)
+    rb = b.run(40.0)
+    assert ra.steps == rb.steps == 400 and ra.rewiring_executions == rb.rewiring_executions == 40
+    assert ra.rewires_per_update == rb.rewires_per_update
+    sa, sb = a.state_arrays(), b.state_arrays()
+    for key in sa:
+        assert np.array_equal(sa[key], sb[key]), key
+
+
+def test_schedule_attempts_and_new_synapses(dev_lib):
+    """pkg/tests/test_topomap.py:191-195, 226-241, 257-267."""
+    from paper_2510_19764_b200.topomap import TopomapModel
+    model = TopomapModel(2, seed=91)
+    model.net.run_update_group("rewiring")
+    assert int(model.ff_rule.attempts.sum()) == 40 and int(model.lat_rule.attempts.sum()) == 40
+    model = TopomapModel(1, seed=72, record_events=False)
+    r = model.run(20.0)
+    assert (r.steps, r.rewiring_executions, r.stimulus_changes) == (200, 20, 1)
+    r2 = model.run(20.0)
+    assert r2.stimulus_changes == 1
+    model = TopomapModel(1, seed=61)
+    m, syn = model.net.matrices["ff"]
+    before = set(zip(*[x.tolist() for x in m.edge_list()]))
+    for _ in range(200):
+        model.net.run_update_group("rewiring")
+    pre, post = m.edge_list()
+    w = syn.planes["g"][m.slot_mask()].cpu().numpy()
+    new = [(k, e) for k, e in enumerate(zip(pre.tolist(), post.tolist())) if e not in before]
+    assert new and all(w[k] == 0.2 for k, _ in new)
+
+
+def test_one_step_transmission_delay(dev_lib):
+    """pkg/tests/test_topomap.py:269-285 with a forced single source spike."""
+    from paper_2510_19764_b200.topomap import TopomapModel
+    model = TopomapModel(1, seed=73, record_events=False, use_graph=False)
+    m, syn = model.net.matrices["ff"]
+    p = model.source.probabilities(0.1)
+    model.source._p = np.zeros(256)
+    model.source._p[5] = 1.0
+    p.copy_(torch.from_numpy(model.source._p))
+    model.source._p_h = 0.1
+    model._launch_step()
+    model.step_index += 1
+    assert float(model.target.g.abs().max()) == 0.0
+    p.zero_()
+    model.source._p[:] = 0.0
+    model._launch_step()
+    decay = math.exp(-0.1 / 5.0)
+    tg = m.row_targets(5).long()
+    assert np.allclose(model.target.g[tg].cpu().numpy(), 0.2 * decay)

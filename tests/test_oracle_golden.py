@@ -141,3 +141,85 @@ def test_trainer_oracle_matches_reference_run():
         assert np.array_equal(m.row_length, rl)
         assert valid_equal(rl, m.target, g[f"{name}_target"])
         assert np.allclose(m.planes["w"], g[f"{name}_w"], rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("tag", ["s1", "s2dep"])
+def test_topomap_rewiring_oracle_golden(tag):
+    from oracle_helpers import check_topomap_post, oracle_topomap_group
+    fx = golden(f"topomap_{tag}.npz")
+    n_upd = int(fx["n_updates"])
+    total_changes = 0
+    for k in range(n_upd):
+        model, rules = oracle_topomap_group(fx, k)
+        model.run_update_group("rewiring")
+        for name, (m, r) in rules.items():
+            check_topomap_post(fx, k, name, m.row_length, m.target, m.planes["g"])
+            assert np.array_equal(r.attempts, fx[f"u{k}_{name}_attempts"])
+            kinds = np.array([e[1] for e in r.events], dtype=np.int8)
+            dists = np.array([e[2] for e in r.events])
+            assert np.array_equal(kinds, fx[f"u{k}_{name}_ev_kind"])
+            assert np.array_equal(dists, fx[f"u{k}_{name}_ev_d"])
+            total_changes += r.stats["removed"] + r.stats["formed"]
+    assert total_changes > 0
+
+
+def test_stdp_oracle_golden():
+    from oracle.ragged import transpose
+    from oracle.topomap import StdpOracle
+    g = golden("stdp.npz")
+    m = Ragged(40, 30, 12, ("g",))
+    m.target[:] = g["target"]
+    m.row_length[:] = g["row_length"]
+    m.planes["g"][:] = g["g0"]
+    st = StdpOracle(m, 0.1)
+    tr = transpose(m)
+    for t in range(40):
+        pre = np.flatnonzero(g[f"pre{t}"])
+        post = np.flatnonzero(g[f"post{t}"])
+        st.decay()
+        if pre.size:
+            st.on_pre(pre)
+        if post.size:
+            st.on_post(tr, post)
+    assert np.array_equal(m.planes["g"], g["g"])
+    assert np.array_equal(st.x, g["x"]) and np.array_equal(st.y, g["y"])
+
+
+def test_transpose_and_propagation_oracle_golden():
+    from oracle.ragged import propagate_spikes, transpose
+    g = golden("transpose_prop.npz")
+    m = Ragged(50, 40, 16, ("g",))
+    m.target[:] = g["target"]
+    m.row_length[:] = g["row_length"]
+    m.planes["g"][:] = g["g"]
+    cl, sp, ss = transpose(m)
+    assert np.array_equal(cl, g["col_length"])
+    assert np.array_equal(sp, g["source_pre"]) and np.array_equal(ss, g["source_slot"])
+    out = np.zeros(40)
+    propagate_spikes(m, m.planes["g"], g["spikes"], out)
+    assert np.array_equal(out, g["out"])
+
+
+def test_topomap_poisson_oracle_golden():
+    """Source spikes of a reference free run: counter-exact Poisson draws
+    with host-numpy probabilities (neurons.py:175-195)."""
+    from oracle.rng import Stream
+    from oracle.topomap import poisson_step
+    g = golden("topomap_run.npz")
+    side = 16
+    gx = np.arange(side * side) % side
+    gy = np.arange(side * side) // side
+    stim = Stream.of(11, "stimulus")
+
+    def wrap(d):
+        d = np.abs(d)
+        return np.minimum(d, side - d)
+    ps = Stream.of(11, "poisson")
+    for t in range(g["src"].shape[0]):
+        if t % 200 == 0:   # stimulus change every t_stim = 20 ms (topomap.py:422-424)
+            bx, by = stim.uniform01() * 16, stim.uniform01() * 16
+            d = np.hypot(wrap(gx - bx), wrap(gy - by))
+            rates = 5.0 + 152.8 * np.exp(-(d * d) / (2.0 * 2.0 ** 2))
+            p = 1.0 - np.exp(-rates * 0.1 * 1e-3)
+        got = poisson_step(ps, p)
+        assert np.array_equal(got, np.flatnonzero(g["src"][t])), t
