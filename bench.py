@@ -140,10 +140,10 @@ def _cpu_reference_sample(w, sample_steps):
     tr = TrainerOracle(task, hidden=w["hidden"], input_density=w["density"],
                        recurrent_density=w["density"], batch_size=w["batch"], seed=1)
     build_s = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    tr.forward(task.train_ids(0, w["batch"]), learn=True)
-    fwd = time.perf_counter() - t0
-    per_step = fwd / task.example_steps
+    times = []
+    tr.forward(task.train_ids(0, w["batch"]), learn=True, step_times=times)
+    # steady state: the first step pays the eligibility arrays' page faults
+    per_step = statistics.median(times[1:]) if len(times) > 1 else times[0]
     t0 = time.perf_counter()
     inv = 1.0 / w["batch"]
     for t in (tr.m_in.planes["grad"], tr.m_rec.planes["grad"]):
@@ -169,7 +169,9 @@ def run_reference(args, w):
         vals.append(r["s_per_epoch"])
     v = statistics.median(vals)
     sample = (f"{r['sample_steps']} of {w['steps']} timesteps of one {w['batch']}-replica batch "
-              f"+ one full update/DEEP R group, extrapolated x{w['steps']} steps x{EPOCH_BATCHES} batches")
+              f"(median step after the first) + one full update/DEEP R group, extrapolated "
+              f"x{w['steps']} steps x{EPOCH_BATCHES} batches; oracle port: numpy + C e-prop "
+              f"(oracle/c/oracle.c), 1 thread")
     line = {"impl": "reference", "metric": "e-prop+DEEP R training time per epoch",
             "value": round(v, 3), "unit": "s/epoch", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": False, "scaling": "strong",
@@ -342,7 +344,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="clf-c1", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-sample-steps", type=int, default=4)
+    ap.add_argument("--ref-sample-steps", type=int, default=6)
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
     if args.impl == "reference":

@@ -1,0 +1,29 @@
+/* Plain-C restatement of sparsewire/_kernels.py:15-39 (eprop_accumulate_batch)
+ * for the CPU baseline and large oracle checks.  TEST INFRASTRUCTURE ONLY.
+ * Compiled with -O2 -ffp-contract=off: every float32 op is separately
+ * rounded, grad accumulates float64(float32 product) in (b, i, s) order,
+ * exactly the numba loop. */
+#include <stdint.h>
+
+void oracle_eprop_accumulate_batch(const int32_t* targets, const int32_t* row_length,
+                                   int64_t P, int64_t S, const float* restrict pre_trace,
+                                   const float* psi, const float* lsig, int64_t B, int64_t H,
+                                   float* restrict eps, float* restrict ebar, double* restrict grad, float beta,
+                                   float rho, float alpha) {
+  for (int64_t b = 0; b < B; ++b) {
+    for (int64_t i = 0; i < P; ++i) {
+      const float zb = pre_trace[b * P + i];
+      const int32_t n = row_length[i];
+      for (int64_t s = 0; s < n; ++s) {
+        const int64_t q = (b * P + i) * S + s;
+        const int32_t j = targets[i * S + s];
+        const float e = psi[b * H + j] * (zb - beta * eps[q]);
+        const float eb = alpha * ebar[q] + e;
+        ebar[q] = eb;
+        const float t = lsig[b * H + j] * eb;
+        grad[i * S + s] += (double)t;
+        eps[q] = rho * eps[q] + e;
+      }
+    }
+  }
+}

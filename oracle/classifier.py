@@ -61,6 +61,15 @@ def eprop_accumulate(targets, row_length, pre_trace, psi, lsig, eps, ebar, grad,
         eps[b, ii, ss] = rho * ep + e
 
 
+def eprop_accumulate_fast(*args):
+    """The C restatement (oracle/c/oracle.c) when gcc is available, else numpy."""
+    try:
+        from .cbuild import eprop_accumulate_c
+        return eprop_accumulate_c(*args)
+    except Exception:
+        return eprop_accumulate(*args)
+
+
 class TaskOracle:
     """classifier.py:28-79."""
 
@@ -144,8 +153,10 @@ class TrainerOracle:
             w[i, m.target[i, :n]] = m.planes["w"][i, :n]
         return w
 
-    def forward(self, ids, learn=True):
-        """classifier.py:188-234."""
+    def forward(self, ids, learn=True, step_times=None):
+        """classifier.py:188-234.  ``step_times`` (list) receives per-step wall
+        seconds (CPU-baseline timing)."""
+        import time
         p, B, H, C = self.p, self.B, self.hidden, self.task.num_classes
         spikes = np.stack([self.task.example_spikes(e) for e in ids]).astype(F)
         labels = np.array([self.task.label(e) for e in ids])
@@ -164,6 +175,7 @@ class TrainerOracle:
         loss_sum, pi_sum = 0.0, np.zeros((B, C))
         al, be, rh = F(p.alpha), F(p.beta), F(p.rho)
         for t in range(self.task.example_steps):
+            t0 = time.perf_counter()
             x = spikes[:, t, :]
             rec, ext = z @ wr, x @ wi
             zbar *= al
@@ -181,11 +193,13 @@ class TrainerOracle:
                 self.g_w_out += d.T @ zbar
                 self.g_b_out += d.sum(axis=0)
                 lsig = (d @ self.w_out).astype(F)
-                eprop_accumulate(self.m_in.target, self.m_in.row_length, xbar, psi, lsig, eps_i,
-                                 ebar_i, self.m_in.planes["grad"], be, rh, al)
-                eprop_accumulate(self.m_rec.target, self.m_rec.row_length, zbar, psi, lsig, eps_r,
-                                 ebar_r, self.m_rec.planes["grad"], be, rh, al)
+                eprop_accumulate_fast(self.m_in.target, self.m_in.row_length, xbar, psi, lsig,
+                                      eps_i, ebar_i, self.m_in.planes["grad"], be, rh, al)
+                eprop_accumulate_fast(self.m_rec.target, self.m_rec.row_length, zbar, psi, lsig,
+                                      eps_r, ebar_r, self.m_rec.planes["grad"], be, rh, al)
             v, a, z = alif_step(v, a, z, rec, ext)
+            if step_times is not None:
+                step_times.append(time.perf_counter() - t0)
         acc = float((pi_sum.argmax(axis=1) == labels).mean())
         return loss_sum / (B * self.task.example_steps), acc
 

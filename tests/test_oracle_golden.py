@@ -223,3 +223,19 @@ def test_topomap_poisson_oracle_golden():
             p = 1.0 - np.exp(-rates * 0.1 * 1e-3)
         got = poisson_step(ps, p)
         assert np.array_equal(got, np.flatnonzero(g["src"][t])), t
+
+
+def test_c_oracle_eprop_matches_golden_and_numpy():
+    from oracle.cbuild import eprop_accumulate_c
+    from oracle.classifier import AlifP
+    g = golden("alif_eprop.npz")
+    p = AlifP()
+    tg, rl = g["target"], g["row_length"]
+    eps = np.zeros((8,) + tg.shape, np.float32)
+    ebar = np.zeros_like(eps)
+    grad = np.zeros(tg.shape)
+    for t in range(25):
+        eprop_accumulate_c(tg, rl, g[f"trace{t}"], g[f"psi_e{t}"], g[f"lsig{t}"], eps, ebar, grad,
+                           np.float32(p.beta), np.float32(p.rho), np.float32(p.alpha))
+    assert np.array_equal(eps, g["eps"]) and np.array_equal(ebar, g["ebar"])
+    assert np.array_equal(grad, g["grad"])
