@@ -185,6 +185,118 @@ def run_reference(args, w):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ microbenchmarks
+def run_mupdate(fracs=(0.001, 0.01, 0.1), P=1 << 20, N=65536, cap=1024, seed=1):
+    """Connectivity-update microbench (SURVEY 8(d) M-update): DEEP R
+    eliminate + form on a 2^20-row ragged matrix, cap 1024, N = 65536,
+    R ~ 512 (Bernoulli(512/65536) rows from counters (seed,"init","M")),
+    four float64 planes, sign flips of a Bernoulli(f) subset per update."""
+    import ctypes
+    import torch
+    from paper_2510_19764_b200 import _lib
+    from paper_2510_19764_b200.connectivity import descriptor, init_pairwise_bernoulli_density
+    from paper_2510_19764_b200.deep_r import DeepR
+    from paper_2510_19764_b200.rng import CounterRng, fold_key
+    from paper_2510_19764_b200.updates import Model
+    planes = ("w", "grad", "adam_m", "adam_v")
+    m, syn = init_pairwise_bernoulli_density(P, N, 512.0 / N, 1.0, CounterRng(seed, "init", "M"),
+                                             var_names=planes, capacity=cap)
+    w = syn.planes["w"]
+    w.normal_(0.0, 0.1)
+    w.mul_(m.slot_mask())
+    dr = DeepR(m, syn, "M", l1_strength=0.0)
+    dr.init_bitfields(CounterRng(seed, "deep_r", "M"))
+    model = Model(seed)
+    model.add_matrix("M", m, syn)
+    dr.register(model, "deep_r", "M")
+    E = m.edge_count()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    peak, _ = measured_peak()
+    out = []
+    for u, f in enumerate(fracs):
+        d = descriptor(m, syn)
+        _lib.call("sw_flip_signs", ctypes.byref(d), 0, fold_key(seed, "flip", u), f, _lib.stream_ptr())
+        flush.add_(1)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        model.run_update_group("deep_r")
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        removed = dr.last_removed
+        alg = E * 12 + E // 8 + P * 24 + removed * (72 + 16 + 52)
+        gbs = alg / (ms * 1e-3) / 1e9
+        out.append({"flip": f, "ms": round(ms, 3), "removed": int(removed), "alg_bytes": int(alg),
+                    "achieved_GBs": round(gbs, 1), "frac": round(gbs / peak, 4)})
+        assert m.edge_count() == E, "DEEP R must conserve the edge count"
+    # spike-propagation microbench on the same matrix (SURVEY 8(d) M-prop)
+    prop = []
+    p_dev = torch.empty(P, dtype=torch.float64, device="cuda")
+    bits = torch.zeros((P + 31) // 32, dtype=torch.int32, device="cuda")
+    lst = torch.zeros(P, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    outv = torch.zeros(N, dtype=torch.float64, device="cuda")
+    for q in (0.001, 0.01, 0.1):
+        p_dev.fill_(q)
+        _lib.call("sw_poisson_step", fold_key(seed, "spk", 0), 0, p_dev.data_ptr(), P, bits.data_ptr(),
+                  _lib.stream_ptr())
+        _lib.call("sw_spike_bits_to_list", bits.data_ptr(), P, lst.data_ptr(), cnt.data_ptr(),
+                  _lib.stream_ptr())
+        S = int(cnt.item())
+        spk = lst[:S].long()
+        Rs = float(m.row_length[spk].double().mean().item()) if S else 0.0
+        reps = 20
+        flush.add_(1)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            _lib.call("sw_propagate_atomic", m.row_length.data_ptr(), m.target.data_ptr(), w.data_ptr(),
+                      m.stride, lst.data_ptr(), cnt.data_ptr(), S, outv.data_ptr(), _lib.stream_ptr())
+        e1.record()
+        e1.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / reps
+        alg = S * 8 + S * Rs * 12 + N * 8
+        gbs = alg / (us * 1e-6) / 1e9
+        prop.append({"q": q, "spiking_rows": S, "us": round(us, 2), "alg_bytes": int(alg),
+                     "achieved_GBs": round(gbs, 1), "frac": round(gbs / peak, 4),
+                     "note": "working set of consecutive reps partly L2-resident" if alg < 100e6 else ""})
+    del m, syn, dr, model, w
+    torch.cuda.empty_cache()
+    return {"rows": P, "num_post": N, "cap": cap, "edges": E, "update_sweep": out,
+            "propagate_atomic": prop}
+
+
+def run_topomap_sweep(scales=(1, 2, 4, 8, 16), model_ms=100.0, seed=1):
+    """Topographic-map simulation speed (x realtime) vs network size,
+    TopomapModel(s) semantics, no recorder, CUDA-graph replay per 1 ms."""
+    import torch
+    from paper_2510_19764_b200.topomap import TopomapModel
+    res = {}
+    for s in scales:
+        t0 = time.perf_counter()
+        model = TopomapModel(s, seed=seed, record_events=False, use_graph=True)
+        torch.cuda.synchronize()
+        build_s = time.perf_counter() - t0
+        model.run(10.0)   # warm-up: capture + first replays
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rec = model.run(model_ms)
+        e1.record()
+        e1.synchronize()
+        wall_ms = e0.elapsed_time(e1)
+        res[f"s{s}"] = {"n": model.geometry.n, "x_realtime": round(model_ms / wall_ms, 3),
+                        "us_per_step": round(wall_ms * 1e3 / rec.steps, 2), "build_s": round(build_s, 2),
+                        "rewires": int(sum(rec.rewires_per_update)),
+                        "ff_edges": model.ff_rule.matrix.edge_count(),
+                        "lat_edges": model.lat_rule.matrix.edge_count()}
+        del model
+        torch.cuda.empty_cache()
+    return res
+
+
 # ------------------------------------------------------------------ device arm
 def run_device(args, w):
     import torch
@@ -331,6 +443,11 @@ def run_device(args, w):
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if ws == 1 and not args.no_micro:
+            del tr
+            torch.cuda.empty_cache()
+            line["mupdate"] = run_mupdate()
+            line["topomap"] = run_topomap_sweep()
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -344,6 +461,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="clf-c1", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-micro", action="store_true",
+                    help="skip the connectivity-update / propagation / topomap sections")
     ap.add_argument("--ref-sample-steps", type=int, default=6)
     args = ap.parse_args()
     w = WORKLOADS[args.workload]

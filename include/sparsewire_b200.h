@@ -141,6 +141,10 @@ SW_API int sw_deepr_form_pass(const sw_ragged_t* m, const sw_bitfield_t* conn,
                        int32_t* activations, int64_t* unplaced,
                        int64_t* counters, void* stream);
 
+/* Microbenchmark sign-flip injection: valid slot (i, s) negates plane value
+ * when uniform01 draw #(i*stride + s) of key < prob (SURVEY 8(d) M-update). */
+SW_API int sw_flip_signs(const sw_ragged_t* m, int32_t plane, uint64_t key, double prob, void* stream);
+
 /* ---- Adam (plasticity.py:198-227) ---------------------------------------- */
 /* p -= lr*(m/c1)/(sqrt(v/c2)+eps) after the moment updates; g := 0.
  * All float64, n elements, exact reference op order. */

@@ -408,3 +408,27 @@ extern "C" int sw_deepr_form_pass(const sw_ragged_t* m, const sw_bitfield_t* con
   SW_CHECK_LAUNCH("sw_deepr_form_pass");
   return SW_OK;
 }
+
+// Sign-flip injection for the connectivity-update microbenchmark (SURVEY
+// 8(d) M-update recipe): valid slot (i, s) flips w when uniform01 draw
+// #(i*stride + s) of `key` is below prob.
+__global__ void k_flip_signs(sw_ragged_t m, int wp, uint64_t key, double prob) {
+  const int64_t total = (int64_t)m.num_pre * m.stride;
+  double* w = (double*)m.planes[wp];
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = x / m.stride;
+    if ((int)(x - i * m.stride) >= m.row_length[i]) continue;
+    if (sw::u01(sw::draw(key, (uint64_t)x)) < prob) w[x] = -w[x];
+  }
+}
+
+extern "C" int sw_flip_signs(const sw_ragged_t* m, int32_t plane, uint64_t key, double prob, void* stream) {
+  const int64_t total = (int64_t)m->num_pre * m->stride;
+  if (total == 0) return SW_OK;
+  int64_t g = (total + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  k_flip_signs<<<(int)g, 256, 0, (cudaStream_t)stream>>>(*m, plane, key, prob); sw::count_launch();
+  SW_CHECK_LAUNCH("sw_flip_signs");
+  return SW_OK;
+}
