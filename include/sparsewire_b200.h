@@ -120,13 +120,20 @@ SW_API int sw_deepr_init_bitfields(const sw_ragged_t* m, int32_t weight_plane,
                             uint64_t sign_key, void* stream);
 /* DeepR.l1_step (deep_r.py:68-77): grad += sign ? +l1 : -l1 on valid slots. */
 SW_API int sw_deepr_l1(const sw_ragged_t* m, int32_t grad_plane, const sw_bitfield_t* sign,
-                double l1, void* stream);
+                const uint32_t* sign_slot, double l1, void* stream);
+/* Slot-aligned sign cache: sign_slot[num_pre, ceil(stride/32)] uint32, bit s
+ * of row i = sign bit of (i, target[i, s]).  Derived state (invisible to
+ * parity): eliminate / form / l1 keep it in step with every slot move and
+ * placement so the eliminate scan reads 1 bit per synapse instead of
+ * gathering 64-bit words from the num_post-wide sign row.  NULL = gather. */
+SW_API int sw_deepr_sign_cache_build(const sw_ragged_t* m, const sw_bitfield_t* sign,
+                                     uint32_t* sign_slot, void* stream);
 /* Eliminate rule host+row phases (deep_r.py:81-99): warp per row; removes
  * sign-mismatched synapses with the exact remove_slots order, clears their
  * conn bits, dormant[i] = count (int64). */
 SW_API int sw_deepr_eliminate(const sw_ragged_t* m, int32_t weight_plane,
                        const sw_bitfield_t* sign, const sw_bitfield_t* conn,
-                       int64_t* dormant, void* stream);
+                       int64_t* dormant, uint32_t* sign_slot, void* stream);
 /* One pass of the form rule (deep_r.py:110-145).
  *   pending_src[num_pre] int64: dormant (pass 0) or unplaced of the previous
  *     pass; summed on device into counters[0] (= D, the number of host draws).
@@ -139,7 +146,8 @@ SW_API int sw_deepr_form_pass(const sw_ragged_t* m, const sw_bitfield_t* conn,
                        int32_t exclude_diagonal, const int64_t* pending_src,
                        uint64_t host_key, uint64_t row_base,
                        int32_t* activations, int64_t* unplaced,
-                       int64_t* counters, void* stream);
+                       int64_t* counters, const sw_bitfield_t* sign, uint32_t* sign_slot,
+                       void* stream);
 
 /* Microbenchmark sign-flip injection: valid slot (i, s) negates plane value
  * when uniform01 draw #(i*stride + s) of key < prob (SURVEY 8(d) M-update). */
@@ -213,6 +221,13 @@ SW_API int sw_lif_cond_step(double* V, double* g, int64_t* ref_until, const doub
 /* PoissonSource.poisson_step (neurons.py:189-195): u = uniform01 #(counter0 + node) < p. */
 SW_API int sw_poisson_step(uint64_t key, int64_t counter0, const double* p, int32_t n,
                            uint32_t* spike_bits, void* stream);
+
+/* Correlated Poisson rates and per-step probabilities on the device
+ * (neurons.py:175-193); centers[2*n_centers] (x, y) device array.  CUDA
+ * exp/hypot (a few ulp from numpy): an option for large grids. */
+SW_API int sw_poisson_rates(int32_t side, const double* centers, int32_t n_centers, double f_base,
+                            double f_peak, double sigma, double h, double* rates, double* p,
+                            void* stream);
 
 /* ---- classifier timestep (classifier.py:188-234) ----------------------------- */
 typedef struct sw_clf_step {

@@ -101,9 +101,10 @@ SIGNATURES: dict[str, list] = {
     "sw_init_bernoulli_count": [I64, I32, U64, U64, I32, F64, P, I32, P, P, P],
     "sw_init_bernoulli_fill": [I64, I32, U64, U64, I32, F64, P, I32, P, P, I32, P],
     "sw_deepr_init_bitfields": [RP, I32, BP, BP, U64, P],
-    "sw_deepr_l1": [RP, I32, BP, F64, P],
-    "sw_deepr_eliminate": [RP, I32, BP, BP, P, P],
-    "sw_deepr_form_pass": [RP, BP, I32, P, U64, U64, P, P, P, P],
+    "sw_deepr_l1": [RP, I32, BP, P, F64, P],
+    "sw_deepr_sign_cache_build": [RP, BP, P, P],
+    "sw_deepr_eliminate": [RP, I32, BP, BP, P, P, P],
+    "sw_deepr_form_pass": [RP, BP, I32, P, U64, U64, P, P, P, BP, P, P],
     "sw_eprop_accumulate_batch": [P, P, I32, I32, P, P, P, I32, I32, P, P, P, F32, F32, F32, P],
     "sw_eprop_plan": [P, P, I32, I32, I32, I32, P, P, P, P, I32, P, P],
     "sw_gather_f64": [P, P, I32, P, P],
@@ -113,6 +114,7 @@ SIGNATURES: dict[str, list] = {
     "sw_alif_surrogate": [P, P, P, I64, F32, F32, P],
     "sw_lif_cond_step": [P, P, P, P, I32, I64, F64, F64, F64, F64, F64, F64, F64, F64, I64, P, P],
     "sw_poisson_step": [U64, I64, P, I32, P, P],
+    "sw_poisson_rates": [I32, P, I32, F64, F64, F64, F64, P, P, P],
     "sw_clf_step": [C.c_void_p, P],
     "sw_clf_batch_stats": [P, P, P, I32, I32, P, P],
     "sw_f64_to_f32": [P, P, I64, P],

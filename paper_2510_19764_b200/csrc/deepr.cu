@@ -60,7 +60,7 @@ __global__ void k_deepr_init_bits(sw_ragged_t m, int wp, sw_bitfield_t sign, sw_
 }
 
 // ---- l1_step (deep_r.py:68-77) -------------------------------------------------
-__global__ void k_deepr_l1(sw_ragged_t m, int gp, sw_bitfield_t sign, double l1) {
+__global__ void k_deepr_l1(sw_ragged_t m, int gp, sw_bitfield_t sign, const uint32_t* cache, double l1) {
   const int64_t total = (int64_t)m.num_pre * m.stride;
   double* g = (double*)m.planes[gp];
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
@@ -68,8 +68,13 @@ __global__ void k_deepr_l1(sw_ragged_t m, int gp, sw_bitfield_t sign, double l1)
     const int64_t i = x / m.stride;
     const int s = (int)(x - i * m.stride);
     if (s >= m.row_length[i]) continue;   // padding gets +-0.0 in the reference: no-op
-    const int j = m.target[x];
-    const bool pos = bit_of(sign.words + i * sign.words_per_row, j);
+    bool pos;
+    if (cache) {
+      const int cw = (m.stride + 31) >> 5;
+      pos = (cache[i * cw + (s >> 5)] >> (s & 31)) & 1u;
+    } else {
+      pos = bit_of(sign.words + i * sign.words_per_row, m.target[x]);
+    }
     g[x] = __dadd_rn(g[x], pos ? l1 : -l1);
   }
 }
@@ -79,39 +84,50 @@ __global__ void k_deepr_l1(sw_ragged_t m, int gp, sw_bitfield_t sign, double l1)
 // ascending marked-slot list in shared memory, conn-bit clears, then the exact
 // chained-removal gather.
 __global__ void __launch_bounds__(kThreads)
-k_deepr_eliminate(sw_ragged_t m, int wp, sw_bitfield_t sign, sw_bitfield_t conn, int64_t* dormant) {
+k_deepr_eliminate(sw_ragged_t m, int wp, sw_bitfield_t sign, sw_bitfield_t conn, int64_t* dormant,
+                  uint32_t* cache) {
   extern __shared__ int s_lists[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int* list = s_lists + warp * m.stride;
   const double* w = (const double*)m.planes[wp];
   const unsigned lt = sw::lanemask_lt();
-  for (int64_t i = (int64_t)blockIdx.x * kWarps + warp; i < m.num_pre;
-       i += (int64_t)gridDim.x * kWarps) {
-    const int n = m.row_length[i];
+  const int64_t step = (int64_t)gridDim.x * kWarps;
+  int64_t i = (int64_t)blockIdx.x * kWarps + warp;
+  int n_next = (i < m.num_pre) ? m.row_length[i] : 0;
+  for (; i < m.num_pre; i += step) {
+    const int n = n_next;
+    // prefetch the next row's length: the row loop is otherwise a chain of
+    // dependent round trips
+    if (i + step < m.num_pre) n_next = m.row_length[i + step];
     const int64_t off = i * (int64_t)m.stride;
     const uint64_t* srow = sign.words + i * sign.words_per_row;
     uint64_t* crow = conn.words + i * conn.words_per_row;
+    const int cw = (m.stride + 31) >> 5;
+    uint32_t* cache_row = cache ? cache + i * (int64_t)cw : nullptr;
     int k = 0;
-    for (int base = 0; base < n; base += 128) {
-      int t[4];
-      double wv[4];
+    constexpr int U = 8;   // 256 slots in flight per warp
+    for (int base = 0; base < n; base += 32 * U) {
+      int t[U];
+      double wv[U];
+      uint32_t cwd[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int s = base + u * 32 + lane;
         t[u] = 0;
         wv[u] = 0.0;
-        if (s < n) { t[u] = __ldg(m.target + off + s); wv[u] = __ldg(w + off + s); }
+        cwd[u] = 0u;
+        if (s < n) {
+          t[u] = __ldg(m.target + off + s);
+          wv[u] = __ldg(w + off + s);
+          if (cache_row) cwd[u] = __ldg(cache_row + (s >> 5));
+        }
       }
-      uint64_t sw_[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int s = base + u * 32 + lane;
-        sw_[u] = (s < n && wv[u] != 0.0) ? __ldg(srow + (t[u] >> 6)) : 0ull;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int s = base + u * 32 + lane;
-        const bool bit = (sw_[u] >> (t[u] & 63)) & 1ull;
+        bool bit;
+        if (cache_row) bit = (cwd[u] >> (s & 31)) & 1u;
+        else bit = (s < n && wv[u] != 0.0) ? ((__ldg(srow + (t[u] >> 6)) >> (t[u] & 63)) & 1ull) : false;
         const bool mis = (s < n) && ((wv[u] < 0.0 && bit) || (wv[u] > 0.0 && !bit));
         if (mis)
           atomicAnd((unsigned long long*)&crow[t[u] >> 6], ~(1ull << (t[u] & 63)));
@@ -123,10 +139,28 @@ k_deepr_eliminate(sw_ragged_t m, int wp, sw_bitfield_t sign, sw_bitfield_t conn,
     __syncwarp();
     if (lane == 0) dormant[i] = k;
     if (k > 0) {
-      sw::warp_apply_removal(m, off, list, n, k);
+      sw::warp_apply_removal(m, off, list, n, k, cache_row);
       if (lane == 0) m.row_length[i] = n - k;
     }
     __syncwarp();
+  }
+}
+
+// build the slot-aligned sign cache: bit s of row i = sign(i, target[i, s])
+__global__ void k_sign_cache(sw_ragged_t m, sw_bitfield_t sign, uint32_t* cache) {
+  const int cw = (m.stride + 31) >> 5;
+  const int64_t total = (int64_t)m.num_pre * cw;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = x / cw;
+    const int w0 = (int)(x - i * cw) * 32;
+    const int n = m.row_length[i];
+    uint32_t v = 0u;
+    for (int b = 0; b < 32 && w0 + b < n; ++b) {
+      const int j = m.target[i * m.stride + w0 + b];
+      v |= (uint32_t)bit_of(sign.words + i * sign.words_per_row, j) << b;
+    }
+    cache[x] = v;
   }
 }
 
@@ -218,30 +252,45 @@ __global__ void k_form_hist_fix(int64_t* counters, uint64_t key, uint64_t P, uin
 // all remaining activations without consuming draws.
 __global__ void __launch_bounds__(kThreads)
 k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row_base,
-                  const int32_t* act, int64_t* unplaced, int64_t* counters) {
+                  const int32_t* act, int64_t* unplaced, int64_t* counters, sw_bitfield_t sign,
+                  uint32_t* cache) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = sw::lanemask_lt();
   const int N = m.num_post;
   const uint64_t rem = sw::reject_rem((uint64_t)N);
   const bool pow2 = (N & (N - 1)) == 0;
   const int cap = m.max_row_length;
-  for (int64_t i = (int64_t)blockIdx.x * kWarps + warp; i < m.num_pre;
-       i += (int64_t)gridDim.x * kWarps) {
-    const int acts = act[i];
-    if (acts == 0) {
-      if (lane == 0) unplaced[i] = 0;
-      continue;
-    }
+  // warp handles groups of 32 rows: activations loaded and zero-unplaced
+  // written coalesced, then the active rows of the group one by one
+  for (int64_t g0 = ((int64_t)blockIdx.x * kWarps + warp) * 32; g0 < m.num_pre;
+       g0 += (int64_t)gridDim.x * kWarps * 32) {
+    const int64_t gi = g0 + lane;
+    const int my_act = gi < m.num_pre ? act[gi] : 0;
+    const int my_len = (gi < m.num_pre && my_act) ? m.row_length[gi] : 0;
+    if (gi < m.num_pre && my_act == 0) unplaced[gi] = 0;
+    unsigned active = __ballot_sync(SW_FULL_MASK, my_act != 0);
+    while (active) {
+    const int src_lane = __ffs(active) - 1;
+    active &= active - 1;
+    const int64_t i = g0 + src_lane;
+    const int acts = __shfl_sync(SW_FULL_MASK, my_act, src_lane);
     const int64_t off = i * (int64_t)m.stride;
     uint64_t* crow = conn.words + i * conn.words_per_row;
     const uint64_t key = sw::child_key(row_base, (uint64_t)i);
     uint64_t ctr = 0;
-    int len = m.row_length[i];
+    int len = __shfl_sync(SW_FULL_MASK, my_len, src_lane);
     int a = 0, streak = 0, unpl = 0;
     while (a < acts) {
       if (len >= cap) { unpl += acts - a; break; }
-      const uint64_t h = sw::draw(key, ctr + lane);
-      const bool valid = sw::draw_valid(h, rem);
+      // lanes evaluated this batch: when no activation can exhaust its
+      // num_post iterations here, only about `need` draws can be used, so
+      // later lanes are neither drawn nor probed (the batch then consumes
+      // exactly L counters)
+      const int need0 = min(acts - a, cap - len);
+      const int L = (streak + 32 < N) ? min(32, need0 + 4) : 32;
+      const bool live = lane < L;
+      const uint64_t h = live ? sw::draw(key, ctr + lane) : 0ull;
+      const bool valid = live && sw::draw_valid(h, rem);
       const int j = (int)(pow2 ? (h & (uint64_t)(N - 1)) : (h % (uint64_t)N));
       bool cand = valid && !(excl_diag && j == (int)i);
       if (cand) cand = !((__ldcg(crow + (j >> 6)) >> (j & 63)) & 1ull);
@@ -257,7 +306,7 @@ k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row
         const int nf = __popc(fmask);
         if (nf <= need) {
           placed = fmask;
-          consumed = 32;
+          consumed = L;
           a += nf;
           len += nf;
           if (fmask) {
@@ -303,6 +352,11 @@ k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row
         m.target[off + slot] = j;
         sw::zero_slot(m, off, slot);
         atomicOr((unsigned long long*)(crow + (j >> 6)), 1ull << (j & 63));
+        if (cache) {
+          uint32_t* cr = cache + i * (int64_t)((m.stride + 31) >> 5);
+          if (bit_of(sign.words + i * sign.words_per_row, j)) atomicOr(&cr[slot >> 5], 1u << (slot & 31));
+          else atomicAnd(&cr[slot >> 5], ~(1u << (slot & 31)));
+        }
       }
       ctr += (uint64_t)consumed;
       __syncwarp();
@@ -311,6 +365,7 @@ k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row
       m.row_length[i] = len;
       unplaced[i] = unpl;
       if (unpl) atomicAdd((unsigned long long*)&counters[1], (unsigned long long)unpl);
+    }
     }
   }
 }
@@ -350,13 +405,13 @@ extern "C" int sw_deepr_init_bitfields(const sw_ragged_t* m, int32_t wp, const s
   return SW_OK;
 }
 
-extern "C" int sw_deepr_l1(const sw_ragged_t* m, int32_t gp, const sw_bitfield_t* sign, double l1,
-                           void* stream) {
+extern "C" int sw_deepr_l1(const sw_ragged_t* m, int32_t gp, const sw_bitfield_t* sign,
+                           const uint32_t* sign_slot, double l1, void* stream) {
   if (int s = check_ragged(m, "sw_deepr_l1: bad matrix")) return s;
   if (l1 == 0.0) return SW_OK;   // deep_r.py:74-75
   const int64_t total = (int64_t)m->num_pre * m->stride;
   if (total == 0) return SW_OK;
-  k_deepr_l1<<<flat_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(*m, gp, *sign, l1); sw::count_launch();
+  k_deepr_l1<<<flat_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(*m, gp, *sign, sign_slot, l1); sw::count_launch();
   SW_CHECK_LAUNCH("sw_deepr_l1");
   return SW_OK;
 }
@@ -370,13 +425,23 @@ static int set_smem(const void* fn, int bytes) {
 }
 
 extern "C" int sw_deepr_eliminate(const sw_ragged_t* m, int32_t wp, const sw_bitfield_t* sign,
-                                  const sw_bitfield_t* conn, int64_t* dormant, void* stream) {
+                                  const sw_bitfield_t* conn, int64_t* dormant, uint32_t* sign_slot,
+                                  void* stream) {
   if (int s = check_ragged(m, "sw_deepr_eliminate: bad matrix")) return s;
   if (m->num_pre == 0) return SW_OK;
   const int smem = elim_smem(m);
   if (int s = set_smem((const void*)k_deepr_eliminate, smem)) return s;
-  k_deepr_eliminate<<<rows_grid(m->num_pre), kThreads, smem, (cudaStream_t)stream>>>(*m, wp, *sign, *conn, dormant); sw::count_launch();
+  k_deepr_eliminate<<<rows_grid(m->num_pre), kThreads, smem, (cudaStream_t)stream>>>(*m, wp, *sign, *conn, dormant, sign_slot); sw::count_launch();
   SW_CHECK_LAUNCH("sw_deepr_eliminate");
+  return SW_OK;
+}
+
+extern "C" int sw_deepr_sign_cache_build(const sw_ragged_t* m, const sw_bitfield_t* sign,
+                                         uint32_t* sign_slot, void* stream) {
+  const int64_t total = (int64_t)m->num_pre * ((m->stride + 31) / 32);
+  if (total == 0) return SW_OK;
+  k_sign_cache<<<flat_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(*m, *sign, sign_slot); sw::count_launch();
+  SW_CHECK_LAUNCH("sw_deepr_sign_cache_build");
   return SW_OK;
 }
 
@@ -393,7 +458,8 @@ extern "C" int sw_ragged_remove_marked(const sw_ragged_t* m, const uint8_t* mark
 
 extern "C" int sw_deepr_form_pass(const sw_ragged_t* m, const sw_bitfield_t* conn, int32_t excl_diag,
                                   const int64_t* pending_src, uint64_t host_key, uint64_t row_base,
-                                  int32_t* act, int64_t* unplaced, int64_t* counters, void* stream) {
+                                  int32_t* act, int64_t* unplaced, int64_t* counters,
+                                  const sw_bitfield_t* sign, uint32_t* sign_slot, void* stream) {
   if (int s = check_ragged(m, "sw_deepr_form_pass: bad matrix")) return s;
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t P = m->num_pre;
@@ -404,7 +470,8 @@ extern "C" int sw_deepr_form_pass(const sw_ragged_t* m, const sw_bitfield_t* con
   const uint64_t rem = sw::reject_rem((uint64_t)P);
   k_form_hist<<<148 * 8, 256, 0, st>>>(counters, host_key, (uint64_t)P, rem, act); sw::count_launch();
   if (rem != 0) { k_form_hist_fix<<<1, 1, 0, st>>>(counters, host_key, (uint64_t)P, rem, act); sw::count_launch(); }
-  k_deepr_form_rows<<<rows_grid(P), kThreads, 0, st>>>(*m, *conn, excl_diag, row_base, act, unplaced, counters); sw::count_launch();
+  k_deepr_form_rows<<<rows_grid(P), kThreads, 0, st>>>(*m, *conn, excl_diag, row_base, act, unplaced, counters,
+      sign ? *sign : sw_bitfield_t{nullptr, 0, 0, 0}, sign ? sign_slot : nullptr); sw::count_launch();
   SW_CHECK_LAUNCH("sw_deepr_form_pass");
   return SW_OK;
 }

@@ -132,3 +132,37 @@ extern "C" int sw_poisson_step(uint64_t key, int64_t counter0, const double* p, 
   SW_CHECK_LAUNCH("sw_poisson_step");
   return SW_OK;
 }
+
+// PoissonSource.set_correlated_rates + probabilities on the device
+// (neurons.py:175-183, 189-193): rate = f_base + f_peak * sum_c exp(-d_c^2 /
+// (2 sigma^2)), d_c the torus distance to centre c, p = 1 - exp(-rate*h*1e-3).
+// CUDA exp/hypot: within a few ulp of numpy, a model option for
+// large grids where the host loop over s^2 centres dominates.
+__global__ void k_poisson_rates(int side, int n, const double* centers, int n_centers, double f_base,
+                                double f_peak, double two_sigma2, double h, double* rates, double* p) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+    const double gx = (double)(x % side), gy = (double)(x / side);
+    double bump = 0.0;
+    for (int c = 0; c < n_centers; ++c) {
+      double dx = fabs(gx - centers[2 * c]), dy = fabs(gy - centers[2 * c + 1]);
+      dx = fmin(dx, side - dx);
+      dy = fmin(dy, side - dy);
+      const double d = hypot(dx, dy);
+      bump = __dadd_rn(bump, exp(-(d * d) / two_sigma2));
+    }
+    const double r = __dadd_rn(f_base, __dmul_rn(f_peak, bump));
+    rates[x] = r;
+    p[x] = 1.0 - exp(-r * h * 1e-3);
+  }
+}
+
+extern "C" int sw_poisson_rates(int32_t side, const double* centers, int32_t n_centers, double f_base,
+                                double f_peak, double sigma, double h, double* rates, double* p,
+                                void* stream) {
+  const int n = side * side;
+  if (n <= 0) return SW_OK;
+  k_poisson_rates<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(side, n, centers, n_centers, f_base, f_peak,
+                                                              2.0 * sigma * sigma, h, rates, p); sw::count_launch();
+  SW_CHECK_LAUNCH("sw_poisson_rates");
+  return SW_OK;
+}

@@ -41,7 +41,8 @@ __device__ __forceinline__ void zero_slot(const sw_ragged_t& m, int64_t off, int
 // destinations < n2, so the gathers are independent and run lane-parallel.
 // Padding beyond n2 is left unspecified (the reference leaves stale values).
 __device__ __forceinline__ void warp_apply_removal(const sw_ragged_t& m, int64_t off,
-                                                   const int* list, int n, int k) {
+                                                   const int* list, int n, int k,
+                                                   uint32_t* cache_row = nullptr) {
   const int lane = threadIdx.x & 31;
   const int n2 = n - k;
   for (int t0 = 1; t0 <= k; t0 += 32) {
@@ -63,6 +64,12 @@ __device__ __forceinline__ void warp_apply_removal(const sw_ragged_t& m, int64_t
           p = n - (k - q);   // rank(list[q]) = k - q
         }
         move_slot(m, off, mt, p);
+        if (cache_row) {
+          // slot-aligned sign cache follows the move (sources are all in the tail)
+          const uint32_t b = (cache_row[p >> 5] >> (p & 31)) & 1u;
+          if (b) atomicOr(&cache_row[mt >> 5], 1u << (mt & 31));
+          else atomicAnd(&cache_row[mt >> 5], ~(1u << (mt & 31)));
+        }
       }
     }
   }

@@ -48,6 +48,10 @@ class DeepR:
         self._counters_host = torch.zeros(4, dtype=torch.int64, pin_memory=True)
         self._last_removed_dev = torch.zeros(1, dtype=torch.int64, device=dev)
         self._no_progress_passes = 0
+        # slot-aligned copy of the sign bits (derived; rebuilt when the matrix
+        # was changed by anything but this rule pair)
+        self._sign_slot = torch.zeros((P, (matrix.stride + 31) // 32), dtype=torch.int32, device=dev)
+        self._cache_version = None
 
     # -- helpers ---------------------------------------------------------------
     def _desc(self):
@@ -55,6 +59,15 @@ class DeepR:
 
     def _plane(self, name):
         return self.syn.plane_index(name)
+
+    def _sync_cache(self) -> int:
+        if self._cache_version != self.matrix.version:
+            d = self._desc()
+            _lib.call("sw_deepr_sign_cache_build", ctypes.byref(d),
+                      ctypes.byref(self.sign_bits.descriptor()), self._sign_slot.data_ptr(),
+                      _lib.stream_ptr())
+            self._cache_version = self.matrix.version
+        return self._sign_slot.data_ptr()
 
     @property
     def last_removed(self) -> int:
@@ -72,6 +85,7 @@ class DeepR:
                   ctypes.byref(self.sign_bits.descriptor()),
                   ctypes.byref(self.conn_bits.descriptor()), key, _lib.stream_ptr())
         rng.counter += self.sign_bits.words.numel()
+        self._cache_version = None
 
     # -- L1 nudge (deep_r.py:68-77) ------------------------------------------------
     def l1_step(self) -> None:
@@ -79,8 +93,8 @@ class DeepR:
             return
         d = self._desc()
         _lib.call("sw_deepr_l1", ctypes.byref(d), self._plane(self.grad_plane),
-                  ctypes.byref(self.sign_bits.descriptor()), float(self.l1_strength),
-                  _lib.stream_ptr())
+                  ctypes.byref(self.sign_bits.descriptor()), self._sync_cache(),
+                  float(self.l1_strength), _lib.stream_ptr())
 
     # -- eliminate rule ----------------------------------------------------------------
     def _eliminate_pass(self, model, binding, pass_index, host_key, row_base) -> bool:
@@ -88,8 +102,9 @@ class DeepR:
         _lib.call("sw_deepr_eliminate", ctypes.byref(d), self._plane(self.weight_plane),
                   ctypes.byref(self.sign_bits.descriptor()),
                   ctypes.byref(self.conn_bits.descriptor()), self.dormant.data_ptr(),
-                  _lib.stream_ptr())
+                  self._sync_cache(), _lib.stream_ptr())
         self.matrix.version += 1
+        self._cache_version = self.matrix.version
         return False
 
     def eliminate_rule(self) -> RuleDescriptor:
@@ -104,10 +119,13 @@ class DeepR:
         _lib.call("sw_deepr_form_pass", ctypes.byref(d),
                   ctypes.byref(self.conn_bits.descriptor()), int(self.exclude_diagonal),
                   src.data_ptr(), host_key, row_base, self._activations.data_ptr(),
-                  self._unplaced.data_ptr(), self._counters.data_ptr(), _lib.stream_ptr())
+                  self._unplaced.data_ptr(), self._counters.data_ptr(),
+                  ctypes.byref(self.sign_bits.descriptor()), self._sync_cache(),
+                  _lib.stream_ptr())
         if pass_index == 0:
             self._last_removed_dev.copy_(self._counters[0:1])
         self.matrix.version += 1
+        self._cache_version = self.matrix.version
         # _form_continue (deep_r.py:147-160): one 32-byte read per pass
         self._counters_host.copy_(self._counters, non_blocking=True)
         torch.cuda.current_stream().synchronize()
@@ -138,3 +156,4 @@ class DeepR:
     def load_state(self, sign_words: np.ndarray, conn_words: np.ndarray) -> None:
         self.sign_bits.load_words(sign_words)
         self.conn_bits.load_words(conn_words)
+        self._cache_version = None

@@ -164,6 +164,27 @@ class PoissonSource:
         self.rates = p.f_base + p.f_peak * bump
         self._p = None
 
+    def set_correlated_rates_device(self, centers, h: float) -> None:
+        """Same rates computed on the device (CUDA exp/hypot; a few ulp from
+        numpy): for large grids where the host loop over centres dominates."""
+        c = np.asarray(centers, dtype=np.float64).reshape(-1)
+        if not hasattr(self, "_rates_dev"):
+            self._rates_dev = torch.zeros(self.geometry.n, dtype=torch.float64, device="cuda")
+            self._centers_dev = torch.zeros(max(2, c.size), dtype=torch.float64, device="cuda")
+        # fresh pinned staging per change: torch's host allocator keeps it alive
+        # until the async copy has run
+        self._centers_dev[:c.size].copy_(torch.from_numpy(c).pin_memory(), non_blocking=True)
+        p = self.params
+        _lib.call("sw_poisson_rates", self.geometry.side, self._centers_dev.data_ptr(), c.size // 2,
+                  p.f_base, p.f_peak, p.sigma_stim, h, self._rates_dev.data_ptr(),
+                  self._p_dev.data_ptr(), _lib.stream_ptr())
+        self.rates = None        # host copy stale: see rates_array()
+        self._p = "device"
+        self._p_h = h
+
+    def rates_array(self) -> np.ndarray:
+        return self.rates.copy() if self.rates is not None else self._rates_dev.cpu().numpy()
+
     def set_uniform_rate(self, rate_hz: float) -> None:
         self.rates = np.full(self.geometry.n, rate_hz, dtype=np.float64)
         self._p = None

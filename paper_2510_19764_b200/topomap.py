@@ -168,7 +168,7 @@ class TopomapModel:
 
     def __init__(self, scale: int, seed: int, workers: int = 1, always_remap: bool = False,
                  capacity_headroom: float = 4.0, record_events: bool = True,
-                 use_graph: bool = True):
+                 use_graph: bool = True, rates_on_device: bool = False):
         _lib.require_cuda()
         scale = max(scale, 1)
         self.scale = scale
@@ -180,6 +180,7 @@ class TopomapModel:
         self.lat_params = RewiringParams.lateral()
         self.stdp_params = StdpParams()
         self.use_graph = use_graph
+        self.rates_on_device = rates_on_device
         self.net = Model(seed, workers=workers, always_remap=always_remap)
         ff_m, ff_syn = self._init_projection("ff", self.ff_params, CounterRng(seed, "init", "ff"),
                                              capacity_headroom)
@@ -286,8 +287,11 @@ class TopomapModel:
         while done < n_steps:
             k = self.step_index
             if k % stim_steps == 0:
-                self.source.set_correlated_rates(self._draw_centers())
-                self.source.probabilities(h)
+                if self.rates_on_device:
+                    self.source.set_correlated_rates_device(self._draw_centers(), h)
+                else:
+                    self.source.set_correlated_rates(self._draw_centers())
+                    self.source.probabilities(h)
                 record.stimulus_changes += 1
             if graph_ok and k % rewire_steps == 0 and n_steps - done >= rewire_steps:
                 self._replay_period(rewire_steps)
@@ -352,7 +356,7 @@ class TopomapModel:
         out["V"] = self.target.V.cpu().numpy()
         out["g_total"] = self.target.g.cpu().numpy()
         out["refractory"] = self.target.refractory_until.cpu().numpy()
-        out["rates"] = self.source.rates.copy()
+        out["rates"] = self.source.rates_array()
         out["stdp_ff_x"] = self.ff_stdp.x.cpu().numpy()
         out["stdp_ff_y"] = self.ff_stdp.y.cpu().numpy()
         out["stdp_lat_x"] = self.lat_stdp.x.cpu().numpy()
