@@ -1,0 +1,21 @@
+#!/bin/bash
+# One GPU-box pass: gpu tests, smoke, bench, ncu launch list + full captures.
+# Usage (under gpurun): bash tools/gpu_round.sh [tag]
+set -x
+TAG=${1:-r1}
+O=gpurun_out/$TAG
+mkdir -p $O
+nvidia-smi > $O/nvidia-smi.txt 2>&1
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench exit $?" >> $O/bench.err
+timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > $O/bench_ref.json 2> $O/bench_ref.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2600 --csv --log-file $O/launches.csv \
+   python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-micro > $O/ncu_launch_bench.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_eprop_fused -s 1000 -c 3 \
+   -o $O/eprop_c1 -f python tools/profile_eprop.py c1 > $O/ncu_eprop.log 2>&1
+timeout 600 env ROWS=262144 ncu --set full --clock-control none --import-source on \
+   -k regex:"k_deepr_eliminate|k_deepr_form_rows|k_remove_marked" -c 6 \
+   -o $O/deepr -f python tools/mupdate_breakdown.py > $O/ncu_deepr.log 2>&1
+ls -la $O
