@@ -212,11 +212,16 @@ def run_mupdate(fracs=(0.001, 0.01, 0.1), P=1 << 20, N=65536, cap=1024, seed=1):
     dr._sync_cache()   # build the slot-aligned sign cache once, outside the timed updates
     E = m.edge_count()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    # warm-up group (no flips: nothing removed): first-launch module loading
+    # and shared-memory attribute setup stay out of the timed updates
+    model.run_update_group("deep_r")
+    torch.cuda.synchronize()
     peak, _ = measured_peak()
     out = []
     for u, f in enumerate(fracs):
         d = descriptor(m, syn)
         _lib.call("sw_flip_signs", ctypes.byref(d), 0, fold_key(seed, "flip", u), f, _lib.stream_ptr())
+        dr._sync_cache()
         flush.add_(1)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -247,22 +252,30 @@ def run_mupdate(fracs=(0.001, 0.01, 0.1), P=1 << 20, N=65536, cap=1024, seed=1):
         S = int(cnt.item())
         spk = lst[:S].long()
         Rs = float(m.row_length[spk].double().mean().item()) if S else 0.0
-        reps = 20
-        flush.add_(1)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(reps):
+        ws_ptr, ws_bytes = _lib.prop_workspace()
+
+        def launch():
             _lib.call("sw_propagate_atomic", m.row_length.data_ptr(), m.target.data_ptr(), w.data_ptr(),
-                      m.stride, lst.data_ptr(), cnt.data_ptr(), S, outv.data_ptr(), _lib.stream_ptr())
-        e1.record()
-        e1.synchronize()
-        us = e0.elapsed_time(e1) * 1e3 / reps
+                      m.num_pre, m.num_post, m.stride, lst.data_ptr(), cnt.data_ptr(), S,
+                      outv.data_ptr(), ws_ptr, ws_bytes, _lib.stream_ptr())
+        for _ in range(3):
+            launch()
+        reps = 20
+        tot_ms = 0.0
+        for _ in range(reps):
+            flush.add_(1)                 # L2 flushed between timed launches
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            launch()
+            e1.record()
+            e1.synchronize()
+            tot_ms += e0.elapsed_time(e1)
+        us = tot_ms * 1e3 / reps
         alg = S * 8 + S * Rs * 12 + N * 8
         gbs = alg / (us * 1e-6) / 1e9
         prop.append({"q": q, "spiking_rows": S, "us": round(us, 2), "alg_bytes": int(alg),
                      "achieved_GBs": round(gbs, 1), "frac": round(gbs / peak, 4),
-                     "note": "working set of consecutive reps partly L2-resident" if alg < 100e6 else ""})
+                     "note": "L2 flushed before each timed launch"})
     del m, syn, dr, model, w
     torch.cuda.empty_cache()
     return {"rows": P, "num_post": N, "cap": cap, "edges": E, "update_sweep": out,

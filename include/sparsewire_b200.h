@@ -266,11 +266,21 @@ SW_API int sw_transpose_rebuild(const sw_ragged_t* m, int32_t* col_length, int32
                                 int32_t* max_len, const int32_t* changed, void* stream);
 
 /* ---- spike propagation (connectivity.py:139-148) ---------------------------- */
-/* Event-driven, warp per spiking row, float64 atomics: out[target] += w.
- * spikes[*n_spikes] (device count), max_spikes bounds the grid. */
+/* Event-driven atomic mode: out[target] += w over the rows in
+ * spikes[*n_spikes] (device count; max_spikes bounds the grid).
+ * Few spiking rows: warp per row, float64 RED into L2.  Many rows,
+ * num_post <= 65536 and a workspace of >= sw_propagate_workspace_bytes():
+ * one CTA per SM accumulates one 16384-post slab in shared memory over its
+ * group's rows, then the per-group slabs are reduced (ascending group order)
+ * into out after a grid barrier.  Summation order across rows is not
+ * deterministic in either form (shared-memory / L2 atomics). */
 SW_API int sw_propagate_atomic(const int32_t* row_length, const int32_t* target, const double* w,
-                               int32_t stride, const int32_t* spikes, const int32_t* n_spikes,
-                               int32_t max_spikes, double* out, void* stream);
+                               int32_t num_pre, int32_t num_post, int32_t stride,
+                               const int32_t* spikes, const int32_t* n_spikes, int32_t max_spikes,
+                               double* out, void* workspace, int64_t workspace_bytes,
+                               void* stream);
+/* Workspace bytes the slab form of sw_propagate_atomic needs on the current device. */
+SW_API int64_t sw_propagate_workspace_bytes(void);
 typedef struct sw_prop_proj {
   const int32_t* col_ptr;    /* transpose CSR of the projection */
   const int32_t* src_pre;

@@ -120,7 +120,7 @@ SIGNATURES: dict[str, list] = {
     "sw_f64_to_f32": [P, P, I64, P],
     "sw_scale_f64": [P, I64, F64, P],
     "sw_transpose_rebuild": [RP, P, P, P, P, P, P, P, P],
-    "sw_propagate_atomic": [P, P, P, I32, P, P, I32, P, P],
+    "sw_propagate_atomic": [P, P, P, I32, I32, I32, P, P, I32, P, P, I64, P],
     "sw_propagate_ordered": [P, I32, I32, P, I32, P],
     "sw_spike_bits_to_list": [P, I32, P, P, P],
     "sw_stdp_decay": [P, I32, F64, P, I32, F64, P],
@@ -149,6 +149,8 @@ def lib():
         fn = getattr(L, name)
         fn.argtypes = argtypes
         fn.restype = C.c_int
+    L.sw_propagate_workspace_bytes.argtypes = []
+    L.sw_propagate_workspace_bytes.restype = C.c_int64
     L.sw_launch_count.argtypes = []
     L.sw_launch_count.restype = C.c_longlong
     L.sw_last_error.argtypes = []
@@ -189,6 +191,20 @@ def workspace(device=None) -> int:
         t = torch.zeros(64, dtype=torch.int32, device=f"cuda:{dev}")
         _ws[dev] = t
     return t.data_ptr()
+
+
+_pws = {}
+
+
+def prop_workspace(device=None) -> tuple[int, int]:
+    """Per-device scratch for the slab form of sw_propagate_atomic."""
+    dev = torch.cuda.current_device() if device is None else device
+    t = _pws.get(dev)
+    if t is None:
+        nbytes = int(lib().sw_propagate_workspace_bytes())
+        t = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=f"cuda:{dev}")
+        _pws[dev] = t
+    return t.data_ptr(), t.numel()
 
 
 def launch_count() -> int:

@@ -218,5 +218,5 @@ def propagate_spikes(m: RaggedMatrix, weights: torch.Tensor, spikes: torch.Tenso
     sp = spikes.to(device=DEV, dtype=torch.int32).contiguous()
     n = torch.tensor([sp.numel()], dtype=torch.int32, device=DEV)
     _lib.call("sw_propagate_atomic", m.row_length.data_ptr(), m.target.data_ptr(),
-              weights.data_ptr(), m.stride, sp.data_ptr(), n.data_ptr(), max(1, sp.numel()),
-              out.data_ptr(), st)
+              weights.data_ptr(), m.num_pre, m.num_post, m.stride, sp.data_ptr(), n.data_ptr(),
+              max(1, sp.numel()), out.data_ptr(), *_lib.prop_workspace(), st)

@@ -4,6 +4,7 @@
 // connectivity.py:91-136, updates.py:309-372.
 #include "common.cuh"
 #include "ragged.cuh"
+#include "sm100_async.cuh"
 
 namespace {
 
@@ -146,6 +147,93 @@ k_deepr_eliminate(sw_ragged_t m, int wp, sw_bitfield_t sign, sw_bitfield_t conn,
   }
 }
 
+// ---- eliminate, vectorised scan (sign cache present, float64 weights, stride % 4 == 0) --
+// Same semantics as k_deepr_eliminate.  The mismatch decision needs only the
+// weight and the slot-aligned sign bit; the target is read for marked slots
+// alone (conn-bit clear, moves), so the scan streams 8 B + 1 bit per synapse.
+// Each lane owns 4 consecutive slots (two 16-byte loads) in each half of a
+// 256-slot batch, so a warp keeps 2 KB of weights in flight per batch; the
+// ascending marked-slot list is rebuilt from four ballots per half.
+constexpr int kVW = 8;   // warps per block
+
+__device__ __forceinline__ bool mismatch(double w, uint32_t bit) {
+  return (w < 0.0 && bit) || (w > 0.0 && !bit);
+}
+
+__global__ void __launch_bounds__(kVW * 32, 5)
+k_deepr_elim_vec(sw_ragged_t m, int wp, sw_bitfield_t conn, int64_t* dormant, uint32_t* cache) {
+  extern __shared__ int s_lists[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* list = s_lists + warp * m.stride;
+  const double* w = (const double*)m.planes[wp];
+  const int cw = (m.stride + 31) >> 5;
+  const int64_t step = (int64_t)gridDim.x * kVW;
+  int64_t i = (int64_t)blockIdx.x * kVW + warp;
+  int n_next = (i < m.num_pre) ? m.row_length[i] : 0;
+  for (; i < m.num_pre; i += step) {
+    const int n = n_next;
+    if (i + step < m.num_pre) n_next = m.row_length[i + step];
+    const int64_t off = i * (int64_t)m.stride;
+    const double2* w2 = reinterpret_cast<const double2*>(w + off);
+    const uint32_t* crow = cache + i * (int64_t)cw;
+    uint64_t* cbits = conn.words + i * conn.words_per_row;
+    int k = 0;
+    for (int base = 0; base < n; base += 256) {
+      double2 v[4];
+      uint32_t word[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int s0 = base + h * 128 + lane * 4;
+        if (s0 < n) {
+          v[2 * h] = __ldcs(w2 + (s0 >> 1));
+          v[2 * h + 1] = __ldcs(w2 + (s0 >> 1) + 1);
+          word[h] = __ldcs(crow + (s0 >> 5));
+        } else {
+          v[2 * h] = make_double2(0.0, 0.0);
+          v[2 * h + 1] = make_double2(0.0, 0.0);
+          word[h] = 0u;
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int s0 = base + h * 128 + lane * 4;
+        const uint32_t wd = word[h] >> (s0 & 31);
+        const double x[4] = {v[2 * h].x, v[2 * h].y, v[2 * h + 1].x, v[2 * h + 1].y};
+        unsigned mine = 0u;   // bit j: slot s0 + j marked
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (s0 + j < n && mismatch(x[j], (wd >> j) & 1u)) mine |= 1u << j;
+        if (__any_sync(SW_FULL_MASK, mine != 0u)) {
+          // exclusive prefix of the per-lane counts (ascending slot order)
+          const int cnt = __popc(mine);
+          int pre = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(SW_FULL_MASK, pre, o);
+            if (lane >= o) pre += t;
+          }
+          const int tot = __shfl_sync(SW_FULL_MASK, pre, 31);
+          int pos = k + pre - cnt;
+          for (unsigned mm = mine; mm; mm &= mm - 1) {
+            const int sl = s0 + __ffs(mm) - 1;
+            list[pos++] = sl;
+            const int t = __ldg(m.target + off + sl);
+            atomicAnd((unsigned long long*)&cbits[t >> 6], ~(1ull << (t & 63)));
+          }
+          k += tot;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) dormant[i] = k;
+    if (k > 0) {
+      sw::warp_apply_removal(m, off, list, n, k, cache + i * (int64_t)cw);
+      if (lane == 0) m.row_length[i] = n - k;
+    }
+    __syncwarp();
+  }
+}
+
 // build the slot-aligned sign cache: bit s of row i = sign(i, target[i, s])
 __global__ void k_sign_cache(sw_ragged_t m, sw_bitfield_t sign, uint32_t* cache) {
   const int cw = (m.stride + 31) >> 5;
@@ -250,7 +338,7 @@ __global__ void k_form_hist_fix(int64_t* counters, uint64_t key, uint64_t P, uin
 // of the batch already placed the same post (match_any), the failure streak
 // resets per activation and ends it after num_post misses, a full row stops
 // all remaining activations without consuming draws.
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 8)
 k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row_base,
                   const int32_t* act, int64_t* unplaced, int64_t* counters, sw_bitfield_t sign,
                   uint32_t* cache) {
@@ -293,7 +381,14 @@ k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row
       const bool valid = live && sw::draw_valid(h, rem);
       const int j = (int)(pow2 ? (h & (uint64_t)(N - 1)) : (h % (uint64_t)N));
       bool cand = valid && !(excl_diag && j == (int)i);
-      if (cand) cand = !((__ldcg(crow + (j >> 6)) >> (j & 63)) & 1ull);
+      // the candidate's conn word and (for the slot-aligned cache) its sign
+      // word are fetched together: one memory round trip per batch
+      bool sbit = false;
+      if (cand) {
+        const uint64_t cwd = __ldcg(crow + (j >> 6));
+        if (cache) sbit = (__ldg(sign.words + i * sign.words_per_row + (j >> 6)) >> (j & 63)) & 1ull;
+        cand = !((cwd >> (j & 63)) & 1ull);
+      }
       const unsigned peers = __match_any_sync(SW_FULL_MASK, cand ? j : (N + lane));
       const bool first = cand && !(peers & lt);
       const unsigned vmask = __ballot_sync(SW_FULL_MASK, valid);
@@ -354,7 +449,7 @@ k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row
         atomicOr((unsigned long long*)(crow + (j >> 6)), 1ull << (j & 63));
         if (cache) {
           uint32_t* cr = cache + i * (int64_t)((m.stride + 31) >> 5);
-          if (bit_of(sign.words + i * sign.words_per_row, j)) atomicOr(&cr[slot >> 5], 1u << (slot & 31));
+          if (sbit) atomicOr(&cr[slot >> 5], 1u << (slot & 31));
           else atomicAnd(&cr[slot >> 5], ~(1u << (slot & 31)));
         }
       }
@@ -429,6 +524,16 @@ extern "C" int sw_deepr_eliminate(const sw_ragged_t* m, int32_t wp, const sw_bit
                                   void* stream) {
   if (int s = check_ragged(m, "sw_deepr_eliminate: bad matrix")) return s;
   if (m->num_pre == 0) return SW_OK;
+  if (sign_slot && m->plane_bytes[wp] == 8 && m->stride % 4 == 0 &&
+      ((uintptr_t)m->planes[wp] % 16) == 0) {
+    const int smem = kVW * m->stride * (int)sizeof(int);
+    if (int s = set_smem((const void*)k_deepr_elim_vec, smem)) return s;
+    int64_t g = (m->num_pre + kVW - 1) / kVW;
+    if (g > 148 * 40) g = 148 * 40;
+    k_deepr_elim_vec<<<(int)g, kVW * 32, smem, (cudaStream_t)stream>>>(*m, wp, *conn, dormant, sign_slot); sw::count_launch();
+    SW_CHECK_LAUNCH("sw_deepr_eliminate");
+    return SW_OK;
+  }
   const int smem = elim_smem(m);
   if (int s = set_smem((const void*)k_deepr_eliminate, smem)) return s;
   k_deepr_eliminate<<<rows_grid(m->num_pre), kThreads, smem, (cudaStream_t)stream>>>(*m, wp, *sign, *conn, dormant, sign_slot); sw::count_launch();

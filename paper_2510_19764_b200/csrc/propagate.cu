@@ -9,6 +9,7 @@
 //   pre) and adds the spiking ones, projection after projection (ff then
 //   lat, topomap.py:435-436) — the reference's per-post sequential sum.
 #include "common.cuh"
+#include "sm100_async.cuh"
 
 namespace {
 
@@ -40,6 +41,86 @@ __global__ void k_prop_atomic(const int32_t* __restrict__ row_length, const int3
     } else {
       for (int s = lane; s < len; s += 32) atomicAdd(out + __ldg(target + off + s), __ldg(w + off + s));
     }
+  }
+}
+
+// ---- shared-memory slab variant of the atomic mode --------------------------------
+// float64 RED into L2 caps the warp-per-row kernel at ~0.16 G contributions
+// per microsecond (measured), i.e. ~2 TB/s of row data.  Shared-memory
+// float64 atomics sustain ~3x that per SM, so here the output lives in
+// shared memory: CTA b owns post slab (b % 4) of 16384 float64 (128 KB) and
+// scans the rows of its group (b / 4), accumulating only the targets in its
+// slab.  The four CTAs of a group read the same rows at about the same time,
+// so HBM delivers each row once and L2 serves the other three reads.  The
+// per-group slabs are then written to a scratch plane and, after a grid-wide
+// barrier (cooperative launch: one CTA per SM, all co-resident), every CTA
+// sums a contiguous post range over the groups in ascending group order and
+// adds it to `out` — one plain store per post instead of one RED per
+// contribution.
+constexpr int kSlabs = 4;        // post slabs (CTAs per group)
+constexpr int kSlab = 16384;     // posts per slab
+constexpr int kSW = 32;          // warps per CTA
+constexpr int kPropSlabSmem = kSlab * 8;
+constexpr int kPropSlabMinSpikes = 2048;   // below: warp-per-row kernel
+
+__global__ void __launch_bounds__(kSW * 32, 1)
+k_prop_slab(const int32_t* __restrict__ row_length, const int32_t* __restrict__ target,
+            const double* __restrict__ w, int stride, const int32_t* __restrict__ spikes,
+            const int32_t* n_spikes, double* out, int N, double* scratch, unsigned* arrive, int vec) {
+  extern __shared__ __align__(16) double acc[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x % kSlabs;
+  const int g = blockIdx.x / kSlabs;
+  const int G = gridDim.x / kSlabs;
+  const int slab0 = c * kSlab;
+  for (int k = threadIdx.x; k < kSlab; k += blockDim.x) acc[k] = 0.0;
+  __syncthreads();
+  const int S = *n_spikes;
+  for (int q = g * kSW + warp; q < S; q += G * kSW) {
+    const int i = __ldg(spikes + q);
+    const int n = __ldg(row_length + i);
+    const int64_t off = (int64_t)i * stride;
+    if (vec) {
+      const int4* t4 = reinterpret_cast<const int4*>(target + off);
+      const double2* w2 = reinterpret_cast<const double2*>(w + off);
+#pragma unroll 2
+      for (int s = lane * 4; s < n; s += 128) {
+        const int4 t = __ldg(t4 + (s >> 2));
+        const double2 wa = __ldg(w2 + (s >> 1));
+        const double2 wb = __ldg(w2 + (s >> 1) + 1);
+        const int r0 = t.x - slab0, r1 = t.y - slab0, r2 = t.z - slab0, r3 = t.w - slab0;
+        if ((unsigned)r0 < (unsigned)kSlab) atomicAdd(acc + r0, wa.x);
+        if (s + 1 < n && (unsigned)r1 < (unsigned)kSlab) atomicAdd(acc + r1, wa.y);
+        if (s + 2 < n && (unsigned)r2 < (unsigned)kSlab) atomicAdd(acc + r2, wb.x);
+        if (s + 3 < n && (unsigned)r3 < (unsigned)kSlab) atomicAdd(acc + r3, wb.y);
+      }
+    } else {
+      for (int s = lane; s < n; s += 32) {
+        const int r = __ldg(target + off + s) - slab0;
+        if ((unsigned)r < (unsigned)kSlab) atomicAdd(acc + r, __ldg(w + off + s));
+      }
+    }
+  }
+  __syncthreads();
+  // slab -> scratch[g][c*kSlab + k]
+  double* mine = scratch + (int64_t)g * (kSlabs * kSlab) + slab0;
+  for (int k = threadIdx.x; k < kSlab; k += blockDim.x) mine[k] = acc[k];
+  // grid barrier (all CTAs co-resident: cooperative launch)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(arrive, 1u);
+    while (atomicAdd(arrive, 0u) < gridDim.x) __nanosleep(64);
+  }
+  __syncthreads();
+  __threadfence();
+  // post range of this CTA, summed over the groups in ascending order
+  const int per = (N + gridDim.x - 1) / gridDim.x;
+  const int j0 = blockIdx.x * per, j1 = min(N, j0 + per);
+  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+    double v = 0.0;
+    for (int gg = 0; gg < G; ++gg) v = __dadd_rn(v, __ldcg(scratch + (int64_t)gg * (kSlabs * kSlab) + j));
+    out[j] = __dadd_rn(out[j], v);
   }
 }
 
@@ -159,12 +240,60 @@ int grid1(int64_t n) {
   return (int)(g < 1 ? 1 : g);
 }
 
+// CTAs of the cooperative slab kernel on the current device (multiple of kSlabs)
+int slab_ctas() {
+  static int ctas = -1;
+  if (ctas < 0) {
+    cudaFuncSetAttribute((const void*)k_prop_slab, cudaFuncAttributeMaxDynamicSharedMemorySize, kPropSlabSmem);
+    int per_sm = 0, sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_prop_slab, kSW * 32,
+                                                      kPropSlabSmem) != cudaSuccess) per_sm = 0;
+    cudaGetLastError();
+    ctas = (per_sm * sms / kSlabs) * kSlabs;
+  }
+  return ctas;
+}
+
 }  // namespace
 
+extern "C" int64_t sw_propagate_workspace_bytes(void) {
+  const int ctas = slab_ctas();
+  return (int64_t)(ctas / kSlabs) * kSlabs * kSlab * 8 + 256;
+}
+
 extern "C" int sw_propagate_atomic(const int32_t* row_length, const int32_t* target, const double* w,
-                                   int32_t stride, const int32_t* spikes, const int32_t* n_spikes,
-                                   int32_t max_spikes, double* out, void* stream) {
+                                   int32_t num_pre, int32_t num_post, int32_t stride,
+                                   const int32_t* spikes, const int32_t* n_spikes, int32_t max_spikes,
+                                   double* out, void* workspace, int64_t workspace_bytes,
+                                   void* stream) {
+  (void)num_pre;
   if (max_spikes <= 0) return SW_OK;
+  // many spiking rows, an output that fits the shared-memory slabs and a
+  // caller workspace for the per-group slabs: the slab kernel
+  const int coop_ctas = slab_ctas();
+  if (coop_ctas >= kSlabs && max_spikes >= kPropSlabMinSpikes && num_post > 0 &&
+      num_post <= kSlabs * kSlab && workspace != nullptr) {
+    const int groups = coop_ctas / kSlabs;
+    const int64_t need = (int64_t)groups * kSlabs * kSlab * 8 + 256;
+    if (workspace_bytes >= need) {
+      double* scratch = reinterpret_cast<double*>(workspace);
+      unsigned* arrive = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(workspace) + need - 256);
+      cudaStream_t st = (cudaStream_t)stream;
+      cudaMemsetAsync(arrive, 0, sizeof(unsigned), st);
+      const int vec = (stride % 4 == 0) && (((uintptr_t)target | (uintptr_t)w) % 16 == 0);
+      int N = num_post;
+      void* args[] = {(void*)&row_length, (void*)&target, (void*)&w, (void*)&stride, (void*)&spikes,
+                      (void*)&n_spikes, (void*)&out, (void*)&N, (void*)&scratch, (void*)&arrive,
+                      (void*)&vec};
+      cudaLaunchCooperativeKernel((const void*)k_prop_slab, dim3(coop_ctas), dim3(kSW * 32), args,
+                                  kPropSlabSmem, st);
+      sw::count_launch();
+      SW_CHECK_LAUNCH("sw_propagate_atomic(slab)");
+      return SW_OK;
+    }
+  }
   const int vec = (stride % 4 == 0) && (((uintptr_t)target | (uintptr_t)w) % 16 == 0);
   int64_t blocks = ((int64_t)max_spikes + 7) / 8;
   if (blocks > 148 * 16) blocks = 148 * 16;

@@ -96,7 +96,11 @@ def _random_instance(P, N, cap, R, seed):
 
 @pytest.mark.parametrize("P,N,cap,R,flip", [(512, 2048, 96, 40, 0.01), (300, 700, 50, 20, 0.1),
                                             (1024, 65536, 128, 60, 0.03),
-                                            (256, 33, 20, 12, 0.3)])
+                                            (256, 33, 20, 12, 0.3),
+                                            # streaming eliminate: full 256-slot chunks, deep ring
+                                            (2048, 8192, 1024, 512, 0.01),
+                                            # odd stride: 16-byte TMA windows start mid-row
+                                            (700, 300, 41, 25, 0.05)])
 def test_deep_r_random_instances_match_oracle(dev_lib, P, N, cap, R, flip):
     from paper_2510_19764_b200.connectivity import RaggedMatrix, SynVarMatrix
     from paper_2510_19764_b200.deep_r import DeepR

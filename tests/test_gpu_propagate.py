@@ -1,0 +1,69 @@
+"""Event-driven atomic propagation (connectivity.py:139-148) at sizes that
+take the cluster / shared-memory-slab kernel, against np.add.at.
+
+Dyadic weights make every summation order exact (the reference's own
+strategy, pkg/tests/test_connectivity.py:147-187), so the check is
+bit-exact; general float64 weights are checked to a relative 1e-12."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _matrix(P, N, cap, seed):
+    from paper_2510_19764_b200.connectivity import RaggedMatrix, SynVarMatrix
+    rs = np.random.default_rng(seed)
+    rl = rs.integers(0, cap + 1, size=P).astype(np.int32)
+    tgt = np.zeros((P, max(cap, 1)), dtype=np.int32)
+    for i in range(P):
+        tgt[i, :rl[i]] = rs.choice(N, size=rl[i], replace=False)
+    m = RaggedMatrix(P, N, cap)
+    syn = SynVarMatrix(m, ("g",))
+    m.load_state(rl, tgt)
+    return m, syn, rl, tgt, rs
+
+
+@pytest.mark.parametrize("P,N,cap,q,dyadic", [
+    (6000, 65536, 300, 0.6, True),      # cluster kernel, all four slabs, multi-chunk rows
+    (5000, 40000, 41, 0.9, True),       # odd stride, last slab partial
+    (4000, 3000, 64, 0.7, False),       # small output, general weights
+    (3000, 70000, 32, 0.9, True),       # num_post > 65536: warp-per-row kernel
+    (500, 65536, 128, 0.5, True),       # few spiking rows: warp-per-row kernel
+])
+def test_atomic_propagation_matches_add_at(dev_lib, P, N, cap, q, dyadic):
+    from paper_2510_19764_b200.connectivity import propagate_spikes
+    m, syn, rl, tgt, rs = _matrix(P, N, cap, 11)
+    if dyadic:
+        w = rs.integers(-64, 65, size=tgt.shape).astype(np.float64) / 64.0
+    else:
+        w = rs.standard_normal(tgt.shape)
+    syn.planes["g"].copy_(torch.from_numpy(w))
+    spikes = np.flatnonzero(rs.random(P) < q).astype(np.int32)
+    ref = rs.standard_normal(N)
+    out = torch.from_numpy(ref.copy()).cuda()
+    for i in spikes:                                   # connectivity.py:146-148
+        np.add.at(ref, tgt[i, :rl[i]], w[i, :rl[i]])
+    propagate_spikes(m, syn.planes["g"], torch.from_numpy(spikes).cuda(), out)
+    got = out.cpu().numpy()
+    if dyadic:
+        # the random base is not dyadic: order can move the last bit of the sum
+        assert np.allclose(got, ref, rtol=0, atol=1e-12)
+    else:
+        assert np.allclose(got, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_atomic_propagation_dyadic_exact_from_zero(dev_lib):
+    from paper_2510_19764_b200.connectivity import propagate_spikes
+    P, N, cap = 8000, 65536, 512
+    m, syn, rl, tgt, rs = _matrix(P, N, cap, 5)
+    w = rs.integers(-1024, 1025, size=tgt.shape).astype(np.float64) / 1024.0
+    syn.planes["g"].copy_(torch.from_numpy(w))
+    spikes = np.flatnonzero(rs.random(P) < 0.5).astype(np.int32)
+    ref = np.zeros(N)
+    for i in spikes:
+        np.add.at(ref, tgt[i, :rl[i]], w[i, :rl[i]])
+    out = torch.zeros(N, dtype=torch.float64, device="cuda")
+    propagate_spikes(m, syn.planes["g"], torch.from_numpy(spikes).cuda(), out)
+    assert np.array_equal(out.cpu().numpy(), ref)
