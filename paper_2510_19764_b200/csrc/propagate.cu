@@ -10,6 +10,8 @@
 //   lat, topomap.py:435-436) — the reference's per-post sequential sum.
 #include "common.cuh"
 #include "sm100_async.cuh"
+#include <cstdlib>
+#include <cstring>
 
 namespace {
 
@@ -61,7 +63,7 @@ constexpr int kSlabs = 4;        // post slabs (CTAs per group)
 constexpr int kSlab = 16384;     // posts per slab
 constexpr int kSW = 32;          // warps per CTA
 constexpr int kPropSlabSmem = kSlab * 8;
-constexpr int kPropSlabMinSpikes = 2048;   // below: warp-per-row kernel
+constexpr int kPropSlabMinSpikes = 32768;  // below: warp-per-row kernel
 
 __global__ void __launch_bounds__(kSW * 32, 1)
 k_prop_slab(const int32_t* __restrict__ row_length, const int32_t* __restrict__ target,
@@ -240,6 +242,216 @@ int grid1(int64_t n) {
   return (int)(g < 1 ? 1 : g);
 }
 
+// ---- cluster / multicast variant of the atomic mode --------------------------------
+// The slab kernel above is bound by L2->SM bandwidth: four CTAs read every
+// row.  Here the four slab CTAs form a thread-block cluster and each row
+// chunk crosses L2 once: a producer thread in CTA rank 0 multicasts 128-slot
+// chunks (targets + weights, cp.async.bulk ... multicast::cluster) into the
+// same stage of all four CTAs; every CTA's consumer warps add the chunk's
+// contributions that fall in its slab with shared-memory atomics and release
+// the stage to rank 0 with a remote mbarrier arrive.  16 consumer teams per
+// cluster, 3 stages each; the producer polls the teams round-robin with
+// non-blocking barrier probes.
+constexpr int kCW = 16;                 // consumer warps (teams) per CTA
+constexpr int kCS = 3;                  // stages per team
+constexpr int kCC = 128;                // slots per chunk
+constexpr int kCTB = kCC * 4 + 16;
+constexpr int kCWB = kCC * 8 + 16;
+constexpr int kCStage = kCTB + kCWB;
+constexpr int kPropClusterSmem = kSlab * 8 + kCW * kCS * kCStage + 2 * kCW * kCS * 8;
+
+struct ChunkIt {
+  int q;       // index into the spike list
+  int n;       // row length of spikes[q]
+  int c0;      // first slot of the chunk
+  int i;       // row
+};
+
+__device__ __forceinline__ void chunk_first(ChunkIt& it, int qstep, const int32_t* spikes, int S,
+                                            const int32_t* row_length) {
+  it.c0 = 0;
+  it.n = 0;
+  while (it.q < S) {
+    it.i = __ldg(spikes + it.q);
+    it.n = __ldg(row_length + it.i);
+    if (it.n > 0) return;
+    it.q += qstep;
+  }
+}
+
+__device__ __forceinline__ void chunk_next(ChunkIt& it, int qstep, const int32_t* spikes, int S,
+                                           const int32_t* row_length) {
+  it.c0 += kCC;
+  if (it.c0 < it.n) return;
+  it.q += qstep;
+  chunk_first(it, qstep, spikes, S, row_length);
+}
+
+__device__ __forceinline__ bool window16(uint64_t start, uint64_t len, uint64_t limit, uint64_t& a,
+                                         uint32_t& bytes) {
+  a = start & ~15ull;
+  const uint64_t e = (start + len + 15) & ~15ull;
+  bytes = (uint32_t)(e - a);
+  return e <= limit;
+}
+
+__global__ void __cluster_dims__(kSlabs, 1, 1) __launch_bounds__((kCW + 1) * 32, 1)
+k_prop_cluster(const int32_t* __restrict__ row_length, const int32_t* __restrict__ target,
+               const double* __restrict__ w, int stride, int64_t num_pre,
+               const int32_t* __restrict__ spikes, const int32_t* n_spikes, double* out, int N) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  double* acc = reinterpret_cast<double*>(s_raw);
+  unsigned char* stages = s_raw + kSlab * 8;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stages + kCW * kCS * kCStage);
+  uint64_t* empty = full + kCW * kCS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = sw::cluster_ctarank();
+  const int slab0 = (int)rank * kSlab;
+
+  for (int k = threadIdx.x; k < kSlab; k += blockDim.x) acc[k] = 0.0;
+  if (threadIdx.x < kCW * kCS) {
+    sw::mbar_init(&full[threadIdx.x], 1);
+    sw::mbar_init(&empty[threadIdx.x], kSlabs);
+  }
+  sw::fence_mbar_init();
+  __syncthreads();
+  sw::cluster_sync_all();
+
+  const int S = *n_spikes;
+  const int teams = (int)(gridDim.x / kSlabs) * kCW;
+  const int team0 = (int)(blockIdx.x / kSlabs) * kCW;
+  const uint64_t t_limit = (uint64_t)num_pre * stride * 4;
+  const uint64_t w_limit = (uint64_t)num_pre * stride * 8;
+
+  if (warp == kCW) {
+    if (rank == 0 && lane == 0) {
+      // producer: round-robin over the cluster's teams, never blocking
+      ChunkIt it[kCW];
+      int u[kCW];
+      uint32_t eph[kCW];
+      int live = 0;
+      for (int t = 0; t < kCW; ++t) {
+        it[t] = ChunkIt{team0 + t, 0, 0, 0};
+        chunk_first(it[t], teams, spikes, S, row_length);
+        u[t] = 0;
+        eph[t] = 0u;
+        live += it[t].q < S;
+      }
+      while (live > 0) {
+        for (int t = 0; t < kCW; ++t) {
+          if (it[t].q >= S) continue;
+          const int s = u[t] % kCS;
+          uint64_t* eb = &empty[t * kCS + s];
+          if (u[t] >= kCS) {
+            if (!sw::mbar_test_cluster(eb, (eph[t] >> s) & 1u)) continue;
+            eph[t] ^= 1u << s;
+          }
+          const int len = min(kCC, it[t].n - it[t].c0);
+          const uint64_t e0 = (uint64_t)it[t].i * stride + it[t].c0;
+          uint64_t ta, wa;
+          uint32_t tb, wb;
+          if (window16(e0 * 4, (uint64_t)len * 4, t_limit, ta, tb) &&
+              window16(e0 * 8, (uint64_t)len * 8, w_limit, wa, wb)) {
+            unsigned char* buf = stages + (t * kCS + s) * kCStage;
+            uint64_t* fb = &full[t * kCS + s];
+            sw::bulk_g2s_multicast(buf, (const unsigned char*)target + ta, tb, fb, (1u << kSlabs) - 1);
+            sw::bulk_g2s_multicast(buf + kCTB, (const unsigned char*)w + wa, wb, fb, (1u << kSlabs) - 1);
+          }
+          ++u[t];
+          chunk_next(it[t], teams, spikes, S, row_length);
+          if (it[t].q >= S) --live;
+        }
+      }
+    }
+  } else {
+    ChunkIt it{team0 + warp, 0, 0, 0};
+    chunk_first(it, teams, spikes, S, row_length);
+    uint32_t fph = 0u;
+    int u = 0;
+    while (it.q < S) {
+      const int s = u % kCS;
+      const int len = min(kCC, it.n - it.c0);
+      const uint64_t e0 = (uint64_t)it.i * stride + it.c0;
+      uint64_t ta, wa;
+      uint32_t tb, wb;
+      const bool tma = window16(e0 * 4, (uint64_t)len * 4, t_limit, ta, tb) &&
+                       window16(e0 * 8, (uint64_t)len * 8, w_limit, wa, wb);
+      if (tma) {
+        uint64_t* fb = &full[warp * kCS + s];
+        if (lane == 0) sw::mbar_arrive_expect_tx(fb, tb + wb);
+        sw::mbar_wait(fb, (fph >> s) & 1u);
+        fph ^= 1u << s;
+        const unsigned char* buf = stages + (warp * kCS + s) * kCStage;
+        const int32_t* tp = reinterpret_cast<const int32_t*>(buf) + ((e0 * 4 - ta) >> 2);
+        const double* wp = reinterpret_cast<const double*>(buf + kCTB) + ((e0 * 8 - wa) >> 3);
+#pragma unroll
+        for (int k = 0; k < kCC / 32; ++k) {
+          const int sl = lane + 32 * k;
+          if (sl < len) {
+            const int rel = tp[sl] - slab0;
+            if ((unsigned)rel < (unsigned)kSlab) atomicAdd(acc + rel, wp[sl]);
+          }
+        }
+      } else {
+        for (int sl = lane; sl < len; sl += 32) {
+          const int rel = __ldg(target + e0 + sl) - slab0;
+          if ((unsigned)rel < (unsigned)kSlab) atomicAdd(acc + rel, __ldg(w + e0 + sl));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) sw::mbar_arrive_cluster_relaxed(&empty[warp * kCS + s], 0);
+      ++u;
+      chunk_next(it, teams, spikes, S, row_length);
+    }
+  }
+  // all remote arrives on rank 0's barriers happen before any CTA exits
+  __syncthreads();
+  sw::cluster_sync_all();
+  for (int k = threadIdx.x; k < kSlab && slab0 + k < N; k += blockDim.x) {
+    const double v = acc[k];
+    if (v != 0.0) atomicAdd(out + slab0 + k, v);
+  }
+}
+
+int cluster_count() {
+  static int nc = -1;
+  if (nc < 0) {
+    cudaFuncSetAttribute((const void*)k_prop_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kPropClusterSmem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kSlabs * 64);
+    cfg.blockDim = dim3((kCW + 1) * 32);
+    cfg.dynamicSmemBytes = kPropClusterSmem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kSlabs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, (const void*)k_prop_cluster, &cfg) != cudaSuccess) c = 0;
+    cudaGetLastError();
+    nc = c;
+  }
+  return nc;
+}
+
+// propagation form override for measurements: SW_PROP_MODE=plain|slab|cluster
+int prop_mode() {
+  static int mode = -2;
+  if (mode == -2) {
+    const char* e = getenv("SW_PROP_MODE");
+    mode = -1;
+    if (e) {
+      if (!strcmp(e, "plain")) mode = 0;
+      else if (!strcmp(e, "slab")) mode = 1;
+      else if (!strcmp(e, "cluster")) mode = 2;
+    }
+  }
+  return mode;
+}
+
 // CTAs of the cooperative slab kernel on the current device (multiple of kSlabs)
 int slab_ctas() {
   static int ctas = -1;
@@ -268,11 +480,25 @@ extern "C" int sw_propagate_atomic(const int32_t* row_length, const int32_t* tar
                                    const int32_t* spikes, const int32_t* n_spikes, int32_t max_spikes,
                                    double* out, void* workspace, int64_t workspace_bytes,
                                    void* stream) {
-  (void)num_pre;
   if (max_spikes <= 0) return SW_OK;
-  // many spiking rows, an output that fits the shared-memory slabs and a
-  // caller workspace for the per-group slabs: the slab kernel
-  const int coop_ctas = slab_ctas();
+  const int mode = prop_mode();
+  const bool big = max_spikes >= kPropSlabMinSpikes && num_post > 0 && num_post <= kSlabs * kSlab;
+  // many spiking rows and an output that fits four shared-memory slabs: the
+  // cluster / multicast kernel
+  // (experimental, SW_PROP_MODE=cluster only: the single producer thread
+  // cannot yet issue chunks as fast as the cluster consumes them)
+  if (big && mode == 2 && cluster_count() > 0) {
+    int clusters = cluster_count();
+    const int need = (max_spikes + kCW - 1) / kCW;
+    if (clusters > need) clusters = need;
+    k_prop_cluster<<<clusters * kSlabs, (kCW + 1) * 32, kPropClusterSmem, (cudaStream_t)stream>>>(
+        row_length, target, w, stride, (int64_t)num_pre, spikes, n_spikes, out, num_post);
+    sw::count_launch();
+    SW_CHECK_LAUNCH("sw_propagate_atomic(cluster)");
+    return SW_OK;
+  }
+  // slab kernel (cooperative, caller workspace)
+  const int coop_ctas = (mode == -1 || mode == 1) ? slab_ctas() : 0;
   if (coop_ctas >= kSlabs && max_spikes >= kPropSlabMinSpikes && num_post > 0 &&
       num_post <= kSlabs * kSlab && workspace != nullptr) {
     const int groups = coop_ctas / kSlabs;
