@@ -323,8 +323,8 @@ def run_device(args, w):
     from paper_2510_19764_b200.classifier import EpropClassifierTrainer, SyntheticTask
 
     B = w["batch"]
-    per = B // ws
-    local_slice = slice(rank * per, (rank + 1) * per if rank < ws - 1 else B)
+    from paper_2510_19764_b200.sharding import shard_batch
+    local_slice = shard_batch(B, rank, ws)
     task = SyntheticTask(num_classes=w["classes"], num_inputs=w["num_inputs"],
                          example_steps=w["steps"], seed=1, num_train=NUM_TRAIN, num_test=2264)
     tr = EpropClassifierTrainer(task, hidden=w["hidden"], input_density=w["density"],

@@ -26,6 +26,7 @@ from .deep_r import DeepR
 from .neurons import AlifParams
 from .plasticity import Adam
 from .rng import CounterRng, fold_key
+from .sharding import allreduce_flat
 from .updates import Model
 
 
@@ -356,16 +357,8 @@ class EpropClassifierTrainer:
     def _allreduce_grads(self) -> None:
         """Batch-DP: sum raw gradients and batch statistics over ranks
         (classifier.py:242-246 order: reduce, then scale)."""
-        import torch.distributed as dist
-        flat = torch.cat([self.s_in.planes["grad"].flatten(), self.s_rec.planes["grad"].flatten(),
-                          self.g_w_out.flatten(), self.g_b_out, self.stats])
-        dist.all_reduce(flat, group=self.pg)
-        o = 0
-        for t in (self.s_in.planes["grad"], self.s_rec.planes["grad"], self.g_w_out, self.g_b_out,
-                  self.stats):
-            n = t.numel()
-            t.copy_(flat[o:o + n].view_as(t))
-            o += n
+        allreduce_flat([self.s_in.planes["grad"], self.s_rec.planes["grad"], self.g_w_out,
+                        self.g_b_out, self.stats], group=self.pg)
 
     def gradient_phase(self, batch_index: int, host=None, resident: bool = False
                        ) -> tuple[float, float]:
