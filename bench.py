@@ -282,27 +282,36 @@ def run_mupdate(fracs=(0.001, 0.01, 0.1), P=1 << 20, N=65536, cap=1024, seed=1):
             "propagate_atomic": prop}
 
 
-def run_topomap_sweep(scales=(1, 2, 4, 8, 16), model_ms=100.0, seed=1):
+def run_topomap_sweep(scales=(1, 2, 4, 8, 16), model_ms=100.0, seed=1, process_group=None):
     """Topographic-map simulation speed (x realtime) vs network size,
-    TopomapModel(s) semantics, no recorder, CUDA-graph replay per 1 ms,
-    stimulus rates computed on the device (rates_on_device)."""
+    TopomapModel(s) semantics, no recorder, stimulus rates computed on the
+    device (rates_on_device).  One GPU: CUDA-graph replay per 1 ms.  Under
+    torchrun: postsynaptic sharding over the ranks with a per-step NCCL
+    all-gather of the target spikes (eager stepping); time = max over ranks."""
     import torch
+    import torch.distributed as dist
     from paper_2510_19764_b200.topomap import TopomapModel
     res = {}
     for s in scales:
         t0 = time.perf_counter()
         model = TopomapModel(s, seed=seed, record_events=False, use_graph=True,
-                             rates_on_device=True)
+                             rates_on_device=True, process_group=process_group)
         torch.cuda.synchronize()
         build_s = time.perf_counter() - t0
         model.run(10.0)   # warm-up: capture + first replays
         torch.cuda.synchronize()
+        if process_group is not None:
+            dist.barrier(group=process_group)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         rec = model.run(model_ms)
         e1.record()
         e1.synchronize()
         wall_ms = e0.elapsed_time(e1)
+        if process_group is not None:
+            t = torch.tensor([wall_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=process_group)
+            wall_ms = float(t.item())
         res[f"s{s}"] = {"n": model.geometry.n, "x_realtime": round(model_ms / wall_ms, 3),
                         "us_per_step": round(wall_ms * 1e3 / rec.steps, 2), "build_s": round(build_s, 2),
                         "rewires": int(sum(rec.rewires_per_update)),
@@ -464,6 +473,13 @@ def run_device(args, w):
             torch.cuda.empty_cache()
             line["mupdate"] = run_mupdate()
             line["topomap"] = run_topomap_sweep()
+    if ws > 1 and not args.no_micro:
+        # every rank takes part in the sharded topomap sweep
+        topo = run_topomap_sweep(model_ms=20.0, process_group=dist.group.WORLD)
+        if rank == 0:
+            line["topomap"] = topo
+            line["topomap_parallelism"] = f"post-sharded x{ws}, NCCL spike all-gather per step"
+    if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

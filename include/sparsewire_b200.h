@@ -350,10 +350,22 @@ typedef struct sw_topomap_step {
   const int32_t* lat_col_ptr; const int32_t* lat_src_pre; const int32_t* lat_src_slot;
   double* ff_x; double* ff_y; double* lat_x; double* lat_y;
   double decay_x, decay_y, a_plus, a_minus, w_min, w_max;
+  /* postsynaptic shard [post_lo, post_hi) of this rank (0, n when unsharded):
+   * the LIF update and the propagation into `pending` cover these posts only;
+   * bounds on 32-post spike-word boundaries.  Source spikes, trace decays,
+   * STDP and the step counter cover the whole sheet. */
+  int32_t post_lo, post_hi;
 } sw_topomap_step_t;
 /* neurons -> ordered propagation + trace decay -> STDP pre -> STDP post ->
  * step += 1; spike_counts[2] (device, may be NULL) accumulate spikes. */
 SW_API int sw_topomap_step(const sw_topomap_step_t* s, int64_t* spike_counts, void* stream);
+/* The same step split around the target-spike exchange of the sharded
+ * model (topomap.py:426-450 with postsynaptic sharding):
+ * sw_topomap_neurons = Poisson sources (all nodes) + LIF (owned posts),
+ * writing src_bits fully and tgt_bits for the owned words; the caller then
+ * all-gathers tgt_bits; sw_topomap_synapses = the rest of the step. */
+SW_API int sw_topomap_neurons(const sw_topomap_step_t* s, void* stream);
+SW_API int sw_topomap_synapses(const sw_topomap_step_t* s, int64_t* spike_counts, void* stream);
 
 #ifdef __cplusplus
 }

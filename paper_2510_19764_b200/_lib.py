@@ -68,7 +68,7 @@ class TopomapStep(C.Structure):
                 ("lat_col_ptr", P), ("lat_src_pre", P), ("lat_src_slot", P),
                 ("ff_x", P), ("ff_y", P), ("lat_x", P), ("lat_y", P),
                 ("decay_x", F64), ("decay_y", F64), ("a_plus", F64), ("a_minus", F64),
-                ("w_min", F64), ("w_max", F64)]
+                ("w_min", F64), ("w_max", F64), ("post_lo", I32), ("post_hi", I32)]
 
 
 class EpropSeg(C.Structure):
@@ -128,6 +128,8 @@ SIGNATURES: dict[str, list] = {
     "sw_stdp_post": [P, P, P, P, I32, I32, P, P, P, F64, F64, F64, P],
     "sw_rewire_update": [RP, I32, P, P, P, P, P, P, P, P, P, P, I32, P],
     "sw_topomap_step": [P, P, P],
+    "sw_topomap_neurons": [P, P],
+    "sw_topomap_synapses": [P, P, P],
     "sw_flip_signs": [RP, I32, U64, F64, P],
     "sw_adam_f64": [P, P, P, P, I64, F64, F64, F64, F64, F64, F64, F64, F64, P],
 }

@@ -23,8 +23,10 @@ __global__ void k_tm_neurons(sw_topomap_step_t S) {
   for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
     const int x = base + threadIdx.x;
     bool src = false, tgt = false;
-    if (x < n) {
-      src = sw::u01(sw::draw(S.poisson_key, (uint64_t)(k * n + x))) < S.p_src[x];
+    // the owned range is word-aligned, so a warp is either owned or not
+    const bool own = x >= S.post_lo && x < S.post_hi;
+    if (x < n) src = sw::u01(sw::draw(S.poisson_key, (uint64_t)(k * n + x))) < S.p_src[x];
+    if (x < n && own) {
       const double gg = __dmul_rn(__dadd_rn(S.g_tot[x], S.pending[x]), S.decay_s);
       S.g_tot[x] = gg;
       const bool active = k > S.ref_until[x];
@@ -44,13 +46,19 @@ __global__ void k_tm_neurons(sw_topomap_step_t S) {
     if (lane == 0 && base + (threadIdx.x & ~31) < n) {
       const int w = (base + (threadIdx.x & ~31)) >> 5;
       S.src_bits[w] = bs;
-      S.tgt_bits[w] = bt;
+      if (own) S.tgt_bits[w] = bt;
     }
   }
 }
 
 __global__ void k_tm_prop(sw_topomap_step_t S) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < S.n; j += gridDim.x * blockDim.x) {
+    // trace decays (x per pre, y per post; square model: n pres and n posts)
+    S.ff_x[j] = __dmul_rn(S.ff_x[j], S.decay_x);
+    S.ff_y[j] = __dmul_rn(S.ff_y[j], S.decay_y);
+    S.lat_x[j] = __dmul_rn(S.lat_x[j], S.decay_x);
+    S.lat_y[j] = __dmul_rn(S.lat_y[j], S.decay_y);
+    if (j < S.post_lo || j >= S.post_hi) continue;
     double acc = 0.0;
     for (int q = S.ff_col_ptr[j]; q < S.ff_col_ptr[j + 1]; ++q) {
       const int i = S.ff_src_pre[q];
@@ -61,11 +69,6 @@ __global__ void k_tm_prop(sw_topomap_step_t S) {
       if (bit(S.tgt_bits, i)) acc = __dadd_rn(acc, S.lat_g[(int64_t)i * S.lat_stride + S.lat_src_slot[q]]);
     }
     S.pending[j] = acc;
-    // trace decays (x per pre, y per post; square model: n pres and n posts)
-    S.ff_x[j] = __dmul_rn(S.ff_x[j], S.decay_x);
-    S.ff_y[j] = __dmul_rn(S.ff_y[j], S.decay_y);
-    S.lat_x[j] = __dmul_rn(S.lat_x[j], S.decay_x);
-    S.lat_y[j] = __dmul_rn(S.lat_y[j], S.decay_y);
   }
 }
 
@@ -155,11 +158,29 @@ int grid1(int64_t n) {
 
 }  // namespace
 
-extern "C" int sw_topomap_step(const sw_topomap_step_t* s, int64_t* spike_counts, void* stream) {
+static int check_step(const sw_topomap_step_t* s) {
+  if (s->post_lo < 0 || s->post_hi > s->n || s->post_lo > s->post_hi || (s->post_lo & 31) ||
+      ((s->post_hi & 31) && s->post_hi != s->n)) {
+    sw::set_last_error("topomap step: post shard must be [lo, hi) on 32-post word boundaries");
+    return SW_ERR_INVALID_ARG;
+  }
+  return SW_OK;
+}
+
+extern "C" int sw_topomap_neurons(const sw_topomap_step_t* s, void* stream) {
+  if (int e = check_step(s)) return e;
+  const int n = s->n;
+  if (n <= 0) return SW_OK;
+  k_tm_neurons<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(*s); sw::count_launch();
+  SW_CHECK_LAUNCH("sw_topomap_neurons");
+  return SW_OK;
+}
+
+extern "C" int sw_topomap_synapses(const sw_topomap_step_t* s, int64_t* spike_counts, void* stream) {
+  if (int e = check_step(s)) return e;
   cudaStream_t st = (cudaStream_t)stream;
   const int n = s->n;
   if (n <= 0) return SW_OK;
-  k_tm_neurons<<<grid1(n), 256, 0, st>>>(*s); sw::count_launch();
   k_tm_prop<<<grid1(n), 256, 0, st>>>(*s); sw::count_launch();
   int groups = (n + 31) / 32;
   int blocks = (2 * groups + 7) / 8;
@@ -167,6 +188,11 @@ extern "C" int sw_topomap_step(const sw_topomap_step_t* s, int64_t* spike_counts
   k_tm_pre<<<blocks, 256, 0, st>>>(*s); sw::count_launch();
   k_tm_post<<<grid1(n), 256, 0, st>>>(*s); sw::count_launch();
   k_tm_tick<<<1, 256, 0, st>>>(*s, spike_counts); sw::count_launch();
-  SW_CHECK_LAUNCH("sw_topomap_step");
+  SW_CHECK_LAUNCH("sw_topomap_synapses");
   return SW_OK;
+}
+
+extern "C" int sw_topomap_step(const sw_topomap_step_t* s, int64_t* spike_counts, void* stream) {
+  if (int e = sw_topomap_neurons(s, stream)) return e;
+  return sw_topomap_synapses(s, spike_counts, stream);
 }

@@ -26,6 +26,7 @@ from .connectivity import descriptor, init_pairwise_bernoulli_torus
 from .geometry import GridGeometry
 from .neurons import LifCondLayer, LifCondParams, PoissonParams, PoissonSource
 from .plasticity import StdpParams, StdpSynapses
+from .sharding import SpikeGather
 from .rng import CounterRng, fold_key
 from .updates import Model, RuleDescriptor
 
@@ -168,7 +169,11 @@ class TopomapModel:
 
     def __init__(self, scale: int, seed: int, workers: int = 1, always_remap: bool = False,
                  capacity_headroom: float = 4.0, record_events: bool = True,
-                 use_graph: bool = True, rates_on_device: bool = False):
+                 use_graph: bool = True, rates_on_device: bool = False, process_group=None):
+        """``process_group`` (torch.distributed, NCCL): postsynaptic sharding
+        over its ranks (sharding.py): this rank updates the LIF state of and
+        propagates into its own post range, target spikes are all-gathered
+        every step, STDP and rewiring run replicated."""
         _lib.require_cuda()
         scale = max(scale, 1)
         self.scale = scale
@@ -188,6 +193,17 @@ class TopomapModel:
                                                CounterRng(seed, "init", "lat"), capacity_headroom)
         self.source = PoissonSource(self.geometry, PoissonParams())
         self.target = LifCondLayer(n)
+        self.pg = process_group
+        if process_group is not None:
+            import torch.distributed as dist
+            rank, world = dist.get_rank(process_group), dist.get_world_size(process_group)
+        else:
+            rank, world = 0, 1
+        self.shard = SpikeGather(n, rank, world, "cuda", process_group)
+        self.post_lo, self.post_hi = self.shard.lo, self.shard.hi
+        if world > 1:
+            # target spikes live in the all-gather buffer (world * words-per-rank words)
+            self.target.spike_bits = self.shard.bits
         self.ff_stdp = StdpSynapses(ff_m, ff_syn, self.h, self.stdp_params)
         self.lat_stdp = StdpSynapses(lat_m, lat_syn, self.h, self.stdp_params)
         self.ff_tmap = self.net.register_transpose("ff")
@@ -250,11 +266,28 @@ class TopomapModel:
         sp = self.stdp_params
         s.decay_x, s.decay_y = self.ff_stdp._decay_x, self.ff_stdp._decay_y
         s.a_plus, s.a_minus, s.w_min, s.w_max = sp.a_plus, sp.a_minus, sp.w_min, sp.w_max
+        s.post_lo, s.post_hi = self.post_lo, self.post_hi
         return s
 
     def _launch_step(self) -> None:
         s = self._step_struct()
-        _lib.call("sw_topomap_step", ctypes.byref(s), self.spike_counts.data_ptr(), _lib.stream_ptr())
+        st = _lib.stream_ptr()
+        if self.shard.world == 1:
+            _lib.call("sw_topomap_step", ctypes.byref(s), self.spike_counts.data_ptr(), st)
+            return
+        self.launch_neurons(s)
+        self.shard.gather()          # NCCL all-gather of the target-spike words
+        self.launch_synapses(s)
+
+    # the two halves of a sharded step (around the target-spike exchange)
+    def launch_neurons(self, s=None) -> None:
+        s = s if s is not None else self._step_struct()
+        _lib.call("sw_topomap_neurons", ctypes.byref(s), _lib.stream_ptr())
+
+    def launch_synapses(self, s=None) -> None:
+        s = s if s is not None else self._step_struct()
+        _lib.call("sw_topomap_synapses", ctypes.byref(s), self.spike_counts.data_ptr(),
+                  _lib.stream_ptr())
 
     def _period(self, rewire_steps: int) -> None:
         """rewire_steps model steps + the rewiring group (device only)."""
@@ -280,7 +313,7 @@ class TopomapModel:
         n_steps = int(round(duration_ms / h))
         if recorder is not None:
             raise NotImplementedError("TopomapRecorder analysis trail is out of scope (SURVEY 2.1)")
-        graph_ok = (self.use_graph and not self.ff_rule.record_events
+        graph_ok = (self.use_graph and self.shard.world == 1 and not self.ff_rule.record_events
                     and not self.lat_rule.record_events and stim_steps % rewire_steps == 0)
         u0 = self.ff_rule._host_update if self.ff_rule._host_update else 0
         done = 0

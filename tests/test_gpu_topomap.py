@@ -193,3 +193,50 @@ def test_one_step_transmission_delay(dev_lib):
     decay = math.exp(-0.1 / 5.0)
     tg = m.row_targets(5).long()
     assert np.allclose(model.target.g[tg].cpu().numpy(), 0.2 * decay)
+
+
+def test_post_sharded_steps_equal_unsharded(dev_lib):
+    """Postsynaptic sharding on one device: two half-sheet
+    'ranks' stepped in lock-step with the target-spike words exchanged by
+    hand (the NCCL all-gather of the multi-GPU run) reproduce the unsharded
+    model: connectivity, weights and traces everywhere, V on the owned posts."""
+    from paper_2510_19764_b200.sharding import SpikeGather
+    from paper_2510_19764_b200.topomap import TopomapModel
+    from paper_2510_19764_b200.neurons import PoissonParams
+    kw = dict(record_events=False, use_graph=False)
+    ref = TopomapModel(2, seed=33, **kw)
+    shards = [TopomapModel(2, seed=33, **kw) for _ in range(2)]
+    n = ref.geometry.n
+    for r, m in enumerate(shards):
+        sg = SpikeGather(n, r, 2, "cuda")
+        m.shard, m.post_lo, m.post_hi = sg, sg.lo, sg.hi
+        m.target.spike_bits = sg.bits
+    h = ref.h
+    stim_steps = int(round(PoissonParams().t_stim / h))
+    for k in range(600):
+        for m in [ref] + shards:
+            if k % stim_steps == 0:
+                m.source.set_correlated_rates(m._draw_centers())
+                m.source.probabilities(h)
+        ref._launch_step()
+        for m in shards:
+            m.launch_neurons()
+        a, b = shards
+        a.shard.bits[b.shard.own_words] = b.shard.bits[b.shard.own_words]
+        b.shard.bits[a.shard.own_words] = a.shard.bits[a.shard.own_words]
+        for m in shards:
+            m.launch_synapses()
+        if (k + 1) % 10 == 0:
+            for m in [ref] + shards:
+                m.net.run_update_group("rewiring")
+    sr = ref.state_arrays()
+    assert int(ref.spike_counts[1]) > 0
+    for m in shards:
+        st = m.state_arrays()
+        for key in sr:
+            if key in ("V", "g_total", "refractory", "pending"):
+                lo, hi = m.post_lo, m.post_hi
+                assert np.array_equal(st[key][lo:hi], sr[key][lo:hi]), key
+            else:
+                assert np.array_equal(st[key], sr[key]), key
+        assert torch.equal(m.spike_counts, ref.spike_counts)
