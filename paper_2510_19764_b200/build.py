@@ -48,7 +48,7 @@ def _compile(src: str, force: bool, verbose: bool) -> str:
     if (not force and os.path.exists(obj)
             and os.path.getmtime(obj) >= max(os.path.getmtime(src), _deps_mtime())):
         return obj
-    cmd = [nvcc(), "-c", src, "-o", obj] + NVFLAGS
+    cmd = [nvcc(), "-c", src, "-o", obj] + NVFLAGS + os.environ.get("SW_NVCC_EXTRA", "").split()
     if verbose:
         cmd += ["-Xptxas", "-v"]
         print(" ".join(cmd))

@@ -214,12 +214,7 @@ k_deepr_elim_vec(sw_ragged_t m, int wp, sw_bitfield_t conn, int64_t* dormant, ui
           }
           const int tot = __shfl_sync(SW_FULL_MASK, pre, 31);
           int pos = k + pre - cnt;
-          for (unsigned mm = mine; mm; mm &= mm - 1) {
-            const int sl = s0 + __ffs(mm) - 1;
-            list[pos++] = sl;
-            const int t = __ldg(m.target + off + sl);
-            atomicAnd((unsigned long long*)&cbits[t >> 6], ~(1ull << (t & 63)));
-          }
+          for (unsigned mm = mine; mm; mm &= mm - 1) list[pos++] = s0 + __ffs(mm) - 1;
           k += tot;
         }
       }
@@ -227,6 +222,11 @@ k_deepr_elim_vec(sw_ragged_t m, int wp, sw_bitfield_t conn, int64_t* dormant, ui
     __syncwarp();
     if (lane == 0) dormant[i] = k;
     if (k > 0) {
+      // conn-bit clears of the whole row in one round of target loads
+      for (int q = lane; q < k; q += 32) {
+        const int t = __ldg(m.target + off + list[q]);
+        atomicAnd((unsigned long long*)&cbits[t >> 6], ~(1ull << (t & 63)));
+      }
       sw::warp_apply_removal(m, off, list, n, k, cache + i * (int64_t)cw);
       if (lane == 0) m.row_length[i] = n - k;
     }
@@ -442,17 +442,14 @@ k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row
           }
         }
       }
-      if ((placed >> lane) & 1u) {
-        const int slot = len - __popc(placed) + __popc(placed & lt);
+      const bool pl = (placed >> lane) & 1u;
+      const int slot = len - __popc(placed) + __popc(placed & lt);
+      if (pl) {
         m.target[off + slot] = j;
         sw::zero_slot(m, off, slot);
         atomicOr((unsigned long long*)(crow + (j >> 6)), 1ull << (j & 63));
-        if (cache) {
-          uint32_t* cr = cache + i * (int64_t)((m.stride + 31) >> 5);
-          if (sbit) atomicOr(&cr[slot >> 5], 1u << (slot & 31));
-          else atomicAnd(&cr[slot >> 5], ~(1u << (slot & 31)));
-        }
       }
+      if (cache) sw::warp_cache_bits(cache + i * (int64_t)((m.stride + 31) >> 5), pl, slot, sbit);
       ctr += (uint64_t)consumed;
       __syncwarp();
     }

@@ -33,6 +33,22 @@ __device__ __forceinline__ void zero_slot(const sw_ragged_t& m, int64_t off, int
   }
 }
 
+// Slot-aligned sign-cache update for the slots of one warp instruction
+// (warp-uniform call): lanes sharing a cache word are combined, and one lane
+// per word issues at most one atomicOr and one atomicAnd.
+__device__ __forceinline__ void warp_cache_bits(uint32_t* cache_row, bool active, int slot, bool bit) {
+  const int lane = threadIdx.x & 31;
+  const int word = active ? (slot >> 5) : -1;
+  const unsigned peers = __match_any_sync(0xffffffffu, word);
+  const uint32_t b = active ? (1u << (slot & 31)) : 0u;
+  const uint32_t s_or = __reduce_or_sync(peers, bit ? b : 0u);
+  const uint32_t c_or = __reduce_or_sync(peers, bit ? 0u : b);
+  if (active && lane == __ffs(peers) - 1) {
+    if (s_or) atomicOr(&cache_row[word], s_or);
+    if (c_or) atomicAnd(&cache_row[word], ~c_or);
+  }
+}
+
 // Exact remove_slots permutation (connectivity.py:130-136).
 // list[0..k) holds the marked slots of a row of length n in ASCENDING order.
 // The t-th largest marked slot m_t (t = 1..k) that lies below n2 = n - k
@@ -47,6 +63,8 @@ __device__ __forceinline__ void warp_apply_removal(const sw_ragged_t& m, int64_t
   const int n2 = n - k;
   for (int t0 = 1; t0 <= k; t0 += 32) {
     const int t = t0 + lane;
+    bool moved = false, cbit = false;
+    int dst = 0;
     if (t <= k) {
       const int mt = list[k - t];
       if (mt < n2) {
@@ -65,13 +83,15 @@ __device__ __forceinline__ void warp_apply_removal(const sw_ragged_t& m, int64_t
         }
         move_slot(m, off, mt, p);
         if (cache_row) {
-          // slot-aligned sign cache follows the move (sources are all in the tail)
-          const uint32_t b = (cache_row[p >> 5] >> (p & 31)) & 1u;
-          if (b) atomicOr(&cache_row[mt >> 5], 1u << (mt & 31));
-          else atomicAnd(&cache_row[mt >> 5], ~(1u << (mt & 31)));
+          // the slot-aligned sign cache follows the move (sources are all in
+          // the tail, destinations below it: no read sees a written word)
+          cbit = (cache_row[p >> 5] >> (p & 31)) & 1u;
+          moved = true;
+          dst = mt;
         }
       }
     }
+    if (cache_row) warp_cache_bits(cache_row, moved, dst, cbit);
   }
 }
 
