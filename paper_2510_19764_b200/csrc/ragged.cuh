@@ -10,26 +10,35 @@ struct RowView {
 };
 
 // Move slot src -> dst in target and every plane (connectivity.py:121-125).
+// All source values are loaded before any store, so the loads of one move
+// are in flight together.
 __device__ __forceinline__ void move_slot(const sw_ragged_t& m, int64_t off, int dst, int src) {
-  m.target[off + dst] = m.target[off + src];
-#pragma unroll 1
-  for (int p = 0; p < m.n_planes; ++p) {
-    if (m.plane_bytes[p] == 8) {
-      uint64_t* pl = (uint64_t*)m.planes[p];
-      pl[off + dst] = pl[off + src];
-    } else {
-      uint32_t* pl = (uint32_t*)m.planes[p];
-      pl[off + dst] = pl[off + src];
+  const int32_t t = m.target[off + src];
+  uint64_t v[SW_MAX_PLANES];
+#pragma unroll
+  for (int p = 0; p < SW_MAX_PLANES; ++p) {
+    if (p < m.n_planes)
+      v[p] = (m.plane_bytes[p] == 8) ? ((const uint64_t*)m.planes[p])[off + src]
+                                     : (uint64_t)((const uint32_t*)m.planes[p])[off + src];
+  }
+  m.target[off + dst] = t;
+#pragma unroll
+  for (int p = 0; p < SW_MAX_PLANES; ++p) {
+    if (p < m.n_planes) {
+      if (m.plane_bytes[p] == 8) ((uint64_t*)m.planes[p])[off + dst] = v[p];
+      else ((uint32_t*)m.planes[p])[off + dst] = (uint32_t)v[p];
     }
   }
 }
 
 // Zero every plane at one slot (add_synapse, connectivity.py:103-105).
 __device__ __forceinline__ void zero_slot(const sw_ragged_t& m, int64_t off, int s) {
-#pragma unroll 1
-  for (int p = 0; p < m.n_planes; ++p) {
-    if (m.plane_bytes[p] == 8) ((uint64_t*)m.planes[p])[off + s] = 0ull;
-    else ((uint32_t*)m.planes[p])[off + s] = 0u;
+#pragma unroll
+  for (int p = 0; p < SW_MAX_PLANES; ++p) {
+    if (p < m.n_planes) {
+      if (m.plane_bytes[p] == 8) ((uint64_t*)m.planes[p])[off + s] = 0ull;
+      else ((uint32_t*)m.planes[p])[off + s] = 0u;
+    }
   }
 }
 
@@ -81,11 +90,12 @@ __device__ __forceinline__ void warp_apply_removal(const sw_ragged_t& m, int64_t
           if (q < 0) break;
           p = n - (k - q);   // rank(list[q]) = k - q
         }
+        // the slot-aligned sign cache follows the move (sources are all in
+        // the tail, destinations below it: no read sees a written word)
+        const uint32_t cw = cache_row ? cache_row[p >> 5] : 0u;
         move_slot(m, off, mt, p);
         if (cache_row) {
-          // the slot-aligned sign cache follows the move (sources are all in
-          // the tail, destinations below it: no read sees a written word)
-          cbit = (cache_row[p >> 5] >> (p & 31)) & 1u;
+          cbit = (cw >> (p & 31)) & 1u;
           moved = true;
           dst = mt;
         }
