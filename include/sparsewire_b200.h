@@ -333,6 +333,13 @@ SW_API int sw_rewire_update(const sw_ragged_t* m, int32_t weight_plane, const sw
                             int64_t* totals, int32_t* changed, int64_t* rej, int32_t* ev_off,
                             int8_t* ev_kind, double* ev_d, int32_t forced_attempts, void* stream);
 
+/* Per-update structural-change log of the two projections (RunRecord
+ * rewires_per_update; topomap.py:457-458 collect()):
+ * log[u] = {removed_a, formed_a, removed_b, formed_b}, u = *update_count - 1
+ * clamped to [0, cap). */
+SW_API int sw_topomap_log(const int64_t* update_count, const int64_t* totals_a,
+                          const int64_t* totals_b, int64_t* log, int64_t cap, void* stream);
+
 /* ---- topographic-map step (topomap.py:419-452) ------------------------------ */
 typedef struct sw_topomap_step {
   int32_t n;                      /* nodes per sheet (num_pre = num_post) */
@@ -365,6 +372,12 @@ SW_API int sw_topomap_step(const sw_topomap_step_t* s, int64_t* spike_counts, vo
  * writing src_bits fully and tgt_bits for the owned words; the caller then
  * all-gathers tgt_bits; sw_topomap_synapses = the rest of the step. */
 SW_API int sw_topomap_neurons(const sw_topomap_step_t* s, void* stream);
+/* n_steps whole steps (unsharded sheet) in one persistent cooperative launch:
+ * the phases of a step are separated by grid-wide barriers instead of kernel
+ * boundaries.  barrier_words: 2 zeroed uint32 (device), left consistent for
+ * the next launch.  Same results as n_steps calls of sw_topomap_step. */
+SW_API int sw_topomap_run_steps(const sw_topomap_step_t* s, int32_t n_steps, int64_t* spike_counts,
+                                uint32_t* barrier_words, void* stream);
 SW_API int sw_topomap_synapses(const sw_topomap_step_t* s, int64_t* spike_counts, void* stream);
 
 #ifdef __cplusplus

@@ -218,3 +218,24 @@ extern "C" int sw_rewire_update(const sw_ragged_t* m, int32_t weight_plane, cons
   SW_CHECK_LAUNCH("sw_rewire_update");
   return SW_OK;
 }
+
+namespace {
+__global__ void k_tm_log(const int64_t* update, const int64_t* ta, const int64_t* tb, int64_t* log,
+                         int64_t cap) {
+  int64_t idx = *update - 1;
+  idx = idx < 0 ? 0 : (idx >= cap ? cap - 1 : idx);
+  log[idx * 4 + 0] = ta[0];
+  log[idx * 4 + 1] = ta[2];
+  log[idx * 4 + 2] = tb[0];
+  log[idx * 4 + 3] = tb[2];
+}
+}  // namespace
+
+extern "C" int sw_topomap_log(const int64_t* update_count, const int64_t* totals_a,
+                              const int64_t* totals_b, int64_t* log, int64_t cap, void* stream) {
+  if (cap <= 0) return SW_OK;
+  k_tm_log<<<1, 1, 0, (cudaStream_t)stream>>>(update_count, totals_a, totals_b, log, cap);
+  sw::count_launch();
+  SW_CHECK_LAUNCH("sw_topomap_log");
+  return SW_OK;
+}

@@ -16,12 +16,13 @@ namespace {
 
 __device__ __forceinline__ bool bit(const uint32_t* b, int i) { return (b[i >> 5] >> (i & 31)) & 1u; }
 
-__global__ void k_tm_neurons(sw_topomap_step_t S) {
+// ---- phase bodies (grid-stride over [t0, n) with step dt) --------------------------
+__device__ __forceinline__ void tm_neurons(const sw_topomap_step_t& S, int64_t k, int t0, int dt) {
   const int lane = threadIdx.x & 31;
-  const int64_t k = *S.step;
   const int n = S.n;
-  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
-    const int x = base + threadIdx.x;
+  // warp-aligned grid stride so that a warp's 32 nodes form one spike word
+  for (int base = t0 & ~31; base < n; base += dt) {
+    const int x = base + lane;
     bool src = false, tgt = false;
     // the owned range is word-aligned, so a warp is either owned or not
     const bool own = x >= S.post_lo && x < S.post_hi;
@@ -43,16 +44,15 @@ __global__ void k_tm_neurons(sw_topomap_step_t S) {
     }
     const unsigned bs = __ballot_sync(SW_FULL_MASK, src);
     const unsigned bt = __ballot_sync(SW_FULL_MASK, tgt);
-    if (lane == 0 && base + (threadIdx.x & ~31) < n) {
-      const int w = (base + (threadIdx.x & ~31)) >> 5;
-      S.src_bits[w] = bs;
-      if (own) S.tgt_bits[w] = bt;
+    if (lane == 0 && base < n) {
+      S.src_bits[base >> 5] = bs;
+      if (own) S.tgt_bits[base >> 5] = bt;
     }
   }
 }
 
-__global__ void k_tm_prop(sw_topomap_step_t S) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < S.n; j += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void tm_prop(const sw_topomap_step_t& S, int t0, int dt) {
+  for (int j = t0; j < S.n; j += dt) {
     // trace decays (x per pre, y per post; square model: n pres and n posts)
     S.ff_x[j] = __dmul_rn(S.ff_x[j], S.decay_x);
     S.ff_y[j] = __dmul_rn(S.ff_y[j], S.decay_y);
@@ -84,11 +84,11 @@ __device__ __forceinline__ void depress_row(const int32_t* rl, const int32_t* tg
   }
 }
 
-__global__ void k_tm_pre(sw_topomap_step_t S) {
+// warp w0, w0 + dw, ... over the 2 * words spike words (ff sources, then lat targets)
+__device__ __forceinline__ void tm_pre(const sw_topomap_step_t& S, int w0, int dw) {
   const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x >> 5;
   const int groups = (S.n + 31) / 32;
-  for (int g = blockIdx.x * wpb + (threadIdx.x >> 5); g < 2 * groups; g += gridDim.x * wpb) {
+  for (int g = w0; g < 2 * groups; g += dw) {
     const bool ff = g < groups;
     const int grp = ff ? g : g - groups;
     unsigned m = ff ? S.src_bits[grp] : S.tgt_bits[grp];
@@ -105,8 +105,8 @@ __global__ void k_tm_pre(sw_topomap_step_t S) {
   }
 }
 
-__global__ void k_tm_post(sw_topomap_step_t S) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < S.n; j += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void tm_post(const sw_topomap_step_t& S, int t0, int dt) {
+  for (int j = t0; j < S.n; j += dt) {
     if (!bit(S.tgt_bits, j)) continue;
     for (int q = S.ff_col_ptr[j]; q < S.ff_col_ptr[j + 1]; ++q) {
       const int i = S.ff_src_pre[q];
@@ -127,27 +127,161 @@ __global__ void k_tm_post(sw_topomap_step_t S) {
   }
 }
 
-__global__ void k_tm_tick(sw_topomap_step_t S, int64_t* spike_counts) {
-  // step += 1 and per-step spike counters (source, target)
-  __shared__ int cs, ct;
-  if (threadIdx.x == 0) { cs = 0; ct = 0; }
-  __syncthreads();
+// per-step spike counts of words [w0, words) step dw, added to cnt[2]
+__device__ __forceinline__ void tm_count(const sw_topomap_step_t& S, int w0, int dw, int64_t* cnt) {
   const int words = (S.n + 31) / 32;
   int a = 0, b = 0;
-  for (int w = threadIdx.x; w < words; w += blockDim.x) {
+  for (int w = w0; w < words; w += dw) {
     a += __popc(S.src_bits[w]);
     b += __popc(S.tgt_bits[w]);
   }
-  atomicAdd(&cs, a);
-  atomicAdd(&ct, b);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    *S.step += 1;
-    if (spike_counts) {
-      spike_counts[0] += cs;
-      spike_counts[1] += ct;
-    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(SW_FULL_MASK, a, o);
+    b += __shfl_xor_sync(SW_FULL_MASK, b, o);
   }
+  if ((threadIdx.x & 31) == 0 && (a | b)) {
+    atomicAdd((unsigned long long*)&cnt[0], (unsigned long long)a);
+    atomicAdd((unsigned long long*)&cnt[1], (unsigned long long)b);
+  }
+}
+
+// ---- one phase per launch (the sharded path splits the step around an all-gather) --
+__global__ void k_tm_neurons(sw_topomap_step_t S) {
+  tm_neurons(S, *S.step, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+
+__global__ void k_tm_prop(sw_topomap_step_t S) {
+  tm_prop(S, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+
+__global__ void k_tm_pre(sw_topomap_step_t S) {
+  tm_pre(S, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gridDim.x * (blockDim.x >> 5));
+}
+
+__global__ void k_tm_post(sw_topomap_step_t S) {
+  tm_post(S, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+
+__global__ void k_tm_tick(sw_topomap_step_t S, int64_t* spike_counts) {
+  // step += 1 and per-step spike counters (source, target); one block
+  if (spike_counts) tm_count(S, threadIdx.x, blockDim.x, spike_counts);
+  __syncthreads();
+  if (threadIdx.x == 0) *S.step += 1;
+}
+
+// ---- persistent multi-step kernel ------------------------------------------------------
+// n_steps whole steps in one launch: the phases of a step are separated by
+// grid-wide barriers (cooperative launch: every CTA resident) — or by
+// __syncthreads when one CTA covers the sheet — instead of kernel
+// boundaries, so a step costs a few barrier latencies instead of five
+// launches.  Same phase bodies, same order, same results as sw_topomap_step.
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (gridDim.x > 1) {
+    if (threadIdx.x == 0) {
+      volatile unsigned* vb = bar;
+      const unsigned gen = vb[1];
+      __threadfence();
+      if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+        bar[0] = 0u;
+        __threadfence();
+        atomicAdd(&bar[1], 1u);
+      } else {
+        while (vb[1] == gen) __nanosleep(32);
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+k_tm_run(sw_topomap_step_t S, int n_steps, int64_t* spike_counts, unsigned* bar) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int gn = gridDim.x * blockDim.x;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  const int64_t k0 = *S.step;
+  grid_barrier(bar);   // everyone has read the step counter
+  for (int st = 0; st < n_steps; ++st) {
+    const int64_t k = k0 + st;
+    tm_neurons(S, k, gw * 32, nw * 32);
+    grid_barrier(bar);
+    tm_prop(S, gt, gn);
+    if (spike_counts) tm_count(S, gt, gn, spike_counts);
+    grid_barrier(bar);
+    tm_pre(S, gw, nw);
+    grid_barrier(bar);
+    tm_post(S, gt, gn);
+    grid_barrier(bar);
+  }
+  if (gt == 0) *S.step = k0 + n_steps;
+}
+
+// Single-CTA variant for small sheets: the per-node state (LIF, pending
+// input, STDP traces, source probabilities), the row lengths, the transpose
+// column pointers and the spike words live in shared memory for the whole
+// period — the phases' dependent memory round trips become shared-memory
+// hits — and are written back at the end.  Synapse arrays (targets,
+// transposes, weights) stay in global memory (L1/L2).
+struct TmSmem {
+  static size_t bytes(int n) {
+    const int words = (n + 31) / 32;
+    return (size_t)n * 8 * 9 + (size_t)(n + 1) * 4 * 2 + (size_t)n * 4 * 2 + (size_t)words * 4 * 2 + 64;
+  }
+};
+
+__global__ void __launch_bounds__(512, 1)
+k_tm_run_staged(sw_topomap_step_t G, int n_steps, int64_t* spike_counts) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int n = G.n, words = (n + 31) / 32;
+  double* d = reinterpret_cast<double*>(sm);
+  double *V = d, *gt = d + n, *pend = d + 2 * n, *fx = d + 3 * n, *fy = d + 4 * n, *lx = d + 5 * n,
+         *ly = d + 6 * n, *ps = d + 7 * n;
+  int64_t* ref = reinterpret_cast<int64_t*>(d + 8 * n);
+  int32_t* ip = reinterpret_cast<int32_t*>(d + 9 * n);
+  int32_t *fcp = ip, *lcp = ip + (n + 1), *frl = ip + 2 * (n + 1), *lrl = frl + n;
+  uint32_t *sb = reinterpret_cast<uint32_t*>(lrl + n), *tb = sb + words;
+  for (int x = threadIdx.x; x < n; x += blockDim.x) {
+    V[x] = G.V[x]; gt[x] = G.g_tot[x]; pend[x] = G.pending[x];
+    fx[x] = G.ff_x[x]; fy[x] = G.ff_y[x]; lx[x] = G.lat_x[x]; ly[x] = G.lat_y[x];
+    ps[x] = G.p_src[x]; ref[x] = G.ref_until[x];
+    frl[x] = G.ff_row_length[x]; lrl[x] = G.lat_row_length[x];
+  }
+  for (int x = threadIdx.x; x <= n; x += blockDim.x) {
+    fcp[x] = G.ff_col_ptr[x];
+    lcp[x] = G.lat_col_ptr[x];
+  }
+  const int64_t k0 = *G.step;
+  sw_topomap_step_t S = G;
+  S.V = V; S.g_tot = gt; S.pending = pend; S.ff_x = fx; S.ff_y = fy; S.lat_x = lx; S.lat_y = ly;
+  S.p_src = ps; S.ref_until = ref; S.ff_row_length = frl; S.lat_row_length = lrl;
+  S.ff_col_ptr = fcp; S.lat_col_ptr = lcp; S.src_bits = sb; S.tgt_bits = tb;
+  __syncthreads();
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int st = 0; st < n_steps; ++st) {
+    tm_neurons(S, k0 + st, w * 32, nw * 32);
+    __syncthreads();
+    tm_prop(S, t, nt);
+    if (spike_counts) tm_count(S, t, nt, spike_counts);
+    __syncthreads();
+    tm_pre(S, w, nw);
+    __syncthreads();
+    tm_post(S, t, nt);
+    __syncthreads();
+  }
+  for (int x = threadIdx.x; x < n; x += blockDim.x) {
+    G.V[x] = V[x]; G.g_tot[x] = gt[x]; G.pending[x] = pend[x];
+    G.ff_x[x] = fx[x]; G.ff_y[x] = fy[x]; G.lat_x[x] = lx[x]; G.lat_y[x] = ly[x];
+    G.ref_until[x] = ref[x];
+  }
+  for (int x = threadIdx.x; x < words; x += blockDim.x) {
+    G.src_bits[x] = sb[x];
+    G.tgt_bits[x] = tb[x];
+  }
+  if (threadIdx.x == 0) *G.step = k0 + n_steps;
 }
 
 int grid1(int64_t n) {
@@ -189,6 +323,51 @@ extern "C" int sw_topomap_synapses(const sw_topomap_step_t* s, int64_t* spike_co
   k_tm_post<<<grid1(n), 256, 0, st>>>(*s); sw::count_launch();
   k_tm_tick<<<1, 256, 0, st>>>(*s, spike_counts); sw::count_launch();
   SW_CHECK_LAUNCH("sw_topomap_synapses");
+  return SW_OK;
+}
+
+extern "C" int sw_topomap_run_steps(const sw_topomap_step_t* s, int32_t n_steps, int64_t* spike_counts,
+                                    uint32_t* barrier_words, void* stream) {
+  if (int e = check_step(s)) return e;
+  if (s->post_lo != 0 || s->post_hi != s->n) {
+    sw::set_last_error("sw_topomap_run_steps: unsharded sheets only (use neurons/synapses)");
+    return SW_ERR_INVALID_ARG;
+  }
+  if (!barrier_words) { sw::set_last_error("sw_topomap_run_steps: barrier words required"); return SW_ERR_INVALID_ARG; }
+  const int n = s->n;
+  if (n <= 0 || n_steps <= 0) return SW_OK;
+  static int max_ctas = 0;
+  if (max_ctas == 0) {
+    int per_sm = 0, sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tm_run, 512, 0);
+    max_ctas = per_sm * sms;
+    if (max_ctas < 1) max_ctas = 1;
+  }
+  // small sheets: one CTA with the per-node state staged in shared memory
+  const size_t sbytes = TmSmem::bytes(n);
+  if (n <= 2048 && sbytes <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute((const void*)k_tm_run_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+      attr = true;
+    }
+    k_tm_run_staged<<<1, 512, sbytes, (cudaStream_t)stream>>>(*s, n_steps, spike_counts);
+    sw::count_launch();
+    SW_CHECK_LAUNCH("sw_topomap_run_steps");
+    return SW_OK;
+  }
+  // one CTA per 2048 nodes, 512 threads, grid barriers
+  int ctas = (n + 2047) / 2048;
+  if (ctas > max_ctas) ctas = max_ctas;
+  sw_topomap_step_t S = *s;
+  int ns = n_steps;
+  void* args[] = {(void*)&S, (void*)&ns, (void*)&spike_counts, (void*)&barrier_words};
+  cudaLaunchCooperativeKernel((const void*)k_tm_run, dim3(ctas), dim3(512), args, 0, (cudaStream_t)stream);
+  sw::count_launch();
+  SW_CHECK_LAUNCH("sw_topomap_run_steps");
   return SW_OK;
 }
 

@@ -33,6 +33,10 @@ from .updates import Model, RuleDescriptor
 BASE_SIDE = 16
 
 
+# sheets up to this size step in one single-CTA persistent launch per period
+PERSISTENT_MAX_NODES = 2048
+
+
 @dataclass
 class RewiringParams:
     p_form: float
@@ -220,6 +224,7 @@ class TopomapModel:
         self._pending = torch.zeros(n, dtype=torch.float64, device="cuda")
         self._step = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.spike_counts = torch.zeros(2, dtype=torch.int64, device="cuda")
+        self._barrier = torch.zeros(2, dtype=torch.int32, device="cuda")
         self.step_index = 0
         self._graph = None
         self._update_log = None
@@ -290,9 +295,17 @@ class TopomapModel:
                   _lib.stream_ptr())
 
     def _period(self, rewire_steps: int) -> None:
-        """rewire_steps model steps + the rewiring group (device only)."""
-        for _ in range(rewire_steps):
-            self._launch_step()
+        """rewire_steps model steps + the rewiring group (device only).
+        Unsharded sheets of up to PERSISTENT_MAX_NODES: the steps run in one
+        single-CTA persistent launch (barriers between the phases of a step);
+        larger sheets: one launch per phase, which keeps every SM busy."""
+        if self.shard.world == 1 and self.geometry.n <= PERSISTENT_MAX_NODES:
+            s = self._step_struct()
+            _lib.call("sw_topomap_run_steps", ctypes.byref(s), rewire_steps,
+                      self.spike_counts.data_ptr(), self._barrier.data_ptr(), _lib.stream_ptr())
+        else:
+            for _ in range(rewire_steps):
+                self._launch_step()
         self.net.run_update_group("rewiring")
         self._log_update()
 
@@ -300,10 +313,9 @@ class TopomapModel:
         """(removed + formed) of both projections into the device update log."""
         if self._update_log is None:
             self._update_log = torch.zeros((1 << 16, 4), dtype=torch.int64, device="cuda")
-        idx = (self.ff_rule._update - 1).clamp(0, self._update_log.shape[0] - 1)
-        row = torch.stack([self.ff_rule._totals[0], self.ff_rule._totals[2],
-                           self.lat_rule._totals[0], self.lat_rule._totals[2]])
-        self._update_log.index_copy_(0, idx, row[None, :])
+        _lib.call("sw_topomap_log", self.ff_rule._update.data_ptr(), self.ff_rule._totals.data_ptr(),
+                  self.lat_rule._totals.data_ptr(), self._update_log.data_ptr(),
+                  self._update_log.shape[0], _lib.stream_ptr())
 
     def run(self, duration_ms: float, recorder=None, record: RunRecord | None = None) -> RunRecord:
         record = record or RunRecord()

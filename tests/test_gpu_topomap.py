@@ -240,3 +240,21 @@ def test_post_sharded_steps_equal_unsharded(dev_lib):
             else:
                 assert np.array_equal(st[key], sr[key]), key
         assert torch.equal(m.spike_counts, ref.spike_counts)
+
+
+@pytest.mark.parametrize("scale", [4, 8])
+def test_persistent_multi_cta_steps_equal_per_step_launches(dev_lib, scale, monkeypatch):
+    """sw_topomap_run_steps (one cooperative launch per rewiring period, grid
+    barriers between phases; several CTAs at these sizes) == one launch per
+    phase and step."""
+    from paper_2510_19764_b200 import topomap
+    from paper_2510_19764_b200.topomap import TopomapModel
+    monkeypatch.setattr(topomap, "PERSISTENT_MAX_NODES", 1 << 30)
+    a = TopomapModel(scale, seed=5, record_events=False, use_graph=True)
+    b = TopomapModel(scale, seed=5, record_events=False, use_graph=False)
+    ra, rb = a.run(20.0), b.run(20.0)
+    assert ra.rewires_per_update == rb.rewires_per_update
+    assert torch.equal(a.spike_counts, b.spike_counts) and int(a.spike_counts[0]) > 0
+    sa, sb = a.state_arrays(), b.state_arrays()
+    for key in sa:
+        assert np.array_equal(sa[key], sb[key]), key
