@@ -407,7 +407,7 @@ def run_device(args, w):
         _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 2, tr.psi.data_ptr(),
                   tr.lsig.data_ptr(), tr.local_b, tr.hidden, b32, r32, a32, tr.d.data_ptr(),
                   tr.zbar.data_ptr(), tr.g_w_out.data_ptr(), tr.g_b_out.data_ptr(),
-                  w["classes"], _lib.workspace(), st.cuda_stream)
+                  w["classes"], 0, _lib.workspace(), st.cuda_stream)
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -416,7 +416,7 @@ def run_device(args, w):
         _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 2, tr.psi.data_ptr(),
                   tr.lsig.data_ptr(), tr.local_b, tr.hidden, b32, r32, a32, tr.d.data_ptr(),
                   tr.zbar.data_ptr(), tr.g_w_out.data_ptr(), tr.g_b_out.data_ptr(),
-                  w["classes"], _lib.workspace(), st.cuda_stream)
+                  w["classes"], 0, _lib.workspace(), st.cuda_stream)
     e1.record(st)
     e1.synchronize()
     k_ms = e0.elapsed_time(e1) / reps

@@ -198,12 +198,15 @@ typedef struct sw_eprop_seg {
  * same synapses) plus, when d != NULL, the readout gradients
  * g_w_out[C,H] += d^T zbar and g_b_out[C] += sum_b d (classifier.py:221-222).
  * workspace: 2 uint32 zeroed once by the caller (tile tickets; the kernel
- * leaves them zeroed, so the launch can be captured in a CUDA graph). */
+ * leaves them zeroed, so the launch can be captured in a CUDA graph).
+ * max_blocks_per_sm: 0 = as many tile workers as fit; a smaller value leaves
+ * room on every SM for a concurrently running kernel (the next timestep's
+ * forward pass, see EpropClassifierTrainer). */
 SW_API int sw_eprop_fused_step(const sw_eprop_seg_t* segs, int32_t n_segs, const float* psi,
                                const float* lsig, int32_t batch, int32_t hidden, float beta,
                                float rho, float alpha, const double* d, const float* zbar,
                                double* g_w_out, double* g_b_out, int32_t num_classes,
-                               uint32_t* workspace, void* stream);
+                               int32_t max_blocks_per_sm, uint32_t* workspace, void* stream);
 
 /* ---- neurons (neurons.py) --------------------------------------------------- */
 /* AlifLayer.step (neurons.py:60-67), float32, n = batch*hidden elements. */
@@ -245,6 +248,10 @@ typedef struct sw_clf_step {
   double* y; double* pi_sum; double* loss; double* d;         /* [B,C] / [B]    */
   float* psi; float* lsig;                                    /* [B,H]          */
   float alpha; float rho; float beta; float v_thr; double alpha64;
+  /* previous-step traces (NULL = update xbar/zbar in place): with separate
+   * in/out trace buffers the next step's forward pass can run while the
+   * e-prop update still reads this step's traces */
+  const float* zbar_in; const float* xbar_in;
 } sw_clf_step_t;
 /* One fused forward timestep for all replicas (block per replica). */
 SW_API int sw_clf_step(const sw_clf_step_t* params, void* stream);

@@ -85,7 +85,8 @@ class ClfStep(C.Structure):
                 ("num_classes", I32), ("p_in", P), ("ex_key", P), ("labels", P), ("t", I32),
                 ("batch", I32), ("v", P), ("a", P), ("z", P), ("zbar", P), ("xbar", P),
                 ("y", P), ("pi_sum", P), ("loss", P), ("d", P), ("psi", P), ("lsig", P),
-                ("alpha", F32), ("rho", F32), ("beta", F32), ("v_thr", F32), ("alpha64", F64)]
+                ("alpha", F32), ("rho", F32), ("beta", F32), ("v_thr", F32), ("alpha64", F64),
+                ("zbar_in", P), ("xbar_in", P)]
 BP = C.POINTER(BitfieldDesc)
 
 # name -> argtypes (restype is int status for all but sw_last_error)
@@ -109,7 +110,7 @@ SIGNATURES: dict[str, list] = {
     "sw_eprop_plan": [P, P, I32, I32, I32, I32, P, P, P, P, I32, P, P],
     "sw_gather_f64": [P, P, I32, P, P],
     "sw_scatter_f64": [P, P, I32, P, P],
-    "sw_eprop_fused_step": [C.c_void_p, I32, P, P, I32, I32, F32, F32, F32, P, P, P, P, I32, P, P],
+    "sw_eprop_fused_step": [C.c_void_p, I32, P, P, I32, I32, F32, F32, F32, P, P, P, P, I32, I32, P, P],
     "sw_alif_step": [P, P, P, P, P, I64, F32, F32, F32, F32, P],
     "sw_alif_surrogate": [P, P, P, I64, F32, F32, P],
     "sw_lif_cond_step": [P, P, P, P, I32, I64, F64, F64, F64, F64, F64, F64, F64, F64, I64, P, P],

@@ -30,6 +30,12 @@ from .sharding import allreduce_flat
 from .updates import Model
 
 
+# tile-worker blocks per SM of the e-prop kernel when it shares the SMs with
+# the next step's forward pass (0 = all that fit: measured best, the forward
+# pass fills the slots that workers with fewer tiles release)
+OVERLAP_EPROP_BLOCKS_PER_SM = 0
+
+
 @dataclass
 class SyntheticTask:
     """classifier.py:28-79: class rate templates; per-example lognormal
@@ -159,6 +165,8 @@ class EpropClassifierTrainer:
         self.deep_r_enabled = deep_r
         self.params = AlifParams()
         self.use_graph = use_graph
+        # graph replays overlap step t's e-prop update with step t+1's forward pass
+        self.overlap = True
         self.pg = process_group
         # replicas handled by this rank (batch-DP); default: all of them
         self.local = local_batch if local_batch is not None else slice(0, batch_size)
@@ -221,10 +229,18 @@ class EpropClassifierTrainer:
         self.xbar = torch.zeros((B, NI), **f32)
         self.psi = torch.zeros((B, H), **f32)
         self.lsig = torch.zeros((B, H), **f32)
+        # timestep-parity twins of the per-step e-prop inputs: step t writes
+        # parity t % 2, so step t+1's forward pass can run while the e-prop
+        # update of step t still reads its traces, psi, lsig and d
+        self.zbar_1 = torch.zeros((B, H), **f32)
+        self.xbar_1 = torch.zeros((B, NI), **f32)
+        self.psi_1 = torch.zeros((B, H), **f32)
+        self.lsig_1 = torch.zeros((B, H), **f32)
         self.y = torch.zeros((B, C), **f64)
         self.pi_sum = torch.zeros((B, C), **f64)
         self.loss_b = torch.zeros(B, **f64)
         self.d = torch.zeros((B, C), **f64)
+        self.d_1 = torch.zeros((B, C), **f64)
         self.p_in = torch.zeros((B, NI), **f64)
         self.keys = torch.zeros(B, dtype=torch.int64, device="cuda")
         self.labels = torch.zeros(B, dtype=torch.int32, device="cuda")
@@ -237,7 +253,7 @@ class EpropClassifierTrainer:
         self.pin_labels = torch.zeros(B, dtype=torch.int32, pin_memory=True)
         self.plan_in = _Plan(self.m_in, B)
         self.plan_rec = _Plan(self.m_rec, B)
-        self._segs = (_lib.EpropSeg * 2)()
+        self._segs = [(_lib.EpropSeg * 2)(), (_lib.EpropSeg * 2)()]
         _lib.workspace()   # allocate the ticket words outside any graph capture
 
     # -- per-step launches ------------------------------------------------------------
@@ -252,30 +268,67 @@ class EpropClassifierTrainer:
         s.w_out, s.b_out, s.num_classes = self.w_out.data_ptr(), self.b_out.data_ptr(), self.task.num_classes
         s.p_in, s.ex_key, s.labels = self.p_in.data_ptr(), self.keys.data_ptr(), self.labels.data_ptr()
         s.t, s.batch = t, self.local_b
-        s.v, s.a, s.z, s.zbar, s.xbar = (x.data_ptr() for x in (self.v, self.a, self.z, self.zbar, self.xbar))
-        s.y, s.pi_sum, s.loss, s.d = (x.data_ptr() for x in (self.y, self.pi_sum, self.loss_b, self.d))
-        s.psi, s.lsig = self.psi.data_ptr(), self.lsig.data_ptr()
+        cur, prev = self._parity(t), self._parity(t + 1)
+        s.v, s.a, s.z = (x.data_ptr() for x in (self.v, self.a, self.z))
+        s.zbar, s.xbar = cur["zbar"].data_ptr(), cur["xbar"].data_ptr()
+        s.zbar_in, s.xbar_in = prev["zbar"].data_ptr(), prev["xbar"].data_ptr()
+        s.y, s.pi_sum, s.loss = (x.data_ptr() for x in (self.y, self.pi_sum, self.loss_b))
+        s.d, s.psi, s.lsig = cur["d"].data_ptr(), cur["psi"].data_ptr(), cur["lsig"].data_ptr()
         s.alpha, s.rho = float(np.float32(p.alpha)), float(np.float32(p.rho))
         s.beta, s.v_thr = float(np.float32(p.beta)), float(np.float32(p.v_thr))
         s.alpha64 = p.alpha
         return s
 
-    def _launch_steps(self, learn: bool) -> None:
-        st = _lib.stream_ptr()
+    def _parity(self, t: int) -> dict:
+        if t % 2 == 0:
+            return dict(zbar=self.zbar, xbar=self.xbar, psi=self.psi, lsig=self.lsig, d=self.d)
+        return dict(zbar=self.zbar_1, xbar=self.xbar_1, psi=self.psi_1, lsig=self.lsig_1, d=self.d_1)
+
+    def _eprop(self, t: int, st: int, blocks_per_sm: int) -> None:
         p = self.params
         a32, r32, b32 = float(np.float32(p.alpha)), float(np.float32(p.rho)), float(np.float32(p.beta))
-        self._segs[0] = self.plan_in.seg(self.xbar)
-        self._segs[1] = self.plan_rec.seg(self.zbar)
-        for t in range(self.task.example_steps):
+        cur = self._parity(t)
+        segs = self._segs[t % 2]
+        segs[0] = self.plan_in.seg(cur["xbar"])
+        segs[1] = self.plan_rec.seg(cur["zbar"])
+        _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 2,
+                  cur["psi"].data_ptr(), cur["lsig"].data_ptr(), self.local_b, self.hidden,
+                  b32, r32, a32, cur["d"].data_ptr(), cur["zbar"].data_ptr(),
+                  self.g_w_out.data_ptr(), self.g_b_out.data_ptr(),
+                  self.task.num_classes, blocks_per_sm, _lib.workspace(), st)
+
+    def _launch_steps(self, learn: bool, overlap: bool = False) -> None:
+        """One trial.  overlap (graph capture only): forward passes on the
+        capturing stream, e-prop updates on a side stream; step t+1's forward
+        pass runs concurrently with step t's e-prop update (the e-prop kernel
+        leaves one block slot per SM free for it), and step t+2's forward pass
+        waits for step t's update (parity buffers)."""
+        T = self.task.example_steps
+        if not (learn and overlap):
+            st = _lib.stream_ptr()
+            for t in range(T):
+                prm = self._step_params(t)
+                _lib.call("sw_clf_step", ctypes.byref(prm), st)
+                if learn:
+                    self._eprop(t, st, 0)
+            self.steps_launched += T
+            return
+        main = torch.cuda.current_stream()
+        side = self._side_stream
+        side.wait_stream(main)
+        fwd_done = [torch.cuda.Event() for _ in range(T)]
+        upd_done = [torch.cuda.Event() for _ in range(T)]
+        for t in range(T):
+            if t >= 2:
+                main.wait_event(upd_done[t - 2])
             prm = self._step_params(t)
-            _lib.call("sw_clf_step", ctypes.byref(prm), st)
-            if learn:
-                _lib.call("sw_eprop_fused_step", ctypes.cast(self._segs, ctypes.c_void_p), 2,
-                          self.psi.data_ptr(), self.lsig.data_ptr(), self.local_b, self.hidden,
-                          b32, r32, a32, self.d.data_ptr(), self.zbar.data_ptr(),
-                          self.g_w_out.data_ptr(), self.g_b_out.data_ptr(),
-                          self.task.num_classes, _lib.workspace(), st)
-        self.steps_launched += self.task.example_steps
+            _lib.call("sw_clf_step", ctypes.byref(prm), main.cuda_stream)
+            fwd_done[t].record(main)
+            side.wait_event(fwd_done[t])
+            self._eprop(t, side.cuda_stream, OVERLAP_EPROP_BLOCKS_PER_SM)
+            upd_done[t].record(side)
+        main.wait_stream(side)
+        self.steps_launched += T
 
     def _run_trial(self, learn: bool) -> None:
         if not self.use_graph:
@@ -286,9 +339,10 @@ class EpropClassifierTrainer:
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
+            self._side_stream = torch.cuda.Stream()
             with torch.cuda.stream(s):
                 with torch.cuda.graph(g, stream=s):
-                    self._launch_steps(learn)
+                    self._launch_steps(learn, overlap=self.overlap)
             torch.cuda.current_stream().wait_stream(s)
             self._graph, self._graph_learn, self._graph_key = g, learn, self._buffers_key()
             self.steps_launched -= self.task.example_steps   # capture is not execution
@@ -326,7 +380,8 @@ class EpropClassifierTrainer:
                   self.w32_in.numel(), st)
         _lib.call("sw_f64_to_f32", self.s_rec.planes["w"].data_ptr(), self.w32_rec.data_ptr(),
                   self.w32_rec.numel(), st)
-        for x in (self.v, self.a, self.z, self.zbar, self.xbar, self.y, self.pi_sum, self.loss_b):
+        for x in (self.v, self.a, self.z, self.zbar, self.xbar, self.zbar_1, self.xbar_1, self.y,
+                  self.pi_sum, self.loss_b):
             x.zero_()
         if learn:
             for plan, syn in ((self.plan_in, self.s_in), (self.plan_rec, self.s_rec)):

@@ -84,6 +84,12 @@ __global__ void __launch_bounds__(kThreads) k_clf_step(sw_clf_step_t P) {
   const int64_t bH = (int64_t)b * H, bI = (int64_t)b * NI, bC = (int64_t)b * C;
 
   PROF(0);
+  // ALIF state of this thread's first hidden unit, needed only in P6: loaded
+  // now so that its latency overlaps the phases before
+  const bool h0_ok = threadIdx.x < H;
+  const float v0 = h0_ok ? P.v[bH + threadIdx.x] : 0.f;
+  const float a0 = h0_ok ? P.a[bH + threadIdx.x] : 0.f;
+  const float z0 = h0_ok ? P.z[bH + threadIdx.x] : 0.f;
   // P0: row lengths to shared memory; zero the current accumulators
   for (int x = threadIdx.x; x < NT; x += kThreads)
     rlen[x] = (x < NI) ? __ldg(P.in_row_length + x) : __ldg(P.rec_row_length + (x - NI));
@@ -109,10 +115,10 @@ __global__ void __launch_bounds__(kThreads) k_clf_step(sw_clf_step_t P) {
     if (j < per && x < NT) {
       if (x < NI) {
         pv[j] = P.p_in[bI + x];
-        tr[j] = P.xbar[bI + x];
+        tr[j] = (P.xbar_in ? P.xbar_in : P.xbar)[bI + x];
       } else {
         zv[j] = P.z[bH + x - NI];
-        tr[j] = P.zbar[bH + x - NI];
+        tr[j] = (P.zbar_in ? P.zbar_in : P.zbar)[bH + x - NI];
       }
     }
   }
@@ -347,13 +353,25 @@ __global__ void __launch_bounds__(kThreads) k_clf_step(sw_clf_step_t P) {
   PROF(9);
   // P6: surrogate (pre-step state), learning signal, ALIF step
   for (int h = threadIdx.x; h < H; h += kThreads) {
-    const float vo = P.v[bH + h], ao = P.a[bH + h], zo = P.z[bH + h];
+    const bool first = h == (int)threadIdx.x;
+    const float vo = first ? v0 : P.v[bH + h];
+    const float ao = first ? a0 : P.a[bH + h];
+    const float zo = first ? z0 : P.z[bH + h];
     const float thr_o = __fadd_rn(P.v_thr, __fmul_rn(P.beta, ao));
     const float cc = __fdiv_rn(__fsub_rn(vo, thr_o), P.v_thr);
     const float r = __fsub_rn(1.0f, fabsf(cc));
     P.psi[bH + h] = __fmul_rn(0.5f, (r > 0.0f || r != r) ? r : 0.0f);
+    // lsig = f32(d @ W_out) (classifier.py:223), classes ascending; the
+    // W_out column is loaded 8 classes at a time ahead of the chained sum
     double ls = 0.0;
-    for (int c = 0; c < C; ++c) ls = __dadd_rn(ls, __dmul_rn(dv[c], __ldg(P.w_out + (int64_t)c * H + h)));
+    for (int c0 = 0; c0 < C; c0 += 8) {
+      double wv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) wv[u] = (c0 + u < C) ? __ldg(P.w_out + (int64_t)(c0 + u) * H + h) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (c0 + u < C) ls = __dadd_rn(ls, __dmul_rn(dv[c0 + u], wv[u]));
+    }
     P.lsig[bH + h] = __double2float_rn(ls);
     float vv = __fmul_rn(P.alpha, __fsub_rn(vo, __fmul_rn(zo, P.v_thr)));
     vv = __fadd_rn(__fadd_rn(vv, acc_rec[h]), acc_ext[h]);

@@ -269,7 +269,7 @@ extern "C" int sw_eprop_fused_step(const sw_eprop_seg_t* segs, int32_t n_segs, c
                                    const float* lsig, int32_t batch, int32_t hidden, float beta,
                                    float rho, float alpha, const double* d, const float* zbar,
                                    double* g_w_out, double* g_b_out, int32_t num_classes,
-                                   uint32_t* workspace, void* stream) {
+                                   int32_t max_blocks_per_sm, uint32_t* workspace, void* stream) {
   if (!workspace) { sw::set_last_error("eprop: workspace (2 zeroed uint32) required"); return SW_ERR_INVALID_ARG; }
   if (n_segs < 1 || n_segs > 2) { sw::set_last_error("eprop: 1 or 2 segments"); return SW_ERR_INVALID_ARG; }
   Seg s[2] = {};
@@ -289,7 +289,8 @@ extern "C" int sw_eprop_fused_step(const sw_eprop_seg_t* segs, int32_t n_segs, c
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eprop_fused, kThreads, smem);
     if (per_sm < 1) per_sm = 1;
   }
-  const int workers = tiles ? min(tiles, 148 * per_sm) : 0;
+  const int bps = (max_blocks_per_sm > 0 && max_blocks_per_sm < per_sm) ? max_blocks_per_sm : per_sm;
+  const int workers = tiles ? min(tiles, 148 * bps) : 0;
   k_eprop_fused<<<ro_blocks + workers, kThreads, smem, (cudaStream_t)stream>>>(
       s[0], s[1], psi, lsig, batch, hidden, beta, rho, alpha, ro, ro_blocks, workspace);
   sw::count_launch();

@@ -82,7 +82,7 @@ def test_fused_eprop_equals_reference_layout(dev_lib, B, P, H, cap, R):
         segs[0] = plan.seg(trace)
         _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 1, psi.data_ptr(),
                   lsig.data_ptr(), B, H, float(np.float32(0.0174)), float(np.float32(0.9995)),
-                  float(np.float32(0.95)), None, None, None, None, 0, _lib.workspace(),
+                  float(np.float32(0.95)), None, None, None, None, 0, 0, _lib.workspace(),
                   _lib.stream_ptr())
     _lib.call("sw_scatter_f64", gplane.data_ptr(), plan.off.data_ptr(), plan.e_pad,
               plan.grad.data_ptr(), _lib.stream_ptr())
@@ -167,3 +167,20 @@ def test_trainer_matches_reference_run_and_rewires_exactly(dev_lib):
             mask = np.arange(rl.size and m.stride)[None, :] < rl[:, None]
             assert np.allclose(s.planes["w"].cpu().numpy()[mask], g[f"{name}_w"][mask],
                                rtol=1e-6, atol=1e-9)
+
+
+def test_overlapped_graph_equals_sequential_steps(dev_lib):
+    """The graph replay overlaps step t's e-prop update with step t+1's
+    forward pass (two streams, parity buffers); gradients, weights and
+    rewiring must be bit-identical to strictly sequential launches."""
+    a = _small_trainer(use_graph=True)
+    b = _small_trainer(use_graph=False)
+    assert a.overlap
+    for k in range(3):
+        ha, hb = a.train_batch(k), b.train_batch(k)
+        assert ha["loss"] == hb["loss"] and ha["removed"] == hb["removed"]
+    for x, y in ((a.s_in, b.s_in), (a.s_rec, b.s_rec)):
+        for p in ("w", "grad", "adam_m", "adam_v"):
+            assert torch.equal(x.planes[p], y.planes[p]), p
+    assert torch.equal(a.w_out, b.w_out) and torch.equal(a.g_w_out, b.g_w_out)
+    assert a.connectivity_fingerprint() == b.connectivity_fingerprint()

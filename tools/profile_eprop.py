@@ -28,6 +28,6 @@ for _ in range(int(os.environ.get("REPS", "3"))):
     _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 2, tr.psi.data_ptr(),
               tr.lsig.data_ptr(), tr.local_b, tr.hidden, b32, r32, a32, tr.d.data_ptr(),
               tr.zbar.data_ptr(), tr.g_w_out.data_ptr(), tr.g_b_out.data_ptr(), 20,
-              _lib.workspace(), _lib.stream_ptr())
+              0, _lib.workspace(), _lib.stream_ptr())
 torch.cuda.synchronize()
 print("done", tr.m_in.edge_count(), tr.m_rec.edge_count())

@@ -41,11 +41,11 @@ segs = tr._segs
 ep = lambda: _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 2,
                        tr.psi.data_ptr(), tr.lsig.data_ptr(), tr.local_b, tr.hidden, b32, r32,
                        a32, tr.d.data_ptr(), tr.zbar.data_ptr(), tr.g_w_out.data_ptr(),
-                       tr.g_b_out.data_ptr(), 20, _lib.workspace(), st)
+                       tr.g_b_out.data_ptr(), 20, 0, _lib.workspace(), st)
 print("eprop us", 1000 * timeit(ep, 200))
 ep_nro = lambda: _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 2,
                            tr.psi.data_ptr(), tr.lsig.data_ptr(), tr.local_b, tr.hidden, b32, r32,
-                           a32, None, None, None, None, 0, _lib.workspace(), st)
+                           a32, None, None, None, None, 0, 0, _lib.workspace(), st)
 print("eprop (no readout) us", 1000 * timeit(ep_nro, 200))
 print("gradient_phase ms", timeit(lambda: tr.gradient_phase(3)))
 print("rewire ms", timeit(lambda: tr.rewire_phase()))
