@@ -15,8 +15,9 @@ N > 1 (torchrun): the 512 replicas are sharded across ranks (batch-DP,
 strong scaling) with one NCCL all-reduce of the raw gradients per batch.
 
 --impl reference times the reference CPU path (the oracle port in
-``oracle/``, single-threaded) on a bounded sample of the same workload and
-extrapolates to s/epoch; rank 0 only.
+``oracle/``: numpy with its default BLAS threads, the e-prop kernel in C with
+OpenMP over rows) on a bounded sample of the same workload and extrapolates
+to s/epoch; rank 0 only.
 """
 
 from __future__ import annotations
@@ -127,9 +128,7 @@ def cpu_reference_sample(w, sample_steps=None):
     """Time the oracle port of the classifier step on the host CPU over a
     bounded number of timesteps of one batch (+ one DEEP R group) and
     extrapolate to s/epoch.  Single-threaded."""
-    from threadpoolctl import threadpool_limits
-    with threadpool_limits(1):
-        return _cpu_reference_sample(w, sample_steps)
+    return _cpu_reference_sample(w, sample_steps)
 
 
 def _cpu_reference_sample(w, sample_steps):
@@ -155,7 +154,9 @@ def _cpu_reference_sample(w, sample_steps):
     tr.rewire_phase()
     upd = time.perf_counter() - t0
     batch_s = per_step * w["steps"] + upd
+    from oracle.cbuild import threads
     return {"s_per_epoch": batch_s * EPOCH_BATCHES, "batch_s": batch_s, "per_step_s": per_step,
+            "cores": threads(),
             "update_s": upd, "build_s": build_s, "sample_steps": task.example_steps}
 
 
@@ -171,14 +172,14 @@ def run_reference(args, w):
     sample = (f"{r['sample_steps']} of {w['steps']} timesteps of one {w['batch']}-replica batch "
               f"(median step after the first) + one full update/DEEP R group, extrapolated "
               f"x{w['steps']} steps x{EPOCH_BATCHES} batches; oracle port: numpy + C e-prop "
-              f"(oracle/c/oracle.c), 1 thread")
+              f"(oracle/c/oracle.c, OpenMP over rows), numpy/BLAS default threads")
     line = {"impl": "reference", "metric": "e-prop+DEEP R training time per epoch",
             "value": round(v, 3), "unit": "s/epoch", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
             "config": {"workload": f"{args.workload}: e-prop ALIF classifier {w['num_inputs']}->{w['hidden']}, "
                                    f"{int(w['density'] * 100)}% + DEEP R, batch {w['batch']}, SHD-shaped synthetic"},
-            "cpu_baseline": {"value": round(v, 3), "unit": "s/epoch", "cores": 1, "kind": "port",
+            "cpu_baseline": {"value": round(v, 3), "unit": "s/epoch", "cores": r["cores"], "kind": "port",
                              "sample": sample},
             "e2e": {"value": round(v, 3), "unit": "s/epoch", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -438,9 +439,9 @@ def run_device(args, w):
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         r = cpu_reference_sample(w, sample_steps=args.ref_sample_steps)
-        cpu = {"value": round(r["s_per_epoch"], 3), "unit": "s/epoch", "cores": 1, "kind": "port",
+        cpu = {"value": round(r["s_per_epoch"], 3), "unit": "s/epoch", "cores": r["cores"], "kind": "port",
                "sample": f"{r['sample_steps']} timesteps of one {w['batch']}-replica batch + one "
-                         f"update/DEEP R group (oracle port, 1 thread), extrapolated to "
+                         f"update/DEEP R group (oracle port: C e-prop with OpenMP over rows, numpy), extrapolated to "
                          f"{w['steps']} steps x {EPOCH_BATCHES} batches"}
     h2d = sum(x.nbytes for x in host[0]) // ws
     if rank == 0:

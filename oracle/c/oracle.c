@@ -2,18 +2,25 @@
  * for the CPU baseline and large oracle checks.  TEST INFRASTRUCTURE ONLY.
  * Compiled with -O2 -ffp-contract=off: every float32 op is separately
  * rounded, grad accumulates float64(float32 product) in (b, i, s) order,
- * exactly the numba loop. */
+ * exactly the numba loop (per synapse; rows run in parallel). */
 #include <stdint.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
+/* Rows are independent (each synapse's grad is accumulated by exactly one
+ * thread, replicas in ascending order), so the OpenMP split over rows keeps
+ * every result bit-identical to the serial loop. */
 void oracle_eprop_accumulate_batch(const int32_t* targets, const int32_t* row_length,
                                    int64_t P, int64_t S, const float* restrict pre_trace,
                                    const float* psi, const float* lsig, int64_t B, int64_t H,
                                    float* restrict eps, float* restrict ebar, double* restrict grad, float beta,
                                    float rho, float alpha) {
-  for (int64_t b = 0; b < B; ++b) {
-    for (int64_t i = 0; i < P; ++i) {
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t i = 0; i < P; ++i) {
+    const int32_t n = row_length[i];
+    for (int64_t b = 0; b < B; ++b) {
       const float zb = pre_trace[b * P + i];
-      const int32_t n = row_length[i];
       for (int64_t s = 0; s < n; ++s) {
         const int64_t q = (b * P + i) * S + s;
         const int32_t j = targets[i * S + s];
@@ -26,4 +33,12 @@ void oracle_eprop_accumulate_batch(const int32_t* targets, const int32_t* row_le
       }
     }
   }
+}
+
+int oracle_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
 }

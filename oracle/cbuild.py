@@ -17,7 +17,8 @@ def build() -> str:
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     if os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(s) for s in srcs):
         return OUT
-    cmd = ["gcc", "-O3", "-mavx2", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC", "-o", OUT] + srcs
+    cmd = ["gcc", "-O3", "-mavx2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC",
+           "-o", OUT] + srcs
     subprocess.run(cmd, check=True)
     return OUT
 
@@ -33,6 +34,8 @@ def lib():
         L.oracle_eprop_accumulate_batch.argtypes = [P, P, I64, I64, P, P, P, I64, I64, P, P, P,
                                                     F32, F32, F32]
         L.oracle_eprop_accumulate_batch.restype = None
+        L.oracle_threads.argtypes = []
+        L.oracle_threads.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -50,3 +53,8 @@ def eprop_accumulate_c(targets, row_length, pre_trace, psi, lsig, eps, ebar, gra
                                         pre_trace.ctypes.data, psi.ctypes.data, lsig.ctypes.data,
                                         B, H, eps.ctypes.data, ebar.ctypes.data, grad.ctypes.data,
                                         float(beta), float(rho), float(alpha))
+
+
+def threads() -> int:
+    """OpenMP threads the C oracle uses (the CPU baseline's core count)."""
+    return int(lib().oracle_threads())

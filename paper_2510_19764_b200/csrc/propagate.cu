@@ -245,47 +245,24 @@ int grid1(int64_t n) {
 // ---- cluster / multicast variant of the atomic mode --------------------------------
 // The slab kernel above is bound by L2->SM bandwidth: four CTAs read every
 // row.  Here the four slab CTAs form a thread-block cluster and each row
-// chunk crosses L2 once: a producer thread in CTA rank 0 multicasts 128-slot
-// chunks (targets + weights, cp.async.bulk ... multicast::cluster) into the
-// same stage of all four CTAs; every CTA's consumer warps add the chunk's
-// contributions that fall in its slab with shared-memory atomics and release
-// the stage to rank 0 with a remote mbarrier arrive.  16 consumer teams per
-// cluster, 3 stages each; the producer polls the teams round-robin with
-// non-blocking barrier probes.
-constexpr int kCW = 16;                 // consumer warps (teams) per CTA
+// chunk crosses L2 once.  16 "teams" per cluster: team t has one producer
+// warp in CTA rank 0, which multicasts the team's 128-slot row chunks
+// (targets + weights, two cp.async.bulk ... multicast::cluster copies) into
+// stage u % 3 of all four CTAs, and one consumer warp in every CTA, which
+// compacts the chunk's contributions to its own post slab through a
+// per-warp shared-memory list (so every lane issues one shared-memory
+// atomic) and then releases the stage with a remote mbarrier arrive on rank
+// 0.  Both sides walk the same row sequence with the row ids and lengths of
+// the next 8 rows prefetched in registers (lane k holds row k of a batch).
+// At the end every CTA adds its slab into `out` (one RED per nonzero post).
+constexpr int kCW = 16;                 // teams (consumer warps = producer warps) per CTA
 constexpr int kCS = 3;                  // stages per team
 constexpr int kCC = 128;                // slots per chunk
 constexpr int kCTB = kCC * 4 + 16;
 constexpr int kCWB = kCC * 8 + 16;
 constexpr int kCStage = kCTB + kCWB;
-constexpr int kPropClusterSmem = kSlab * 8 + kCW * kCS * kCStage + 2 * kCW * kCS * 8;
-
-struct ChunkIt {
-  int q;       // index into the spike list
-  int n;       // row length of spikes[q]
-  int c0;      // first slot of the chunk
-  int i;       // row
-};
-
-__device__ __forceinline__ void chunk_first(ChunkIt& it, int qstep, const int32_t* spikes, int S,
-                                            const int32_t* row_length) {
-  it.c0 = 0;
-  it.n = 0;
-  while (it.q < S) {
-    it.i = __ldg(spikes + it.q);
-    it.n = __ldg(row_length + it.i);
-    if (it.n > 0) return;
-    it.q += qstep;
-  }
-}
-
-__device__ __forceinline__ void chunk_next(ChunkIt& it, int qstep, const int32_t* spikes, int S,
-                                           const int32_t* row_length) {
-  it.c0 += kCC;
-  if (it.c0 < it.n) return;
-  it.q += qstep;
-  chunk_first(it, qstep, spikes, S, row_length);
-}
+constexpr int kCListB = kCC * 12;       // per consumer warp: compacted (post, weight) list
+constexpr int kPropClusterSmem = kSlab * 8 + kCW * kCS * kCStage + kCW * kCListB + 2 * kCW * kCS * 8;
 
 __device__ __forceinline__ bool window16(uint64_t start, uint64_t len, uint64_t limit, uint64_t& a,
                                          uint32_t& bytes) {
@@ -295,14 +272,47 @@ __device__ __forceinline__ bool window16(uint64_t start, uint64_t len, uint64_t 
   return e <= limit;
 }
 
-__global__ void __cluster_dims__(kSlabs, 1, 1) __launch_bounds__((kCW + 1) * 32, 1)
+// Row sequence of a team: spike-list entries team, team + teams, ... in
+// batches of 8 (lane k < 8 holds entry k of a batch); ids prefetched two
+// batches ahead, lengths one batch ahead.
+struct RowStream {
+  int team, teams, S;
+  int k;          // current batch
+  int id0, id1, id2;   // row ids of batches k, k+1, k+2 (lane-held)
+  int n0, n1;          // row lengths of batches k, k+1
+  __device__ int q(int kb, int lane) const { return team + (kb * 8 + lane) * teams; }
+  __device__ int load_id(const int32_t* spikes, int kb, int lane) const {
+    const int qq = q(kb, lane);
+    return (lane < 8 && qq < S) ? __ldg(spikes + qq) : -1;
+  }
+  __device__ void init(const int32_t* spikes, const int32_t* rl, int lane) {
+    k = 0;
+    id0 = load_id(spikes, 0, lane);
+    id1 = load_id(spikes, 1, lane);
+    n0 = id0 >= 0 ? __ldg(rl + id0) : 0;
+    id2 = load_id(spikes, 2, lane);
+    n1 = id1 >= 0 ? __ldg(rl + id1) : 0;
+  }
+  __device__ bool live() const { return q(k, 0) < S; }
+  __device__ void advance(const int32_t* spikes, const int32_t* rl, int lane) {
+    ++k;
+    id0 = id1;
+    n0 = n1;
+    id1 = id2;
+    n1 = id1 >= 0 ? __ldg(rl + id1) : 0;
+    id2 = load_id(spikes, k + 2, lane);
+  }
+};
+
+__global__ void __cluster_dims__(kSlabs, 1, 1) __launch_bounds__(2 * kCW * 32, 1)
 k_prop_cluster(const int32_t* __restrict__ row_length, const int32_t* __restrict__ target,
                const double* __restrict__ w, int stride, int64_t num_pre,
                const int32_t* __restrict__ spikes, const int32_t* n_spikes, double* out, int N) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   double* acc = reinterpret_cast<double*>(s_raw);
   unsigned char* stages = s_raw + kSlab * 8;
-  uint64_t* full = reinterpret_cast<uint64_t*>(stages + kCW * kCS * kCStage);
+  unsigned char* lists = stages + kCW * kCS * kCStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(lists + kCW * kCListB);
   uint64_t* empty = full + kCW * kCS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = sw::cluster_ctarank();
@@ -319,89 +329,103 @@ k_prop_cluster(const int32_t* __restrict__ row_length, const int32_t* __restrict
 
   const int S = *n_spikes;
   const int teams = (int)(gridDim.x / kSlabs) * kCW;
-  const int team0 = (int)(blockIdx.x / kSlabs) * kCW;
   const uint64_t t_limit = (uint64_t)num_pre * stride * 4;
   const uint64_t w_limit = (uint64_t)num_pre * stride * 8;
+  const bool producer = warp >= kCW;
+  const int t = producer ? warp - kCW : warp;
+  RowStream rs{(int)(blockIdx.x / kSlabs) * kCW + t, teams, S, 0, 0, 0, 0, 0, 0};
 
-  if (warp == kCW) {
-    if (rank == 0 && lane == 0) {
-      // producer: round-robin over the cluster's teams, never blocking
-      ChunkIt it[kCW];
-      int u[kCW];
-      uint32_t eph[kCW];
-      int live = 0;
-      for (int t = 0; t < kCW; ++t) {
-        it[t] = ChunkIt{team0 + t, 0, 0, 0};
-        chunk_first(it[t], teams, spikes, S, row_length);
-        u[t] = 0;
-        eph[t] = 0u;
-        live += it[t].q < S;
-      }
-      while (live > 0) {
-        for (int t = 0; t < kCW; ++t) {
-          if (it[t].q >= S) continue;
-          const int s = u[t] % kCS;
-          uint64_t* eb = &empty[t * kCS + s];
-          if (u[t] >= kCS) {
-            if (!sw::mbar_test_cluster(eb, (eph[t] >> s) & 1u)) continue;
-            eph[t] ^= 1u << s;
+  if (producer) {
+    if (rank == 0) {
+      rs.init(spikes, row_length, lane);
+      uint32_t eph = 0u;
+      int u = 0;
+      while (rs.live()) {
+        for (int r = 0; r < 8; ++r) {
+          const int i = __shfl_sync(SW_FULL_MASK, rs.id0, r);
+          const int n = __shfl_sync(SW_FULL_MASK, rs.n0, r);
+          if (i < 0) break;
+          for (int c0 = 0; c0 < n; c0 += kCC, ++u) {
+            if (lane == 0) {
+              const int s = u % kCS;
+              if (u >= kCS) {
+                sw::mbar_wait_cluster(&empty[t * kCS + s], (eph >> s) & 1u);
+                eph ^= 1u << s;
+              }
+              const int len = min(kCC, n - c0);
+              const uint64_t e0 = (uint64_t)i * stride + c0;
+              uint64_t ta, wa;
+              uint32_t tb, wb;
+              if (window16(e0 * 4, (uint64_t)len * 4, t_limit, ta, tb) &&
+                  window16(e0 * 8, (uint64_t)len * 8, w_limit, wa, wb)) {
+                unsigned char* buf = stages + (t * kCS + s) * kCStage;
+                uint64_t* fb = &full[t * kCS + s];
+                sw::bulk_g2s_multicast(buf, (const unsigned char*)target + ta, tb, fb, (1u << kSlabs) - 1);
+                sw::bulk_g2s_multicast(buf + kCTB, (const unsigned char*)w + wa, wb, fb, (1u << kSlabs) - 1);
+              }
+            }
+            __syncwarp();
           }
-          const int len = min(kCC, it[t].n - it[t].c0);
-          const uint64_t e0 = (uint64_t)it[t].i * stride + it[t].c0;
-          uint64_t ta, wa;
-          uint32_t tb, wb;
-          if (window16(e0 * 4, (uint64_t)len * 4, t_limit, ta, tb) &&
-              window16(e0 * 8, (uint64_t)len * 8, w_limit, wa, wb)) {
-            unsigned char* buf = stages + (t * kCS + s) * kCStage;
-            uint64_t* fb = &full[t * kCS + s];
-            sw::bulk_g2s_multicast(buf, (const unsigned char*)target + ta, tb, fb, (1u << kSlabs) - 1);
-            sw::bulk_g2s_multicast(buf + kCTB, (const unsigned char*)w + wa, wb, fb, (1u << kSlabs) - 1);
-          }
-          ++u[t];
-          chunk_next(it[t], teams, spikes, S, row_length);
-          if (it[t].q >= S) --live;
         }
+        rs.advance(spikes, row_length, lane);
       }
     }
   } else {
-    ChunkIt it{team0 + warp, 0, 0, 0};
-    chunk_first(it, teams, spikes, S, row_length);
+    rs.init(spikes, row_length, lane);
+    int* lpost = reinterpret_cast<int*>(lists + t * kCListB);
+    double* lw = reinterpret_cast<double*>(lists + t * kCListB + kCC * 4);
+    const unsigned lt = sw::lanemask_lt();
     uint32_t fph = 0u;
     int u = 0;
-    while (it.q < S) {
-      const int s = u % kCS;
-      const int len = min(kCC, it.n - it.c0);
-      const uint64_t e0 = (uint64_t)it.i * stride + it.c0;
-      uint64_t ta, wa;
-      uint32_t tb, wb;
-      const bool tma = window16(e0 * 4, (uint64_t)len * 4, t_limit, ta, tb) &&
-                       window16(e0 * 8, (uint64_t)len * 8, w_limit, wa, wb);
-      if (tma) {
-        uint64_t* fb = &full[warp * kCS + s];
-        if (lane == 0) sw::mbar_arrive_expect_tx(fb, tb + wb);
-        sw::mbar_wait(fb, (fph >> s) & 1u);
-        fph ^= 1u << s;
-        const unsigned char* buf = stages + (warp * kCS + s) * kCStage;
-        const int32_t* tp = reinterpret_cast<const int32_t*>(buf) + ((e0 * 4 - ta) >> 2);
-        const double* wp = reinterpret_cast<const double*>(buf + kCTB) + ((e0 * 8 - wa) >> 3);
-#pragma unroll
-        for (int k = 0; k < kCC / 32; ++k) {
-          const int sl = lane + 32 * k;
-          if (sl < len) {
-            const int rel = tp[sl] - slab0;
-            if ((unsigned)rel < (unsigned)kSlab) atomicAdd(acc + rel, wp[sl]);
+    while (rs.live()) {
+      for (int r = 0; r < 8; ++r) {
+        const int i = __shfl_sync(SW_FULL_MASK, rs.id0, r);
+        const int n = __shfl_sync(SW_FULL_MASK, rs.n0, r);
+        if (i < 0) break;
+        for (int c0 = 0; c0 < n; c0 += kCC, ++u) {
+          const int s = u % kCS;
+          const int len = min(kCC, n - c0);
+          const uint64_t e0 = (uint64_t)i * stride + c0;
+          uint64_t ta, wa;
+          uint32_t tb, wb;
+          const bool tma = window16(e0 * 4, (uint64_t)len * 4, t_limit, ta, tb) &&
+                           window16(e0 * 8, (uint64_t)len * 8, w_limit, wa, wb);
+          const int32_t* tp;
+          const double* wp;
+          if (tma) {
+            uint64_t* fb = &full[t * kCS + s];
+            if (lane == 0) sw::mbar_arrive_expect_tx(fb, tb + wb);
+            sw::mbar_wait(fb, (fph >> s) & 1u);
+            fph ^= 1u << s;
+            const unsigned char* buf = stages + (t * kCS + s) * kCStage;
+            tp = reinterpret_cast<const int32_t*>(buf) + ((e0 * 4 - ta) >> 2);
+            wp = reinterpret_cast<const double*>(buf + kCTB) + ((e0 * 8 - wa) >> 3);
+          } else {
+            tp = target + e0;
+            wp = w + e0;
           }
-        }
-      } else {
-        for (int sl = lane; sl < len; sl += 32) {
-          const int rel = __ldg(target + e0 + sl) - slab0;
-          if ((unsigned)rel < (unsigned)kSlab) atomicAdd(acc + rel, __ldg(w + e0 + sl));
+          // compact the slab hits of the chunk, then one atomic per entry
+          int cnt = 0;
+#pragma unroll
+          for (int kk = 0; kk < kCC / 32; ++kk) {
+            const int sl = lane + 32 * kk;
+            const int rel = sl < len ? tp[sl] - slab0 : -1;
+            const bool hit = (unsigned)rel < (unsigned)kSlab;
+            const unsigned b = __ballot_sync(SW_FULL_MASK, hit);
+            if (hit) {
+              const int pos = cnt + __popc(b & lt);
+              lpost[pos] = rel;
+              lw[pos] = wp[sl];
+            }
+            cnt += __popc(b);
+          }
+          __syncwarp();
+          if (lane == 0) sw::mbar_arrive_cluster_relaxed(&empty[t * kCS + s], 0);
+          for (int e = lane; e < cnt; e += 32) atomicAdd(acc + lpost[e], lw[e]);
+          __syncwarp();
         }
       }
-      __syncwarp();
-      if (lane == 0) sw::mbar_arrive_cluster_relaxed(&empty[warp * kCS + s], 0);
-      ++u;
-      chunk_next(it, teams, spikes, S, row_length);
+      rs.advance(spikes, row_length, lane);
     }
   }
   // all remote arrives on rank 0's barriers happen before any CTA exits
@@ -420,7 +444,7 @@ int cluster_count() {
                          kPropClusterSmem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kSlabs * 64);
-    cfg.blockDim = dim3((kCW + 1) * 32);
+    cfg.blockDim = dim3(2 * kCW * 32);
     cfg.dynamicSmemBytes = kPropClusterSmem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -489,9 +513,9 @@ extern "C" int sw_propagate_atomic(const int32_t* row_length, const int32_t* tar
   // cannot yet issue chunks as fast as the cluster consumes them)
   if (big && mode == 2 && cluster_count() > 0) {
     int clusters = cluster_count();
-    const int need = (max_spikes + kCW - 1) / kCW;
+    const int need = (max_spikes + kCW * 8 - 1) / (kCW * 8);
     if (clusters > need) clusters = need;
-    k_prop_cluster<<<clusters * kSlabs, (kCW + 1) * 32, kPropClusterSmem, (cudaStream_t)stream>>>(
+    k_prop_cluster<<<clusters * kSlabs, 2 * kCW * 32, kPropClusterSmem, (cudaStream_t)stream>>>(
         row_length, target, w, stride, (int64_t)num_pre, spikes, n_spikes, out, num_post);
     sw::count_launch();
     SW_CHECK_LAUNCH("sw_propagate_atomic(cluster)");
