@@ -2,25 +2,27 @@
  * for the CPU baseline and large oracle checks.  TEST INFRASTRUCTURE ONLY.
  * Compiled with -O2 -ffp-contract=off: every float32 op is separately
  * rounded, grad accumulates float64(float32 product) in (b, i, s) order,
- * exactly the numba loop (per synapse; rows run in parallel). */
+ * exactly the numba loop (per synapse; the rows of a replica run in parallel). */
 #include <stdint.h>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
 
-/* Rows are independent (each synapse's grad is accumulated by exactly one
- * thread, replicas in ascending order), so the OpenMP split over rows keeps
- * every result bit-identical to the serial loop. */
+/* Within one replica the rows are independent, so each replica's rows are
+ * split over OpenMP threads; replicas stay in ascending order (one parallel
+ * loop per replica), so every synapse's grad sees the same sequence of
+ * float64 additions as the serial loop: bit-identical results. */
 void oracle_eprop_accumulate_batch(const int32_t* targets, const int32_t* row_length,
                                    int64_t P, int64_t S, const float* restrict pre_trace,
                                    const float* psi, const float* lsig, int64_t B, int64_t H,
                                    float* restrict eps, float* restrict ebar, double* restrict grad, float beta,
                                    float rho, float alpha) {
-#pragma omp parallel for schedule(dynamic, 4)
-  for (int64_t i = 0; i < P; ++i) {
-    const int32_t n = row_length[i];
-    for (int64_t b = 0; b < B; ++b) {
+#pragma omp parallel
+  for (int64_t b = 0; b < B; ++b) {
+#pragma omp for schedule(static)
+    for (int64_t i = 0; i < P; ++i) {
       const float zb = pre_trace[b * P + i];
+      const int32_t n = row_length[i];
       for (int64_t s = 0; s < n; ++s) {
         const int64_t q = (b * P + i) * S + s;
         const int32_t j = targets[i * S + s];

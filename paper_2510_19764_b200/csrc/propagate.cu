@@ -242,226 +242,7 @@ int grid1(int64_t n) {
   return (int)(g < 1 ? 1 : g);
 }
 
-// ---- cluster / multicast variant of the atomic mode --------------------------------
-// The slab kernel above is bound by L2->SM bandwidth: four CTAs read every
-// row.  Here the four slab CTAs form a thread-block cluster and each row
-// chunk crosses L2 once.  16 "teams" per cluster: team t has one producer
-// warp in CTA rank 0, which multicasts the team's 128-slot row chunks
-// (targets + weights, two cp.async.bulk ... multicast::cluster copies) into
-// stage u % 3 of all four CTAs, and one consumer warp in every CTA, which
-// compacts the chunk's contributions to its own post slab through a
-// per-warp shared-memory list (so every lane issues one shared-memory
-// atomic) and then releases the stage with a remote mbarrier arrive on rank
-// 0.  Both sides walk the same row sequence with the row ids and lengths of
-// the next 8 rows prefetched in registers (lane k holds row k of a batch).
-// At the end every CTA adds its slab into `out` (one RED per nonzero post).
-constexpr int kCW = 16;                 // teams (consumer warps = producer warps) per CTA
-constexpr int kCS = 3;                  // stages per team
-constexpr int kCC = 128;                // slots per chunk
-constexpr int kCTB = kCC * 4 + 16;
-constexpr int kCWB = kCC * 8 + 16;
-constexpr int kCStage = kCTB + kCWB;
-constexpr int kCListB = kCC * 12;       // per consumer warp: compacted (post, weight) list
-constexpr int kPropClusterSmem = kSlab * 8 + kCW * kCS * kCStage + kCW * kCListB + 2 * kCW * kCS * 8;
-
-__device__ __forceinline__ bool window16(uint64_t start, uint64_t len, uint64_t limit, uint64_t& a,
-                                         uint32_t& bytes) {
-  a = start & ~15ull;
-  const uint64_t e = (start + len + 15) & ~15ull;
-  bytes = (uint32_t)(e - a);
-  return e <= limit;
-}
-
-// Row sequence of a team: spike-list entries team, team + teams, ... in
-// batches of 8 (lane k < 8 holds entry k of a batch); ids prefetched two
-// batches ahead, lengths one batch ahead.
-struct RowStream {
-  int team, teams, S;
-  int k;          // current batch
-  int id0, id1, id2;   // row ids of batches k, k+1, k+2 (lane-held)
-  int n0, n1;          // row lengths of batches k, k+1
-  __device__ int q(int kb, int lane) const { return team + (kb * 8 + lane) * teams; }
-  __device__ int load_id(const int32_t* spikes, int kb, int lane) const {
-    const int qq = q(kb, lane);
-    return (lane < 8 && qq < S) ? __ldg(spikes + qq) : -1;
-  }
-  __device__ void init(const int32_t* spikes, const int32_t* rl, int lane) {
-    k = 0;
-    id0 = load_id(spikes, 0, lane);
-    id1 = load_id(spikes, 1, lane);
-    n0 = id0 >= 0 ? __ldg(rl + id0) : 0;
-    id2 = load_id(spikes, 2, lane);
-    n1 = id1 >= 0 ? __ldg(rl + id1) : 0;
-  }
-  __device__ bool live() const { return q(k, 0) < S; }
-  __device__ void advance(const int32_t* spikes, const int32_t* rl, int lane) {
-    ++k;
-    id0 = id1;
-    n0 = n1;
-    id1 = id2;
-    n1 = id1 >= 0 ? __ldg(rl + id1) : 0;
-    id2 = load_id(spikes, k + 2, lane);
-  }
-};
-
-__global__ void __cluster_dims__(kSlabs, 1, 1) __launch_bounds__(2 * kCW * 32, 1)
-k_prop_cluster(const int32_t* __restrict__ row_length, const int32_t* __restrict__ target,
-               const double* __restrict__ w, int stride, int64_t num_pre,
-               const int32_t* __restrict__ spikes, const int32_t* n_spikes, double* out, int N) {
-  extern __shared__ __align__(16) unsigned char s_raw[];
-  double* acc = reinterpret_cast<double*>(s_raw);
-  unsigned char* stages = s_raw + kSlab * 8;
-  unsigned char* lists = stages + kCW * kCS * kCStage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(lists + kCW * kCListB);
-  uint64_t* empty = full + kCW * kCS;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = sw::cluster_ctarank();
-  const int slab0 = (int)rank * kSlab;
-
-  for (int k = threadIdx.x; k < kSlab; k += blockDim.x) acc[k] = 0.0;
-  if (threadIdx.x < kCW * kCS) {
-    sw::mbar_init(&full[threadIdx.x], 1);
-    sw::mbar_init(&empty[threadIdx.x], kSlabs);
-  }
-  sw::fence_mbar_init();
-  __syncthreads();
-  sw::cluster_sync_all();
-
-  const int S = *n_spikes;
-  const int teams = (int)(gridDim.x / kSlabs) * kCW;
-  const uint64_t t_limit = (uint64_t)num_pre * stride * 4;
-  const uint64_t w_limit = (uint64_t)num_pre * stride * 8;
-  const bool producer = warp >= kCW;
-  const int t = producer ? warp - kCW : warp;
-  RowStream rs{(int)(blockIdx.x / kSlabs) * kCW + t, teams, S, 0, 0, 0, 0, 0, 0};
-
-  if (producer) {
-    if (rank == 0) {
-      rs.init(spikes, row_length, lane);
-      uint32_t eph = 0u;
-      int u = 0;
-      while (rs.live()) {
-        for (int r = 0; r < 8; ++r) {
-          const int i = __shfl_sync(SW_FULL_MASK, rs.id0, r);
-          const int n = __shfl_sync(SW_FULL_MASK, rs.n0, r);
-          if (i < 0) break;
-          for (int c0 = 0; c0 < n; c0 += kCC, ++u) {
-            if (lane == 0) {
-              const int s = u % kCS;
-              if (u >= kCS) {
-                sw::mbar_wait_cluster(&empty[t * kCS + s], (eph >> s) & 1u);
-                eph ^= 1u << s;
-              }
-              const int len = min(kCC, n - c0);
-              const uint64_t e0 = (uint64_t)i * stride + c0;
-              uint64_t ta, wa;
-              uint32_t tb, wb;
-              if (window16(e0 * 4, (uint64_t)len * 4, t_limit, ta, tb) &&
-                  window16(e0 * 8, (uint64_t)len * 8, w_limit, wa, wb)) {
-                unsigned char* buf = stages + (t * kCS + s) * kCStage;
-                uint64_t* fb = &full[t * kCS + s];
-                sw::bulk_g2s_multicast(buf, (const unsigned char*)target + ta, tb, fb, (1u << kSlabs) - 1);
-                sw::bulk_g2s_multicast(buf + kCTB, (const unsigned char*)w + wa, wb, fb, (1u << kSlabs) - 1);
-              }
-            }
-            __syncwarp();
-          }
-        }
-        rs.advance(spikes, row_length, lane);
-      }
-    }
-  } else {
-    rs.init(spikes, row_length, lane);
-    int* lpost = reinterpret_cast<int*>(lists + t * kCListB);
-    double* lw = reinterpret_cast<double*>(lists + t * kCListB + kCC * 4);
-    const unsigned lt = sw::lanemask_lt();
-    uint32_t fph = 0u;
-    int u = 0;
-    while (rs.live()) {
-      for (int r = 0; r < 8; ++r) {
-        const int i = __shfl_sync(SW_FULL_MASK, rs.id0, r);
-        const int n = __shfl_sync(SW_FULL_MASK, rs.n0, r);
-        if (i < 0) break;
-        for (int c0 = 0; c0 < n; c0 += kCC, ++u) {
-          const int s = u % kCS;
-          const int len = min(kCC, n - c0);
-          const uint64_t e0 = (uint64_t)i * stride + c0;
-          uint64_t ta, wa;
-          uint32_t tb, wb;
-          const bool tma = window16(e0 * 4, (uint64_t)len * 4, t_limit, ta, tb) &&
-                           window16(e0 * 8, (uint64_t)len * 8, w_limit, wa, wb);
-          const int32_t* tp;
-          const double* wp;
-          if (tma) {
-            uint64_t* fb = &full[t * kCS + s];
-            if (lane == 0) sw::mbar_arrive_expect_tx(fb, tb + wb);
-            sw::mbar_wait(fb, (fph >> s) & 1u);
-            fph ^= 1u << s;
-            const unsigned char* buf = stages + (t * kCS + s) * kCStage;
-            tp = reinterpret_cast<const int32_t*>(buf) + ((e0 * 4 - ta) >> 2);
-            wp = reinterpret_cast<const double*>(buf + kCTB) + ((e0 * 8 - wa) >> 3);
-          } else {
-            tp = target + e0;
-            wp = w + e0;
-          }
-          // compact the slab hits of the chunk, then one atomic per entry
-          int cnt = 0;
-#pragma unroll
-          for (int kk = 0; kk < kCC / 32; ++kk) {
-            const int sl = lane + 32 * kk;
-            const int rel = sl < len ? tp[sl] - slab0 : -1;
-            const bool hit = (unsigned)rel < (unsigned)kSlab;
-            const unsigned b = __ballot_sync(SW_FULL_MASK, hit);
-            if (hit) {
-              const int pos = cnt + __popc(b & lt);
-              lpost[pos] = rel;
-              lw[pos] = wp[sl];
-            }
-            cnt += __popc(b);
-          }
-          __syncwarp();
-          if (lane == 0) sw::mbar_arrive_cluster_relaxed(&empty[t * kCS + s], 0);
-          for (int e = lane; e < cnt; e += 32) atomicAdd(acc + lpost[e], lw[e]);
-          __syncwarp();
-        }
-      }
-      rs.advance(spikes, row_length, lane);
-    }
-  }
-  // all remote arrives on rank 0's barriers happen before any CTA exits
-  __syncthreads();
-  sw::cluster_sync_all();
-  for (int k = threadIdx.x; k < kSlab && slab0 + k < N; k += blockDim.x) {
-    const double v = acc[k];
-    if (v != 0.0) atomicAdd(out + slab0 + k, v);
-  }
-}
-
-int cluster_count() {
-  static int nc = -1;
-  if (nc < 0) {
-    cudaFuncSetAttribute((const void*)k_prop_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kPropClusterSmem);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kSlabs * 64);
-    cfg.blockDim = dim3(2 * kCW * 32);
-    cfg.dynamicSmemBytes = kPropClusterSmem;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = kSlabs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int c = 0;
-    if (cudaOccupancyMaxActiveClusters(&c, (const void*)k_prop_cluster, &cfg) != cudaSuccess) c = 0;
-    cudaGetLastError();
-    nc = c;
-  }
-  return nc;
-}
-
-// propagation form override for measurements: SW_PROP_MODE=plain|slab|cluster
+// propagation form override for measurements: SW_PROP_MODE=plain|slab
 int prop_mode() {
   static int mode = -2;
   if (mode == -2) {
@@ -470,7 +251,6 @@ int prop_mode() {
     if (e) {
       if (!strcmp(e, "plain")) mode = 0;
       else if (!strcmp(e, "slab")) mode = 1;
-      else if (!strcmp(e, "cluster")) mode = 2;
     }
   }
   return mode;
@@ -507,24 +287,10 @@ extern "C" int sw_propagate_atomic(const int32_t* row_length, const int32_t* tar
   if (max_spikes <= 0) return SW_OK;
   const int mode = prop_mode();
   const bool big = max_spikes >= kPropSlabMinSpikes && num_post > 0 && num_post <= kSlabs * kSlab;
-  // many spiking rows and an output that fits four shared-memory slabs: the
-  // cluster / multicast kernel
-  // (experimental, SW_PROP_MODE=cluster only: the single producer thread
-  // cannot yet issue chunks as fast as the cluster consumes them)
-  if (big && mode == 2 && cluster_count() > 0) {
-    int clusters = cluster_count();
-    const int need = (max_spikes + kCW * 8 - 1) / (kCW * 8);
-    if (clusters > need) clusters = need;
-    k_prop_cluster<<<clusters * kSlabs, 2 * kCW * 32, kPropClusterSmem, (cudaStream_t)stream>>>(
-        row_length, target, w, stride, (int64_t)num_pre, spikes, n_spikes, out, num_post);
-    sw::count_launch();
-    SW_CHECK_LAUNCH("sw_propagate_atomic(cluster)");
-    return SW_OK;
-  }
-  // slab kernel (cooperative, caller workspace)
+  // many spiking rows and an output that fits the shared-memory slabs: the
+  // slab kernel (cooperative launch, per-group slabs in the caller workspace)
   const int coop_ctas = (mode == -1 || mode == 1) ? slab_ctas() : 0;
-  if (coop_ctas >= kSlabs && max_spikes >= kPropSlabMinSpikes && num_post > 0 &&
-      num_post <= kSlabs * kSlab && workspace != nullptr) {
+  if (coop_ctas >= kSlabs && big && workspace != nullptr) {
     const int groups = coop_ctas / kSlabs;
     const int64_t need = (int64_t)groups * kSlabs * kSlab * 8 + 256;
     if (workspace_bytes >= need) {
