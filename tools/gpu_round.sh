@@ -16,6 +16,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2600 --
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_eprop_fused -s 1000 -c 3 \
    -o $O/eprop_c1 -f python tools/profile_eprop.py c1 > $O/ncu_eprop.log 2>&1
 timeout 600 env ROWS=262144 ncu --set full --clock-control none --import-source on \
-   -k regex:"k_deepr_eliminate|k_deepr_form_rows|k_remove_marked" -c 6 \
+   -k regex:"k_deepr_elim|k_deepr_form_rows|k_remove_marked" -c 6 \
    -o $O/deepr -f python tools/mupdate_breakdown.py > $O/ncu_deepr.log 2>&1
 ls -la $O
