@@ -15,8 +15,8 @@ N > 1 (torchrun): the 512 replicas are sharded across ranks (batch-DP,
 strong scaling) with one NCCL all-reduce of the raw gradients per batch.
 
 --impl reference times the reference CPU path (the oracle port in
-``oracle/``: numpy with its default BLAS threads, the e-prop kernel in C with
-OpenMP over rows) on a bounded sample of the same workload and extrapolates
+``oracle/``: numpy with one BLAS thread, the e-prop kernel in C with OpenMP
+over the rows of each replica) on a bounded sample of the same workload and extrapolates
 to s/epoch; rank 0 only.
 """
 
@@ -128,7 +128,12 @@ def cpu_reference_sample(w, sample_steps=None):
     """Time the oracle port of the classifier step on the host CPU over a
     bounded number of timesteps of one batch (+ one DEEP R group) and
     extrapolate to s/epoch.  Single-threaded."""
-    return _cpu_reference_sample(w, sample_steps)
+    # numpy's BLAS stays single-threaded: its spinning worker threads would
+    # compete with the OpenMP threads of the C e-prop kernel, which carries
+    # ~90% of the reference step
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1, user_api="blas"):
+        return _cpu_reference_sample(w, sample_steps)
 
 
 def _cpu_reference_sample(w, sample_steps):
@@ -172,7 +177,7 @@ def run_reference(args, w):
     sample = (f"{r['sample_steps']} of {w['steps']} timesteps of one {w['batch']}-replica batch "
               f"(median step after the first) + one full update/DEEP R group, extrapolated "
               f"x{w['steps']} steps x{EPOCH_BATCHES} batches; oracle port: numpy + C e-prop "
-              f"(oracle/c/oracle.c, OpenMP over rows), numpy/BLAS default threads")
+              f"(oracle/c/oracle.c, OpenMP over the rows of each replica), numpy with 1 BLAS thread")
     line = {"impl": "reference", "metric": "e-prop+DEEP R training time per epoch",
             "value": round(v, 3), "unit": "s/epoch", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": False, "scaling": "strong",
