@@ -9,8 +9,17 @@
 //   k_tm_pre      STDP depression of the spiking source rows (ff) and
 //                 spiking target rows (lat), then x += 1 (plasticity.py:68-81);
 //   k_tm_post     STDP potentiation through the transposes for the spiking
-//                 targets, then y += 1 (plasticity.py:83-95); step += 1.
+//                 targets (warp per spiking post), then y += 1
+//                 (plasticity.py:83-95); step += 1.
 #include "common.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+#ifndef SW_TM_NODES_PER_CTA
+#define SW_TM_NODES_PER_CTA 512
+#endif
+#ifndef SW_TM_CG_SYNC
+#define SW_TM_CG_SYNC 1
+#endif
 
 namespace {
 
@@ -51,6 +60,27 @@ __device__ __forceinline__ void tm_neurons(const sw_topomap_step_t& S, int64_t k
   }
 }
 
+// Ordered sum over one transpose column (ascending pre): the column's
+// source ids and their spike words are loaded kColU at a time (independent
+// loads in flight), then the spiking entries are added in column order.
+constexpr int kColU = 8;
+__device__ __forceinline__ void col_sum(double& acc, int a, int e, const int32_t* src_pre,
+                                        const int32_t* src_slot, const uint32_t* bits,
+                                        const double* g, int stride) {
+  for (int q0 = a; q0 < e; q0 += kColU) {
+    int pre[kColU];
+    uint32_t wd[kColU];
+#pragma unroll
+    for (int u = 0; u < kColU; ++u) pre[u] = (q0 + u < e) ? src_pre[q0 + u] : -1;
+#pragma unroll
+    for (int u = 0; u < kColU; ++u) wd[u] = pre[u] >= 0 ? bits[pre[u] >> 5] : 0u;
+#pragma unroll
+    for (int u = 0; u < kColU; ++u)
+      if ((wd[u] >> (pre[u] & 31)) & 1u)
+        acc = __dadd_rn(acc, g[(int64_t)pre[u] * stride + src_slot[q0 + u]]);
+  }
+}
+
 __device__ __forceinline__ void tm_prop(const sw_topomap_step_t& S, int t0, int dt) {
   for (int j = t0; j < S.n; j += dt) {
     // trace decays (x per pre, y per post; square model: n pres and n posts)
@@ -60,14 +90,10 @@ __device__ __forceinline__ void tm_prop(const sw_topomap_step_t& S, int t0, int 
     S.lat_y[j] = __dmul_rn(S.lat_y[j], S.decay_y);
     if (j < S.post_lo || j >= S.post_hi) continue;
     double acc = 0.0;
-    for (int q = S.ff_col_ptr[j]; q < S.ff_col_ptr[j + 1]; ++q) {
-      const int i = S.ff_src_pre[q];
-      if (bit(S.src_bits, i)) acc = __dadd_rn(acc, S.ff_g[(int64_t)i * S.ff_stride + S.ff_src_slot[q]]);
-    }
-    for (int q = S.lat_col_ptr[j]; q < S.lat_col_ptr[j + 1]; ++q) {
-      const int i = S.lat_src_pre[q];
-      if (bit(S.tgt_bits, i)) acc = __dadd_rn(acc, S.lat_g[(int64_t)i * S.lat_stride + S.lat_src_slot[q]]);
-    }
+    col_sum(acc, S.ff_col_ptr[j], S.ff_col_ptr[j + 1], S.ff_src_pre, S.ff_src_slot, S.src_bits, S.ff_g,
+            S.ff_stride);
+    col_sum(acc, S.lat_col_ptr[j], S.lat_col_ptr[j + 1], S.lat_src_pre, S.lat_src_slot, S.tgt_bits,
+            S.lat_g, S.lat_stride);
     S.pending[j] = acc;
   }
 }
@@ -105,25 +131,39 @@ __device__ __forceinline__ void tm_pre(const sw_topomap_step_t& S, int w0, int d
   }
 }
 
-__device__ __forceinline__ void tm_post(const sw_topomap_step_t& S, int t0, int dt) {
-  for (int j = t0; j < S.n; j += dt) {
-    if (!bit(S.tgt_bits, j)) continue;
-    for (int q = S.ff_col_ptr[j]; q < S.ff_col_ptr[j + 1]; ++q) {
-      const int i = S.ff_src_pre[q];
-      const int64_t o = (int64_t)i * S.ff_stride + S.ff_src_slot[q];
-      double v = __dadd_rn(S.ff_g[o], __dmul_rn(S.a_plus, S.ff_x[i]));
-      v = fmax(v, S.w_min);
-      S.ff_g[o] = fmin(v, S.w_max);
+// potentiation through the transposes: warp w0, w0 + dw, ... over the
+// target spike words; the lanes of a warp share each spiking post's column
+// (distinct synapses, so no ordering between them), then y[post] += 1
+__device__ __forceinline__ void potentiate_col(int a, int e, const int32_t* src_pre,
+                                               const int32_t* src_slot, double* g, int stride,
+                                               const double* x, double a_plus, double w_min,
+                                               double w_max, int lane) {
+  for (int q = a + lane; q < e; q += 32) {
+    const int i = src_pre[q];
+    const int64_t o = (int64_t)i * stride + src_slot[q];
+    double v = __dadd_rn(g[o], __dmul_rn(a_plus, x[i]));
+    v = fmax(v, w_min);
+    g[o] = fmin(v, w_max);
+  }
+}
+
+__device__ __forceinline__ void tm_post(const sw_topomap_step_t& S, int w0, int dw) {
+  const int lane = threadIdx.x & 31;
+  const int words = (S.n + 31) / 32;
+  for (int gw = w0; gw < words; gw += dw) {
+    unsigned m = S.tgt_bits[gw];
+    while (m) {
+      const int j = gw * 32 + __ffs(m) - 1;
+      m &= m - 1;
+      potentiate_col(S.ff_col_ptr[j], S.ff_col_ptr[j + 1], S.ff_src_pre, S.ff_src_slot, S.ff_g,
+                     S.ff_stride, S.ff_x, S.a_plus, S.w_min, S.w_max, lane);
+      potentiate_col(S.lat_col_ptr[j], S.lat_col_ptr[j + 1], S.lat_src_pre, S.lat_src_slot, S.lat_g,
+                     S.lat_stride, S.lat_x, S.a_plus, S.w_min, S.w_max, lane);
+      if (lane == 0) {
+        S.ff_y[j] = __dadd_rn(S.ff_y[j], 1.0);
+        S.lat_y[j] = __dadd_rn(S.lat_y[j], 1.0);
+      }
     }
-    S.ff_y[j] = __dadd_rn(S.ff_y[j], 1.0);
-    for (int q = S.lat_col_ptr[j]; q < S.lat_col_ptr[j + 1]; ++q) {
-      const int i = S.lat_src_pre[q];
-      const int64_t o = (int64_t)i * S.lat_stride + S.lat_src_slot[q];
-      double v = __dadd_rn(S.lat_g[o], __dmul_rn(S.a_plus, S.lat_x[i]));
-      v = fmax(v, S.w_min);
-      S.lat_g[o] = fmin(v, S.w_max);
-    }
-    S.lat_y[j] = __dadd_rn(S.lat_y[j], 1.0);
   }
 }
 
@@ -151,8 +191,10 @@ __global__ void k_tm_neurons(sw_topomap_step_t S) {
   tm_neurons(S, *S.step, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
-__global__ void k_tm_prop(sw_topomap_step_t S) {
-  tm_prop(S, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+__global__ void k_tm_prop(sw_topomap_step_t S, int64_t* spike_counts) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gn = gridDim.x * blockDim.x;
+  tm_prop(S, gt, gn);
+  if (spike_counts) tm_count(S, gt, gn, spike_counts);
 }
 
 __global__ void k_tm_pre(sw_topomap_step_t S) {
@@ -160,14 +202,9 @@ __global__ void k_tm_pre(sw_topomap_step_t S) {
 }
 
 __global__ void k_tm_post(sw_topomap_step_t S) {
-  tm_post(S, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
-}
-
-__global__ void k_tm_tick(sw_topomap_step_t S, int64_t* spike_counts) {
-  // step += 1 and per-step spike counters (source, target); one block
-  if (spike_counts) tm_count(S, threadIdx.x, blockDim.x, spike_counts);
-  __syncthreads();
-  if (threadIdx.x == 0) *S.step += 1;
+  tm_post(S, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gridDim.x * (blockDim.x >> 5));
+  // the step counter is read only by the next step's neuron phase
+  if (blockIdx.x == 0 && threadIdx.x == 0) *S.step += 1;
 }
 
 // ---- persistent multi-step kernel ------------------------------------------------------
@@ -177,6 +214,11 @@ __global__ void k_tm_tick(sw_topomap_step_t S, int64_t* spike_counts) {
 // boundaries, so a step costs a few barrier latencies instead of five
 // launches.  Same phase bodies, same order, same results as sw_topomap_step.
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
+#if SW_TM_CG_SYNC
+  (void)bar;
+  cg::this_grid().sync();
+  return;
+#endif
   __syncthreads();
   if (gridDim.x > 1) {
     if (threadIdx.x == 0) {
@@ -213,7 +255,7 @@ k_tm_run(sw_topomap_step_t S, int n_steps, int64_t* spike_counts, unsigned* bar)
     grid_barrier(bar);
     tm_pre(S, gw, nw);
     grid_barrier(bar);
-    tm_post(S, gt, gn);
+    tm_post(S, gw, nw);
     grid_barrier(bar);
   }
   if (gt == 0) *S.step = k0 + n_steps;
@@ -269,7 +311,7 @@ k_tm_run_staged(sw_topomap_step_t G, int n_steps, int64_t* spike_counts) {
     __syncthreads();
     tm_pre(S, w, nw);
     __syncthreads();
-    tm_post(S, t, nt);
+    tm_post(S, w, nw);
     __syncthreads();
   }
   for (int x = threadIdx.x; x < n; x += blockDim.x) {
@@ -315,13 +357,14 @@ extern "C" int sw_topomap_synapses(const sw_topomap_step_t* s, int64_t* spike_co
   cudaStream_t st = (cudaStream_t)stream;
   const int n = s->n;
   if (n <= 0) return SW_OK;
-  k_tm_prop<<<grid1(n), 256, 0, st>>>(*s); sw::count_launch();
+  k_tm_prop<<<grid1(n), 256, 0, st>>>(*s, spike_counts); sw::count_launch();
   int groups = (n + 31) / 32;
   int blocks = (2 * groups + 7) / 8;
   if (blocks > 148 * 8) blocks = 148 * 8;
   k_tm_pre<<<blocks, 256, 0, st>>>(*s); sw::count_launch();
-  k_tm_post<<<grid1(n), 256, 0, st>>>(*s); sw::count_launch();
-  k_tm_tick<<<1, 256, 0, st>>>(*s, spike_counts); sw::count_launch();
+  int pblocks = (groups + 7) / 8;
+  if (pblocks > 148 * 8) pblocks = 148 * 8;
+  k_tm_post<<<pblocks, 256, 0, st>>>(*s); sw::count_launch();
   SW_CHECK_LAUNCH("sw_topomap_synapses");
   return SW_OK;
 }
@@ -359,8 +402,8 @@ extern "C" int sw_topomap_run_steps(const sw_topomap_step_t* s, int32_t n_steps,
     SW_CHECK_LAUNCH("sw_topomap_run_steps");
     return SW_OK;
   }
-  // one CTA per 2048 nodes, 512 threads, grid barriers
-  int ctas = (n + 2047) / 2048;
+  // one CTA per SW_TM_NODES_PER_CTA nodes, 512 threads, grid barriers
+  int ctas = (n + SW_TM_NODES_PER_CTA - 1) / SW_TM_NODES_PER_CTA;
   if (ctas > max_ctas) ctas = max_ctas;
   sw_topomap_step_t S = *s;
   int ns = n_steps;
