@@ -128,12 +128,16 @@ SW_API int sw_deepr_l1(const sw_ragged_t* m, int32_t grad_plane, const sw_bitfie
  * gathering 64-bit words from the num_post-wide sign row.  NULL = gather. */
 SW_API int sw_deepr_sign_cache_build(const sw_ragged_t* m, const sw_bitfield_t* sign,
                                      uint32_t* sign_slot, void* stream);
-/* Eliminate rule host+row phases (deep_r.py:81-99): warp per row; removes
- * sign-mismatched synapses with the exact remove_slots order, clears their
- * conn bits, dormant[i] = count (int64). */
+/* Eliminate rule host+row phases (deep_r.py:81-99): removes sign-mismatched
+ * synapses with the exact remove_slots order, clears their conn bits,
+ * dormant[i] = count (int64).  With sign_slot and mark_scratch (same shape
+ * as sign_slot, caller scratch) it runs as a streaming scan kernel plus a
+ * removal kernel over the rows with removals; without mark_scratch, one
+ * warp-per-row kernel does both. */
 SW_API int sw_deepr_eliminate(const sw_ragged_t* m, int32_t weight_plane,
                        const sw_bitfield_t* sign, const sw_bitfield_t* conn,
-                       int64_t* dormant, uint32_t* sign_slot, void* stream);
+                       int64_t* dormant, uint32_t* sign_slot, uint32_t* mark_scratch,
+                       void* stream);
 /* One pass of the form rule (deep_r.py:110-145).
  *   pending_src[num_pre] int64: dormant (pass 0) or unplaced of the previous
  *     pass; summed on device into counters[0] (= D, the number of host draws).

@@ -104,7 +104,7 @@ SIGNATURES: dict[str, list] = {
     "sw_deepr_init_bitfields": [RP, I32, BP, BP, U64, P],
     "sw_deepr_l1": [RP, I32, BP, P, F64, P],
     "sw_deepr_sign_cache_build": [RP, BP, P, P],
-    "sw_deepr_eliminate": [RP, I32, BP, BP, P, P, P],
+    "sw_deepr_eliminate": [RP, I32, BP, BP, P, P, P, P],
     "sw_deepr_form_pass": [RP, BP, I32, P, U64, U64, P, P, P, BP, P, P],
     "sw_eprop_accumulate_batch": [P, P, I32, I32, P, P, P, I32, I32, P, P, P, F32, F32, F32, P],
     "sw_eprop_plan": [P, P, I32, I32, I32, I32, P, P, P, P, I32, P, P],

@@ -234,6 +234,130 @@ k_deepr_elim_vec(sw_ragged_t m, int wp, sw_bitfield_t conn, int64_t* dormant, ui
   }
 }
 
+// ---- eliminate in two kernels (sign cache + mark scratch) -------------------------
+// k_deepr_elim_scan: pure streaming mismatch scan (weights + sign-cache
+// words), warp per row; writes dormant[i] and, for rows with removals, the
+// row's marked-slot bitmask marks[i, 0:ceil(n/32)].  k_deepr_elim_apply:
+// warp per group of 32 rows, visits only rows with removals: ascending
+// marked list from the bitmask, conn-bit clears, the exact chained removal.
+// The scan then runs at streaming speed whatever the removal count, and the
+// dependent round trips of the removals overlap across many warps.
+constexpr int kSW_ = 8;   // warps per block (scan and apply)
+
+__global__ void __launch_bounds__(kSW_ * 32, 6)
+k_deepr_elim_scan(sw_ragged_t m, int wp, int64_t* dormant, const uint32_t* cache, uint32_t* marks) {
+  __shared__ uint32_t s_mask[kSW_][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* mask = s_mask[warp];
+  const double* w = (const double*)m.planes[wp];
+  const int cw = (m.stride + 31) >> 5;
+  const int64_t step = (int64_t)gridDim.x * kSW_;
+  int64_t i = (int64_t)blockIdx.x * kSW_ + warp;
+  int n_next = (i < m.num_pre) ? m.row_length[i] : 0;
+  mask[lane] = 0u;
+  __syncwarp();
+  for (; i < m.num_pre; i += step) {
+    const int n = n_next;
+    if (i + step < m.num_pre) n_next = m.row_length[i + step];
+    const int64_t off = i * (int64_t)m.stride;
+    const double2* w2 = reinterpret_cast<const double2*>(w + off);
+    const uint32_t* crow = cache + i * (int64_t)cw;
+    int k = 0;
+    for (int base = 0; base < n; base += 256) {
+      double2 v[4];
+      uint32_t word[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int s0 = base + h * 128 + lane * 4;
+        if (s0 < n) {
+          v[2 * h] = __ldcs(w2 + (s0 >> 1));
+          v[2 * h + 1] = __ldcs(w2 + (s0 >> 1) + 1);
+          word[h] = __ldcs(crow + (s0 >> 5));
+        } else {
+          v[2 * h] = make_double2(0.0, 0.0);
+          v[2 * h + 1] = make_double2(0.0, 0.0);
+          word[h] = 0u;
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int s0 = base + h * 128 + lane * 4;
+        const uint32_t wd = word[h] >> (s0 & 31);
+        const double x[4] = {v[2 * h].x, v[2 * h].y, v[2 * h + 1].x, v[2 * h + 1].y};
+        unsigned mine = 0u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (s0 + j < n && mismatch(x[j], (wd >> j) & 1u)) mine |= 1u << j;
+        if (__any_sync(SW_FULL_MASK, mine != 0u)) {
+          if (mine) atomicOr(&mask[(s0 >> 5) & 31], mine << (s0 & 31));
+          k += __reduce_add_sync(SW_FULL_MASK, __popc(mine));
+        }
+      }
+    }
+    if (lane == 0) dormant[i] = k;
+    if (k > 0) {
+      __syncwarp();
+      const int nw = (n + 31) >> 5;
+      if (lane < nw) {
+        marks[i * (int64_t)cw + lane] = mask[lane];
+        mask[lane] = 0u;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSW_ * 32)
+k_deepr_elim_apply(sw_ragged_t m, sw_bitfield_t conn, const int64_t* dormant, uint32_t* cache,
+                   const uint32_t* marks) {
+  extern __shared__ int s_lists[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* list = s_lists + warp * m.stride;
+  const int cw = (m.stride + 31) >> 5;
+  const unsigned lt = sw::lanemask_lt();
+  for (int64_t g0 = ((int64_t)blockIdx.x * kSW_ + warp) * 32; g0 < m.num_pre;
+       g0 += (int64_t)gridDim.x * kSW_ * 32) {
+    const int64_t gi = g0 + lane;
+    const int my_k = gi < m.num_pre ? (int)dormant[gi] : 0;
+    const int my_n = my_k ? m.row_length[gi] : 0;
+    unsigned active = __ballot_sync(SW_FULL_MASK, my_k > 0);
+    while (active) {
+      const int src = __ffs(active) - 1;
+      active &= active - 1;
+      const int64_t i = g0 + src;
+      const int k = __shfl_sync(SW_FULL_MASK, my_k, src);
+      const int n = __shfl_sync(SW_FULL_MASK, my_n, src);
+      const int64_t off = i * (int64_t)m.stride;
+      // ascending marked list from the bitmask (lane = word)
+      const int nw = (n + 31) >> 5;
+      int pos = 0;
+      for (int w0 = 0; w0 < nw; w0 += 32) {
+        const uint32_t mw = (w0 + lane < nw) ? marks[i * (int64_t)cw + w0 + lane] : 0u;
+        const int c = __popc(mw);
+        int pre = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(SW_FULL_MASK, pre, o);
+          if (lane >= o) pre += t;
+        }
+        int p = pos + pre - c;
+        for (uint32_t mm = mw; mm; mm &= mm - 1) list[p++] = (w0 + lane) * 32 + __ffs(mm) - 1;
+        pos += __shfl_sync(SW_FULL_MASK, pre, 31);
+      }
+      __syncwarp();
+      uint64_t* cbits = conn.words + i * conn.words_per_row;
+      for (int q = lane; q < k; q += 32) {
+        const int t = __ldg(m.target + off + list[q]);
+        atomicAnd((unsigned long long*)&cbits[t >> 6], ~(1ull << (t & 63)));
+      }
+      sw::warp_apply_removal(m, off, list, n, k, cache + i * (int64_t)cw);
+      if (lane == 0) m.row_length[i] = n - k;
+      __syncwarp();
+    }
+  }
+  (void)lt;
+}
+
 // build the slot-aligned sign cache: bit s of row i = sign(i, target[i, s])
 __global__ void k_sign_cache(sw_ragged_t m, sw_bitfield_t sign, uint32_t* cache) {
   const int cw = (m.stride + 31) >> 5;
@@ -518,9 +642,23 @@ static int set_smem(const void* fn, int bytes) {
 
 extern "C" int sw_deepr_eliminate(const sw_ragged_t* m, int32_t wp, const sw_bitfield_t* sign,
                                   const sw_bitfield_t* conn, int64_t* dormant, uint32_t* sign_slot,
-                                  void* stream) {
+                                  uint32_t* mark_scratch, void* stream) {
   if (int s = check_ragged(m, "sw_deepr_eliminate: bad matrix")) return s;
   if (m->num_pre == 0) return SW_OK;
+  if (sign_slot && mark_scratch && m->plane_bytes[wp] == 8 && m->stride % 4 == 0 &&
+      m->stride <= 1024 && ((uintptr_t)m->planes[wp] % 16) == 0) {
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t g = (m->num_pre + kSW_ - 1) / kSW_;
+    if (g > 148 * 48) g = 148 * 48;
+    k_deepr_elim_scan<<<(int)g, kSW_ * 32, 0, st>>>(*m, wp, dormant, sign_slot, mark_scratch); sw::count_launch();
+    const int smem = kSW_ * m->stride * (int)sizeof(int);
+    if (int s = set_smem((const void*)k_deepr_elim_apply, smem)) return s;
+    int64_t g2 = (m->num_pre + kSW_ * 32 - 1) / (kSW_ * 32);
+    if (g2 > 148 * 16) g2 = 148 * 16;
+    k_deepr_elim_apply<<<(int)g2, kSW_ * 32, smem, st>>>(*m, *conn, dormant, sign_slot, mark_scratch); sw::count_launch();
+    SW_CHECK_LAUNCH("sw_deepr_eliminate");
+    return SW_OK;
+  }
   if (sign_slot && m->plane_bytes[wp] == 8 && m->stride % 4 == 0 &&
       ((uintptr_t)m->planes[wp] % 16) == 0) {
     const int smem = kVW * m->stride * (int)sizeof(int);

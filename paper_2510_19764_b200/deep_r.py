@@ -51,6 +51,8 @@ class DeepR:
         # slot-aligned copy of the sign bits (derived; rebuilt when the matrix
         # was changed by anything but this rule pair)
         self._sign_slot = torch.zeros((P, (matrix.stride + 31) // 32), dtype=torch.int32, device=dev)
+        # per-row marked-slot bitmasks between the eliminate scan and removal kernels
+        self._marks = torch.zeros_like(self._sign_slot)
         self._cache_version = None
 
     # -- helpers ---------------------------------------------------------------
@@ -102,7 +104,7 @@ class DeepR:
         _lib.call("sw_deepr_eliminate", ctypes.byref(d), self._plane(self.weight_plane),
                   ctypes.byref(self.sign_bits.descriptor()),
                   ctypes.byref(self.conn_bits.descriptor()), self.dormant.data_ptr(),
-                  self._sync_cache(), _lib.stream_ptr())
+                  self._sync_cache(), self._marks.data_ptr(), _lib.stream_ptr())
         self.matrix.version += 1
         self._cache_version = self.matrix.version
         return False

@@ -42,7 +42,8 @@ for u, f in enumerate((0.001, 0.01, 0.1)):
     torch.cuda.synchronize()
     e0 = ev()
     _lib.call("sw_deepr_eliminate", ctypes.byref(d), 0, ctypes.byref(dr.sign_bits.descriptor()),
-              ctypes.byref(dr.conn_bits.descriptor()), dr.dormant.data_ptr(), dr._sync_cache(), st)
+              ctypes.byref(dr.conn_bits.descriptor()), dr.dormant.data_ptr(), dr._sync_cache(),
+              dr._marks.data_ptr(), st)
     e1 = ev()
     hk, rk = fold_key(seed, "host", 1, u, 0), fold_key(seed, "row", 1, u, 0)
     _lib.call("sw_deepr_form_pass", ctypes.byref(d), ctypes.byref(dr.conn_bits.descriptor()), 0,
