@@ -307,7 +307,7 @@ k_deepr_elim_scan(sw_ragged_t m, int wp, int64_t* dormant, const uint32_t* cache
   }
 }
 
-__global__ void __launch_bounds__(kSW_ * 32)
+__global__ void __launch_bounds__(kSW_ * 32, 6)
 k_deepr_elim_apply(sw_ragged_t m, sw_bitfield_t conn, const int64_t* dormant, uint32_t* cache,
                    const uint32_t* marks) {
   extern __shared__ int s_lists[];
@@ -654,7 +654,7 @@ extern "C" int sw_deepr_eliminate(const sw_ragged_t* m, int32_t wp, const sw_bit
     const int smem = kSW_ * m->stride * (int)sizeof(int);
     if (int s = set_smem((const void*)k_deepr_elim_apply, smem)) return s;
     int64_t g2 = (m->num_pre + kSW_ * 32 - 1) / (kSW_ * 32);
-    if (g2 > 148 * 16) g2 = 148 * 16;
+    if (g2 > 148 * 6) g2 = 148 * 6;
     k_deepr_elim_apply<<<(int)g2, kSW_ * 32, smem, st>>>(*m, *conn, dormant, sign_slot, mark_scratch); sw::count_launch();
     SW_CHECK_LAUNCH("sw_deepr_eliminate");
     return SW_OK;
