@@ -275,6 +275,13 @@ SW_API int sw_scale_f64(double* x, int64_t n, double s, void* stream);
 SW_API int sw_transpose_rebuild(const sw_ragged_t* m, int32_t* col_length, int32_t* col_ptr,
                                 int32_t* src_pre, int32_t* src_slot, int32_t* cursor,
                                 int32_t* max_len, const int32_t* changed, void* stream);
+/* The same rebuild as one cooperative launch (grid barriers between the
+ * count / scan / scatter / sort phases; a single launch that exits at once
+ * when *changed reads 0).  block_scratch: >= 2048 int32 (device). */
+SW_API int sw_transpose_rebuild_coop(const sw_ragged_t* m, int32_t* col_length, int32_t* col_ptr,
+                                     int32_t* src_pre, int32_t* src_slot, int32_t* cursor,
+                                     int32_t* max_len, const int32_t* changed,
+                                     int32_t* block_scratch, void* stream);
 
 /* ---- spike propagation (connectivity.py:139-148) ---------------------------- */
 /* Event-driven atomic mode: out[target] += w over the rows in

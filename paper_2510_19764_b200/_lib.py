@@ -121,6 +121,7 @@ SIGNATURES: dict[str, list] = {
     "sw_f64_to_f32": [P, P, I64, P],
     "sw_scale_f64": [P, I64, F64, P],
     "sw_transpose_rebuild": [RP, P, P, P, P, P, P, P, P],
+    "sw_transpose_rebuild_coop": [RP, P, P, P, P, P, P, P, P, P],
     "sw_propagate_atomic": [P, P, P, I32, I32, I32, P, P, I32, P, P, I64, P],
     "sw_propagate_ordered": [P, I32, I32, P, I32, P],
     "sw_spike_bits_to_list": [P, I32, P, P, P],

@@ -20,6 +20,8 @@
 #include "common.cuh"
 #include "ragged.cuh"
 #include "util.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -61,10 +63,10 @@ __device__ __forceinline__ int fy_get(const int* key, const int* val, int n, int
   return p;
 }
 
-__global__ void k_rw_rows(RwArgs A) {
+__device__ __forceinline__ void rw_rows(const RwArgs& A, int64_t t0, int64_t dt) {
   const sw_ragged_t& m = A.m;
   const int N = m.num_post;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.num_pre; i += gridDim.x * blockDim.x) {
+  for (int i = (int)t0; i < m.num_pre; i += (int)dt) {
     const int k = A.attempts[i];
     if (k == 0) continue;
     if (k > kKMax || k > N) { atomicAdd((unsigned long long*)&A.totals[7], 1ull); continue; }
@@ -176,6 +178,55 @@ __global__ void k_rw_rows(RwArgs A) {
   }
 }
 
+__global__ void k_rw_rows(RwArgs A) {
+  rw_rows(A, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+}
+
+// One rewiring update in one cooperative launch (keys, host-phase
+// histogram, row phase behind grid barriers) when no per-attempt events are
+// recorded: one graph node per rule instead of five.
+__global__ void __launch_bounds__(256)
+k_rw_fused(RwArgs A, uint64_t host_prefix, uint64_t row_prefix, int32_t rule_id, int64_t* update_count,
+           uint64_t* keys, int32_t* attempts, int64_t total_attempts, int64_t* rej) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gn = (int64_t)gridDim.x * blockDim.x;
+  const uint64_t u = (uint64_t)*update_count;
+  const uint64_t hk = sw::fold_int(sw::fold_int(sw::fold_int(host_prefix, (uint64_t)rule_id), u), 0);
+  const uint64_t P = (uint64_t)A.m.num_pre;
+  for (int64_t i = gt; i < (int64_t)P; i += gn) attempts[i] = 0;
+  if (gt == 0) {
+    keys[0] = hk;
+    keys[1] = sw::fold_int(sw::fold_int(sw::fold_int(row_prefix, (uint64_t)rule_id), u), 0);
+    for (int k = 0; k < 8; ++k) A.totals[k] = 0;
+    *A.changed = 0;
+    *rej = 0;
+  }
+  grid.sync();
+  if (gt == 0) *update_count = (int64_t)u + 1;
+  const uint64_t rem = sw::reject_rem(P);
+  const bool pow2 = (P & (P - 1)) == 0;
+  int64_t r = 0;
+  for (int64_t c = gt; c < total_attempts; c += gn) {
+    const uint64_t h = sw::draw(hk, (uint64_t)c);
+    if (sw::draw_valid(h, rem)) atomicAdd(attempts + (pow2 ? (h & (P - 1)) : (h % P)), 1);
+    else ++r;
+  }
+  if (r) atomicAdd((unsigned long long*)rej, (unsigned long long)r);
+  grid.sync();
+  if (gt == 0 && *rej) {
+    // rejected draws (probability < P / 2^64): continue the stream serially
+    int64_t need = *rej;
+    uint64_t c = (uint64_t)total_attempts;
+    while (need > 0) {
+      const uint64_t h = sw::draw(hk, c++);
+      if (sw::draw_valid(h, rem)) { attempts[h % P] += 1; --need; }
+    }
+  }
+  if (rem != 0) grid.sync();
+  rw_rows(A, gt, gn);
+}
+
 __global__ void k_copy_i32(const int32_t* a, int32_t* b, int n) {
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) b[x] = a[x];
 }
@@ -194,6 +245,30 @@ extern "C" int sw_rewire_update(const sw_ragged_t* m, int32_t weight_plane, cons
                                 int8_t* ev_kind, double* ev_d, int32_t forced_attempts, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int P = m->num_pre;
+  if (!forced_attempts && !ev_kind && P > 0) {
+    static int max_blocks = 0;
+    if (max_blocks == 0) {
+      int per_sm = 0, sms = 0, dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rw_fused, 256, 0);
+      max_blocks = per_sm * sms;
+      if (max_blocks < 1) max_blocks = 1;
+    }
+    int blocks = grid1(P);
+    if (blocks > max_blocks) blocks = max_blocks;
+    RwArgs A{*m, weight_plane, attempts, keys, prm->form_lut, prm->dist_lut, prm->side,
+             prm->g_theta, prm->p_dep, prm->p_pot, prm->g_init, totals, changed, nullptr, nullptr, nullptr};
+    uint64_t hp = prm->host_prefix, rp = prm->row_prefix;
+    int32_t rid = prm->rule_id;
+    int64_t ta = prm->total_attempts;
+    void* args[] = {(void*)&A, (void*)&hp, (void*)&rp, (void*)&rid, (void*)&update_count, (void*)&keys,
+                    (void*)&attempts, (void*)&ta, (void*)&rej};
+    cudaLaunchCooperativeKernel((const void*)k_rw_fused, dim3(blocks), dim3(256), args, 0, st);
+    sw::count_launch();
+    SW_CHECK_LAUNCH("sw_rewire_update");
+    return SW_OK;
+  }
   k_rw_keys<<<1, 1, 0, st>>>(prm->host_prefix, prm->row_prefix, prm->rule_id, update_count, keys,
                              totals, changed); sw::count_launch();
   if (!forced_attempts) {

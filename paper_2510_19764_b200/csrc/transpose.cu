@@ -8,6 +8,8 @@
 // is decided on the device and the rebuild can sit in a CUDA graph.
 #include "common.cuh"
 #include "util.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -115,6 +117,105 @@ __global__ void k_zero_i32_guard(int32_t* a, int n, const int32_t* changed) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) a[j] = 0;
 }
 
+// ---- the whole rebuild in one cooperative launch -------------------------------------
+__global__ void __launch_bounds__(512)
+k_tr_coop(sw_ragged_t m, int32_t* col_length, int32_t* col_ptr, int32_t* src_pre, int32_t* src_slot,
+          int32_t* cursor, int32_t* max_len, const int32_t* changed, int32_t* bsum) {
+  if (skip(changed)) return;   // uniform: every block returns before any grid barrier
+  cg::grid_group grid = cg::this_grid();
+  const int N = m.num_post;
+  const int64_t total = (int64_t)m.num_pre * m.stride;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gn = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = gt; j < N; j += gn) {
+    col_length[j] = 0;
+    cursor[j] = 0;
+  }
+  if (gt == 0) *max_len = 0;
+  grid.sync();
+  for (int64_t x = gt; x < total; x += gn) {
+    const int64_t i = x / m.stride;
+    if ((int)(x - i * m.stride) < m.row_length[i]) atomicAdd(&col_length[m.target[x]], 1);
+  }
+  grid.sync();
+  // exclusive scan: block b owns the contiguous columns [c0, c1)
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t carry, boff;
+  const int per = (N + gridDim.x - 1) / gridDim.x;
+  const int c0 = min(N, (int)blockIdx.x * per), c1 = min(N, c0 + per);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto block_scan = [&](bool write) {
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = c0; base < c1; base += blockDim.x) {
+      const int x = base + threadIdx.x;
+      const int v = x < c1 ? col_length[x] : 0;
+      int inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(SW_FULL_MASK, inc, o);
+        if (lane >= o) inc += t;
+      }
+      if (lane == 31) wsum[warp] = inc;
+      __syncthreads();
+      if (warp == 0) {
+        int w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(SW_FULL_MASK, w, o);
+          if (lane >= o) w += t;
+        }
+        wsum[lane] = w;
+      }
+      __syncthreads();
+      const int before = carry + (warp ? wsum[warp - 1] : 0);
+      if (write && x < c1) col_ptr[x] = boff + before + inc - v;
+      __syncthreads();
+      if (threadIdx.x == blockDim.x - 1) carry = before + inc;
+      __syncthreads();
+    }
+  };
+  if (threadIdx.x == 0) boff = 0;
+  block_scan(false);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = carry;
+  grid.sync();
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int b = 0; b < (int)blockIdx.x; ++b) o += bsum[b];
+    boff = o;
+    if (blockIdx.x == gridDim.x - 1) col_ptr[N] = o + bsum[blockIdx.x];
+  }
+  __syncthreads();
+  block_scan(true);
+  grid.sync();
+  for (int64_t x = gt; x < total; x += gn) {
+    const int64_t i = x / m.stride;
+    const int s = (int)(x - i * m.stride);
+    if (s < m.row_length[i]) {
+      const int j = m.target[x];
+      const int pos = col_ptr[j] + atomicAdd(&cursor[j], 1);
+      src_pre[pos] = (int32_t)i;
+      src_slot[pos] = s;
+    }
+  }
+  grid.sync();
+  for (int64_t j = gt; j < N; j += gn) {
+    const int a = col_ptr[j], e = col_ptr[j + 1];
+    for (int q = a + 1; q < e; ++q) {
+      const int p = src_pre[q], s = src_slot[q];
+      int r = q - 1;
+      while (r >= a && (src_pre[r] > p || (src_pre[r] == p && src_slot[r] > s))) {
+        src_pre[r + 1] = src_pre[r];
+        src_slot[r + 1] = src_slot[r];
+        --r;
+      }
+      src_pre[r + 1] = p;
+      src_slot[r + 1] = s;
+    }
+    atomicMax(max_len, e - a);
+  }
+}
+
 int grid1(int64_t n) {
   int64_t g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
@@ -139,5 +240,34 @@ extern "C" int sw_transpose_rebuild(const sw_ragged_t* m, int32_t* col_length, i
   }
   k_tr_sort<<<grid1(N), 256, 0, st>>>(col_ptr, src_pre, src_slot, N, max_len, changed); sw::count_launch();
   SW_CHECK_LAUNCH("sw_transpose_rebuild");
+  return SW_OK;
+}
+
+extern "C" int sw_transpose_rebuild_coop(const sw_ragged_t* m, int32_t* col_length, int32_t* col_ptr,
+                                         int32_t* src_pre, int32_t* src_slot, int32_t* cursor,
+                                         int32_t* max_len, const int32_t* changed,
+                                         int32_t* block_scratch, void* stream) {
+  if (!block_scratch) { sw::set_last_error("sw_transpose_rebuild_coop: block scratch required"); return SW_ERR_INVALID_ARG; }
+  static int max_blocks = 0;
+  if (max_blocks == 0) {
+    int per_sm = 0, sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tr_coop, 512, 0);
+    max_blocks = per_sm * sms;
+    if (max_blocks > 2048) max_blocks = 2048;
+    if (max_blocks < 1) max_blocks = 1;
+  }
+  const int64_t total = (int64_t)m->num_pre * m->stride;
+  int64_t want = (total + 2047) / 2048;
+  const int64_t byn = (m->num_post + 511) / 512;
+  if (byn > want) want = byn;
+  int blocks = (int)(want < 1 ? 1 : (want > max_blocks ? max_blocks : want));
+  sw_ragged_t M = *m;
+  void* args[] = {(void*)&M, (void*)&col_length, (void*)&col_ptr, (void*)&src_pre, (void*)&src_slot,
+                  (void*)&cursor, (void*)&max_len, (void*)&changed, (void*)&block_scratch};
+  cudaLaunchCooperativeKernel((const void*)k_tr_coop, dim3(blocks), dim3(512), args, 0, (cudaStream_t)stream);
+  sw::count_launch();
+  SW_CHECK_LAUNCH("sw_transpose_rebuild_coop");
   return SW_OK;
 }

@@ -30,16 +30,19 @@ class TransposeMap:
         self.src_slot = torch.zeros(cap, dtype=torch.int32, device=dev)
         self._cursor = torch.zeros(N, dtype=torch.int32, device=dev)
         self._max_len = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._block_scratch = torch.zeros(2048, dtype=torch.int32, device=dev)
         self.version = -1
 
     def rebuild(self, changed_flag: torch.Tensor | None = None) -> None:
         """Rebuild from the matrix; with a device ``changed_flag`` the kernels
         skip the work when it reads 0 (remap-only-if-changed on the device)."""
         d = descriptor(self.matrix, None)
-        _lib.call("sw_transpose_rebuild", ctypes.byref(d), self.col_length.data_ptr(),
+        # one cooperative launch (count / scan / scatter / sort behind grid
+        # barriers; exits at once when the matrix did not change)
+        _lib.call("sw_transpose_rebuild_coop", ctypes.byref(d), self.col_length.data_ptr(),
                   self.col_ptr.data_ptr(), self.src_pre.data_ptr(), self.src_slot.data_ptr(),
                   self._cursor.data_ptr(), self._max_len.data_ptr(), _lib.ptr(changed_flag),
-                  _lib.stream_ptr())
+                  self._block_scratch.data_ptr(), _lib.stream_ptr())
         self.version = self.matrix.version
 
     @property
