@@ -243,6 +243,8 @@ k_deepr_elim_vec(sw_ragged_t m, int wp, sw_bitfield_t conn, int64_t* dormant, ui
 // The scan then runs at streaming speed whatever the removal count, and the
 // dependent round trips of the removals overlap across many warps.
 constexpr int kSW_ = 8;   // warps per block (scan and apply)
+constexpr int kSmallK = 4;   // rows with at most this many removals take the per-thread path
+__host__ __device__ __forceinline__ int small_k(int cw) { return 2 * cw < kSmallK ? 2 * cw : kSmallK; }
 
 __global__ void __launch_bounds__(kSW_ * 32, 6)
 k_deepr_elim_scan(sw_ragged_t m, int wp, int64_t* dormant, const uint32_t* cache, uint32_t* marks) {
@@ -251,6 +253,9 @@ k_deepr_elim_scan(sw_ragged_t m, int wp, int64_t* dormant, const uint32_t* cache
   uint32_t* mask = s_mask[warp];
   const double* w = (const double*)m.planes[wp];
   const int cw = (m.stride + 31) >> 5;
+  // same test as k_deepr_elim_apply: rows it handles per thread get a slot list
+  bool lane_ok = m.n_planes == 4;
+  for (int pl = 0; pl < 4 && lane_ok; ++pl) lane_ok = m.plane_bytes[pl] == 8;
   const int64_t step = (int64_t)gridDim.x * kSW_;
   int64_t i = (int64_t)blockIdx.x * kSW_ + warp;
   int n_next = (i < m.num_pre) ? m.row_length[i] : 0;
@@ -298,16 +303,105 @@ k_deepr_elim_scan(sw_ragged_t m, int wp, int64_t* dormant, const uint32_t* cache
     if (k > 0) {
       __syncwarp();
       const int nw = (n + 31) >> 5;
-      if (lane < nw) {
-        marks[i * (int64_t)cw + lane] = mask[lane];
-        mask[lane] = 0u;
+      const uint32_t mw = lane < nw ? mask[lane] : 0u;
+      if (k <= small_k(cw) && lane_ok) {
+        // few removals: the ascending slot list, packed 2 x uint16 per word
+        const int c = __popc(mw);
+        int pre = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(SW_FULL_MASK, pre, o);
+          if (lane >= o) pre += t;
+        }
+        __syncwarp();
+        uint16_t* lst = reinterpret_cast<uint16_t*>(mask);   // reuse the row mask buffer
+        int p = pre - c;
+        for (uint32_t mm = mw; mm; mm &= mm - 1) lst[p++] = (uint16_t)(lane * 32 + __ffs(mm) - 1);
+        __syncwarp();
+        if (lane < (k + 1) / 2) marks[i * (int64_t)cw + lane] = mask[lane];
+      } else if (lane < nw) {
+        marks[i * (int64_t)cw + lane] = mw;
       }
+      __syncwarp();
+      mask[lane] = 0u;
       __syncwarp();
     }
   }
 }
 
-__global__ void __launch_bounds__(kSW_ * 32, 6)
+// one thread per row: the exact chained removal of up to kSmallK slots
+// (SURVEY App. D1).  The (dst, src) pairs are resolved in registers first,
+// then every load of the row (marked targets, source target + planes +
+// sign-cache words) is issued before any store.
+__device__ __forceinline__ void lane_apply_removal(const sw_ragged_t& m, const sw_bitfield_t& conn,
+                                                   uint32_t* cache, const uint32_t* marks, int cw,
+                                                   int64_t i, int n, int k) {
+  const int64_t off = i * (int64_t)m.stride;
+  int mk[kSmallK];
+#pragma unroll
+  for (int q = 0; q < kSmallK; q += 2) {
+    if (q < k) {
+      const uint32_t wd = marks[i * (int64_t)cw + q / 2];
+      mk[q] = (int)(wd & 0xffffu);
+      mk[q + 1] = (int)(wd >> 16);
+    }
+  }
+  const int n2 = n - k;
+  int dst[kSmallK], src[kSmallK];
+#pragma unroll
+  for (int t = 1; t <= kSmallK; ++t) {
+    dst[t - 1] = -1;
+    if (t > k) continue;
+    const int mt = mk[k - t];
+    if (mt >= n2) continue;
+    int p = n - t;
+#pragma unroll 1
+    for (int guard = 0; guard <= kSmallK; ++guard) {
+      int idx = -1;
+#pragma unroll
+      for (int q = 0; q < kSmallK; ++q)
+        if (q < k && mk[q] == p) idx = q;
+      if (idx < 0) break;
+      p = n - (k - idx);
+    }
+    dst[t - 1] = mt;
+    src[t - 1] = p;
+  }
+  // loads
+  int tm[kSmallK], st[kSmallK];
+  uint64_t pv[kSmallK][4];
+  uint32_t cwd[kSmallK];
+  const uint32_t* crow_s = cache + i * (int64_t)cw;
+#pragma unroll
+  for (int q = 0; q < kSmallK; ++q) {
+    if (q < k) tm[q] = m.target[off + mk[q]];
+    if (dst[q] >= 0) {
+      st[q] = m.target[off + src[q]];
+#pragma unroll
+      for (int pl = 0; pl < 4; ++pl)
+        pv[q][pl] = ((const uint64_t*)m.planes[pl])[off + src[q]];
+      cwd[q] = crow_s[src[q] >> 5];
+    }
+  }
+  // stores and bit updates
+  uint64_t* crow = conn.words + i * conn.words_per_row;
+  uint32_t* crow_w = cache + i * (int64_t)cw;
+#pragma unroll
+  for (int q = 0; q < kSmallK; ++q) {
+    if (q < k) atomicAnd((unsigned long long*)&crow[tm[q] >> 6], ~(1ull << (tm[q] & 63)));
+    if (dst[q] >= 0) {
+      m.target[off + dst[q]] = st[q];
+#pragma unroll
+      for (int pl = 0; pl < 4; ++pl) ((uint64_t*)m.planes[pl])[off + dst[q]] = pv[q][pl];
+      const int d = dst[q];
+      if ((cwd[q] >> (src[q] & 31)) & 1u) atomicOr(&crow_w[d >> 5], 1u << (d & 31));
+      else atomicAnd(&crow_w[d >> 5], ~(1u << (d & 31)));
+    }
+  }
+  m.row_length[i] = n2;
+}
+
+__global__ void __launch_bounds__(kSW_ * 32)
 k_deepr_elim_apply(sw_ragged_t m, sw_bitfield_t conn, const int64_t* dormant, uint32_t* cache,
                    const uint32_t* marks) {
   extern __shared__ int s_lists[];
@@ -315,12 +409,17 @@ k_deepr_elim_apply(sw_ragged_t m, sw_bitfield_t conn, const int64_t* dormant, ui
   int* list = s_lists + warp * m.stride;
   const int cw = (m.stride + 31) >> 5;
   const unsigned lt = sw::lanemask_lt();
+  bool lane_ok = m.n_planes == 4;
+  for (int pl = 0; pl < 4 && lane_ok; ++pl) lane_ok = m.plane_bytes[pl] == 8;
   for (int64_t g0 = ((int64_t)blockIdx.x * kSW_ + warp) * 32; g0 < m.num_pre;
        g0 += (int64_t)gridDim.x * kSW_ * 32) {
     const int64_t gi = g0 + lane;
     const int my_k = gi < m.num_pre ? (int)dormant[gi] : 0;
     const int my_n = my_k ? m.row_length[gi] : 0;
-    unsigned active = __ballot_sync(SW_FULL_MASK, my_k > 0);
+    // rows with few removals: one thread per row (four 8-byte planes)
+    const int ks = lane_ok ? small_k(cw) : 0;
+    if (my_k > 0 && my_k <= ks) lane_apply_removal(m, conn, cache, marks, cw, gi, my_n, my_k);
+    unsigned active = __ballot_sync(SW_FULL_MASK, my_k > ks);
     while (active) {
       const int src = __ffs(active) - 1;
       active &= active - 1;
@@ -654,7 +753,7 @@ extern "C" int sw_deepr_eliminate(const sw_ragged_t* m, int32_t wp, const sw_bit
     const int smem = kSW_ * m->stride * (int)sizeof(int);
     if (int s = set_smem((const void*)k_deepr_elim_apply, smem)) return s;
     int64_t g2 = (m->num_pre + kSW_ * 32 - 1) / (kSW_ * 32);
-    if (g2 > 148 * 6) g2 = 148 * 6;
+    if (g2 > 148 * 8) g2 = 148 * 8;
     k_deepr_elim_apply<<<(int)g2, kSW_ * 32, smem, st>>>(*m, *conn, dormant, sign_slot, mark_scratch); sw::count_launch();
     SW_CHECK_LAUNCH("sw_deepr_eliminate");
     return SW_OK;
