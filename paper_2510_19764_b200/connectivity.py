@@ -220,3 +220,26 @@ def propagate_spikes(m: RaggedMatrix, weights: torch.Tensor, spikes: torch.Tenso
     _lib.call("sw_propagate_atomic", m.row_length.data_ptr(), m.target.data_ptr(),
               weights.data_ptr(), m.num_pre, m.num_post, m.stride, sp.data_ptr(), n.data_ptr(),
               max(1, sp.numel()), out.data_ptr(), *_lib.prop_workspace(), st)
+
+
+def write_snapshot_csv(fh, m: RaggedMatrix, syn: SynVarMatrix | None = None,
+                       columns=(("weight", "g"),)) -> None:
+    """Connectivity snapshot ``pre,post[,var...]`` sorted by (pre, post), in
+    the reference's text format (connectivity.py:265-283): the valid slots
+    are compacted and sorted on the device, then formatted on the host."""
+    mask = m.slot_mask()
+    pre = torch.arange(m.num_pre, device=m.target.device, dtype=torch.int64)[:, None].expand_as(mask)[mask]
+    post = m.target[mask].to(torch.int64)
+    order = torch.argsort(pre * m.num_post + post)
+    header = "pre,post"
+    cols = []
+    if syn is not None:
+        for label, plane in columns:
+            header += "," + label
+            cols.append(syn.planes[plane][mask][order].cpu().numpy())
+    pre = pre[order].cpu().numpy()
+    post = post[order].cpu().numpy()
+    fh.write(header + "\n")
+    for k in range(pre.size):
+        extra = "".join("," + repr(float(c[k])) for c in cols)
+        fh.write(f"{pre[k]},{post[k]}{extra}\n")

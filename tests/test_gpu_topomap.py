@@ -258,3 +258,37 @@ def test_persistent_multi_cta_steps_equal_per_step_launches(dev_lib, scale, monk
     sa, sb = a.state_arrays(), b.state_arrays()
     for key in sa:
         assert np.array_equal(sa[key], sb[key]), key
+
+
+def test_snapshot_csv_matches_reference_bytes(dev_lib):
+    """connectivity.py:265-283 write_snapshot_csv: byte-identical to the
+    reference's output for the same matrix (tests/golden/make_snapshot_csv.py)."""
+    import io
+    import os
+    from conftest import GOLDEN
+    from paper_2510_19764_b200.connectivity import RaggedMatrix, SynVarMatrix, write_snapshot_csv
+    g = golden("transpose_prop.npz")
+    m = RaggedMatrix(50, 40, 16)
+    syn = SynVarMatrix(m, ("g",))
+    m.load_state(g["row_length"], g["target"])
+    syn.planes["g"].copy_(torch.from_numpy(g["g"]))
+    buf = io.StringIO()
+    write_snapshot_csv(buf, m, syn)
+    assert buf.getvalue() == open(os.path.join(GOLDEN, "snapshot_transpose_prop.csv")).read()
+
+
+def test_phase_timer_csv_schema(dev_lib):
+    """updates.py:50-54 timing.csv schema: phase,seconds rows for the six
+    phases, then total."""
+    import io
+    from paper_2510_19764_b200.topomap import TopomapModel
+    from paper_2510_19764_b200.updates import PHASES
+    model = TopomapModel(1, seed=3, record_events=False, use_graph=False)
+    model.run(2.0)
+    buf = io.StringIO()
+    model.net.timers.write_csv(buf)
+    lines = buf.getvalue().splitlines()
+    assert lines[0] == "phase,seconds"
+    assert [ln.split(",")[0] for ln in lines[1:]] == list(PHASES) + ["total"]
+    vals = [float(ln.split(",")[1]) for ln in lines[1:]]
+    assert abs(sum(vals[:-1]) - vals[-1]) < 1e-6 and vals[PHASES.index("row_update")] > 0
