@@ -561,6 +561,61 @@ __global__ void k_form_hist_fix(int64_t* counters, uint64_t key, uint64_t P, uin
 // of the batch already placed the same post (match_any), the failure streak
 // resets per activation and ends it after num_post misses, a full row stops
 // all remaining activations without consuming draws.
+// One thread per row: the sequential loop of deep_r.py:126-145 verbatim
+// (draw by draw with exact rejection, failure streak per activation, full
+// row stops all remaining activations without draws).  Posts placed earlier
+// in this row are also checked from registers, so the result never depends
+// on when the thread's own conn-bit atomics become visible.
+constexpr int kFormSmall = 4;
+
+__device__ __forceinline__ void lane_form_row(const sw_ragged_t& m, const sw_bitfield_t& conn,
+                                              int excl_diag, uint64_t row_base, int64_t i, int acts,
+                                              int len, int64_t* unplaced, int64_t* counters,
+                                              const sw_bitfield_t& sign, uint32_t* cache, int N,
+                                              uint64_t rem, bool pow2, int cap) {
+  const int64_t off = i * (int64_t)m.stride;
+  uint64_t* crow = conn.words + i * conn.words_per_row;
+  const uint64_t key = sw::child_key(row_base, (uint64_t)i);
+  uint64_t ctr = 0;
+  int placed[kFormSmall];
+  int np = 0, a = 0, streak = 0, unpl = 0;
+  while (a < acts) {
+    if (len >= cap) { unpl += acts - a; break; }
+    const uint64_t h = sw::draw(key, ctr++);
+    if (!sw::draw_valid(h, rem)) continue;   // a rejected draw is not an iteration
+    const int j = (int)(pow2 ? (h & (uint64_t)(N - 1)) : (h % (uint64_t)N));
+    bool fail = excl_diag && j == (int)i;
+    bool sbit = false;
+    if (!fail) {
+      const uint64_t cw = __ldcg(crow + (j >> 6));
+      if (cache) sbit = (__ldg(sign.words + i * sign.words_per_row + (j >> 6)) >> (j & 63)) & 1ull;
+      fail = (cw >> (j & 63)) & 1ull;
+#pragma unroll
+      for (int q = 0; q < kFormSmall; ++q) fail |= (q < np && placed[q] == j);
+    }
+    if (fail) {
+      if (++streak == N) { ++unpl; ++a; streak = 0; }
+      continue;
+    }
+    m.target[off + len] = j;
+    sw::zero_slot(m, off, len);
+    atomicOr((unsigned long long*)(crow + (j >> 6)), 1ull << (j & 63));
+    if (cache) {
+      uint32_t* cr = cache + i * (int64_t)((m.stride + 31) >> 5);
+      if (sbit) atomicOr(&cr[len >> 5], 1u << (len & 31));
+      else atomicAnd(&cr[len >> 5], ~(1u << (len & 31)));
+    }
+    placed[np < kFormSmall ? np : kFormSmall - 1] = j;
+    ++np;
+    ++len;
+    ++a;
+    streak = 0;
+  }
+  m.row_length[i] = len;
+  unplaced[i] = unpl;
+  if (unpl) atomicAdd((unsigned long long*)&counters[1], (unsigned long long)unpl);
+}
+
 __global__ void __launch_bounds__(kThreads, 8)
 k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row_base,
                   const int32_t* act, int64_t* unplaced, int64_t* counters, sw_bitfield_t sign,
@@ -579,7 +634,11 @@ k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row
     const int my_act = gi < m.num_pre ? act[gi] : 0;
     const int my_len = (gi < m.num_pre && my_act) ? m.row_length[gi] : 0;
     if (gi < m.num_pre && my_act == 0) unplaced[gi] = 0;
-    unsigned active = __ballot_sync(SW_FULL_MASK, my_act != 0);
+    // rows with few activations: one thread per row, all 32 rows in flight
+    if (my_act > 0 && my_act <= kFormSmall)
+      lane_form_row(m, conn, excl_diag, row_base, gi, my_act, my_len, unplaced, counters, sign, cache,
+                    N, rem, pow2, cap);
+    unsigned active = __ballot_sync(SW_FULL_MASK, my_act > kFormSmall);
     while (active) {
     const int src_lane = __ffs(active) - 1;
     active &= active - 1;
