@@ -243,7 +243,8 @@ k_deepr_elim_vec(sw_ragged_t m, int wp, sw_bitfield_t conn, int64_t* dormant, ui
 // The scan then runs at streaming speed whatever the removal count, and the
 // dependent round trips of the removals overlap across many warps.
 constexpr int kSW_ = 8;   // warps per block (scan and apply)
-constexpr int kSmallK = 4;   // rows with at most this many removals take the per-thread path
+constexpr int kSmallK = 8;   // rows with at most this many removals take the per-thread path
+constexpr int kMoveBatch = 4;
 __host__ __device__ __forceinline__ int small_k(int cw) { return 2 * cw < kSmallK ? 2 * cw : kSmallK; }
 
 __global__ void __launch_bounds__(kSW_ * 32, 6)
@@ -367,35 +368,46 @@ __device__ __forceinline__ void lane_apply_removal(const sw_ragged_t& m, const s
     dst[t - 1] = mt;
     src[t - 1] = p;
   }
-  // loads
-  int tm[kSmallK], st[kSmallK];
-  uint64_t pv[kSmallK][4];
-  uint32_t cwd[kSmallK];
-  const uint32_t* crow_s = cache + i * (int64_t)cw;
+  // conn clears: every marked slot's target, read before any move
+  int tm[kSmallK];
 #pragma unroll
-  for (int q = 0; q < kSmallK; ++q) {
+  for (int q = 0; q < kSmallK; ++q)
     if (q < k) tm[q] = m.target[off + mk[q]];
-    if (dst[q] >= 0) {
-      st[q] = m.target[off + src[q]];
-#pragma unroll
-      for (int pl = 0; pl < 4; ++pl)
-        pv[q][pl] = ((const uint64_t*)m.planes[pl])[off + src[q]];
-      cwd[q] = crow_s[src[q] >> 5];
-    }
-  }
-  // stores and bit updates
   uint64_t* crow = conn.words + i * conn.words_per_row;
+#pragma unroll
+  for (int q = 0; q < kSmallK; ++q)
+    if (q < k) atomicAnd((unsigned long long*)&crow[tm[q] >> 6], ~(1ull << (tm[q] & 63)));
+  // moves, kMoveBatch at a time: all loads of a batch, then its stores
+  const uint32_t* crow_s = cache + i * (int64_t)cw;
   uint32_t* crow_w = cache + i * (int64_t)cw;
 #pragma unroll
-  for (int q = 0; q < kSmallK; ++q) {
-    if (q < k) atomicAnd((unsigned long long*)&crow[tm[q] >> 6], ~(1ull << (tm[q] & 63)));
-    if (dst[q] >= 0) {
-      m.target[off + dst[q]] = st[q];
+  for (int g = 0; g < kSmallK; g += kMoveBatch) {
+    if (g >= k) break;
+    int st[kMoveBatch];
+    uint64_t pv[kMoveBatch][4];
+    uint32_t cwd[kMoveBatch];
 #pragma unroll
-      for (int pl = 0; pl < 4; ++pl) ((uint64_t*)m.planes[pl])[off + dst[q]] = pv[q][pl];
-      const int d = dst[q];
-      if ((cwd[q] >> (src[q] & 31)) & 1u) atomicOr(&crow_w[d >> 5], 1u << (d & 31));
-      else atomicAnd(&crow_w[d >> 5], ~(1u << (d & 31)));
+    for (int u = 0; u < kMoveBatch; ++u) {
+      const int q = g + u;
+      if (dst[q] >= 0) {
+        st[u] = m.target[off + src[q]];
+#pragma unroll
+        for (int pl = 0; pl < 4; ++pl)
+          pv[u][pl] = ((const uint64_t*)m.planes[pl])[off + src[q]];
+        cwd[u] = crow_s[src[q] >> 5];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kMoveBatch; ++u) {
+      const int q = g + u;
+      if (dst[q] >= 0) {
+        const int d = dst[q];
+        m.target[off + d] = st[u];
+#pragma unroll
+        for (int pl = 0; pl < 4; ++pl) ((uint64_t*)m.planes[pl])[off + d] = pv[u][pl];
+        if ((cwd[u] >> (src[q] & 31)) & 1u) atomicOr(&crow_w[d >> 5], 1u << (d & 31));
+        else atomicAnd(&crow_w[d >> 5], ~(1u << (d & 31)));
+      }
     }
   }
   m.row_length[i] = n2;
@@ -566,7 +578,7 @@ __global__ void k_form_hist_fix(int64_t* counters, uint64_t key, uint64_t P, uin
 // row stops all remaining activations without draws).  Posts placed earlier
 // in this row are also checked from registers, so the result never depends
 // on when the thread's own conn-bit atomics become visible.
-constexpr int kFormSmall = 4;
+constexpr int kFormSmall = 2;
 
 __device__ __forceinline__ void lane_form_row(const sw_ragged_t& m, const sw_bitfield_t& conn,
                                               int excl_diag, uint64_t row_base, int64_t i, int acts,
