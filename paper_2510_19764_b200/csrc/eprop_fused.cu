@@ -5,7 +5,7 @@
 // then pre, then slot — sw_eprop_plan), so one (tile, replica chunk) is one
 // contiguous run that the TMA bulk engine moves with a single copy.
 //
-// Block = 10 warps, one tile-chunk "stage" at a time through a 4-deep
+// Block = 2 + SW_EPROP_COMPUTE (4) warps, one tile-chunk "stage" at a time through a 4-deep
 // shared-memory ring:
 //   warp 0      loader:  takes tiles from an atomic ticket, issues
 //                        cp.async.bulk global->shared for eps and ebar of
@@ -13,7 +13,7 @@
 //                        L2 evict-first policy, so the 200 MB/step stream does
 //                        not evict the small per-replica state of the forward
 //                        kernel;
-//   warps 2..9  compute: 4 replicas each per stage — gathers zb/psi/lsig
+//   warps 2..5  compute: 8 replicas each per stage — gathers zb/psi/lsig
 //                        (L2-resident, 128-byte lines thanks to the plan
 //                        order), updates eps/ebar in place in shared memory,
 //                        writes the float32 gradient terms;
@@ -48,8 +48,17 @@ struct ReadoutArgs {
 };
 
 constexpr int kCB = 32;                   // replicas per stage
-constexpr int kStages = 4;                // ring depth
-constexpr int kCompute = 8;               // compute warps
+#ifndef SW_EPROP_STAGES
+#define SW_EPROP_STAGES 4
+#endif
+#ifndef SW_EPROP_MINB
+#define SW_EPROP_MINB 1
+#endif
+#ifndef SW_EPROP_COMPUTE
+#define SW_EPROP_COMPUTE 4
+#endif
+constexpr int kStages = SW_EPROP_STAGES;  // ring depth
+constexpr int kCompute = SW_EPROP_COMPUTE; // compute warps
 constexpr int kWarps = kCompute + 2;
 constexpr int kThreads = kWarps * 32;
 constexpr int kBPW = kCB / kCompute;      // replicas per compute warp per stage
@@ -115,7 +124,7 @@ __device__ __forceinline__ const Seg& seg_of(const Seg& s0, const Seg& s1, int t
   return s1;
 }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, SW_EPROP_MINB)
 k_eprop_fused(Seg s0, Seg s1, const float* __restrict__ psi, const float* __restrict__ lsig,
               int B, int H, float beta, float rho, float alpha, ReadoutArgs ro, int ro_blocks,
               unsigned* tickets) {
