@@ -98,6 +98,19 @@ SW_API int sw_bitfield_randomize(const sw_bitfield_t* bf, uint64_t key, void* st
 SW_API int sw_ragged_remove_marked(const sw_ragged_t* m, const uint8_t* marked,
                             int64_t* removed, void* stream);
 
+/* add_synapse (connectivity.py:91-112) on one row: RowFull, DuplicateEdge
+ * (when multapse_free), else append post with every plane zeroed and
+ * values[p] stored where set_mask[p] != 0.  status (device int32[1]) gets
+ * the new slot, or -SW_ERR_ROW_FULL / -SW_ERR_DUPLICATE_EDGE. */
+SW_API int sw_ragged_add_synapse(const sw_ragged_t* m, int32_t pre, int32_t post,
+                                 const double* values, const uint8_t* set_mask,
+                                 int32_t multapse_free, int32_t* status, void* stream);
+/* remove_slots / remove_synapse (connectivity.py:115-136) on one row, the
+ * reference's descending chained swap-with-last order.  slots[k] (device);
+ * status (device int32[2]): [0] = 0 or -SW_ERR_SLOT_OUT_OF_RANGE. */
+SW_API int sw_ragged_remove_row_slots(const sw_ragged_t* m, int32_t pre, const int32_t* slots,
+                                      int32_t k, int32_t* status, void* stream);
+
 /* Pairwise-Bernoulli initialisation (init_pairwise_bernoulli, connectivity.py:212-245):
  * pair (i, j) uses uniform01 draw #(counter0 + i*num_post + j) of `key` and
  * connects iff u < p.  mode 0: p = density; mode 1: density with p(i,i) = 0;

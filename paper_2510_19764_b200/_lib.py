@@ -99,6 +99,8 @@ SIGNATURES: dict[str, list] = {
     "sw_rng_child_keys": [U64, I64, P, P],
     "sw_bitfield_randomize": [BP, U64, P],
     "sw_ragged_remove_marked": [RP, P, P, P],
+    "sw_ragged_add_synapse": [RP, I32, I32, P, P, I32, P, P],
+    "sw_ragged_remove_row_slots": [RP, I32, P, I32, P, P],
     "sw_init_bernoulli_count": [I64, I32, U64, U64, I32, F64, P, I32, P, P, P],
     "sw_init_bernoulli_fill": [I64, I32, U64, U64, I32, F64, P, I32, P, P, I32, P],
     "sw_deepr_init_bitfields": [RP, I32, BP, BP, U64, P],

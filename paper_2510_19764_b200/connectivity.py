@@ -129,6 +129,54 @@ def remove_marked(m: RaggedMatrix, syn: SynVarMatrix | None, marked: torch.Tenso
     m.version += 1
 
 
+def add_synapse(m: RaggedMatrix, syn: SynVarMatrix | None, pre: int, post: int,
+                values: dict | None = None) -> int:
+    """Append pre -> post and return its slot (connectivity.py:91-112): every
+    plane is zeroed at the new slot, then ``values`` are set.  Raises
+    RowFull / DuplicateEdge like the reference (one device round trip)."""
+    from .errors import DuplicateEdge, RowFull
+    d = descriptor(m, syn)
+    names = list(syn.planes) if syn is not None else []
+    vals = torch.zeros(max(1, len(names)), dtype=torch.float64)
+    mask = torch.zeros(max(1, len(names)), dtype=torch.uint8)
+    for name, v in (values or {}).items():
+        k = names.index(name)
+        vals[k] = float(v)
+        mask[k] = 1
+    dv, dm = vals.to(DEV), mask.to(DEV)
+    status = torch.zeros(2, dtype=torch.int32, device=DEV)
+    _lib.call("sw_ragged_add_synapse", C_ref(d), int(pre), int(post), dv.data_ptr(), dm.data_ptr(),
+              int(m.multapse_free), status.data_ptr(), _lib.stream_ptr())
+    st = int(status[0].item())
+    if st == -1:
+        raise RowFull(f"row {pre} at capacity {m.max_row_length}")
+    if st == -2:
+        raise DuplicateEdge(f"edge ({pre}, {post}) already exists")
+    m.version += 1
+    return st
+
+
+def remove_slots(m: RaggedMatrix, syn: SynVarMatrix | None, pre: int, slots) -> None:
+    """Remove several slots of one row, descending order with swap-from-the-end
+    moves (connectivity.py:130-136).  Raises SlotOutOfRange like the
+    reference's loop."""
+    from .errors import SlotOutOfRange
+    sl = torch.as_tensor(np.asarray(slots, dtype=np.int32).reshape(-1)).to(DEV)
+    d = descriptor(m, syn)
+    status = torch.zeros(2, dtype=torch.int32, device=DEV)
+    _lib.call("sw_ragged_remove_row_slots", C_ref(d), int(pre), sl.data_ptr(), int(sl.numel()),
+              status.data_ptr(), _lib.stream_ptr())
+    m.version += 1
+    if int(status[0].item()) != 0:
+        raise SlotOutOfRange(f"slot out of range in row {pre}")
+
+
+def remove_synapse(m: RaggedMatrix, syn: SynVarMatrix | None, pre: int, slot: int) -> None:
+    """Remove one synapse: the last valid slot moves into its place
+    (connectivity.py:115-127)."""
+    remove_slots(m, syn, pre, [slot])
+
+
 def C_ref(d):
     import ctypes
     return ctypes.byref(d)

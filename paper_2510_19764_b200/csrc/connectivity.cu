@@ -5,6 +5,7 @@
 // (topomap.py:376-388: p = formation_probability(toroidal_distance(i, j)),
 // which depends only on the wrapped offset between the grid nodes).
 #include "common.cuh"
+#include "ragged.cuh"
 
 namespace {
 
@@ -91,5 +92,112 @@ extern "C" int sw_init_bernoulli_fill(int64_t num_pre, int32_t num_post, uint64_
                                                         density, lut, side, row_length, target,
                                                         stride, nullptr); sw::count_launch();
   SW_CHECK_LAUNCH("sw_init_bernoulli_fill");
+  return SW_OK;
+}
+
+// ---- single-synapse edits (connectivity.py:91-136), one warp ---------------------------
+namespace {
+
+// add_synapse: RowFull, then (multapse-free) DuplicateEdge by a lane-parallel
+// scan of the row, then append with every plane zeroed and the given values
+// set.  status[0] = slot (>= 0) or -SW_ERR_*.
+__global__ void k_add_synapse(sw_ragged_t m, int pre, int post, const double* vals,
+                              const uint8_t* set_mask, int multapse_free, int32_t* status) {
+  const int lane = threadIdx.x;
+  const int n = m.row_length[pre];
+  const int64_t off = (int64_t)pre * m.stride;
+  if (n >= m.max_row_length) {
+    if (lane == 0) status[0] = -SW_ERR_ROW_FULL;
+    return;
+  }
+  bool dup = false;
+  if (multapse_free)
+    for (int s = lane; s < n; s += 32) dup |= m.target[off + s] == post;
+  if (__any_sync(SW_FULL_MASK, dup)) {
+    if (lane == 0) status[0] = -SW_ERR_DUPLICATE_EDGE;
+    return;
+  }
+  if (lane == 0) {
+    m.target[off + n] = post;
+    sw::zero_slot(m, off, n);
+    for (int p = 0; p < m.n_planes; ++p) {
+      if (!(set_mask && set_mask[p])) continue;
+      if (m.plane_bytes[p] == 8) ((double*)m.planes[p])[off + n] = vals[p];
+      else ((float*)m.planes[p])[off + n] = (float)vals[p];
+    }
+    m.row_length[pre] = n + 1;
+    status[0] = n;
+  }
+}
+
+// remove_slots of one row: slots[0..k) in any order.  Distinct, in-range
+// slots take the exact chained swap-with-last permutation (warp); anything
+// else (duplicates) replays remove_synapse one slot at a time in descending
+// order, as the reference loop does, stopping at the first out-of-range slot.
+__global__ void k_remove_row_slots(sw_ragged_t m, int pre, const int32_t* slots, int k, int32_t* status) {
+  extern __shared__ int lst[];
+  const int lane = threadIdx.x;
+  const int n = m.row_length[pre];
+  const int64_t off = (int64_t)pre * m.stride;
+  if (lane == 0) {
+    for (int q = 0; q < k; ++q) lst[q] = slots[q];
+    // insertion sort ascending
+    for (int q = 1; q < k; ++q) {
+      const int v = lst[q];
+      int r = q - 1;
+      while (r >= 0 && lst[r] > v) { lst[r + 1] = lst[r]; --r; }
+      lst[r + 1] = v;
+    }
+    bool distinct = true;
+    for (int q = 1; q < k; ++q) distinct &= lst[q] != lst[q - 1];
+    status[1] = distinct && (k == 0 || (lst[0] >= 0 && lst[k - 1] < n));
+  }
+  __syncwarp();
+  if (status[1]) {
+    if (k > 0) {
+      sw::warp_apply_removal(m, off, lst, n, k);
+      if (lane == 0) m.row_length[pre] = n - k;
+    }
+    if (lane == 0) status[0] = 0;
+    return;
+  }
+  if (lane == 0) {
+    int len = n;
+    status[0] = 0;
+    for (int q = k - 1; q >= 0; --q) {
+      const int slot = lst[q];
+      if (slot < 0 || slot >= len) { status[0] = -SW_ERR_SLOT_OUT_OF_RANGE; break; }
+      const int last = len - 1;
+      if (slot != last) sw::move_slot(m, off, slot, last);
+      len = last;
+    }
+    m.row_length[pre] = len;
+  }
+}
+
+}  // namespace
+
+extern "C" int sw_ragged_add_synapse(const sw_ragged_t* m, int32_t pre, int32_t post,
+                                     const double* values, const uint8_t* set_mask,
+                                     int32_t multapse_free, int32_t* status, void* stream) {
+  if (pre < 0 || pre >= m->num_pre || post < 0 || post >= m->num_post) {
+    sw::set_last_error("add_synapse: pre/post out of range");
+    return SW_ERR_INVALID_ARG;
+  }
+  k_add_synapse<<<1, 32, 0, (cudaStream_t)stream>>>(*m, pre, post, values, set_mask, multapse_free,
+                                                     status); sw::count_launch();
+  SW_CHECK_LAUNCH("sw_ragged_add_synapse");
+  return SW_OK;
+}
+
+extern "C" int sw_ragged_remove_row_slots(const sw_ragged_t* m, int32_t pre, const int32_t* slots,
+                                          int32_t k, int32_t* status, void* stream) {
+  if (pre < 0 || pre >= m->num_pre || k < 0 || k > m->stride) {
+    sw::set_last_error("remove_slots: bad row or slot count");
+    return SW_ERR_INVALID_ARG;
+  }
+  k_remove_row_slots<<<1, 32, (size_t)(k > 0 ? k : 1) * sizeof(int), (cudaStream_t)stream>>>(
+      *m, pre, slots, k, status); sw::count_launch();
+  SW_CHECK_LAUNCH("sw_ragged_remove_row_slots");
   return SW_OK;
 }

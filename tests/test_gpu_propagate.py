@@ -67,3 +67,64 @@ def test_atomic_propagation_dyadic_exact_from_zero(dev_lib):
     out = torch.zeros(N, dtype=torch.float64, device="cuda")
     propagate_spikes(m, syn.planes["g"], torch.from_numpy(spikes).cuda(), out)
     assert np.array_equal(out.cpu().numpy(), ref)
+
+
+def test_single_synapse_edits_match_reference_semantics(dev_lib):
+    """add_synapse / remove_synapse / remove_slots (connectivity.py:91-136)
+    against the oracle on a random operation sequence; the reference's own
+    known answers (pkg/tests/test_connectivity.py:54-61: [2,0,3] remove slot
+    0 -> [3,0]) included."""
+    from oracle.ragged import Ragged
+    from paper_2510_19764_b200.connectivity import (RaggedMatrix, SynVarMatrix, add_synapse,
+                                                    remove_slots, remove_synapse)
+    from paper_2510_19764_b200.errors import DuplicateEdge, RowFull, SlotOutOfRange
+    m = RaggedMatrix(3, 5, 4)
+    syn = SynVarMatrix(m, ("g",))
+    for post in (2, 0, 3):
+        add_synapse(m, syn, 0, post, {"g": float(post)})
+    remove_synapse(m, syn, 0, 0)
+    assert m.row_targets(0).cpu().tolist() == [3, 0]
+    assert syn.planes["g"][0, :2].cpu().tolist() == [3.0, 0.0]
+    with pytest.raises(DuplicateEdge):
+        add_synapse(m, syn, 0, 3)
+    with pytest.raises(SlotOutOfRange):
+        remove_synapse(m, syn, 0, 2)
+
+    rs = np.random.default_rng(9)
+    P, N, cap = 20, 30, 12
+    m = RaggedMatrix(P, N, cap)
+    syn = SynVarMatrix(m, ("w", "g"))
+    o = Ragged(P, N, cap, ("w", "g"))
+    for _ in range(600):
+        i = int(rs.integers(P))
+        op = rs.random()
+        if op < 0.55:
+            j = int(rs.integers(N))
+            v = {"w": float(rs.standard_normal())}
+            err_o = err_d = None
+            try:
+                so = o.add_synapse(i, j, v)
+            except Exception as e:   # oracle RowFull / DuplicateEdge
+                err_o = type(e).__name__
+            try:
+                sd = add_synapse(m, syn, i, j, v)
+            except (RowFull, DuplicateEdge) as e:
+                err_d = type(e).__name__
+            assert (err_o is None) == (err_d is None)
+            if err_o is None:
+                assert so == sd
+        elif op < 0.8 and o.row_length[i] > 0:
+            s = int(rs.integers(o.row_length[i]))
+            o.remove_synapse(i, s)
+            remove_synapse(m, syn, i, s)
+        elif o.row_length[i] > 0:
+            k = int(rs.integers(1, o.row_length[i] + 1))
+            sl = rs.choice(int(o.row_length[i]), size=k, replace=False)
+            o.remove_slots(i, sl)
+            remove_slots(m, syn, i, sl)
+    rl = o.row_length
+    assert np.array_equal(m.row_length.cpu().numpy(), rl)
+    mask = np.arange(cap)[None, :] < rl[:, None]
+    assert np.array_equal(m.target.cpu().numpy()[mask], o.target[mask])
+    for p in ("w", "g"):
+        assert np.array_equal(syn.planes[p].cpu().numpy()[mask], o.planes[p][mask])
