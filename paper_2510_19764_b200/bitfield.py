@@ -61,3 +61,66 @@ class Bitfield:
 
     def test_bit(self, i: int, j: int) -> bool:
         return bool((int(self.words[i, j >> 6].item()) >> (j & 63)) & 1)
+
+    # -- the rest of the reference Bitfield API (bitfield.py:32-90), as
+    #    vectorised device ops on the int64 word view --------------------------
+    @staticmethod
+    def _word_masks(cols) -> tuple[np.ndarray, np.ndarray]:
+        """Unique word indices and the OR of the bits each of them gets."""
+        cols = np.asarray(cols, dtype=np.int64).reshape(-1)
+        words = cols >> 6
+        uw, inv = np.unique(words, return_inverse=True)
+        masks = np.zeros(uw.size, dtype=np.uint64)
+        np.bitwise_or.at(masks, inv, np.uint64(1) << (cols & 63).astype(np.uint64))
+        return uw, masks.view(np.int64)
+
+    def set_bit(self, i: int, j: int) -> None:
+        self.set_bits(i, [j])
+
+    def clear_bit(self, i: int, j: int) -> None:
+        self.clear_bits(i, [j])
+
+    def set_bits(self, i: int, cols) -> None:
+        uw, m = self._word_masks(cols)
+        if uw.size:
+            idx = torch.from_numpy(uw).to(self.words.device)
+            self.words[i, idx] |= torch.from_numpy(m).to(self.words.device)
+
+    def clear_bits(self, i: int, cols) -> None:
+        uw, m = self._word_masks(cols)
+        if uw.size:
+            idx = torch.from_numpy(uw).to(self.words.device)
+            self.words[i, idx] &= ~torch.from_numpy(m).to(self.words.device)
+
+    def test_bits(self, i: int, cols) -> np.ndarray:
+        cols = torch.as_tensor(np.asarray(cols, dtype=np.int64)).to(self.words.device)
+        return ((self.words[i, cols >> 6] >> (cols & 63)) & 1).bool().cpu().numpy()
+
+    def test_bits_rows(self, rows_cols: np.ndarray) -> np.ndarray:
+        """Test bit (r, rows_cols[r, c]) for a full column-index matrix."""
+        rc = torch.as_tensor(np.asarray(rows_cols, dtype=np.int64)).to(self.words.device)
+        w = torch.gather(self.words, 1, rc >> 6)
+        return ((w >> (rc & 63)) & 1).bool().cpu().numpy()
+
+    def clear_row(self, i: int) -> None:
+        self.words[i].zero_()
+
+    def set_k_random_bits_in_row(self, i: int, k: int, rng: CounterRng) -> np.ndarray:
+        """Exactly k distinct bits, in the reference's draw order (bitfield.py:67-77)."""
+        from .errors import KTooLarge
+        if k > self.num_post:
+            raise KTooLarge(f"k={k} exceeds row width {self.num_post}")
+        cols = rng.sample_k_distinct(k, self.num_post)
+        if k:
+            self.set_bits(i, cols)
+        return cols
+
+    def set_bits_in_row(self, i: int) -> np.ndarray:
+        """Ascending column indices of all set bits in row i."""
+        row = self.words[i].cpu().numpy().view(np.uint64)
+        bits = (row[:, None] >> np.arange(64, dtype=np.uint64)[None, :]) & np.uint64(1)
+        idx = np.flatnonzero(bits.ravel())
+        return idx[idx < self.num_post]
+
+    def row_popcount(self, i: int) -> int:
+        return int(self.set_bits_in_row(i).size)
