@@ -17,14 +17,16 @@
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
+// k_clf_step is instantiated for 256 and 512 threads per replica block
+// (512 pays off for the 1024-hidden layer, 256 for the 256-hidden one)
+constexpr int kThreads = 256;             // auxiliary kernels
 
 constexpr int kStageCap = 2048;   // staged (target, w) entries of the spiking rows
 constexpr int kPerThread = 8;     // (NI + H) <= kThreads * kPerThread
 
 // Block-wide exclusive scan of two ints (count, length-sum); returns the
 // exclusive prefixes for this thread and the totals.
+template <int kWarps>
 __device__ __forceinline__ void block_scan2(int a, int b, int& ea, int& eb, int& ta, int& tb,
                                             int2* wsum) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -60,7 +62,9 @@ __device__ long long g_clf_prof[16];
 #define PROF(i) do { } while (0)
 #endif
 
+template <int kThreads>
 __global__ void __launch_bounds__(kThreads) k_clf_step(sw_clf_step_t P) {
+  constexpr int kWarps = kThreads / 32;
   extern __shared__ unsigned char smem_raw[];
   const int H = P.hidden, NI = P.num_inputs, C = P.num_classes;
   const int NT = NI + H;
@@ -146,7 +150,7 @@ __global__ void __launch_bounds__(kThreads) k_clf_step(sw_clf_step_t P) {
   for (int j = 0; j < per; ++j)
     if ((flags >> j) & 1u) { ++cnt; lsum += rlen[x0 + j]; }
   int ec, el, tc, tl;
-  block_scan2(cnt, lsum, ec, el, tc, tl, wsum);
+  block_scan2<kWarps>(cnt, lsum, ec, el, tc, tl, wsum);
   for (int j = 0; j < per; ++j) {
     if ((flags >> j) & 1u) {
       list[ec] = x0 + j;
@@ -237,7 +241,7 @@ __global__ void __launch_bounds__(kThreads) k_clf_step(sw_clf_step_t P) {
     int loc = 0;
     for (int j = 0; j < kper; ++j) if (k0 + j < NK) loc += kcur[k0 + j];
     int ex, dummy_e, tot, dummy_t;
-    block_scan2(loc, 0, ex, dummy_e, tot, dummy_t, wsum);
+    block_scan2<kWarps>(loc, 0, ex, dummy_e, tot, dummy_t, wsum);
     for (int j = 0; j < kper; ++j) {
       if (k0 + j < NK) {
         const int c = kcur[k0 + j];
@@ -442,11 +446,17 @@ extern "C" int sw_clf_step(const sw_clf_step_t* p, void* stream) {
   }
   const size_t smem = (size_t)(2 * H) * 4 + (size_t)(NI + H) * 8 + (size_t)(NI + H + 1) * 4 +
                       (size_t)kStageCap * 16 + (size_t)(4 * H + 1) * 4 + 16 + (size_t)2 * C * 8;
-  if (smem > 48 * 1024) {
-    if (smem > 227 * 1024) { sw::set_last_error("clf_step: layer too large"); return SW_ERR_INVALID_ARG; }
-    cudaFuncSetAttribute((const void*)k_clf_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 227 * 1024) { sw::set_last_error("clf_step: layer too large"); return SW_ERR_INVALID_ARG; }
+  if (p->hidden >= 512) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute((const void*)k_clf_step<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_clf_step<512><<<p->batch, 512, smem, (cudaStream_t)stream>>>(*p);
+  } else {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute((const void*)k_clf_step<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_clf_step<256><<<p->batch, 256, smem, (cudaStream_t)stream>>>(*p);
   }
-  k_clf_step<<<p->batch, kThreads, smem, (cudaStream_t)stream>>>(*p); sw::count_launch();
+  sw::count_launch();
   SW_CHECK_LAUNCH("sw_clf_step");
   return SW_OK;
 }
