@@ -52,7 +52,7 @@ constexpr int kCB = 32;                   // replicas per stage
 #define SW_EPROP_STAGES 4
 #endif
 #ifndef SW_EPROP_MINB
-#define SW_EPROP_MINB 1
+#define SW_EPROP_MINB 4
 #endif
 #ifndef SW_EPROP_COMPUTE
 #define SW_EPROP_COMPUTE 4
@@ -230,27 +230,50 @@ k_eprop_fused(Seg s0, Seg s1, const float* __restrict__ psi, const float* __rest
         const int nb = min(kCB, B - ch * kCB);
         const int bl0 = cw * kBPW;
         float zb[kBPW], p[kBPW], l[kBPW];
-#pragma unroll
-        for (int q = 0; q < kBPW; ++q) {
-          const int bl = bl0 + q;
-          if (bl < nb) {
-            const int64_t b = (int64_t)ch * kCB + bl;
-            zb[q] = __ldg(trace + b * P + pre);
-            p[q] = __ldg(psi + b * H + post);
-            l[q] = __ldg(lsig + b * H + post);
-          }
-        }
+        // per-stage base pointers; replica q of this warp is one row further
+        const int64_t b0 = (int64_t)ch * kCB + bl0;
+        const float* trp = trace + b0 * P + pre;
+        const float* psp = psi + b0 * H + post;
+        const float* lsp = lsig + b0 * H + post;
         Stage& st = S.st[slot];
+        if (bl0 + kBPW <= nb) {
+          // full chunk: no per-replica guards
 #pragma unroll
-        for (int q = 0; q < kBPW; ++q) {
-          const int bl = bl0 + q;
-          if (bl < nb) {
+          for (int q = 0; q < kBPW; ++q) {
+            zb[q] = __ldg(trp + q * P);
+            p[q] = __ldg(psp + q * H);
+            l[q] = __ldg(lsp + q * H);
+          }
+#pragma unroll
+          for (int q = 0; q < kBPW; ++q) {
+            const int bl = bl0 + q;
             const float ep = st.eps[bl][lane];
             const float ee = __fmul_rn(p[q], __fsub_rn(zb[q], __fmul_rn(beta, ep)));
             const float ebn = __fadd_rn(__fmul_rn(alpha, st.ebar[bl][lane]), ee);
             st.ebar[bl][lane] = ebn;
             st.eps[bl][lane] = __fadd_rn(__fmul_rn(rho, ep), ee);
             st.terms[bl][lane] = __fmul_rn(l[q], ebn);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < kBPW; ++q) {
+            if (bl0 + q < nb) {
+              zb[q] = __ldg(trp + q * P);
+              p[q] = __ldg(psp + q * H);
+              l[q] = __ldg(lsp + q * H);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kBPW; ++q) {
+            const int bl = bl0 + q;
+            if (bl < nb) {
+              const float ep = st.eps[bl][lane];
+              const float ee = __fmul_rn(p[q], __fsub_rn(zb[q], __fmul_rn(beta, ep)));
+              const float ebn = __fadd_rn(__fmul_rn(alpha, st.ebar[bl][lane]), ee);
+              st.ebar[bl][lane] = ebn;
+              st.eps[bl][lane] = __fadd_rn(__fmul_rn(rho, ep), ee);
+              st.terms[bl][lane] = __fmul_rn(l[q], ebn);
+            }
           }
         }
         sw::fence_proxy_async_smem();
