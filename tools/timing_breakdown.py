@@ -37,7 +37,9 @@ prm = tr._step_params(5)
 print("clf_step us", 1000 * timeit(lambda: _lib.call("sw_clf_step", ctypes.byref(prm), st), 200))
 p = tr.params
 a32, r32, b32 = (float(np.float32(x)) for x in (p.alpha, p.rho, p.beta))
-segs = tr._segs
+segs = (_lib.EpropSeg * 2)()
+segs[0] = tr.plan_in.seg(tr.xbar)
+segs[1] = tr.plan_rec.seg(tr.zbar)
 ep = lambda: _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 2,
                        tr.psi.data_ptr(), tr.lsig.data_ptr(), tr.local_b, tr.hidden, b32, r32,
                        a32, tr.d.data_ptr(), tr.zbar.data_ptr(), tr.g_w_out.data_ptr(),
