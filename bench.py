@@ -396,39 +396,39 @@ def run_device(args, w):
 
     ms_dev, eager_dev, steps_dev, clocks = timed(run_resident, "resident")
     ms_e2e, _, _, clocks_e2e = timed(run_e2e, "e2e")
-    # graph kernels per trial: 2 per timestep (clf_step + fused e-prop)
-    graph_kernels = 2 * steps_dev
+    # graph kernels per trial: one forward pass per timestep + one e-prop
+    # pass per EPROP_BLOCK_STEPS timesteps
+    graph_kernels = steps_dev * tr.kernels_per_trial() // w["steps"]
     launches_per_step = (eager_dev + graph_kernels) / args.steps
 
-    # ---- roofline of the dominant kernel (fused e-prop step), timed live
+    # ---- roofline of the dominant kernel (one temporally blocked e-prop
+    # pass over K timesteps on the trainer's live state), timed live
     import ctypes
+    from paper_2510_19764_b200.classifier import EPROP_BLOCK_STEPS as K
     p = tr.params
     a32, r32, b32 = (float(np.float32(x)) for x in (p.alpha, p.rho, p.beta))
-    segs = (_lib.EpropSeg * 2)()
-    segs[0] = tr.plan_in.seg(tr.xbar)
-    segs[1] = tr.plan_rec.seg(tr.zbar)
     st = torch.cuda.current_stream()
+
+    def eprop_pass():
+        tr._eprop_block(0, K, st.cuda_stream)
     reps = 50
     for _ in range(3):
-        _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 2, tr.psi.data_ptr(),
-                  tr.lsig.data_ptr(), tr.local_b, tr.hidden, b32, r32, a32, tr.d.data_ptr(),
-                  tr.zbar.data_ptr(), tr.g_w_out.data_ptr(), tr.g_b_out.data_ptr(),
-                  w["classes"], 0, _lib.workspace(), st.cuda_stream)
+        eprop_pass()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(st)
     for _ in range(reps):
-        _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 2, tr.psi.data_ptr(),
-                  tr.lsig.data_ptr(), tr.local_b, tr.hidden, b32, r32, a32, tr.d.data_ptr(),
-                  tr.zbar.data_ptr(), tr.g_w_out.data_ptr(), tr.g_b_out.data_ptr(),
-                  w["classes"], 0, _lib.workspace(), st.cuda_stream)
+        eprop_pass()
     e1.record(st)
     e1.synchronize()
     k_ms = e0.elapsed_time(e1) / reps
     E = tr.m_in.edge_count() + tr.m_rec.edge_count()
     Bl = tr.local_b
-    alg_bytes = Bl * E * 16 + E * (16 + 4) + Bl * (w["num_inputs"] + w["hidden"] + 2 * w["hidden"]) * 4
+    # eligibility state read + written once per pass, gradient r/w + plan,
+    # and K steps of per-replica vectors (SURVEY 8(d) E-step with the state
+    # term once per K steps)
+    alg_bytes = Bl * E * 16 + E * (16 + 4) + K * Bl * (w["num_inputs"] + w["hidden"] + 2 * w["hidden"]) * 4
     achieved = alg_bytes / (k_ms * 1e-3) / 1e9
     peak, peak_kind = measured_peak()
     traffic = None
@@ -465,11 +465,13 @@ def run_device(args, w):
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16 + 8 * 4},
             "gpu_launches": int(round(launches_per_step * args.steps)),
             "gpu_launches_per_step": round(launches_per_step, 1),
-            "roofline": {"kernel": "k_eprop_fused (sw_eprop_fused_step)", "bound": "hbm",
+            "roofline": {"kernel": f"k_eprop_block<{K}> (sw_eprop_fused_block, {K} timesteps per pass)",
+                         "bound": "hbm",
                          "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "alg_bytes_per_launch": int(alg_bytes), "kernel_us": round(k_ms * 1e3, 2),
-                         "share_of_step": round(k_ms * w["steps"] / ms_dev, 3)},
+                         "kernel_us_per_timestep": round(k_ms * 1e3 / K, 2),
+                         "share_of_step": round(k_ms * (w["steps"] / K) / ms_dev, 3)},
             "clocks": clocks,
         }
         if cpu is not None:

@@ -225,6 +225,28 @@ SW_API int sw_eprop_fused_step(const sw_eprop_seg_t* segs, int32_t n_segs, const
                                double* g_w_out, double* g_b_out, int32_t num_classes,
                                int32_t max_blocks_per_sm, uint32_t* workspace, void* stream);
 
+/* k consecutive timesteps (1 <= k <= 4) of the fused step in one pass over
+ * the eligibility state (temporal blocking: the forward pass of the k steps
+ * runs first, it never reads eps/ebar/grad).  Per step s < k: psi[s],
+ * lsig[s] [B,H]; pre_trace[seg][s] [B, num_pre]; d[s] [B,C] and zbar[s]
+ * [B,H] for the readout gradients (d[0] == NULL: no readout).  The segment's
+ * own pre_trace field is ignored.  eps/ebar are bit-identical to k calls of
+ * sw_eprop_fused_step; the gradient too for k = 1, and for k > 1 up to the
+ * float64 rounding of adding k per-step partial sums (each in ascending
+ * replica order). */
+typedef struct sw_eprop_block {
+  int32_t k;
+  const float* psi[4];
+  const float* lsig[4];
+  const float* pre_trace[2][4];
+  const double* d[4];
+  const float* zbar[4];
+} sw_eprop_block_t;
+SW_API int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, const sw_eprop_block_t* blk,
+                                int32_t batch, int32_t hidden, float beta, float rho, float alpha,
+                                double* g_w_out, double* g_b_out, int32_t num_classes,
+                                uint32_t* workspace, void* stream);
+
 /* ---- neurons (neurons.py) --------------------------------------------------- */
 /* AlifLayer.step (neurons.py:60-67), float32, n = batch*hidden elements. */
 SW_API int sw_alif_step(float* v, float* a, float* z, const float* rec, const float* ext,

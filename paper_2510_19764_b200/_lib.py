@@ -77,6 +77,12 @@ class EpropSeg(C.Structure):
                 ("grad", P), ("num_pre", I32), ("e_pad", I32)]
 
 
+class EpropBlock(C.Structure):
+    """sw_eprop_block_t"""
+    _fields_ = [("k", I32), ("psi", P * 4), ("lsig", P * 4), ("pre_trace", (P * 4) * 2),
+                ("d", P * 4), ("zbar", P * 4)]
+
+
 class ClfStep(C.Structure):
     """sw_clf_step_t"""
     _fields_ = [("in_row_length", P), ("in_target", P), ("in_w32", P), ("in_stride", I32),
@@ -113,6 +119,7 @@ SIGNATURES: dict[str, list] = {
     "sw_gather_f64": [P, P, I32, P, P],
     "sw_scatter_f64": [P, P, I32, P, P],
     "sw_eprop_fused_step": [C.c_void_p, I32, P, P, I32, I32, F32, F32, F32, P, P, P, P, I32, I32, P, P],
+    "sw_eprop_fused_block": [C.c_void_p, I32, P, I32, I32, F32, F32, F32, P, P, I32, P, P],
     "sw_alif_step": [P, P, P, P, P, I64, F32, F32, F32, F32, P],
     "sw_alif_surrogate": [P, P, P, I64, F32, F32, P],
     "sw_lif_cond_step": [P, P, P, P, I32, I64, F64, F64, F64, F64, F64, F64, F64, F64, I64, P, P],

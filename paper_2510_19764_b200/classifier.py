@@ -30,10 +30,10 @@ from .sharding import allreduce_flat
 from .updates import Model
 
 
-# tile-worker blocks per SM of the e-prop kernel when it shares the SMs with
-# the next step's forward pass (0 = all that fit: measured best, the forward
-# pass fills the slots that workers with fewer tiles release)
-OVERLAP_EPROP_BLOCKS_PER_SM = 0
+# timesteps per e-prop pass over the eligibility state (temporal blocking,
+# sw_eprop_fused_block): K forward steps run first, then one pass applies K
+# recursion steps to every (replica, synapse) element
+EPROP_BLOCK_STEPS = 4
 
 
 @dataclass
@@ -225,22 +225,23 @@ class EpropClassifierTrainer:
         self.v = torch.zeros((B, H), **f32)
         self.a = torch.zeros((B, H), **f32)
         self.z = torch.zeros((B, H), **f32)
-        self.zbar = torch.zeros((B, H), **f32)
-        self.xbar = torch.zeros((B, NI), **f32)
-        self.psi = torch.zeros((B, H), **f32)
-        self.lsig = torch.zeros((B, H), **f32)
-        # timestep-parity twins of the per-step e-prop inputs: step t writes
-        # parity t % 2, so step t+1's forward pass can run while the e-prop
-        # update of step t still reads its traces, psi, lsig and d
-        self.zbar_1 = torch.zeros((B, H), **f32)
-        self.xbar_1 = torch.zeros((B, NI), **f32)
-        self.psi_1 = torch.zeros((B, H), **f32)
-        self.lsig_1 = torch.zeros((B, H), **f32)
+        # per-step e-prop inputs in 2*K rotating slots (K = EPROP_BLOCK_STEPS):
+        # step t writes slot t % 2K.  The e-prop pass over steps [gK, gK+K)
+        # reads one half while the forward passes of the next K steps write
+        # the other half, so both can run at once.
+        K2 = 2 * EPROP_BLOCK_STEPS
+        self._slot_zbar = [torch.zeros((B, H), **f32) for _ in range(K2)]
+        self._slot_xbar = [torch.zeros((B, NI), **f32) for _ in range(K2)]
+        self._slot_psi = [torch.zeros((B, H), **f32) for _ in range(K2)]
+        self._slot_lsig = [torch.zeros((B, H), **f32) for _ in range(K2)]
+        self._slot_d = [torch.zeros((B, C), **f64) for _ in range(K2)]
+        # slot-0 views under the reference attribute names
+        self.zbar, self.xbar = self._slot_zbar[0], self._slot_xbar[0]
+        self.psi, self.lsig = self._slot_psi[0], self._slot_lsig[0]
         self.y = torch.zeros((B, C), **f64)
         self.pi_sum = torch.zeros((B, C), **f64)
         self.loss_b = torch.zeros(B, **f64)
-        self.d = torch.zeros((B, C), **f64)
-        self.d_1 = torch.zeros((B, C), **f64)
+        self.d = self._slot_d[0]
         self.p_in = torch.zeros((B, NI), **f64)
         self.keys = torch.zeros(B, dtype=torch.int64, device="cuda")
         self.labels = torch.zeros(B, dtype=torch.int32, device="cuda")
@@ -253,7 +254,7 @@ class EpropClassifierTrainer:
         self.pin_labels = torch.zeros(B, dtype=torch.int32, pin_memory=True)
         self.plan_in = _Plan(self.m_in, B)
         self.plan_rec = _Plan(self.m_rec, B)
-        self._segs = [(_lib.EpropSeg * 2)(), (_lib.EpropSeg * 2)()]
+        self._segs = (_lib.EpropSeg * 2)()
         _lib.workspace()   # allocate the ticket words outside any graph capture
 
     # -- per-step launches ------------------------------------------------------------
@@ -268,7 +269,7 @@ class EpropClassifierTrainer:
         s.w_out, s.b_out, s.num_classes = self.w_out.data_ptr(), self.b_out.data_ptr(), self.task.num_classes
         s.p_in, s.ex_key, s.labels = self.p_in.data_ptr(), self.keys.data_ptr(), self.labels.data_ptr()
         s.t, s.batch = t, self.local_b
-        cur, prev = self._parity(t), self._parity(t + 1)
+        cur, prev = self._slot(t), self._slot(t - 1)
         s.v, s.a, s.z = (x.data_ptr() for x in (self.v, self.a, self.z))
         s.zbar, s.xbar = cur["zbar"].data_ptr(), cur["xbar"].data_ptr()
         s.zbar_in, s.xbar_in = prev["zbar"].data_ptr(), prev["xbar"].data_ptr()
@@ -279,56 +280,71 @@ class EpropClassifierTrainer:
         s.alpha64 = p.alpha
         return s
 
-    def _parity(self, t: int) -> dict:
-        if t % 2 == 0:
-            return dict(zbar=self.zbar, xbar=self.xbar, psi=self.psi, lsig=self.lsig, d=self.d)
-        return dict(zbar=self.zbar_1, xbar=self.xbar_1, psi=self.psi_1, lsig=self.lsig_1, d=self.d_1)
+    def _slot(self, t: int) -> dict:
+        k = t % (2 * EPROP_BLOCK_STEPS)
+        return dict(zbar=self._slot_zbar[k], xbar=self._slot_xbar[k], psi=self._slot_psi[k],
+                    lsig=self._slot_lsig[k], d=self._slot_d[k])
 
-    def _eprop(self, t: int, st: int, blocks_per_sm: int) -> None:
+    def _eprop_block(self, t0: int, k: int, st: int) -> None:
+        """e-prop of steps t0 .. t0+k-1 in one pass (sw_eprop_fused_block)."""
         p = self.params
         a32, r32, b32 = float(np.float32(p.alpha)), float(np.float32(p.rho)), float(np.float32(p.beta))
-        cur = self._parity(t)
-        segs = self._segs[t % 2]
-        segs[0] = self.plan_in.seg(cur["xbar"])
-        segs[1] = self.plan_rec.seg(cur["zbar"])
-        _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 2,
-                  cur["psi"].data_ptr(), cur["lsig"].data_ptr(), self.local_b, self.hidden,
-                  b32, r32, a32, cur["d"].data_ptr(), cur["zbar"].data_ptr(),
-                  self.g_w_out.data_ptr(), self.g_b_out.data_ptr(),
-                  self.task.num_classes, blocks_per_sm, _lib.workspace(), st)
+        blk = _lib.EpropBlock()
+        blk.k = k
+        for j in range(k):
+            sl = self._slot(t0 + j)
+            blk.psi[j], blk.lsig[j] = sl["psi"].data_ptr(), sl["lsig"].data_ptr()
+            blk.pre_trace[0][j], blk.pre_trace[1][j] = sl["xbar"].data_ptr(), sl["zbar"].data_ptr()
+            blk.d[j], blk.zbar[j] = sl["d"].data_ptr(), sl["zbar"].data_ptr()
+        self._segs[0] = self.plan_in.seg(self.xbar)
+        self._segs[1] = self.plan_rec.seg(self.zbar)
+        _lib.call("sw_eprop_fused_block", ctypes.cast(self._segs, ctypes.c_void_p), 2,
+                  ctypes.byref(blk), self.local_b, self.hidden, b32, r32, a32,
+                  self.g_w_out.data_ptr(), self.g_b_out.data_ptr(), self.task.num_classes,
+                  _lib.workspace(), st)
 
     def _launch_steps(self, learn: bool, overlap: bool = False) -> None:
-        """One trial.  overlap (graph capture only): forward passes on the
-        capturing stream, e-prop updates on a side stream; step t+1's forward
-        pass runs concurrently with step t's e-prop update (the e-prop kernel
-        leaves one block slot per SM free for it), and step t+2's forward pass
-        waits for step t's update (parity buffers)."""
+        """One trial: the forward pass of K = EPROP_BLOCK_STEPS steps, then
+        one e-prop pass over those K steps (temporal blocking).  overlap
+        (graph capture only): forward passes on the capturing stream, e-prop
+        passes on a side stream, so the forward passes of group g+1 run while
+        group g's e-prop pass streams the eligibility state; group g+2's
+        forward passes wait for group g's e-prop (rotating slots)."""
         T = self.task.example_steps
+        K = EPROP_BLOCK_STEPS
+        groups = [(t0, min(K, T - t0)) for t0 in range(0, T, K)]
         if not (learn and overlap):
             st = _lib.stream_ptr()
-            for t in range(T):
-                prm = self._step_params(t)
-                _lib.call("sw_clf_step", ctypes.byref(prm), st)
+            for t0, k in groups:
+                for t in range(t0, t0 + k):
+                    prm = self._step_params(t)
+                    _lib.call("sw_clf_step", ctypes.byref(prm), st)
                 if learn:
-                    self._eprop(t, st, 0)
+                    self._eprop_block(t0, k, st)
             self.steps_launched += T
             return
         main = torch.cuda.current_stream()
         side = self._side_stream
         side.wait_stream(main)
-        fwd_done = [torch.cuda.Event() for _ in range(T)]
-        upd_done = [torch.cuda.Event() for _ in range(T)]
-        for t in range(T):
-            if t >= 2:
-                main.wait_event(upd_done[t - 2])
-            prm = self._step_params(t)
-            _lib.call("sw_clf_step", ctypes.byref(prm), main.cuda_stream)
-            fwd_done[t].record(main)
-            side.wait_event(fwd_done[t])
-            self._eprop(t, side.cuda_stream, OVERLAP_EPROP_BLOCKS_PER_SM)
-            upd_done[t].record(side)
+        fwd_done = [torch.cuda.Event() for _ in groups]
+        upd_done = [torch.cuda.Event() for _ in groups]
+        for g, (t0, k) in enumerate(groups):
+            if g >= 2:
+                main.wait_event(upd_done[g - 2])
+            for t in range(t0, t0 + k):
+                prm = self._step_params(t)
+                _lib.call("sw_clf_step", ctypes.byref(prm), main.cuda_stream)
+            fwd_done[g].record(main)
+            side.wait_event(fwd_done[g])
+            self._eprop_block(t0, k, side.cuda_stream)
+            upd_done[g].record(side)
         main.wait_stream(side)
         self.steps_launched += T
+
+    def kernels_per_trial(self, learn: bool = True) -> int:
+        T = self.task.example_steps
+        groups = -(-T // EPROP_BLOCK_STEPS)
+        return T + (groups if learn else 0)
 
     def _run_trial(self, learn: bool) -> None:
         if not self.use_graph:
@@ -380,8 +396,7 @@ class EpropClassifierTrainer:
                   self.w32_in.numel(), st)
         _lib.call("sw_f64_to_f32", self.s_rec.planes["w"].data_ptr(), self.w32_rec.data_ptr(),
                   self.w32_rec.numel(), st)
-        for x in (self.v, self.a, self.z, self.zbar, self.xbar, self.zbar_1, self.xbar_1, self.y,
-                  self.pi_sum, self.loss_b):
+        for x in [self.v, self.a, self.z, self.y, self.pi_sum, self.loss_b] + self._slot_zbar + self._slot_xbar:
             x.zero_()
         if learn:
             for plan, syn in ((self.plan_in, self.s_in), (self.plan_rec, self.s_rec)):

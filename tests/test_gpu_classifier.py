@@ -184,3 +184,66 @@ def test_overlapped_graph_equals_sequential_steps(dev_lib):
             assert torch.equal(x.planes[p], y.planes[p]), p
     assert torch.equal(a.w_out, b.w_out) and torch.equal(a.g_w_out, b.g_w_out)
     assert a.connectivity_fingerprint() == b.connectivity_fingerprint()
+
+
+@pytest.mark.parametrize("B,P,H,cap,R,k", [(64, 700, 256, 82, 26, 4), (37, 100, 1024, 40, 10, 3),
+                                           (8, 30, 48, 12, 6, 1)])
+def test_blocked_eprop_equals_single_steps(dev_lib, B, P, H, cap, R, k):
+    """sw_eprop_fused_block over k steps == k calls of sw_eprop_fused_step:
+    eps/ebar bit-identical, readout gradients to float64 rounding, the
+    synapse gradient bit-identical for k = 1 and within 1e-13 relative for
+    k > 1 (k per-step partial chains added at the end)."""
+    import ctypes
+    from paper_2510_19764_b200 import _lib
+    from paper_2510_19764_b200.classifier import _Plan
+    from paper_2510_19764_b200.connectivity import RaggedMatrix
+    rs = np.random.default_rng(P + k)
+    tg = np.zeros((P, cap), np.int32)
+    rl = np.zeros(P, np.int32)
+    for i in range(P):
+        n = int(min(cap, rs.poisson(R)))
+        tg[i, :n] = rs.choice(H, size=n, replace=False)
+        rl[i] = n
+    m = RaggedMatrix(P, H, cap)
+    m.load_state(rl, tg)
+    plans = [_Plan(m, B), _Plan(m, B)]
+    for pl in plans:
+        pl.ensure(int(rl.sum()))
+        pl.build()
+        pl.eps.copy_(torch.from_numpy(rs.random(pl.eps.shape).astype(np.float32)).cuda())
+        pl.grad.copy_(torch.from_numpy(rs.standard_normal(pl.grad.shape)).cuda())
+    plans[1].eps.copy_(plans[0].eps)
+    plans[1].ebar.copy_(plans[0].ebar)
+    plans[1].grad.copy_(plans[0].grad)
+    C = 5
+    f = lambda *s: torch.from_numpy(rs.random(s).astype(np.float32)).cuda()
+    steps = [dict(trace=f(B, P) * 2, psi=f(B, H) * 0.5, lsig=f(B, H) - 0.5,
+                  d=torch.from_numpy(rs.standard_normal((B, C))).cuda(), zbar=f(B, H))
+             for _ in range(k)]
+    beta, rho, alpha = (float(np.float32(x)) for x in (0.0174, 0.9995, 0.95))
+    gw = [torch.zeros((C, H), dtype=torch.float64, device="cuda") for _ in range(2)]
+    gb = [torch.zeros(C, dtype=torch.float64, device="cuda") for _ in range(2)]
+    segs = (_lib.EpropSeg * 1)()
+    for s in steps:
+        segs[0] = plans[0].seg(s["trace"])
+        _lib.call("sw_eprop_fused_step", ctypes.cast(segs, ctypes.c_void_p), 1, s["psi"].data_ptr(),
+                  s["lsig"].data_ptr(), B, H, beta, rho, alpha, s["d"].data_ptr(),
+                  s["zbar"].data_ptr(), gw[0].data_ptr(), gb[0].data_ptr(), C, 0,
+                  _lib.workspace(), _lib.stream_ptr())
+    blk = _lib.EpropBlock()
+    blk.k = k
+    for j, s in enumerate(steps):
+        blk.psi[j], blk.lsig[j] = s["psi"].data_ptr(), s["lsig"].data_ptr()
+        blk.pre_trace[0][j] = s["trace"].data_ptr()
+        blk.d[j], blk.zbar[j] = s["d"].data_ptr(), s["zbar"].data_ptr()
+    segs[0] = plans[1].seg(steps[0]["trace"])
+    _lib.call("sw_eprop_fused_block", ctypes.cast(segs, ctypes.c_void_p), 1, ctypes.byref(blk), B, H,
+              beta, rho, alpha, gw[1].data_ptr(), gb[1].data_ptr(), C, _lib.workspace(),
+              _lib.stream_ptr())
+    assert torch.equal(plans[0].eps, plans[1].eps) and torch.equal(plans[0].ebar, plans[1].ebar)
+    if k == 1:
+        assert torch.equal(plans[0].grad, plans[1].grad)
+    else:
+        assert torch.allclose(plans[1].grad, plans[0].grad, rtol=1e-13, atol=1e-13)
+    assert torch.allclose(gw[1], gw[0], rtol=1e-12, atol=1e-12)
+    assert torch.allclose(gb[1], gb[0], rtol=1e-12, atol=1e-12)
