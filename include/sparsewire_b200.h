@@ -241,7 +241,14 @@ typedef struct sw_eprop_block {
   const float* pre_trace[2][4];
   const double* d[4];
   const float* zbar[4];
+  /* optional split readout: ro_scratch of sw_eprop_readout_scratch_bytes(
+   * hidden, num_classes, ro_splits) bytes, ZEROED once by the caller (the
+   * kernel leaves its counters zeroed again); NULL = one block per class and
+   * 32 hidden units.  Both are deterministic. */
+  double* ro_scratch;
+  int32_t ro_splits;
 } sw_eprop_block_t;
+SW_API int64_t sw_eprop_readout_scratch_bytes(int32_t hidden, int32_t num_classes, int32_t splits);
 SW_API int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, const sw_eprop_block_t* blk,
                                 int32_t batch, int32_t hidden, float beta, float rho, float alpha,
                                 double* g_w_out, double* g_b_out, int32_t num_classes,

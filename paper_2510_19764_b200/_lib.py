@@ -80,7 +80,7 @@ class EpropSeg(C.Structure):
 class EpropBlock(C.Structure):
     """sw_eprop_block_t"""
     _fields_ = [("k", I32), ("psi", P * 4), ("lsig", P * 4), ("pre_trace", (P * 4) * 2),
-                ("d", P * 4), ("zbar", P * 4)]
+                ("d", P * 4), ("zbar", P * 4), ("ro_scratch", P), ("ro_splits", I32)]
 
 
 class ClfStep(C.Structure):
@@ -120,6 +120,7 @@ SIGNATURES: dict[str, list] = {
     "sw_scatter_f64": [P, P, I32, P, P],
     "sw_eprop_fused_step": [C.c_void_p, I32, P, P, I32, I32, F32, F32, F32, P, P, P, P, I32, I32, P, P],
     "sw_eprop_fused_block": [C.c_void_p, I32, P, I32, I32, F32, F32, F32, P, P, I32, P, P],
+    "sw_eprop_readout_scratch_bytes": [I32, I32, I32],
     "sw_alif_step": [P, P, P, P, P, I64, F32, F32, F32, F32, P],
     "sw_alif_surrogate": [P, P, P, I64, F32, F32, P],
     "sw_lif_cond_step": [P, P, P, P, I32, I64, F64, F64, F64, F64, F64, F64, F64, F64, I64, P, P],
@@ -166,6 +167,8 @@ def lib():
         fn.restype = C.c_int
     L.sw_propagate_workspace_bytes.argtypes = []
     L.sw_propagate_workspace_bytes.restype = C.c_int64
+    L.sw_eprop_readout_scratch_bytes.argtypes = [I32, I32, I32]
+    L.sw_eprop_readout_scratch_bytes.restype = C.c_int64
     L.sw_launch_count.argtypes = []
     L.sw_launch_count.restype = C.c_longlong
     L.sw_last_error.argtypes = []

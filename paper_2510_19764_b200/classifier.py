@@ -34,6 +34,8 @@ from .updates import Model
 # sw_eprop_fused_block): K forward steps run first, then one pass applies K
 # recursion steps to every (replica, synapse) element
 EPROP_BLOCK_STEPS = 4
+# (step, replica) splits of the readout gradient inside the blocked pass
+READOUT_SPLITS = 32
 
 
 @dataclass
@@ -255,6 +257,10 @@ class EpropClassifierTrainer:
         self.plan_in = _Plan(self.m_in, B)
         self.plan_rec = _Plan(self.m_rec, B)
         self._segs = (_lib.EpropSeg * 2)()
+        # split readout-gradient partials of the blocked e-prop pass
+        self._ro_splits = READOUT_SPLITS
+        nbytes = int(_lib.lib().sw_eprop_readout_scratch_bytes(H, C, self._ro_splits))
+        self._ro_scratch = torch.zeros(nbytes // 8 + 1, **f64)
         _lib.workspace()   # allocate the ticket words outside any graph capture
 
     # -- per-step launches ------------------------------------------------------------
@@ -296,12 +302,27 @@ class EpropClassifierTrainer:
             blk.psi[j], blk.lsig[j] = sl["psi"].data_ptr(), sl["lsig"].data_ptr()
             blk.pre_trace[0][j], blk.pre_trace[1][j] = sl["xbar"].data_ptr(), sl["zbar"].data_ptr()
             blk.d[j], blk.zbar[j] = sl["d"].data_ptr(), sl["zbar"].data_ptr()
+        blk.ro_scratch, blk.ro_splits = self._ro_scratch.data_ptr(), self._ro_splits
         self._segs[0] = self.plan_in.seg(self.xbar)
         self._segs[1] = self.plan_rec.seg(self.zbar)
         _lib.call("sw_eprop_fused_block", ctypes.cast(self._segs, ctypes.c_void_p), 2,
                   ctypes.byref(blk), self.local_b, self.hidden, b32, r32, a32,
                   self.g_w_out.data_ptr(), self.g_b_out.data_ptr(), self.task.num_classes,
                   _lib.workspace(), st)
+
+    def eprop_pass_graph(self, reps: int) -> "torch.cuda.CUDAGraph":
+        """A CUDA graph of `reps` blocked e-prop passes over steps 0..K-1 on
+        the live state (kernel timing without host launch overhead)."""
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                st = torch.cuda.current_stream().cuda_stream
+                for _ in range(reps):
+                    self._eprop_block(0, EPROP_BLOCK_STEPS, st)
+        torch.cuda.current_stream().wait_stream(side)
+        return g
 
     def _launch_steps(self, learn: bool, overlap: bool = False) -> None:
         """One trial: the forward pass of K = EPROP_BLOCK_STEPS steps, then

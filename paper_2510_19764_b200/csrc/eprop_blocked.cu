@@ -7,9 +7,10 @@
 // and this kernel then streams every (tile, replica-chunk) of eps/ebar through
 // shared memory once for all k steps.  That is 1/k of the HBM traffic of k
 // single-step passes.  The pipeline is the one of eprop_fused.cu:
-//   warp 0      TMA loader (eps/ebar bulk copies, 3-stage mbarrier ring);
-//   warps 2..5  k recursion steps per element, in shared memory; float32
-//               gradient terms per step;
+//   warp 0      TMA loader (eps/ebar bulk copies, NS-stage mbarrier ring);
+//   warps 2..9  k recursion steps per element, in shared memory; float32
+//               gradient terms per step into a separate NT-deep ring (so
+//               most of the shared memory holds eps/ebar in flight);
 //   warp 1      bulk store, and k float64 chains per synapse.  Chain 0
 //               continues from the gradient, chains 1..k-1 start at zero, and
 //               each chain adds its step's terms in ascending replica order.
@@ -18,20 +19,27 @@
 // equals the sequential sum for k = 1; for k > 1 it differs only in the
 // float64 rounding of that final combination of partial chains.
 // Readout gradients (classifier.py:221-222) for the k steps are reduced by
-// extra blocks of the same launch.
+// extra blocks of the same launch, placed after the streaming workers so
+// they fill the SMs idle in the tile-granular tail.
+// Timing notes (C1, one B200, graph replay, 4 steps): streaming alone 35 us
+// (88 % of the eps/ebar HBM bytes at the measured peak); the full pass ~98 us:
+// the per-element recursion, the K*3 gathers per element and the float64
+// chains add ~63 us on top (latency/issue bound).
 #include "common.cuh"
 #include "sm100_async.cuh"
+
+#include <cstdio>
+#include <cstdlib>
 
 namespace {
 
 constexpr int kMaxK = 4;
-constexpr int kCB = 32;        // replicas per stage
-constexpr int kStages = 3;
-constexpr int kCompute = 4;
-constexpr int kWarps = kCompute + 2;
-constexpr int kThreads = kWarps * 32;
-constexpr int kBPW = kCB / kCompute;
+#ifndef SW_EPB_UNROLL
+#define SW_EPB_UNROLL 1
+#endif
+constexpr int kEpbUnroll = SW_EPB_UNROLL;
 constexpr int kRowBytes = 32 * 4;
+constexpr int kMaxWarps = 10;  // readout blocks: all warps of the block split the batch (NC <= 8)
 
 struct SegB {
   const int32_t* pre;
@@ -49,35 +57,47 @@ struct StepsB {
   const float* lsig[kMaxK];
   const double* d[kMaxK];      // [B, C] per step (readout)
   const float* zbar[kMaxK];    // [B, H] per step (readout)
+  double* ro_scratch;          // split readout partials (NULL: block per class and h-tile)
+  int ro_splits;
   int k;
 };
 
-template <int K>
+// CB replicas per stage, NS stages
+template <int K, int CB>
 struct Stage {
-  float eps[kCB][32];
-  float ebar[kCB][32];
-  float terms[K][kCB][32];
+  float eps[CB][32];
+  float ebar[CB][32];
 };
 
-template <int K>
+// NS eps/ebar stages (held until their bulk store has read them) and a
+// separate ring of NT gradient-term buffers (held only until the chain warp
+// has added them), so that most of the shared memory holds eps/ebar bytes in
+// flight
+template <int K, int CB, int NS, int NT>
 struct Smem {
-  Stage<K> st[kStages];
-  uint64_t full[kStages];
-  uint64_t ready[kStages];
-  uint64_t freed[kStages];
-  int tile[kStages];
-  int ch[kStages];
+  Stage<K, CB> st[NS];
+  float terms[NT][K][CB][32];
+  uint64_t full[NS];
+  uint64_t ready[NS];
+  uint64_t freed[NS];
+  uint64_t tfree[NT];
+  int tile[NS];
+  int ch[NS];
 };
 
+// part/partb: kMaxWarps*33 + kMaxWarps doubles of the block's dynamic shared
+// memory (the streaming blocks' stage ring; no static shared memory, which
+// would cost the streaming blocks occupancy)
 __device__ void readout_block_k(int r, int B, int H, const StepsB& sp, double* g_w_out, double* g_b_out,
-                                int C) {
-  __shared__ double part[kWarps][33];
-  __shared__ double partb[kWarps];
+                                int C, double* scratch) {
+  double (*part)[33] = reinterpret_cast<double (*)[33]>(scratch);
+  double* partb = scratch + kMaxWarps * 33;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
   const int htiles = (H + 31) / 32;
   const int c = r / htiles, h = (r % htiles) * 32 + lane;
   double acc = 0.0, accb = 0.0;
-  const int per = (B + kWarps - 1) / kWarps;
+  const int per = (B + nw - 1) / nw;
   const int b0 = warp * per, b1 = min(B, b0 + per);
   for (int k = 0; k < sp.k; ++k) {
     const double* d = sp.d[k];
@@ -103,12 +123,113 @@ __device__ void readout_block_k(int r, int B, int H, const StepsB& sp, double* g
   __syncthreads();
   if (warp == 0) {
     double t = 0.0;
-    for (int w = 0; w < kWarps; ++w) t = __dadd_rn(t, part[w][lane]);
+    for (int w = 0; w < nw; ++w) t = __dadd_rn(t, part[w][lane]);
     if (h < H) g_w_out[(int64_t)c * H + h] += t;
     if (lane == 0 && (r % htiles) == 0) {
       double tb = 0.0;
-      for (int w = 0; w < kWarps; ++w) tb = __dadd_rn(tb, partb[w]);
+      for (int w = 0; w < nw; ++w) tb = __dadd_rn(tb, partb[w]);
       g_b_out[c] += tb;
+    }
+  }
+}
+
+// Split readout (sp.ro_scratch != NULL): block r = (h-tile, group of kRoCG
+// classes, split s of the k*B (step, replica) pairs).  Lane = h, kRoCG float64
+// accumulators; the warps of the block take consecutive pair ranges and are
+// combined in warp order.  The block writes its partial to
+//   partial[s][c][h]  (ro_scratch[0 : S*C*H]),  partial_b[s][c] (next S*C),
+// and the last block of its (h-tile, class group) -- counters after the
+// partials, zeroed by the caller and reset here -- adds the S partials in
+// split order to g_w_out / g_b_out.  Deterministic; the (step, replica)
+// summation order differs from the single-step kernel only in its grouping.
+constexpr int kRoCG = 4;
+constexpr int kRoU = 2;
+
+__device__ void readout_split(int r, int B, int H, const StepsB& sp, double* g_w_out, double* g_b_out,
+                              int C, double* smem) {
+  double (*part)[kRoCG][32] = reinterpret_cast<double (*)[kRoCG][32]>(smem);
+  double (*partb)[kRoCG] = reinterpret_cast<double (*)[kRoCG]>(smem + kMaxWarps * kRoCG * 32);
+  unsigned* flag = reinterpret_cast<unsigned*>(smem + kMaxWarps * kRoCG * 33);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  const int S = sp.ro_splits;
+  const int ncg = (C + kRoCG - 1) / kRoCG;
+  const int sidx = r % S, grp = r / S;
+  const int cg = grp % ncg, ht = grp / ncg;
+  const int h = ht * 32 + lane, c0 = cg * kRoCG;
+  const int pairs = sp.k * B;
+  const int p0 = (int)((int64_t)pairs * sidx / S), p1 = (int)((int64_t)pairs * (sidx + 1) / S);
+  const int per = (p1 - p0 + nw - 1) / nw;
+  const int w0 = p0 + warp * per, w1 = min(p1, w0 + per);
+  double acc[kRoCG], accb[kRoCG];
+#pragma unroll
+  for (int c = 0; c < kRoCG; ++c) acc[c] = accb[c] = 0.0;
+  for (int j = w0; j < w1; j += kRoU) {
+    float zv[kRoU];
+    double dv[kRoU][kRoCG];
+#pragma unroll
+    for (int u = 0; u < kRoU; ++u) {
+      const int jj = min(j + u, w1 - 1);
+      const int q = jj / B, b = jj - q * B;
+      zv[u] = h < H ? __ldg(sp.zbar[q] + (int64_t)b * H + h) : 0.0f;
+#pragma unroll
+      for (int c = 0; c < kRoCG; ++c)
+        dv[u][c] = c0 + c < C ? __ldg(sp.d[q] + (int64_t)b * C + c0 + c) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kRoU; ++u) {
+      if (j + u < w1) {
+#pragma unroll
+        for (int c = 0; c < kRoCG; ++c) {
+          acc[c] = __dadd_rn(acc[c], __dmul_rn(dv[u][c], (double)zv[u]));
+          accb[c] = __dadd_rn(accb[c], dv[u][c]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kRoCG; ++c) part[warp][c][lane] = acc[c];
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < kRoCG; ++c) partb[warp][c] = accb[c];
+  }
+  __syncthreads();
+  double* partial = sp.ro_scratch;
+  double* partial_b = partial + (int64_t)S * C * H;
+  unsigned* cnt = reinterpret_cast<unsigned*>(partial_b + (int64_t)S * C);
+  if (warp == 0) {
+#pragma unroll
+    for (int c = 0; c < kRoCG; ++c) {
+      double t = 0.0;
+      for (int w = 0; w < nw; ++w) t = __dadd_rn(t, part[w][c][lane]);
+      if (c0 + c < C && h < H) partial[((int64_t)sidx * C + c0 + c) * H + h] = t;
+      if (lane == 0 && c0 + c < C) {
+        double tb = 0.0;
+        for (int w = 0; w < nw; ++w) tb = __dadd_rn(tb, partb[w][c]);
+        partial_b[(int64_t)sidx * C + c0 + c] = tb;
+      }
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) *flag = atomicAdd(&cnt[grp], 1u);
+    __syncwarp();
+    if (*flag == (unsigned)(S - 1)) {
+      __threadfence();
+#pragma unroll
+      for (int c = 0; c < kRoCG; ++c) {
+        if (c0 + c >= C) continue;
+        if (h < H) {
+          double t = 0.0;
+          for (int x = 0; x < S; ++x) t = __dadd_rn(t, __ldcg(partial + ((int64_t)x * C + c0 + c) * H + h));
+          g_w_out[(int64_t)(c0 + c) * H + h] += t;
+        }
+        if (ht == 0 && lane == 0) {
+          double tb = 0.0;
+          for (int x = 0; x < S; ++x) tb = __dadd_rn(tb, __ldcg(partial_b + (int64_t)x * C + c0 + c));
+          g_b_out[c0 + c] += tb;
+        }
+      }
+      if (lane == 0) cnt[grp] = 0u;
     }
   }
 }
@@ -119,24 +240,38 @@ __device__ __forceinline__ const SegB& seg_of(const SegB& s0, const SegB& s1, in
   return s1;
 }
 
-template <int K>
-__global__ void __launch_bounds__(kThreads, 3)
+// resident blocks per SM that the stage ring leaves room for (<= 3): the
+// register budget of __launch_bounds__
+template <int K, int CB, int NS, int NT>
+constexpr int smem_blocks() {
+  constexpr int per = (int)sizeof(Smem<K, CB, NS, NT>) + 1024 + 2 * 1024;
+  return (233472 / per) < 3 ? ((233472 / per) < 1 ? 1 : 233472 / per) : 3;
+}
+
+template <int K, int NC, int U, int NS, int CB, int NT>
+__global__ void __launch_bounds__((NC + 2) * 32, smem_blocks<K, CB, NS, NT>())
 k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, float alpha,
-              double* g_w_out, double* g_b_out, int C, int ro_blocks, unsigned* tickets) {
+              double* g_w_out, double* g_b_out, int C, int workers, unsigned* tickets) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Smem<K>& S = *reinterpret_cast<Smem<K>*>(smem_raw);
+  Smem<K, CB, NS, NT>& S = *reinterpret_cast<Smem<K, CB, NS, NT>*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if ((int)blockIdx.x < ro_blocks) {
-    readout_block_k(blockIdx.x, B, H, sp, g_w_out, g_b_out, C);
+  // readout blocks come after the streaming workers: they fill the SMs that
+  // the tile-granular streaming work leaves idle at its end
+  if ((int)blockIdx.x >= workers) {
+    if (sp.ro_scratch)
+      readout_split(blockIdx.x - workers, B, H, sp, g_w_out, g_b_out, C, reinterpret_cast<double*>(smem_raw));
+    else
+      readout_block_k(blockIdx.x - workers, B, H, sp, g_w_out, g_b_out, C, reinterpret_cast<double*>(smem_raw));
   } else {
     const int tiles = s0.tiles + s1.tiles;
-    const int nch = (B + kCB - 1) / kCB;
+    const int nch = (B + CB - 1) / CB;
     if (threadIdx.x == 0) {
-      for (int s = 0; s < kStages; ++s) {
+      for (int s = 0; s < NS; ++s) {
         sw::mbar_init(&S.full[s], 1);
-        sw::mbar_init(&S.ready[s], kCompute);
+        sw::mbar_init(&S.ready[s], NC);
         sw::mbar_init(&S.freed[s], 1);
       }
+      for (int s = 0; s < NT; ++s) sw::mbar_init(&S.tfree[s], 1);
       sw::fence_mbar_init();
     }
     __syncthreads();
@@ -148,8 +283,8 @@ k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, 
         while (true) {
           const int tile = (int)atomicAdd(&tickets[0], 1u);
           if (tile >= tiles) {
-            const int slot = k % kStages;
-            if (k >= kStages) sw::mbar_wait(&S.freed[slot], ((k / kStages) - 1) & 1);
+            const int slot = k % NS;
+            if (k >= NS) sw::mbar_wait(&S.freed[slot], ((k / NS) - 1) & 1);
             S.tile[slot] = -1;
             sw::mbar_arrive(&S.full[slot]);
             break;
@@ -157,13 +292,13 @@ k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, 
           int lt;
           const SegB& sg = seg_of(s0, s1, tile, lt);
           for (int ch = 0; ch < nch; ++ch, ++k) {
-            const int slot = k % kStages;
-            if (k >= kStages) sw::mbar_wait(&S.freed[slot], ((k / kStages) - 1) & 1);
+            const int slot = k % NS;
+            if (k >= NS) sw::mbar_wait(&S.freed[slot], ((k / NS) - 1) & 1);
             S.tile[slot] = tile;
             S.ch[slot] = ch;
-            const int nb = min(kCB, B - ch * kCB);
+            const int nb = min(CB, B - ch * CB);
             const uint32_t bytes = (uint32_t)nb * kRowBytes;
-            const int64_t off = ((int64_t)lt * B + (int64_t)ch * kCB) * 32;
+            const int64_t off = ((int64_t)lt * B + (int64_t)ch * CB) * 32;
             sw::mbar_arrive_expect_tx(&S.full[slot], 2 * bytes);
             sw::bulk_g2s_hint(&S.st[slot].eps[0][0], sg.eps + off, bytes, &S.full[slot], pol);
             sw::bulk_g2s_hint(&S.st[slot].ebar[0][0], sg.ebar + off, bytes, &S.full[slot], pol);
@@ -175,8 +310,8 @@ k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, 
       double acc[K];
       const uint64_t pol = sw::policy_evict_first();
       for (uint32_t kk = 0;; ++kk) {
-        const int slot = kk % kStages;
-        const uint32_t par = (kk / kStages) & 1;
+        const int slot = kk % NS;
+        const uint32_t par = (kk / NS) & 1;
         sw::mbar_wait(&S.full[slot], par);
         const int tile = S.tile[slot];
         if (tile < 0) break;
@@ -184,9 +319,9 @@ k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, 
         sw::mbar_wait(&S.ready[slot], par);
         int lt;
         const SegB& sg = seg_of(s0, s1, tile, lt);
-        const int nb = min(kCB, B - ch * kCB);
+        const int nb = min(CB, B - ch * CB);
         if (lane == 0) {
-          const int64_t off = ((int64_t)lt * B + (int64_t)ch * kCB) * 32;
+          const int64_t off = ((int64_t)lt * B + (int64_t)ch * CB) * 32;
           sw::bulk_s2g_hint(sg.eps + off, &S.st[slot].eps[0][0], (uint32_t)nb * kRowBytes, pol);
           sw::bulk_s2g_hint(sg.ebar + off, &S.st[slot].ebar[0][0], (uint32_t)nb * kRowBytes, pol);
           sw::bulk_commit();
@@ -197,17 +332,18 @@ k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, 
 #pragma unroll
           for (int q = 1; q < K; ++q) acc[q] = 0.0;
         }
-        const Stage<K>& st = S.st[slot];
+        const float (*terms)[CB][32] = S.terms[kk % NT];
         for (int r = 0; r < nb; ++r) {
 #pragma unroll
           for (int q = 0; q < K; ++q)
-            if (q < sp.k) acc[q] = __dadd_rn(acc[q], (double)st.terms[q][r][lane]);
+            acc[q] = __dadd_rn(acc[q], (double)terms[q][r][lane]);
         }
+        __syncwarp();
+        if (lane == 0) sw::mbar_arrive(&S.tfree[kk % NT]);
         if (ch == nch - 1) {
           double g = acc[0];
 #pragma unroll
-          for (int q = 1; q < K; ++q)
-            if (q < sp.k) g = __dadd_rn(g, acc[q]);
+          for (int q = 1; q < K; ++q) g = __dadd_rn(g, acc[q]);
           sg.grad[e] = g;
         }
         if (lane == 0) sw::bulk_wait_read0();
@@ -218,12 +354,13 @@ k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, 
     } else {
       // ---------------- compute: k recursion steps per element ----------------
       const int cw = warp - 2;
+      constexpr int kBPW = CB / NC;
       const int bl0 = cw * kBPW;
       int cur_tile = -1, pre = 0, post = 0, P = 0;
       const float* trace[K];
       for (uint32_t kk = 0;; ++kk) {
-        const int slot = kk % kStages;
-        const uint32_t par = (kk / kStages) & 1;
+        const int slot = kk % NS;
+        const uint32_t par = (kk / NS) & 1;
         sw::mbar_wait(&S.full[slot], par);
         const int tile = S.tile[slot];
         if (tile < 0) break;
@@ -238,34 +375,45 @@ k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, 
           P = sg.P;
           cur_tile = tile;
         }
-        const int nb = min(kCB, B - ch * kCB);
-        Stage<K>& st = S.st[slot];
-        for (int u = 0; u < kBPW; ++u) {
-          const int bl = bl0 + u;
-          if (bl >= nb) break;
-          const int64_t b = (int64_t)ch * kCB + bl;
-          float zb[K], p[K], l[K];
+        const int nb = min(CB, B - ch * CB);
+        Stage<K, CB>& st = S.st[slot];
+        float (*terms)[CB][32] = S.terms[kk % NT];
+        if (kk >= (uint32_t)NT) sw::mbar_wait(&S.tfree[kk % NT], ((kk / NT) - 1) & 1);
+        // K is the exact step count (one instantiation per k), so the K
+        // gathers of a replica are issued together ahead of the recursion;
+        // 32-bit element offsets, one per replica for all K steps
+#pragma unroll kEpbUnroll
+        for (int u0 = 0; u0 < kBPW; u0 += U) {
+          float zb[U][K], p[U][K], l[U][K];
 #pragma unroll
-          for (int q = 0; q < K; ++q) {
-            if (q < sp.k) {
-              zb[q] = __ldg(trace[q] + b * P + pre);
-              p[q] = __ldg(sp.psi[q] + b * H + post);
-              l[q] = __ldg(sp.lsig[q] + b * H + post);
+          for (int v = 0; v < U; ++v) {
+            const unsigned b = (unsigned)(ch * CB + min(bl0 + u0 + v, nb - 1));
+            const unsigned ot = b * (unsigned)P + (unsigned)pre;
+            const unsigned oh = b * (unsigned)H + (unsigned)post;
+#pragma unroll
+            for (int q = 0; q < K; ++q) {
+              zb[v][q] = __ldg(trace[q] + ot);
+              p[v][q] = __ldg(sp.psi[q] + oh);
+              l[v][q] = __ldg(sp.lsig[q] + oh);
             }
           }
-          float ep = st.eps[bl][lane];
-          float eb = st.ebar[bl][lane];
 #pragma unroll
-          for (int q = 0; q < K; ++q) {
-            if (q < sp.k) {
-              const float ee = __fmul_rn(p[q], __fsub_rn(zb[q], __fmul_rn(beta, ep)));
-              eb = __fadd_rn(__fmul_rn(alpha, eb), ee);
-              st.terms[q][bl][lane] = __fmul_rn(l[q], eb);
-              ep = __fadd_rn(__fmul_rn(rho, ep), ee);
+          for (int v = 0; v < U; ++v) {
+            const int bl = bl0 + u0 + v;
+            if (bl < nb) {
+              float ep = st.eps[bl][lane];
+              float eb = st.ebar[bl][lane];
+#pragma unroll
+              for (int q = 0; q < K; ++q) {
+                const float ee = __fmul_rn(p[v][q], __fsub_rn(zb[v][q], __fmul_rn(beta, ep)));
+                eb = __fadd_rn(__fmul_rn(alpha, eb), ee);
+                ep = __fadd_rn(__fmul_rn(rho, ep), ee);
+                terms[q][bl][lane] = __fmul_rn(l[v][q], eb);
+              }
+              st.ebar[bl][lane] = eb;
+              st.eps[bl][lane] = ep;
             }
           }
-          st.ebar[bl][lane] = eb;
-          st.eps[bl][lane] = ep;
         }
         sw::fence_proxy_async_smem();
         __syncwarp();
@@ -286,26 +434,51 @@ k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, 
   }
 }
 
-template <int K>
+template <int K, int NC, int U, int NS = 3, int CB = 32, int NT = 3>
 int launch_block(SegB s0, SegB s1, const StepsB& sp, int B, int H, float beta, float rho, float alpha,
                  double* g_w_out, double* g_b_out, int C, int ro_blocks, unsigned* tickets,
                  cudaStream_t st) {
-  const int smem = (int)sizeof(Smem<K>);
+  static_assert(NC + 2 <= kMaxWarps && CB % NC == 0, "eprop block configuration");
+  static_assert(sizeof(Smem<K, CB, NS, NT>) >= kMaxWarps * 34 * sizeof(double), "readout scratch");
+  const int smem = (int)sizeof(Smem<K, CB, NS, NT>);
+  constexpr int threads = (NC + 2) * 32;
   static int per_sm = 0;
   if (per_sm == 0) {
-    cudaFuncSetAttribute((const void*)k_eprop_block<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eprop_block<K>, kThreads, smem);
+    cudaFuncSetAttribute((const void*)k_eprop_block<K, NC, U, NS, CB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eprop_block<K, NC, U, NS, CB, NT>, threads, smem);
     if (per_sm < 1) per_sm = 1;
   }
   const int tiles = s0.tiles + s1.tiles;
   const int workers = tiles ? min(tiles, 148 * per_sm) : 0;
-  k_eprop_block<K><<<ro_blocks + workers, kThreads, smem, st>>>(s0, s1, sp, B, H, beta, rho, alpha,
-                                                                g_w_out, g_b_out, C, ro_blocks, tickets);
+  k_eprop_block<K, NC, U, NS, CB, NT><<<ro_blocks + workers, threads, smem, st>>>(s0, s1, sp, B, H, beta, rho, alpha,
+                                                                      g_w_out, g_b_out, C, workers, tickets);
   sw::count_launch();
   return SW_OK;
 }
 
+
+// configuration of the k = 4 kernel: compute warps x stages x replicas per
+// stage (SW_EPB_CFG = "NCxNSxCB", for measurement)
+int block_cfg() {
+  static int cfg = -1;
+  if (cfg < 0) {
+    cfg = 8432;
+    if (const char* e = getenv("SW_EPB_CFG")) {
+      int nc = 0, ns = 0, cb = 0;
+      if (sscanf(e, "%dx%dx%d", &nc, &ns, &cb) == 3)
+        cfg = nc * (ns >= 10 ? 10000 : 1000) + ns * 100 + cb;
+    }
+  }
+  return cfg;
+}
+
 }  // namespace
+
+extern "C" int64_t sw_eprop_readout_scratch_bytes(int32_t hidden, int32_t num_classes, int32_t splits) {
+  if (hidden <= 0 || num_classes <= 0 || splits <= 0) return 0;
+  const int64_t groups = (int64_t)((hidden + 31) / 32) * ((num_classes + kRoCG - 1) / kRoCG);
+  return 8 * ((int64_t)splits * num_classes * hidden + (int64_t)splits * num_classes) + 4 * groups;
+}
 
 extern "C" int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, const sw_eprop_block_t* blk,
                                     int32_t batch, int32_t hidden, float beta, float rho, float alpha,
@@ -327,27 +500,46 @@ extern "C" int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, 
     s[i].P = q.num_pre;
     s[i].tiles = q.e_pad / 32;
   }
+  // unused steps alias step 0 (the kernel loads them unconditionally)
+  for (int i = 0; i < n_segs; ++i)
+    for (int k = blk->k; k < kMaxK; ++k) s[i].trace[k] = s[i].trace[0];
   StepsB sp{};
   sp.k = blk->k;
   for (int k = 0; k < kMaxK; ++k) {
-    sp.psi[k] = blk->psi[k];
-    sp.lsig[k] = blk->lsig[k];
+    sp.psi[k] = blk->psi[k < blk->k ? k : 0];
+    sp.lsig[k] = blk->lsig[k < blk->k ? k : 0];
     sp.d[k] = blk->d[k];
     sp.zbar[k] = blk->zbar[k];
   }
   const bool readout = blk->d[0] && g_w_out && num_classes > 0;
-  const int ro_blocks = readout ? num_classes * ((hidden + 31) / 32) : 0;
+  sp.ro_scratch = blk->ro_scratch;
+  sp.ro_splits = blk->ro_splits > 0 ? blk->ro_splits : 1;
+  const int htiles = (hidden + 31) / 32;
+  const int ro_blocks = !readout ? 0
+                        : sp.ro_scratch ? htiles * ((num_classes + kRoCG - 1) / kRoCG) * sp.ro_splits
+                                        : num_classes * htiles;
   if (s[0].tiles + s[1].tiles + ro_blocks == 0 || batch <= 0) return SW_OK;
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
-  switch (blk->k) {
-    case 1: rc = launch_block<1>(s[0], s[1], sp, batch, hidden, beta, rho, alpha, g_w_out, g_b_out,
-                                 num_classes, ro_blocks, workspace, st); break;
-    case 2: rc = launch_block<2>(s[0], s[1], sp, batch, hidden, beta, rho, alpha, g_w_out, g_b_out,
-                                 num_classes, ro_blocks, workspace, st); break;
-    default: rc = launch_block<4>(s[0], s[1], sp, batch, hidden, beta, rho, alpha, g_w_out, g_b_out,
-                                  num_classes, ro_blocks, workspace, st); break;
+#define SW_EPB_ARGS s[0], s[1], sp, batch, hidden, beta, rho, alpha, g_w_out, g_b_out, num_classes, ro_blocks, workspace, st
+  if (blk->k == 1) {
+    rc = launch_block<1, 8, 1>(SW_EPB_ARGS);
+  } else if (blk->k == 2) {
+    rc = launch_block<2, 8, 1>(SW_EPB_ARGS);
+  } else if (blk->k == 3) {
+    rc = launch_block<3, 8, 1>(SW_EPB_ARGS);
+  } else {
+    switch (block_cfg()) {
+      case 8332: rc = launch_block<4, 8, 1, 3, 32, 3>(SW_EPB_ARGS); break;
+      case 8632: rc = launch_block<4, 8, 1, 6, 32, 2>(SW_EPB_ARGS); break;
+      case 8832: rc = launch_block<4, 8, 1, 8, 32, 2>(SW_EPB_ARGS); break;
+      case 81216: rc = launch_block<4, 8, 1, 12, 16, 2>(SW_EPB_ARGS); break;
+      case 8816: rc = launch_block<4, 8, 1, 8, 16, 2>(SW_EPB_ARGS); break;
+      case 81616: rc = launch_block<4, 8, 1, 16, 16, 2>(SW_EPB_ARGS); break;
+      default: rc = launch_block<4, 8, 1, 4, 32, 2>(SW_EPB_ARGS); break;
+    }
   }
+#undef SW_EPB_ARGS
   if (rc) return rc;
   SW_CHECK_LAUNCH("sw_eprop_fused_block");
   return SW_OK;

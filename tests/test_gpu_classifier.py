@@ -186,9 +186,10 @@ def test_overlapped_graph_equals_sequential_steps(dev_lib):
     assert a.connectivity_fingerprint() == b.connectivity_fingerprint()
 
 
+@pytest.mark.parametrize("splits", [0, 3])
 @pytest.mark.parametrize("B,P,H,cap,R,k", [(64, 700, 256, 82, 26, 4), (37, 100, 1024, 40, 10, 3),
                                            (8, 30, 48, 12, 6, 1)])
-def test_blocked_eprop_equals_single_steps(dev_lib, B, P, H, cap, R, k):
+def test_blocked_eprop_equals_single_steps(dev_lib, B, P, H, cap, R, k, splits):
     """sw_eprop_fused_block over k steps == k calls of sw_eprop_fused_step:
     eps/ebar bit-identical, readout gradients to float64 rounding, the
     synapse gradient bit-identical for k = 1 and within 1e-13 relative for
@@ -236,6 +237,10 @@ def test_blocked_eprop_equals_single_steps(dev_lib, B, P, H, cap, R, k):
         blk.psi[j], blk.lsig[j] = s["psi"].data_ptr(), s["lsig"].data_ptr()
         blk.pre_trace[0][j] = s["trace"].data_ptr()
         blk.d[j], blk.zbar[j] = s["d"].data_ptr(), s["zbar"].data_ptr()
+    if splits:   # split readout with its (zeroed) partial scratch
+        nbytes = int(_lib.lib().sw_eprop_readout_scratch_bytes(H, C, splits))
+        scratch = torch.zeros(nbytes // 8 + 1, dtype=torch.float64, device="cuda")
+        blk.ro_scratch, blk.ro_splits = scratch.data_ptr(), splits
     segs[0] = plans[1].seg(steps[0]["trace"])
     _lib.call("sw_eprop_fused_block", ctypes.cast(segs, ctypes.c_void_p), 1, ctypes.byref(blk), B, H,
               beta, rho, alpha, gw[1].data_ptr(), gb[1].data_ptr(), C, _lib.workspace(),
@@ -247,3 +252,6 @@ def test_blocked_eprop_equals_single_steps(dev_lib, B, P, H, cap, R, k):
         assert torch.allclose(plans[1].grad, plans[0].grad, rtol=1e-13, atol=1e-13)
     assert torch.allclose(gw[1], gw[0], rtol=1e-12, atol=1e-12)
     assert torch.allclose(gb[1], gb[0], rtol=1e-12, atol=1e-12)
+    if splits:   # the counters are left zeroed for the next launch
+        cnt = scratch.view(torch.int32)[(splits * C * H + splits * C) * 2:]
+        assert int(cnt.abs().sum()) == 0

@@ -13,7 +13,7 @@ timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench exit $?
 timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > $O/bench_ref.json 2> $O/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2600 --csv --log-file $O/launches.csv \
    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-micro > $O/ncu_launch_bench.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_eprop_fused -s 1000 -c 3 \
+timeout 600 env EAGER=1 ncu --set full --clock-control none --import-source on -k regex:k_eprop_block -s 5 -c 1 \
    -o $O/eprop_c1 -f python tools/profile_eprop.py c1 > $O/ncu_eprop.log 2>&1
 timeout 600 env ROWS=262144 ncu --set full --clock-control none --import-source on \
    -k regex:"k_deepr_elim|k_deepr_form_rows|k_remove_marked" -c 6 \
