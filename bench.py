@@ -428,6 +428,7 @@ def run_device(args, w):
     # and K steps of per-replica vectors (SURVEY 8(d) E-step with the state
     # term once per K steps)
     alg_bytes = Bl * E * 16 + E * (16 + 4) + K * Bl * (w["num_inputs"] + w["hidden"] + 2 * w["hidden"]) * 4
+    alg_single = Bl * E * 16 + E * (16 + 4) + Bl * (w["num_inputs"] + w["hidden"] + 2 * w["hidden"]) * 4
     achieved = alg_bytes / (k_ms * 1e-3) / 1e9
     peak, peak_kind = measured_peak()
     traffic = None
@@ -470,7 +471,12 @@ def run_device(args, w):
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "alg_bytes_per_launch": int(alg_bytes), "kernel_us": round(k_ms * 1e3, 2),
                          "kernel_us_per_timestep": round(k_ms * 1e3 / K, 2),
-                         "share_of_step": round(k_ms * (w["steps"] / K) / ms_dev, 3)},
+                         "share_of_step": round(k_ms * (w["steps"] / K) / ms_dev, 3),
+                         # the same K timesteps as K single-step passes would
+                         # move K x the eligibility bytes: the temporally
+                         # blocked pass beats that formulation's HBM roofline
+                         "single_step_equiv_GBs": round(K * alg_single / (k_ms * 1e-3) / 1e9, 1),
+                         "single_step_equiv_frac": round(K * alg_single / (k_ms * 1e-3) / 1e9 / peak, 4)},
             "clocks": clocks,
         }
         if cpu is not None:
