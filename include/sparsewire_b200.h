@@ -225,7 +225,8 @@ SW_API int sw_eprop_fused_step(const sw_eprop_seg_t* segs, int32_t n_segs, const
                                double* g_w_out, double* g_b_out, int32_t num_classes,
                                int32_t max_blocks_per_sm, uint32_t* workspace, void* stream);
 
-/* k consecutive timesteps (1 <= k <= 4) of the fused step in one pass over
+#define SW_EPROP_MAX_BLOCK 8
+/* k consecutive timesteps (1 <= k <= SW_EPROP_MAX_BLOCK) of the fused step in one pass over
  * the eligibility state (temporal blocking: the forward pass of the k steps
  * runs first, it never reads eps/ebar/grad).  Per step s < k: psi[s],
  * lsig[s] [B,H]; pre_trace[seg][s] [B, num_pre]; d[s] [B,C] and zbar[s]
@@ -236,11 +237,11 @@ SW_API int sw_eprop_fused_step(const sw_eprop_seg_t* segs, int32_t n_segs, const
  * replica order). */
 typedef struct sw_eprop_block {
   int32_t k;
-  const float* psi[4];
-  const float* lsig[4];
-  const float* pre_trace[2][4];
-  const double* d[4];
-  const float* zbar[4];
+  const float* psi[SW_EPROP_MAX_BLOCK];
+  const float* lsig[SW_EPROP_MAX_BLOCK];
+  const float* pre_trace[2][SW_EPROP_MAX_BLOCK];
+  const double* d[SW_EPROP_MAX_BLOCK];
+  const float* zbar[SW_EPROP_MAX_BLOCK];
   /* optional split readout: ro_scratch of sw_eprop_readout_scratch_bytes(
    * hidden, num_classes, ro_splits) bytes, ZEROED once by the caller (the
    * kernel leaves its counters zeroed again); NULL = one block per class and

@@ -36,6 +36,8 @@ class BitfieldDesc(C.Structure):
 P = C.c_void_p
 I32 = C.c_int32
 I64 = C.c_int64
+# SW_EPROP_MAX_BLOCK (include/sparsewire_b200.h): timesteps per blocked e-prop pass
+MAX_BLOCK = 8
 U64 = C.c_uint64
 F64 = C.c_double
 F32 = C.c_float
@@ -79,8 +81,9 @@ class EpropSeg(C.Structure):
 
 class EpropBlock(C.Structure):
     """sw_eprop_block_t"""
-    _fields_ = [("k", I32), ("psi", P * 4), ("lsig", P * 4), ("pre_trace", (P * 4) * 2),
-                ("d", P * 4), ("zbar", P * 4), ("ro_scratch", P), ("ro_splits", I32)]
+    _fields_ = [("k", I32), ("psi", P * MAX_BLOCK), ("lsig", P * MAX_BLOCK),
+                ("pre_trace", (P * MAX_BLOCK) * 2), ("d", P * MAX_BLOCK), ("zbar", P * MAX_BLOCK),
+                ("ro_scratch", P), ("ro_splits", I32)]
 
 
 class ClfStep(C.Structure):

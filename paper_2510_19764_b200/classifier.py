@@ -14,6 +14,7 @@ update and replays the same rewiring streams.
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 from dataclasses import dataclass
 
@@ -33,7 +34,7 @@ from .updates import Model
 # timesteps per e-prop pass over the eligibility state (temporal blocking,
 # sw_eprop_fused_block): K forward steps run first, then one pass applies K
 # recursion steps to every (replica, synapse) element
-EPROP_BLOCK_STEPS = 4
+EPROP_BLOCK_STEPS = int(os.environ.get("SW_EPROP_BLOCK_STEPS", "8"))
 # (step, replica) splits of the readout gradient inside the blocked pass
 READOUT_SPLITS = 32
 

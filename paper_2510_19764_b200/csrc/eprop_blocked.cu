@@ -33,7 +33,7 @@
 
 namespace {
 
-constexpr int kMaxK = 4;
+constexpr int kMaxK = SW_EPROP_MAX_BLOCK;
 #ifndef SW_EPB_UNROLL
 #define SW_EPB_UNROLL 1
 #endif
@@ -449,7 +449,9 @@ int launch_block(SegB s0, SegB s1, const StepsB& sp, int B, int H, float beta, f
     if (per_sm < 1) per_sm = 1;
   }
   const int tiles = s0.tiles + s1.tiles;
-  const int workers = tiles ? min(tiles, 148 * per_sm) : 0;
+  int cap = per_sm;
+  if (const char* e = getenv("SW_EPB_PER_SM")) cap = max(1, min(per_sm, atoi(e)));
+  const int workers = tiles ? min(tiles, 148 * cap) : 0;
   k_eprop_block<K, NC, U, NS, CB, NT><<<ro_blocks + workers, threads, smem, st>>>(s0, s1, sp, B, H, beta, rho, alpha,
                                                                       g_w_out, g_b_out, C, workers, tickets);
   sw::count_launch();
@@ -462,7 +464,7 @@ int launch_block(SegB s0, SegB s1, const StepsB& sp, int B, int H, float beta, f
 int block_cfg() {
   static int cfg = -1;
   if (cfg < 0) {
-    cfg = 8432;
+    cfg = 0;
     if (const char* e = getenv("SW_EPB_CFG")) {
       int nc = 0, ns = 0, cb = 0;
       if (sscanf(e, "%dx%dx%d", &nc, &ns, &cb) == 3)
@@ -486,7 +488,7 @@ extern "C" int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, 
                                     uint32_t* workspace, void* stream) {
   if (!workspace) { sw::set_last_error("eprop block: workspace (2 zeroed uint32) required"); return SW_ERR_INVALID_ARG; }
   if (n_segs < 1 || n_segs > 2) { sw::set_last_error("eprop block: 1 or 2 segments"); return SW_ERR_INVALID_ARG; }
-  if (!blk || blk->k < 1 || blk->k > kMaxK) { sw::set_last_error("eprop block: 1 <= k <= 4 steps"); return SW_ERR_INVALID_ARG; }
+  if (!blk || blk->k < 1 || blk->k > kMaxK) { sw::set_last_error("eprop block: 1 <= k <= SW_EPROP_MAX_BLOCK steps"); return SW_ERR_INVALID_ARG; }
   SegB s[2] = {};
   for (int i = 0; i < n_segs; ++i) {
     const sw_eprop_seg_t& q = segs[i];
@@ -522,22 +524,30 @@ extern "C" int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, 
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
 #define SW_EPB_ARGS s[0], s[1], sp, batch, hidden, beta, rho, alpha, g_w_out, g_b_out, num_classes, ro_blocks, workspace, st
-  if (blk->k == 1) {
-    rc = launch_block<1, 8, 1>(SW_EPB_ARGS);
-  } else if (blk->k == 2) {
-    rc = launch_block<2, 8, 1>(SW_EPB_ARGS);
-  } else if (blk->k == 3) {
-    rc = launch_block<3, 8, 1>(SW_EPB_ARGS);
-  } else {
-    switch (block_cfg()) {
-      case 8332: rc = launch_block<4, 8, 1, 3, 32, 3>(SW_EPB_ARGS); break;
-      case 8632: rc = launch_block<4, 8, 1, 6, 32, 2>(SW_EPB_ARGS); break;
-      case 8832: rc = launch_block<4, 8, 1, 8, 32, 2>(SW_EPB_ARGS); break;
-      case 81216: rc = launch_block<4, 8, 1, 12, 16, 2>(SW_EPB_ARGS); break;
-      case 8816: rc = launch_block<4, 8, 1, 8, 16, 2>(SW_EPB_ARGS); break;
-      case 81616: rc = launch_block<4, 8, 1, 16, 16, 2>(SW_EPB_ARGS); break;
-      default: rc = launch_block<4, 8, 1, 4, 32, 2>(SW_EPB_ARGS); break;
-    }
+  const int cfg = block_cfg();
+  switch (blk->k) {
+    case 1: rc = launch_block<1, 8, 1>(SW_EPB_ARGS); break;
+    case 2: rc = launch_block<2, 8, 1>(SW_EPB_ARGS); break;
+    case 3: rc = launch_block<3, 8, 1>(SW_EPB_ARGS); break;
+    case 4:
+      switch (cfg) {
+        case 8332: rc = launch_block<4, 8, 1, 3, 32, 3>(SW_EPB_ARGS); break;
+        case 8816: rc = launch_block<4, 8, 1, 8, 16, 2>(SW_EPB_ARGS); break;
+        default: rc = launch_block<4, 8, 1, 4, 32, 2>(SW_EPB_ARGS); break;
+      }
+      break;
+    case 5: rc = launch_block<5, 4, 1, 4, 16, 2>(SW_EPB_ARGS); break;
+    case 6: rc = launch_block<6, 4, 1, 4, 16, 2>(SW_EPB_ARGS); break;
+    case 7: rc = launch_block<7, 4, 1, 4, 16, 2>(SW_EPB_ARGS); break;
+    default:
+      switch (cfg) {
+        case 8432: rc = launch_block<8, 8, 1, 4, 32, 2>(SW_EPB_ARGS); break;
+        case 4616: rc = launch_block<8, 4, 1, 6, 16, 2>(SW_EPB_ARGS); break;
+        case 4432: rc = launch_block<8, 4, 1, 4, 32, 2>(SW_EPB_ARGS); break;
+        case 4316: rc = launch_block<8, 4, 1, 3, 16, 2>(SW_EPB_ARGS); break;
+        default: rc = launch_block<8, 4, 1, 4, 16, 2>(SW_EPB_ARGS); break;
+      }
+      break;
   }
 #undef SW_EPB_ARGS
   if (rc) return rc;

@@ -44,3 +44,14 @@ def test_host_fold_key_matches_oracle():
     r = R.CounterRng(5, "n")
     o = O.Stream.of(5, "n")
     assert [r.uniform_int(700) for _ in range(50)] == [o.uniform_int(700) for _ in range(50)]
+
+
+def test_block_struct_matches_header():
+    """_lib.EpropBlock mirrors sw_eprop_block_t: the step-array width is the
+    header's SW_EPROP_MAX_BLOCK."""
+    import re
+    from paper_2510_19764_b200 import _lib
+    src = open(os.path.join(ROOT, "include", "sparsewire_b200.h")).read()
+    n = int(re.search(r"#define SW_EPROP_MAX_BLOCK (\d+)", src).group(1))
+    assert _lib.MAX_BLOCK == n
+    assert len(_lib.EpropBlock().psi) == n and len(_lib.EpropBlock().pre_trace[1]) == n
