@@ -342,6 +342,33 @@ SW_API int sw_propagate_atomic(const int32_t* row_length, const int32_t* target,
                                void* stream);
 /* Workspace bytes the slab form of sw_propagate_atomic needs on the current device. */
 SW_API int64_t sw_propagate_workspace_bytes(void);
+
+/* Post-slab bucketed rows (a derived copy for propagate_spikes over a matrix
+ * whose connectivity and weights stay fixed across many steps; SURVEY §8e
+ * "column slices of every row").  G = sw_prop_bucket_slabs(num_post) slabs of
+ * 16384 posts (num_post <= 131072).  Arrays, caller-allocated:
+ *   bt, bslot uint16 [num_pre*stride], bw float64 [num_pre*stride],
+ *   soff uint16 [num_pre*(G+1)].
+ * Row i's synapses, grouped by slab and in slot order within a slab, sit in
+ * the row's own padded slot range; soff[i*(G+1)+j] is slab j's first entry.
+ * Rebuild after a structural change (like TransposeMap, connectivity.py:173);
+ * after a weight-only change sw_prop_buckets_refresh re-gathers bw. */
+SW_API int32_t sw_prop_bucket_slabs(int32_t num_post);
+SW_API int sw_prop_buckets_build(const int32_t* row_length, const int32_t* target, const double* w,
+                                 int32_t num_pre, int32_t num_post, int32_t stride, uint16_t* bt,
+                                 uint16_t* bslot, double* bw, uint16_t* soff, void* stream);
+SW_API int sw_prop_buckets_refresh(const int32_t* row_length, const double* w, int32_t num_pre,
+                                   int32_t stride, const uint16_t* bslot, double* bw, void* stream);
+/* propagate_spikes (connectivity.py:139-148), atomic-mode semantics (float64,
+ * summation order not fixed: shared-memory atomics per slab, then the groups'
+ * partial slabs summed in ascending group order): out[j] += sum over the
+ * spiking rows.  One cooperative launch; workspace >=
+ * sw_prop_bucketed_workspace_bytes(num_post). */
+SW_API int64_t sw_prop_bucketed_workspace_bytes(int32_t num_post);
+SW_API int sw_propagate_bucketed(const uint16_t* soff, const uint16_t* bt, const double* bw, int32_t num_post,
+                                 int32_t stride, const int32_t* spikes, const int32_t* n_spikes,
+                                 int32_t max_spikes, double* out, void* workspace, int64_t workspace_bytes,
+                                 void* stream);
 typedef struct sw_prop_proj {
   const int32_t* col_ptr;    /* transpose CSR of the projection */
   const int32_t* src_pre;

@@ -124,6 +124,11 @@ SIGNATURES: dict[str, list] = {
     "sw_eprop_fused_step": [C.c_void_p, I32, P, P, I32, I32, F32, F32, F32, P, P, P, P, I32, I32, P, P],
     "sw_eprop_fused_block": [C.c_void_p, I32, P, I32, I32, F32, F32, F32, P, P, I32, P, P],
     "sw_eprop_readout_scratch_bytes": [I32, I32, I32],
+    "sw_prop_bucket_slabs": [I32],
+    "sw_prop_buckets_build": [P, P, P, I32, I32, I32, P, P, P, P, P],
+    "sw_prop_buckets_refresh": [P, P, I32, I32, P, P, P],
+    "sw_prop_bucketed_workspace_bytes": [I32],
+    "sw_propagate_bucketed": [P, P, P, I32, I32, P, P, I32, P, P, I64, P],
     "sw_alif_step": [P, P, P, P, P, I64, F32, F32, F32, F32, P],
     "sw_alif_surrogate": [P, P, P, I64, F32, F32, P],
     "sw_lif_cond_step": [P, P, P, P, I32, I64, F64, F64, F64, F64, F64, F64, F64, F64, I64, P, P],
@@ -172,6 +177,7 @@ def lib():
     L.sw_propagate_workspace_bytes.restype = C.c_int64
     L.sw_eprop_readout_scratch_bytes.argtypes = [I32, I32, I32]
     L.sw_eprop_readout_scratch_bytes.restype = C.c_int64
+    L.sw_prop_bucketed_workspace_bytes.restype = C.c_int64
     L.sw_launch_count.argtypes = []
     L.sw_launch_count.restype = C.c_longlong
     L.sw_last_error.argtypes = []

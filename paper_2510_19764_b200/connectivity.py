@@ -239,8 +239,77 @@ def spikes_to_bits(spikes: torch.Tensor, n: int) -> torch.Tensor:
     return torch.where(w >= 2**31, w - 2**32, w).to(torch.int32)
 
 
+class PropBuckets:
+    """Post-slab bucketed copy of a matrix and its weights for
+    propagate_spikes over a matrix whose structure and weights stay fixed
+    across many steps (sw_prop_buckets_build; SURVEY §8e "column slices of
+    every row").  Each row's synapses are grouped by 16384-post slab inside
+    the row's own slot range, so the propagation reads every synapse of a
+    spiking row once and accumulates in shared memory instead of L2 atomics.
+    Like TransposeMap (connectivity.py:151-192) it goes stale on a structural
+    change (``m.version``); after a weight-only change call ``refresh()``."""
+
+    def __init__(self, m: RaggedMatrix, weights: torch.Tensor):
+        if weights.dtype != torch.float64:
+            raise TypeError("float64 weights expected")
+        self.m, self.weights = m, weights
+        self.slabs = int(_lib.lib().sw_prop_bucket_slabs(m.num_post))
+        if self.slabs == 0:
+            raise ValueError("bucketed propagation needs 1 <= num_post <= 131072")
+        n = m.num_pre * m.stride
+        dev = m.target.device
+        self.bt = torch.empty(n, dtype=torch.int16, device=dev)
+        self.bslot = torch.empty(n, dtype=torch.int16, device=dev)
+        self.bw = torch.empty(n, dtype=torch.float64, device=dev)
+        self.soff = torch.empty(m.num_pre * (self.slabs + 1), dtype=torch.int16, device=dev)
+        nbytes = int(_lib.lib().sw_prop_bucketed_workspace_bytes(m.num_post))
+        self.workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=dev)
+        self.version = -1
+        self.build()
+
+    def build(self) -> None:
+        m = self.m
+        _lib.call("sw_prop_buckets_build", m.row_length.data_ptr(), m.target.data_ptr(),
+                  self.weights.data_ptr(), m.num_pre, m.num_post, m.stride, self.bt.data_ptr(),
+                  self.bslot.data_ptr(), self.bw.data_ptr(), self.soff.data_ptr(), _lib.stream_ptr())
+        self.version = m.version
+
+    def refresh(self) -> None:
+        """Re-gather the weight copy after the weights (not the structure) changed."""
+        self.check_fresh()
+        m = self.m
+        _lib.call("sw_prop_buckets_refresh", m.row_length.data_ptr(), self.weights.data_ptr(),
+                  m.num_pre, m.stride, self.bslot.data_ptr(), self.bw.data_ptr(), _lib.stream_ptr())
+
+    def check_fresh(self) -> None:
+        if self.version != self.m.version:
+            from .errors import StaleTranspose
+            raise StaleTranspose("bucketed rows older than their matrix")
+
+    # below this many spiking rows the fixed cost of the slab pass (zeroing,
+    # partial slabs, grid barrier, reduction) exceeds the L2-atomic kernel's
+    MIN_SPIKES = 4096
+
+    def propagate(self, spikes: torch.Tensor, n_spikes: torch.Tensor, max_spikes: int,
+                  out: torch.Tensor) -> str:
+        """out[j] += weights of the spiking rows onto j (device spike list and
+        count); returns the kernel used ("bucketed" or "atomic")."""
+        self.check_fresh()
+        m = self.m
+        if max_spikes < self.MIN_SPIKES:
+            _lib.call("sw_propagate_atomic", m.row_length.data_ptr(), m.target.data_ptr(),
+                      self.weights.data_ptr(), m.num_pre, m.num_post, m.stride, spikes.data_ptr(),
+                      n_spikes.data_ptr(), max(1, int(max_spikes)), out.data_ptr(), *_lib.prop_workspace(),
+                      _lib.stream_ptr())
+            return "atomic"
+        _lib.call("sw_propagate_bucketed", self.soff.data_ptr(), self.bt.data_ptr(), self.bw.data_ptr(),
+                  m.num_post, m.stride, spikes.data_ptr(), n_spikes.data_ptr(), max(1, int(max_spikes)),
+                  out.data_ptr(), self.workspace.data_ptr(), self.workspace.numel(), _lib.stream_ptr())
+        return "bucketed"
+
+
 def propagate_spikes(m: RaggedMatrix, weights: torch.Tensor, spikes: torch.Tensor,
-                     out: torch.Tensor, tmap=None) -> None:
+                     out: torch.Tensor, tmap=None, buckets: PropBuckets | None = None) -> None:
     """out[j] += weights of synapses from spiking rows onto j
     (connectivity.py:139-148).
 
@@ -248,10 +317,19 @@ def propagate_spikes(m: RaggedMatrix, weights: torch.Tensor, spikes: torch.Tenso
     in ascending-spike order through the transpose: bit-identical to the
     reference's np.add.at for an ascending spike set.  Without one the
     event-driven atomic kernel runs (warp per spiking row; summation order,
-    and so the last bits, may vary between runs)."""
+    and so the last bits, may vary between runs).  With fresh ``buckets``
+    (PropBuckets of ``m`` and ``weights``) the bucketed kernel runs (same
+    atomic-mode contract, no L2 atomics)."""
     if weights.dtype != torch.float64 or out.dtype != torch.float64:
         raise TypeError("float64 weights/out expected")
     st = _lib.stream_ptr()
+    if buckets is not None:
+        if buckets.m is not m or buckets.weights.data_ptr() != weights.data_ptr():
+            raise ValueError("buckets were built for another matrix / weight plane")
+        sp = spikes.to(device=DEV, dtype=torch.int32).contiguous()
+        n = torch.tensor([sp.numel()], dtype=torch.int32, device=DEV)
+        buckets.propagate(sp, n, sp.numel(), out)
+        return
     if tmap is not None:
         tmap.check_fresh()
         bits = spikes_to_bits(spikes, m.num_pre)

@@ -128,3 +128,72 @@ def test_single_synapse_edits_match_reference_semantics(dev_lib):
     assert np.array_equal(m.target.cpu().numpy()[mask], o.target[mask])
     for p in ("w", "g"):
         assert np.array_equal(syn.planes[p].cpu().numpy()[mask], o.planes[p][mask])
+
+
+@pytest.mark.parametrize("P,N,cap,q", [
+    (6000, 65536, 300, 0.6),      # 4 slabs, multi-chunk rows
+    (5000, 40000, 41, 0.9),       # odd stride, 3 slabs, last one partial
+    (4000, 3000, 64, 0.7),        # one slab smaller than 16384
+    (3000, 131072, 96, 0.5),      # 8 slabs
+    (400, 65536, 1024, 0.01),     # full-capacity rows, very few spikes
+])
+def test_bucketed_propagation_matches_add_at(dev_lib, P, N, cap, q):
+    """Post-slab bucketed rows (sw_prop_buckets_build / sw_propagate_bucketed):
+    the layout is a stable per-slab regrouping of every row, and the
+    propagation equals np.add.at exactly for dyadic weights from zero."""
+    from paper_2510_19764_b200.connectivity import PropBuckets, propagate_spikes
+    m, syn, rl, tgt, rs = _matrix(P, N, cap, 23)
+    w = rs.integers(-64, 65, size=tgt.shape).astype(np.float64) / 64.0
+    syn.planes["g"].copy_(torch.from_numpy(w))
+    pb = PropBuckets(m, syn.planes["g"])
+    pb.MIN_SPIKES = 0                  # the bucketed kernel at every size
+    G = pb.slabs
+    assert G == -(-N // 16384)
+    stride = m.stride
+    bt = pb.bt.cpu().numpy().view(np.uint16).reshape(P, stride)
+    bs = pb.bslot.cpu().numpy().view(np.uint16).reshape(P, stride)
+    bw = pb.bw.cpu().numpy().reshape(P, stride)
+    so = pb.soff.cpu().numpy().view(np.uint16).reshape(P, G + 1)
+    for i in rs.choice(P, 60, replace=False):
+        n = rl[i]
+        assert so[i, 0] == 0 and so[i, G] == n
+        slots = bs[i, :n].astype(np.int64)
+        assert np.array_equal(np.sort(slots), np.arange(n))
+        for j in range(G):
+            a, b = so[i, j], so[i, j + 1]
+            sl = slots[a:b]
+            assert np.all(np.diff(sl) > 0)                       # slot order within a slab
+            assert np.all(tgt[i, sl] // 16384 == j)
+            assert np.array_equal(bt[i, a:b].astype(np.int64) + j * 16384, tgt[i, sl])
+            assert np.array_equal(bw[i, a:b], w[i, sl])
+    spikes = np.flatnonzero(rs.random(P) < q).astype(np.int32)
+    ref = np.zeros(N)
+    for i in spikes:
+        np.add.at(ref, tgt[i, :rl[i]], w[i, :rl[i]])
+    out = torch.zeros(N, dtype=torch.float64, device="cuda")
+    propagate_spikes(m, syn.planes["g"], torch.from_numpy(spikes).cuda(), out, buckets=pb)
+    assert np.array_equal(out.cpu().numpy(), ref)
+    # weight-only change: refresh, then general weights to 1e-12
+    w2 = rs.standard_normal(tgt.shape)
+    syn.planes["g"].copy_(torch.from_numpy(w2))
+    pb.refresh()
+    ref2 = rs.standard_normal(N)
+    out2 = torch.from_numpy(ref2.copy()).cuda()
+    for i in spikes:
+        np.add.at(ref2, tgt[i, :rl[i]], w2[i, :rl[i]])
+    propagate_spikes(m, syn.planes["g"], torch.from_numpy(spikes).cuda(), out2, buckets=pb)
+    assert np.allclose(out2.cpu().numpy(), ref2, rtol=1e-12, atol=1e-12)
+
+
+def test_bucketed_propagation_goes_stale(dev_lib):
+    from paper_2510_19764_b200.connectivity import PropBuckets, add_synapse, propagate_spikes
+    from paper_2510_19764_b200.errors import StaleTranspose
+    m, syn, rl, tgt, rs = _matrix(200, 5000, 16, 3)
+    pb = PropBuckets(m, syn.planes["g"])
+    row = int(np.flatnonzero(rl < 16)[0])
+    add_synapse(m, syn, row, int(np.setdiff1d(np.arange(5000), tgt[row, :rl[row]])[0]))
+    out = torch.zeros(5000, dtype=torch.float64, device="cuda")
+    with pytest.raises(StaleTranspose):
+        propagate_spikes(m, syn.planes["g"], torch.tensor([row]).cuda(), out, buckets=pb)
+    pb.build()
+    propagate_spikes(m, syn.planes["g"], torch.tensor([row]).cuda(), out, buckets=pb)
