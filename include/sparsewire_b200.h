@@ -299,8 +299,14 @@ typedef struct sw_clf_step {
    * in/out trace buffers the next step's forward pass can run while the
    * e-prop update still reads this step's traces */
   const float* zbar_in; const float* xbar_in;
+  /* n_steps >= 1: one launch runs timesteps t .. t+n_steps-1 (block per
+   * replica, steps back to back).  zbar/xbar/psi/lsig/d are then the bases of
+   * slot_count contiguous per-step slots [slot][batch][width]; step t writes
+   * slot t % slot_count and reads the traces of slot (t-1) % slot_count
+   * (zbar_in/xbar_in ignored).  n_steps = 0: one step, fields as above. */
+  int32_t n_steps; int32_t slot_count;
 } sw_clf_step_t;
-/* One fused forward timestep for all replicas (block per replica). */
+/* Fused forward timestep(s) for all replicas (block per replica). */
 SW_API int sw_clf_step(const sw_clf_step_t* params, void* stream);
 /* out2[0] = sum of per-replica cross-entropy, out2[1] = #correct (argmax pi_sum). */
 SW_API int sw_clf_batch_stats(const double* loss, const double* pi_sum, const int32_t* labels,

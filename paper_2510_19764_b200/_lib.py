@@ -95,7 +95,7 @@ class ClfStep(C.Structure):
                 ("batch", I32), ("v", P), ("a", P), ("z", P), ("zbar", P), ("xbar", P),
                 ("y", P), ("pi_sum", P), ("loss", P), ("d", P), ("psi", P), ("lsig", P),
                 ("alpha", F32), ("rho", F32), ("beta", F32), ("v_thr", F32), ("alpha64", F64),
-                ("zbar_in", P), ("xbar_in", P)]
+                ("zbar_in", P), ("xbar_in", P), ("n_steps", I32), ("slot_count", I32)]
 BP = C.POINTER(BitfieldDesc)
 
 # name -> argtypes (restype is int status for all but sw_last_error)

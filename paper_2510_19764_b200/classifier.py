@@ -233,11 +233,18 @@ class EpropClassifierTrainer:
         # reads one half while the forward passes of the next K steps write
         # the other half, so both can run at once.
         K2 = 2 * EPROP_BLOCK_STEPS
-        self._slot_zbar = [torch.zeros((B, H), **f32) for _ in range(K2)]
-        self._slot_xbar = [torch.zeros((B, NI), **f32) for _ in range(K2)]
-        self._slot_psi = [torch.zeros((B, H), **f32) for _ in range(K2)]
-        self._slot_lsig = [torch.zeros((B, H), **f32) for _ in range(K2)]
-        self._slot_d = [torch.zeros((B, C), **f64) for _ in range(K2)]
+        # contiguous [slot][B][width] arrays (the grouped forward launch
+        # addresses slot t % K2 from the base), listed as per-slot views
+        self._slots_zbar = torch.zeros((K2, B, H), **f32)
+        self._slots_xbar = torch.zeros((K2, B, NI), **f32)
+        self._slots_psi = torch.zeros((K2, B, H), **f32)
+        self._slots_lsig = torch.zeros((K2, B, H), **f32)
+        self._slots_d = torch.zeros((K2, B, C), **f64)
+        self._slot_zbar = list(self._slots_zbar.unbind(0))
+        self._slot_xbar = list(self._slots_xbar.unbind(0))
+        self._slot_psi = list(self._slots_psi.unbind(0))
+        self._slot_lsig = list(self._slots_lsig.unbind(0))
+        self._slot_d = list(self._slots_d.unbind(0))
         # slot-0 views under the reference attribute names
         self.zbar, self.xbar = self._slot_zbar[0], self._slot_xbar[0]
         self.psi, self.lsig = self._slot_psi[0], self._slot_lsig[0]
@@ -287,6 +294,17 @@ class EpropClassifierTrainer:
         s.alpha64 = p.alpha
         return s
 
+    def _group_params(self, t0: int, k: int) -> _lib.ClfStep:
+        """One launch for steps t0 .. t0+k-1 (sw_clf_step with n_steps = k)
+        over the contiguous slot arrays."""
+        s = self._step_params(t0)
+        s.zbar, s.xbar = self._slots_zbar.data_ptr(), self._slots_xbar.data_ptr()
+        s.psi, s.lsig, s.d = (self._slots_psi.data_ptr(), self._slots_lsig.data_ptr(),
+                              self._slots_d.data_ptr())
+        s.zbar_in = s.xbar_in = 0
+        s.n_steps, s.slot_count = k, 2 * EPROP_BLOCK_STEPS
+        return s
+
     def _slot(self, t: int) -> dict:
         k = t % (2 * EPROP_BLOCK_STEPS)
         return dict(zbar=self._slot_zbar[k], xbar=self._slot_xbar[k], psi=self._slot_psi[k],
@@ -326,8 +344,9 @@ class EpropClassifierTrainer:
         return g
 
     def _launch_steps(self, learn: bool, overlap: bool = False) -> None:
-        """One trial: the forward pass of K = EPROP_BLOCK_STEPS steps, then
-        one e-prop pass over those K steps (temporal blocking).  overlap
+        """One trial: one launch running the forward pass of K =
+        EPROP_BLOCK_STEPS steps, then one e-prop pass over those K steps
+        (temporal blocking).  overlap
         (graph capture only): forward passes on the capturing stream, e-prop
         passes on a side stream, so the forward passes of group g+1 run while
         group g's e-prop pass streams the eligibility state; group g+2's
@@ -338,9 +357,8 @@ class EpropClassifierTrainer:
         if not (learn and overlap):
             st = _lib.stream_ptr()
             for t0, k in groups:
-                for t in range(t0, t0 + k):
-                    prm = self._step_params(t)
-                    _lib.call("sw_clf_step", ctypes.byref(prm), st)
+                prm = self._group_params(t0, k)
+                _lib.call("sw_clf_step", ctypes.byref(prm), st)
                 if learn:
                     self._eprop_block(t0, k, st)
             self.steps_launched += T
@@ -353,9 +371,8 @@ class EpropClassifierTrainer:
         for g, (t0, k) in enumerate(groups):
             if g >= 2:
                 main.wait_event(upd_done[g - 2])
-            for t in range(t0, t0 + k):
-                prm = self._step_params(t)
-                _lib.call("sw_clf_step", ctypes.byref(prm), main.cuda_stream)
+            prm = self._group_params(t0, k)
+            _lib.call("sw_clf_step", ctypes.byref(prm), main.cuda_stream)
             fwd_done[g].record(main)
             side.wait_event(fwd_done[g])
             self._eprop_block(t0, k, side.cuda_stream)
@@ -364,9 +381,11 @@ class EpropClassifierTrainer:
         self.steps_launched += T
 
     def kernels_per_trial(self, learn: bool = True) -> int:
+        """One grouped forward launch and (learning) one e-prop pass per
+        EPROP_BLOCK_STEPS timesteps."""
         T = self.task.example_steps
         groups = -(-T // EPROP_BLOCK_STEPS)
-        return T + (groups if learn else 0)
+        return groups * (2 if learn else 1)
 
     def _run_trial(self, learn: bool) -> None:
         if not self.use_graph:

@@ -63,7 +63,7 @@ __device__ long long g_clf_prof[16];
 #endif
 
 template <int kThreads>
-__global__ void __launch_bounds__(kThreads) k_clf_step(sw_clf_step_t P) {
+__device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P) {
   constexpr int kWarps = kThreads / 32;
   extern __shared__ unsigned char smem_raw[];
   const int H = P.hidden, NI = P.num_inputs, C = P.num_classes;
@@ -386,6 +386,37 @@ __global__ void __launch_bounds__(kThreads) k_clf_step(sw_clf_step_t P) {
   }
 }
 
+// One launch for n_steps consecutive timesteps (P.n_steps >= 1): the replicas
+// are independent within a trial (the weights only change between batches),
+// so each block runs its replica's steps back to back, with no inter-kernel
+// gap or tail between them.  zbar/xbar/psi/lsig/d are then the bases of
+// slot_count contiguous per-step slots ([slot][B][width]); step t writes slot
+// t % slot_count and reads the traces of slot (t - 1) % slot_count.
+template <int kThreads>
+__global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_clf_step(sw_clf_step_t P) {
+  if (P.n_steps <= 0) {
+    clf_step_body<kThreads>(P);
+    return;
+  }
+  const int64_t B = P.batch, H = P.hidden, NI = P.num_inputs, C = P.num_classes;
+  const int n = P.slot_count;
+  for (int s = 0; s < P.n_steps; ++s) {
+    sw_clf_step_t Q = P;
+    const int t = P.t + s;
+    const int64_t cur = t % n, prev = ((t - 1) % n + n) % n;
+    Q.t = t;
+    Q.zbar = P.zbar + cur * B * H;
+    Q.zbar_in = P.zbar + prev * B * H;
+    Q.xbar = P.xbar + cur * B * NI;
+    Q.xbar_in = P.xbar + prev * B * NI;
+    Q.psi = P.psi + cur * B * H;
+    Q.lsig = P.lsig + cur * B * H;
+    Q.d = P.d + cur * B * C;
+    if (s) __syncthreads();   // this block's step s-1 writes are visible to its step s
+    clf_step_body<kThreads>(Q);
+  }
+}
+
 // loss / accuracy of a batch (classifier.py:231-233)
 __global__ void k_clf_batch_stats(const double* loss, const double* pi_sum, const int32_t* labels,
                                   int B, int C, double* out2) {
@@ -440,6 +471,10 @@ extern "C" __attribute__((visibility("default"))) int sw_debug_clf_prof(long lon
 extern "C" int sw_clf_step(const sw_clf_step_t* p, void* stream) {
   const int H = p->hidden, NI = p->num_inputs, C = p->num_classes;
   if (p->batch <= 0) return SW_OK;
+  if (p->n_steps > 0 && p->slot_count < 2) {
+    sw::set_last_error("clf_step: n_steps > 0 needs slot_count >= 2 (step t reads slot t-1)");
+    return SW_ERR_INVALID_ARG;
+  }
   if (NI + H > kThreads * kPerThread) {
     sw::set_last_error("clf_step: num_inputs + hidden must be <= 2048");
     return SW_ERR_INVALID_ARG;

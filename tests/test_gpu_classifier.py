@@ -188,7 +188,8 @@ def test_overlapped_graph_equals_sequential_steps(dev_lib):
 
 @pytest.mark.parametrize("splits", [0, 3])
 @pytest.mark.parametrize("B,P,H,cap,R,k", [(64, 700, 256, 82, 26, 4), (37, 100, 1024, 40, 10, 3),
-                                           (8, 30, 48, 12, 6, 1)])
+                                           (8, 30, 48, 12, 6, 1), (48, 700, 256, 82, 26, 8),
+                                           (20, 120, 300, 30, 9, 5)])
 def test_blocked_eprop_equals_single_steps(dev_lib, B, P, H, cap, R, k, splits):
     """sw_eprop_fused_block over k steps == k calls of sw_eprop_fused_step:
     eps/ebar bit-identical, readout gradients to float64 rounding, the
@@ -255,3 +256,31 @@ def test_blocked_eprop_equals_single_steps(dev_lib, B, P, H, cap, R, k, splits):
     if splits:   # the counters are left zeroed for the next launch
         cnt = scratch.view(torch.int32)[(splits * C * H + splits * C) * 2:]
         assert int(cnt.abs().sum()) == 0
+
+
+def test_grouped_forward_equals_single_steps(dev_lib):
+    """sw_clf_step with n_steps = k (one launch, steps back to back per
+    replica, slot bases) == k single-step launches: state, per-step slots and
+    readout accumulators bit-identical."""
+    import ctypes
+    from paper_2510_19764_b200 import _lib
+    from paper_2510_19764_b200.classifier import EPROP_BLOCK_STEPS
+    tr = [_small_trainer(use_graph=False), _small_trainer(use_graph=False)]
+    ids = tr[0].task.train_ids(0, tr[0].batch_size)
+    for x in tr:
+        x._upload_batch(ids)
+        x._prepare(False)
+    st = _lib.stream_ptr()
+    T = 2 * EPROP_BLOCK_STEPS + 3
+    for t in range(T):
+        prm = tr[0]._step_params(t)
+        _lib.call("sw_clf_step", ctypes.byref(prm), st)
+    for t0 in range(0, T, EPROP_BLOCK_STEPS):
+        prm = tr[1]._group_params(t0, min(EPROP_BLOCK_STEPS, T - t0))
+        _lib.call("sw_clf_step", ctypes.byref(prm), st)
+    torch.cuda.synchronize()
+    a, b = tr
+    for name in ("v", "a", "z", "y", "pi_sum", "loss_b"):
+        assert torch.equal(getattr(a, name), getattr(b, name)), name
+    for name in ("_slots_zbar", "_slots_xbar", "_slots_psi", "_slots_lsig", "_slots_d"):
+        assert torch.equal(getattr(a, name), getattr(b, name)), name
