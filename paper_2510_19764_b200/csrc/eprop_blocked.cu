@@ -248,8 +248,8 @@ constexpr int smem_blocks() {
   return (233472 / per) < 3 ? ((233472 / per) < 1 ? 1 : 233472 / per) : 3;
 }
 
-template <int K, int NC, int U, int NS, int CB, int NT>
-__global__ void __launch_bounds__((NC + 2) * 32, smem_blocks<K, CB, NS, NT>())
+template <int K, int NC, int U, int NS, int CB, int NT, int MB>
+__global__ void __launch_bounds__((NC + 2) * 32, MB > 0 ? MB : smem_blocks<K, CB, NS, NT>())
 k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, float alpha,
               double* g_w_out, double* g_b_out, int C, int workers, unsigned* tickets) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -434,7 +434,7 @@ k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, 
   }
 }
 
-template <int K, int NC, int U, int NS = 3, int CB = 32, int NT = 3>
+template <int K, int NC, int U, int NS = 3, int CB = 32, int NT = 3, int MB = 0>
 int launch_block(SegB s0, SegB s1, const StepsB& sp, int B, int H, float beta, float rho, float alpha,
                  double* g_w_out, double* g_b_out, int C, int ro_blocks, unsigned* tickets,
                  cudaStream_t st) {
@@ -444,15 +444,15 @@ int launch_block(SegB s0, SegB s1, const StepsB& sp, int B, int H, float beta, f
   constexpr int threads = (NC + 2) * 32;
   static int per_sm = 0;
   if (per_sm == 0) {
-    cudaFuncSetAttribute((const void*)k_eprop_block<K, NC, U, NS, CB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eprop_block<K, NC, U, NS, CB, NT>, threads, smem);
+    cudaFuncSetAttribute((const void*)k_eprop_block<K, NC, U, NS, CB, NT, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eprop_block<K, NC, U, NS, CB, NT, MB>, threads, smem);
     if (per_sm < 1) per_sm = 1;
   }
   const int tiles = s0.tiles + s1.tiles;
   int cap = per_sm;
   if (const char* e = getenv("SW_EPB_PER_SM")) cap = max(1, min(per_sm, atoi(e)));
   const int workers = tiles ? min(tiles, 148 * cap) : 0;
-  k_eprop_block<K, NC, U, NS, CB, NT><<<ro_blocks + workers, threads, smem, st>>>(s0, s1, sp, B, H, beta, rho, alpha,
+  k_eprop_block<K, NC, U, NS, CB, NT, MB><<<ro_blocks + workers, threads, smem, st>>>(s0, s1, sp, B, H, beta, rho, alpha,
                                                                       g_w_out, g_b_out, C, workers, tickets);
   sw::count_launch();
   return SW_OK;
@@ -545,7 +545,10 @@ extern "C" int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, 
         case 4616: rc = launch_block<8, 4, 1, 6, 16, 2>(SW_EPB_ARGS); break;
         case 4432: rc = launch_block<8, 4, 1, 4, 32, 2>(SW_EPB_ARGS); break;
         case 4316: rc = launch_block<8, 4, 1, 3, 16, 2>(SW_EPB_ARGS); break;
-        default: rc = launch_block<8, 4, 1, 4, 16, 2>(SW_EPB_ARGS); break;
+        case 4416: rc = launch_block<8, 4, 1, 4, 16, 2>(SW_EPB_ARGS); break;
+        // default: <= 85 registers (4 CTAs/SM by registers), so a CTA also
+        // fits next to 3 forward blocks of the overlapping k_clf_step launch
+        default: rc = launch_block<8, 4, 1, 4, 16, 2, 4>(SW_EPB_ARGS); break;
       }
       break;
   }
