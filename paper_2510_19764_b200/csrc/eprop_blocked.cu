@@ -21,10 +21,14 @@
 // Readout gradients (classifier.py:221-222) for the k steps are reduced by
 // extra blocks of the same launch, placed after the streaming workers so
 // they fill the SMs idle in the tile-granular tail.
-// Timing notes (C1, one B200, graph replay, 4 steps): streaming alone 35 us
-// (88 % of the eps/ebar HBM bytes at the measured peak); the full pass ~98 us:
-// the per-element recursion, the K*3 gathers per element and the float64
-// chains add ~63 us on top (latency/issue bound).
+// Timing notes (C1, one B200, graph replay; ablation builds since removed):
+// K = 4: the eps/ebar stream alone 35 us (88 % of the measured HBM peak on
+// its bytes), the full pass ~98 us.  K = 8 (the trainer's): full pass 179 us;
+// without the float64 chains 179 us (hidden behind the recursion); without
+// the recursion 98 us; without both 66 us (stream + readout).  With every
+// gather forced onto L1-resident lines 172 us: the recursion is issue-bound
+// (~15 instructions per element-step at ~2 IPC), not gather-latency-bound
+// (see DESIGN.md 4).
 #include "common.cuh"
 #include "sm100_async.cuh"
 
