@@ -238,6 +238,35 @@ __device__ void readout_split(int r, int B, int H, const StepsB& sp, double* g_w
   }
 }
 
+// packed float32x2 (FADD2 / FMUL2 on sm_100): two separately rounded IEEE
+// ops.  Only adds, subtracts and the final product (stored, never added)
+// are packed: ptxas contracts mul.rn.f32x2 feeding add.rn.f32x2 into FFMA2
+// even under -fmad=false, so the products that feed adds stay scalar
+// __fmul_rn, which it does not contract.
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void up2(unsigned long long r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
 __device__ __forceinline__ const SegB& seg_of(const SegB& s0, const SegB& s1, int tile, int& lt) {
   if (tile < s0.tiles) { lt = tile; return s0; }
   lt = tile - s0.tiles;
@@ -401,6 +430,35 @@ k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, 
               l[v][q] = __ldg(sp.lsig[q] + oh);
             }
           }
+          if constexpr (U == 2) {
+            // two replicas per thread: the adds and the term product packed
+            const int ba = bl0 + u0, bb = bl0 + u0 + 1;
+            if (ba < nb) {
+              const bool okb = bb < nb;
+              float epa = st.eps[ba][lane], eba = st.ebar[ba][lane];
+              float epb = okb ? st.eps[bb][lane] : 0.f, ebb = okb ? st.ebar[bb][lane] : 0.f;
+#pragma unroll
+              for (int q = 0; q < K; ++q) {
+                float xa, xb;
+                up2(sub2(pk2(zb[0][q], zb[1][q]), pk2(__fmul_rn(beta, epa), __fmul_rn(beta, epb))), xa, xb);
+                const unsigned long long ee = pk2(__fmul_rn(p[0][q], xa), __fmul_rn(p[1][q], xb));
+                const unsigned long long ebn = add2(pk2(__fmul_rn(alpha, eba), __fmul_rn(alpha, ebb)), ee);
+                const unsigned long long epn = add2(pk2(__fmul_rn(rho, epa), __fmul_rn(rho, epb)), ee);
+                float ta, tb;
+                up2(mul2(pk2(l[0][q], l[1][q]), ebn), ta, tb);
+                up2(ebn, eba, ebb);
+                up2(epn, epa, epb);
+                terms[q][ba][lane] = ta;
+                if (okb) terms[q][bb][lane] = tb;
+              }
+              st.ebar[ba][lane] = eba;
+              st.eps[ba][lane] = epa;
+              if (okb) {
+                st.ebar[bb][lane] = ebb;
+                st.eps[bb][lane] = epb;
+              }
+            }
+          } else {
 #pragma unroll
           for (int v = 0; v < U; ++v) {
             const int bl = bl0 + u0 + v;
@@ -417,6 +475,7 @@ k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, 
               st.ebar[bl][lane] = eb;
               st.eps[bl][lane] = ep;
             }
+          }
           }
         }
         sw::fence_proxy_async_smem();
@@ -536,6 +595,7 @@ extern "C" int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, 
     case 4:
       switch (cfg) {
         case 8332: rc = launch_block<4, 8, 1, 3, 32, 3>(SW_EPB_ARGS); break;
+        case 8333: rc = launch_block<4, 8, 2, 4, 32, 2>(SW_EPB_ARGS); break;     // "8x3x33": K=4 packed pairs
         case 8816: rc = launch_block<4, 8, 1, 8, 16, 2>(SW_EPB_ARGS); break;
         default: rc = launch_block<4, 8, 1, 4, 32, 2>(SW_EPB_ARGS); break;
       }
@@ -550,6 +610,8 @@ extern "C" int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, 
         case 4432: rc = launch_block<8, 4, 1, 4, 32, 2>(SW_EPB_ARGS); break;
         case 4316: rc = launch_block<8, 4, 1, 3, 16, 2>(SW_EPB_ARGS); break;
         case 4416: rc = launch_block<8, 4, 1, 4, 16, 2>(SW_EPB_ARGS); break;
+        case 4419: rc = launch_block<8, 4, 2, 4, 16, 2, 4>(SW_EPB_ARGS); break;   // "4x4x19": packed pairs
+        case 4420: rc = launch_block<8, 4, 2, 4, 16, 2, 3>(SW_EPB_ARGS); break;   // "4x4x20": packed pairs, <= 113 regs
         // default: <= 85 registers (4 CTAs/SM by registers), so a CTA also
         // fits next to 3 forward blocks of the overlapping k_clf_step launch
         default: rc = launch_block<8, 4, 1, 4, 16, 2, 4>(SW_EPB_ARGS); break;
