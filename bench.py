@@ -338,6 +338,62 @@ def run_mupdate(fracs=(0.001, 0.01, 0.1), P=1 << 20, N=65536, cap=1024, seed=1):
             "bucket_build_ms": round(build_ms, 3), "bucket_refresh_ms": round(refresh_ms, 3)}
 
 
+def cpu_micro_sample(P=16384, N=65536, cap=1024, seed=1, fracs=(0.001, 0.01, 0.1),
+                     qs=(0.001, 0.01, 0.1)):
+    """CPU baseline of the M-update and M-prop microbenchmarks (BASELINE.md
+    section 3): the oracle port (numpy restatement of deep_r.py:81-160 and
+    connectivity.py:139-148, one thread) on a 16 384-row slice with the GPU
+    instance's row statistics (R ~ 512, cap 1024, N = 65 536, 4 float64
+    planes), extrapolated x (2^20 / P).  Test infrastructure, timed only."""
+    import time
+    from oracle.deep_r import DeepROracle
+    from oracle.ragged import Ragged, bf_words, propagate_spikes as prop_oracle
+    from oracle.updates import OracleModel
+    rs = np.random.default_rng(seed)
+    planes = ("w", "grad", "adam_m", "adam_v")
+    m = Ragged(P, N, cap, planes)
+    rl = np.minimum(rs.binomial(N, 512.0 / N, size=P), cap).astype(np.int32)
+    for i in range(P):
+        m.target[i, :rl[i]] = np.sort(rs.choice(N, rl[i], replace=False))
+    m.row_length[:] = rl
+    mask = m.slot_mask()
+    m.planes["w"][:] = rs.normal(0.0, 0.1, m.target.shape) * mask
+    dr = DeepROracle(m, l1=0.0)
+    W = bf_words(N)
+    rows = np.broadcast_to(np.arange(P)[:, None], m.target.shape)[mask]
+    t = m.target[mask].astype(np.int64)
+    bit = np.left_shift(np.uint64(1), (t & 63).astype(np.uint64))
+    np.bitwise_or.at(dr.conn, (rows, t >> 6), bit)
+    pos = m.planes["w"][mask] > 0
+    np.bitwise_or.at(dr.sign, (rows[pos], (t >> 6)[pos]), bit[pos])
+    assert dr.conn.shape[1] == W
+    om = OracleModel(seed)
+    om.add_matrix("M", m)
+    dr.register(om, "deep_r", "M")
+    scale = (1 << 20) / P
+    upd = []
+    for f in fracs:
+        flips = (rs.random(m.target.shape) < f) & m.slot_mask()
+        m.planes["w"][flips] *= -1.0
+        t0 = time.perf_counter()
+        om.run_update_group("deep_r")
+        dt = time.perf_counter() - t0
+        upd.append({"flip": f, "slice_s": round(dt, 3), "removed": int(dr.last_removed),
+                    "extrapolated_ms": round(dt * scale * 1e3, 1)})
+    prop = []
+    out = np.zeros(N)
+    for q in qs:
+        spikes = np.flatnonzero(rs.random(P) < q)
+        t0 = time.perf_counter()
+        prop_oracle(m, m.planes["w"], spikes, out)
+        dt = time.perf_counter() - t0
+        prop.append({"q": q, "slice_ms": round(dt * 1e3, 3), "extrapolated_us": round(dt * scale * 1e6, 1)})
+    return {"kind": "port", "cores": 1, "rows_sampled": P,
+            "sample": f"{P}-row slice (R~512, cap {cap}, N={N}, 4 float64 planes), oracle port "
+                      f"(numpy, 1 thread), timed on the host and extrapolated x{scale:g} to 2^20 rows",
+            "update": upd, "propagate": prop}
+
+
 def run_topomap_sweep(scales=(1, 2, 4, 8, 16), model_ms=100.0, seed=1, process_group=None):
     """Topographic-map simulation speed (x realtime) vs network size,
     TopomapModel(s) semantics, no recorder, stimulus rates computed on the
@@ -535,6 +591,8 @@ def run_device(args, w):
             del tr
             torch.cuda.empty_cache()
             line["mupdate"] = run_mupdate()
+            if not args.no_cpu_baseline:
+                line["mupdate"]["cpu_baseline"] = cpu_micro_sample()
             line["topomap"] = run_topomap_sweep()
     if ws > 1 and not args.no_micro:
         # every rank takes part in the sharded topomap sweep
