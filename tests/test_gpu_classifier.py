@@ -284,3 +284,50 @@ def test_grouped_forward_equals_single_steps(dev_lib):
         assert torch.equal(getattr(a, name), getattr(b, name)), name
     for name in ("_slots_zbar", "_slots_xbar", "_slots_psi", "_slots_lsig", "_slots_d"):
         assert torch.equal(getattr(a, name), getattr(b, name)), name
+
+
+def test_forward_currents_are_ascending_pre_sequential_sums(dev_lib):
+    """k_clf_step's event-driven propagation: per post, the float32 sum of the
+    spiking rows' weights in ascending pre order, starting from 0 (the order
+    the staging/sort phases must preserve).  Spikes are forced: p_in in
+    {0, 1} and a chosen hidden z; v = a = 0, so after one step
+    v = f32(alpha * (0 - z*v_thr)) + rec + ext exactly."""
+    import ctypes
+    from paper_2510_19764_b200 import _lib
+    from paper_2510_19764_b200.classifier import EpropClassifierTrainer, SyntheticTask
+    task = SyntheticTask(num_classes=5, num_inputs=300, example_steps=10, seed=7)
+    tr = EpropClassifierTrainer(task, hidden=200, batch_size=6, seed=7, deep_r=False,
+                                input_density=0.3, recurrent_density=0.25, use_graph=False)
+    ids = task.train_ids(0, tr.batch_size)
+    tr._upload_batch(ids)
+    tr._prepare(False)
+    rs = np.random.default_rng(7)
+    B, NI, H = tr.batch_size, task.num_inputs, tr.hidden
+    pin = (rs.random((B, NI)) < 0.5).astype(np.float64)
+    z = (rs.random((B, H)) < 0.3).astype(np.float32)
+    tr.p_in.copy_(torch.from_numpy(pin))
+    tr.z.copy_(torch.from_numpy(z))
+    prm = tr._step_params(0)
+    _lib.call("sw_clf_step", ctypes.byref(prm), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    v = tr.v.cpu().numpy()
+    f32 = np.float32
+    p = tr.params
+    alpha, vthr = f32(p.alpha), f32(p.v_thr)
+
+    def sums(m, w32, spiking):
+        rl, tg = m.row_length.cpu().numpy(), m.target.cpu().numpy()
+        acc = np.zeros(H, np.float32)
+        for x in np.flatnonzero(spiking):          # ascending pre
+            for s in range(rl[x]):
+                acc[tg[x, s]] = f32(acc[tg[x, s]] + w32[x, s])
+        return acc
+
+    w_in, w_rec = tr.w32_in.cpu().numpy(), tr.w32_rec.cpu().numpy()
+    for b in range(B):
+        ext = sums(tr.m_in, w_in, pin[b] == 1.0)
+        rec = sums(tr.m_rec, w_rec, z[b] != 0)
+        for h in range(H):
+            vv = f32(alpha * f32(f32(0) - f32(z[b, h] * vthr)))
+            vv = f32(f32(vv + rec[h]) + ext[h])
+            assert v[b, h] == vv, (b, h)
