@@ -193,3 +193,23 @@ def run_topomap(rank, world, steps, side=16, seed=4):
     state["V"] = V
     state["range"] = np.array([lo, hi])
     return state
+
+
+def device_trainer_dp(rank, world, port, out):
+    """Device trainer with a process group (batch DP over gloo on one GPU):
+    each rank trains its batch shard; returns what must agree across ranks."""
+    from paper_2510_19764_b200.classifier import EpropClassifierTrainer, SyntheticTask
+    from paper_2510_19764_b200.sharding import shard_batch
+    _init(rank, world, port)
+    try:
+        task = SyntheticTask(num_classes=3, num_inputs=20, example_steps=40, seed=4)
+        B = 8
+        tr = EpropClassifierTrainer(task, hidden=24, batch_size=B, seed=4, deep_r=True,
+                                    input_density=0.3, recurrent_density=0.2,
+                                    process_group=dist.group.WORLD, local_batch=shard_batch(B, rank, world))
+        hist = [tr.train_batch(k) for k in range(2)]
+        w = tr.s_in.planes["w"].cpu().numpy()
+        out.put((rank, [(h["loss"], h["removed"]) for h in hist], w,
+                 hashlib.sha256(tr.connectivity_fingerprint()).hexdigest()))
+    finally:
+        dist.destroy_process_group()
