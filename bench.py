@@ -113,9 +113,12 @@ def dist_setup(n_gpus):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if ws > 1:
         lr = int(os.environ.get("LOCAL_RANK", "0"))
-        torch.cuda.set_device(lr)
-        dist.init_process_group("nccl")
-        return dist.get_rank(), ws, lr
+        # SW_BENCH_BACKEND=gloo exercises the multi-rank path on fewer GPUs
+        # than ranks (validation only: ranks then share a device)
+        backend = os.environ.get("SW_BENCH_BACKEND", "nccl")
+        torch.cuda.set_device(lr % torch.cuda.device_count())
+        dist.init_process_group(backend)
+        return dist.get_rank(), ws, lr % torch.cuda.device_count()
     return 0, 1, 0
 
 
