@@ -36,7 +36,7 @@ from .updates import Model
 # recursion steps to every (replica, synapse) element
 EPROP_BLOCK_STEPS = int(os.environ.get("SW_EPROP_BLOCK_STEPS", "8"))
 # (step, replica) splits of the readout gradient inside the blocked pass
-READOUT_SPLITS = 32
+READOUT_SPLITS = int(os.environ.get("SW_READOUT_SPLITS", "16"))
 
 
 @dataclass

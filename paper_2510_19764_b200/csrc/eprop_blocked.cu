@@ -137,65 +137,91 @@ __device__ void readout_block_k(int r, int B, int H, const StepsB& sp, double* g
   }
 }
 
-// Split readout (sp.ro_scratch != NULL): block r = (h-tile, group of kRoCG
-// classes, split s of the k*B (step, replica) pairs).  Lane = h, kRoCG float64
-// accumulators; the warps of the block take consecutive pair ranges and are
-// combined in warp order.  The block writes its partial to
-//   partial[s][c][h]  (ro_scratch[0 : S*C*H]),  partial_b[s][c] (next S*C),
-// and the last block of its (h-tile, class group) -- counters after the
+// Split readout (sp.ro_scratch != NULL): block r = (64-unit h-tile, group
+// of kRoCG classes, split s of the k*B (step, replica) pairs).  The block
+// stages the d values of its pairs in shared memory (one coalesced pass),
+// then every lane accumulates two hidden units (float2 zbar loads, 4 pairs
+// in flight) in float64 for the kRoCG classes; the warps take consecutive
+// pair ranges and are combined in warp order.  The block writes its partial
+// to partial[s][c][h] (ro_scratch[0 : S*C*H]) and partial_b[s][c] (next
+// S*C), and the last block of its (h-tile, class group) -- counters after the
 // partials, zeroed by the caller and reset here -- adds the S partials in
 // split order to g_w_out / g_b_out.  Deterministic; the (step, replica)
 // summation order differs from the single-step kernel only in its grouping.
 constexpr int kRoCG = 4;
-constexpr int kRoU = 2;
+constexpr int kRoH = 64;      // hidden units per readout block (2 per lane)
+constexpr int kRoU = 4;
+constexpr int kRoFixed = kMaxWarps * kRoCG * kRoH + kMaxWarps * kRoCG + 2;   // doubles before the d stage
 
 __device__ void readout_split(int r, int B, int H, const StepsB& sp, double* g_w_out, double* g_b_out,
-                              int C, double* smem) {
-  double (*part)[kRoCG][32] = reinterpret_cast<double (*)[kRoCG][32]>(smem);
-  double (*partb)[kRoCG] = reinterpret_cast<double (*)[kRoCG]>(smem + kMaxWarps * kRoCG * 32);
-  unsigned* flag = reinterpret_cast<unsigned*>(smem + kMaxWarps * kRoCG * 33);
+                              int C, double* smem, int smem_doubles) {
+  double* part = smem;                                   // [kMaxWarps][kRoCG][kRoH]
+  double* partb = part + kMaxWarps * kRoCG * kRoH;       // [kMaxWarps][kRoCG]
+  unsigned* flag = reinterpret_cast<unsigned*>(partb + kMaxWarps * kRoCG);
+  double* sd = smem + kRoFixed;                          // staged d of a pair chunk [pair][kRoCG]
+  const int cap = (smem_doubles - kRoFixed) / kRoCG;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
   const int S = sp.ro_splits;
   const int ncg = (C + kRoCG - 1) / kRoCG;
   const int sidx = r % S, grp = r / S;
   const int cg = grp % ncg, ht = grp / ncg;
-  const int h = ht * 32 + lane, c0 = cg * kRoCG;
+  const int h0 = ht * kRoH + 2 * lane, c0 = cg * kRoCG;
+  const bool ok0 = h0 < H, ok1 = h0 + 1 < H;
+  const bool vec = (H & 1) == 0;
   const int pairs = sp.k * B;
   const int p0 = (int)((int64_t)pairs * sidx / S), p1 = (int)((int64_t)pairs * (sidx + 1) / S);
-  const int per = (p1 - p0 + nw - 1) / nw;
-  const int w0 = p0 + warp * per, w1 = min(p1, w0 + per);
-  double acc[kRoCG], accb[kRoCG];
+  double acc[kRoCG][2], accb[kRoCG];
 #pragma unroll
-  for (int c = 0; c < kRoCG; ++c) acc[c] = accb[c] = 0.0;
-  for (int j = w0; j < w1; j += kRoU) {
-    float zv[kRoU];
-    double dv[kRoU][kRoCG];
-#pragma unroll
-    for (int u = 0; u < kRoU; ++u) {
-      const int jj = min(j + u, w1 - 1);
-      const int q = jj / B, b = jj - q * B;
-      zv[u] = h < H ? __ldg(sp.zbar[q] + (int64_t)b * H + h) : 0.0f;
-#pragma unroll
-      for (int c = 0; c < kRoCG; ++c)
-        dv[u][c] = c0 + c < C ? __ldg(sp.d[q] + (int64_t)b * C + c0 + c) : 0.0;
+  for (int c = 0; c < kRoCG; ++c) acc[c][0] = acc[c][1] = accb[c] = 0.0;
+  for (int q0 = p0; q0 < p1; q0 += cap) {
+    const int q1 = min(p1, q0 + cap);
+    __syncthreads();
+    for (int x = threadIdx.x; x < (q1 - q0) * kRoCG; x += blockDim.x) {
+      const int j = q0 + x / kRoCG, c = x % kRoCG;
+      const int q = j / B, b = j - q * B;
+      sd[x] = c0 + c < C ? __ldg(sp.d[q] + (int64_t)b * C + c0 + c) : 0.0;
     }
+    __syncthreads();
+    const int per = (q1 - q0 + nw - 1) / nw;
+    const int w0 = q0 + warp * per, w1 = min(q1, w0 + per);
+    for (int j = w0; j < w1; j += kRoU) {
+      float2 zv[kRoU];
 #pragma unroll
-    for (int u = 0; u < kRoU; ++u) {
-      if (j + u < w1) {
+      for (int u = 0; u < kRoU; ++u) {
+        const int jj = min(j + u, w1 - 1);
+        const int q = jj / B, b = jj - q * B;
+        const float* zr = sp.zbar[q] + (int64_t)b * H + h0;
+        if (vec && ok1) {
+          zv[u] = __ldg(reinterpret_cast<const float2*>(zr));
+        } else {
+          zv[u].x = ok0 ? __ldg(zr) : 0.0f;
+          zv[u].y = ok1 ? __ldg(zr + 1) : 0.0f;
+        }
+      }
 #pragma unroll
-        for (int c = 0; c < kRoCG; ++c) {
-          acc[c] = __dadd_rn(acc[c], __dmul_rn(dv[u][c], (double)zv[u]));
-          accb[c] = __dadd_rn(accb[c], dv[u][c]);
+      for (int u = 0; u < kRoU; ++u) {
+        if (j + u < w1) {
+          const double* dr = sd + (j + u - q0) * kRoCG;
+#pragma unroll
+          for (int c = 0; c < kRoCG; ++c) {
+            const double dv = dr[c];
+            acc[c][0] = __dadd_rn(acc[c][0], __dmul_rn(dv, (double)zv[u].x));
+            acc[c][1] = __dadd_rn(acc[c][1], __dmul_rn(dv, (double)zv[u].y));
+            accb[c] = __dadd_rn(accb[c], dv);
+          }
         }
       }
     }
   }
 #pragma unroll
-  for (int c = 0; c < kRoCG; ++c) part[warp][c][lane] = acc[c];
+  for (int c = 0; c < kRoCG; ++c) {
+    part[(warp * kRoCG + c) * kRoH + 2 * lane] = acc[c][0];
+    part[(warp * kRoCG + c) * kRoH + 2 * lane + 1] = acc[c][1];
+  }
   if (lane == 0) {
 #pragma unroll
-    for (int c = 0; c < kRoCG; ++c) partb[warp][c] = accb[c];
+    for (int c = 0; c < kRoCG; ++c) partb[warp * kRoCG + c] = accb[c];
   }
   __syncthreads();
   double* partial = sp.ro_scratch;
@@ -204,12 +230,15 @@ __device__ void readout_split(int r, int B, int H, const StepsB& sp, double* g_w
   if (warp == 0) {
 #pragma unroll
     for (int c = 0; c < kRoCG; ++c) {
-      double t = 0.0;
-      for (int w = 0; w < nw; ++w) t = __dadd_rn(t, part[w][c][lane]);
-      if (c0 + c < C && h < H) partial[((int64_t)sidx * C + c0 + c) * H + h] = t;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        double t = 0.0;
+        for (int w = 0; w < nw; ++w) t = __dadd_rn(t, part[(w * kRoCG + c) * kRoH + 2 * lane + i]);
+        if (c0 + c < C && h0 + i < H) partial[((int64_t)sidx * C + c0 + c) * H + h0 + i] = t;
+      }
       if (lane == 0 && c0 + c < C) {
         double tb = 0.0;
-        for (int w = 0; w < nw; ++w) tb = __dadd_rn(tb, partb[w][c]);
+        for (int w = 0; w < nw; ++w) tb = __dadd_rn(tb, partb[w * kRoCG + c]);
         partial_b[(int64_t)sidx * C + c0 + c] = tb;
       }
     }
@@ -222,10 +251,14 @@ __device__ void readout_split(int r, int B, int H, const StepsB& sp, double* g_w
 #pragma unroll
       for (int c = 0; c < kRoCG; ++c) {
         if (c0 + c >= C) continue;
-        if (h < H) {
-          double t = 0.0;
-          for (int x = 0; x < S; ++x) t = __dadd_rn(t, __ldcg(partial + ((int64_t)x * C + c0 + c) * H + h));
-          g_w_out[(int64_t)(c0 + c) * H + h] += t;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (h0 + i < H) {
+            double t = 0.0;
+            for (int x = 0; x < S; ++x)
+              t = __dadd_rn(t, __ldcg(partial + ((int64_t)x * C + c0 + c) * H + h0 + i));
+            g_w_out[(int64_t)(c0 + c) * H + h0 + i] += t;
+          }
         }
         if (ht == 0 && lane == 0) {
           double tb = 0.0;
@@ -292,7 +325,8 @@ k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, 
   // the tile-granular streaming work leaves idle at its end
   if ((int)blockIdx.x >= workers) {
     if (sp.ro_scratch)
-      readout_split(blockIdx.x - workers, B, H, sp, g_w_out, g_b_out, C, reinterpret_cast<double*>(smem_raw));
+      readout_split(blockIdx.x - workers, B, H, sp, g_w_out, g_b_out, C, reinterpret_cast<double*>(smem_raw),
+                    (int)(sizeof(Smem<K, CB, NS, NT>) / sizeof(double)));
     else
       readout_block_k(blockIdx.x - workers, B, H, sp, g_w_out, g_b_out, C, reinterpret_cast<double*>(smem_raw));
   } else {
@@ -502,7 +536,7 @@ int launch_block(SegB s0, SegB s1, const StepsB& sp, int B, int H, float beta, f
                  double* g_w_out, double* g_b_out, int C, int ro_blocks, unsigned* tickets,
                  cudaStream_t st) {
   static_assert(NC + 2 <= kMaxWarps && CB % NC == 0, "eprop block configuration");
-  static_assert(sizeof(Smem<K, CB, NS, NT>) >= kMaxWarps * 34 * sizeof(double), "readout scratch");
+  static_assert(sizeof(Smem<K, CB, NS, NT>) >= (kRoFixed + 64 * kRoCG) * sizeof(double), "readout scratch");
   const int smem = (int)sizeof(Smem<K, CB, NS, NT>);
   constexpr int threads = (NC + 2) * 32;
   static int per_sm = 0;
@@ -581,7 +615,7 @@ extern "C" int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, 
   sp.ro_splits = blk->ro_splits > 0 ? blk->ro_splits : 1;
   const int htiles = (hidden + 31) / 32;
   const int ro_blocks = !readout ? 0
-                        : sp.ro_scratch ? htiles * ((num_classes + kRoCG - 1) / kRoCG) * sp.ro_splits
+                        : sp.ro_scratch ? ((hidden + kRoH - 1) / kRoH) * ((num_classes + kRoCG - 1) / kRoCG) * sp.ro_splits
                                         : num_classes * htiles;
   if (s[0].tiles + s[1].tiles + ro_blocks == 0 || batch <= 0) return SW_OK;
   cudaStream_t st = (cudaStream_t)stream;
