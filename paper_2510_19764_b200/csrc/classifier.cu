@@ -15,6 +15,9 @@
 //   6. ALIF step with the new currents (neurons.py:60-67).
 #include "common.cuh"
 
+#include <cstdlib>
+#include <type_traits>
+
 namespace {
 
 // k_clf_step is instantiated for 256 and 512 threads per replica block
@@ -62,24 +65,40 @@ __device__ long long g_clf_prof[16];
 #define PROF(i) do { } while (0)
 #endif
 
-template <int kThreads>
-__device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P) {
+// kCompact: 16-bit row lengths, bucket offsets and sorted-row indices (the
+// layout of large layers, to keep 4 blocks per SM); else 32-bit
+template <int kThreads, bool kCompact>
+__device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_arg, int rcap_arg) {
+  using idx_t = typename std::conditional<kCompact, uint16_t, int>::type;
+  // the 32-bit layout uses the compile-time capacities (kStageCap, all rows)
+  const int scap = kCompact ? scap_arg : kStageCap;
+  const int rcap = kCompact ? rcap_arg : P.num_inputs + P.hidden;
   constexpr int kWarps = kThreads / 32;
   extern __shared__ unsigned char smem_raw[];
   const int H = P.hidden, NI = P.num_inputs, C = P.num_classes;
   const int NT = NI + H;
-  float* acc_ext = (float*)smem_raw;
-  float* acc_rec = acc_ext + H;
-  int* rlen = (int*)(acc_rec + H);          // [NT] row lengths (inputs | hidden)
-  int* list = rlen + NT;                    // [NT] spiking rows, ascending (inputs | hidden)
-  int* roff = list + NT;                    // [NT + 1]
-  int* st_kr = roff + NT + 1;               // [kStageCap] key | row << 16
-  float* st_w = (float*)(st_kr + kStageCap); // [kStageCap]
-  int* srow = (int*)(st_w + kStageCap);      // [kStageCap] sorted by key
-  float* sw_ = (float*)(srow + kStageCap);   // [kStageCap]
-  int* koff = (int*)(sw_ + kStageCap);       // [2H + 1] key offsets
-  int* kcur = koff + 2 * H + 1;              // [2H] counts, then cursors
-  double* yv = (double*)(((uintptr_t)(kcur + 2 * H) + 15) & ~(uintptr_t)15);
+  // shared-memory layout (clf_smem_bytes on the host mirrors it); scap
+  // staged entries and rcap spiking rows are the capacities of the staged
+  // propagation path (beyond them: the warp-serial fallback)
+  // byte offsets into smem_raw (not integer-cast pointers, which would turn
+  // the shared-memory accesses into generic ones)
+  size_t o = 0;
+  float* acc_ext = (float*)(smem_raw + o); o += (size_t)H * 4;
+  float* acc_rec = (float*)(smem_raw + o); o += (size_t)H * 4;
+  idx_t* rlen = (idx_t*)(smem_raw + o);   o += (size_t)NT * sizeof(idx_t);    // [NT] row lengths
+  o = (o + 3) & ~(size_t)3;
+  int* list = (int*)(smem_raw + o);       o += (size_t)NT * 4;                // [NT] spiking rows, ascending
+  int* roff = (int*)(smem_raw + o);       o += (size_t)(rcap + 1) * 4;        // [rcap + 1]
+  int* st_kr = (int*)(smem_raw + o);      o += (size_t)scap * 4;              // [scap] key | row << 16
+  float* st_w = (float*)(smem_raw + o);   o += (size_t)scap * 4;              // [scap]
+  idx_t* srow = (idx_t*)(smem_raw + o);   o += (size_t)scap * sizeof(idx_t);  // [scap] sorted by key
+  o = (o + 3) & ~(size_t)3;
+  float* sw_ = (float*)(smem_raw + o);    o += (size_t)scap * 4;              // [scap]
+  idx_t* koff = (idx_t*)(smem_raw + o);   o += (size_t)(2 * H + 1) * sizeof(idx_t);   // [2H + 1] key offsets
+  o = (o + 3) & ~(size_t)3;
+  int* kcur = (int*)(smem_raw + o);       o += (size_t)2 * H * 4;             // [2H] counts, then cursors
+  o = (o + 15) & ~(size_t)15;
+  double* yv = (double*)(smem_raw + o);
   double* dv = yv + C;
   __shared__ int2 wsum[kWarps];
   __shared__ int s_nx, s_nrows, s_total;
@@ -96,7 +115,7 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P) {
   const float z0 = h0_ok ? P.z[bH + threadIdx.x] : 0.f;
   // P0: row lengths to shared memory; zero the current accumulators
   for (int x = threadIdx.x; x < NT; x += kThreads)
-    rlen[x] = (x < NI) ? __ldg(P.in_row_length + x) : __ldg(P.rec_row_length + (x - NI));
+    rlen[x] = (idx_t)((x < NI) ? __ldg(P.in_row_length + x) : __ldg(P.rec_row_length + (x - NI)));
   for (int h = threadIdx.x; h < H; h += kThreads) {
     acc_ext[h] = 0.0f;
     acc_rec[h] = 0.0f;
@@ -154,13 +173,17 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P) {
   for (int j = 0; j < per; ++j) {
     if ((flags >> j) & 1u) {
       list[ec] = x0 + j;
-      roff[ec] = el;
+      if constexpr (kCompact) {
+        if (ec < rcap) roff[ec] = el;
+      } else {
+        roff[ec] = el;
+      }
       el += rlen[x0 + j];
       ++ec;
     }
   }
   if (threadIdx.x == 0) {
-    roff[tc] = tl;
+    if (!kCompact || tc <= rcap) roff[tc] = tl;
     s_nrows = tc;
     s_total = tl;
   }
@@ -183,7 +206,7 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P) {
   const int nrows = s_nrows, nx = s_nx, nz = nrows - nx;
   
   const int* zl = list + nx;   // hidden entries are NI + h
-  const bool staged = s_total <= kStageCap;
+  const bool staged = kCompact ? (s_total <= scap && nrows <= rcap) : (s_total <= kStageCap);
   // P3: stage every spiking row's (target, w) with coalesced loads; the
   // readout warps also issue their W_out gathers here
   // P3: stage every spiking row's (key = [in|rec] post, row, w) with
@@ -245,18 +268,18 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P) {
     for (int j = 0; j < kper; ++j) {
       if (k0 + j < NK) {
         const int c = kcur[k0 + j];
-        koff[k0 + j] = ex;
+        koff[k0 + j] = (idx_t)ex;
         kcur[k0 + j] = ex;
         ex += c;
       }
     }
-    if (threadIdx.x == 0) koff[NK] = tot;
+    if (threadIdx.x == 0) koff[NK] = (idx_t)tot;
     PROF(10);
     __syncthreads();
     for (int q = threadIdx.x; q < T; q += kThreads) {
       const int kr = st_kr[q];
       const int dst = atomicAdd(&kcur[kr & 0xFFFF], 1);
-      srow[dst] = kr >> 16;
+      srow[dst] = (idx_t)(kr >> 16);
       sw_[dst] = st_w[q];
     }
     PROF(11);
@@ -392,10 +415,10 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P) {
 // gap or tail between them.  zbar/xbar/psi/lsig/d are then the bases of
 // slot_count contiguous per-step slots ([slot][B][width]); step t writes slot
 // t % slot_count and reads the traces of slot (t - 1) % slot_count.
-template <int kThreads>
-__global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_clf_step(sw_clf_step_t P) {
+template <int kThreads, bool kCompact>
+__global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_clf_step(sw_clf_step_t P, int scap, int rcap) {
   if (P.n_steps <= 0) {
-    clf_step_body<kThreads>(P);
+    clf_step_body<kThreads, kCompact>(P, scap, rcap);
     return;
   }
   const int64_t B = P.batch, H = P.hidden, NI = P.num_inputs, C = P.num_classes;
@@ -413,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_clf_step(sw_clf_s
     Q.lsig = P.lsig + cur * B * H;
     Q.d = P.d + cur * B * C;
     if (s) __syncthreads();   // this block's step s-1 writes are visible to its step s
-    clf_step_body<kThreads>(Q);
+    clf_step_body<kThreads, kCompact>(Q, scap, rcap);
   }
 }
 
@@ -468,6 +491,24 @@ extern "C" __attribute__((visibility("default"))) int sw_debug_clf_prof(long lon
   return cudaMemcpyFromSymbol(out16, g_clf_prof, 16 * sizeof(long long)) == cudaSuccess ? 0 : SW_ERR_CUDA;
 }
 
+// bytes of clf_step_body's shared-memory layout
+size_t clf_smem_bytes(int H, int NI, int C, int scap, int rcap, bool compact) {
+  const size_t NT = (size_t)NI + H, ix = compact ? 2 : 4;
+  size_t o = (size_t)2 * H * 4;                 // acc_ext, acc_rec
+  o += NT * ix;                                 // rlen
+  o = (o + 3) & ~(size_t)3;
+  o += NT * 4 + (size_t)(rcap + 1) * 4;         // list, roff
+  o += (size_t)scap * 8;                        // st_kr, st_w
+  o += (size_t)scap * ix;                       // srow
+  o = (o + 3) & ~(size_t)3;
+  o += (size_t)scap * 4;                        // sw_
+  o += (size_t)(2 * H + 1) * ix;                // koff
+  o = (o + 3) & ~(size_t)3;
+  o += (size_t)2 * H * 4;                       // kcur
+  o = (o + 15) & ~(size_t)15;
+  return o + (size_t)2 * C * 8 + 16;            // yv, dv
+}
+
 extern "C" int sw_clf_step(const sw_clf_step_t* p, void* stream) {
   const int H = p->hidden, NI = p->num_inputs, C = p->num_classes;
   if (p->batch <= 0) return SW_OK;
@@ -479,18 +520,42 @@ extern "C" int sw_clf_step(const sw_clf_step_t* p, void* stream) {
     sw::set_last_error("clf_step: num_inputs + hidden must be <= 2048");
     return SW_ERR_INVALID_ARG;
   }
-  const size_t smem = (size_t)(2 * H) * 4 + (size_t)(NI + H) * 8 + (size_t)(NI + H + 1) * 4 +
-                      (size_t)kStageCap * 16 + (size_t)(4 * H + 1) * 4 + 16 + (size_t)2 * C * 8;
-  if (smem > 227 * 1024) { sw::set_last_error("clf_step: layer too large"); return SW_ERR_INVALID_ARG; }
-  if (p->hidden >= 512) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute((const void*)k_clf_step<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_clf_step<512><<<p->batch, 512, smem, (cudaStream_t)stream>>>(*p);
-  } else {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute((const void*)k_clf_step<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_clf_step<256><<<p->batch, 256, smem, (cudaStream_t)stream>>>(*p);
+  // 256-thread blocks (64 registers) reach 4 blocks per SM, i.e. one wave of
+  // the batch's replica blocks, if a block's shared memory stays <= ~56 KB:
+  // shrink the staged-path capacities (spiking rows, then staged entries;
+  // beyond them the warp-serial fallback runs) until it does; else 512-thread
+  // blocks.  SW_CLF_THREADS=512 forces the latter (measurement).
+  const int NT = NI + H;
+  const size_t budget = 56 * 1024;
+  int threads = 256, scap = kStageCap, rcap = NT;
+  bool compact = false;
+  size_t smem = clf_smem_bytes(H, NI, C, scap, rcap, false);
+  if (smem > budget) {
+    compact = true;
+    rcap = NT < 1024 ? NT : 1024;
+    smem = clf_smem_bytes(H, NI, C, scap, rcap, true);
+    if (smem > budget) { scap = 1536; smem = clf_smem_bytes(H, NI, C, scap, rcap, true); }
   }
+  const char* force = getenv("SW_CLF_THREADS");
+  if (smem > budget || (force && atoi(force) == 512)) {
+    threads = 512;
+    compact = false;
+    scap = kStageCap;
+    rcap = NT;
+    smem = clf_smem_bytes(H, NI, C, scap, rcap, false);
+  }
+  if (smem > 227 * 1024) { sw::set_last_error("clf_step: layer too large"); return SW_ERR_INVALID_ARG; }
+  cudaStream_t st = (cudaStream_t)stream;
+  const void* fn = threads == 512 ? (const void*)k_clf_step<512, false>
+                   : compact      ? (const void*)k_clf_step<256, true>
+                                  : (const void*)k_clf_step<256, false>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (threads == 512)
+    k_clf_step<512, false><<<p->batch, 512, smem, st>>>(*p, scap, rcap);
+  else if (compact)
+    k_clf_step<256, true><<<p->batch, 256, smem, st>>>(*p, scap, rcap);
+  else
+    k_clf_step<256, false><<<p->batch, 256, smem, st>>>(*p, scap, rcap);
   sw::count_launch();
   SW_CHECK_LAUNCH("sw_clf_step");
   return SW_OK;
