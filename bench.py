@@ -413,7 +413,7 @@ def run_topomap_sweep(scales=(1, 2, 4, 8, 16), model_ms=100.0, seed=1, process_g
                              rates_on_device=True, process_group=process_group)
         torch.cuda.synchronize()
         build_s = time.perf_counter() - t0
-        model.run(10.0)   # warm-up: capture + first replays
+        model.run(40.0)   # warm-up: graph captures, first replays, two stimulus changes
         torch.cuda.synchronize()
         if process_group is not None:
             dist.barrier(group=process_group)

@@ -35,6 +35,10 @@ BASE_SIDE = 16
 
 # sheets up to this size step in one single-CTA persistent launch per period
 PERSISTENT_MAX_NODES = 2048
+# rewiring periods captured per CUDA graph (a divisor of the periods per
+# stimulus interval is used): one replay per 10 ms of model time keeps the
+# host loop off the critical path for small sheets
+PERIODS_PER_GRAPH = 10
 
 
 @dataclass
@@ -226,7 +230,7 @@ class TopomapModel:
         self.spike_counts = torch.zeros(2, dtype=torch.int64, device="cuda")
         self._barrier = torch.zeros(2, dtype=torch.int32, device="cuda")
         self.step_index = 0
-        self._graph = None
+        self._graphs = {}        # periods per graph -> captured CUDA graph
         self._update_log = None
 
     def _init_projection(self, name, params, rng, headroom):
@@ -328,6 +332,13 @@ class TopomapModel:
         graph_ok = (self.use_graph and self.shard.world == 1 and not self.ff_rule.record_events
                     and not self.lat_rule.record_events and stim_steps % rewire_steps == 0)
         u0 = self.ff_rule._host_update if self.ff_rule._host_update else 0
+        # periods per replay: the largest divisor of the periods per stimulus
+        # interval that is <= PERIODS_PER_GRAPH (a replay never crosses a
+        # stimulus change)
+        multi = 1
+        if graph_ok:
+            stim_periods = stim_steps // rewire_steps
+            multi = max(d for d in range(1, min(PERIODS_PER_GRAPH, stim_periods) + 1) if stim_periods % d == 0)
         done = 0
         while done < n_steps:
             k = self.step_index
@@ -339,11 +350,13 @@ class TopomapModel:
                     self.source.probabilities(h)
                 record.stimulus_changes += 1
             if graph_ok and k % rewire_steps == 0 and n_steps - done >= rewire_steps:
-                self._replay_period(rewire_steps)
-                self.step_index += rewire_steps
-                done += rewire_steps
-                record.steps += rewire_steps
-                record.rewiring_executions += 1
+                span = multi * rewire_steps
+                periods = multi if ((k % stim_steps) % span == 0 and n_steps - done >= span) else 1
+                self._replay_period(rewire_steps, periods)
+                self.step_index += periods * rewire_steps
+                done += periods * rewire_steps
+                record.steps += periods * rewire_steps
+                record.rewiring_executions += periods
                 continue
             self._launch_step()
             self.step_index += 1
@@ -362,8 +375,12 @@ class TopomapModel:
             record.rewires_per_update.extend(int(x) for x in log.sum(axis=1))
         return record
 
-    def _replay_period(self, rewire_steps: int) -> None:
-        if self._graph is None:
+    def _replay_period(self, rewire_steps: int, periods: int = 1) -> None:
+        """Replay `periods` consecutive rewiring periods from one captured
+        graph (every per-period input -- step counter, update counters, RNG
+        keys -- lives on the device)."""
+        g = self._graphs.get(periods)
+        if g is None:
             # one eager period first (allocations, lazy init), then capture
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
@@ -376,7 +393,8 @@ class TopomapModel:
             try:
                 with torch.cuda.stream(s):
                     with torch.cuda.graph(g, stream=s):
-                        self._period(rewire_steps)
+                        for _ in range(periods):
+                            self._period(rewire_steps)
             finally:
                 self.net.timers.enabled = True
             torch.cuda.current_stream().wait_stream(s)
@@ -384,10 +402,10 @@ class TopomapModel:
             for (r, u), b, c in zip(saved, self.net.groups["rewiring"], counts):
                 r._host_update = u
                 b.update_count = c
-            self._graph = g
-        self._graph.replay()
+            self._graphs[periods] = g
+        g.replay()
         for r, b in zip((self.ff_rule, self.lat_rule), self.net.groups["rewiring"]):
-            b.update_count += 1
+            b.update_count += periods
             r._host_update = b.update_count
 
     def state_arrays(self) -> dict[str, np.ndarray]:
