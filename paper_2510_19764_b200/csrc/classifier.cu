@@ -68,7 +68,8 @@ __device__ long long g_clf_prof[16];
 // kCompact: 16-bit row lengths, bucket offsets and sorted-row indices (the
 // layout of large layers, to keep 4 blocks per SM); else 32-bit
 template <int kThreads, bool kCompact>
-__device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_arg, int rcap_arg) {
+__device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_arg, int rcap_arg,
+                                              bool load_rlen = true) {
   using idx_t = typename std::conditional<kCompact, uint16_t, int>::type;
   // the 32-bit layout uses the compile-time capacities (kStageCap, all rows)
   const int scap = kCompact ? scap_arg : kStageCap;
@@ -114,8 +115,11 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
   const float a0 = h0_ok ? P.a[bH + threadIdx.x] : 0.f;
   const float z0 = h0_ok ? P.z[bH + threadIdx.x] : 0.f;
   // P0: row lengths to shared memory; zero the current accumulators
-  for (int x = threadIdx.x; x < NT; x += kThreads)
-    rlen[x] = (idx_t)((x < NI) ? __ldg(P.in_row_length + x) : __ldg(P.rec_row_length + (x - NI)));
+  // (the row lengths stay in shared memory across the steps of a launch:
+  // the connectivity only changes between batches)
+  if (load_rlen)
+    for (int x = threadIdx.x; x < NT; x += kThreads)
+      rlen[x] = (idx_t)((x < NI) ? __ldg(P.in_row_length + x) : __ldg(P.rec_row_length + (x - NI)));
   for (int h = threadIdx.x; h < H; h += kThreads) {
     acc_ext[h] = 0.0f;
     acc_rec[h] = 0.0f;
@@ -436,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_clf_step(sw_clf_s
     Q.lsig = P.lsig + cur * B * H;
     Q.d = P.d + cur * B * C;
     if (s) __syncthreads();   // this block's step s-1 writes are visible to its step s
-    clf_step_body<kThreads, kCompact>(Q, scap, rcap);
+    clf_step_body<kThreads, kCompact>(Q, scap, rcap, s == 0);
   }
 }
 
