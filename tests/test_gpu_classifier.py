@@ -286,25 +286,30 @@ def test_grouped_forward_equals_single_steps(dev_lib):
         assert torch.equal(getattr(a, name), getattr(b, name)), name
 
 
-def test_forward_currents_are_ascending_pre_sequential_sums(dev_lib):
+@pytest.mark.parametrize("NI,H,din,drec,p_spk,z_spk", [
+    (300, 200, 0.3, 0.25, 0.5, 0.3),     # staged path, 32-bit layout
+    (300, 1024, 0.05, 0.02, 0.5, 0.3),   # staged path, compact 16-bit layout (large layer)
+    (300, 200, 0.3, 0.25, 1.0, 1.0),     # every row spikes: > 2048 entries, warp-serial fallback
+])
+def test_forward_currents_are_ascending_pre_sequential_sums(dev_lib, NI, H, din, drec, p_spk, z_spk):
     """k_clf_step's event-driven propagation: per post, the float32 sum of the
     spiking rows' weights in ascending pre order, starting from 0 (the order
-    the staging/sort phases must preserve).  Spikes are forced: p_in in
-    {0, 1} and a chosen hidden z; v = a = 0, so after one step
-    v = f32(alpha * (0 - z*v_thr)) + rec + ext exactly."""
+    the staging/sort phases and the fallback walk must preserve).  Spikes are
+    forced: p_in in {0, 1} and a chosen hidden z; v = a = 0, so after one
+    step v = f32(alpha * (0 - z*v_thr)) + rec + ext exactly."""
     import ctypes
     from paper_2510_19764_b200 import _lib
     from paper_2510_19764_b200.classifier import EpropClassifierTrainer, SyntheticTask
-    task = SyntheticTask(num_classes=5, num_inputs=300, example_steps=10, seed=7)
-    tr = EpropClassifierTrainer(task, hidden=200, batch_size=6, seed=7, deep_r=False,
-                                input_density=0.3, recurrent_density=0.25, use_graph=False)
+    task = SyntheticTask(num_classes=5, num_inputs=NI, example_steps=10, seed=7)
+    tr = EpropClassifierTrainer(task, hidden=H, batch_size=4, seed=7, deep_r=False,
+                                input_density=din, recurrent_density=drec, use_graph=False)
     ids = task.train_ids(0, tr.batch_size)
     tr._upload_batch(ids)
     tr._prepare(False)
     rs = np.random.default_rng(7)
     B, NI, H = tr.batch_size, task.num_inputs, tr.hidden
-    pin = (rs.random((B, NI)) < 0.5).astype(np.float64)
-    z = (rs.random((B, H)) < 0.3).astype(np.float32)
+    pin = (rs.random((B, NI)) < p_spk).astype(np.float64)
+    z = (rs.random((B, H)) < z_spk).astype(np.float32)
     tr.p_in.copy_(torch.from_numpy(pin))
     tr.z.copy_(torch.from_numpy(z))
     prm = tr._step_params(0)
