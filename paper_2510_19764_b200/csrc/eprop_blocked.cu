@@ -314,7 +314,9 @@ constexpr int smem_blocks() {
   return (233472 / per) < 3 ? ((233472 / per) < 1 ? 1 : 233472 / per) : 3;
 }
 
-template <int K, int NC, int U, int NS, int CB, int NT, int MB>
+// KH < K (U == 1 only): the K steps' gathers of a replica are loaded KH
+// steps at a time (fewer live registers, more resident warps)
+template <int K, int NC, int U, int NS, int CB, int NT, int MB, int KH>
 __global__ void __launch_bounds__((NC + 2) * 32, MB > 0 ? MB : smem_blocks<K, CB, NS, NT>())
 k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, float alpha,
               double* g_w_out, double* g_b_out, int C, int workers, unsigned* tickets) {
@@ -451,6 +453,41 @@ k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, 
         // 32-bit element offsets, one per replica for all K steps
 #pragma unroll kEpbUnroll
         for (int u0 = 0; u0 < kBPW; u0 += U) {
+          if constexpr (U == 1 && KH < K) {
+            const int bl = bl0 + u0;
+            const unsigned b = (unsigned)(ch * CB + min(bl, nb - 1));
+            const unsigned ot = b * (unsigned)P + (unsigned)pre;
+            const unsigned oh = b * (unsigned)H + (unsigned)post;
+            float ep = 0.f, eb = 0.f;
+            if (bl < nb) {
+              ep = st.eps[bl][lane];
+              eb = st.ebar[bl][lane];
+            }
+#pragma unroll
+            for (int q0 = 0; q0 < K; q0 += KH) {
+              float zh[KH], ph[KH], lh[KH];
+#pragma unroll
+              for (int q = 0; q < KH; ++q) {
+                zh[q] = __ldg(trace[q0 + q] + ot);
+                ph[q] = __ldg(sp.psi[q0 + q] + oh);
+                lh[q] = __ldg(sp.lsig[q0 + q] + oh);
+              }
+              if (bl < nb) {
+#pragma unroll
+                for (int q = 0; q < KH; ++q) {
+                  const float ee = __fmul_rn(ph[q], __fsub_rn(zh[q], __fmul_rn(beta, ep)));
+                  eb = __fadd_rn(__fmul_rn(alpha, eb), ee);
+                  ep = __fadd_rn(__fmul_rn(rho, ep), ee);
+                  terms[q0 + q][bl][lane] = __fmul_rn(lh[q], eb);
+                }
+              }
+            }
+            if (bl < nb) {
+              st.ebar[bl][lane] = eb;
+              st.eps[bl][lane] = ep;
+            }
+            continue;
+          }
           float zb[U][K], p[U][K], l[U][K];
 #pragma unroll
           for (int v = 0; v < U; ++v) {
@@ -531,7 +568,7 @@ k_eprop_block(SegB s0, SegB s1, StepsB sp, int B, int H, float beta, float rho, 
   }
 }
 
-template <int K, int NC, int U, int NS = 3, int CB = 32, int NT = 3, int MB = 0>
+template <int K, int NC, int U, int NS = 3, int CB = 32, int NT = 3, int MB = 0, int KH = K>
 int launch_block(SegB s0, SegB s1, const StepsB& sp, int B, int H, float beta, float rho, float alpha,
                  double* g_w_out, double* g_b_out, int C, int ro_blocks, unsigned* tickets,
                  cudaStream_t st) {
@@ -541,15 +578,15 @@ int launch_block(SegB s0, SegB s1, const StepsB& sp, int B, int H, float beta, f
   constexpr int threads = (NC + 2) * 32;
   static int per_sm = 0;
   if (per_sm == 0) {
-    cudaFuncSetAttribute((const void*)k_eprop_block<K, NC, U, NS, CB, NT, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eprop_block<K, NC, U, NS, CB, NT, MB>, threads, smem);
+    cudaFuncSetAttribute((const void*)k_eprop_block<K, NC, U, NS, CB, NT, MB, KH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eprop_block<K, NC, U, NS, CB, NT, MB, KH>, threads, smem);
     if (per_sm < 1) per_sm = 1;
   }
   const int tiles = s0.tiles + s1.tiles;
   int cap = per_sm;
   if (const char* e = getenv("SW_EPB_PER_SM")) cap = max(1, min(per_sm, atoi(e)));
   const int workers = tiles ? min(tiles, 148 * cap) : 0;
-  k_eprop_block<K, NC, U, NS, CB, NT, MB><<<ro_blocks + workers, threads, smem, st>>>(s0, s1, sp, B, H, beta, rho, alpha,
+  k_eprop_block<K, NC, U, NS, CB, NT, MB, KH><<<ro_blocks + workers, threads, smem, st>>>(s0, s1, sp, B, H, beta, rho, alpha,
                                                                       g_w_out, g_b_out, C, workers, tickets);
   sw::count_launch();
   return SW_OK;
@@ -644,11 +681,21 @@ extern "C" int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, 
         case 4432: rc = launch_block<8, 4, 1, 4, 32, 2>(SW_EPB_ARGS); break;
         case 4316: rc = launch_block<8, 4, 1, 3, 16, 2>(SW_EPB_ARGS); break;
         case 4416: rc = launch_block<8, 4, 1, 4, 16, 2>(SW_EPB_ARGS); break;
+        case 4417: rc = launch_block<8, 4, 1, 4, 16, 2, 4>(SW_EPB_ARGS); break;      // "4x4x17": the narrow-layer default
+        case 4221: rc = launch_block<8, 4, 1, 2, 16, 2, 5, 4>(SW_EPB_ARGS); break;   // "4x2x21": halves, 5 CTAs/SM
+        case 4321: rc = launch_block<8, 4, 1, 3, 16, 2, 5, 4>(SW_EPB_ARGS); break;   // "4x3x21"
+        case 4421: rc = launch_block<8, 4, 1, 4, 16, 2, 4, 4>(SW_EPB_ARGS); break;   // "4x4x21": halves, 4 CTAs/SM
         case 4419: rc = launch_block<8, 4, 2, 4, 16, 2, 4>(SW_EPB_ARGS); break;   // "4x4x19": packed pairs
         case 4420: rc = launch_block<8, 4, 2, 4, 16, 2, 3>(SW_EPB_ARGS); break;   // "4x4x20": packed pairs, <= 113 regs
         // default: <= 85 registers (4 CTAs/SM by registers), so a CTA also
-        // fits next to 3 forward blocks of the overlapping k_clf_step launch
-        default: rc = launch_block<8, 4, 1, 4, 16, 2, 4>(SW_EPB_ARGS); break;
+        // fits next to 3 forward blocks of the overlapping k_clf_step launch;
+        // wide hidden layers (psi/lsig rows >= 2 KB, more gather misses) gain
+        // from the half-loaded gathers at 5 CTAs/SM (C2: 226 -> 211 us; C1
+        // loses 175 -> 182 us with it)
+        default:
+          if (hidden >= 512) rc = launch_block<8, 4, 1, 2, 16, 2, 5, 4>(SW_EPB_ARGS);
+          else rc = launch_block<8, 4, 1, 4, 16, 2, 4>(SW_EPB_ARGS);
+          break;
       }
       break;
   }
