@@ -411,6 +411,7 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
     P.a[bH + h] = aa;
     P.z[bH + h] = (vv >= __fadd_rn(P.v_thr, __fmul_rn(P.beta, aa))) ? 1.0f : 0.0f;
   }
+  PROF(13);
 }
 
 // One launch for n_steps consecutive timesteps (P.n_steps >= 1): the replicas
