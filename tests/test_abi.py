@@ -55,3 +55,11 @@ def test_block_struct_matches_header():
     n = int(re.search(r"#define SW_EPROP_MAX_BLOCK (\d+)", src).group(1))
     assert _lib.MAX_BLOCK == n
     assert len(_lib.EpropBlock().psi) == n and len(_lib.EpropBlock().pre_trace[1]) == n
+
+
+def test_integration_doc_lists_every_export():
+    """INTEGRATION.md maps every C-ABI entry the header declares to the
+    reference interface it replaces."""
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    missing = [s for s in header_symbols() if s not in doc]
+    assert not missing, missing
