@@ -417,6 +417,15 @@ class EpropClassifierTrainer:
 
     def _upload_batch(self, ids, host=None) -> None:
         p, keys, labels = host if host is not None else self.task.batch_inputs(ids)
+        if isinstance(p, torch.Tensor) and p.is_pinned():
+            # inputs already in pinned host memory (a pin_memory data
+            # loader): asynchronous host->device copies, no staging
+            loc = self.local
+            self.p_in.copy_(p[loc], non_blocking=True)
+            self.keys.copy_(keys[loc], non_blocking=True)
+            self.labels.copy_(labels[loc], non_blocking=True)
+            self.h2d_bytes = sum(int(x[loc].numel() * x.element_size()) for x in (p, keys, labels))
+            return
         self.pin_p.copy_(torch.from_numpy(p[self.local]))
         self.pin_keys.copy_(torch.from_numpy(keys[self.local].view(np.int64)))
         self.pin_labels.copy_(torch.from_numpy(labels[self.local]))

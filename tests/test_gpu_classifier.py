@@ -336,3 +336,17 @@ def test_forward_currents_are_ascending_pre_sequential_sums(dev_lib, NI, H, din,
             vv = f32(alpha * f32(f32(0) - f32(z[b, h] * vthr)))
             vv = f32(f32(vv + rec[h]) + ext[h])
             assert v[b, h] == vv, (b, h)
+
+
+def test_pinned_host_inputs_equal_numpy_inputs(dev_lib):
+    """train_batch from host inputs already in pinned memory (direct async
+    copies) == from numpy arrays (staged through the trainer's pinned buffers)."""
+    a, b = _small_trainer(use_graph=True), _small_trainer(use_graph=True)
+    for k in range(2):
+        h = a.host_inputs(k)
+        pinned = (torch.from_numpy(h[0]).pin_memory(), torch.from_numpy(h[1].view(np.int64)).pin_memory(),
+                  torch.from_numpy(h[2]).pin_memory())
+        ra, rb = a.train_batch(k, host=h), b.train_batch(k, host=pinned)
+        assert ra["loss"] == rb["loss"] and ra["removed"] == rb["removed"]
+    assert torch.equal(a.s_in.planes["w"], b.s_in.planes["w"])
+    assert a.connectivity_fingerprint() == b.connectivity_fingerprint()
