@@ -1,10 +1,13 @@
 """Recurrent ALIF classifier trained with e-prop + DEEP R on the device
 (``sparsewire/classifier.py`` API).
 
-Per timestep two sm_100a launches (``sw_clf_step``: fused per-replica
-forward; ``sw_eprop_fused_step``: eligibility/gradient update of both
-projections + readout gradients); the whole 1000-step trial is captured
-once as a CUDA graph and replayed every batch.  Per batch: gradient scale,
+Per group of K = EPROP_BLOCK_STEPS timesteps two sm_100a launches:
+``sw_clf_step`` (n_steps = K) runs the fused per-replica forward of the K
+steps, and ``sw_eprop_fused_block`` updates the eligibility state and the
+gradients of both projections plus the readout gradients for all K steps in
+one pass (temporal blocking).  The whole 1000-step trial is captured once as
+a CUDA graph (forward on one stream, e-prop passes on a second) and replayed
+every batch.  Per batch: gradient scale,
 L1 nudge, Adam, DEEP R (classifier.py:236-263).  With ``process_group``
 set, replicas are sharded across ranks and the raw gradient sums are
 all-reduced (NCCL) before the update, so every rank applies the same
@@ -130,7 +133,7 @@ class _Plan:
         self.post = torch.zeros(e_pad, dtype=torch.int32, device=dev)
         self.off = torch.zeros(e_pad, dtype=torch.int32, device=dev)
         self.grad = torch.zeros(e_pad, dtype=torch.float64, device=dev)
-        # tile-major eligibility state [tile, replica, lane] (sw_eprop_fused_step)
+        # tile-major eligibility state [tile, replica, lane] (sw_eprop_fused_block)
         self.eps = torch.zeros((e_pad // 32, self.batch, 32), dtype=torch.float32, device=dev)
         self.ebar = torch.zeros_like(self.eps)
 
@@ -168,7 +171,7 @@ class EpropClassifierTrainer:
         self.deep_r_enabled = deep_r
         self.params = AlifParams()
         self.use_graph = use_graph
-        # graph replays overlap step t's e-prop update with step t+1's forward pass
+        # graph replays overlap group g's e-prop pass with group g+1's forward launch
         self.overlap = True
         self.pg = process_group
         # replicas handled by this rank (batch-DP); default: all of them
