@@ -1,14 +1,15 @@
-// One timestep of the e-prop ALIF classifier forward pass, fused per replica
-// (sparsewire/classifier.py:188-234).  Block per replica:
+// The e-prop ALIF classifier forward pass, fused per replica
+// (sparsewire/classifier.py:188-234).  Block per replica; one launch runs one
+// timestep or a group of n_steps timesteps back to back.  Per step:
 //   1. input spikes of the synthetic task from the example's counter stream
 //      (classifier.py:63-67: u = uniform01 #(t*NI + k) < p_e[k]); xbar update;
 //   2. ascending spike lists (input, hidden) in shared memory; zbar update;
-//   3. event-driven ragged propagation: warp 0 walks the spiking input rows,
-//      warp 1 the spiking hidden rows, in ascending row order, lanes over a
-//      row's slots (targets are distinct within a row), accumulating float32
-//      currents in shared memory — per post this is the ascending-pre
-//      sequential sum (classifier.py:208-209 computes the same sums as a
-//      dense sgemm on a float32 weight copy);
+//   3. event-driven ragged propagation: the spiking rows' (post, w) entries
+//      are staged in shared memory, bucketed by post (counting sort) and each
+//      post's bucket is summed in ascending row order -- per post the
+//      ascending-pre float32 sequential sum (classifier.py:208-209 computes
+//      the same sums as a dense sgemm on a float32 weight copy); above the
+//      staging capacities a warp-serial ordered walk gives the same sums;
 //   4. surrogate psi from the pre-step state (neurons.py:69-73);
 //   5. leaky readout y, softmax, cross-entropy, d = pi - onehot, pi_sum,
 //      learning signal lsig = f32(d @ W_out) (classifier.py:215-223);
