@@ -171,10 +171,13 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
   PROF(2);
   // P2: one block scan -> ascending spike list + staged row offsets
   int cnt = 0, lsum = 0;
+  // spiking rows (low 16 bits) and spiking inputs (high 16 bits) in one scan
   for (int j = 0; j < per; ++j)
-    if ((flags >> j) & 1u) { ++cnt; lsum += rlen[x0 + j]; }
-  int ec, el, tc, tl;
-  block_scan2<kWarps>(cnt, lsum, ec, el, tc, tl, wsum);
+    if ((flags >> j) & 1u) { cnt += 1 + ((x0 + j < NI) ? 0x10000 : 0); lsum += rlen[x0 + j]; }
+  int ecp, el, tcp, tl;
+  block_scan2<kWarps>(cnt, lsum, ecp, el, tcp, tl, wsum);
+  int ec = ecp & 0xFFFF;
+  const int tc = tcp & 0xFFFF;
   for (int j = 0; j < per; ++j) {
     if ((flags >> j) & 1u) {
       list[ec] = x0 + j;
@@ -191,20 +194,7 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
     if (!kCompact || tc <= rcap) roff[tc] = tl;
     s_nrows = tc;
     s_total = tl;
-  }
-  // number of spiking inputs = count of flags with x < NI
-  int cin = 0;
-  for (int j = 0; j < per; ++j)
-    if (((flags >> j) & 1u) && x0 + j < NI) ++cin;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) cin += __shfl_xor_sync(SW_FULL_MASK, cin, o);
-  __syncthreads();
-  if (lane == 0) wsum[warp].x = cin;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int w = 0; w < kWarps; ++w) t += wsum[w].x;
-    s_nx = t;
+    s_nx = tcp >> 16;
   }
   __syncthreads();
   PROF(3);
