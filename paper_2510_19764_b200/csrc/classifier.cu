@@ -125,6 +125,8 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
     acc_ext[h] = 0.0f;
     acc_rec[h] = 0.0f;
   }
+  // per-key counters of the staged propagation (read after several barriers)
+  for (int k = threadIdx.x; k < 2 * H; k += kThreads) kcur[k] = 0;
   // P1: this thread's contiguous chunk of [inputs | hidden]: spike flags,
   // xbar/zbar updates (classifier.py:63-67, 207-213)
   const int per = (NT + kThreads - 1) / kThreads;
@@ -210,8 +212,6 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
   // stable in row order, and each thread sums its posts' entries in
   // ascending row (= ascending pre) order: the same float32 sequential sum
   // per post as the reference, without a serial walk over the rows.
-  for (int k = threadIdx.x; k < 2 * H; k += kThreads) kcur[k] = 0;
-  __syncthreads();
   const int T = s_total;
   if (staged) {
     for (int q0 = threadIdx.x; q0 < T; q0 += 4 * kThreads) {
