@@ -64,38 +64,37 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.path = None
-        self.thread = None
+        self.nvml = False
+
+    # sampler process: NVML every 5 ms, one "sm_mhz,reason_mask" line per
+    # sample; a separate process so the timed loop's GIL cannot starve it
+    _SCRIPT = (
+        "import sys, time, pynvml\n"
+        "pynvml.nvmlInit(); h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))\n"
+        "print('max', pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)\n"
+        "while True:\n"
+        "    try:\n"
+        "        print(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),\n"
+        "              pynvml.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)\n"
+        "    except Exception:\n"
+        "        pass\n"
+        "    time.sleep(0.005)\n")
 
     def __enter__(self):
-        # NVML from a thread (5 ms period, starts at once); nvidia-smi -lms
-        # as the fallback (its start-up eats most of a sub-second region)
-        self.samples, self.stop, self.thread = [], None, None
+        self.samples, self.max_mhz, self.nvml = [], None, False
         try:
-            import threading
-            import pynvml
-            pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-            self.stop = threading.Event()
-            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
-                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
-                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
-                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
-
-            def loop():
-                while not self.stop.is_set():
-                    try:
-                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                        self.samples.append((sm, [k for k, b in bits.items() if r & b]))
-                    except Exception:
-                        pass
-                    self.stop.wait(0.005)
-            self.thread = threading.Thread(target=loop, daemon=True)
-            self.thread.start()
-            return self
+            import sys
+            self.proc = subprocess.Popen([sys.executable, "-c", self._SCRIPT, str(self.index)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            first = self.proc.stdout.readline().split()
+            if len(first) == 2 and first[0] == "max":
+                self.max_mhz = int(first[1])
+                self.proc.stdout.readline()          # one live sample: the sampler runs
+                self.nvml = True
+                return self
+            self.proc.kill()
         except Exception:
-            self.thread = None
+            self.proc = None
         try:
             fd, self.path = tempfile.mkstemp(suffix=".csv")
             os.close(fd)
@@ -108,21 +107,31 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
-        if self.thread is not None:
-            self.stop.set()
-            self.thread.join(timeout=5)
+        if self.proc is None:
             return
-        if self.proc is not None:
+        if self.nvml:
             self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+            out, _ = self.proc.communicate(timeout=5)
+            for line in out.splitlines():
+                f = line.split()
+                if len(f) == 2:
+                    try:
+                        self.samples.append((int(f[0]), int(f[1])))
+                    except ValueError:
+                        pass
+            return
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
 
     def summary(self):
-        if self.thread is not None:
+        if self.nvml:
+            bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                    "sw_power_cap": 0x4}   # nvmlClocksEventReason* masks
             sms = [x[0] for x in self.samples]
-            reasons = sorted({r for x in self.samples for r in x[1]})
+            reasons = sorted({k for _, m in self.samples for k, b in bits.items() if m & b})
             return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": self.max_mhz,
                     "reasons": reasons, "samples": len(sms), "source": "nvml"}
         if not self.path or not os.path.exists(self.path):
