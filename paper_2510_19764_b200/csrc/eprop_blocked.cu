@@ -682,6 +682,10 @@ extern "C" int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, 
         case 4316: rc = launch_block<8, 4, 1, 3, 16, 2>(SW_EPB_ARGS); break;
         case 4416: rc = launch_block<8, 4, 1, 4, 16, 2>(SW_EPB_ARGS); break;
         case 4417: rc = launch_block<8, 4, 1, 4, 16, 2, 4>(SW_EPB_ARGS); break;      // "4x4x17": the narrow-layer default
+        case 4408: rc = launch_block<8, 4, 1, 4, 8, 4, 4>(SW_EPB_ARGS); break;        // "4x4x8": 8 replicas, 4 term buffers
+        case 4608: rc = launch_block<8, 4, 1, 6, 8, 3, 4>(SW_EPB_ARGS); break;        // "4x6x8"
+        case 4418: rc = launch_block<8, 4, 1, 4, 16, 3, 4>(SW_EPB_ARGS); break;       // "4x4x18": 3 term buffers (3 CTAs/SM)
+        case 2408: rc = launch_block<8, 2, 1, 4, 8, 4, 4>(SW_EPB_ARGS); break;        // "2x4x8"
         case 4221: rc = launch_block<8, 4, 1, 2, 16, 2, 5, 4>(SW_EPB_ARGS); break;   // "4x2x21": halves, 5 CTAs/SM
         case 4321: rc = launch_block<8, 4, 1, 3, 16, 2, 5, 4>(SW_EPB_ARGS); break;   // "4x3x21"
         case 4421: rc = launch_block<8, 4, 1, 4, 16, 2, 4, 4>(SW_EPB_ARGS); break;   // "4x4x21": halves, 4 CTAs/SM
@@ -690,10 +694,10 @@ extern "C" int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, 
         // default: <= 85 registers (4 CTAs/SM by registers), so a CTA also
         // fits next to 3 forward blocks of the overlapping k_clf_step launch;
         // wide hidden layers (psi/lsig rows >= 2 KB, more gather misses) gain
-        // from the half-loaded gathers at 5 CTAs/SM (C2: 226 -> 211 us; C1
-        // loses 175 -> 182 us with it)
+        // from 8-replica stages with a 4-deep term ring, i.e. more stages in
+        // flight per CTA (C2: 226 -> 203 us; C1 loses 175 -> 185 us with it)
         default:
-          if (hidden >= 512) rc = launch_block<8, 4, 1, 2, 16, 2, 5, 4>(SW_EPB_ARGS);
+          if (hidden >= 512) rc = launch_block<8, 4, 1, 4, 8, 4, 4>(SW_EPB_ARGS);
           else rc = launch_block<8, 4, 1, 4, 16, 2, 4>(SW_EPB_ARGS);
           break;
       }
