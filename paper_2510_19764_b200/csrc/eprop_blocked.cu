@@ -683,12 +683,7 @@ extern "C" int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, 
         case 4416: rc = launch_block<8, 4, 1, 4, 16, 2>(SW_EPB_ARGS); break;
         case 4417: rc = launch_block<8, 4, 1, 4, 16, 2, 4>(SW_EPB_ARGS); break;      // "4x4x17": the narrow-layer default
         case 4408: rc = launch_block<8, 4, 1, 4, 8, 4, 4>(SW_EPB_ARGS); break;        // "4x4x8": 8 replicas, 4 term buffers
-        case 4608: rc = launch_block<8, 4, 1, 6, 8, 3, 4>(SW_EPB_ARGS); break;        // "4x6x8"
-        case 4418: rc = launch_block<8, 4, 1, 4, 16, 3, 4>(SW_EPB_ARGS); break;       // "4x4x18": 3 term buffers (3 CTAs/SM)
-        case 2408: rc = launch_block<8, 2, 1, 4, 8, 4, 4>(SW_EPB_ARGS); break;        // "2x4x8"
         case 4221: rc = launch_block<8, 4, 1, 2, 16, 2, 5, 4>(SW_EPB_ARGS); break;   // "4x2x21": halves, 5 CTAs/SM
-        case 4321: rc = launch_block<8, 4, 1, 3, 16, 2, 5, 4>(SW_EPB_ARGS); break;   // "4x3x21"
-        case 4421: rc = launch_block<8, 4, 1, 4, 16, 2, 4, 4>(SW_EPB_ARGS); break;   // "4x4x21": halves, 4 CTAs/SM
         case 4419: rc = launch_block<8, 4, 2, 4, 16, 2, 4>(SW_EPB_ARGS); break;   // "4x4x19": packed pairs
         case 4420: rc = launch_block<8, 4, 2, 4, 16, 2, 3>(SW_EPB_ARGS); break;   // "4x4x20": packed pairs, <= 113 regs
         // default: <= 85 registers (4 CTAs/SM by registers), so a CTA also
