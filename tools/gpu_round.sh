@@ -18,4 +18,8 @@ timeout 600 env EAGER=1 ncu --set full --clock-control none --import-source on -
 timeout 600 env ROWS=262144 ncu --set full --clock-control none --import-source on \
    -k regex:"k_deepr_elim|k_deepr_form_rows|k_remove_marked" -c 6 \
    -o $O/deepr -f python tools/mupdate_breakdown.py > $O/ncu_deepr.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_clf_step -s 3 -c 1 \
+   -o $O/forward_c1 -f python tools/profile_forward.py c1 > $O/ncu_forward.log 2>&1
+timeout 600 ncu --set full --clock-control none -k regex:k_prop_bucketed -s 1 -c 1 \
+   -o $O/prop_bucketed -f python tools/profile_prop.py > $O/ncu_prop.log 2>&1
 ls -la $O

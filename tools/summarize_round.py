@@ -88,6 +88,12 @@ def main() -> None:
     if os.path.exists(os.path.join(src, "deepr.ncu-rep")):
         ncu_export(os.path.join(src, "deepr.ncu-rep"), os.path.join(out, "deepr_ncu_full.csv"),
                    "ROWS=262144 instance of the M-update recipe (tools/mupdate_breakdown.py), ncu --set full")
+    if os.path.exists(os.path.join(src, "forward_c1.ncu-rep")):
+        ncu_export(os.path.join(src, "forward_c1.ncu-rep"), os.path.join(out, "forward_c1_ncu_full.csv"),
+                   "C1 grouped forward launch (8 timesteps, tools/profile_forward.py c1), ncu --set full")
+    if os.path.exists(os.path.join(src, "prop_bucketed.ncu-rep")):
+        ncu_export(os.path.join(src, "prop_bucketed.ncu-rep"), os.path.join(out, "prop_bucketed_ncu_full.csv"),
+                   "M-prop q=10% on 2^20 rows through PropBuckets (tools/profile_prop.py), ncu --set full")
     print("wrote", sorted(os.listdir(out)))
 
 
