@@ -26,7 +26,7 @@ namespace {
 constexpr int kThreads = 256;             // auxiliary kernels
 
 constexpr int kStageCap = 2048;   // staged (target, w) entries of the spiking rows
-constexpr int kPerThread = 8;     // (NI + H) <= kThreads * kPerThread
+constexpr int kPerThread = 8;     // max rows per thread: (NI + H) <= kThreads * kPerThread
 
 // Block-wide exclusive scan of two ints (count, length-sum); returns the
 // exclusive prefixes for this thread and the totals.
@@ -68,7 +68,9 @@ __device__ long long g_clf_prof[16];
 
 // kCompact: 16-bit row lengths, bucket offsets and sorted-row indices (the
 // layout of large layers, to keep 4 blocks per SM); else 32-bit
-template <int kThreads, bool kCompact>
+// kPT: rows of [inputs | hidden] per thread in the spike phase (the host
+// picks 4 when NI + H <= 4 * kThreads: smaller per-thread arrays)
+template <int kThreads, bool kCompact, int kPT>
 __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_arg, int rcap_arg,
                                               bool load_rlen = true) {
   using idx_t = typename std::conditional<kCompact, uint16_t, int>::type;
@@ -134,10 +136,10 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
   const uint64_t key = P.ex_key[b];
   const uint64_t c0 = (uint64_t)P.t * (uint64_t)NI;
   unsigned flags = 0;
-  float tr[kPerThread], zv[kPerThread];
-  double pv[kPerThread];
+  float tr[kPT], zv[kPT];
+  double pv[kPT];
 #pragma unroll
-  for (int j = 0; j < kPerThread; ++j) {   // all loads first
+  for (int j = 0; j < kPT; ++j) {   // all loads first
     const int x = x0 + j;
     tr[j] = 0.f;
     zv[j] = 0.f;
@@ -154,7 +156,7 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
   }
   PROF(12);
 #pragma unroll
-  for (int j = 0; j < kPerThread; ++j) {
+  for (int j = 0; j < kPT; ++j) {
     const int x = x0 + j;
     if (j < per && x < NT) {
       bool f;
@@ -411,10 +413,10 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
 // gap or tail between them.  zbar/xbar/psi/lsig/d are then the bases of
 // slot_count contiguous per-step slots ([slot][B][width]); step t writes slot
 // t % slot_count and reads the traces of slot (t - 1) % slot_count.
-template <int kThreads, bool kCompact>
+template <int kThreads, bool kCompact, int kPT>
 __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_clf_step(sw_clf_step_t P, int scap, int rcap) {
   if (P.n_steps <= 0) {
-    clf_step_body<kThreads, kCompact>(P, scap, rcap);
+    clf_step_body<kThreads, kCompact, kPT>(P, scap, rcap);
     return;
   }
   const int64_t B = P.batch, H = P.hidden, NI = P.num_inputs, C = P.num_classes;
@@ -432,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_clf_step(sw_clf_s
     Q.lsig = P.lsig + cur * B * H;
     Q.d = P.d + cur * B * C;
     if (s) __syncthreads();   // this block's step s-1 writes are visible to its step s
-    clf_step_body<kThreads, kCompact>(Q, scap, rcap, s == 0);
+    clf_step_body<kThreads, kCompact, kPT>(Q, scap, rcap, s == 0);
   }
 }
 
@@ -542,16 +544,20 @@ extern "C" int sw_clf_step(const sw_clf_step_t* p, void* stream) {
   }
   if (smem > 227 * 1024) { sw::set_last_error("clf_step: layer too large"); return SW_ERR_INVALID_ARG; }
   cudaStream_t st = (cudaStream_t)stream;
-  const void* fn = threads == 512 ? (const void*)k_clf_step<512, false>
-                   : compact      ? (const void*)k_clf_step<256, true>
-                                  : (const void*)k_clf_step<256, false>;
+  const bool pt4 = threads == 256 && !compact && NT <= 4 * 256;
+  const void* fn = threads == 512 ? (const void*)k_clf_step<512, false, 8>
+                   : compact      ? (const void*)k_clf_step<256, true, 8>
+                   : pt4          ? (const void*)k_clf_step<256, false, 4>
+                                  : (const void*)k_clf_step<256, false, 8>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (threads == 512)
-    k_clf_step<512, false><<<p->batch, 512, smem, st>>>(*p, scap, rcap);
+    k_clf_step<512, false, 8><<<p->batch, 512, smem, st>>>(*p, scap, rcap);
   else if (compact)
-    k_clf_step<256, true><<<p->batch, 256, smem, st>>>(*p, scap, rcap);
+    k_clf_step<256, true, 8><<<p->batch, 256, smem, st>>>(*p, scap, rcap);
+  else if (pt4)
+    k_clf_step<256, false, 4><<<p->batch, 256, smem, st>>>(*p, scap, rcap);
   else
-    k_clf_step<256, false><<<p->batch, 256, smem, st>>>(*p, scap, rcap);
+    k_clf_step<256, false, 8><<<p->batch, 256, smem, st>>>(*p, scap, rcap);
   sw::count_launch();
   SW_CHECK_LAUNCH("sw_clf_step");
   return SW_OK;
