@@ -28,6 +28,16 @@ constexpr int kThreads = 256;             // auxiliary kernels
 constexpr int kStageCap = 2048;   // staged (target, w) entries of the spiking rows
 constexpr int kPerThread = 8;     // max rows per thread: (NI + H) <= kThreads * kPerThread
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // Block-wide exclusive scan of two ints (count, length-sum); returns the
 // exclusive prefixes for this thread and the totals.
 template <int kWarps>
@@ -103,7 +113,12 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
   int* kcur = (int*)(smem_raw + o);       o += (size_t)2 * H * 4;             // [2H] counts, then cursors
   o = (o + 15) & ~(size_t)15;
   double* yv = (double*)(smem_raw + o);
+  double* ypre = yv + 2 * C;                // [C] previous y, pi_sum, b_out (prefetched)
+  double* pipre = ypre + C;
+  double* bpre = pipre + C;
   double* dv = yv + C;
+  __shared__ double s_loss;
+  __shared__ int s_label;
   __shared__ int2 wsum[kWarps];
   __shared__ int s_nx, s_nrows, s_total;
   const int b = blockIdx.x;
@@ -117,6 +132,19 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
   const float v0 = h0_ok ? P.v[bH + threadIdx.x] : 0.f;
   const float a0 = h0_ok ? P.a[bH + threadIdx.x] : 0.f;
   const float z0 = h0_ok ? P.z[bH + threadIdx.x] : 0.f;
+  // per-replica readout state read only in the readout/softmax phases:
+  // asynchronous global->shared copies, waited for at the barrier after P1
+  // (32-bit layout only: the compact layout's shared memory is at its budget)
+  if constexpr (!kCompact) {
+    if ((int)threadIdx.x < C) {
+      cp_async8(ypre + threadIdx.x, P.y + bC + threadIdx.x);
+      cp_async8(pipre + threadIdx.x, P.pi_sum + bC + threadIdx.x);
+      cp_async8(bpre + threadIdx.x, P.b_out + threadIdx.x);
+    } else if (threadIdx.x == kThreads - 1) {
+      cp_async8(&s_loss, P.loss + b);
+      cp_async4(&s_label, P.labels + b);
+    }
+  }
   // P0: row lengths to shared memory; zero the current accumulators
   // (the row lengths stay in shared memory across the steps of a launch:
   // the connectivity only changes between batches)
@@ -171,7 +199,8 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
     }
   }
   PROF(1);
-  __syncthreads();   // rlen ready
+  if constexpr (!kCompact) cp_async_wait_all();
+  __syncthreads();   // rlen ready (and the prefetched readout state)
   PROF(2);
   // P2: one block scan -> ascending spike list + staged row offsets
   int cnt = 0, lsum = 0;
@@ -340,7 +369,8 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s[u] += __shfl_xor_sync(SW_FULL_MASK, s[u], o);
       if (lane == 0 && c < C)
-        yv[c] = __dadd_rn(__dadd_rn(__dmul_rn(P.alpha64, P.y[bC + c]), s[u]), P.b_out[c]);
+        yv[c] = kCompact ? __dadd_rn(__dadd_rn(__dmul_rn(P.alpha64, P.y[bC + c]), s[u]), P.b_out[c])
+                         : __dadd_rn(__dadd_rn(__dmul_rn(P.alpha64, ypre[c]), s[u]), bpre[c]);
     }
   }
   PROF(6);
@@ -361,15 +391,15 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(SW_FULL_MASK, se, o);
-    const int label = P.labels[b];
+    const int label = kCompact ? P.labels[b] : s_label;
     for (int c = lane, u = 0; c < C; c += 32, ++u) {
       const double pi = (u < 2 ? ex[u] : exp(yv[c] - mx)) / se;
       P.y[bC + c] = yv[c];
-      P.pi_sum[bC + c] += pi;
+      P.pi_sum[bC + c] = (kCompact ? P.pi_sum[bC + c] : pipre[c]) + pi;
       const double dd = pi - (c == label ? 1.0 : 0.0);
       dv[c] = dd;
       P.d[bC + c] = dd;
-      if (c == label) P.loss[b] += -log(pi);
+      if (c == label) P.loss[b] = (kCompact ? P.loss[b] : s_loss) + -log(pi);
     }
   }
   PROF(8);
@@ -504,7 +534,7 @@ size_t clf_smem_bytes(int H, int NI, int C, int scap, int rcap, bool compact) {
   o = (o + 3) & ~(size_t)3;
   o += (size_t)2 * H * 4;                       // kcur
   o = (o + 15) & ~(size_t)15;
-  return o + (size_t)2 * C * 8 + 16;            // yv, dv
+  return o + (size_t)(compact ? 2 : 5) * C * 8 + 16;   // yv, dv (+ ypre, pipre, bpre)
 }
 
 extern "C" int sw_clf_step(const sw_clf_step_t* p, void* stream) {
