@@ -17,8 +17,8 @@
 // to L2 as an atomic.  After a grid barrier every CTA sums a post range over
 // the groups in ascending group order (one store per post).
 //
-// Measured (2^20 x 1024 rows, N = 65536, L2 flushed, q = 10 %): 174 us =
-// 57 % of HBM on the SURVEY M-prop bytes (the L2-atomic kernel: 344 us);
+// Measured (2^20 x 1024 rows, N = 65536, L2 flushed, q = 10 %): 172 us =
+// 57.5 % of HBM on the SURVEY M-prop bytes (the L2-atomic kernel: 344 us);
 // without the shared-memory atomics (a CAS loop for float64) the same pass
 // takes 148 us, so ~25 us are the atomics and the rest is load latency.
 //
@@ -27,12 +27,13 @@
 // re-gathers bw through bslot after a weight change).
 #include "common.cuh"
 
+#include <cstdlib>
+#include <string>
+
 namespace {
 
 constexpr int kBSlab = 16384;
 constexpr int kBMaxSlabs = 8;
-constexpr int kBW = 32;   // warps per propagation CTA
-constexpr int kRB = 4;    // spiking rows per warp iteration
 
 __global__ void k_bucket_build(const int32_t* __restrict__ row_length, const int32_t* __restrict__ target,
                                const double* __restrict__ w, int P, int stride, int G, uint16_t* bt,
@@ -95,6 +96,7 @@ __global__ void k_bucket_refresh(const int32_t* __restrict__ row_length, const d
   }
 }
 
+template <int kBW, int kRB, int kH>   // kBW warps per CTA
 __global__ void __launch_bounds__(kBW * 32, 1)
 k_prop_bucketed(const uint16_t* __restrict__ soff, const uint16_t* __restrict__ bt, const double* __restrict__ bw,
                 int G, int stride, const int32_t* __restrict__ spikes, const int32_t* n_spikes, double* out,
@@ -108,7 +110,7 @@ k_prop_bucketed(const uint16_t* __restrict__ soff, const uint16_t* __restrict__ 
   __syncthreads();
   const int S = *n_spikes;
   // kRB spiking rows per warp iteration: their metadata loads, then their
-  // data loads (2 x kRB per lane per 64-entry step), are issued together;
+  // data loads (kH x kRB per lane per 32*kH-entry step), are issued together;
   // the next iteration's spike ids are fetched ahead
   const int stepq = NG * kBW;
   int inext[kRB];
@@ -141,11 +143,11 @@ k_prop_bucketed(const uint16_t* __restrict__ soff, const uint16_t* __restrict__ 
       nmax = max(nmax, n[r]);
       base[r] = (int64_t)max(i[r], 0) * stride + a[r];
     }
-    for (int k = lane; k < nmax; k += 64) {
-      uint16_t t[2][kRB];
-      double v[2][kRB];
+    for (int k = lane; k < nmax; k += 32 * kH) {
+      uint16_t t[kH][kRB];
+      double v[kH][kRB];
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+      for (int h = 0; h < kH; ++h)
 #pragma unroll
         for (int r = 0; r < kRB; ++r) {
           const int kk = k + 32 * h;
@@ -154,7 +156,7 @@ k_prop_bucketed(const uint16_t* __restrict__ soff, const uint16_t* __restrict__ 
           v[h][r] = ok ? __ldg(bw + base[r] + kk) : 0.0;
         }
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+      for (int h = 0; h < kH; ++h)
 #pragma unroll
         for (int r = 0; r < kRB; ++r) {
           if (k + 32 * h < n[r]) atomicAdd(acc + t[h][r], v[h][r]);
@@ -185,14 +187,35 @@ k_prop_bucketed(const uint16_t* __restrict__ soff, const uint16_t* __restrict__ 
 
 int slabs_for(int num_post) { return (num_post + kBSlab - 1) / kBSlab; }
 
+using BucketFn = void (*)(const uint16_t*, const uint16_t*, const double*, int, int, const int32_t*,
+                         const int32_t*, double*, int, double*, unsigned*);
+
+struct BucketVariant { BucketFn fn; int warps; };
+
+// SW_PROP_BCFG = "WARPSxRBxH" (measurement knob).  Sweep at 2^20 rows,
+// q = 1 % / 10 %: 32x2x4 38.9 / 172.1 us, 32x4x2 41.0 / 172.1, 16x8x2
+// 43.0 / 186.4, 16x4x4 41.0 / 192.5 (fewer warps lose; 32 warps with more
+// loads per lane spill at the 64-register cap of a 1024-thread CTA).
+BucketVariant bucket_fn() {
+  static BucketVariant v{nullptr, 0};
+  if (!v.fn) {
+    const char* e = getenv("SW_PROP_BCFG");
+    const std::string c = e ? e : "32x2x4";
+    v = c == "32x4x2" ? BucketVariant{k_prop_bucketed<32, 4, 2>, 32}
+      : c == "16x8x2" ? BucketVariant{k_prop_bucketed<16, 8, 2>, 16}
+      : BucketVariant{k_prop_bucketed<32, 2, 4>, 32};
+  }
+  return v;
+}
+
 int bucket_ctas(int G) {
   static int per_sm = -1, sms = 0;
   if (per_sm < 0) {
-    cudaFuncSetAttribute((const void*)k_prop_bucketed, cudaFuncAttributeMaxDynamicSharedMemorySize, kBSlab * 8);
+    cudaFuncSetAttribute((const void*)bucket_fn().fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kBSlab * 8);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_prop_bucketed, kBW * 32,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)bucket_fn().fn, bucket_fn().warps * 32,
                                                       kBSlab * 8) != cudaSuccess) per_sm = 0;
     cudaGetLastError();
   }
@@ -262,7 +285,7 @@ extern "C" int sw_propagate_bucketed(const uint16_t* soff, const uint16_t* bt, c
   int g = G, s = stride, N = num_post;
   void* args[] = {(void*)&soff, (void*)&bt, (void*)&bw, (void*)&g, (void*)&s, (void*)&spikes,
                   (void*)&n_spikes, (void*)&out, (void*)&N, (void*)&scratch, (void*)&arrive};
-  cudaLaunchCooperativeKernel((const void*)k_prop_bucketed, dim3(ctas), dim3(kBW * 32), args, kBSlab * 8, st);
+  cudaLaunchCooperativeKernel((const void*)bucket_fn().fn, dim3(ctas), dim3(bucket_fn().warps * 32), args, kBSlab * 8, st);
   sw::count_launch();
   SW_CHECK_LAUNCH("sw_propagate_bucketed");
   return SW_OK;
