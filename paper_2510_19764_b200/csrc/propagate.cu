@@ -119,9 +119,19 @@ k_prop_slab(const int32_t* __restrict__ row_length, const int32_t* __restrict__ 
   // post range of this CTA, summed over the groups in ascending order
   const int per = (N + gridDim.x - 1) / gridDim.x;
   const int j0 = blockIdx.x * per, j1 = min(N, j0 + per);
+  // partials loaded kGB groups at a time, added in ascending group order
+  constexpr int kGB = 16;
   for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
     double v = 0.0;
-    for (int gg = 0; gg < G; ++gg) v = __dadd_rn(v, __ldcg(scratch + (int64_t)gg * (kSlabs * kSlab) + j));
+    for (int g0 = 0; g0 < G; g0 += kGB) {
+      double p[kGB];
+#pragma unroll
+      for (int u = 0; u < kGB; ++u)
+        p[u] = g0 + u < G ? __ldcg(scratch + (int64_t)(g0 + u) * (kSlabs * kSlab) + j) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kGB; ++u)
+        if (g0 + u < G) v = __dadd_rn(v, p[u]);
+    }
     out[j] = __dadd_rn(out[j], v);
   }
 }

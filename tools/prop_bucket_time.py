@@ -49,3 +49,20 @@ for q in (0.01, 0.1):
     alg = S * 8 + S * Rs * 12 + N * 8
     print(f"cfg {os.environ.get('SW_PROP_BCFG', 'default')} q {q} S {S} median_us {us:.1f} "
           f"min_us {ts[0]:.1f} frac {alg / us / 1e3 / 6547.5:.3f} max_rel_err {err:.2e}")
+
+# fixed cost of the bucketed pass: one spiking row (zeroing the slab,
+# partial-slab write, grid barrier, ordered reduction over the groups)
+one = torch.ones(1, dtype=torch.int32, device="cuda")
+ts = []
+for _ in range(20):
+    flush.add_(1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _lib.call("sw_propagate_bucketed", pb.soff.data_ptr(), pb.bt.data_ptr(), pb.bw.data_ptr(), m.num_post,
+              m.stride, lst.data_ptr(), one.data_ptr(), 1, out.data_ptr(), pb.workspace.data_ptr(),
+              pb.workspace.numel(), st)
+    e1.record()
+    e1.synchronize()
+    ts.append(e0.elapsed_time(e1) * 1e3)
+ts.sort()
+print(f"cfg {os.environ.get('SW_PROP_BCFG', 'default')} fixed (1 spiking row) median_us {ts[len(ts) // 2]:.1f}")
