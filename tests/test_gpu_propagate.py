@@ -197,3 +197,23 @@ def test_bucketed_propagation_goes_stale(dev_lib):
         propagate_spikes(m, syn.planes["g"], torch.tensor([row]).cuda(), out, buckets=pb)
     pb.build()
     propagate_spikes(m, syn.planes["g"], torch.tensor([row]).cuda(), out, buckets=pb)
+
+
+@pytest.mark.parametrize("cfg", ["32x4x2", "16x8x2"])
+def test_bucketed_propagation_variants(cfg):
+    """The non-default k_prop_bucketed shapes behind the SW_PROP_BCFG
+    measurement knob (read once per process, so each runs in a child):
+    dyadic weights, exact against np.add.at."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import test_gpu_propagate as t\n"
+        "t.test_bucketed_propagation_matches_add_at(None, 6000, 65536, 300, 0.6)\n"
+        "t.test_bucketed_propagation_matches_add_at(None, 400, 65536, 1024, 0.01)\n"
+        "print('ok')\n" % (root, os.path.join(root, "tests")))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SW_PROP_BCFG=cfg),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
