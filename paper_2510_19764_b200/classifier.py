@@ -38,6 +38,9 @@ from .updates import Model
 # sw_eprop_fused_block): K forward steps run first, then one pass applies K
 # recursion steps to every (replica, synapse) element
 EPROP_BLOCK_STEPS = int(os.environ.get("SW_EPROP_BLOCK_STEPS", "8"))
+if not 1 <= EPROP_BLOCK_STEPS <= _lib.MAX_BLOCK:
+    raise ValueError(f"SW_EPROP_BLOCK_STEPS={EPROP_BLOCK_STEPS}: must be in 1..{_lib.MAX_BLOCK} "
+                     "(SW_EPROP_MAX_BLOCK in include/sparsewire_b200.h)")
 # (step, replica) splits of the readout gradient inside the blocked pass
 READOUT_SPLITS = int(os.environ.get("SW_READOUT_SPLITS", "16"))
 
