@@ -375,6 +375,13 @@ SW_API int sw_propagate_bucketed(const uint16_t* soff, const uint16_t* bt, const
                                  int32_t stride, const int32_t* spikes, const int32_t* n_spikes,
                                  int32_t max_spikes, double* out, void* workspace, int64_t workspace_bytes,
                                  void* stream);
+/* Same contract over the same bucketed copy (its weight snapshot), one warp
+ * per spiking row with float64 L2 atomics: for few spiking rows, where the
+ * slab pass's fixed cost dominates. */
+SW_API int sw_propagate_bucketed_atomic(const uint16_t* soff, const uint16_t* bt, const double* bw,
+                                        int32_t num_post, int32_t stride, const int32_t* spikes,
+                                        const int32_t* n_spikes, int32_t max_spikes, double* out,
+                                        void* stream);
 typedef struct sw_prop_proj {
   const int32_t* col_ptr;    /* transpose CSR of the projection */
   const int32_t* src_pre;
@@ -414,12 +421,17 @@ typedef struct sw_rewire_params {
   const double* form_lut;    /* [num_post] formation probability by torus offset */
   const double* dist_lut;    /* [num_post] toroidal distance by torus offset */
   double g_theta, p_dep, p_pot, g_init;
+  void* scratch;             /* sw_rewire_scratch_bytes(num_post, total_attempts) bytes for rows with
+                                more than 64 attempts (processed serially, exact); NULL: such rows
+                                count as errors (totals[7]) */
 } sw_rewire_params_t;
+SW_API int64_t sw_rewire_scratch_bytes(int32_t num_post, int64_t total_attempts);
 /* One RewiringRule update (host + row phases), no host round trip.
  * attempts[num_pre] int32 (input when forced_attempts != 0), update_count
- * (device int64, read then incremented), keys[2] scratch, totals[8] int64
+ * (device int64, read then incremented), keys[2] scratch, totals[16] int64
  * out ([0] removed [1] kept [2] formed [3] form_missed [4] form_full
- * [5] attempts [7] error count), changed (device flag for the remap),
+ * [5] attempts [7] error count (a row with more attempts than num_post);
+ * [8], [9] internal), changed (device flag for the remap),
  * rej scratch int64; ev_off/ev_kind/ev_d (may be NULL): per-attempt event
  * records in row order (kind 1 = elimination, 2 = formation, distance). */
 SW_API int sw_rewire_update(const sw_ragged_t* m, int32_t weight_plane, const sw_rewire_params_t* prm,

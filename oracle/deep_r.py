@@ -36,13 +36,16 @@ class DeepROracle:
         self.conn[:] = 0
         w = m.planes[self.wp]
         for i in range(m.num_pre):
-            for s in range(m.row_length[i]):
-                j = int(m.target[i, s])
-                bf_set(self.conn, i, j)
+            n = m.row_length[i]
+            for s in range(n):
+                bf_set(self.conn, i, int(m.target[i, s]))
+            # all sets of the row, then all clears (two vector calls, :62-64)
+            for s in range(n):
                 if w[i, s] > 0:
-                    bf_set(self.sign, i, j)
-                elif w[i, s] < 0:
-                    bf_clear(self.sign, i, j)
+                    bf_set(self.sign, i, int(m.target[i, s]))
+            for s in range(n):
+                if w[i, s] < 0:
+                    bf_clear(self.sign, i, int(m.target[i, s]))
 
     def sign_of_slots(self):
         """Sign bit of every slot's target (bitfield.py:93-102 test_bits_rows)."""

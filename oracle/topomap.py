@@ -20,6 +20,20 @@ def torus_offset(i, j, side):
     return (xj - xi) % side + side * ((yj - yi) % side)
 
 
+def offset_luts(side, p_form, sigma_form):
+    """(formation probability, toroidal distance) by wrapped offset
+    dx + side*dy: formation_probability (topomap.py:49-52) of
+    toroidal_distance(0, arange(n)) (geometry.py:23-31), one vector call as
+    the reference evaluates it (F10b)."""
+    idx = np.arange(side * side)
+    x = (idx % side).astype(np.float64)
+    y = (idx // side).astype(np.float64)
+    dx = np.abs(x[0] - x)
+    dy = np.abs(y[0] - y)
+    d = np.hypot(np.minimum(dx, side - dx), np.minimum(dy, side - dy))
+    return p_form * np.exp(-(d ** 2) / (2.0 * sigma_form ** 2)), d
+
+
 class RewiringOracle:
     def __init__(self, m: Ragged, side: int, form_lut, dist_lut, total_attempts, g_theta=0.1,
                  p_dep=2.45e-2 * 50, p_pot=1.36e-4 * 50, g_init=0.2, plane="g"):

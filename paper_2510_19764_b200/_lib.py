@@ -54,7 +54,7 @@ class RewireParams(C.Structure):
     """sw_rewire_params_t"""
     _fields_ = [("host_prefix", U64), ("row_prefix", U64), ("rule_id", I32), ("side", I32),
                 ("total_attempts", I64), ("form_lut", P), ("dist_lut", P), ("g_theta", F64),
-                ("p_dep", F64), ("p_pot", F64), ("g_init", F64)]
+                ("p_dep", F64), ("p_pot", F64), ("g_init", F64), ("scratch", P)]
 
 
 class TopomapStep(C.Structure):
@@ -129,6 +129,7 @@ SIGNATURES: dict[str, list] = {
     "sw_prop_buckets_refresh": [P, P, I32, I32, P, P, P],
     "sw_prop_bucketed_workspace_bytes": [I32],
     "sw_propagate_bucketed": [P, P, P, I32, I32, P, P, I32, P, P, I64, P],
+    "sw_propagate_bucketed_atomic": [P, P, P, I32, I32, P, P, I32, P, P],
     "sw_alif_step": [P, P, P, P, P, I64, F32, F32, F32, F32, P],
     "sw_alif_surrogate": [P, P, P, I64, F32, F32, P],
     "sw_lif_cond_step": [P, P, P, P, I32, I64, F64, F64, F64, F64, F64, F64, F64, F64, I64, P, P],
@@ -147,6 +148,7 @@ SIGNATURES: dict[str, list] = {
     "sw_stdp_pre": [P, P, P, I32, I32, P, P, P, F64, F64, F64, P],
     "sw_stdp_post": [P, P, P, P, I32, I32, P, P, P, F64, F64, F64, P],
     "sw_rewire_update": [RP, I32, P, P, P, P, P, P, P, P, P, P, I32, P],
+    "sw_rewire_scratch_bytes": [I32, I64],
     "sw_topomap_step": [P, P, P],
     "sw_topomap_log": [P, P, P, P, I64, P],
     "sw_topomap_neurons": [P, P],
@@ -178,6 +180,7 @@ def lib():
     L.sw_eprop_readout_scratch_bytes.argtypes = [I32, I32, I32]
     L.sw_eprop_readout_scratch_bytes.restype = C.c_int64
     L.sw_prop_bucketed_workspace_bytes.restype = C.c_int64
+    L.sw_rewire_scratch_bytes.restype = C.c_int64
     L.sw_launch_count.argtypes = []
     L.sw_launch_count.restype = C.c_longlong
     L.sw_last_error.argtypes = []

@@ -493,6 +493,12 @@ class EpropClassifierTrainer:
         ``resident`` = the batch inputs are already in HBM (benchmarking)."""
         ids = self.task.train_ids(batch_index, self.batch_size)
         self._forward_batch(ids, learn=True, host=host, resident=resident)
+        return self.update_phase(batch_index)
+
+    def update_phase(self, batch_index: int) -> tuple[float, float]:
+        """The part of gradient_phase after the trial (classifier.py:236-253):
+        (batch-DP all-reduce,) loss/accuracy read-back, 1/B gradient scale,
+        L1 nudge and Adam on every parameter."""
         if self.pg is not None:
             self._allreduce_grads()
         self.stats_host.copy_(self.stats, non_blocking=True)

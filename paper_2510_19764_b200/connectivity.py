@@ -196,6 +196,11 @@ def _init_rows(num_pre, num_post, key, counter0, mode, density, lut, side, headr
         cap = math.ceil(headroom * int(mx.item()))
         if multapse_free:
             cap = min(cap, num_post)
+    elif int(mx.item()) > cap:
+        # an explicit capacity must hold every drawn row: never truncate
+        from .errors import RowFull
+        raise RowFull(f"init_pairwise_bernoulli: a row draws {int(mx.item())} synapses, "
+                      f"more than capacity {cap}")
     m = RaggedMatrix(num_pre, num_post, cap, multapse_free)
     _lib.call("sw_init_bernoulli_fill", num_pre, num_post, key, counter0, mode, float(density),
               _lib.ptr(lut_t), side, m.row_length.data_ptr(), m.target.data_ptr(), m.stride, st)
@@ -247,7 +252,10 @@ class PropBuckets:
     the row's own slot range, so the propagation reads every synapse of a
     spiking row once and accumulates in shared memory instead of L2 atomics.
     Like TransposeMap (connectivity.py:151-192) it goes stale on a structural
-    change (``m.version``); after a weight-only change call ``refresh()``."""
+    change (``m.version``, checked).  Both kernels read the copy's weight
+    snapshot taken at build()/refresh(): after a weight-only change call
+    ``refresh()`` (until then every propagation, whatever its spike count,
+    uses the snapshot)."""
 
     def __init__(self, m: RaggedMatrix, weights: torch.Tensor):
         if weights.dtype != torch.float64:
@@ -297,10 +305,11 @@ class PropBuckets:
         self.check_fresh()
         m = self.m
         if max_spikes < self.MIN_SPIKES:
-            _lib.call("sw_propagate_atomic", m.row_length.data_ptr(), m.target.data_ptr(),
-                      self.weights.data_ptr(), m.num_pre, m.num_post, m.stride, spikes.data_ptr(),
-                      n_spikes.data_ptr(), max(1, int(max_spikes)), out.data_ptr(), *_lib.prop_workspace(),
-                      _lib.stream_ptr())
+            # same weight snapshot as the slab pass (bw), so the result never
+            # depends on which kernel the spike count selects
+            _lib.call("sw_propagate_bucketed_atomic", self.soff.data_ptr(), self.bt.data_ptr(),
+                      self.bw.data_ptr(), m.num_post, m.stride, spikes.data_ptr(), n_spikes.data_ptr(),
+                      max(1, int(max_spikes)), out.data_ptr(), _lib.stream_ptr())
             return "atomic"
         _lib.call("sw_propagate_bucketed", self.soff.data_ptr(), self.bt.data_ptr(), self.bw.data_ptr(),
                   m.num_post, m.stride, spikes.data_ptr(), n_spikes.data_ptr(), max(1, int(max_spikes)),

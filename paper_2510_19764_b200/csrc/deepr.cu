@@ -40,8 +40,11 @@ __global__ void k_bf_randomize(sw_bitfield_t bf, uint64_t key, uint64_t tail_mas
   }
 }
 
-// conn bits := edges; sign bit set for w > 0, cleared for w < 0 (deep_r.py:56-64)
-__global__ void k_deepr_init_bits(sw_ragged_t m, int wp, sw_bitfield_t sign, sw_bitfield_t conn) {
+// conn bits := edges; sign bit set for w > 0, cleared for w < 0 (deep_r.py:56-64).
+// Two launches, as the reference's two vector calls: phase 0 sets conn and
+// the w > 0 sign bits, phase 1 clears the w < 0 ones, so with multapses of
+// opposite sign the clear wins deterministically (deep_r.py:62-64).
+__global__ void k_deepr_init_bits(sw_ragged_t m, int wp, sw_bitfield_t sign, sw_bitfield_t conn, int phase) {
   const int64_t total = (int64_t)m.num_pre * m.stride;
   const double* w = (const double*)m.planes[wp];
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
@@ -51,12 +54,13 @@ __global__ void k_deepr_init_bits(sw_ragged_t m, int wp, sw_bitfield_t sign, sw_
     if (s >= m.row_length[i]) continue;
     const int j = m.target[x];
     const uint64_t bit = 1ull << (j & 63);
-    atomicOr((unsigned long long*)&conn.words[i * conn.words_per_row + (j >> 6)], bit);
     const double wv = w[x];
-    if (wv > 0.0)
-      atomicOr((unsigned long long*)&sign.words[i * sign.words_per_row + (j >> 6)], bit);
-    else if (wv < 0.0)
+    if (phase == 0) {
+      atomicOr((unsigned long long*)&conn.words[i * conn.words_per_row + (j >> 6)], bit);
+      if (wv > 0.0) atomicOr((unsigned long long*)&sign.words[i * sign.words_per_row + (j >> 6)], bit);
+    } else if (wv < 0.0) {
       atomicAnd((unsigned long long*)&sign.words[i * sign.words_per_row + (j >> 6)], ~bit);
+    }
   }
 }
 
@@ -786,7 +790,10 @@ extern "C" int sw_deepr_init_bitfields(const sw_ragged_t* m, int32_t wp, const s
   cudaMemsetAsync(conn->words, 0, (size_t)conn->num_pre * conn->words_per_row * 8, (cudaStream_t)stream);
   const int64_t total = (int64_t)m->num_pre * m->stride;
   if (total == 0) return SW_OK;
-  k_deepr_init_bits<<<flat_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(*m, wp, *sign, *conn); sw::count_launch();
+  for (int phase = 0; phase < 2; ++phase) {
+    k_deepr_init_bits<<<flat_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(*m, wp, *sign, *conn, phase);
+    sw::count_launch();
+  }
   SW_CHECK_LAUNCH("sw_deepr_init_bitfields");
   return SW_OK;
 }

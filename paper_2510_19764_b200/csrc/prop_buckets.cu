@@ -197,6 +197,27 @@ k_prop_bucketed(const uint16_t* __restrict__ soff, const uint16_t* __restrict__ 
   }
 }
 
+// Few spiking rows: one warp per spiking row over the same bucketed copy,
+// float64 L2 atomics (the slab pass's fixed cost dominates there).  Reading
+// the copy, not the live plane, keeps both kernels on one weight snapshot.
+__global__ void k_prop_bucketed_atomic(const uint16_t* __restrict__ soff, const uint16_t* __restrict__ bt,
+                                       const double* __restrict__ bw, int G, int stride,
+                                       const int32_t* __restrict__ spikes, const int32_t* n_spikes,
+                                       double* out) {
+  const int lane = threadIdx.x & 31;
+  const int S = *n_spikes;
+  for (int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < S; q += gridDim.x * (blockDim.x >> 5)) {
+    const int i = __ldg(spikes + q);
+    const int64_t base = (int64_t)i * stride;
+    const uint16_t* so = soff + (int64_t)i * (G + 1);
+    for (int c = 0; c < G; ++c) {
+      const int a = __ldg(so + c), b = __ldg(so + c + 1);
+      for (int k = a + lane; k < b; k += 32)
+        atomicAdd(out + c * kBSlab + __ldg(bt + base + k), __ldg(bw + base + k));
+    }
+  }
+}
+
 int slabs_for(int num_post) { return (num_post + kBSlab - 1) / kBSlab; }
 
 using BucketFn = void (*)(const uint16_t*, const uint16_t*, const double*, int, int, const int32_t*,
@@ -300,5 +321,20 @@ extern "C" int sw_propagate_bucketed(const uint16_t* soff, const uint16_t* bt, c
   cudaLaunchCooperativeKernel((const void*)bucket_fn().fn, dim3(ctas), dim3(bucket_fn().warps * 32), args, kBSlab * 8, st);
   sw::count_launch();
   SW_CHECK_LAUNCH("sw_propagate_bucketed");
+  return SW_OK;
+}
+
+extern "C" int sw_propagate_bucketed_atomic(const uint16_t* soff, const uint16_t* bt, const double* bw,
+                                            int32_t num_post, int32_t stride, const int32_t* spikes,
+                                            const int32_t* n_spikes, int32_t max_spikes, double* out,
+                                            void* stream) {
+  const int G = sw_prop_bucket_slabs(num_post);
+  if (G == 0) { sw::set_last_error("propagate_bucketed_atomic: 1 <= num_post <= 131072"); return SW_ERR_INVALID_ARG; }
+  if (max_spikes <= 0) return SW_OK;
+  int blocks = (max_spikes + 7) / 8;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_prop_bucketed_atomic<<<blocks, 256, 0, (cudaStream_t)stream>>>(soff, bt, bw, G, stride, spikes, n_spikes, out);
+  sw::count_launch();
+  SW_CHECK_LAUNCH("sw_propagate_bucketed_atomic");
   return SW_OK;
 }

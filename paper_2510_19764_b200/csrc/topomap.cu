@@ -26,6 +26,7 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int kKMax = 64;   // attempts per row handled by one thread
+constexpr int kTotals = 16;  // totals[] words: see sw_rewire_update
 
 __global__ void k_rw_keys(uint64_t host_prefix, uint64_t row_prefix, int32_t rule_id,
                           int64_t* update_count, uint64_t* keys, int64_t* totals, int32_t* changed) {
@@ -33,7 +34,7 @@ __global__ void k_rw_keys(uint64_t host_prefix, uint64_t row_prefix, int32_t rul
   keys[0] = sw::fold_int(sw::fold_int(sw::fold_int(host_prefix, (uint64_t)rule_id), u), 0);
   keys[1] = sw::fold_int(sw::fold_int(sw::fold_int(row_prefix, (uint64_t)rule_id), u), 0);
   *update_count = (int64_t)u + 1;
-  for (int k = 0; k < 8; ++k) totals[k] = 0;
+  for (int k = 0; k < kTotals; ++k) totals[k] = 0;
   *changed = 0;
 }
 
@@ -52,10 +53,13 @@ struct RwArgs {
   int side;
   double g_theta, p_dep, p_pot, g_init;
   int64_t* totals;              // [0]=removed [1]=kept [2]=formed [3]=missed [4]=full [5]=attempts [7]=error
+                                // [8]=blocks done [9]=heavy rows
   int32_t* changed;
   const int32_t* ev_off;        // [P] exclusive scan of attempts (or null)
   int8_t* ev_kind;              // 1 = elimination, 2 = formation
   double* ev_d;
+  int32_t* heavy;               // rows with kKMax < attempts <= N, then the heavy-row scratch (or null)
+  int64_t heavy_cap;
 };
 
 __device__ __forceinline__ int fy_get(const int* key, const int* val, int n, int p) {
@@ -69,7 +73,12 @@ __device__ __forceinline__ void rw_rows(const RwArgs& A, int64_t t0, int64_t dt)
   for (int i = (int)t0; i < m.num_pre; i += (int)dt) {
     const int k = A.attempts[i];
     if (k == 0) continue;
-    if (k > kKMax || k > N) { atomicAdd((unsigned long long*)&A.totals[7], 1ull); continue; }
+    if (k > N || (k > kKMax && !A.heavy)) { atomicAdd((unsigned long long*)&A.totals[7], 1ull); continue; }
+    if (k > kKMax) {   // deferred to the serial heavy-row path (rw_heavy_rows)
+      const unsigned long long h = atomicAdd((unsigned long long*)&A.totals[9], 1ull);
+      if ((int64_t)h < A.heavy_cap) A.heavy[h] = i;
+      continue;
+    }
     const uint64_t key = sw::child_key(A.keys[1], (uint64_t)i);
     uint64_t ctr = 0;
     int cand[kKMax];
@@ -178,8 +187,117 @@ __device__ __forceinline__ void rw_rows(const RwArgs& A, int64_t t0, int64_t dt)
   }
 }
 
+// One row with kKMax < k <= N attempts, serially, with the attempt set as a
+// bitmap over the posts (the reference's own attempt-bitfield formulation,
+// topomap.py:142-196): same draws in the same order as rw_rows.  Scratch
+// after the heavy-row list: W bitmap words, then N int32 (Fisher-Yates
+// array, reused for the selected slots).  Such rows are vanishingly rare
+// (10 s^2 attempts over 256 s^2 rows per update) but must not change the
+// result (KTooLarge only for k > N, as bitfield.py:67-77).
+__device__ void rw_row_heavy(const RwArgs& A, int i) {
+  const sw_ragged_t& m = A.m;
+  const int N = m.num_post;
+  const int W = (N + 63) >> 6;
+  uint64_t* bits = reinterpret_cast<uint64_t*>(A.heavy + ((A.heavy_cap + 1) & ~1LL));
+  int32_t* arr = reinterpret_cast<int32_t*>(bits + W);
+  const int k = A.attempts[i];
+  const uint64_t key = sw::child_key(A.keys[1], (uint64_t)i);
+  uint64_t ctr = 0;
+  for (int w = 0; w < W; ++w) bits[w] = 0ull;
+  if (2 * k < N) {
+    const uint64_t rem = sw::reject_rem((uint64_t)N);
+    int filled = 0;
+    while (filled < k) {
+      const int v = (int)sw::uniform_int_seq(key, ctr, (uint64_t)N, rem);
+      const uint64_t b = 1ull << (v & 63);
+      if (!(bits[v >> 6] & b)) { bits[v >> 6] |= b; ++filled; }
+    }
+  } else {
+    for (int q = 0; q < N; ++q) arr[q] = q;
+    for (int q = 0; q < k; ++q) {
+      const uint64_t nn = (uint64_t)(N - q);
+      const int j = q + (int)sw::uniform_int_seq(key, ctr, nn, sw::reject_rem(nn));
+      const int t = arr[q]; arr[q] = arr[j]; arr[j] = t;
+    }
+    for (int q = 0; q < k; ++q) bits[arr[q] >> 6] |= 1ull << (arr[q] & 63);
+  }
+  const int64_t off = (int64_t)i * m.stride;
+  double* g = (double*)m.planes[A.gp];
+  int n = m.row_length[i];
+  // selected slots ascending; elimination draws in slot order; hit = sign bit
+  int ns = 0;
+  for (int s = 0; s < n; ++s) {
+    const int t = m.target[off + s];
+    if ((bits[t >> 6] >> (t & 63)) & 1ull) arr[ns++] = s;
+  }
+  int removed = 0;
+  int ev = A.ev_kind ? A.ev_off[i] : 0;
+  for (int q = 0; q < ns; ++q) {
+    const int s = arr[q];
+    const int t = m.target[off + s];
+    const double u = sw::u01(sw::draw(key, ctr++));
+    const double p = g[off + s] < A.g_theta ? A.p_dep : A.p_pot;
+    bits[t >> 6] &= ~(1ull << (t & 63));
+    if (u < p) {
+      arr[q] = -1 - s;
+      ++removed;
+      if (A.ev_kind) { A.ev_kind[ev] = 1; A.ev_d[ev] = A.dist_lut[torus_offset(i, t, A.side)]; ++ev; }
+    }
+  }
+  for (int q = ns - 1; q >= 0; --q) {
+    if (arr[q] >= 0) continue;
+    const int s = -1 - arr[q], last = n - 1;
+    if (s != last) sw::move_slot(m, off, s, last);
+    n = last;
+  }
+  int formed = 0, missed = 0, full = 0;
+  for (int w = 0; w < W; ++w) {
+    uint64_t word = bits[w];
+    while (word) {
+      const int j = (w << 6) + __ffsll((long long)word) - 1;
+      word &= word - 1;
+      const int o = torus_offset(i, j, A.side);
+      const double u = sw::u01(sw::draw(key, ctr++));
+      if (!(u < A.form_lut[o])) { ++missed; continue; }
+      if (n >= m.max_row_length) { ++full; continue; }
+      m.target[off + n] = j;
+      sw::zero_slot(m, off, n);
+      g[off + n] = A.g_init;
+      ++n;
+      ++formed;
+      if (A.ev_kind) { A.ev_kind[ev] = 2; A.ev_d[ev] = A.dist_lut[o]; ++ev; }
+    }
+  }
+  if (A.ev_kind)
+    for (; ev < A.ev_off[i] + k; ++ev) A.ev_kind[ev] = 0;
+  m.row_length[i] = n;
+  A.totals[0] += removed;
+  A.totals[1] += ns - removed;
+  A.totals[2] += formed;
+  A.totals[3] += missed;
+  A.totals[4] += full;
+  A.totals[5] += k;
+  if (removed + formed) *A.changed = 1;
+}
+
+// The last block to finish its rows runs the deferred heavy rows (if any):
+// no extra launch or grid barrier on the common path.
+__device__ __forceinline__ void rw_heavy_tail(const RwArgs& A) {
+  if (!A.heavy) return;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  __threadfence();
+  const unsigned long long prev = atomicAdd((unsigned long long*)&A.totals[8], 1ull);
+  if (prev != gridDim.x - 1) return;
+  __threadfence();
+  const int64_t nh = *(volatile int64_t*)&A.totals[9];
+  if (nh > A.heavy_cap) { atomicAdd((unsigned long long*)&A.totals[7], 1ull); return; }
+  for (int64_t h = 0; h < nh; ++h) rw_row_heavy(A, ((volatile int32_t*)A.heavy)[h]);
+}
+
 __global__ void k_rw_rows(RwArgs A) {
   rw_rows(A, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+  rw_heavy_tail(A);
 }
 
 // One rewiring update in one cooperative launch (keys, host-phase
@@ -198,7 +316,7 @@ k_rw_fused(RwArgs A, uint64_t host_prefix, uint64_t row_prefix, int32_t rule_id,
   if (gt == 0) {
     keys[0] = hk;
     keys[1] = sw::fold_int(sw::fold_int(sw::fold_int(row_prefix, (uint64_t)rule_id), u), 0);
-    for (int k = 0; k < 8; ++k) A.totals[k] = 0;
+    for (int k = 0; k < kTotals; ++k) A.totals[k] = 0;
     *A.changed = 0;
     *rej = 0;
   }
@@ -225,6 +343,7 @@ k_rw_fused(RwArgs A, uint64_t host_prefix, uint64_t row_prefix, int32_t rule_id,
   }
   if (rem != 0) grid.sync();
   rw_rows(A, gt, gn);
+  rw_heavy_tail(A);
 }
 
 __global__ void k_copy_i32(const int32_t* a, int32_t* b, int n) {
@@ -237,7 +356,16 @@ int grid1(int64_t n) {
   return (int)(g < 1 ? 1 : g);
 }
 
+// heavy-row list entries: at most total_attempts / (kKMax + 1) rows
+int64_t heavy_cap(const sw_rewire_params_t* prm) { return prm->total_attempts / (kKMax + 1) + 1; }
+
 }  // namespace
+
+extern "C" int64_t sw_rewire_scratch_bytes(int32_t num_post, int64_t total_attempts) {
+  const int64_t cap = total_attempts / (kKMax + 1) + 1;
+  const int64_t W = ((int64_t)num_post + 63) / 64;
+  return ((cap + 1) & ~1LL) * 4 + W * 8 + (int64_t)num_post * 4;
+}
 
 extern "C" int sw_rewire_update(const sw_ragged_t* m, int32_t weight_plane, const sw_rewire_params_t* prm,
                                 int32_t* attempts, int64_t* update_count, uint64_t* keys,
@@ -258,7 +386,8 @@ extern "C" int sw_rewire_update(const sw_ragged_t* m, int32_t weight_plane, cons
     int blocks = grid1(P);
     if (blocks > max_blocks) blocks = max_blocks;
     RwArgs A{*m, weight_plane, attempts, keys, prm->form_lut, prm->dist_lut, prm->side,
-             prm->g_theta, prm->p_dep, prm->p_pot, prm->g_init, totals, changed, nullptr, nullptr, nullptr};
+             prm->g_theta, prm->p_dep, prm->p_pot, prm->g_init, totals, changed, nullptr, nullptr, nullptr,
+             (int32_t*)prm->scratch, heavy_cap(prm)};
     uint64_t hp = prm->host_prefix, rp = prm->row_prefix;
     int32_t rid = prm->rule_id;
     int64_t ta = prm->total_attempts;
@@ -288,7 +417,8 @@ extern "C" int sw_rewire_update(const sw_ragged_t* m, int32_t weight_plane, cons
     sw::k_scan_excl_i32<<<1, 1024, 0, st>>>(ev_off, P, nullptr); sw::count_launch();
   }
   RwArgs A{*m, weight_plane, attempts, keys, prm->form_lut, prm->dist_lut, prm->side,
-           prm->g_theta, prm->p_dep, prm->p_pot, prm->g_init, totals, changed, ev_off, ev_kind, ev_d};
+           prm->g_theta, prm->p_dep, prm->p_pot, prm->g_init, totals, changed, ev_off, ev_kind, ev_d,
+           (int32_t*)prm->scratch, heavy_cap(prm)};
   if (P > 0) { k_rw_rows<<<grid1(P), 256, 0, st>>>(A); sw::count_launch(); }
   SW_CHECK_LAUNCH("sw_rewire_update");
   return SW_OK;

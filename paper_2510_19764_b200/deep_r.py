@@ -105,7 +105,10 @@ class DeepR:
                   ctypes.byref(self.sign_bits.descriptor()),
                   ctypes.byref(self.conn_bits.descriptor()), self.dormant.data_ptr(),
                   self._sync_cache(), self._marks.data_ptr(), _lib.stream_ptr())
-        self.matrix.version += 1
+        # the removal count is known on the host only at the form pass (its
+        # one counter read per pass): the version bump for this pass's
+        # removals happens there, so a no-op update leaves derived
+        # structures (TransposeMap, PropBuckets) fresh (updates.py:367-372)
         self._cache_version = self.matrix.version
         return False
 
@@ -126,12 +129,15 @@ class DeepR:
                   _lib.stream_ptr())
         if pass_index == 0:
             self._last_removed_dev.copy_(self._counters[0:1])
-        self.matrix.version += 1
-        self._cache_version = self.matrix.version
         # _form_continue (deep_r.py:147-160): one 32-byte read per pass
         self._counters_host.copy_(self._counters, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         drawn, unplaced = int(self._counters_host[0]), int(self._counters_host[1])
+        # version: bumped only when the structure changed -- pass 0 with
+        # removals (the eliminate pass's change), or any pass placing synapses
+        if (pass_index == 0 and drawn > 0) or drawn - unplaced > 0:
+            self.matrix.version += 1
+        self._cache_version = self.matrix.version
         if unplaced == 0:
             return False
         if drawn - unplaced == 0:

@@ -95,15 +95,12 @@ class RewiringRule:
         self.attempt_bits = Bitfield(P, matrix.num_post)   # kept clear, as the reference leaves it
         self.attempts = torch.zeros(P, dtype=torch.int32, device=dev)
         self._keys = torch.zeros(2, dtype=torch.int64, device=dev)
-        self._totals = torch.zeros(8, dtype=torch.int64, device=dev)
+        self._totals = torch.zeros(16, dtype=torch.int64, device=dev)
         self.changed = torch.zeros(1, dtype=torch.int32, device=dev)
         self._rej = torch.zeros(1, dtype=torch.int64, device=dev)
         self._update = torch.zeros(1, dtype=torch.int64, device=dev)
         self._host_update = 0
-        cap_ev = max(1, total_attempts)
         self._ev_off = torch.zeros(P, dtype=torch.int32, device=dev)
-        self._ev_kind = torch.zeros(cap_ev, dtype=torch.int8, device=dev)
-        self._ev_d = torch.zeros(cap_ev, dtype=torch.float64, device=dev)
         # host-numpy LUTs by torus offset; injectable for parity tests
         dist = geometry.offset_distance_lut() if dist_lut is None else np.asarray(dist_lut)
         if form_lut is None:
@@ -117,10 +114,31 @@ class RewiringRule:
         p.form_lut, p.dist_lut = self._form_lut.data_ptr(), self._dist_lut.data_ptr()
         p.g_theta, p.p_dep, p.p_pot, p.g_init = (params.g_theta, params.p_elim_dep,
                                                  params.p_elim_pot, params.g_init)
+        self._alloc_update_buffers(total_attempts)
         self.forced_attempts = False
         self.last_stats: dict[str, int] = {}
         self.elim_events: list[tuple[float, float]] = []
         self.form_events: list[tuple[float, float]] = []
+
+    def _alloc_update_buffers(self, attempts_total: int) -> None:
+        """Event records (one per attempt) and the scratch of the serial path
+        for rows with more than 64 attempts, sized for attempts_total."""
+        dev = self.attempts.device
+        cap_ev = max(1, attempts_total)
+        self._ev_kind = torch.zeros(cap_ev, dtype=torch.int8, device=dev)
+        self._ev_d = torch.zeros(cap_ev, dtype=torch.float64, device=dev)
+        nb = int(_lib.lib().sw_rewire_scratch_bytes(self.matrix.num_post, attempts_total))
+        self._heavy = torch.zeros((nb + 7) // 8, dtype=torch.int64, device=dev)
+        self._prm.total_attempts = attempts_total
+        self._prm.scratch = self._heavy.data_ptr()
+
+    def force_attempts(self, attempts) -> None:
+        """Use these per-row attempt counts instead of the host-phase draws
+        (tests and microbenchmarks; the host stream is then not drawn)."""
+        a = np.ascontiguousarray(attempts, dtype=np.int32)
+        self.forced_attempts = True
+        self.attempts.copy_(torch.from_numpy(a))
+        self._alloc_update_buffers(max(int(a.sum()), self.total_attempts))
 
     def _device_pass(self, model, binding, pass_index, host_key, row_base) -> bool:
         p = self._prm
@@ -151,7 +169,7 @@ class RewiringRule:
         t = self._totals.cpu().numpy()
         if t[7]:
             from .errors import KTooLarge
-            raise KTooLarge(f"{self.name}: more than 64 attempts on one row")
+            raise KTooLarge(f"{self.name}: more attempts on one row than num_post")
         self.last_stats = {"attempts": int(t[5]), "elim_candidates": int(t[0] + t[1]),
                            "form_candidates": int(t[2] + t[3] + t[4]), "removed": int(t[0]),
                            "kept": int(t[1]), "formed": int(t[2]), "form_missed": int(t[3]),

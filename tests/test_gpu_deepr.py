@@ -173,3 +173,54 @@ def test_remove_marked_matches_golden(dev_lib):
         assert list(got[r, : n - k]) == list(res[: n - k])
         assert list(w[r, : n - k]) == list(res[: n - k] * 0.5)
     assert np.array_equal(removed.cpu().numpy(), g["k"])
+
+
+def test_init_bitfields_multapses_clear_wins(dev_lib):
+    """with multapses of opposite sign, deep_r.py:62-64 sets every
+    w > 0 bit of the row, then clears every w < 0 bit (clear wins), in any
+    slot order; w == 0 keeps the random bit."""
+    from oracle.deep_r import DeepROracle
+    from oracle.ragged import Ragged
+    from paper_2510_19764_b200.connectivity import RaggedMatrix, SynVarMatrix
+    from paper_2510_19764_b200.deep_r import DeepR
+    from paper_2510_19764_b200.rng import CounterRng
+    P, N, cap = 64, 130, 8
+    rs = np.random.default_rng(4)
+    tg = rs.integers(0, 8, size=(P, cap)).astype(np.int32) * 16 + rs.integers(0, 2, size=(P, cap)).astype(np.int32)
+    rl = rs.integers(0, cap + 1, size=P).astype(np.int32)
+    w = rs.choice([-1.0, 0.0, 1.0], size=(P, cap))
+    m = RaggedMatrix(P, N, cap, multapse_free=False)
+    syn = SynVarMatrix(m, PLANES)
+    m.load_state(rl, tg)
+    syn.planes["w"].copy_(torch.from_numpy(w))
+    dr = DeepR(m, syn, "mx")
+    dr.init_bitfields(CounterRng(3, "bits"))
+    o = Ragged(P, N, cap, PLANES)
+    o.row_length[:] = rl
+    o.target[:] = tg
+    o.planes["w"][:] = w
+    od = DeepROracle(o)
+    od.init_bitfields(O.Stream.of(3, "bits"))
+    assert np.array_equal(dr.conn_bits.host_words(), od.conn)
+    assert np.array_equal(dr.sign_bits.host_words(), od.sign)
+
+
+def test_version_bumped_only_on_structural_change(dev_lib):
+    """a DEEP R group that removes nothing leaves m.version (and so
+    derived structures) untouched, as the reference bumps it only inside
+    add/remove (connectivity.py:91-136, updates.py:367-372)."""
+    fx = golden("deepr_small16.npz")
+    model, m, syn, dr, cycles = device_deepr_from_fixture(fx)
+    w = syn.planes["w"]
+    # no sign mismatches: make every weight agree with its sign bit
+    sign = dr.sign_bits.host_words()
+    tg = m.target.cpu().numpy()
+    bit = (np.take_along_axis(sign, (tg >> 6).astype(np.int64), axis=1) >> (tg & 63).astype(np.uint64)) & np.uint64(1)
+    w.copy_(torch.from_numpy(np.where(bit.astype(bool), 1.0, -1.0)))
+    dr.l1_strength = 0.0
+    v0 = m.version
+    model.run_update_group("deep_r")
+    assert dr.last_removed == 0 and m.version == v0
+    w.copy_(-w)                                  # every synapse now mismatches
+    model.run_update_group("deep_r")
+    assert dr.last_removed > 0 and m.version > v0

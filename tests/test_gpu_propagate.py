@@ -199,6 +199,34 @@ def test_bucketed_propagation_goes_stale(dev_lib):
     propagate_spikes(m, syn.planes["g"], torch.tensor([row]).cuda(), out, buckets=pb)
 
 
+def test_bucketed_kernels_share_one_weight_snapshot(dev_lib):
+    """ADVICE r1: PropBuckets.propagate picks its kernel from the spike count;
+    both must read the snapshot taken at build()/refresh(), so an in-place
+    weight change without refresh() affects neither, and after refresh()
+    both see it.  Dyadic weights: exact against np.add.at."""
+    from paper_2510_19764_b200.connectivity import PropBuckets
+    P, N = 6000, 40000
+    m, syn, rl, tgt, rs = _matrix(P, N, 64, 5)
+    w = rs.integers(-64, 65, size=tgt.shape).astype(np.float64) / 64.0
+    syn.planes["g"].copy_(torch.from_numpy(w))
+    pb = PropBuckets(m, syn.planes["g"])
+    syn.planes["g"].mul_(2.0)                     # not yet refreshed
+    few = np.flatnonzero(rs.random(P) < 0.05).astype(np.int32)
+    many = np.flatnonzero(rs.random(P) < 0.9).astype(np.int32)
+    assert few.size < pb.MIN_SPIKES <= many.size
+    for scale in (1.0, 2.0):
+        for sp in (few, many):
+            ref = np.zeros(N)
+            for i in sp:
+                np.add.at(ref, tgt[i, :rl[i]], scale * w[i, :rl[i]])
+            out = torch.zeros(N, dtype=torch.float64, device="cuda")
+            d = torch.from_numpy(sp).cuda()
+            kern = pb.propagate(d, torch.tensor([sp.size], dtype=torch.int32, device="cuda"), sp.size, out)
+            assert kern == ("atomic" if sp is few else "bucketed")
+            assert np.array_equal(out.cpu().numpy(), ref), (scale, kern)
+        pb.refresh()
+
+
 @pytest.mark.parametrize("cfg", ["32x4x2", "16x8x2"])
 def test_bucketed_propagation_variants(cfg):
     """The non-default k_prop_bucketed shapes behind the SW_PROP_BCFG
@@ -217,3 +245,18 @@ def test_bucketed_propagation_variants(cfg):
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SW_PROP_BCFG=cfg),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def test_explicit_capacity_never_truncates_rows(dev_lib):
+    """init_pairwise_bernoulli_density with an explicit capacity
+    below the realised maximum row length raises RowFull instead of silently
+    dropping synapses; a sufficient capacity keeps every drawn synapse."""
+    from paper_2510_19764_b200.connectivity import init_pairwise_bernoulli_density
+    from paper_2510_19764_b200.errors import RowFull
+    from paper_2510_19764_b200.rng import CounterRng
+    m, _ = init_pairwise_bernoulli_density(300, 400, 0.2, 1.0, CounterRng(2, "init", "cap"))
+    mx = int(m.row_length.max())
+    with pytest.raises(RowFull):
+        init_pairwise_bernoulli_density(300, 400, 0.2, 1.0, CounterRng(2, "init", "cap"), capacity=mx - 1)
+    m2, _ = init_pairwise_bernoulli_density(300, 400, 0.2, 1.0, CounterRng(2, "init", "cap"), capacity=mx)
+    assert torch.equal(m2.row_length, m.row_length)

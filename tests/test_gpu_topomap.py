@@ -292,3 +292,43 @@ def test_phase_timer_csv_schema(dev_lib):
     assert [ln.split(",")[0] for ln in lines[1:]] == list(PHASES) + ["total"]
     vals = [float(ln.split(",")[1]) for ln in lines[1:]]
     assert abs(sum(vals[:-1]) - vals[-1]) < 1e-6 and vals[PHASES.index("row_update")] > 0
+
+
+def test_rows_with_more_than_64_attempts_are_exact(dev_lib):
+    """rows with 64 < k <= N attempts (both sample_k_distinct
+    branches, k == N included) go through the serial bitmap path and match
+    the oracle bit for bit, together with ordinary rows in the same update
+    (ref topomap.py:142-196, bitfield.py:67-77)."""
+    from oracle_helpers import oracle_topomap_group
+    fx = golden("topomap_s1.npz")
+    model, objs = _device_group(fx, 0)
+    om, orules = oracle_topomap_group(fx, 0)
+    N = 256
+    att = np.zeros(N, dtype=np.int64)
+    att[[3, 7, 9, 11, 12, 200]] = [100, 200, 65, 5, 256, 64]
+    for name, (m, syn, rule) in objs.items():
+        rule.force_attempts(att)
+        o, r = orules[name]
+
+        def host(ctx, r=r):
+            r.attempts[:] = att
+            r.events = []
+            r.stats = dict(removed=0, kept=0, formed=0, form_missed=0, form_full=0)
+        r.host_phase = host
+    model.run_update_group("rewiring")
+    om.run_update_group("rewiring")
+    for name, (m, syn, rule) in objs.items():
+        rule.collect(1.0)
+        o, r = orules[name]
+        rl = o.row_length
+        assert np.array_equal(m.row_length.cpu().numpy(), rl), name
+        mask = np.arange(o.target.shape[1])[None, :] < rl[:, None]
+        assert np.array_equal(m.target.cpu().numpy()[mask], o.target[mask]), name
+        assert np.array_equal(syn.planes["g"].cpu().numpy()[mask], o.planes["g"][mask]), name
+        st = rule.last_stats
+        assert (st["removed"], st["kept"], st["formed"], st["form_missed"], st["form_full"]) == (
+            r.stats["removed"], r.stats["kept"], r.stats["formed"], r.stats["form_missed"],
+            r.stats["form_full"]), name
+        assert st["attempts"] == int(att.sum())
+        assert [d for _, d in rule.elim_events] == [d for _, k, d in r.events if k == 1]
+        assert [d for _, d in rule.form_events] == [d for _, k, d in r.events if k == 2]

@@ -239,3 +239,16 @@ def test_c_oracle_eprop_matches_golden_and_numpy():
                            np.float32(p.beta), np.float32(p.rho), np.float32(p.alpha))
     assert np.array_equal(eps, g["eps"]) and np.array_equal(ebar, g["ebar"])
     assert np.array_equal(grad, g["grad"])
+
+
+@pytest.mark.parametrize("tag", ["topomap_s1.npz", "topomap_s2dep.npz"])
+def test_offset_luts_match_reference_luts(tag):
+    """oracle.topomap.offset_luts (used by the s = 4..16 rewiring parity
+    tests) reproduces the LUTs the real reference produced (F10b)."""
+    from oracle.topomap import offset_luts
+    g = golden(tag)
+    side = 16 * int(g["meta"][0])
+    ff, d = offset_luts(side, 0.16, 2.5)
+    lat, d2 = offset_luts(side, 1.0, 1.0)
+    assert np.array_equal(d, g["dist"]) and np.array_equal(d2, g["dist"])
+    assert np.array_equal(ff, g["ff_lut"]) and np.array_equal(lat, g["lat_lut"])
