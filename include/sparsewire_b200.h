@@ -98,6 +98,15 @@ SW_API int sw_bitfield_randomize(const sw_bitfield_t* bf, uint64_t key, void* st
 SW_API int sw_ragged_remove_marked(const sw_ragged_t* m, const uint8_t* marked,
                             int64_t* removed, void* stream);
 
+/* Column slice for post-sharded propagation (SURVEY 8e M-prop; no
+ * reference counterpart -- the reference propagates over whole rows,
+ * connectivity.py:139-148).  dst row i = the synapses of src row i with
+ * lo <= target < hi, in src slot order, target - lo, every plane copied;
+ * dst->num_post = hi - lo, same num_pre and plane types.  Rows longer than
+ * dst->stride are truncated; *max_len (device int32, optional, caller
+ * zeroed) gets the longest slice row so the caller can check. */
+SW_API int sw_ragged_column_slice(const sw_ragged_t* src, int32_t lo, int32_t hi, const sw_ragged_t* dst,
+                                  int32_t* max_len, void* stream);
 /* add_synapse (connectivity.py:91-112) on one row: RowFull, DuplicateEdge
  * (when multapse_free), else append post with every plane zeroed and
  * values[p] stored where set_mask[p] != 0.  status (device int32[1]) gets
@@ -165,6 +174,34 @@ SW_API int sw_deepr_form_pass(const sw_ragged_t* m, const sw_bitfield_t* conn,
                        int32_t* activations, int64_t* unplaced,
                        int64_t* counters, const sw_bitfield_t* sign, uint32_t* sign_slot,
                        void* stream);
+
+/* Row-sharded form pass (SURVEY 8e M-update; replaces the single-process
+ * _form_host / _form_row phases of deep_r.py:110-145 when rows are split
+ * over ranks).  Each rank owns rows [row0, row0 + m->num_pre) of a
+ * num_pre_global-row matrix.  Order per pass, with the host collectives
+ * between (integer sums, so the result is bit-exact with sw_deepr_form_pass):
+ *   sw_deepr_form_pending     counters[0..3] = 0; counters[0] = local sum of
+ *                             pending_src                 -> all-reduce counters[0]
+ *   sw_deepr_form_hist_chunk  act_full[num_pre_global] = histogram of host
+ *                             draws [D*rank/world, D*(rank+1)/world); rejected
+ *                             draws into counters[2]      -> all-reduce counters[2]
+ *   sw_deepr_form_hist_fix    (one rank only) the draws that replace the
+ *                             rejected ones, from counter D -> reduce-scatter
+ *                             act_full by row owner into activations[num_pre]
+ *   sw_deepr_form_rows_shard  placement of the local rows with the global
+ *                             row's stream key child(row_base, row0 + i); the
+ *                             local unplaced sum into counters[1]
+ *                                                         -> all-reduce counters[1] */
+SW_API int sw_deepr_form_pending(const int64_t* pending_src, int64_t num_rows, int64_t* counters,
+                                 void* stream);
+SW_API int sw_deepr_form_hist_chunk(int64_t* counters, uint64_t host_key, int64_t num_pre_global,
+                                    int32_t rank, int32_t world, int32_t* act_full, void* stream);
+SW_API int sw_deepr_form_hist_fix(int64_t* counters, uint64_t host_key, int64_t num_pre_global,
+                                  int32_t* act_full, void* stream);
+SW_API int sw_deepr_form_rows_shard(const sw_ragged_t* m, const sw_bitfield_t* conn,
+                                    int32_t exclude_diagonal, uint64_t row_base, int64_t row0,
+                                    const int32_t* activations, int64_t* unplaced, int64_t* counters,
+                                    const sw_bitfield_t* sign, uint32_t* sign_slot, void* stream);
 
 /* Microbenchmark sign-flip injection: valid slot (i, s) negates plane value
  * when uniform01 draw #(i*stride + s) of key < prob (SURVEY 8(d) M-update). */

@@ -110,6 +110,7 @@ SIGNATURES: dict[str, list] = {
     "sw_ragged_remove_marked": [RP, P, P, P],
     "sw_ragged_add_synapse": [RP, I32, I32, P, P, I32, P, P],
     "sw_ragged_remove_row_slots": [RP, I32, P, I32, P, P],
+    "sw_ragged_column_slice": [RP, I32, I32, RP, P, P],
     "sw_init_bernoulli_count": [I64, I32, U64, U64, I32, F64, P, I32, P, P, P],
     "sw_init_bernoulli_fill": [I64, I32, U64, U64, I32, F64, P, I32, P, P, I32, P],
     "sw_deepr_init_bitfields": [RP, I32, BP, BP, U64, P],
@@ -117,6 +118,10 @@ SIGNATURES: dict[str, list] = {
     "sw_deepr_sign_cache_build": [RP, BP, P, P],
     "sw_deepr_eliminate": [RP, I32, BP, BP, P, P, P, P],
     "sw_deepr_form_pass": [RP, BP, I32, P, U64, U64, P, P, P, BP, P, P],
+    "sw_deepr_form_pending": [P, I64, P, P],
+    "sw_deepr_form_hist_chunk": [P, U64, I64, I32, I32, P, P],
+    "sw_deepr_form_hist_fix": [P, U64, I64, P, P],
+    "sw_deepr_form_rows_shard": [RP, BP, I32, U64, I64, P, P, P, BP, P, P],
     "sw_eprop_accumulate_batch": [P, P, I32, I32, P, P, P, I32, I32, P, P, P, F32, F32, F32, P],
     "sw_eprop_plan": [P, P, I32, I32, I32, I32, P, P, P, P, I32, P, P],
     "sw_gather_f64": [P, P, I32, P, P],

@@ -117,6 +117,55 @@ def descriptor(m: RaggedMatrix, syn: SynVarMatrix | None) -> _lib.Ragged:
     return d
 
 
+def row_slice(m: RaggedMatrix, syn: SynVarMatrix | None, lo: int, hi: int
+              ) -> tuple[RaggedMatrix, SynVarMatrix | None]:
+    """Rows [lo, hi) as their own matrix (copies; same num_post, capacity and
+    planes): the local part of a row-sharded matrix (SURVEY 8e M-update)."""
+    out = RaggedMatrix(hi - lo, m.num_post, m.max_row_length, m.multapse_free, device=m.target.device)
+    out.row_length.copy_(m.row_length[lo:hi])
+    out.target.copy_(m.target[lo:hi])
+    osyn = None
+    if syn is not None:
+        osyn = SynVarMatrix(out)
+        for n, t in syn.planes.items():
+            osyn.add_plane(n, t.dtype).copy_(t[lo:hi])
+    return out, osyn
+
+
+def column_slice(m: RaggedMatrix, syn: SynVarMatrix | None, lo: int, hi: int,
+                 capacity: int | None = None) -> tuple[RaggedMatrix, SynVarMatrix | None]:
+    """The synapses onto posts [lo, hi) (targets renumbered from 0, slot
+    order kept): the local part of a post-sharded matrix (SURVEY 8e M-prop).
+    ``capacity`` defaults to the longest sliced row."""
+    from .errors import RowFull
+    src = descriptor(m, syn)
+    mx = torch.zeros(1, dtype=torch.int32, device=m.target.device)
+    cap = m.max_row_length if capacity is None else int(capacity)
+    out = RaggedMatrix(m.num_pre, hi - lo, cap, m.multapse_free, device=m.target.device)
+    osyn = None
+    if syn is not None:
+        osyn = SynVarMatrix(out)
+        for n, t in syn.planes.items():
+            osyn.add_plane(n, t.dtype)
+    dst = descriptor(out, osyn)
+    _lib.call("sw_ragged_column_slice", C_ref(src), lo, hi, C_ref(dst), mx.data_ptr(), _lib.stream_ptr())
+    longest = int(mx.item())
+    if longest > out.stride:
+        raise RowFull(f"column slice row of {longest} synapses exceeds capacity {out.stride}")
+    if capacity is None and longest < cap:
+        # shrink to the longest slice row (every sliced row fits)
+        small = RaggedMatrix(m.num_pre, hi - lo, max(longest, 1), m.multapse_free, device=m.target.device)
+        small.row_length.copy_(out.row_length)
+        small.target.copy_(out.target[:, :small.stride])
+        ssyn = None
+        if osyn is not None:
+            ssyn = SynVarMatrix(small)
+            for n, t in osyn.planes.items():
+                ssyn.add_plane(n, t.dtype).copy_(t[:, :small.stride])
+        return small, ssyn
+    return out, osyn
+
+
 def remove_marked(m: RaggedMatrix, syn: SynVarMatrix | None, marked: torch.Tensor,
                   removed: torch.Tensor | None = None) -> None:
     """Remove every marked slot of every row with the exact ``remove_slots``

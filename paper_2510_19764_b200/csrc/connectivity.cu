@@ -201,3 +201,62 @@ extern "C" int sw_ragged_remove_row_slots(const sw_ragged_t* m, int32_t pre, con
   SW_CHECK_LAUNCH("sw_ragged_remove_row_slots");
   return SW_OK;
 }
+
+// ---- column slice (SURVEY 8e M-prop: posts sharded) --------------------------
+// dst row i = the synapses of src row i whose target lies in [lo, hi), in
+// src slot order, target - lo, every plane copied.  Warp per row: ballot
+// compaction keeps the slot order, so an ordered propagation over the
+// slice sums each owned post's inputs in exactly the unsharded order.
+namespace {
+__global__ void k_column_slice(sw_ragged_t src, int lo, int hi, sw_ragged_t dst, int32_t* max_len) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const unsigned lt = sw::lanemask_lt();
+  for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < src.num_pre;
+       i += (int64_t)gridDim.x * wpb) {
+    const int len = src.row_length[i];
+    const int64_t so = i * (int64_t)src.stride, dofs = i * (int64_t)dst.stride;
+    int n = 0;
+    for (int s0 = 0; s0 < len; s0 += 32) {
+      const int s = s0 + lane;
+      const int t = s < len ? src.target[so + s] : -1;
+      const bool keep = t >= lo && t < hi;
+      const unsigned b = __ballot_sync(SW_FULL_MASK, keep);
+      const int d = n + __popc(b & lt);
+      if (keep && d < dst.stride) {
+        dst.target[dofs + d] = t - lo;
+        for (int p = 0; p < src.n_planes; ++p) {
+          if (src.plane_bytes[p] == 8)
+            ((uint64_t*)dst.planes[p])[dofs + d] = ((const uint64_t*)src.planes[p])[so + s];
+          else
+            ((uint32_t*)dst.planes[p])[dofs + d] = ((const uint32_t*)src.planes[p])[so + s];
+        }
+      }
+      n += __popc(b);
+    }
+    if (lane == 0) {
+      dst.row_length[i] = n < dst.stride ? n : dst.stride;
+      if (max_len) atomicMax(max_len, n);
+    }
+  }
+}
+}  // namespace
+
+extern "C" int sw_ragged_column_slice(const sw_ragged_t* src, int32_t lo, int32_t hi, const sw_ragged_t* dst,
+                                      int32_t* max_len, void* stream) {
+  if (!src || !dst || lo < 0 || hi < lo || hi > src->num_post || dst->num_pre != src->num_pre ||
+      dst->n_planes != src->n_planes || dst->num_post != hi - lo) {
+    sw::set_last_error("sw_ragged_column_slice: bad slice or destination shape");
+    return SW_ERR_INVALID_ARG;
+  }
+  for (int p = 0; p < src->n_planes; ++p)
+    if (src->plane_bytes[p] != dst->plane_bytes[p]) {
+      sw::set_last_error("sw_ragged_column_slice: plane types differ");
+      return SW_ERR_INVALID_ARG;
+    }
+  if (src->num_pre == 0) return SW_OK;
+  k_column_slice<<<grid_rows(src->num_pre), 256, 0, (cudaStream_t)stream>>>(*src, lo, hi, *dst, max_len);
+  sw::count_launch();
+  SW_CHECK_LAUNCH("sw_ragged_column_slice");
+  return SW_OK;
+}

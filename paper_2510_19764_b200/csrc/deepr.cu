@@ -542,12 +542,16 @@ __global__ void k_sum_i64(const int64_t* x, int64_t n, int64_t* out) {
 // D draws of uniform_int(num_pre) on the host stream: draw c lands in row
 // h mod P when valid.  Invalid (rejected) counters are counted; the serial
 // fix-up kernel then continues from counter D until D valid draws exist.
+// Row-sharded form (world > 1): this rank draws only counters
+// [D*rank/world, D*(rank+1)/world) into a histogram over all rows; the
+// per-rank histograms are then reduce-scattered by row owner.
 __global__ void k_form_hist(int64_t* counters, uint64_t key, uint64_t P, uint64_t rem,
-                            int32_t* act) {
+                            int32_t* act, int rank, int world) {
   const int64_t D = counters[0];
+  const int64_t c_lo = D * rank / world, c_hi = D * (rank + 1) / world;
   const bool pow2 = (P & (P - 1)) == 0;
   int64_t rej = 0;
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < D;
+  for (int64_t c = c_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < c_hi;
        c += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t h = sw::draw(key, (uint64_t)c);
     if (sw::draw_valid(h, rem)) {
@@ -585,13 +589,15 @@ __global__ void k_form_hist_fix(int64_t* counters, uint64_t key, uint64_t P, uin
 constexpr int kFormSmall = 2;
 
 __device__ __forceinline__ void lane_form_row(const sw_ragged_t& m, const sw_bitfield_t& conn,
-                                              int excl_diag, uint64_t row_base, int64_t i, int acts,
-                                              int len, int64_t* unplaced, int64_t* counters,
+                                              int excl_diag, uint64_t row_base, int64_t row0, int64_t i,
+                                              int acts, int len, int64_t* unplaced, int64_t* counters,
                                               const sw_bitfield_t& sign, uint32_t* cache, int N,
                                               uint64_t rem, bool pow2, int cap) {
   const int64_t off = i * (int64_t)m.stride;
   uint64_t* crow = conn.words + i * conn.words_per_row;
-  const uint64_t key = sw::child_key(row_base, (uint64_t)i);
+  // row0: global index of local row 0 (row-sharded matrices): the row stream
+  // and the diagonal are those of the global row
+  const uint64_t key = sw::child_key(row_base, (uint64_t)(row0 + i));
   uint64_t ctr = 0;
   int placed[kFormSmall];
   int np = 0, a = 0, streak = 0, unpl = 0;
@@ -600,7 +606,7 @@ __device__ __forceinline__ void lane_form_row(const sw_ragged_t& m, const sw_bit
     const uint64_t h = sw::draw(key, ctr++);
     if (!sw::draw_valid(h, rem)) continue;   // a rejected draw is not an iteration
     const int j = (int)(pow2 ? (h & (uint64_t)(N - 1)) : (h % (uint64_t)N));
-    bool fail = excl_diag && j == (int)i;
+    bool fail = excl_diag && (int64_t)j == row0 + i;
     bool sbit = false;
     if (!fail) {
       const uint64_t cw = __ldcg(crow + (j >> 6));
@@ -633,7 +639,7 @@ __device__ __forceinline__ void lane_form_row(const sw_ragged_t& m, const sw_bit
 }
 
 __global__ void __launch_bounds__(kThreads, 8)
-k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row_base,
+k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row_base, int64_t row0,
                   const int32_t* act, int64_t* unplaced, int64_t* counters, sw_bitfield_t sign,
                   uint32_t* cache) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -652,7 +658,7 @@ k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row
     if (gi < m.num_pre && my_act == 0) unplaced[gi] = 0;
     // rows with few activations: one thread per row, all 32 rows in flight
     if (my_act > 0 && my_act <= kFormSmall)
-      lane_form_row(m, conn, excl_diag, row_base, gi, my_act, my_len, unplaced, counters, sign, cache,
+      lane_form_row(m, conn, excl_diag, row_base, row0, gi, my_act, my_len, unplaced, counters, sign, cache,
                     N, rem, pow2, cap);
     unsigned active = __ballot_sync(SW_FULL_MASK, my_act > kFormSmall);
     while (active) {
@@ -662,7 +668,7 @@ k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row
     const int acts = __shfl_sync(SW_FULL_MASK, my_act, src_lane);
     const int64_t off = i * (int64_t)m.stride;
     uint64_t* crow = conn.words + i * conn.words_per_row;
-    const uint64_t key = sw::child_key(row_base, (uint64_t)i);
+    const uint64_t key = sw::child_key(row_base, (uint64_t)(row0 + i));
     uint64_t ctr = 0;
     int len = __shfl_sync(SW_FULL_MASK, my_len, src_lane);
     int a = 0, streak = 0, unpl = 0;
@@ -678,7 +684,7 @@ k_deepr_form_rows(sw_ragged_t m, sw_bitfield_t conn, int excl_diag, uint64_t row
       const uint64_t h = live ? sw::draw(key, ctr + lane) : 0ull;
       const bool valid = live && sw::draw_valid(h, rem);
       const int j = (int)(pow2 ? (h & (uint64_t)(N - 1)) : (h % (uint64_t)N));
-      bool cand = valid && !(excl_diag && j == (int)i);
+      bool cand = valid && !(excl_diag && (int64_t)j == row0 + i);
       // the candidate's conn word and (for the slot-aligned cache) its sign
       // word are fetched together: one memory round trip per batch
       bool sbit = false;
@@ -885,9 +891,9 @@ extern "C" int sw_deepr_form_pass(const sw_ragged_t* m, const sw_bitfield_t* con
   cudaMemsetAsync(act, 0, (size_t)P * sizeof(int32_t), st);
   k_sum_i64<<<flat_grid(P, 256), 256, 0, st>>>(pending_src, P, counters); sw::count_launch();
   const uint64_t rem = sw::reject_rem((uint64_t)P);
-  k_form_hist<<<148 * 8, 256, 0, st>>>(counters, host_key, (uint64_t)P, rem, act); sw::count_launch();
+  k_form_hist<<<148 * 8, 256, 0, st>>>(counters, host_key, (uint64_t)P, rem, act, 0, 1); sw::count_launch();
   if (rem != 0) { k_form_hist_fix<<<1, 1, 0, st>>>(counters, host_key, (uint64_t)P, rem, act); sw::count_launch(); }
-  k_deepr_form_rows<<<rows_grid(P), kThreads, 0, st>>>(*m, *conn, excl_diag, row_base, act, unplaced, counters,
+  k_deepr_form_rows<<<rows_grid(P), kThreads, 0, st>>>(*m, *conn, excl_diag, row_base, 0, act, unplaced, counters,
       sign ? *sign : sw_bitfield_t{nullptr, 0, 0, 0}, sign ? sign_slot : nullptr); sw::count_launch();
   SW_CHECK_LAUNCH("sw_deepr_form_pass");
   return SW_OK;
@@ -914,5 +920,61 @@ extern "C" int sw_flip_signs(const sw_ragged_t* m, int32_t plane, uint64_t key, 
   if (g > 148 * 32) g = 148 * 32;
   k_flip_signs<<<(int)g, 256, 0, (cudaStream_t)stream>>>(*m, plane, key, prob); sw::count_launch();
   SW_CHECK_LAUNCH("sw_flip_signs");
+  return SW_OK;
+}
+
+// ---- row-sharded form pass (SURVEY 8e M-update): the phases of
+// sw_deepr_form_pass split at its collectives.  The host all-reduces
+// counters[0] (D) after sw_deepr_form_pending, counters[2] (rejected draws)
+// after sw_deepr_form_hist_chunk, reduce-scatters the num_pre_global
+// histogram by row owner, and all-reduces counters[1] (unplaced) after
+// sw_deepr_form_rows_shard.  Integer sums: bit-exact with the unsharded pass.
+extern "C" int sw_deepr_form_pending(const int64_t* pending_src, int64_t num_rows, int64_t* counters,
+                                     void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(counters, 0, 4 * sizeof(int64_t), st);
+  if (num_rows > 0) {
+    k_sum_i64<<<flat_grid(num_rows, 256), 256, 0, st>>>(pending_src, num_rows, counters); sw::count_launch();
+  }
+  SW_CHECK_LAUNCH("sw_deepr_form_pending");
+  return SW_OK;
+}
+
+extern "C" int sw_deepr_form_hist_chunk(int64_t* counters, uint64_t host_key, int64_t num_pre_global,
+                                        int32_t rank, int32_t world, int32_t* act_full, void* stream) {
+  if (world < 1 || rank < 0 || rank >= world || num_pre_global < 0) {
+    sw::set_last_error("sw_deepr_form_hist_chunk: bad rank/world");
+    return SW_ERR_INVALID_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (num_pre_global == 0) return SW_OK;
+  cudaMemsetAsync(act_full, 0, (size_t)num_pre_global * sizeof(int32_t), st);
+  const uint64_t rem = sw::reject_rem((uint64_t)num_pre_global);
+  k_form_hist<<<148 * 8, 256, 0, st>>>(counters, host_key, (uint64_t)num_pre_global, rem, act_full, rank, world);
+  sw::count_launch();
+  SW_CHECK_LAUNCH("sw_deepr_form_hist_chunk");
+  return SW_OK;
+}
+
+extern "C" int sw_deepr_form_hist_fix(int64_t* counters, uint64_t host_key, int64_t num_pre_global,
+                                      int32_t* act_full, void* stream) {
+  const uint64_t rem = sw::reject_rem((uint64_t)num_pre_global);
+  if (num_pre_global == 0 || rem == 0) return SW_OK;   // no draw can be rejected
+  k_form_hist_fix<<<1, 1, 0, (cudaStream_t)stream>>>(counters, host_key, (uint64_t)num_pre_global, rem, act_full);
+  sw::count_launch();
+  SW_CHECK_LAUNCH("sw_deepr_form_hist_fix");
+  return SW_OK;
+}
+
+extern "C" int sw_deepr_form_rows_shard(const sw_ragged_t* m, const sw_bitfield_t* conn, int32_t excl_diag,
+                                        uint64_t row_base, int64_t row0, const int32_t* act, int64_t* unplaced,
+                                        int64_t* counters, const sw_bitfield_t* sign, uint32_t* sign_slot,
+                                        void* stream) {
+  if (int s = check_ragged(m, "sw_deepr_form_rows_shard: bad matrix")) return s;
+  if (m->num_pre == 0) return SW_OK;
+  k_deepr_form_rows<<<rows_grid(m->num_pre), kThreads, 0, (cudaStream_t)stream>>>(*m, *conn, excl_diag, row_base,
+      row0, act, unplaced, counters, sign ? *sign : sw_bitfield_t{nullptr, 0, 0, 0}, sign ? sign_slot : nullptr);
+  sw::count_launch();
+  SW_CHECK_LAUNCH("sw_deepr_form_rows_shard");
   return SW_OK;
 }

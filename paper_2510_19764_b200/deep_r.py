@@ -30,8 +30,19 @@ from .updates import RuleDescriptor
 class DeepR:
     def __init__(self, matrix: RaggedMatrix, syn: SynVarMatrix, name: str,
                  weight_plane: str = "w", grad_plane: str = "grad",
-                 l1_strength: float = 0.005, exclude_diagonal: bool = False):
+                 l1_strength: float = 0.005, exclude_diagonal: bool = False,
+                 process_group=None, row0: int = 0, num_pre_global: int | None = None):
+        """``process_group``/``row0``/``num_pre_global``: row sharding (SURVEY
+        8e M-update).  ``matrix`` then holds rows [row0, row0 + num_pre) of a
+        ``num_pre_global``-row matrix; every rank of the group runs the same
+        update group and the result is bit-identical to one unsharded DeepR
+        (see ``_form_pass_sharded``)."""
         self.matrix = matrix
+        self.pg = process_group
+        self.row0 = int(row0)
+        self.num_pre_global = int(num_pre_global if num_pre_global is not None else matrix.num_pre)
+        if self.pg is None and (self.row0 != 0 or self.num_pre_global != matrix.num_pre):
+            raise ValueError("row0/num_pre_global need a process_group")
         self.syn = syn
         self.name = name
         self.weight_plane = weight_plane
@@ -54,6 +65,7 @@ class DeepR:
         # per-row marked-slot bitmasks between the eliminate scan and removal kernels
         self._marks = torch.zeros_like(self._sign_slot)
         self._cache_version = None
+        self._act_full = None     # [num_pre_global] histogram (sharded form)
 
     # -- helpers ---------------------------------------------------------------
     def _desc(self):
@@ -117,6 +129,8 @@ class DeepR:
 
     # -- form rule ------------------------------------------------------------------------
     def _form_pass(self, model, binding, pass_index, host_key, row_base) -> bool:
+        if self.pg is not None:
+            return self._form_pass_sharded(pass_index, host_key, row_base)
         d = self._desc()
         src = self.dormant if pass_index == 0 else self._unplaced
         if pass_index == 0:
@@ -135,6 +149,10 @@ class DeepR:
         drawn, unplaced = int(self._counters_host[0]), int(self._counters_host[1])
         # version: bumped only when the structure changed -- pass 0 with
         # removals (the eliminate pass's change), or any pass placing synapses
+        return self._form_continue(pass_index, drawn, unplaced)
+
+    def _form_continue(self, pass_index: int, drawn: int, unplaced: int) -> bool:
+        """_form_continue (deep_r.py:147-160) on the pass's global counts."""
         if (pass_index == 0 and drawn > 0) or drawn - unplaced > 0:
             self.matrix.version += 1
         self._cache_version = self.matrix.version
@@ -142,12 +160,54 @@ class DeepR:
             return False
         if drawn - unplaced == 0:
             self._no_progress_passes += 1
-            if self._no_progress_passes >= self.matrix.num_pre:
+            if self._no_progress_passes >= self.num_pre_global:
                 raise RowFull(f"{self.name}: could not place {unplaced} new synapses "
                               f"after {self._no_progress_passes} stalled passes")
         else:
             self._no_progress_passes = 0
         return True
+
+    def _form_pass_sharded(self, pass_index, host_key, row_base) -> bool:
+        """Row-sharded form pass (SURVEY 8e M-update).  The D host draws of
+        deep_r.py:110-121 are split into equal counter chunks, one per rank,
+        each histogrammed over all rows; the histograms are reduce-scattered
+        to the row owners, which place their rows with the global row's
+        stream (deep_r.py:126-145).  D, the rejected-draw count and the
+        unplaced count are all-reduced, so every rank takes the same
+        pass-loop decision.  Integer sums throughout: bit-exact with the
+        unsharded pass."""
+        from .sharding import reduce_scatter_rows
+        import torch.distributed as dist
+        rank, world = dist.get_rank(self.pg), dist.get_world_size(self.pg)
+        st = _lib.stream_ptr()
+        src = self.dormant if pass_index == 0 else self._unplaced
+        if pass_index == 0:
+            self._no_progress_passes = 0
+        P, PG = self.matrix.num_pre, self.num_pre_global
+        if self._act_full is None:
+            self._act_full = torch.zeros(PG, dtype=torch.int32, device=self.matrix.target.device)
+        _lib.call("sw_deepr_form_pending", src.data_ptr(), P, self._counters.data_ptr(), st)
+        dist.all_reduce(self._counters[0:1], group=self.pg)
+        _lib.call("sw_deepr_form_hist_chunk", self._counters.data_ptr(), host_key, PG, rank, world,
+                  self._act_full.data_ptr(), _lib.stream_ptr())
+        dist.all_reduce(self._counters[2:3], group=self.pg)
+        if rank == 0:
+            _lib.call("sw_deepr_form_hist_fix", self._counters.data_ptr(), host_key, PG,
+                      self._act_full.data_ptr(), _lib.stream_ptr())
+        reduce_scatter_rows(self._act_full, self._activations, self.row0, self.pg)
+        d = self._desc()
+        _lib.call("sw_deepr_form_rows_shard", ctypes.byref(d), ctypes.byref(self.conn_bits.descriptor()),
+                  int(self.exclude_diagonal), row_base, self.row0, self._activations.data_ptr(),
+                  self._unplaced.data_ptr(), self._counters.data_ptr(),
+                  ctypes.byref(self.sign_bits.descriptor()), self._sync_cache(), _lib.stream_ptr())
+        dist.all_reduce(self._counters[1:2], group=self.pg)
+        if pass_index == 0:
+            self._last_removed_dev.copy_(self._counters[0:1])
+        self._counters_host.copy_(self._counters, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        drawn, unplaced = int(self._counters_host[0]), int(self._counters_host[1])
+        # structure changed somewhere: every rank bumps its version alike
+        return self._form_continue(pass_index, drawn, unplaced)
 
     def form_rule(self) -> RuleDescriptor:
         return RuleDescriptor(name=f"{self.name}_form", device_pass=self._form_pass)

@@ -84,3 +84,36 @@ def allreduce_flat(tensors, group=None) -> None:
         n = t.numel()
         t.copy_(flat[o:o + n].view_as(t))
         o += n
+
+
+# ---- M-update microbench: rows sharded ---------------------------
+def shard_rows(num_pre: int, rank: int, world: int) -> tuple[int, int]:
+    """Rows [lo, hi) owned by ``rank``: equal contiguous chunks (the last
+    rank takes the remainder)."""
+    per = num_pre // world
+    lo = rank * per
+    return lo, (num_pre if rank == world - 1 else lo + per)
+
+
+def reduce_scatter_rows(full: torch.Tensor, local: torch.Tensor, row0: int, group=None) -> None:
+    """``local[:] = sum over ranks of full[row0 : row0 + len(local)]``.
+
+    NCCL with equal row chunks: one reduce-scatter (the activation
+    histogram, 4 B per row).  Otherwise (gloo, ragged chunks): all-reduce of
+    the full vector, then the owner's slice."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    n = local.numel()
+    equal = full.numel() == n * world and row0 == dist.get_rank(group) * n
+    if equal and dist.get_backend(group) == "nccl":
+        dist.reduce_scatter_tensor(local, full, group=group)
+        return
+    dist.all_reduce(full, group=group)
+    local.copy_(full[row0:row0 + n])
+
+
+# ---- M-prop microbench: posts sharded (SURVEY 8e) ----------------------------
+def shard_posts(num_post: int, rank: int, world: int) -> tuple[int, int]:
+    """Posts [lo, hi) owned by ``rank`` in the column-sliced propagation:
+    equal contiguous ranges (the last rank takes the remainder)."""
+    return shard_rows(num_post, rank, world)

@@ -182,6 +182,108 @@ class RewiringRule:
             self.form_events.extend((time_ms, float(x)) for x in dist[kind == 2])
 
 
+class TopomapRecorder:
+    """The reference's analysis trail (topomap.py:235-318) over the device
+    model: degree statistics and the on-axis displacement profile at every
+    snapshot, edge lists at the start and end, rewiring events and
+    (optionally) spikes, with the reference's CSV writers (same formats,
+    byte-identical for the same state; cli.py:117-125 for the edge lists).
+    Snapshots copy the connectivity to the host, so they run between
+    CUDA-graph replays, never inside one."""
+
+    def __init__(self, snapshot_every_ms: float = 200.0, record_spikes: bool = False):
+        self.snapshot_every_ms = snapshot_every_ms
+        self.record_spikes = record_spikes
+        self.degrees: list[tuple] = []
+        self.profile: list[tuple] = []
+        self.snapshots: dict[tuple[str, str], tuple] = {}
+        self.events: dict[tuple[str, str], list[tuple[float, float]]] = {}
+        self.spikes: dict[str, list[tuple[float, int]]] = {"source": [], "target": []}
+
+    def on_spikes(self, population: str, t_ms: float, ids) -> None:
+        if self.record_spikes and len(ids):
+            self.spikes[population].extend((t_ms, int(i)) for i in ids)
+
+    @staticmethod
+    def host_edges(model, proj: str):
+        """(pre, post, w, row_length, num_post) of a projection, row-major slot
+        order (RaggedMatrix.edge_list, connectivity.py:55-60)."""
+        m, syn = model.net.matrices[proj]
+        mask = m.slot_mask()
+        pre, post = m.edge_list()
+        w = syn.planes["g"][mask].cpu().numpy()
+        return pre, post, w, m.row_length.cpu().numpy(), m.num_post
+
+    def snapshot(self, t_ms: float, model, tag: str | None = None, rows: bool = True) -> None:
+        for proj in ("ff", "lat"):
+            self.snapshot_edges(t_ms, proj, model.geometry, *self.host_edges(model, proj), tag=tag, rows=rows)
+
+    def snapshot_edges(self, t_ms, proj, geometry, pre, post, w, row_length, num_post,
+                       tag=None, rows=True) -> None:
+        if rows:
+            in_deg = np.bincount(post, minlength=num_post)
+            out_deg = row_length
+            self.degrees.append((t_ms, proj, float(in_deg.mean()), float(in_deg.std()),
+                                 float(out_deg.mean()), float(out_deg.std())))
+            self._profile_rows(t_ms, proj, geometry, pre, post, w)
+        if tag is not None:
+            self.snapshots[(proj, tag)] = (pre.copy(), post.copy(), w.copy())
+
+    def _profile_rows(self, t_ms, proj, geom, pre, post, w):
+        half = geom.side // 2
+        dx, dy = geom.displacement(pre, post)
+        on_axis = dx == 0
+        dy_idx = (dy[on_axis] + half).astype(np.int64)
+        counts = np.bincount(dy_idx, minlength=geom.side)
+        weight_sums = np.bincount(dy_idx, weights=w[on_axis], minlength=geom.side)
+        for b in range(geom.side):
+            mean_w = weight_sums[b] / counts[b] if counts[b] else 0.0
+            self.profile.append((t_ms, proj, b - half, counts[b] / geom.n, mean_w))
+
+    def take_events(self, model) -> None:
+        for proj, rule in (("ff", model.ff_rule), ("lat", model.lat_rule)):
+            self.events[(proj, "elimination")] = rule.elim_events
+            self.events[(proj, "formation")] = rule.form_events
+
+    # -- CSV output (topomap.py:287-318, cli.py:117-125) --------------------------
+    def write_spikes_csv(self, fh, population: str) -> None:
+        fh.write("time_ms,neuron_id\n")
+        for t, i in self.spikes[population]:
+            fh.write(f"{t:g},{i}\n")
+
+    def write_degrees_csv(self, fh) -> None:
+        fh.write("time_ms,projection,mean_in,std_in,mean_out,std_out\n")
+        for t, proj, mi, si, mo, so in self.degrees:
+            fh.write(f"{t:g},{proj},{mi:.9g},{si:.9g},{mo:.9g},{so:.9g}\n")
+
+    def write_profile_csv(self, fh) -> None:
+        fh.write("time_ms,projection,y_displacement,conn_prob,mean_weight\n")
+        for t, proj, dy, cp, mw in self.profile:
+            fh.write(f"{t:g},{proj},{dy},{cp:.9g},{mw:.9g}\n")
+
+    def write_events_csv(self, fh, kind: str) -> None:
+        """Counts per (time bin, integer distance bin), both projections."""
+        fh.write("time_bin_ms,distance_bin,count\n")
+        bin_ms = self.snapshot_every_ms
+        merged: dict[tuple[float, int], int] = {}
+        for (proj, k), events in sorted(self.events.items()):
+            if k != kind:
+                continue
+            for t, d in events:
+                key = (math.floor(t / bin_ms) * bin_ms, int(d))
+                merged[key] = merged.get(key, 0) + 1
+        for (tb, db) in sorted(merged):
+            fh.write(f"{tb:g},{db},{merged[(tb, db)]}\n")
+
+    def write_connectivity_csv(self, fh, proj: str, tag: str) -> None:
+        """``pre,post,weight`` sorted by (pre, post), weights repr'd
+        (cli.py:117-125)."""
+        pre, post, w = self.snapshots[(proj, tag)]
+        fh.write("pre,post,weight\n")
+        for k in np.lexsort((post, pre)):
+            fh.write(f"{pre[k]},{post[k]},{float(w[k])!r}\n")
+
+
 @dataclass
 class RunRecord:
     steps: int = 0
@@ -345,10 +447,14 @@ class TopomapModel:
         stim_steps = int(round(PoissonParams().t_stim / h))
         rewire_steps = int(round(self.ff_params.t_rewiring / h))
         n_steps = int(round(duration_ms / h))
-        if recorder is not None:
-            raise NotImplementedError("TopomapRecorder analysis trail is out of scope (SURVEY 2.1)")
+        snap_steps = int(round(recorder.snapshot_every_ms / h)) if recorder is not None else 0
+        if recorder is not None and self.step_index == 0:
+            recorder.snapshot(0.0, self, tag="initial")
+        spikes_each_step = recorder is not None and recorder.record_spikes
         graph_ok = (self.use_graph and self.shard.world == 1 and not self.ff_rule.record_events
-                    and not self.lat_rule.record_events and stim_steps % rewire_steps == 0)
+                    and not self.lat_rule.record_events and stim_steps % rewire_steps == 0
+                    and not spikes_each_step
+                    and (not snap_steps or snap_steps % rewire_steps == 0))
         u0 = self.ff_rule._host_update if self.ff_rule._host_update else 0
         # periods per replay: the largest divisor of the periods per stimulus
         # interval that is <= PERIODS_PER_GRAPH (a replay never crosses a
@@ -356,6 +462,8 @@ class TopomapModel:
         multi = 1
         if graph_ok:
             stim_periods = stim_steps // rewire_steps
+            if snap_steps:
+                stim_periods = math.gcd(stim_periods, snap_steps // rewire_steps)
             multi = max(d for d in range(1, min(PERIODS_PER_GRAPH, stim_periods) + 1) if stim_periods % d == 0)
         done = 0
         while done < n_steps:
@@ -375,8 +483,15 @@ class TopomapModel:
                 done += periods * rewire_steps
                 record.steps += periods * rewire_steps
                 record.rewiring_executions += periods
+                if snap_steps and self.step_index % snap_steps == 0:
+                    recorder.snapshot(self.step_index * h, self)
                 continue
             self._launch_step()
+            if spikes_each_step:
+                from .neurons import unpack_spike_bits
+                n = self.geometry.n
+                recorder.on_spikes("source", k * h, unpack_spike_bits(self.source.spike_bits, n).cpu().numpy())
+                recorder.on_spikes("target", k * h, unpack_spike_bits(self.target.spike_bits, n).cpu().numpy())
             self.step_index += 1
             done += 1
             record.steps += 1
@@ -387,6 +502,12 @@ class TopomapModel:
                 self.ff_rule.collect(t_ms)
                 self.lat_rule.collect(t_ms)
                 record.rewiring_executions += 1
+            if snap_steps and self.step_index % snap_steps == 0:
+                recorder.snapshot(self.step_index * h, self)
+        if recorder is not None:
+            just_written = n_steps == 0 or (snap_steps and self.step_index % snap_steps == 0)
+            recorder.snapshot(self.step_index * h, self, tag="final", rows=not just_written)
+            recorder.take_events(self)
         if record.rewiring_executions:
             n_up = self.ff_rule._host_update - u0
             log = self._update_log[u0:u0 + n_up].cpu().numpy() if n_up > 0 else np.zeros((0, 4))

@@ -376,7 +376,69 @@ def gen_stdp():
     save("stdp.npz", **out)
 
 
+def gen_recorder():
+    """TopomapRecorder CSV outputs of a short reference run (topomap.py:235-318,
+    cli.py:117-125) with the edge lists of every snapshot and the rewiring
+    events, so the device recorder's writers can be checked byte-for-byte on
+    the same state."""
+    import io
+    from sparsewire.topomap import TopomapModel, TopomapRecorder
+    model = TopomapModel(1, seed=6)
+    rec = TopomapRecorder(snapshot_every_ms=10.0, record_spikes=True)
+    states = []
+    orig = rec.snapshot
+
+    def snap(t_ms, mdl, tag=None, rows=True, _orig=orig):
+        st = {"t": np.float64(t_ms), "tag": np.array(tag or ""), "rows": np.bool_(rows)}
+        for proj in ("ff", "lat"):
+            m, syn = mdl.net.matrices[proj]
+            st[f"{proj}_row_length"] = m.row_length.copy()
+            st[f"{proj}_target"] = m.target.copy()
+            st[f"{proj}_g"] = syn.planes["g"].copy()
+        states.append(st)
+        _orig(t_ms, mdl, tag=tag, rows=rows)
+    rec.snapshot = snap
+    model.run(30.0, rec)
+    out = {"n_states": np.int64(len(states))}
+    for k, st in enumerate(states):
+        for key, v in st.items():
+            out[f"s{k}_{key}"] = v
+    texts = {}
+    for name, fn in (("degrees", rec.write_degrees_csv), ("profile", rec.write_profile_csv)):
+        fh = io.StringIO()
+        fn(fh)
+        texts[name] = fh.getvalue()
+    for kind in ("elimination", "formation"):
+        fh = io.StringIO()
+        rec.write_events_csv(fh, kind)
+        texts[f"events_{kind}"] = fh.getvalue()
+    for pop in ("source", "target"):
+        fh = io.StringIO()
+        rec.write_spikes_csv(fh, pop)
+        texts[f"spikes_{pop}"] = fh.getvalue()
+        sp = np.array(rec.spikes[pop], dtype=np.float64).reshape(-1, 2)
+        out[f"spikes_{pop}"] = sp
+    for (proj, kind), ev in rec.events.items():
+        out[f"events_{proj}_{kind}"] = np.array(ev, dtype=np.float64).reshape(-1, 2)
+    for proj in ("ff", "lat"):
+        for tag in ("initial", "final"):
+            pre, post, w = rec.snapshots[(proj, tag)]
+            fh = io.StringIO()
+            fh.write("pre,post,weight\n")
+            for k in np.lexsort((post, pre)):
+                fh.write(f"{pre[k]},{post[k]},{float(w[k])!r}\n")
+            texts[f"connectivity_{proj}_{tag}"] = fh.getvalue()
+    for k, v in texts.items():
+        out[f"csv_{k}"] = np.array(v)
+    save("recorder.npz", **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[f"gen_{name}"]()
+        sys.exit(0)
+    gen_recorder()
     gen_topomap()
     gen_stdp()
     gen_trainer()

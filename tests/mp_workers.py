@@ -213,3 +213,104 @@ def device_trainer_dp(rank, world, port, out):
                  hashlib.sha256(tr.connectivity_fingerprint()).hexdigest()))
     finally:
         dist.destroy_process_group()
+
+
+# ---- M-update / M-prop microbench sharding -----------------------
+def mupdate_instance(P=4096, N=8192, cap=160, seed=5, flip=0.05):
+    """A small M-update instance on cuda:0 (same recipe as bench.run_mupdate):
+    Bernoulli rows, four float64 planes, DEEP R bitfields, sign flips."""
+    import ctypes
+    from paper_2510_19764_b200 import _lib
+    from paper_2510_19764_b200.connectivity import descriptor, init_pairwise_bernoulli_density
+    from paper_2510_19764_b200.rng import CounterRng, fold_key
+    planes = ("w", "grad", "adam_m", "adam_v")
+    m, syn = init_pairwise_bernoulli_density(P, N, 64.0 / N, 1.0, CounterRng(seed, "init", "M"),
+                                             var_names=planes, capacity=cap)
+    w = syn.planes["w"]
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    w.copy_(torch.randn(w.shape, generator=g, device="cuda", dtype=torch.float64) * 0.1)
+    w.mul_(m.slot_mask())
+    from paper_2510_19764_b200.deep_r import DeepR
+    dr = DeepR(m, syn, "M", l1_strength=0.0, exclude_diagonal=True)
+    dr.init_bitfields(CounterRng(seed, "deep_r", "M"))
+    return m, syn, dr, lambda u: _lib.call("sw_flip_signs", ctypes.byref(descriptor(m, syn)), 0,
+                                           fold_key(seed, "flip", u), flip, _lib.stream_ptr())
+
+
+def mupdate_state(m, syn, dr):
+    return {"row_length": m.row_length.cpu().numpy(), "target": (m.target * m.slot_mask()).cpu().numpy(),
+            "w": (syn.planes["w"] * m.slot_mask()).cpu().numpy(),
+            "conn": dr.conn_bits.words.cpu().numpy(), "sign": dr.sign_bits.words.cpu().numpy()}
+
+
+def run_mupdate(rank, world, updates=3, pg=None):
+    """``updates`` DEEP R groups on the instance; rows [lo, hi) of this rank
+    (world == 1: the unsharded run).  Returns the local state after each."""
+    from paper_2510_19764_b200.connectivity import row_slice
+    from paper_2510_19764_b200.deep_r import DeepR
+    from paper_2510_19764_b200.sharding import shard_rows
+    from paper_2510_19764_b200.updates import Model
+    m, syn, dr, flip = mupdate_instance()
+    P = m.num_pre
+    lo, hi = shard_rows(P, rank, world)
+    if world > 1:
+        ms, ss = row_slice(m, syn, lo, hi)
+        drs = DeepR(ms, ss, "M", l1_strength=0.0, exclude_diagonal=True, process_group=pg,
+                    row0=lo, num_pre_global=P)
+        drs.load_state(dr.sign_bits.words[lo:hi].cpu().numpy(), dr.conn_bits.words[lo:hi].cpu().numpy())
+        full = (m, syn)
+    else:
+        ms, ss, drs = m, syn, dr
+    model = Model(5)
+    model.add_matrix("M", ms, ss)
+    drs.register(model, "deep_r", "M")
+    res = []
+    for u in range(updates):
+        if world > 1:
+            # the flips are drawn on the full matrix (counter = i*stride + s)
+            # and copied to this rank's rows
+            full[1].planes["w"][lo:hi].copy_(ss.planes["w"])
+            full[0].row_length[lo:hi].copy_(ms.row_length)
+            flip(u)
+            ss.planes["w"].copy_(full[1].planes["w"][lo:hi])
+        else:
+            flip(u)
+        model.run_update_group("deep_r")
+        st = mupdate_state(ms, ss, drs)
+        st["removed"] = drs.last_removed
+        res.append(st)
+    return (lo, hi), res
+
+
+def mupdate_sharded(rank, world, port, out):
+    """Row-sharded DEEP R (gloo, both ranks on cuda:0)."""
+    _init(rank, world, port)
+    try:
+        rng, res = run_mupdate(rank, world, pg=dist.group.WORLD)
+        out.put((rank, rng, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def form_hist_sharded(rank, world, port, out):
+    """Host logic of the row-sharded form pass on CPU (gloo): rank r
+    histograms host draws [D*r/W, D*(r+1)/W) over all rows (oracle draw
+    arithmetic, deep_r.py:119-120), the histograms are reduce-scattered to
+    the row owners.  Returns this rank's rows of the activation histogram."""
+    from oracle.rng import draw_u64, fold_key
+    from paper_2510_19764_b200.sharding import reduce_scatter_rows, shard_rows
+    _init(rank, world, port)
+    try:
+        res = []
+        for P, D in ((1000, 5000), (1 << 12, 777), (37, 3)):
+            key = fold_key(9, "host", 1, 2, 0)
+            lo, hi = shard_rows(P, rank, world)
+            full = torch.zeros(P, dtype=torch.int32)
+            for c in range(D * rank // world, D * (rank + 1) // world):
+                full[draw_u64(key, c) % P] += 1     # P < 2^32: no rejection
+            local = torch.zeros(hi - lo, dtype=torch.int32)
+            reduce_scatter_rows(full, local, lo)
+            res.append((P, lo, hi, local.numpy().copy()))
+        out.put((rank, res))
+    finally:
+        dist.destroy_process_group()

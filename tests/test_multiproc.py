@@ -93,3 +93,21 @@ def test_topomap_post_sharding_matches_unsharded():
         assert np.array_equal(st["V"][lo:hi], ref["V"][lo:hi]), r
     # the run exercised rewiring and spikes
     assert ref["ff.y"].sum() > 0
+
+
+def test_row_sharded_form_histogram_two_ranks():
+    """M-update row sharding: per-rank counter chunks of the
+    host draws, reduce-scattered by row owner == the serial histogram of
+    deep_r.py:119-120 (oracle stream)."""
+    from oracle.rng import Stream, fold_key
+    res = _run(mp_workers.form_hist_sharded)
+    for k, (P, D) in enumerate(((1000, 5000), (1 << 12, 777), (37, 3))):
+        rng = Stream(fold_key(9, "host", 1, 2, 0))
+        ref = np.zeros(P, dtype=np.int32)
+        for _ in range(D):
+            ref[rng.uniform_int(P)] += 1
+        got = np.zeros(P, dtype=np.int32)
+        for r in range(2):
+            P_, lo, hi, local = res[r][0][k]
+            got[lo:hi] = local
+        assert np.array_equal(got, ref)
