@@ -292,6 +292,55 @@ SW_API int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, cons
                                 double* g_w_out, double* g_b_out, int32_t num_classes,
                                 uint32_t* workspace, void* stream);
 
+/* ---- replica-minor e-prop pass (the trainer's hot path) ----------------------
+ * The forward pass writes its per-step vectors replica-major ([B, n]).
+ * sw_eprop_prep makes replica-minor copies of a group of k steps --
+ * xbar_t[k][num_inputs][ldb], zbar_t/psi_t[k][hidden][ldb] -- and the learning
+ * signal lsig_t[k][hidden][ldb] = f32(sum_c d[b][c] * w_out[c][h]) (classes
+ * ascending: classifier.py:223).  Columns b in [batch, ldb) are zero.
+ * sw_eprop_pass runs k recursion steps of _kernels.py:15-39 over both
+ * projections on those copies: eps/ebar in [e_pad/8][ldb/32][32][8] order
+ * (8-synapse tile, 32-replica chunk, lane = 4*synapse + replica group,
+ * 8 replicas), ldb a multiple of 32, bit-identical to the
+ * reference's; the float64 gradient terms are summed per synapse in
+ * 64-replica splits and the splits added in order (within float64 rounding
+ * of the reference's replica-ordered sum).  scratch:
+ * sw_eprop_pass_scratch_bytes(total e_pad, ldb) bytes, zeroed once (the kernel
+ * leaves its counters zero). */
+typedef struct sw_eprop_prep {
+  int32_t k, batch, ldb, num_inputs, hidden, num_classes;
+  const float* xbar[SW_EPROP_MAX_BLOCK];   /* [batch, num_inputs] per step */
+  const float* zbar[SW_EPROP_MAX_BLOCK];   /* [batch, hidden] */
+  const float* psi[SW_EPROP_MAX_BLOCK];    /* [batch, hidden] */
+  const double* d[SW_EPROP_MAX_BLOCK];     /* [batch, num_classes] */
+  const double* w_out;                     /* [num_classes, hidden] */
+  float* xbar_t; float* zbar_t; float* psi_t; float* lsig_t;
+  /* optional readout gradients (classifier.py:221-222) over the group:
+   * g_w_out[C, H] += sum d^T zbar, g_b_out[C] += sum d, through ro_partial
+   * (sw_eprop_prep_scratch_bytes); g_w_out NULL = none */
+  double* g_w_out; double* g_b_out; double* ro_partial;
+} sw_eprop_prep_t;
+SW_API int64_t sw_eprop_prep_scratch_bytes(int32_t k, int32_t batch, int32_t hidden, int32_t num_classes);
+SW_API int sw_eprop_prep(const sw_eprop_prep_t* p, void* stream);
+
+typedef struct sw_eprop_tseg {
+  const int32_t* pre;                        /* [e_pad] plan order */
+  const int32_t* post;
+  const float* trace_t[SW_EPROP_MAX_BLOCK];  /* [num_pre, ldb] per step */
+  float* eps; float* ebar;                   /* [e_pad/8][ldb/32][32][8] */
+  double* grad;                              /* [e_pad] compact gradient */
+  int32_t e_pad;
+} sw_eprop_tseg_t;
+typedef struct sw_eprop_tpass {
+  int32_t k;
+  const float* psi_t[SW_EPROP_MAX_BLOCK];    /* [hidden, ldb] per step */
+  const float* lsig_t[SW_EPROP_MAX_BLOCK];
+  void* scratch;
+} sw_eprop_tpass_t;
+SW_API int64_t sw_eprop_pass_scratch_bytes(int32_t e_pad_total, int32_t ldb);
+SW_API int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const sw_eprop_tpass_t* p,
+                           int32_t ldb, float beta, float rho, float alpha, void* stream);
+
 /* ---- neurons (neurons.py) --------------------------------------------------- */
 /* AlifLayer.step (neurons.py:60-67), float32, n = batch*hidden elements. */
 SW_API int sw_alif_step(float* v, float* a, float* z, const float* rec, const float* ext,

@@ -86,6 +86,26 @@ class EpropBlock(C.Structure):
                 ("ro_scratch", P), ("ro_splits", I32)]
 
 
+class EpropPrep(C.Structure):
+    """sw_eprop_prep_t"""
+    _fields_ = [("k", I32), ("batch", I32), ("ldb", I32), ("num_inputs", I32), ("hidden", I32),
+                ("num_classes", I32), ("xbar", P * MAX_BLOCK), ("zbar", P * MAX_BLOCK),
+                ("psi", P * MAX_BLOCK), ("d", P * MAX_BLOCK), ("w_out", P), ("xbar_t", P),
+                ("zbar_t", P), ("psi_t", P), ("lsig_t", P), ("g_w_out", P), ("g_b_out", P),
+                ("ro_partial", P)]
+
+
+class EpropTSeg(C.Structure):
+    """sw_eprop_tseg_t"""
+    _fields_ = [("pre", P), ("post", P), ("trace_t", P * MAX_BLOCK), ("eps", P), ("ebar", P),
+                ("grad", P), ("e_pad", I32)]
+
+
+class EpropTPass(C.Structure):
+    """sw_eprop_tpass_t"""
+    _fields_ = [("k", I32), ("psi_t", P * MAX_BLOCK), ("lsig_t", P * MAX_BLOCK), ("scratch", P)]
+
+
 class ClfStep(C.Structure):
     """sw_clf_step_t"""
     _fields_ = [("in_row_length", P), ("in_target", P), ("in_w32", P), ("in_stride", I32),
@@ -129,6 +149,10 @@ SIGNATURES: dict[str, list] = {
     "sw_eprop_fused_step": [C.c_void_p, I32, P, P, I32, I32, F32, F32, F32, P, P, P, P, I32, I32, P, P],
     "sw_eprop_fused_block": [C.c_void_p, I32, P, I32, I32, F32, F32, F32, P, P, I32, P, P],
     "sw_eprop_readout_scratch_bytes": [I32, I32, I32],
+    "sw_eprop_prep": [P, P],
+    "sw_eprop_prep_scratch_bytes": [I32, I32, I32, I32],
+    "sw_eprop_pass": [C.c_void_p, I32, P, I32, F32, F32, F32, P],
+    "sw_eprop_pass_scratch_bytes": [I32, I32],
     "sw_prop_bucket_slabs": [I32],
     "sw_prop_buckets_build": [P, P, P, I32, I32, I32, P, P, P, P, P],
     "sw_prop_buckets_refresh": [P, P, I32, I32, P, P, P],
@@ -185,6 +209,8 @@ def lib():
     L.sw_eprop_readout_scratch_bytes.argtypes = [I32, I32, I32]
     L.sw_eprop_readout_scratch_bytes.restype = C.c_int64
     L.sw_prop_bucketed_workspace_bytes.restype = C.c_int64
+    L.sw_eprop_pass_scratch_bytes.restype = C.c_int64
+    L.sw_eprop_prep_scratch_bytes.restype = C.c_int64
     L.sw_rewire_scratch_bytes.restype = C.c_int64
     L.sw_launch_count.argtypes = []
     L.sw_launch_count.restype = C.c_longlong

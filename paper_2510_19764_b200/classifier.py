@@ -115,13 +115,19 @@ class SyntheticTask:
 
 
 class _Plan:
-    """Compact per-batch synapse order of one projection (sw_eprop_plan)."""
+    """Compact per-batch synapse order of one projection (sw_eprop_plan:
+    bucketed by post >> shift, then pre, then slot) and its eligibility state.
+    layout "chunk" (the trainer's, sw_eprop_pass): [e_pad/8][ldb/32][32][8],
+    with shift 0 (synapses by post); layout "tile" (sw_eprop_fused_step /
+    _block): [tile][batch][32]."""
 
-    def __init__(self, m, batch, shift=5):
+    def __init__(self, m, batch, shift=5, layout="tile"):
         self.m = m
         self.shift = shift
+        self.layout = layout
         self.e_pad = 0
         self.batch = batch
+        self.ldb = -(-batch // 32) * 32
         G = ((m.num_post - 1) >> shift) + 1
         self.scratch = torch.zeros(2 * G * m.num_pre, dtype=torch.int32, device="cuda")
         self.total = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -136,9 +142,21 @@ class _Plan:
         self.post = torch.zeros(e_pad, dtype=torch.int32, device=dev)
         self.off = torch.zeros(e_pad, dtype=torch.int32, device=dev)
         self.grad = torch.zeros(e_pad, dtype=torch.float64, device=dev)
-        # tile-major eligibility state [tile, replica, lane] (sw_eprop_fused_block)
-        self.eps = torch.zeros((e_pad // 32, self.batch, 32), dtype=torch.float32, device=dev)
+        if self.layout == "chunk":
+            # [8-synapse tile, 32-replica chunk, lane = 4 * synapse + group,
+            # 8 replicas of the group] (sw_eprop_pass)
+            self.eps = torch.zeros((e_pad // 8, self.ldb // 32, 32, 8), dtype=torch.float32, device=dev)
+        else:
+            # [tile, replica, lane] (sw_eprop_fused_step / sw_eprop_fused_block)
+            self.eps = torch.zeros((e_pad // 32, self.batch, 32), dtype=torch.float32, device=dev)
         self.ebar = torch.zeros_like(self.eps)
+
+    def replica_major(self, state: torch.Tensor) -> torch.Tensor:
+        """[batch, e_pad] copy of eps or ebar (tests, inspection)."""
+        if self.layout == "chunk":
+            t = state.view(self.e_pad // 8, self.ldb // 32, 8, 4, 8)      # [t8, c, s, g, r]
+            return t.permute(1, 3, 4, 0, 2).reshape(self.ldb, self.e_pad)[:self.batch]
+        return state.permute(1, 0, 2).reshape(self.batch, self.e_pad)
 
     def build(self) -> None:
         m = self.m
@@ -146,6 +164,15 @@ class _Plan:
                   m.stride, m.num_post, self.shift, self.scratch.data_ptr(), self.pre.data_ptr(),
                   self.post.data_ptr(), self.off.data_ptr(), self.e_pad, self.total.data_ptr(),
                   _lib.stream_ptr())
+
+    def tseg(self, trace_t: list) -> _lib.EpropTSeg:
+        s = _lib.EpropTSeg()
+        s.pre, s.post = self.pre.data_ptr(), self.post.data_ptr()
+        for k, t in enumerate(trace_t):
+            s.trace_t[k] = t.data_ptr()
+        s.eps, s.ebar, s.grad = self.eps.data_ptr(), self.ebar.data_ptr(), self.grad.data_ptr()
+        s.e_pad = self.e_pad
+        return s
 
     def seg(self, trace: torch.Tensor) -> _lib.EpropSeg:
         s = _lib.EpropSeg()
@@ -268,9 +295,22 @@ class EpropClassifierTrainer:
         self.pin_p = torch.zeros((B, NI), dtype=torch.float64, pin_memory=True)
         self.pin_keys = torch.zeros(B, dtype=torch.int64, pin_memory=True)
         self.pin_labels = torch.zeros(B, dtype=torch.int32, pin_memory=True)
-        self.plan_in = _Plan(self.m_in, B)
-        self.plan_rec = _Plan(self.m_rec, B)
+        self.plan_in = _Plan(self.m_in, B, shift=0, layout="chunk")
+        self.plan_rec = _Plan(self.m_rec, B, shift=0, layout="chunk")
         self._segs = (_lib.EpropSeg * 2)()
+        # replica-minor copies of one group's e-prop inputs (sw_eprop_prep):
+        # [K][rows][ldb], and the pass kernel's split partials / tickets
+        K, L = EPROP_BLOCK_STEPS, self.plan_in.ldb
+        self.xbar_t = torch.zeros((K, NI, L), **f32)
+        self.zbar_t = torch.zeros((K, H, L), **f32)
+        self.psi_t = torch.zeros((K, H, L), **f32)
+        self.lsig_t = torch.zeros((K, H, L), **f32)
+        self._tsegs = (_lib.EpropTSeg * 2)()
+        nb = int(_lib.lib().sw_eprop_prep_scratch_bytes(K, B, H, C))
+        self._ro_partial = torch.zeros(nb // 8 + 1, **f64)
+        self._pass_scratch = None
+        self._pass_scratch_key = None
+        self._empty_segs = (_lib.EpropSeg * 2)()
         # split readout-gradient partials of the blocked e-prop pass
         self._ro_splits = READOUT_SPLITS
         nbytes = int(_lib.lib().sw_eprop_readout_scratch_bytes(H, C, self._ro_splits))
@@ -309,6 +349,9 @@ class EpropClassifierTrainer:
                               self._slots_d.data_ptr())
         s.zbar_in = s.xbar_in = 0
         s.n_steps, s.slot_count = k, 2 * EPROP_BLOCK_STEPS
+        # the learning signal is computed by sw_eprop_prep, directly in the
+        # e-prop pass's layout (the forward pass never reads it)
+        s.lsig = 0
         return s
 
     def _slot(self, t: int) -> dict:
@@ -316,24 +359,43 @@ class EpropClassifierTrainer:
         return dict(zbar=self._slot_zbar[k], xbar=self._slot_xbar[k], psi=self._slot_psi[k],
                     lsig=self._slot_lsig[k], d=self._slot_d[k])
 
+    def _pass_scratch_ptr(self) -> int:
+        key = (self.plan_in.e_pad, self.plan_rec.e_pad)
+        if self._pass_scratch_key != key:
+            nb = int(_lib.lib().sw_eprop_pass_scratch_bytes(sum(key), self.plan_in.ldb))
+            self._pass_scratch = torch.zeros(nb // 8 + 1, dtype=torch.float64, device="cuda")
+            self._pass_scratch_key = key
+        return self._pass_scratch.data_ptr()
+
     def _eprop_block(self, t0: int, k: int, st: int) -> None:
-        """e-prop of steps t0 .. t0+k-1 in one pass (sw_eprop_fused_block)."""
+        """e-prop of steps t0 .. t0+k-1: sw_eprop_prep (replica-minor copies,
+        the learning signal and the readout gradients, classifier.py:221-223)
+        and one sw_eprop_pass over both projections."""
         p = self.params
         a32, r32, b32 = float(np.float32(p.alpha)), float(np.float32(p.rho)), float(np.float32(p.beta))
-        blk = _lib.EpropBlock()
-        blk.k = k
+        B, L = self.local_b, self.plan_in.ldb
+        pr = _lib.EpropPrep()
+        pr.k, pr.batch, pr.ldb = k, B, L
+        pr.num_inputs, pr.hidden, pr.num_classes = self.task.num_inputs, self.hidden, self.task.num_classes
+        tp = _lib.EpropTPass()
+        tp.k = k
         for j in range(k):
             sl = self._slot(t0 + j)
-            blk.psi[j], blk.lsig[j] = sl["psi"].data_ptr(), sl["lsig"].data_ptr()
-            blk.pre_trace[0][j], blk.pre_trace[1][j] = sl["xbar"].data_ptr(), sl["zbar"].data_ptr()
-            blk.d[j], blk.zbar[j] = sl["d"].data_ptr(), sl["zbar"].data_ptr()
-        blk.ro_scratch, blk.ro_splits = self._ro_scratch.data_ptr(), self._ro_splits
-        self._segs[0] = self.plan_in.seg(self.xbar)
-        self._segs[1] = self.plan_rec.seg(self.zbar)
-        _lib.call("sw_eprop_fused_block", ctypes.cast(self._segs, ctypes.c_void_p), 2,
-                  ctypes.byref(blk), self.local_b, self.hidden, b32, r32, a32,
-                  self.g_w_out.data_ptr(), self.g_b_out.data_ptr(), self.task.num_classes,
-                  _lib.workspace(), st)
+            pr.xbar[j], pr.zbar[j] = sl["xbar"].data_ptr(), sl["zbar"].data_ptr()
+            pr.psi[j], pr.d[j] = sl["psi"].data_ptr(), sl["d"].data_ptr()
+            tp.psi_t[j], tp.lsig_t[j] = self.psi_t[j].data_ptr(), self.lsig_t[j].data_ptr()
+        pr.w_out = self.w_out.data_ptr()
+        pr.xbar_t, pr.zbar_t = self.xbar_t.data_ptr(), self.zbar_t.data_ptr()
+        pr.psi_t, pr.lsig_t = self.psi_t.data_ptr(), self.lsig_t.data_ptr()
+        pr.g_w_out, pr.g_b_out = self.g_w_out.data_ptr(), self.g_b_out.data_ptr()
+        pr.ro_partial = self._ro_partial.data_ptr()
+        _lib.call("sw_eprop_prep", ctypes.byref(pr), st)
+        self._tsegs[0] = self.plan_in.tseg([self.xbar_t[j] for j in range(k)])
+        self._tsegs[1] = self.plan_rec.tseg([self.zbar_t[j] for j in range(k)])
+        tp.scratch = self._pass_scratch_ptr()
+        _lib.call("sw_eprop_pass", ctypes.cast(self._tsegs, ctypes.c_void_p), 2, ctypes.byref(tp),
+                  L, b32, r32, a32, st)
+
 
     def eprop_pass_graph(self, reps: int) -> "torch.cuda.CUDAGraph":
         """A CUDA graph of `reps` blocked e-prop passes over steps 0..K-1 on
@@ -391,7 +453,8 @@ class EpropClassifierTrainer:
         EPROP_BLOCK_STEPS timesteps."""
         T = self.task.example_steps
         groups = -(-T // EPROP_BLOCK_STEPS)
-        return groups * (2 if learn else 1)
+        # learning: forward + prep (+ readout reduction) + pass
+        return groups * (4 if learn else 1)
 
     def _run_trial(self, learn: bool) -> None:
         if not self.use_graph:

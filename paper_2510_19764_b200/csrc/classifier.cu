@@ -418,7 +418,7 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
     // lsig = f32(d @ W_out) (classifier.py:223), classes ascending; the
     // W_out column is loaded 8 classes at a time ahead of the chained sum
     double ls = 0.0;
-    for (int c0 = 0; c0 < C; c0 += 8) {
+    for (int c0 = 0; P.lsig && c0 < C; c0 += 8) {
       double wv[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) wv[u] = (c0 + u < C) ? __ldg(P.w_out + (int64_t)(c0 + u) * H + h) : 0.0;
@@ -426,7 +426,7 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
       for (int u = 0; u < 8; ++u)
         if (c0 + u < C) ls = __dadd_rn(ls, __dmul_rn(dv[c0 + u], wv[u]));
     }
-    P.lsig[bH + h] = __double2float_rn(ls);
+    if (P.lsig) P.lsig[bH + h] = __double2float_rn(ls);
     float vv = __fmul_rn(P.alpha, __fsub_rn(vo, __fmul_rn(zo, P.v_thr)));
     vv = __fadd_rn(__fadd_rn(vv, acc_rec[h]), acc_ext[h]);
     const float aa = __fadd_rn(__fmul_rn(P.rho, ao), zo);
@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_clf_step(sw_clf_s
     Q.xbar = P.xbar + cur * B * NI;
     Q.xbar_in = P.xbar + prev * B * NI;
     Q.psi = P.psi + cur * B * H;
-    Q.lsig = P.lsig + cur * B * H;
+    Q.lsig = P.lsig ? P.lsig + cur * B * H : nullptr;
     Q.d = P.d + cur * B * C;
     if (s) __syncthreads();   // this block's step s-1 writes are visible to its step s
     clf_step_body<kThreads, kCompact, kPT>(Q, scap, rcap, s == 0);
@@ -537,12 +537,24 @@ size_t clf_smem_bytes(int H, int NI, int C, int scap, int rcap, bool compact) {
   return o + (size_t)(compact ? 2 : 5) * C * 8 + 16;   // yv, dv (+ ypre, pipre, bpre)
 }
 
+int clf_fwd_launch(const sw_clf_step_t* p, void* stream);   // classifier_fwd.cu
+
 extern "C" int sw_clf_step(const sw_clf_step_t* p, void* stream) {
   const int H = p->hidden, NI = p->num_inputs, C = p->num_classes;
   if (p->batch <= 0) return SW_OK;
   if (p->n_steps > 0 && p->slot_count < 2) {
     sw::set_last_error("clf_step: n_steps > 0 needs slot_count >= 2 (step t reads slot t-1)");
     return SW_ERR_INVALID_ARG;
+  }
+  // register-resident forward (classifier_fwd.cu) for layers up to 1024
+  // inputs and 1024 hidden units; SW_CLF_KERNEL=staged selects k_clf_step
+  static const bool legacy = [] {
+    const char* e = getenv("SW_CLF_KERNEL");
+    return e && e[0] == 's';
+  }();
+  if (!legacy && clf_fwd_launch(p, stream) == SW_OK) {
+    SW_CHECK_LAUNCH("sw_clf_step");
+    return SW_OK;
   }
   if (NI + H > kThreads * kPerThread) {
     sw::set_last_error("clf_step: num_inputs + hidden must be <= 2048");

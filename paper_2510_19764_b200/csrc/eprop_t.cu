@@ -1,0 +1,671 @@
+// Replica-minor e-prop pass (sparsewire/_kernels.py:15-39 recursion over K
+// timesteps per pass; classifier.py:223 learning signal).
+//
+// Layout: the forward pass writes its per-step vectors replica-major ([B, n]);
+// sw_eprop_prep turns a group of K steps into replica-minor copies
+// ([n, B]: pre traces, psi) and computes the learning signal
+// lsig[h, b] = f32(sum_c d[b, c] * W_out[c, h]) (classes ascending, as the
+// forward pass did) straight into that layout.  The pass kernel then gives
+// each lane one synapse and R consecutive replicas: the K steps' inputs of
+// the lane are three runs of R floats (trace[pre, b0:b0+R], psi[post, ...],
+// lsig[post, ...]), loaded with 16-byte vector loads, and the eligibility
+// state of the lane is R contiguous floats ([tile][chunk][lane][R]).  Per
+// element-step: one 0.75-instruction share of the loads, the eight float32
+// operations of the recursion (op for op those of _kernels.py:33-38, so eps
+// and ebar are bit-identical to the reference) and one float64 add of the
+// gradient term into the lane's accumulator.
+//
+// Work items are (tile of 8 synapses, split of 64 replicas), statically
+// round-robin over the warps; a warp runs an item's 32-replica chunks, writes
+// its float64 partial per synapse, and k_grad_reduce adds the splits'
+// partials to the gradient in split order: deterministic, and a float64
+// regrouping of the reference's replica-ordered sum (within rounding of it).  The plan order of the
+// synapses (sw_eprop_plan with shift 0: by post, then pre) makes a warp's
+// psi/lsig runs mostly the same address (broadcast) and its trace runs
+// distinct 32-byte sectors.
+#include "common.cuh"
+#include "sm100_async.cuh"
+
+#include <cstdio>
+#include <cstdlib>
+
+namespace {
+
+constexpr int kTW = 8;          // warps per pass block
+
+// ---------------------------------------------------------------- prep ----
+// Block = (hidden tile of kHT units, replica tile of kBT, step k), 256 threads.
+//   A  replica-minor copies: zbar and psi of the tile, and a share of the
+//      xbar rows, through a [kBT][kHT + 1] shared tile (coalesced both ways);
+//   B  lsig_t[k][h][b] = f32(sum_c d[b][c] * W_out[c][h]), c ascending, one
+//      unfused multiply-add pair per class (the forward pass's arithmetic):
+//      lane = replica with its d row in registers, W_out[:, tile] in shared
+//      memory, each warp kHT/8 hidden units;
+//   C  readout-gradient partials over the tile's replicas, b ascending:
+//      part[k][bt][c][h] = sum_b d[b][c] * zbar[b][h] (thread = hidden unit x
+//      class group) and, in h tile 0, sum_b d[b][c]; k_readout_reduce adds
+//      the (k, bt) partials into g_w_out / g_b_out in a fixed order
+//      (classifier.py:221-222 summed over the group's steps and replicas; a
+//      regrouping of the reference's float64 sums).
+constexpr int kHT = 64;
+constexpr int kBT = 32;
+constexpr int kMaxC = 32;
+
+__host__ __device__ inline size_t prep_smem_bytes(int C) {
+  return (size_t)kBT * (kHT + 1) * 4 + (size_t)C * kHT * 8 + (size_t)kBT * C * 8;
+}
+
+// CT: the class count as a compile-time constant (0 = runtime, any count)
+template <int CT>
+__global__ void __launch_bounds__(256) k_prep(const sw_eprop_prep_t P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float (*tile)[kHT + 1] = reinterpret_cast<float (*)[kHT + 1]>(smem_raw);
+  double* ws = reinterpret_cast<double*>(smem_raw + (size_t)kBT * (kHT + 1) * 4);   // [C][kHT]
+  const int C = CT ? CT : P.num_classes;
+  const int H = P.hidden, NI = P.num_inputs, B = P.batch;
+  const int64_t L = P.ldb;
+  double* dt = ws + (size_t)C * kHT;                                                  // [C][kBT]
+  const int ht = blockIdx.x, bt = blockIdx.y, k = blockIdx.z;
+  const int h0 = ht * kHT, b0 = bt * kBT;
+  const int nh = min(kHT, H - h0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool ro = P.g_w_out != nullptr;
+  const bool want_lsig = P.lsig_t != nullptr && P.d[0] != nullptr;
+
+  // ---- A: transposes (psi, zbar of the tile; xbar rows split over the h tiles) ----
+  auto load_tile = [&](const float* in, int n, int r0, int nr) {
+    for (int x = tid; x < kBT * kHT; x += 256) {
+      const int b = x / kHT, r = x % kHT;
+      tile[b][r] = (r < nr && b0 + b < B) ? in[(int64_t)(b0 + b) * n + r0 + r] : 0.f;
+    }
+  };
+  auto store_tile = [&](int r0, int nr, float* out) {
+    for (int x = tid; x < kBT * kHT; x += 256) {
+      const int r = x / kBT, b = x % kBT;
+      if (r < nr && b0 + b < L) out[(int64_t)(r0 + r) * L + b0 + b] = tile[b][r];
+    }
+  };
+  const int nht = gridDim.x;
+  const int xper = (NI + nht - 1) / nht, x0 = min(NI, ht * xper), x1 = min(NI, x0 + xper);
+  for (int r0 = x0; r0 < x1; r0 += kHT) {
+    load_tile(P.xbar[k], NI, r0, min(kHT, x1 - r0));
+    __syncthreads();
+    store_tile(r0, min(kHT, x1 - r0), P.xbar_t + (int64_t)k * NI * L);
+    __syncthreads();
+  }
+  load_tile(P.psi[k], H, h0, nh);
+  __syncthreads();
+  store_tile(h0, nh, P.psi_t + (int64_t)k * H * L);
+  __syncthreads();
+  // zbar last: its tile stays in shared memory for the readout partials
+  load_tile(P.zbar[k], H, h0, nh);
+  if (want_lsig || ro) {
+    for (int x = tid; x < C * kHT; x += 256) {
+      const int c = x / kHT, r = x % kHT;
+      ws[x] = r < nh ? P.w_out[(int64_t)c * H + h0 + r] : 0.0;
+    }
+    for (int x = tid; x < kBT * C; x += 256) {   // coalesced read of d, class-major store
+      const int b = x / C, c = x - b * C;
+      dt[c * kBT + b] = b0 + b < B ? P.d[k][(int64_t)(b0 + b) * C + c] : 0.0;
+    }
+  }
+  __syncthreads();
+  store_tile(h0, nh, P.zbar_t + (int64_t)k * H * L);
+
+  // ---- B: learning signal, lane = replica ----
+  if (want_lsig) {
+    float* out = P.lsig_t + (int64_t)k * H * L + b0 + lane;
+    if constexpr (CT > 0) {
+      double dr[CT];
+#pragma unroll
+      for (int c = 0; c < CT; ++c) dr[c] = dt[c * kBT + lane];
+      for (int r = warp; r < nh; r += 8) {
+        double ls = 0.0;
+#pragma unroll
+        for (int c = 0; c < CT; ++c) ls = __dadd_rn(ls, __dmul_rn(dr[c], ws[c * kHT + r]));
+        if (b0 + lane < L) out[(int64_t)(h0 + r) * L] = b0 + lane < B ? __double2float_rn(ls) : 0.f;
+      }
+    } else {
+      for (int r = warp; r < nh; r += 8) {
+        double ls = 0.0;
+        for (int c = 0; c < C; ++c) ls = __dadd_rn(ls, __dmul_rn(dt[c * kBT + lane], ws[c * kHT + r]));
+        if (b0 + lane < L) out[(int64_t)(h0 + r) * L] = b0 + lane < B ? __double2float_rn(ls) : 0.f;
+      }
+    }
+  }
+
+  // ---- C: readout partials, thread = (hidden unit, class group of 4) ----
+  if (ro) {
+    double* part = P.ro_partial + ((int64_t)k * gridDim.y + bt) * (C * (int64_t)H + C);
+    const int r = tid % kHT, cg = tid / kHT;   // 4 class groups
+    if (r < nh) {
+      if constexpr (CT > 0 && CT % 4 == 0) {
+        constexpr int CP = CT / 4;
+        double acc[CP];
+#pragma unroll
+        for (int u = 0; u < CP; ++u) acc[u] = 0.0;
+        const double* dg = dt + cg * CP * kBT;
+        for (int b = 0; b < kBT; ++b) {
+          const double z = (double)tile[b][r];
+#pragma unroll
+          for (int u = 0; u < CP; ++u) acc[u] = __dadd_rn(acc[u], __dmul_rn(dg[u * kBT + b], z));
+        }
+#pragma unroll
+        for (int u = 0; u < CP; ++u) part[(int64_t)(cg * CP + u) * H + h0 + r] = acc[u];
+      } else {
+        const int cper = (C + 3) / 4, ca = cg * cper, cb = min(C, ca + cper);
+        for (int c = ca; c < cb; ++c) {
+          double acc = 0.0;
+          for (int b = 0; b < kBT; ++b) acc = __dadd_rn(acc, __dmul_rn(dt[c * kBT + b], (double)tile[b][r]));
+          part[(int64_t)c * H + h0 + r] = acc;
+        }
+      }
+    }
+    if (ht == 0 && tid < C) {
+      double sb = 0.0;
+      for (int b = 0; b < kBT; ++b) sb = __dadd_rn(sb, dt[tid * kBT + b]);
+      part[(int64_t)C * H + tid] = sb;
+    }
+  }
+}
+
+// g_w_out[c][h] += sum of the (k, bt) partials; g_b_out likewise.  Block = 32
+// outputs; warp w sums the partials of its eighth of the (k, bt) range in
+// order, then warp 0 adds the 8 warp sums in order (a fixed grouping).
+__global__ void __launch_bounds__(256) k_readout_reduce(const sw_eprop_prep_t P, int nparts) {
+  __shared__ double ws8[8][32];
+  const int C = P.num_classes, H = P.hidden;
+  const int64_t stride = C * (int64_t)H + C;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int x = blockIdx.x * 32 + lane;
+  const int q0 = (int)((int64_t)nparts * warp / 8), q1 = (int)((int64_t)nparts * (warp + 1) / 8);
+  double s = 0.0;
+  if (x < stride) {
+    int q = q0;
+    for (; q + 8 <= q1; q += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(P.ro_partial + (q + u) * stride + x);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+    }
+    for (; q < q1; ++q) s = __dadd_rn(s, __ldcg(P.ro_partial + q * stride + x));
+  }
+  ws8[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && x < stride) {
+    double t = ws8[0][lane];
+    for (int w = 1; w < 8; ++w) t = __dadd_rn(t, ws8[w][lane]);
+    if (x < C * H) P.g_w_out[x] = __dadd_rn(P.g_w_out[x], t);
+    else P.g_b_out[x - C * H] = __dadd_rn(P.g_b_out[x - C * H], t);
+  }
+}
+
+// ---------------------------------------------------------------- pass ----
+// A warp = 8 synapses x 32 replicas: lane = 4 * s + g holds synapse s of the
+// work item's 8-synapse tile and replicas [b0 + 8g, b0 + 8g + 8) of the
+// current 32-replica chunk.  Every input run and state run of a lane is 32
+// contiguous bytes (one 256-bit access), and the 4 lanes of a synapse read one
+// full 128-byte line: a warp-wide load touches 8 lines (trace: 8 distinct
+// pres) or 1-2 lines (psi/lsig: the plan's post order makes the 8 synapses
+// share posts), which keeps the L1 tag stage -- the limit of the lane-per-
+// synapse form -- off the critical path.
+struct TSeg {
+  const int32_t* pre;
+  const int32_t* post;
+  const float* trace[SW_EPROP_MAX_BLOCK];
+  float* eps;
+  float* ebar;
+  double* grad;
+  int tiles;             // 8-synapse tiles
+};
+
+struct TPass {
+  TSeg s[2];
+  const float* psi[SW_EPROP_MAX_BLOCK];
+  const float* lsig[SW_EPROP_MAX_BLOCK];
+  double* partial;       // [tiles][splits][8]
+  int ldb, splits, chunks_per_split;
+  float beta, rho, alpha;
+};
+
+// packed float32x2 helpers (add/sub/mul .rn.f32x2, sm_100)
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void up2(unsigned long long r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+__device__ __forceinline__ void ld256(float (&v)[8], const float* p) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void ld256_cs(float (&v)[8], const float* p) {
+  asm("ld.global.cs.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void st256_cs(float* p, const float (&v)[8]) {
+  asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+               "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+
+// grad[e] += the splits' partials, split order
+__global__ void k_grad_reduce(const TPass T) {
+  const int tiles0 = T.s[0].tiles, tiles = tiles0 + T.s[1].tiles;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < tiles * 8; x += gridDim.x * blockDim.x) {
+    const int tile = x >> 3, sl = x & 7;
+    const bool first = tile < tiles0;
+    double* grad = first ? T.s[0].grad : T.s[1].grad;
+    const int e = (first ? tile : tile - tiles0) * 8 + sl;
+    double gr = grad[e];
+    for (int q = 0; q < T.splits; ++q) gr = __dadd_rn(gr, __ldcg(T.partial + ((int64_t)tile * T.splits + q) * 8 + sl));
+    grad[e] = gr;
+  }
+}
+
+// PD: steps of inputs loaded ahead of the recursion; SP: the next chunk's
+// eligibility state is loaded during the current chunk
+template <int K, int PD, bool SP, int MB>
+__global__ void __launch_bounds__(kTW * 32, MB) k_eprop_t(const TPass T) {
+  const int lane = threadIdx.x & 31;
+  const int sl = lane >> 2, g = lane & 3;
+  const int tiles0 = T.s[0].tiles;
+  const int tiles = tiles0 + T.s[1].tiles;
+  const int items = tiles * T.splits;
+  const int nchunk = T.ldb / 32;
+  const int64_t L = T.ldb;
+  // static round-robin over the uniform work items (no ticket atomics)
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  for (int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < items; item += nwarps) {
+    // split-major item order: the warps working at any moment share replica ranges
+    const int split = item / tiles, tile = item - split * tiles;
+    const bool first = tile < tiles0;
+    const TSeg& S = first ? T.s[0] : T.s[1];
+    const int lt = first ? tile : tile - tiles0;
+    const int e = lt * 8 + sl;
+    const int pre = __ldg(S.pre + e), post = __ldg(S.post + e);
+    const int c0 = split * T.chunks_per_split, c1 = min(nchunk, c0 + T.chunks_per_split);
+    const int64_t tofs = (int64_t)pre * L + g * 8, pofs = (int64_t)post * L + g * 8;
+    double acc = 0.0;
+    float ep[8], eb[8];
+    const int64_t so0 = (((int64_t)lt * nchunk + c0) * 32 + lane) * 8;
+    ld256_cs(ep, S.eps + so0);
+    ld256_cs(eb, S.ebar + so0);
+    for (int c = c0; c < c1; ++c) {
+      const int b0 = c * 32;
+      const int64_t so = (((int64_t)lt * nchunk + c) * 32 + lane) * 8;
+      float zin[K][8], pin[K][8], lin[K][8];
+#pragma unroll
+      for (int k = 0; k < PD && k < K; ++k) {
+        ld256(zin[k], S.trace[k] + tofs + b0);
+        ld256(pin[k], T.psi[k] + pofs + b0);
+        ld256(lin[k], T.lsig[k] + pofs + b0);
+      }
+      float nep[8], neb[8];
+      if (SP && c + 1 < c1) {
+        ld256_cs(nep, S.eps + so + 32 * 8);
+        ld256_cs(neb, S.ebar + so + 32 * 8);
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (k + PD < K) {
+          ld256(zin[k + PD], S.trace[k + PD] + tofs + b0);
+          ld256(pin[k + PD], T.psi[k + PD] + pofs + b0);
+          ld256(lin[k + PD], T.lsig[k + PD] + pofs + b0);
+        }
+        // replicas in pairs: the subtract, the two adds and the gradient-term
+        // product as packed f32x2 ops (FADD2 / FMUL2: two separately rounded
+        // IEEE ops); the products that feed an add stay scalar (ptxas would
+        // contract a packed multiply feeding a packed add into FFMA2)
+#pragma unroll
+        for (int r = 0; r < 8; r += 2) {
+          const unsigned long long x =
+              sub2(pk2(zin[k][r], zin[k][r + 1]), pk2(__fmul_rn(T.beta, ep[r]), __fmul_rn(T.beta, ep[r + 1])));
+          float x0, x1;
+          up2(x, x0, x1);
+          const float e0 = __fmul_rn(pin[k][r], x0), e1 = __fmul_rn(pin[k][r + 1], x1);
+          const unsigned long long ee = pk2(e0, e1);
+          const unsigned long long ebn = add2(pk2(__fmul_rn(T.alpha, eb[r]), __fmul_rn(T.alpha, eb[r + 1])), ee);
+          const unsigned long long epn = add2(pk2(__fmul_rn(T.rho, ep[r]), __fmul_rn(T.rho, ep[r + 1])), ee);
+          float t0, t1;
+          up2(mul2(pk2(lin[k][r], lin[k][r + 1]), ebn), t0, t1);
+          acc = __dadd_rn(acc, (double)t0);
+          acc = __dadd_rn(acc, (double)t1);
+          up2(ebn, eb[r], eb[r + 1]);
+          up2(epn, ep[r], ep[r + 1]);
+        }
+      }
+      st256_cs(S.eps + so, ep);
+      st256_cs(S.ebar + so, eb);
+      if (c + 1 < c1) {
+        if (SP) {
+#pragma unroll
+          for (int r = 0; r < 8; ++r) { ep[r] = nep[r]; eb[r] = neb[r]; }
+        } else {
+          ld256_cs(ep, S.eps + so + 32 * 8);
+          ld256_cs(eb, S.ebar + so + 32 * 8);
+        }
+      }
+    }
+    // the synapse's 4 replica groups: (g0 + g1) + (g2 + g3)
+    acc = __dadd_rn(acc, __shfl_xor_sync(SW_FULL_MASK, acc, 1));
+    acc = __dadd_rn(acc, __shfl_xor_sync(SW_FULL_MASK, acc, 2));
+    // this split's partial; k_grad_reduce adds the splits in order
+    if (g == 0) T.partial[((int64_t)tile * T.splits + split) * 8 + sl] = acc;
+  }
+}
+
+// The same recursion with the eligibility state streamed through a per-warp
+// ring of NST shared-memory stages by bulk copies (cp.async.bulk, one lane
+// issues them, an mbarrier per stage): the state of the chunk NST-1 ahead is
+// in flight while the current chunk computes, so its DRAM latency is off the
+// critical path without holding it in registers.  Inputs as in k_eprop_t.
+template <int K, int NST, int MB>
+__global__ void __launch_bounds__(kTW * 32, MB) k_eprop_tma(const TPass T) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int sl = lane >> 2, g = lane & 3;
+  float* ring = reinterpret_cast<float*>(smem_raw) + (size_t)wib * NST * 512;   // [NST][eps 256 | ebar 256]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kTW * NST * 2048) + wib * NST;
+  const int tiles0 = T.s[0].tiles;
+  const int tiles = tiles0 + T.s[1].tiles;
+  const int items = tiles * T.splits;
+  const int nchunk = T.ldb / 32;
+  const int64_t L = T.ldb;
+  const int nwarps = gridDim.x * kTW;
+  const int gw = blockIdx.x * kTW + wib;
+  if (lane == 0)
+    for (int q = 0; q < NST; ++q) sw::mbar_init(&bars[q], 1);
+  sw::fence_mbar_init();
+  __syncwarp();
+  // chunk cursor over this warp's (item, chunk) sequence
+  struct Cur { int item, c, c1; };
+  auto first_chunk = [&](int item) {
+    Cur u{item, 0, 0};
+    if (item < items) {
+      const int split = item / tiles;
+      u.c = split * T.chunks_per_split;
+      u.c1 = min(nchunk, u.c + T.chunks_per_split);
+    }
+    return u;
+  };
+  auto advance = [&](Cur& u) {
+    if (++u.c >= u.c1) u = first_chunk(u.item + nwarps);
+  };
+  auto state_ptrs = [&](const Cur& u, const float*& pe, const float*& pb) {
+    const int tile = u.item % tiles;
+    const bool first = tile < tiles0;
+    const TSeg& S = first ? T.s[0] : T.s[1];
+    const int lt = first ? tile : tile - tiles0;
+    const int64_t so = ((int64_t)lt * nchunk + u.c) * 32 * 8;
+    pe = S.eps + so;
+    pb = S.ebar + so;
+  };
+  Cur prod = first_chunk(gw);
+  for (int q = 0; q < NST; ++q) {
+    if (prod.item < items && lane == 0) {
+      const float *pe, *pb;
+      state_ptrs(prod, pe, pb);
+      sw::mbar_arrive_expect_tx(&bars[q], 2048);
+      sw::bulk_g2s(ring + q * 512, pe, 1024, &bars[q]);
+      sw::bulk_g2s(ring + q * 512 + 256, pb, 1024, &bars[q]);
+    }
+    if (prod.item < items) advance(prod);
+  }
+  Cur cons = first_chunk(gw);
+  double acc = 0.0;
+  for (uint32_t n = 0; cons.item < items; ++n) {
+    const int split = cons.item / tiles, tile = cons.item - split * tiles;
+    const bool first = tile < tiles0;
+    const TSeg& S = first ? T.s[0] : T.s[1];
+    const int lt = first ? tile : tile - tiles0;
+    const int e = lt * 8 + sl;
+    const int pre = __ldg(S.pre + e), post = __ldg(S.post + e);
+    const int64_t tofs = (int64_t)pre * L + g * 8, pofs = (int64_t)post * L + g * 8;
+    const int b0 = cons.c * 32;
+    float zin[K][8], pin[K][8], lin[K][8];
+    ld256(zin[0], S.trace[0] + tofs + b0);
+    ld256(pin[0], T.psi[0] + pofs + b0);
+    ld256(lin[0], T.lsig[0] + pofs + b0);
+    const int q = n % NST;
+    sw::mbar_wait(&bars[q], (n / NST) & 1);
+    float ep[8], eb[8];
+    {
+      const float4* se = reinterpret_cast<const float4*>(ring + q * 512 + lane * 8);
+      const float4* sb = reinterpret_cast<const float4*>(ring + q * 512 + 256 + lane * 8);
+      const float4 a0 = se[0], a1 = se[1], c0 = sb[0], c1 = sb[1];
+      ep[0] = a0.x; ep[1] = a0.y; ep[2] = a0.z; ep[3] = a0.w; ep[4] = a1.x; ep[5] = a1.y; ep[6] = a1.z; ep[7] = a1.w;
+      eb[0] = c0.x; eb[1] = c0.y; eb[2] = c0.z; eb[3] = c0.w; eb[4] = c1.x; eb[5] = c1.y; eb[6] = c1.z; eb[7] = c1.w;
+    }
+    __syncwarp();
+    // refill this stage with the chunk NST ahead
+    if (prod.item < items) {
+      if (lane == 0) {
+        sw::fence_proxy_async_smem();
+        const float *pe, *pb;
+        state_ptrs(prod, pe, pb);
+        sw::mbar_arrive_expect_tx(&bars[q], 2048);
+        sw::bulk_g2s(ring + q * 512, pe, 1024, &bars[q]);
+        sw::bulk_g2s(ring + q * 512 + 256, pb, 1024, &bars[q]);
+      }
+      advance(prod);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (k + 1 < K) {
+        ld256(zin[k + 1], S.trace[k + 1] + tofs + b0);
+        ld256(pin[k + 1], T.psi[k + 1] + pofs + b0);
+        ld256(lin[k + 1], T.lsig[k + 1] + pofs + b0);
+      }
+#pragma unroll
+      for (int r = 0; r < 8; r += 2) {
+        const unsigned long long x =
+            sub2(pk2(zin[k][r], zin[k][r + 1]), pk2(__fmul_rn(T.beta, ep[r]), __fmul_rn(T.beta, ep[r + 1])));
+        float x0, x1;
+        up2(x, x0, x1);
+        const unsigned long long ee = pk2(__fmul_rn(pin[k][r], x0), __fmul_rn(pin[k][r + 1], x1));
+        const unsigned long long ebn = add2(pk2(__fmul_rn(T.alpha, eb[r]), __fmul_rn(T.alpha, eb[r + 1])), ee);
+        const unsigned long long epn = add2(pk2(__fmul_rn(T.rho, ep[r]), __fmul_rn(T.rho, ep[r + 1])), ee);
+        float t0, t1;
+        up2(mul2(pk2(lin[k][r], lin[k][r + 1]), ebn), t0, t1);
+        acc = __dadd_rn(acc, (double)t0);
+        acc = __dadd_rn(acc, (double)t1);
+        up2(ebn, eb[r], eb[r + 1]);
+        up2(epn, ep[r], ep[r + 1]);
+      }
+    }
+    const int64_t so = (((int64_t)lt * nchunk + cons.c) * 32 + lane) * 8;
+    st256_cs(S.eps + so, ep);
+    st256_cs(S.ebar + so, eb);
+    if (cons.c + 1 >= cons.c1) {
+      // item done: the synapse's 4 replica groups (g0 + g1) + (g2 + g3), then the split partial
+      acc = __dadd_rn(acc, __shfl_xor_sync(SW_FULL_MASK, acc, 1));
+      acc = __dadd_rn(acc, __shfl_xor_sync(SW_FULL_MASK, acc, 2));
+      if (g == 0) T.partial[((int64_t)tile * T.splits + split) * 8 + sl] = acc;
+      acc = 0.0;
+    }
+    advance(cons);
+  }
+}
+
+}  // namespace
+
+extern "C" int64_t sw_eprop_prep_scratch_bytes(int32_t k, int32_t batch, int32_t hidden, int32_t num_classes) {
+  if (k < 1 || batch < 1 || hidden < 1 || num_classes < 1) return 0;
+  return (int64_t)k * ((batch + kBT - 1) / kBT) * ((int64_t)num_classes * hidden + num_classes) * 8;
+}
+
+extern "C" int sw_eprop_prep(const sw_eprop_prep_t* p, void* stream) {
+  if (!p || p->k < 1 || p->k > SW_EPROP_MAX_BLOCK || p->batch < 1 || p->ldb < p->batch || p->ldb % 32) {
+    sw::set_last_error("sw_eprop_prep: 1 <= k <= SW_EPROP_MAX_BLOCK, batch >= 1, ldb >= batch, ldb % 32 == 0");
+    return SW_ERR_INVALID_ARG;
+  }
+  if (p->num_classes > kMaxC || (p->g_w_out && (!p->ro_partial || !p->g_b_out || !p->d[0]))) {
+    sw::set_last_error("sw_eprop_prep: num_classes <= 32; readout needs d, g_b_out and ro_partial");
+    return SW_ERR_INVALID_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t smem = prep_smem_bytes(p->num_classes);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute((const void*)k_prep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute((const void*)k_prep<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  if (smem > 200 * 1024) { sw::set_last_error("sw_eprop_prep: shared memory"); return SW_ERR_INVALID_ARG; }
+  // the replica tiles cover ldb (the padding columns are written as zeros)
+  dim3 grid((p->hidden + kHT - 1) / kHT, (p->ldb + kBT - 1) / kBT, p->k);
+  if (p->num_classes == 20) k_prep<20><<<grid, 256, smem, st>>>(*p);   // the SHD-shaped task
+  else k_prep<0><<<grid, 256, smem, st>>>(*p);
+  sw::count_launch();
+  if (p->g_w_out) {
+    const int n = p->num_classes * p->hidden + p->num_classes;
+    k_readout_reduce<<<(n + 31) / 32, 256, 0, st>>>(*p, p->k * (int)grid.y);
+    sw::count_launch();
+  }
+  SW_CHECK_LAUNCH("sw_eprop_prep");
+  return SW_OK;
+}
+
+extern "C" int64_t sw_eprop_pass_scratch_bytes(int32_t e_pad_total, int32_t ldb) {
+  if (e_pad_total <= 0 || ldb <= 0) return 0;
+  const int64_t tiles = e_pad_total / 8;
+  const int64_t splits = (ldb + 63) / 64;
+  return tiles * splits * 8 * 8;
+}
+
+extern "C" int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const sw_eprop_tpass_t* p,
+                             int32_t ldb, float beta, float rho, float alpha, void* stream) {
+  if (!p || n_segs < 1 || n_segs > 2 || p->k < 1 || p->k > SW_EPROP_MAX_BLOCK) {
+    sw::set_last_error("sw_eprop_pass: 1 or 2 segments, 1 <= k <= SW_EPROP_MAX_BLOCK");
+    return SW_ERR_INVALID_ARG;
+  }
+  if (ldb < 32 || ldb % 32) {
+    sw::set_last_error("sw_eprop_pass: ldb (padded batch) must be a positive multiple of 32");
+    return SW_ERR_INVALID_ARG;
+  }
+  if (!p->scratch) {
+    sw::set_last_error("sw_eprop_pass: scratch of sw_eprop_pass_scratch_bytes() bytes (zeroed once) required");
+    return SW_ERR_INVALID_ARG;
+  }
+  TPass T{};
+  int etot = 0;
+  for (int i = 0; i < n_segs; ++i) {
+    const sw_eprop_tseg_t& q = segs[i];
+    if (q.e_pad % 32) { sw::set_last_error("sw_eprop_pass: e_pad must be a multiple of 32"); return SW_ERR_INVALID_ARG; }
+    T.s[i].pre = q.pre;
+    T.s[i].post = q.post;
+    for (int k = 0; k < SW_EPROP_MAX_BLOCK; ++k) T.s[i].trace[k] = q.trace_t[k < p->k ? k : 0];
+    T.s[i].eps = q.eps;
+    T.s[i].ebar = q.ebar;
+    T.s[i].grad = q.grad;
+    T.s[i].tiles = q.e_pad / 8;
+    etot += q.e_pad;
+  }
+  for (int k = 0; k < SW_EPROP_MAX_BLOCK; ++k) {
+    T.psi[k] = p->psi_t[k < p->k ? k : 0];
+    T.lsig[k] = p->lsig_t[k < p->k ? k : 0];
+  }
+  const int tiles = etot / 8;
+  if (tiles == 0) return SW_OK;
+  const int nchunk = ldb / 32;
+  T.ldb = ldb;
+  T.splits = (ldb + 63) / 64;
+  T.chunks_per_split = (nchunk + T.splits - 1) / T.splits;
+  unsigned char* sc = (unsigned char*)p->scratch;
+  T.partial = (double*)sc;
+  T.beta = beta;
+  T.rho = rho;
+  T.alpha = alpha;
+  cudaStream_t st = (cudaStream_t)stream;
+  // variant (SW_EPT_CFG = "PD,SP,MB" for measurement): inputs PD steps
+  // ahead, next-chunk state prefetch SP, MB blocks per SM
+  static int cfg = -1;
+  if (cfg < 0) {
+    cfg = 0;
+    if (const char* ev = getenv("SW_EPT_CFG")) {
+      int pd = 0, sp = 0, mb = 0;
+      if (sscanf(ev, "%d,%d,%d", &pd, &sp, &mb) == 3) cfg = pd * 100 + sp * 10 + mb;
+    }
+  }
+  const int items = tiles * T.splits;
+  const void* fn = nullptr;
+  int kern = 0;
+#define SW_EPT_VARIANTS(X) X(1, false, 3) X(2, false, 2) X(2, true, 2) X(1, true, 3) X(2, false, 3) X(1, true, 2)
+  const int want = cfg ? cfg : 202;
+  if (want / 100 == 9) {
+    const int nst = (want / 10) % 10, mb = want % 10;
+    auto launch_tma = [&](auto kfn, int NST) {
+      const int smem = kTW * NST * 2048 + kTW * NST * 8;
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kTW * 32, smem);
+      if (per_sm < 1) per_sm = 1;
+      int blocks = 148 * per_sm;
+      if (blocks * kTW > items) blocks = (items + kTW - 1) / kTW;
+      kfn<<<blocks, kTW * 32, smem, st>>>(T);
+    };
+    if (p->k != 8) { sw::set_last_error("sw_eprop_pass: TMA variant is k = 8 only"); return SW_ERR_INVALID_ARG; }
+    if (nst == 3 && mb == 3) launch_tma(k_eprop_tma<8, 3, 3>, 3);
+    else if (nst == 4 && mb == 3) launch_tma(k_eprop_tma<8, 4, 3>, 4);
+    else if (nst == 2 && mb == 3) launch_tma(k_eprop_tma<8, 2, 3>, 2);
+    else launch_tma(k_eprop_tma<8, 4, 2>, 4);
+    sw::count_launch();
+    const int n = tiles * 8;
+    k_grad_reduce<<<(n + 255) / 256, 256, 0, st>>>(T);
+    sw::count_launch();
+    SW_CHECK_LAUNCH("sw_eprop_pass");
+    return SW_OK;
+  }
+  auto launch = [&](auto kfn, int mb) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kTW * 32, 0);
+    if (per_sm < 1) per_sm = 1;
+    int blocks = 148 * per_sm;
+    if (blocks * kTW > items) blocks = (items + kTW - 1) / kTW;
+    kfn<<<blocks, kTW * 32, 0, st>>>(T);
+    (void)mb;
+  };
+  (void)fn; (void)kern;
+  bool done = false;
+  switch (p->k) {
+#define SW_EPT_CASE(PD, SP, MB) \
+    if (!done && want == PD * 100 + (SP ? 1 : 0) * 10 + MB) { launch(k_eprop_t<KK, PD, SP, MB>, MB); done = true; }
+#define SW_K(KK_) case KK_: { constexpr int KK = KK_; SW_EPT_VARIANTS(SW_EPT_CASE) \
+    if (!done) { launch(k_eprop_t<KK, 1, false, 3>, 3); done = true; } break; }
+    SW_K(1) SW_K(2) SW_K(3) SW_K(4) SW_K(5) SW_K(6) SW_K(7) SW_K(8)
+#undef SW_K
+#undef SW_EPT_CASE
+#undef SW_EPT_VARIANTS
+    default: sw::set_last_error("sw_eprop_pass: k"); return SW_ERR_INVALID_ARG;
+  }
+  sw::count_launch();
+  {
+    const int n = tiles * 8;
+    k_grad_reduce<<<(n + 255) / 256, 256, 0, st>>>(T);
+  }
+  sw::count_launch();
+  SW_CHECK_LAUNCH("sw_eprop_pass");
+  return SW_OK;
+}

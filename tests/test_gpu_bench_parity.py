@@ -164,7 +164,17 @@ def test_trainer_at_bench_config_matches_oracle(dev_lib, cfg):
     for t in range(T):
         sl = {k: v.cpu().numpy() for k, v in tr._slot(t).items()}
         for k in sl:
-            assert np.array_equal(sl[k], snaps[t][k]), (t, k)
+            if k != "lsig":   # the grouped path computes it in sw_eprop_prep (below)
+                assert np.array_equal(sl[k], snaps[t][k]), (t, k)
+    # the last group's replica-minor e-prop inputs (sw_eprop_prep) == the
+    # single-step forward's own slots, learning signal included
+    K = EPROP_BLOCK_STEPS
+    for j in range(K):
+        s = snaps[T - K + j]
+        assert np.array_equal(tr.lsig_t[j, :, :B].cpu().numpy().T, s["lsig"]), j
+        assert np.array_equal(tr.psi_t[j, :, :B].cpu().numpy().T, s["psi"]), j
+        assert np.array_equal(tr.zbar_t[j, :, :B].cpu().numpy().T, s["zbar"]), j
+        assert np.array_equal(tr.xbar_t[j, :, :B].cpu().numpy().T, s["xbar"]), j
     assert np.array_equal(tr.v.cpu().numpy(), prev["v"]) and np.array_equal(tr.z.cpu().numpy(), prev["z"])
     assert float(tr.loss_b.sum()) == loss_d
 
@@ -183,7 +193,7 @@ def test_trainer_at_bench_config_matches_oracle(dev_lib, cfg):
                                eps, ebar, grad, beta, rho, al)
         E = int(rl.sum())
         off = plan.off.cpu().numpy()[:E]
-        flat = lambda a: a.permute(1, 0, 2).reshape(B, -1).cpu().numpy()[:, :E]  # noqa: E731
+        flat = lambda a: plan.replica_major(a).cpu().numpy()[:, :E]  # noqa: E731
         assert np.array_equal(flat(plan.eps), eps.reshape(B, -1)[:, off])
         assert np.array_equal(flat(plan.ebar), ebar.reshape(B, -1)[:, off])
         gd = syn.planes["grad"].cpu().numpy()

@@ -282,7 +282,8 @@ def test_grouped_forward_equals_single_steps(dev_lib):
     a, b = tr
     for name in ("v", "a", "z", "y", "pi_sum", "loss_b"):
         assert torch.equal(getattr(a, name), getattr(b, name)), name
-    for name in ("_slots_zbar", "_slots_xbar", "_slots_psi", "_slots_lsig", "_slots_d"):
+    # (the grouped launch leaves the learning signal to sw_eprop_prep)
+    for name in ("_slots_zbar", "_slots_xbar", "_slots_psi", "_slots_d"):
         assert torch.equal(getattr(a, name), getattr(b, name)), name
 
 
@@ -350,3 +351,103 @@ def test_pinned_host_inputs_equal_numpy_inputs(dev_lib):
         assert ra["loss"] == rb["loss"] and ra["removed"] == rb["removed"]
     assert torch.equal(a.s_in.planes["w"], b.s_in.planes["w"])
     assert a.connectivity_fingerprint() == b.connectivity_fingerprint()
+
+
+@pytest.mark.parametrize("P,H,cap,R,B,k", [(40, 64, 12, 6.0, 8, 8), (700, 256, 82, 25.6, 64, 8),
+                                         (33, 50, 9, 4.0, 20, 3), (256, 256, 40, 20.0, 136, 5)])
+def test_eprop_pass_replica_minor(dev_lib, P, H, cap, R, B, k):
+    """sw_eprop_prep + sw_eprop_pass (the trainer's e-prop path) vs the
+    reference-layout kernel (sw_eprop_accumulate_batch, _kernels.py:15-39
+    semantics) over k steps: eps and ebar bit-identical, the gradient within
+    1e-13 relative (float64 regrouping of the replica sum); the learning
+    signal lsig_t bit-identical to the forward pass's f32(d @ W_out) in class
+    order; ragged batches (B not a multiple of 32) padded with zeros."""
+    import ctypes
+    from paper_2510_19764_b200 import _lib
+    from paper_2510_19764_b200.classifier import _Plan
+    from paper_2510_19764_b200.connectivity import RaggedMatrix
+    from paper_2510_19764_b200.plasticity import eprop_accumulate_batch
+    rs = np.random.default_rng(P + B)
+    C = 7
+    tg = np.zeros((P, cap), np.int32)
+    rl = np.zeros(P, np.int32)
+    for i in range(P):
+        n = int(min(cap, rs.poisson(R)))
+        tg[i, :n] = rs.choice(H, size=n, replace=False)
+        rl[i] = n
+    m = RaggedMatrix(P, H, cap)
+    m.load_state(rl, tg)
+    plan = _Plan(m, B, shift=0, layout="chunk")
+    plan.ensure(int(rl.sum()))
+    plan.build()
+    L = plan.ldb
+    grad0 = rs.standard_normal((P, cap))
+    gplane = torch.from_numpy(grad0).cuda()
+    _lib.call("sw_gather_f64", gplane.data_ptr(), plan.off.data_ptr(), plan.e_pad, plan.grad.data_ptr(),
+              _lib.stream_ptr())
+    ref_eps = torch.zeros((B, P, cap), dtype=torch.float32, device="cuda")
+    ref_ebar = torch.zeros_like(ref_eps)
+    ref_grad = torch.from_numpy(grad0.copy()).cuda()
+    beta, rho, alpha = (float(np.float32(x)) for x in (0.0174, 0.9995, 0.95))
+    w_out = torch.from_numpy(rs.standard_normal((C, H))).cuda()
+    f = lambda *s: torch.from_numpy(rs.random(s).astype(np.float32)).cuda()  # noqa: E731
+    xt = torch.zeros((k, P, L), dtype=torch.float32, device="cuda")
+    zt, pt, lt = (torch.zeros((k, H, L), dtype=torch.float32, device="cuda") for _ in range(3))
+    for rep in range(2):   # two passes: the state carries over
+        steps = [dict(trace=f(B, P) * 2, psi=f(B, H) * 0.5, zbar=f(B, H),
+                      d=torch.from_numpy(rs.standard_normal((B, C))).cuda()) for _ in range(k)]
+        pr = _lib.EpropPrep()
+        pr.k, pr.batch, pr.ldb, pr.num_inputs, pr.hidden, pr.num_classes = k, B, L, P, H, C
+        for j, s in enumerate(steps):
+            pr.xbar[j], pr.zbar[j] = s["trace"].data_ptr(), s["zbar"].data_ptr()
+            pr.psi[j], pr.d[j] = s["psi"].data_ptr(), s["d"].data_ptr()
+        pr.w_out = w_out.data_ptr()
+        pr.xbar_t, pr.zbar_t, pr.psi_t, pr.lsig_t = (t.data_ptr() for t in (xt, zt, pt, lt))
+        gw = torch.zeros((C, H), dtype=torch.float64, device="cuda")
+        gb = torch.zeros(C, dtype=torch.float64, device="cuda")
+        part = torch.zeros(int(_lib.lib().sw_eprop_prep_scratch_bytes(k, B, H, C)) // 8 + 1,
+                           dtype=torch.float64, device="cuda")
+        pr.g_w_out, pr.g_b_out, pr.ro_partial = gw.data_ptr(), gb.data_ptr(), part.data_ptr()
+        _lib.call("sw_eprop_prep", ctypes.byref(pr), _lib.stream_ptr())
+        # readout gradients (classifier.py:221-222) summed over the group
+        gw_o = sum(s["d"].cpu().numpy().T @ s["zbar"].cpu().numpy().astype(np.float64) for s in steps)
+        gb_o = sum(s["d"].cpu().numpy().sum(axis=0) for s in steps)
+        assert np.allclose(gw.cpu().numpy(), gw_o, rtol=1e-12, atol=1e-12)
+        assert np.allclose(gb.cpu().numpy(), gb_o, rtol=1e-12, atol=1e-12)
+        for j, s in enumerate(steps):
+            dn, wn = s["d"].cpu().numpy(), w_out.cpu().numpy()
+            ls = np.zeros((B, H))
+            for c in range(C):
+                ls = ls + dn[:, c:c + 1] * wn[c][None, :]
+            s["lsig"] = torch.from_numpy(ls.astype(np.float32)).cuda()
+            assert torch.equal(lt[j, :, :B].T, s["lsig"]), j
+            assert torch.equal(xt[j, :, :B].T, s["trace"]) and torch.equal(zt[j, :, :B].T, s["zbar"])
+            assert torch.equal(pt[j, :, :B].T, s["psi"])
+            assert int((lt[j, :, B:] != 0).sum()) == 0 and int((xt[j, :, B:] != 0).sum()) == 0
+            eprop_accumulate_batch(m.target, m.row_length, s["trace"], s["psi"], s["lsig"], ref_eps, ref_ebar,
+                                   ref_grad, beta, rho, alpha)
+        segs = (_lib.EpropTSeg * 1)()
+        segs[0] = plan.tseg([xt[j] for j in range(k)])
+        tp = _lib.EpropTPass()
+        tp.k = k
+        for j in range(k):
+            tp.psi_t[j], tp.lsig_t[j] = pt[j].data_ptr(), lt[j].data_ptr()
+        nb = int(_lib.lib().sw_eprop_pass_scratch_bytes(plan.e_pad, L))
+        if rep == 0:
+            scratch = torch.empty(nb // 8 + 1, dtype=torch.float64, device="cuda")
+        tp.scratch = scratch.data_ptr()
+        _lib.call("sw_eprop_pass", ctypes.cast(segs, ctypes.c_void_p), 1, ctypes.byref(tp), L, beta, rho,
+                  alpha, _lib.stream_ptr())
+        torch.cuda.synchronize()
+        off = plan.off.cpu().numpy()
+        E = int(rl.sum())
+        re = ref_eps.reshape(B, -1).cpu().numpy()[:, off[:E]]
+        assert np.array_equal(plan.replica_major(plan.eps).cpu().numpy()[:, :E], re)
+        rb = ref_ebar.reshape(B, -1).cpu().numpy()[:, off[:E]]
+        assert np.array_equal(plan.replica_major(plan.ebar).cpu().numpy()[:, :E], rb)
+        g = gplane.clone()
+        _lib.call("sw_scatter_f64", g.data_ptr(), plan.off.data_ptr(), plan.e_pad, plan.grad.data_ptr(),
+                  _lib.stream_ptr())
+        gr = ref_grad.cpu().numpy()
+        mask = np.arange(cap)[None, :] < rl[:, None]
+        assert np.allclose(g.cpu().numpy()[mask], gr[mask], rtol=1e-13, atol=1e-13 * np.abs(gr).max())
