@@ -391,7 +391,16 @@ typedef struct sw_clf_step {
    * slot t % slot_count and reads the traces of slot (t-1) % slot_count
    * (zbar_in/xbar_in ignored).  n_steps = 0: one step, fields as above. */
   int32_t n_steps; int32_t slot_count;
+  /* packed (target, f32 weight) rows, [num_pre][tw_stride] int32 pairs with
+   * an even tw_stride (sw_clf_pack_rows): the register-resident forward
+   * kernel stages a spiking row with one bulk copy.  NULL: k_clf_step. */
+  const int32_t* in_tw; const int32_t* rec_tw;
+  int32_t in_tw_stride; int32_t rec_tw_stride;
 } sw_clf_step_t;
+/* tw[i][s] = (target[i][s], f32(w[i][s])) for s < row_length[i], (0, 0)
+ * after; tw_stride >= stride, even. */
+SW_API int sw_clf_pack_rows(const int32_t* row_length, const int32_t* target, const double* w,
+                            int32_t num_pre, int32_t stride, int32_t tw_stride, int32_t* tw, void* stream);
 /* Fused forward timestep(s) for all replicas (block per replica). */
 SW_API int sw_clf_step(const sw_clf_step_t* params, void* stream);
 /* out2[0] = sum of per-replica cross-entropy, out2[1] = #correct (argmax pi_sum). */

@@ -115,7 +115,8 @@ class ClfStep(C.Structure):
                 ("batch", I32), ("v", P), ("a", P), ("z", P), ("zbar", P), ("xbar", P),
                 ("y", P), ("pi_sum", P), ("loss", P), ("d", P), ("psi", P), ("lsig", P),
                 ("alpha", F32), ("rho", F32), ("beta", F32), ("v_thr", F32), ("alpha64", F64),
-                ("zbar_in", P), ("xbar_in", P), ("n_steps", I32), ("slot_count", I32)]
+                ("zbar_in", P), ("xbar_in", P), ("n_steps", I32), ("slot_count", I32),
+                ("in_tw", P), ("rec_tw", P), ("in_tw_stride", I32), ("rec_tw_stride", I32)]
 BP = C.POINTER(BitfieldDesc)
 
 # name -> argtypes (restype is int status for all but sw_last_error)
@@ -165,6 +166,7 @@ SIGNATURES: dict[str, list] = {
     "sw_poisson_step": [U64, I64, P, I32, P, P],
     "sw_poisson_rates": [I32, P, I32, F64, F64, F64, F64, P, P, P],
     "sw_clf_step": [C.c_void_p, P],
+    "sw_clf_pack_rows": [P, P, P, I32, I32, I32, P, P],
     "sw_clf_batch_stats": [P, P, P, I32, I32, P, P],
     "sw_f64_to_f32": [P, P, I64, P],
     "sw_scale_f64": [P, I64, F64, P],

@@ -290,6 +290,11 @@ class EpropClassifierTrainer:
         self.labels = torch.zeros(B, dtype=torch.int32, device="cuda")
         self.w32_in = torch.zeros(self.m_in.target.shape, **f32)
         self.w32_rec = torch.zeros(self.m_rec.target.shape, **f32)
+        # packed (target, f32 weight) rows for the forward kernel's bulk staging
+        self._tw_stride = {n: m.stride + (m.stride & 1) for n, m in (("in", self.m_in), ("rec", self.m_rec))}
+        self.tw_in = torch.zeros((self.m_in.num_pre, self._tw_stride["in"], 2), dtype=torch.int32, device="cuda")
+        self.tw_rec = torch.zeros((self.m_rec.num_pre, self._tw_stride["rec"], 2), dtype=torch.int32,
+                                  device="cuda")
         self.stats = torch.zeros(2, **f64)
         self.stats_host = torch.zeros(2, dtype=torch.float64, pin_memory=True)
         self.pin_p = torch.zeros((B, NI), dtype=torch.float64, pin_memory=True)
@@ -338,6 +343,8 @@ class EpropClassifierTrainer:
         s.alpha, s.rho = float(np.float32(p.alpha)), float(np.float32(p.rho))
         s.beta, s.v_thr = float(np.float32(p.beta)), float(np.float32(p.v_thr))
         s.alpha64 = p.alpha
+        s.in_tw, s.rec_tw = self.tw_in.data_ptr(), self.tw_rec.data_ptr()
+        s.in_tw_stride, s.rec_tw_stride = self._tw_stride["in"], self._tw_stride["rec"]
         return s
 
     def _group_params(self, t0: int, k: int) -> _lib.ClfStep:
@@ -515,6 +522,9 @@ class EpropClassifierTrainer:
                   self.w32_in.numel(), st)
         _lib.call("sw_f64_to_f32", self.s_rec.planes["w"].data_ptr(), self.w32_rec.data_ptr(),
                   self.w32_rec.numel(), st)
+        for m, syn, tw, key in ((self.m_in, self.s_in, self.tw_in, "in"), (self.m_rec, self.s_rec, self.tw_rec, "rec")):
+            _lib.call("sw_clf_pack_rows", m.row_length.data_ptr(), m.target.data_ptr(),
+                      syn.planes["w"].data_ptr(), m.num_pre, m.stride, self._tw_stride[key], tw.data_ptr(), st)
         for x in [self.v, self.a, self.z, self.y, self.pi_sum, self.loss_b] + self._slot_zbar + self._slot_xbar:
             x.zero_()
         if learn:

@@ -20,10 +20,17 @@
 // The arithmetic of every output is that of k_clf_step (classifier.cu), op for
 // op; only the work distribution differs.
 #include "common.cuh"
+#include "sm100_async.cuh"
 
 #include <cmath>
 
 namespace {
+
+// phase timestamps of block 7, step 3 (tools/fwd_phases.py); armed by sw_debug_fwd_prof
+__device__ long long g_fwd_prof[16];
+__device__ int g_fwd_prof_on;
+#define FWD_PROF(i) do { if (g_fwd_prof_on && blockIdx.x == 7 && s == 3 && (threadIdx.x & 31) == 0) \
+    g_fwd_prof[(i) + 8 * (threadIdx.x >= 32)] = clock64(); } while (0)
 
 constexpr int kT = 256;          // threads per replica block
 constexpr int kW = kT / 32;
@@ -36,16 +43,23 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* g) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// row groups of the event-driven current sums (see P2b)
+__host__ __device__ inline int fwd_groups(int H) {
+  const int g = 4096 / H;
+  return g < 1 ? 1 : (g > kW ? kW : g);
+}
+
 // bytes of the dynamic shared-memory layout
 __host__ __device__ inline size_t fwd_smem_bytes(int H, int NI, int C) {
   const size_t NT = (size_t)NI + H;
   size_t o = 0;
-  o += (size_t)2 * H * 4;            // acc_ext, acc_rec
+  o += (size_t)fwd_groups(H) * H * 4; // per-group partial sums
   o += NT * 4;                       // rlen
   o += NT * 4;                       // list (spiking rows: inputs, then hidden units NI + h)
   o += (NT + 1) * 4;                 // staging offset per list entry
-  o += (size_t)kStage * 8;           // staged targets + weights
   o = (o + 15) & ~(size_t)15;
+  o += (size_t)kStage * 8;           // staged (target, weight) pairs
+  o += 16;                           // staging mbarrier
   o += (size_t)4 * C * 8;            // y, pi_sum, d, b_out
   o += (size_t)NI * 8;               // input-spike thresholds
   return o;
@@ -57,14 +71,14 @@ __global__ void __launch_bounds__(kT, 4) k_clf_fwd(sw_clf_step_t P) {
   const int H = P.hidden, NI = P.num_inputs, C = P.num_classes;
   const int NT = NI + H;
   size_t o = 0;
-  float* acc_ext = (float*)(smem_raw + o); o += (size_t)H * 4;
-  float* acc_rec = (float*)(smem_raw + o); o += (size_t)H * 4;
+  const int G = fwd_groups(H);
+  float* part = (float*)(smem_raw + o);    o += (size_t)G * H * 4;
   int* rlen = (int*)(smem_raw + o);        o += (size_t)NT * 4;
   int* list = (int*)(smem_raw + o);        o += (size_t)NT * 4;
   int* soff = (int*)(smem_raw + o);        o += (size_t)(NT + 1) * 4;
-  int* st_t = (int*)(smem_raw + o);        o += (size_t)kStage * 4;
-  float* st_w = (float*)(smem_raw + o);    o += (size_t)kStage * 4;
   o = (o + 15) & ~(size_t)15;
+  int2* st = (int2*)(smem_raw + o);        o += (size_t)kStage * 8;
+  uint64_t* sbar = (uint64_t*)(smem_raw + o); o += 16;
   double* yv = (double*)(smem_raw + o);
   double* pis = yv + C;
   double* dv = pis + C;
@@ -90,8 +104,12 @@ __global__ void __launch_bounds__(kT, 4) k_clf_fwd(sw_clf_step_t P) {
     pis[c] = P.pi_sum[bC + c];
     bo[c] = P.b_out[c];
   }
-  if (tid == 0) s_loss = P.loss[b];
-  for (int h = tid; h < H; h += kT) { acc_ext[h] = 0.0f; acc_rec[h] = 0.0f; }
+  if (tid == 0) {
+    s_loss = P.loss[b];
+    sw::mbar_init(sbar, 1);
+    sw::fence_mbar_init();
+  }
+  for (int x = tid; x < G * H; x += kT) part[x] = 0.0f;
   const float* zin0;
   const float* xin0;
   if (grouped) {
@@ -128,6 +146,7 @@ __global__ void __launch_bounds__(kT, 4) k_clf_fwd(sw_clf_step_t P) {
   const float alpha = P.alpha, rho = P.rho, beta = P.beta, v_thr = P.v_thr;
   __syncthreads();   // thresholds staged
 
+  uint32_t sphase = 0;
   for (int s = 0; s < nsteps; ++s) {
     const int t = P.t + s;
     const int cur = grouped ? t % nslot : 0;
@@ -137,6 +156,7 @@ __global__ void __launch_bounds__(kT, 4) k_clf_fwd(sw_clf_step_t P) {
     float* lsig_o = P.lsig + cur * B * H;
     double* d_o = P.d + cur * B * C;
 
+    FWD_PROF(0);
     // ---- P1: spikes, traces, ascending spiking-row lists ----
     unsigned fin = 0, frec = 0;
     int len_in = 0, len_rec = 0;
@@ -148,7 +168,7 @@ __global__ void __launch_bounds__(kT, 4) k_clf_fwd(sw_clf_step_t P) {
         const bool f = (sw::draw(key, c0 + j) >> 11) < thr[x];
         xb[j] = __fadd_rn(__fmul_rn(xb[j], alpha), f ? 1.0f : 0.0f);
         xbar_o[bI + x] = xb[j];
-        if (f) { fin |= 1u << j; len_in += rlen[x]; }
+        if (f) { fin |= 1u << j; len_in += (rlen[x] + 1) & ~1; }
       }
     }
 #pragma unroll
@@ -157,7 +177,7 @@ __global__ void __launch_bounds__(kT, 4) k_clf_fwd(sw_clf_step_t P) {
       if (h < H) {
         zb[j] = __fadd_rn(__fmul_rn(zb[j], alpha), z[j]);
         zbar_o[bH + h] = zb[j];
-        if (z[j] != 0.0f) { frec |= 1u << j; len_rec += rlen[NI + h]; }
+        if (z[j] != 0.0f) { frec |= 1u << j; len_rec += (rlen[NI + h] + 1) & ~1; }
       }
     }
     // block scan of (input count, input entries, hidden count, hidden entries)
@@ -183,100 +203,128 @@ __global__ void __launch_bounds__(kT, 4) k_clf_fwd(sw_clf_step_t P) {
       int pos = pre.x + inc.x - mine.x, off = pre.y + inc.y - mine.y;
 #pragma unroll
       for (int j = 0; j < IPT; ++j)
-        if ((fin >> j) & 1u) { list[pos] = x0 + j; soff[pos] = off; off += rlen[x0 + j]; ++pos; }
+        if ((fin >> j) & 1u) { list[pos] = x0 + j; soff[pos] = off; off += (rlen[x0 + j] + 1) & ~1; ++pos; }
       pos = nx + pre.z + inc.z - mine.z;
       off = tot.y + pre.w + inc.w - mine.w;
 #pragma unroll
       for (int j = 0; j < HPT; ++j)
-        if ((frec >> j) & 1u) { list[pos] = NI + h0 + j; soff[pos] = off; off += rlen[NI + h0 + j]; ++pos; }
+        if ((frec >> j) & 1u) { list[pos] = NI + h0 + j; soff[pos] = off; off += (rlen[NI + h0 + j] + 1) & ~1; ++pos; }
     }
     if (tid == 0) soff[nx + nz] = ent;
     const bool staged = ent <= kStage;
+    // one mbarrier phase per step: tid 0 expects every staged byte, the
+    // row copies complete them
+    if (tid == 0 && staged) sw::mbar_arrive_expect_tx(sbar, (uint32_t)ent * 8u);
     __syncthreads();   // B1b: lists and offsets ready
+    FWD_PROF(1);
 
-    // ---- P2a: stage the spiking rows' entries (warp per row) ----
+    // ---- P2a: stage the spiking rows' packed (target, w) entries: one bulk
+    // copy per row (16-byte multiples: rows padded to even entries) ----
     if (staged) {
-      for (int r = warp; r < nx + nz; r += kW) {
+      for (int r = tid; r < nx + nz; r += kT) {
         const int x = list[r];
         const bool in = x < NI;
-        const int64_t go = in ? (int64_t)x * P.in_stride : (int64_t)(x - NI) * P.rec_stride;
-        const int32_t* tg = (in ? P.in_target : P.rec_target) + go;
-        const float* wg = (in ? P.in_w32 : P.rec_w32) + go;
-        const int so = soff[r], len = rlen[x];
-        for (int q = lane; q < len; q += 32) {
-          cp_async4(st_t + so + q, tg + q);
-          cp_async4(st_w + so + q, wg + q);
-        }
+        const int32_t* src = in ? P.in_tw + (int64_t)x * P.in_tw_stride * 2
+                                : P.rec_tw + (int64_t)(x - NI) * P.rec_tw_stride * 2;
+        const uint32_t bytes = (uint32_t)((rlen[x] + 1) & ~1) * 8u;
+        if (bytes) sw::bulk_g2s(st + soff[r], src, bytes, sbar);
       }
-      cp_async_wait_all();
     }
-    __syncthreads();   // B2: staged entries visible
 
-    // ---- P2b: ordered accumulation (warps 0, 1) | readout + softmax (warps 2..) ----
-    if (warp < 2) {
-      float* acc = warp == 0 ? acc_ext : acc_rec;
-      const int r0 = warp == 0 ? 0 : nx, r1 = warp == 0 ? nx : nx + nz;
-      for (int r = r0; r < r1; ++r) {
-        const int x = list[r];
-        const int len = rlen[x];
-        if (staged) {
-          const int so = soff[r];
-          for (int q = lane; q < len; q += 32) {
-            const int tj = st_t[so + q];
-            acc[tj] = __fadd_rn(acc[tj], st_w[so + q]);
-          }
-        } else {
-          const bool in = x < NI;
-          const int64_t go = in ? (int64_t)x * P.in_stride : (int64_t)(x - NI) * P.rec_stride;
-          const int32_t* tg = (in ? P.in_target : P.rec_target) + go;
-          const float* wg = (in ? P.in_w32 : P.rec_w32) + go;
-          for (int q = lane; q < len; q += 32) {
-            const int tj = __ldg(tg + q);
-            acc[tj] = __fadd_rn(acc[tj], __ldg(wg + q));
-          }
-        }
-        __syncwarp();
-      }
-    } else {
-      // readout y = alpha*y + z @ W_out^T + b (classifier.py:215), per class:
-      // lane-strided partial sums over the spiking hidden units, then the
-      // xor butterfly (k_clf_step's order)
-      const int rw = warp - 2, nrw = kW - 2;
+    // ---- P2b: readout + softmax (last warp) while the staged rows land ----
+    if (warp == kW - 1) {
+      // readout y = alpha*y + z @ W_out^T + b (classifier.py:215), lane = class:
+      // the spiking hidden units' W_out columns added in ascending unit
+      // order; then softmax / cross-entropy / d (plasticity.py:156-165,
+      // classifier.py:216-219) on the same lanes
       const int* zl = list + nx;
-      for (int c = rw; c < C; c += nrw) {
-        double sacc = 0.0;
-        for (int q = lane; q < nz; q += 32) sacc += __ldg(P.w_out + (int64_t)c * H + (zl[q] - NI));
-#pragma unroll
-        for (int o2 = 16; o2 > 0; o2 >>= 1) sacc += __shfl_xor_sync(SW_FULL_MASK, sacc, o2);
-        if (lane == 0) yv[c] = __dadd_rn(__dadd_rn(__dmul_rn(P.alpha64, yv[c]), sacc), bo[c]);
+      for (int c0 = 0; c0 < C; c0 += 32) {
+        const int c = c0 + lane;
+        if (c < C) {
+          double sacc = 0.0;
+          const double* wr = P.w_out + (int64_t)c * H - NI;
+          for (int q = 0; q < nz; ++q) sacc = __dadd_rn(sacc, __ldg(wr + zl[q]));
+          yv[c] = __dadd_rn(__dadd_rn(__dmul_rn(P.alpha64, yv[c]), sacc), bo[c]);
+        }
       }
-      named_bar(1, (kW - 2) * 32);
-      if (warp == 2) {
-        // softmax / cross-entropy / d (plasticity.py:156-165, classifier.py:216-219)
-        double mx = -INFINITY;
-        for (int c = lane; c < C; c += 32) mx = fmax(mx, yv[c]);
+      __syncwarp();
+      double mx = -INFINITY;
+      for (int c = lane; c < C; c += 32) mx = fmax(mx, yv[c]);
 #pragma unroll
-        for (int o2 = 16; o2 > 0; o2 >>= 1) mx = fmax(mx, __shfl_xor_sync(SW_FULL_MASK, mx, o2));
-        double se = 0.0;
-        double ex[2] = {0.0, 0.0};
-        for (int c = lane, u = 0; c < C; c += 32, ++u) {
-          const double e = exp(yv[c] - mx);
-          if (u < 2) ex[u] = e;
-          se += e;
-        }
+      for (int o2 = 16; o2 > 0; o2 >>= 1) mx = fmax(mx, __shfl_xor_sync(SW_FULL_MASK, mx, o2));
+      double se = 0.0;
+      double ex[2] = {0.0, 0.0};
+      for (int c = lane, u = 0; c < C; c += 32, ++u) {
+        const double e = exp(yv[c] - mx);
+        if (u < 2) ex[u] = e;
+        se += e;
+      }
 #pragma unroll
-        for (int o2 = 16; o2 > 0; o2 >>= 1) se += __shfl_xor_sync(SW_FULL_MASK, se, o2);
-        for (int c = lane, u = 0; c < C; c += 32, ++u) {
-          const double pi = (u < 2 ? ex[u] : exp(yv[c] - mx)) / se;
-          pis[c] = pis[c] + pi;
-          const double dd = pi - (c == label ? 1.0 : 0.0);
-          dv[c] = dd;
-          d_o[bC + c] = dd;
-          if (c == label) s_loss = s_loss + -log(pi);
-        }
+      for (int o2 = 16; o2 > 0; o2 >>= 1) se += __shfl_xor_sync(SW_FULL_MASK, se, o2);
+      for (int c = lane, u = 0; c < C; c += 32, ++u) {
+        const double pi = (u < 2 ? ex[u] : exp(yv[c] - mx)) / se;
+        pis[c] = pis[c] + pi;
+        const double dd = pi - (c == label ? 1.0 : 0.0);
+        dv[c] = dd;
+        d_o[bC + c] = dd;
+        if (c == label) s_loss = s_loss + -log(pi);
       }
     }
-    __syncthreads();   // B3: currents, d ready
+    if (staged) sw::mbar_wait(sbar, sphase & 1u);
+    sphase += staged ? 1u : 0u;   // one barrier phase per staged step
+    FWD_PROF(2);
+
+    // ---- P2c: event-driven currents (classifier.py:208-209 as ragged sums).
+    // The ascending spiking rows of a projection are split into G contiguous
+    // groups, group g = rows [n*g/G, n*(g+1)/G) summed by warp g into its
+    // own partial row (row after row in ascending order, lanes over a row's
+    // distinct targets); then per post the group sums are added in group
+    // order: sum = ((p_0 + p_1) + ...) + p_{G-1}, every p_g starting from
+    // +0.0 (a group without an entry for the post adds +0.0, which changes
+    // nothing).  Input rows first, then the recurrent rows. ----
+    float aext[HPT], arec[HPT];
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int rb = half == 0 ? 0 : nx, n = half == 0 ? nx : nz;
+      if (warp < G) {
+        float* pg = part + warp * H;
+        const int g0 = rb + (int)((int64_t)n * warp / G), g1 = rb + (int)((int64_t)n * (warp + 1) / G);
+        for (int r = g0; r < g1; ++r) {
+          const int x = list[r];
+          const int len = rlen[x];
+          const int2* e;
+          if (staged) {
+            e = st + soff[r];
+          } else {
+            const bool in = x < NI;
+            e = reinterpret_cast<const int2*>(in ? P.in_tw + (int64_t)x * P.in_tw_stride * 2
+                                                 : P.rec_tw + (int64_t)(x - NI) * P.rec_tw_stride * 2);
+          }
+          for (int q = lane; q < len; q += 32) {
+            const int2 tw = staged ? e[q] : __ldg(e + q);
+            pg[tw.x] = __fadd_rn(pg[tw.x], __int_as_float(tw.y));
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < HPT; ++j) {
+        const int h = h0 + j;
+        float a0 = 0.0f;
+        if (h < H) {
+          a0 = part[h];
+          part[h] = 0.0f;
+          for (int g = 1; g < G; ++g) {
+            a0 = __fadd_rn(a0, part[g * H + h]);
+            part[g * H + h] = 0.0f;
+          }
+        }
+        if (half == 0) aext[j] = a0; else arec[j] = a0;
+      }
+      __syncthreads();
+      FWD_PROF(3 + half);
+    }
 
     // ---- P3: psi (pre-step state), lsig, ALIF step ----
 #pragma unroll
@@ -303,14 +351,13 @@ __global__ void __launch_bounds__(kT, 4) k_clf_fwd(sw_clf_step_t P) {
         lsig_o[bH + h] = __double2float_rn(ls);
       }
       float vv = __fmul_rn(alpha, __fsub_rn(v[j], __fmul_rn(z[j], v_thr)));
-      vv = __fadd_rn(__fadd_rn(vv, acc_rec[h]), acc_ext[h]);
-      acc_rec[h] = 0.0f;
-      acc_ext[h] = 0.0f;
+      vv = __fadd_rn(__fadd_rn(vv, arec[j]), aext[j]);
       const float aa = __fadd_rn(__fmul_rn(rho, a[j]), z[j]);
       v[j] = vv;
       a[j] = aa;
       z[j] = (vv >= __fadd_rn(v_thr, __fmul_rn(beta, aa))) ? 1.0f : 0.0f;
     }
+    FWD_PROF(5);
     // the next step's P1 reads only this thread's registers and writes the
     // lists after its own barrier B1a, which every thread reaches only after
     // finishing this step's P3
@@ -346,14 +393,46 @@ int launch_fwd(const sw_clf_step_t* p, size_t smem, cudaStream_t st) {
   return SW_OK;
 }
 
+__global__ void k_pack_rows(const int32_t* row_length, const int32_t* target, const double* w, int P,
+                            int stride, int tws, int32_t* tw) {
+  const int64_t n = (int64_t)P * tws;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(x / tws), q = (int)(x - (int64_t)i * tws);
+    const bool ok = q < row_length[i];
+    tw[2 * x] = ok ? target[(int64_t)i * stride + q] : 0;
+    tw[2 * x + 1] = ok ? __float_as_int(__double2float_rn(w[(int64_t)i * stride + q])) : 0;
+  }
+}
+
 }  // namespace
+
+extern "C" __attribute__((visibility("default"))) int sw_debug_fwd_prof(int enable, long long* out16) {
+  if (out16 && cudaMemcpyFromSymbol(out16, g_fwd_prof, 16 * sizeof(long long)) != cudaSuccess) return SW_ERR_CUDA;
+  return cudaMemcpyToSymbol(g_fwd_prof_on, &enable, sizeof(int)) == cudaSuccess ? 0 : SW_ERR_CUDA;
+}
+
+extern "C" int sw_clf_pack_rows(const int32_t* row_length, const int32_t* target, const double* w,
+                                int32_t num_pre, int32_t stride, int32_t tw_stride, int32_t* tw, void* stream) {
+  if (tw_stride < stride || (tw_stride & 1)) {
+    sw::set_last_error("sw_clf_pack_rows: tw_stride must be even and >= stride");
+    return SW_ERR_INVALID_ARG;
+  }
+  const int64_t n = (int64_t)num_pre * tw_stride;
+  if (n == 0) return SW_OK;
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  k_pack_rows<<<(int)g, 256, 0, (cudaStream_t)stream>>>(row_length, target, w, num_pre, stride, tw_stride, tw);
+  sw::count_launch();
+  SW_CHECK_LAUNCH("sw_clf_pack_rows");
+  return SW_OK;
+}
 
 // sw_clf_step's fast path (classifier.cu); returns SW_ERR_INVALID_ARG when
 // the layer shapes are outside its register layout (the caller then runs
 // k_clf_step).
 int clf_fwd_launch(const sw_clf_step_t* p, void* stream) {
   const int H = p->hidden, NI = p->num_inputs, C = p->num_classes;
-  if (H < 1 || H > 4 * kT || NI < 1 || NI > 4 * kT || C < 1) return SW_ERR_INVALID_ARG;
+  if (H < 1 || H > 4 * kT || NI < 1 || NI > 4 * kT || C < 1 || !p->in_tw || !p->rec_tw) return SW_ERR_INVALID_ARG;
   const size_t smem = fwd_smem_bytes(H, NI, C);
   if (smem > 200 * 1024) return SW_ERR_INVALID_ARG;
   const int hpt = (H + kT - 1) / kT, ipt = (NI + kT - 1) / kT;

@@ -62,3 +62,34 @@ def check_topomap_post(fx, k, name, row_length, target, g):
     assert np.array_equal(row_length, rl), (k, name)
     assert valid_equal(rl, target, fx[f"u{k}_post_{name}_target"]), (k, name)
     assert valid_equal(rl, g, fx[f"u{k}_post_{name}_g"]), (k, name)
+
+
+def fwd_groups(H: int, warps: int = 8) -> int:
+    """Row groups of the forward kernel's event-driven current sums
+    (classifier_fwd.cu fwd_groups)."""
+    return max(1, min(warps, 4096 // H))
+
+
+def grouped_currents(rl, tg, w32, spiking, H):
+    """The forward kernel's per-post float32 current (classifier_fwd.cu P2c):
+    the ascending spiking rows split into G contiguous groups (group g =
+    rows[n*g//G : n*(g+1)//G]), each summed sequentially from +0.0, the group
+    sums added in group order.  spiking: [B, P] bool -> [B, H] float32."""
+    import numpy as np
+    F = np.float32
+    G = fwd_groups(H)
+    B = spiking.shape[0]
+    out = np.zeros((B, H), F)
+    for b in range(B):
+        rows = np.flatnonzero(spiking[b])
+        n = rows.size
+        acc = None
+        for g in range(G):
+            part = np.zeros(H, F)
+            for i in rows[n * g // G:n * (g + 1) // G]:
+                k = int(rl[i])
+                if k:
+                    part[tg[i, :k]] = part[tg[i, :k]] + w32[i, :k]
+            acc = part if acc is None else (acc + part).astype(F)
+        out[b] = acc
+    return out

@@ -23,6 +23,8 @@ The oracle is test infrastructure (oracle/); nothing here is timed.
 
 import numpy as np
 import pytest
+
+from oracle_helpers import grouped_currents
 import torch
 
 from oracle_helpers import valid_equal
@@ -135,8 +137,8 @@ def test_trainer_at_bench_config_matches_oracle(dev_lib, cfg):
         assert np.array_equal(sl["xbar"], xbar_o), t
         assert np.array_equal(sl["zbar"], zbar_o), t
         assert np.array_equal(sl["psi"], alif_surrogate(prev["v"], prev["a"])), t
-        ext = _seq_currents(rl_in, tg_in, w32_in, spikes[:, t, :], hidden)
-        rec = _seq_currents(rl_rec, tg_rec, w32_rec, prev["z"] != 0, hidden)
+        ext = grouped_currents(rl_in, tg_in, w32_in, spikes[:, t, :], hidden)
+        rec = grouped_currents(rl_rec, tg_rec, w32_rec, prev["z"] != 0, hidden)
         v_o, a_o, z_o = alif_step(prev["v"], prev["a"], prev["z"], rec, ext)
         assert np.array_equal(cur["v"], v_o), t
         assert np.array_equal(cur["a"], a_o), t

@@ -292,12 +292,15 @@ def test_grouped_forward_equals_single_steps(dev_lib):
     (300, 1024, 0.05, 0.02, 0.5, 0.3),   # staged path, compact 16-bit layout (large layer)
     (300, 200, 0.3, 0.25, 1.0, 1.0),     # every row spikes: > 2048 entries, warp-serial fallback
 ])
-def test_forward_currents_are_ascending_pre_sequential_sums(dev_lib, NI, H, din, drec, p_spk, z_spk):
-    """k_clf_step's event-driven propagation: per post, the float32 sum of the
-    spiking rows' weights in ascending pre order, starting from 0 (the order
-    the staging/sort phases and the fallback walk must preserve).  Spikes are
-    forced: p_in in {0, 1} and a chosen hidden z; v = a = 0, so after one
-    step v = f32(alpha * (0 - z*v_thr)) + rec + ext exactly."""
+def test_forward_currents_are_grouped_ordered_sums(dev_lib, NI, H, din, drec, p_spk, z_spk):
+    """The forward kernel's event-driven propagation (classifier_fwd.cu P2c):
+    per post, the ascending spiking rows in G contiguous groups, each summed
+    in row order from +0.0, the group sums added in group order
+    (oracle_helpers.grouped_currents) -- on the staged path and on the
+    unstaged one (every row spiking: more entries than the staging holds).
+    Spikes are forced: p_in in {0, 1} and a chosen hidden z; v = a = 0, so
+    after one step v = f32(alpha * (0 - z*v_thr)) + rec + ext exactly."""
+    from oracle_helpers import grouped_currents
     import ctypes
     from paper_2510_19764_b200 import _lib
     from paper_2510_19764_b200.classifier import EpropClassifierTrainer, SyntheticTask
@@ -321,18 +324,12 @@ def test_forward_currents_are_ascending_pre_sequential_sums(dev_lib, NI, H, din,
     p = tr.params
     alpha, vthr = f32(p.alpha), f32(p.v_thr)
 
-    def sums(m, w32, spiking):
-        rl, tg = m.row_length.cpu().numpy(), m.target.cpu().numpy()
-        acc = np.zeros(H, np.float32)
-        for x in np.flatnonzero(spiking):          # ascending pre
-            for s in range(rl[x]):
-                acc[tg[x, s]] = f32(acc[tg[x, s]] + w32[x, s])
-        return acc
-
     w_in, w_rec = tr.w32_in.cpu().numpy(), tr.w32_rec.cpu().numpy()
+    mi, mr = tr.m_in, tr.m_rec
+    ext_all = grouped_currents(mi.row_length.cpu().numpy(), mi.target.cpu().numpy(), w_in, pin == 1.0, H)
+    rec_all = grouped_currents(mr.row_length.cpu().numpy(), mr.target.cpu().numpy(), w_rec, z != 0, H)
     for b in range(B):
-        ext = sums(tr.m_in, w_in, pin[b] == 1.0)
-        rec = sums(tr.m_rec, w_rec, z[b] != 0)
+        ext, rec = ext_all[b], rec_all[b]
         for h in range(H):
             vv = f32(alpha * f32(f32(0) - f32(z[b, h] * vthr)))
             vv = f32(f32(vv + rec[h]) + ext[h])
