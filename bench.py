@@ -164,6 +164,12 @@ def dist_setup(n_gpus):
         # SW_BENCH_BACKEND=gloo exercises the multi-rank path on fewer GPUs
         # than ranks (validation only: ranks then share a device)
         backend = os.environ.get("SW_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            # communicator set-up lines (NVLS / NVLink transport) on stderr;
+            # stdout stays the one JSON line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         torch.cuda.set_device(lr % torch.cuda.device_count())
         dist.init_process_group(backend)
         return dist.get_rank(), ws, lr % torch.cuda.device_count()
@@ -172,6 +178,15 @@ def dist_setup(n_gpus):
 
 def flush_l2(buf):
     buf.add_(1)   # 256 MiB write > 126 MB L2
+
+
+def workload_config(args, w, ws):
+    """The config object of both arms' JSON lines (identical text)."""
+    return {"workload": f"{args.workload}: e-prop ALIF classifier {w['num_inputs']}->{w['hidden']}, "
+                        f"{int(w['density'] * 100)}% in/rec + DEEP R, 20 classes, batch {w['batch']}, "
+                        f"{w['steps']}-step SHD-shaped synthetic trials, {EPOCH_BATCHES} batches/epoch",
+            "global_batch": w["batch"], "seq_len": w["steps"], "parallelism": f"dp{ws}",
+            "l2": "flushed (256 MiB write) between timed steps"}
 
 
 # ------------------------------------------------------------------ reference arm
@@ -233,8 +248,7 @@ def run_reference(args, w):
             "value": round(v, 3), "unit": "s/epoch", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: e-prop ALIF classifier {w['num_inputs']}->{w['hidden']}, "
-                                   f"{int(w['density'] * 100)}% + DEEP R, batch {w['batch']}, SHD-shaped synthetic"},
+            "config": workload_config(args, w, int(os.environ.get("WORLD_SIZE", "1"))),
             "cpu_baseline": {"value": round(v, 3), "unit": "s/epoch", "cores": r["cores"], "kind": "port",
                              "sample": sample},
             "e2e": {"value": round(v, 3), "unit": "s/epoch", "h2d_bytes_per_step": 0,
@@ -243,11 +257,42 @@ def run_reference(args, w):
 
 
 # ------------------------------------------------------------------ microbenchmarks
-def run_mupdate(fracs=(0.001, 0.01, 0.1), P=1 << 20, N=65536, cap=1024, seed=1):
+FLIPS = (0.001, 0.003, 0.01, 0.03, 0.1)
+SPIKE_QS = (0.001, 0.01, 0.1)
+
+
+def count_moves(m, w, sign_slot, chunk=1 << 14):
+    """Plane moves the eliminate pass will make (bench accounting, outside
+    the timed region): per row with k sign-mismatched valid slots, the
+    marked slots below n - k are the holes the chained swap-with-last fills
+    (connectivity.py:130-136); tail removals move nothing."""
+    import torch
+    moves = 0
+    S = m.stride
+    cw = sign_slot.shape[1]
+    shifts = torch.arange(32, device=w.device, dtype=torch.int64)
+    for r0 in range(0, m.num_pre, chunk):
+        r1 = min(m.num_pre, r0 + chunk)
+        n = m.row_length[r0:r1].to(torch.int64)
+        bits = ((sign_slot[r0:r1].to(torch.int64) & 0xFFFFFFFF)[:, :, None] >> shifts) & 1
+        bits = bits.reshape(r1 - r0, cw * 32)[:, :S].bool()
+        x = w[r0:r1]
+        valid = torch.arange(S, device=w.device)[None, :] < n[:, None]
+        mis = ((x < 0) & bits) | ((x > 0) & ~bits)
+        mis &= valid
+        k = mis.sum(dim=1)
+        below = torch.arange(S, device=w.device)[None, :] < (n - k)[:, None]
+        moves += int((mis & below).sum().item())
+    return moves
+
+
+def run_mupdate(fracs=FLIPS, P=1 << 20, N=65536, cap=1024, seed=1):
     """Connectivity-update microbench (SURVEY 8(d) M-update): DEEP R
     eliminate + form on a 2^20-row ragged matrix, cap 1024, N = 65536,
     R ~ 512 (Bernoulli(512/65536) rows from counters (seed,"init","M")),
-    four float64 planes, sign flips of a Bernoulli(f) subset per update."""
+    four float64 planes, sign flips of a Bernoulli(f) subset per update.
+    Then the spike-propagation microbench (M-prop) on the same matrix:
+    atomic, post-slab bucketed and ordered (bit-exact, transpose) modes."""
     import ctypes
     import torch
     from paper_2510_19764_b200 import _lib
@@ -279,6 +324,7 @@ def run_mupdate(fracs=(0.001, 0.01, 0.1), P=1 << 20, N=65536, cap=1024, seed=1):
         d = descriptor(m, syn)
         _lib.call("sw_flip_signs", ctypes.byref(d), 0, fold_key(seed, "flip", u), f, _lib.stream_ptr())
         dr._sync_cache()
+        moves = count_moves(m, w, dr._sign_slot)
         flush.add_(1)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -288,63 +334,93 @@ def run_mupdate(fracs=(0.001, 0.01, 0.1), P=1 << 20, N=65536, cap=1024, seed=1):
         e1.synchronize()
         ms = e0.elapsed_time(e1)
         removed = dr.last_removed
-        alg = E * 12 + E // 8 + P * 24 + removed * (72 + 16 + 52)
+        # ind + w scan, 1 sign bit per slot, per-row words, plane
+        # moves (72 B each: 4 planes + target, read + write), conn-bit RMW per
+        # removal, appends + conn test-and-set per formed synapse (D = removed)
+        alg = E * 12 + E // 8 + P * 24 + moves * 72 + removed * 16 + removed * 52
         gbs = alg / (ms * 1e-3) / 1e9
-        out.append({"flip": f, "ms": round(ms, 3), "removed": int(removed), "alg_bytes": int(alg),
-                    "achieved_GBs": round(gbs, 1), "frac": round(gbs / peak, 4)})
+        out.append({"flip": f, "ms": round(ms, 3), "removed": int(removed), "moves": int(moves),
+                    "alg_bytes": int(alg), "achieved_GBs": round(gbs, 1), "frac": round(gbs / peak, 4)})
         assert m.edge_count() == E, "DEEP R must conserve the edge count"
-    # spike-propagation microbench on the same matrix (SURVEY 8(d) M-prop)
-    prop = []
-    p_dev = torch.empty(P, dtype=torch.float64, device="cuda")
+    res = {"rows": P, "num_post": N, "cap": cap, "edges": E, "update_sweep": out,
+           "note": "moves = holes below n - k filled by the chained swap-with-last (tail removals move nothing)"}
+    del dr, model
+    res.update(run_mprop(m, syn, seed, flush, peak))
+    del m, syn, w
+    torch.cuda.empty_cache()
+    return res
+
+
+def _spike_list(P, q, seed):
+    import torch
+    from paper_2510_19764_b200 import _lib
+    from paper_2510_19764_b200.rng import fold_key
+    p_dev = torch.full((P,), q, dtype=torch.float64, device="cuda")
     bits = torch.zeros((P + 31) // 32, dtype=torch.int32, device="cuda")
     lst = torch.zeros(P, dtype=torch.int32, device="cuda")
     cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
-    outv = torch.zeros(N, dtype=torch.float64, device="cuda")
-    for q in (0.001, 0.01, 0.1):
-        p_dev.fill_(q)
-        _lib.call("sw_poisson_step", fold_key(seed, "spk", 0), 0, p_dev.data_ptr(), P, bits.data_ptr(),
-                  _lib.stream_ptr())
-        _lib.call("sw_spike_bits_to_list", bits.data_ptr(), P, lst.data_ptr(), cnt.data_ptr(),
-                  _lib.stream_ptr())
-        S = int(cnt.item())
-        spk = lst[:S].long()
-        Rs = float(m.row_length[spk].double().mean().item()) if S else 0.0
-        ws_ptr, ws_bytes = _lib.prop_workspace()
+    _lib.call("sw_poisson_step", fold_key(seed, "spk", 0), 0, p_dev.data_ptr(), P, bits.data_ptr(),
+              _lib.stream_ptr())
+    _lib.call("sw_spike_bits_to_list", bits.data_ptr(), P, lst.data_ptr(), cnt.data_ptr(), _lib.stream_ptr())
+    return bits, lst, cnt, int(cnt.item())
 
-        def launch():
-            _lib.call("sw_propagate_atomic", m.row_length.data_ptr(), m.target.data_ptr(), w.data_ptr(),
-                      m.num_pre, m.num_post, m.stride, lst.data_ptr(), cnt.data_ptr(), S,
-                      outv.data_ptr(), ws_ptr, ws_bytes, _lib.stream_ptr())
-        for _ in range(3):
-            launch()
-        reps = 20
-        tot_ms = 0.0
-        for _ in range(reps):
-            flush.add_(1)                 # L2 flushed between timed launches
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            launch()
-            e1.record()
-            e1.synchronize()
-            tot_ms += e0.elapsed_time(e1)
-        us = tot_ms * 1e3 / reps
+
+def _time_launch(launch, flush, reps=20):
+    import torch
+    for _ in range(3):
+        launch()
+    tot = 0.0
+    for _ in range(reps):
+        flush.add_(1)                 # L2 flushed between timed launches
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        launch()
+        e1.record()
+        e1.synchronize()
+        tot += e0.elapsed_time(e1)
+    return tot * 1e3 / reps
+
+
+def run_mprop(m, syn, seed, flush, peak, qs=SPIKE_QS):
+    """Spike propagation (SURVEY 8(d) M-prop, connectivity.py:139-148) on the
+    M matrix: the atomic event-driven kernel, the post-slab bucketed rows and
+    the ordered (bit-exact, transpose-gathered) mode.  Bytes per step:
+    S*(4+4) + S*R*(4+8) + N*8 (spike index + row length, the spiking rows'
+    targets and weights, the output)."""
+    import ctypes
+    import torch
+    from paper_2510_19764_b200 import _lib
+    from paper_2510_19764_b200.connectivity import PropBuckets
+    from paper_2510_19764_b200.transpose import remap_transpose
+    P, N = m.num_pre, m.num_post
+    w = syn.planes["w"]
+    outv = torch.zeros(N, dtype=torch.float64, device="cuda")
+    for name in ("grad", "adam_m", "adam_v"):
+        syn.planes.pop(name, None)
+    torch.cuda.empty_cache()
+
+    def line(q, S, us, mode, note):
+        Rs = float(m.row_length[lst[:S].long()].double().mean().item()) if S else 0.0
         alg = S * 8 + S * Rs * 12 + N * 8
         gbs = alg / (us * 1e-6) / 1e9
-        prop.append({"q": q, "spiking_rows": S, "us": round(us, 2), "alg_bytes": int(alg),
-                     "achieved_GBs": round(gbs, 1), "frac": round(gbs / peak, 4),
-                     "note": "L2 flushed before each timed launch"})
-    # the same sweep through the post-slab bucketed rows (PropBuckets): the
-    # derived copy is built once for the fixed matrix (cost reported), then
-    # every step reads each spiking row's synapses once, without L2 atomics
-    from paper_2510_19764_b200.connectivity import PropBuckets
-    del syn.planes["grad"], syn.planes["adam_m"], syn.planes["adam_v"]
-    torch.cuda.empty_cache()
-    torch.cuda.synchronize()
-    pb = PropBuckets(m, w)            # allocates the copy and builds it once
+        return {"q": q, "spiking_rows": S, "mode": mode, "us": round(us, 2), "alg_bytes": int(alg),
+                "achieved_GBs": round(gbs, 1), "frac": round(gbs / peak, 4), "note": note}
+    atomic, bucketed, ordered = [], [], []
+    ws_ptr, ws_bytes = _lib.prop_workspace()
+    for q in qs:
+        bits, lst, cnt, S = _spike_list(P, q, seed)
+        us = _time_launch(lambda: _lib.call("sw_propagate_atomic", m.row_length.data_ptr(), m.target.data_ptr(),
+                                            w.data_ptr(), P, N, m.stride, lst.data_ptr(), cnt.data_ptr(), S,
+                                            outv.data_ptr(), ws_ptr, ws_bytes, _lib.stream_ptr()), flush)
+        atomic.append(line(q, S, us, "atomic", "L2 flushed before each timed launch"))
+    # post-slab bucketed rows: the derived copy is built once for the fixed
+    # matrix (cost reported), then every step reads each spiking row's
+    # synapses once, without L2 atomics
+    pb = PropBuckets(m, w)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    pb.build()                        # timed: a rebuild after a structural change
+    pb.build()
     e1.record()
     e1.synchronize()
     build_ms = e0.elapsed_time(e1)
@@ -353,44 +429,80 @@ def run_mupdate(fracs=(0.001, 0.01, 0.1), P=1 << 20, N=65536, cap=1024, seed=1):
     e1.record()
     e1.synchronize()
     refresh_ms = e0.elapsed_time(e1)
-    propb = []
-    for q in (0.001, 0.01, 0.1):
-        p_dev.fill_(q)
-        _lib.call("sw_poisson_step", fold_key(seed, "spk", 0), 0, p_dev.data_ptr(), P, bits.data_ptr(),
-                  _lib.stream_ptr())
-        _lib.call("sw_spike_bits_to_list", bits.data_ptr(), P, lst.data_ptr(), cnt.data_ptr(),
-                  _lib.stream_ptr())
-        S = int(cnt.item())
-        spk = lst[:S].long()
-        Rs = float(m.row_length[spk].double().mean().item()) if S else 0.0
+    for q in qs:
+        bits, lst, cnt, S = _spike_list(P, q, seed)
         kern = pb.propagate(lst, cnt, S, outv)
-        for _ in range(2):
-            pb.propagate(lst, cnt, S, outv)
-        reps = 20
-        tot_ms = 0.0
-        for _ in range(reps):
-            flush.add_(1)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            pb.propagate(lst, cnt, S, outv)
-            e1.record()
-            e1.synchronize()
-            tot_ms += e0.elapsed_time(e1)
-        us = tot_ms * 1e3 / reps
-        alg = S * 8 + S * Rs * 12 + N * 8
-        gbs = alg / (us * 1e-6) / 1e9
-        propb.append({"q": q, "spiking_rows": S, "kernel": kern, "us": round(us, 2), "alg_bytes": int(alg),
-                      "achieved_GBs": round(gbs, 1), "frac": round(gbs / peak, 4),
-                      "note": "L2 flushed before each timed launch; reads 10 B/synapse of the bucketed copy"})
-    del pb, m, syn, dr, model, w
+        us = _time_launch(lambda: pb.propagate(lst, cnt, S, outv), flush)
+        r = line(q, S, us, "bucketed", "L2 flushed before each timed launch; reads 10 B/synapse of the bucketed copy")
+        r["kernel"] = kern
+        bucketed.append(r)
+    del pb
     torch.cuda.empty_cache()
-    return {"rows": P, "num_post": N, "cap": cap, "edges": E, "update_sweep": out,
-            "propagate_atomic": prop, "propagate_bucketed": propb,
+    # ordered mode: per post, the spiking rows' weights in ascending pre
+    # order through the transpose (bit-identical to np.add.at on an ascending
+    # spike list); it walks every column entry, so it is O(E) per step
+    tm = remap_transpose(m)
+    for q in qs:
+        bits, lst, cnt, S = _spike_list(P, q, seed)
+        pr = (_lib.PropProj * 1)()
+        pr[0].col_ptr, pr[0].src_pre, pr[0].src_slot = tm.col_ptr.data_ptr(), tm.src_pre.data_ptr(), tm.src_slot.data_ptr()
+        pr[0].weights, pr[0].spike_bits, pr[0].stride = w.data_ptr(), bits.data_ptr(), m.stride
+        us = _time_launch(lambda: _lib.call("sw_propagate_ordered", ctypes.cast(pr, ctypes.c_void_p), 1, N,
+                                            outv.data_ptr(), 0, _lib.stream_ptr()), flush, reps=5)
+        r = line(q, S, us, "ordered", "bit-exact mode: walks all E transpose entries + spike bits per step "
+                 "(E*8 B + gathers), so frac on the event-driven formula is low by construction")
+        r["transpose_bytes_per_step"] = int(m.edge_count() * 8 + (P + 31) // 32 * 4)
+        ordered.append(r)
+    del tm
+    torch.cuda.empty_cache()
+    return {"propagate_atomic": atomic, "propagate_bucketed": bucketed, "propagate_ordered": ordered,
             "bucket_build_ms": round(build_ms, 3), "bucket_refresh_ms": round(refresh_ms, 3)}
 
 
-def cpu_micro_sample(P=16384, N=65536, cap=1024, seed=1, fracs=(0.001, 0.01, 0.1),
-                     qs=(0.001, 0.01, 0.1)):
+def run_alif_bench(batch=512, hiddens=(256, 1024), reps=50):
+    """ALIF step (neurons.py:60-67) + surrogate (:69-73) on [B, H] float32
+    state (SURVEY 8(d) ALIF-step: B*H*(3*4*2 + 2*4 + 4) bytes), standalone
+    kernels (the trainer fuses them into the forward pass)."""
+    import torch
+    from paper_2510_19764_b200 import _lib
+    peak, _ = measured_peak()
+    res = []
+    for H in hiddens:
+        n = batch * H
+        v, a, z, rec, ext, psi = (torch.rand(n, dtype=torch.float32, device="cuda") for _ in range(6))
+        z = (z < 0.05).float()
+
+        def launch():
+            _lib.call("sw_alif_surrogate", v.data_ptr(), a.data_ptr(), psi.data_ptr(), n, 0.0174, 0.6,
+                      _lib.stream_ptr())
+            _lib.call("sw_alif_step", v.data_ptr(), a.data_ptr(), z.data_ptr(), rec.data_ptr(), ext.data_ptr(),
+                      n, 0.95, 0.9995, 0.0174, 0.6, _lib.stream_ptr())
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(reps):
+                    launch()
+        torch.cuda.current_stream().wait_stream(side)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        e1.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / reps
+        alg = n * (3 * 4 * 2 + 2 * 4 + 4)
+        gbs = alg / (us * 1e-6) / 1e9
+        res.append({"batch": batch, "hidden": H, "us": round(us, 2), "alg_bytes": alg,
+                    "achieved_GBs": round(gbs, 1), "frac": round(gbs / peak, 4),
+                    "note": "surrogate + step launches back to back in a CUDA graph (L2-resident: latency-bound, "
+                            "SURVEY 8(d) 'report')"})
+    return res
+
+
+def cpu_micro_sample(P=16384, N=65536, cap=1024, seed=1, fracs=FLIPS, qs=SPIKE_QS):
     """CPU baseline of the M-update and M-prop microbenchmarks (BASELINE.md
     section 3): the oracle port (numpy restatement of deep_r.py:81-160 and
     connectivity.py:139-148, one thread) on a 16 384-row slice with the GPU
@@ -443,6 +555,110 @@ def cpu_micro_sample(P=16384, N=65536, cap=1024, seed=1, fracs=(0.001, 0.01, 0.1
             "sample": f"{P}-row slice (R~512, cap {cap}, N={N}, 4 float64 planes), oracle port "
                       f"(numpy, 1 thread), timed on the host and extrapolated x{scale:g} to 2^20 rows",
             "update": upd, "propagate": prop}
+
+
+def run_micro_sharded(pg, P=1 << 20, N=65536, cap=1024, seed=1, fracs=(0.01, 0.1)):
+    """SURVEY 8(e) microbench sharding under torchrun: M-update with the rows
+    sharded over the ranks (DeepR process_group: D and unplaced all-reduced,
+    the activation histogram reduce-scattered by row owner) and M-prop with
+    the posts sharded (each rank propagates into its column slice, no
+    collective).  Times are the max over ranks; strong scaling (the matrix
+    is the 2^20-row instance at every N)."""
+    import ctypes
+    import torch
+    import torch.distributed as dist
+    from paper_2510_19764_b200 import _lib
+    from paper_2510_19764_b200.connectivity import column_slice, descriptor, init_pairwise_bernoulli_density
+    from paper_2510_19764_b200.deep_r import DeepR
+    from paper_2510_19764_b200.rng import CounterRng, fold_key
+    from paper_2510_19764_b200.sharding import shard_posts, shard_rows
+    from paper_2510_19764_b200.updates import Model
+    rank, world = dist.get_rank(pg), dist.get_world_size(pg)
+    lo, hi = shard_rows(P, rank, world)
+    rng = CounterRng(seed, "init", "M")
+    rng.counter = lo * N                  # this rank's rows of the global draw sequence
+    planes = ("w", "grad", "adam_m", "adam_v")
+    m, syn = init_pairwise_bernoulli_density(hi - lo, N, 512.0 / N, 1.0, rng, var_names=planes, capacity=cap)
+    w = syn.planes["w"]
+    w.normal_(0.0, 0.1)
+    w.mul_(m.slot_mask())
+    dr = DeepR(m, syn, "M", l1_strength=0.0, process_group=pg, row0=lo, num_pre_global=P)
+    srng = CounterRng(seed, "deep_r", "M")
+    srng.counter = lo * dr.sign_bits.words.shape[1]
+    dr.init_bitfields(srng)
+    model = Model(seed)
+    model.add_matrix("M", m, syn)
+    dr.register(model, "deep_r", "M")
+    model.run_update_group("deep_r")
+    torch.cuda.synchronize()
+
+    def max_ms(ms):
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=pg)
+        return float(t.item())
+    upd = []
+    for u, f in enumerate(fracs):
+        _lib.call("sw_flip_signs", ctypes.byref(descriptor(m, syn)), 0, fold_key(seed, "flip", u), f,
+                  _lib.stream_ptr())
+        dr._sync_cache()
+        torch.cuda.synchronize()
+        dist.barrier(group=pg)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        model.run_update_group("deep_r")
+        e1.record()
+        e1.synchronize()
+        upd.append({"flip": f, "ms_max_over_ranks": round(max_ms(e0.elapsed_time(e1)), 3),
+                    "removed_global": int(dr.last_removed)})
+    del dr, model, m, syn, w
+    torch.cuda.empty_cache()
+    # M-prop: every rank holds all rows' synapses onto its post range
+    full, fsyn = init_pairwise_bernoulli_density(P, N, 512.0 / N, 1.0, CounterRng(seed, "init", "M"),
+                                                 var_names=("w",), capacity=cap)
+    fsyn.planes["w"].normal_(0.0, 0.1)
+    plo, phi = shard_posts(N, rank, world)
+    ms_, ssyn = column_slice(full, fsyn, plo, phi)
+    del full, fsyn
+    torch.cuda.empty_cache()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    outv = torch.zeros(phi - plo, dtype=torch.float64, device="cuda")
+    ws_ptr, ws_bytes = _lib.prop_workspace()
+    prop = []
+    for q in SPIKE_QS:
+        bits, lst, cnt, S = _spike_list(P, q, seed)
+        us = _time_launch(lambda: _lib.call("sw_propagate_atomic", ms_.row_length.data_ptr(), ms_.target.data_ptr(),
+                                            ssyn.planes["w"].data_ptr(), P, phi - plo, ms_.stride, lst.data_ptr(),
+                                            cnt.data_ptr(), S, outv.data_ptr(), ws_ptr, ws_bytes,
+                                            _lib.stream_ptr()), flush)
+        prop.append({"q": q, "spiking_rows": S, "us_max_over_ranks": round(max_ms(us * 1e-3) * 1e3, 2)})
+    return {"rows": P, "parallelism": f"M-update rows / M-prop posts sharded x{world}",
+            "update": upd, "propagate_atomic": prop}
+
+
+def topomap_cpu_baseline(seed=1, timed=((1, 200.0), (2, 50.0), (4, 10.0))):
+    """CPU baseline of the topomap sweep: the oracle port of
+    TopomapModel.run (oracle/topomap_port.py: numpy, np.add.at propagation,
+    the reference's Python rewiring row loop; 1 thread) timed at s = 1, 2, 4
+    on this host; s = 8 and 16 extrapolated from s = 4 with wall time per
+    model ms proportional to N (the port's step cost is O(N) per step),
+    stated as such."""
+    from oracle.topomap_port import time_topomap
+    res = {}
+    for s_, ms in timed:
+        r = time_topomap(s_, ms, seed)
+        r["kind"] = "timed"
+        res[f"s{s_}"] = r
+    last_s, last_ms = timed[-1]
+    base = res[f"s{last_s}"]
+    for s_ in (8, 16):
+        if f"s{s_}" in res:
+            continue
+        f = (s_ / last_s) ** 2
+        res[f"s{s_}"] = {"n": 256 * s_ * s_, "x_realtime": round(base["x_realtime"] / f, 6),
+                         "kind": f"extrapolated from s={last_s} x (N ratio {f:g})"}
+    return {"kind": "port", "cores": 1, "sample": "oracle/topomap_port.py (numpy restatement of "
+            "TopomapModel.run, topomap.py:398-474; no recorder), build excluded; "
+            + ", ".join(f"s={a}: {b:g} ms model" for a, b in timed) + "; s=8,16 extrapolated", "per_scale": res}
 
 
 def run_topomap_sweep(scales=(1, 2, 4, 8, 16), model_ms=100.0, seed=1, process_group=None):
@@ -564,27 +780,29 @@ def run_device(args, w):
     graph_kernels = steps_dev * tr.kernels_per_trial() // w["steps"]
     launches_per_step = (eager_dev + graph_kernels) / args.steps
 
-    # ---- roofline of the dominant kernel (one temporally blocked e-prop
-    # pass over K timesteps on the trainer's live state), timed live
-    import ctypes
+    # ---- roofline of the dominant kernel: one sw_eprop_pass (the
+    # replica-minor e-prop recursion over K timesteps, k_eprop_t) on the
+    # trainer's live state, replayed from a CUDA graph; its companion
+    # sw_eprop_prep (transposes, learning signal, readout partials) timed
+    # the same way
     from paper_2510_19764_b200.classifier import EPROP_BLOCK_STEPS as K
-    p = tr.params
-    a32, r32, b32 = (float(np.float32(x)) for x in (p.alpha, p.rho, p.beta))
     st = torch.cuda.current_stream()
-
-    # graph replay: the kernel back to back without host launch overhead
     reps = 50
-    g = tr.eprop_pass_graph(reps)
-    g.replay()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    g.replay()
-    e1.record(st)
-    e1.synchronize()
-    k_ms = e0.elapsed_time(e1) / reps
-    del g
+
+    def graph_us(part):
+        g = tr.eprop_kernel_graph(reps, part)
+        g.replay()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        g.replay()
+        e1.record(st)
+        e1.synchronize()
+        del g
+        return e0.elapsed_time(e1) * 1e3 / reps
+    k_us = graph_us("pass")
+    prep_us = graph_us("prep")
     E = tr.m_in.edge_count() + tr.m_rec.edge_count()
     Bl = tr.local_b
     # eligibility state read + written once per pass, gradient r/w + plan,
@@ -592,7 +810,7 @@ def run_device(args, w):
     # term once per K steps)
     alg_bytes = Bl * E * 16 + E * (16 + 4) + K * Bl * (w["num_inputs"] + w["hidden"] + 2 * w["hidden"]) * 4
     alg_single = Bl * E * 16 + E * (16 + 4) + Bl * (w["num_inputs"] + w["hidden"] + 2 * w["hidden"]) * 4
-    achieved = alg_bytes / (k_ms * 1e-3) / 1e9
+    achieved = alg_bytes / (k_us * 1e-6) / 1e9
     peak, peak_kind = measured_peak()
     traffic = None
     prof = os.path.join(ROOT, "profiles", "eprop_ncu_traffic.json")
@@ -618,28 +836,26 @@ def run_device(args, w):
             "unit": "s/epoch", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms_dev, 3), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: e-prop ALIF classifier {w['num_inputs']}->{w['hidden']}, "
-                                   f"{int(w['density'] * 100)}% in/rec + DEEP R, 20 classes, batch {B}, "
-                                   f"{w['steps']}-step SHD-shaped synthetic trials, {EPOCH_BATCHES} batches/epoch",
-                       "global_batch": B, "seq_len": w["steps"], "parallelism": f"dp{ws}",
-                       "l2": "flushed (256 MiB write) between timed steps",
-                       "edges": E},
+            "config": workload_config(args, w, ws),
             "e2e": {"value": round(s_epoch_e2e, 4), "unit": "s/epoch",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16 + 8 * 4},
             "gpu_launches": int(round(launches_per_step * args.steps)),
             "gpu_launches_per_step": round(launches_per_step, 1),
-            "roofline": {"kernel": f"k_eprop_block<{K}> (sw_eprop_fused_block, {K} timesteps per pass)",
+            "roofline": {"kernel": f"k_eprop_t<{K}> (sw_eprop_pass, {K} timesteps per pass)",
                          "bound": "hbm",
                          "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "alg_bytes_per_launch": int(alg_bytes), "kernel_us": round(k_ms * 1e3, 2),
-                         "kernel_us_per_timestep": round(k_ms * 1e3 / K, 2),
-                         "share_of_step": round(k_ms * (w["steps"] / K) / ms_dev, 3),
+                         "alg_bytes_per_launch": int(alg_bytes), "kernel_us": round(k_us, 2),
+                         "kernel_us_per_timestep": round(k_us / K, 2),
+                         "share_of_step": round(k_us * 1e-3 * (w["steps"] / K) / ms_dev, 3),
+                         "prep_us": round(prep_us, 2),
+                         "note": "the pass re-reads its K steps of trace/psi/lsig runs from L2 per "
+                                 "8-synapse tile (L2 throughput, not HBM, is its ceiling: see DESIGN.md)",
                          # the same K timesteps as K single-step passes would
                          # move K x the eligibility bytes: the temporally
                          # blocked pass beats that formulation's HBM roofline
-                         "single_step_equiv_GBs": round(K * alg_single / (k_ms * 1e-3) / 1e9, 1),
-                         "single_step_equiv_frac": round(K * alg_single / (k_ms * 1e-3) / 1e9 / peak, 4)},
+                         "single_step_equiv_GBs": round(K * alg_single / (k_us * 1e-6) / 1e9, 1),
+                         "single_step_equiv_frac": round(K * alg_single / (k_us * 1e-6) / 1e9 / peak, 4)},
             "clocks": clocks,
         }
         if cpu is not None:
@@ -647,16 +863,29 @@ def run_device(args, w):
         if ws == 1 and not args.no_micro:
             del tr
             torch.cuda.empty_cache()
+            line["alif_step"] = run_alif_bench()
             line["mupdate"] = run_mupdate()
             if not args.no_cpu_baseline:
                 line["mupdate"]["cpu_baseline"] = cpu_micro_sample()
             line["topomap"] = run_topomap_sweep()
+            if not args.no_cpu_baseline:
+                cb = topomap_cpu_baseline()
+                line["topomap_cpu_baseline"] = cb
+                for k, v in line["topomap"].items():
+                    c = cb["per_scale"].get(k)
+                    if c:
+                        v["cpu_x_realtime"] = c["x_realtime"]
+                        v["speedup_vs_cpu"] = round(v["x_realtime"] / c["x_realtime"], 1)
     if ws > 1 and not args.no_micro:
-        # every rank takes part in the sharded topomap sweep
+        # every rank takes part in the sharded topomap sweep and microbenchmarks
+        del tr
+        torch.cuda.empty_cache()
         topo = run_topomap_sweep(model_ms=20.0, process_group=dist.group.WORLD)
+        micro = run_micro_sharded(dist.group.WORLD)
         if rank == 0:
             line["topomap"] = topo
             line["topomap_parallelism"] = f"post-sharded x{ws}, NCCL spike all-gather per step"
+            line["micro_sharded"] = micro
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -418,6 +418,36 @@ class EpropClassifierTrainer:
         torch.cuda.current_stream().wait_stream(side)
         return g
 
+    def eprop_kernel_graph(self, reps: int, part: str = "pass") -> "torch.cuda.CUDAGraph":
+        """A CUDA graph of `reps` launches of one part of the e-prop group over
+        steps 0..K-1 on the live state: "pass" (sw_eprop_pass, the dominant
+        kernel) or "prep" (sw_eprop_prep), for per-kernel timing."""
+        calls = []
+        orig = _lib.call
+
+        def rec(name, *args):
+            calls.append((name, args))
+            return orig(name, *args)
+        _lib.call = rec
+        try:
+            self._eprop_block(0, EPROP_BLOCK_STEPS, _lib.stream_ptr())
+        finally:
+            _lib.call = orig
+        want = "sw_eprop_pass" if part == "pass" else "sw_eprop_prep"
+        name, args = next(c for c in calls if c[0] == want)
+        keep = (self._tsegs, )   # ctypes buffers referenced by the recorded args stay alive
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                st = torch.cuda.current_stream().cuda_stream
+                for _ in range(reps):
+                    orig(name, *args[:-1], st)
+        torch.cuda.current_stream().wait_stream(side)
+        g._sw_keep = (keep, args)
+        return g
+
     def _launch_steps(self, learn: bool, overlap: bool = False) -> None:
         """One trial: one launch running the forward pass of K =
         EPROP_BLOCK_STEPS steps, then one e-prop pass over those K steps
