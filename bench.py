@@ -447,6 +447,7 @@ def run_mprop(m, syn, seed, flush, peak, qs=SPIKE_QS):
         pr = (_lib.PropProj * 1)()
         pr[0].col_ptr, pr[0].src_pre, pr[0].src_slot = tm.col_ptr.data_ptr(), tm.src_pre.data_ptr(), tm.src_slot.data_ptr()
         pr[0].weights, pr[0].spike_bits, pr[0].stride = w.data_ptr(), bits.data_ptr(), m.stride
+        pr[0].col_length = tm.col_length.data_ptr()
         us = _time_launch(lambda: _lib.call("sw_propagate_ordered", ctypes.cast(pr, ctypes.c_void_p), 1, N,
                                             outv.data_ptr(), 0, _lib.stream_ptr()), flush, reps=5)
         r = line(q, S, us, "ordered", "bit-exact mode: walks all E transpose entries + spike bits per step "

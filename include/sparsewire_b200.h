@@ -410,22 +410,40 @@ SW_API int sw_f64_to_f32(const double* in, float* out, int64_t n, void* stream);
 SW_API int sw_scale_f64(double* x, int64_t n, double s, void* stream);
 
 /* ---- transpose (connectivity.py:151-203) ----------------------------------- */
-/* TransposeMap.rebuild in CSR form: for post j, (pre, slot) of its incoming
- * synapses in [col_ptr[j], col_ptr[j+1]) ordered by (pre, slot) (the
- * reference's lexsort order).  col_length[N], col_ptr[N+1],
- * src_pre/src_slot[>= edges], cursor[N] scratch, *max_len = widest column.
- * changed: device flag (NULL = always); when it reads 0 nothing is rebuilt
- * (remap-only-if-changed, updates.py:367-369). */
+/* TransposeMap.rebuild in CSR form with slack: for post j, (pre, slot) of
+ * its incoming synapses in [col_ptr[j], col_ptr[j] + col_length[j]) ordered
+ * by (pre, slot) (the reference's lexsort order); column j has room for
+ * col_ptr[j+1] - col_ptr[j] = col_length[j] + slack entries (slack >= 0;
+ * room for sw_transpose_patch).  col_length[N], col_ptr[N+1],
+ * src_pre/src_slot[>= edges + N*slack], cursor[N] scratch, *max_len =
+ * widest column.  changed: device flag (NULL = always); when it reads 0
+ * nothing is rebuilt (remap-only-if-changed, updates.py:367-369). */
 SW_API int sw_transpose_rebuild(const sw_ragged_t* m, int32_t* col_length, int32_t* col_ptr,
                                 int32_t* src_pre, int32_t* src_slot, int32_t* cursor,
-                                int32_t* max_len, const int32_t* changed, void* stream);
+                                int32_t* max_len, const int32_t* changed, int32_t slack, void* stream);
 /* The same rebuild as one cooperative launch (grid barriers between the
  * count / scan / scatter / sort phases; a single launch that exits at once
  * when *changed reads 0).  block_scratch: >= 2048 int32 (device). */
 SW_API int sw_transpose_rebuild_coop(const sw_ragged_t* m, int32_t* col_length, int32_t* col_ptr,
                                      int32_t* src_pre, int32_t* src_slot, int32_t* cursor,
                                      int32_t* max_len, const int32_t* changed,
-                                     int32_t* block_scratch, void* stream);
+                                     int32_t* block_scratch, int32_t slack, void* stream);
+/* Incremental remap (connectivity.py:173-192 applied to one update's
+ * changes instead of the whole matrix).  patch_log (device int32, written by
+ * the mutating kernel, e.g. sw_rewire_update with prm->patch_log):
+ *   [0] = rows whose structure changed, [1] = removed (pre, post) pairs,
+ *   [2] = overflow flag, [3] reserved, then cap row ids, then cap pairs.
+ * For every column touched by those rows (their current targets and their
+ * removed targets) the entries of the changed rows are dropped and the rows'
+ * current synapses merged back in (pre, slot) order, in place.  A column
+ * that outgrows its slack, or a log that overflowed, sets *rebuild = 1 (the
+ * caller's gated sw_transpose_rebuild_coop then rebuilds everything; the
+ * result is identical either way).  The log counters are reset for the next
+ * update.  scratch: sw_transpose_patch_scratch_bytes(num_pre, num_post). */
+SW_API int64_t sw_transpose_patch_scratch_bytes(int32_t num_pre, int32_t num_post);
+SW_API int sw_transpose_patch(const sw_ragged_t* m, int32_t* col_length, const int32_t* col_ptr,
+                              int32_t* src_pre, int32_t* src_slot, int32_t* patch_log, int32_t cap,
+                              int32_t* rebuild, void* scratch, void* stream);
 
 /* ---- spike propagation (connectivity.py:139-148) ---------------------------- */
 /* Event-driven atomic mode: out[target] += w over the rows in
@@ -478,7 +496,8 @@ SW_API int sw_propagate_bucketed_atomic(const uint16_t* soff, const uint16_t* bt
                                         const int32_t* n_spikes, int32_t max_spikes, double* out,
                                         void* stream);
 typedef struct sw_prop_proj {
-  const int32_t* col_ptr;    /* transpose CSR of the projection */
+  const int32_t* col_ptr;    /* transpose CSR of the projection (column j: col_ptr[j], col_length[j]) */
+  const int32_t* col_length;
   const int32_t* src_pre;
   const int32_t* src_slot;
   const double* weights;     /* [num_pre, stride] */
@@ -501,7 +520,7 @@ SW_API int sw_stdp_pre(const int32_t* row_length, const int32_t* target, double*
                        int32_t num_pre, const uint32_t* pre_bits, const double* y, double* x,
                        double a_minus, double w_min, double w_max, void* stream);
 /* on_post_spikes through the transpose: w = clip(w + a_plus*x[pre]), then y[post] += 1 */
-SW_API int sw_stdp_post(const int32_t* col_ptr, const int32_t* src_pre, const int32_t* src_slot,
+SW_API int sw_stdp_post(const int32_t* col_ptr, const int32_t* col_length, const int32_t* src_pre, const int32_t* src_slot,
                         double* w, int32_t stride, int32_t num_post, const uint32_t* post_bits,
                         const double* x, double* y, double a_plus, double w_min, double w_max,
                         void* stream);
@@ -519,6 +538,8 @@ typedef struct sw_rewire_params {
   void* scratch;             /* sw_rewire_scratch_bytes(num_post, total_attempts) bytes for rows with
                                 more than 64 attempts (processed serially, exact); NULL: such rows
                                 count as errors (totals[7]) */
+  int32_t* patch_log;        /* optional sw_transpose_patch log (rows changed, removed pairs) */
+  int32_t patch_cap;
 } sw_rewire_params_t;
 SW_API int64_t sw_rewire_scratch_bytes(int32_t num_post, int64_t total_attempts);
 /* One RewiringRule update (host + row phases), no host round trip.
@@ -553,9 +574,9 @@ typedef struct sw_topomap_step {
   double decay_s, g_leak, v_rest, e_exc, v_theta, v_reset, h, tau_m;
   int64_t ref_steps;
   const int32_t* ff_row_length; const int32_t* ff_target; double* ff_g; int32_t ff_stride;
-  const int32_t* ff_col_ptr; const int32_t* ff_src_pre; const int32_t* ff_src_slot;
+  const int32_t* ff_col_ptr; const int32_t* ff_col_len; const int32_t* ff_src_pre; const int32_t* ff_src_slot;
   const int32_t* lat_row_length; const int32_t* lat_target; double* lat_g; int32_t lat_stride;
-  const int32_t* lat_col_ptr; const int32_t* lat_src_pre; const int32_t* lat_src_slot;
+  const int32_t* lat_col_ptr; const int32_t* lat_col_len; const int32_t* lat_src_pre; const int32_t* lat_src_slot;
   double* ff_x; double* ff_y; double* lat_x; double* lat_y;
   double decay_x, decay_y, a_plus, a_minus, w_min, w_max;
   /* postsynaptic shard [post_lo, post_hi) of this rank (0, n when unsharded):

@@ -46,7 +46,7 @@ RP = C.POINTER(Ragged)
 
 class PropProj(C.Structure):
     """sw_prop_proj_t"""
-    _fields_ = [("col_ptr", P), ("src_pre", P), ("src_slot", P), ("weights", P),
+    _fields_ = [("col_ptr", P), ("col_length", P), ("src_pre", P), ("src_slot", P), ("weights", P),
                 ("spike_bits", P), ("stride", I32)]
 
 
@@ -54,7 +54,8 @@ class RewireParams(C.Structure):
     """sw_rewire_params_t"""
     _fields_ = [("host_prefix", U64), ("row_prefix", U64), ("rule_id", I32), ("side", I32),
                 ("total_attempts", I64), ("form_lut", P), ("dist_lut", P), ("g_theta", F64),
-                ("p_dep", F64), ("p_pot", F64), ("g_init", F64), ("scratch", P)]
+                ("p_dep", F64), ("p_pot", F64), ("g_init", F64), ("scratch", P), ("patch_log", P),
+                ("patch_cap", I32)]
 
 
 class TopomapStep(C.Structure):
@@ -65,9 +66,9 @@ class TopomapStep(C.Structure):
                 ("v_theta", F64), ("v_reset", F64), ("h", F64), ("tau_m", F64),
                 ("ref_steps", I64),
                 ("ff_row_length", P), ("ff_target", P), ("ff_g", P), ("ff_stride", I32),
-                ("ff_col_ptr", P), ("ff_src_pre", P), ("ff_src_slot", P),
+                ("ff_col_ptr", P), ("ff_col_len", P), ("ff_src_pre", P), ("ff_src_slot", P),
                 ("lat_row_length", P), ("lat_target", P), ("lat_g", P), ("lat_stride", I32),
-                ("lat_col_ptr", P), ("lat_src_pre", P), ("lat_src_slot", P),
+                ("lat_col_ptr", P), ("lat_col_len", P), ("lat_src_pre", P), ("lat_src_slot", P),
                 ("ff_x", P), ("ff_y", P), ("lat_x", P), ("lat_y", P),
                 ("decay_x", F64), ("decay_y", F64), ("a_plus", F64), ("a_minus", F64),
                 ("w_min", F64), ("w_max", F64), ("post_lo", I32), ("post_hi", I32)]
@@ -170,14 +171,16 @@ SIGNATURES: dict[str, list] = {
     "sw_clf_batch_stats": [P, P, P, I32, I32, P, P],
     "sw_f64_to_f32": [P, P, I64, P],
     "sw_scale_f64": [P, I64, F64, P],
-    "sw_transpose_rebuild": [RP, P, P, P, P, P, P, P, P],
-    "sw_transpose_rebuild_coop": [RP, P, P, P, P, P, P, P, P, P],
+    "sw_transpose_rebuild": [RP, P, P, P, P, P, P, P, I32, P],
+    "sw_transpose_rebuild_coop": [RP, P, P, P, P, P, P, P, P, I32, P],
+    "sw_transpose_patch": [RP, P, P, P, P, P, I32, P, P, P],
+    "sw_transpose_patch_scratch_bytes": [I32, I32],
     "sw_propagate_atomic": [P, P, P, I32, I32, I32, P, P, I32, P, P, I64, P],
     "sw_propagate_ordered": [P, I32, I32, P, I32, P],
     "sw_spike_bits_to_list": [P, I32, P, P, P],
     "sw_stdp_decay": [P, I32, F64, P, I32, F64, P],
     "sw_stdp_pre": [P, P, P, I32, I32, P, P, P, F64, F64, F64, P],
-    "sw_stdp_post": [P, P, P, P, I32, I32, P, P, P, F64, F64, F64, P],
+    "sw_stdp_post": [P, P, P, P, P, I32, I32, P, P, P, F64, F64, F64, P],
     "sw_rewire_update": [RP, I32, P, P, P, P, P, P, P, P, P, P, I32, P],
     "sw_rewire_scratch_bytes": [I32, I64],
     "sw_topomap_step": [P, P, P],
@@ -214,6 +217,7 @@ def lib():
     L.sw_eprop_pass_scratch_bytes.restype = C.c_int64
     L.sw_eprop_prep_scratch_bytes.restype = C.c_int64
     L.sw_rewire_scratch_bytes.restype = C.c_int64
+    L.sw_transpose_patch_scratch_bytes.restype = C.c_int64
     L.sw_launch_count.argtypes = []
     L.sw_launch_count.restype = C.c_longlong
     L.sw_last_error.argtypes = []

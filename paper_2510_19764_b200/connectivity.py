@@ -395,6 +395,7 @@ def propagate_spikes(m: RaggedMatrix, weights: torch.Tensor, spikes: torch.Tenso
         pr[0].col_ptr, pr[0].src_pre, pr[0].src_slot = (tmap.col_ptr.data_ptr(),
                                                         tmap.src_pre.data_ptr(),
                                                         tmap.src_slot.data_ptr())
+        pr[0].col_length = tmap.col_length.data_ptr()
         pr[0].weights, pr[0].spike_bits, pr[0].stride = weights.data_ptr(), bits.data_ptr(), m.stride
         import ctypes as _c
         _lib.call("sw_propagate_ordered", _c.cast(pr, _c.c_void_p), 1, m.num_post, out.data_ptr(), 1, st)

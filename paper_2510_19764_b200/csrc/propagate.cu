@@ -138,6 +138,7 @@ k_prop_slab(const int32_t* __restrict__ row_length, const int32_t* __restrict__ 
 
 struct Proj {
   const int32_t* col_ptr;
+  const int32_t* col_len;
   const int32_t* src_pre;
   const int32_t* src_slot;
   const double* w;
@@ -150,7 +151,7 @@ __global__ void k_prop_ordered(Proj p0, Proj p1, int n_proj, int N, double* out,
     double acc = accumulate ? out[j] : 0.0;
     for (int k = 0; k < n_proj; ++k) {
       const Proj& p = k ? p1 : p0;
-      const int a = p.col_ptr[j], e = p.col_ptr[j + 1];
+      const int a = p.col_ptr[j], e = a + p.col_len[j];
       for (int q = a; q < e; ++q) {
         const int i = p.src_pre[q];
         if (spk(p.bits, i)) acc = __dadd_rn(acc, p.w[(int64_t)i * p.stride + p.src_slot[q]]);
@@ -193,12 +194,12 @@ __global__ void k_stdp_pre(const int32_t* __restrict__ row_length, const int32_t
 }
 
 // potentiation of the incoming synapses of spiking posts (transpose), then y[post] += 1
-__global__ void k_stdp_post(const int32_t* col_ptr, const int32_t* src_pre, const int32_t* src_slot,
+__global__ void k_stdp_post(const int32_t* col_ptr, const int32_t* col_len, const int32_t* src_pre, const int32_t* src_slot,
                             double* w, int stride, int N, const uint32_t* bits, const double* x,
                             double* y, double a_plus, double w_min, double w_max) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
     if (!spk(bits, j)) continue;
-    const int a = col_ptr[j], e = col_ptr[j + 1];
+    const int a = col_ptr[j], e = a + col_len[j];
     for (int q = a; q < e; ++q) {
       const int i = src_pre[q];
       const int64_t o = (int64_t)i * stride + src_slot[q];
@@ -334,7 +335,7 @@ extern "C" int sw_propagate_ordered(const sw_prop_proj_t* projs, int32_t n_proj,
   if (n_proj < 1 || n_proj > 2) { sw::set_last_error("propagate_ordered: 1 or 2 projections"); return SW_ERR_INVALID_ARG; }
   Proj p[2] = {};
   for (int k = 0; k < n_proj; ++k)
-    p[k] = Proj{projs[k].col_ptr, projs[k].src_pre, projs[k].src_slot, projs[k].weights,
+    p[k] = Proj{projs[k].col_ptr, projs[k].col_length, projs[k].src_pre, projs[k].src_slot, projs[k].weights,
                 projs[k].spike_bits, projs[k].stride};
   if (num_post <= 0) return SW_OK;
   k_prop_ordered<<<grid1(num_post), 256, 0, (cudaStream_t)stream>>>(p[0], p[1], n_proj, num_post, out,
@@ -372,12 +373,12 @@ extern "C" int sw_stdp_pre(const int32_t* row_length, const int32_t* target, dou
   return SW_OK;
 }
 
-extern "C" int sw_stdp_post(const int32_t* col_ptr, const int32_t* src_pre, const int32_t* src_slot,
+extern "C" int sw_stdp_post(const int32_t* col_ptr, const int32_t* col_len, const int32_t* src_pre, const int32_t* src_slot,
                             double* w, int32_t stride, int32_t num_post, const uint32_t* post_bits,
                             const double* x, double* y, double a_plus, double w_min, double w_max,
                             void* stream) {
   if (num_post <= 0) return SW_OK;
-  k_stdp_post<<<grid1(num_post), 256, 0, (cudaStream_t)stream>>>(col_ptr, src_pre, src_slot, w, stride,
+  k_stdp_post<<<grid1(num_post), 256, 0, (cudaStream_t)stream>>>(col_ptr, col_len, src_pre, src_slot, w, stride,
                                                                  num_post, post_bits, x, y, a_plus,
                                                                  w_min, w_max); sw::count_launch();
   SW_CHECK_LAUNCH("sw_stdp_post");

@@ -60,7 +60,27 @@ struct RwArgs {
   double* ev_d;
   int32_t* heavy;               // rows with kKMax < attempts <= N, then the heavy-row scratch (or null)
   int64_t heavy_cap;
+  int32_t* plog;                // sw_transpose_patch log (or null): [0] rows, [1] pairs, [2] overflow
+  int32_t pcap;
 };
+
+// patch log: a removed (pre, post) pair, then (at the row's end) the row itself
+__device__ __forceinline__ void plog_pair(const RwArgs& A, int i, int j) {
+  if (!A.plog) return;
+  const int k = atomicAdd(&A.plog[1], 1);
+  if (k < A.pcap) {
+    A.plog[4 + A.pcap + 2 * k] = i;
+    A.plog[4 + A.pcap + 2 * k + 1] = j;
+  } else {
+    A.plog[2] = 1;
+  }
+}
+__device__ __forceinline__ void plog_row(const RwArgs& A, int i) {
+  if (!A.plog) return;
+  const int k = atomicAdd(&A.plog[0], 1);
+  if (k < A.pcap) A.plog[4 + k] = i;
+  else A.plog[2] = 1;
+}
 
 __device__ __forceinline__ int fy_get(const int* key, const int* val, int n, int p) {
   for (int q = 0; q < n; ++q) if (key[q] == p) return val[q];
@@ -139,6 +159,8 @@ __device__ __forceinline__ void rw_rows(const RwArgs& A, int64_t t0, int64_t dt)
           ++ev;
         }
     }
+    for (int q = 0; q < ns; ++q)
+      if ((hit >> q) & 1ull) plog_pair(A, i, m.target[off + sel[q]]);
     // chained removal, descending slots (connectivity.py:130-136)
     for (int q = ns - 1; q >= 0; --q) {
       if (!((hit >> q) & 1ull)) continue;
@@ -183,7 +205,10 @@ __device__ __forceinline__ void rw_rows(const RwArgs& A, int64_t t0, int64_t dt)
     atomicAdd((unsigned long long*)&A.totals[3], (unsigned long long)missed);
     atomicAdd((unsigned long long*)&A.totals[4], (unsigned long long)full);
     atomicAdd((unsigned long long*)&A.totals[5], (unsigned long long)k);
-    if (removed + formed) *A.changed = 1;
+    if (removed + formed) {
+      *A.changed = 1;
+      plog_row(A, i);
+    }
   }
 }
 
@@ -241,6 +266,7 @@ __device__ void rw_row_heavy(const RwArgs& A, int i) {
     if (u < p) {
       arr[q] = -1 - s;
       ++removed;
+      plog_pair(A, i, t);
       if (A.ev_kind) { A.ev_kind[ev] = 1; A.ev_d[ev] = A.dist_lut[torus_offset(i, t, A.side)]; ++ev; }
     }
   }
@@ -277,7 +303,10 @@ __device__ void rw_row_heavy(const RwArgs& A, int i) {
   A.totals[3] += missed;
   A.totals[4] += full;
   A.totals[5] += k;
-  if (removed + formed) *A.changed = 1;
+  if (removed + formed) {
+    *A.changed = 1;
+    plog_row(A, i);
+  }
 }
 
 // The last block to finish its rows runs the deferred heavy rows (if any):
@@ -373,6 +402,7 @@ extern "C" int sw_rewire_update(const sw_ragged_t* m, int32_t weight_plane, cons
                                 int8_t* ev_kind, double* ev_d, int32_t forced_attempts, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int P = m->num_pre;
+  if (prm->patch_log) cudaMemsetAsync(prm->patch_log, 0, 4 * sizeof(int32_t), st);   // this update's log
   if (!forced_attempts && !ev_kind && P > 0) {
     static int max_blocks = 0;
     if (max_blocks == 0) {
@@ -387,7 +417,7 @@ extern "C" int sw_rewire_update(const sw_ragged_t* m, int32_t weight_plane, cons
     if (blocks > max_blocks) blocks = max_blocks;
     RwArgs A{*m, weight_plane, attempts, keys, prm->form_lut, prm->dist_lut, prm->side,
              prm->g_theta, prm->p_dep, prm->p_pot, prm->g_init, totals, changed, nullptr, nullptr, nullptr,
-             (int32_t*)prm->scratch, heavy_cap(prm)};
+             (int32_t*)prm->scratch, heavy_cap(prm), prm->patch_log, prm->patch_cap};
     uint64_t hp = prm->host_prefix, rp = prm->row_prefix;
     int32_t rid = prm->rule_id;
     int64_t ta = prm->total_attempts;
@@ -418,7 +448,7 @@ extern "C" int sw_rewire_update(const sw_ragged_t* m, int32_t weight_plane, cons
   }
   RwArgs A{*m, weight_plane, attempts, keys, prm->form_lut, prm->dist_lut, prm->side,
            prm->g_theta, prm->p_dep, prm->p_pot, prm->g_init, totals, changed, ev_off, ev_kind, ev_d,
-           (int32_t*)prm->scratch, heavy_cap(prm)};
+           (int32_t*)prm->scratch, heavy_cap(prm), prm->patch_log, prm->patch_cap};
   if (P > 0) { k_rw_rows<<<grid1(P), 256, 0, st>>>(A); sw::count_launch(); }
   SW_CHECK_LAUNCH("sw_rewire_update");
   return SW_OK;

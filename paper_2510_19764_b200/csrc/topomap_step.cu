@@ -90,9 +90,9 @@ __device__ __forceinline__ void tm_prop(const sw_topomap_step_t& S, int t0, int 
     S.lat_y[j] = __dmul_rn(S.lat_y[j], S.decay_y);
     if (j < S.post_lo || j >= S.post_hi) continue;
     double acc = 0.0;
-    col_sum(acc, S.ff_col_ptr[j], S.ff_col_ptr[j + 1], S.ff_src_pre, S.ff_src_slot, S.src_bits, S.ff_g,
+    col_sum(acc, S.ff_col_ptr[j], S.ff_col_ptr[j] + S.ff_col_len[j], S.ff_src_pre, S.ff_src_slot, S.src_bits, S.ff_g,
             S.ff_stride);
-    col_sum(acc, S.lat_col_ptr[j], S.lat_col_ptr[j + 1], S.lat_src_pre, S.lat_src_slot, S.tgt_bits,
+    col_sum(acc, S.lat_col_ptr[j], S.lat_col_ptr[j] + S.lat_col_len[j], S.lat_src_pre, S.lat_src_slot, S.tgt_bits,
             S.lat_g, S.lat_stride);
     S.pending[j] = acc;
   }
@@ -155,9 +155,9 @@ __device__ __forceinline__ void tm_post(const sw_topomap_step_t& S, int w0, int 
     while (m) {
       const int j = gw * 32 + __ffs(m) - 1;
       m &= m - 1;
-      potentiate_col(S.ff_col_ptr[j], S.ff_col_ptr[j + 1], S.ff_src_pre, S.ff_src_slot, S.ff_g,
+      potentiate_col(S.ff_col_ptr[j], S.ff_col_ptr[j] + S.ff_col_len[j], S.ff_src_pre, S.ff_src_slot, S.ff_g,
                      S.ff_stride, S.ff_x, S.a_plus, S.w_min, S.w_max, lane);
-      potentiate_col(S.lat_col_ptr[j], S.lat_col_ptr[j + 1], S.lat_src_pre, S.lat_src_slot, S.lat_g,
+      potentiate_col(S.lat_col_ptr[j], S.lat_col_ptr[j] + S.lat_col_len[j], S.lat_src_pre, S.lat_src_slot, S.lat_g,
                      S.lat_stride, S.lat_x, S.a_plus, S.w_min, S.w_max, lane);
       if (lane == 0) {
         S.ff_y[j] = __dadd_rn(S.ff_y[j], 1.0);
@@ -270,7 +270,7 @@ k_tm_run(sw_topomap_step_t S, int n_steps, int64_t* spike_counts, unsigned* bar)
 struct TmSmem {
   static size_t bytes(int n) {
     const int words = (n + 31) / 32;
-    return (size_t)n * 8 * 9 + (size_t)(n + 1) * 4 * 2 + (size_t)n * 4 * 2 + (size_t)words * 4 * 2 + 64;
+    return (size_t)n * 8 * 9 + (size_t)(n + 1) * 4 * 2 + (size_t)n * 4 * 4 + (size_t)words * 4 * 2 + 64;
   }
 };
 
@@ -284,12 +284,14 @@ k_tm_run_staged(sw_topomap_step_t G, int n_steps, int64_t* spike_counts) {
   int64_t* ref = reinterpret_cast<int64_t*>(d + 8 * n);
   int32_t* ip = reinterpret_cast<int32_t*>(d + 9 * n);
   int32_t *fcp = ip, *lcp = ip + (n + 1), *frl = ip + 2 * (n + 1), *lrl = frl + n;
-  uint32_t *sb = reinterpret_cast<uint32_t*>(lrl + n), *tb = sb + words;
+  int32_t *fcl = lrl + n, *lcl = fcl + n;
+  uint32_t *sb = reinterpret_cast<uint32_t*>(lcl + n), *tb = sb + words;
   for (int x = threadIdx.x; x < n; x += blockDim.x) {
     V[x] = G.V[x]; gt[x] = G.g_tot[x]; pend[x] = G.pending[x];
     fx[x] = G.ff_x[x]; fy[x] = G.ff_y[x]; lx[x] = G.lat_x[x]; ly[x] = G.lat_y[x];
     ps[x] = G.p_src[x]; ref[x] = G.ref_until[x];
     frl[x] = G.ff_row_length[x]; lrl[x] = G.lat_row_length[x];
+    fcl[x] = G.ff_col_len[x]; lcl[x] = G.lat_col_len[x];
   }
   for (int x = threadIdx.x; x <= n; x += blockDim.x) {
     fcp[x] = G.ff_col_ptr[x];
@@ -299,7 +301,8 @@ k_tm_run_staged(sw_topomap_step_t G, int n_steps, int64_t* spike_counts) {
   sw_topomap_step_t S = G;
   S.V = V; S.g_tot = gt; S.pending = pend; S.ff_x = fx; S.ff_y = fy; S.lat_x = lx; S.lat_y = ly;
   S.p_src = ps; S.ref_until = ref; S.ff_row_length = frl; S.lat_row_length = lrl;
-  S.ff_col_ptr = fcp; S.lat_col_ptr = lcp; S.src_bits = sb; S.tgt_bits = tb;
+  S.ff_col_ptr = fcp; S.lat_col_ptr = lcp; S.ff_col_len = fcl; S.lat_col_len = lcl;
+  S.src_bits = sb; S.tgt_bits = tb;
   __syncthreads();
   const int t = threadIdx.x, nt = blockDim.x;
   const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;

@@ -127,7 +127,7 @@ class StdpSynapses:
         tmap.check_fresh()
         m, p = self.matrix, self.params
         bits = _as_bits(post, m.num_post)
-        _lib.call("sw_stdp_post", tmap.col_ptr.data_ptr(), tmap.src_pre.data_ptr(),
+        _lib.call("sw_stdp_post", tmap.col_ptr.data_ptr(), tmap.col_length.data_ptr(), tmap.src_pre.data_ptr(),
                   tmap.src_slot.data_ptr(), self.syn.planes[self.weight_plane].data_ptr(),
                   m.stride, m.num_post, bits.data_ptr(), self.x.data_ptr(), self.y.data_ptr(),
                   p.a_plus, p.w_min, p.w_max, _lib.stream_ptr())

@@ -131,6 +131,10 @@ class RewiringRule:
         self._heavy = torch.zeros((nb + 7) // 8, dtype=torch.int64, device=dev)
         self._prm.total_attempts = attempts_total
         self._prm.scratch = self._heavy.data_ptr()
+        # transpose patch log (sw_transpose_patch): changed rows + removed pairs
+        self.patch_cap = max(1, attempts_total)
+        self.patch_log = torch.zeros(4 + 3 * self.patch_cap, dtype=torch.int32, device=dev)
+        self._prm.patch_log, self._prm.patch_cap = self.patch_log.data_ptr(), self.patch_cap
 
     def force_attempts(self, attempts) -> None:
         """Use these per-row attempt counts instead of the host-phase draws
@@ -162,6 +166,7 @@ class RewiringRule:
     def descriptor(self) -> RuleDescriptor:
         d = RuleDescriptor(name=self.name, device_pass=self._device_pass)
         d.changed_flag = self.changed
+        d.patch_source = self      # patch_log / patch_cap for an incremental remap
         return d
 
     def collect(self, time_ms: float) -> None:
@@ -296,6 +301,7 @@ class TopomapModel:
     """topomap.py:329-493 on the device."""
 
     def __init__(self, scale: int, seed: int, workers: int = 1, always_remap: bool = False,
+                 incremental_remap: bool = True,
                  capacity_headroom: float = 4.0, record_events: bool = True,
                  use_graph: bool = True, rates_on_device: bool = False, process_group=None):
         """``process_group`` (torch.distributed, NCCL): postsynaptic sharding
@@ -314,7 +320,8 @@ class TopomapModel:
         self.stdp_params = StdpParams()
         self.use_graph = use_graph
         self.rates_on_device = rates_on_device
-        self.net = Model(seed, workers=workers, always_remap=always_remap)
+        self.net = Model(seed, workers=workers, always_remap=always_remap,
+                         incremental_remap=incremental_remap)
         ff_m, ff_syn = self._init_projection("ff", self.ff_params, CounterRng(seed, "init", "ff"),
                                              capacity_headroom)
         lat_m, lat_syn = self._init_projection("lat", self.lat_params,
@@ -388,6 +395,7 @@ class TopomapModel:
             setattr(s, f"{pre}_g", stdp.syn.planes["g"].data_ptr())
             setattr(s, f"{pre}_stride", m.stride)
             setattr(s, f"{pre}_col_ptr", tm.col_ptr.data_ptr())
+            setattr(s, f"{pre}_col_len", tm.col_length.data_ptr())
             setattr(s, f"{pre}_src_pre", tm.src_pre.data_ptr())
             setattr(s, f"{pre}_src_slot", tm.src_slot.data_ptr())
             setattr(s, f"{pre}_x", stdp.x.data_ptr())

@@ -19,11 +19,17 @@ from .errors import StaleTranspose
 
 
 class TransposeMap:
-    def __init__(self, matrix: RaggedMatrix):
+    """CSR with slack: column j = entries [col_ptr[j], col_ptr[j] + col_length[j]),
+    room for SLACK more (incremental patches, sw_transpose_patch)."""
+
+    SLACK = 8
+
+    def __init__(self, matrix: RaggedMatrix, slack: int | None = None):
         self.matrix = matrix
         dev = matrix.target.device
         N = matrix.num_post
-        cap = max(1, matrix.num_pre * matrix.stride)
+        self.slack = self.SLACK if slack is None else int(slack)
+        cap = max(1, matrix.num_pre * matrix.stride + N * self.slack)
         self.col_length = torch.zeros(N, dtype=torch.int32, device=dev)
         self.col_ptr = torch.zeros(N + 1, dtype=torch.int32, device=dev)
         self.src_pre = torch.zeros(cap, dtype=torch.int32, device=dev)
@@ -31,7 +37,11 @@ class TransposeMap:
         self._cursor = torch.zeros(N, dtype=torch.int32, device=dev)
         self._max_len = torch.zeros(1, dtype=torch.int32, device=dev)
         self._block_scratch = torch.zeros(2048, dtype=torch.int32, device=dev)
+        self._need_rebuild = torch.zeros(1, dtype=torch.int32, device=dev)
+        nb = int(_lib.lib().sw_transpose_patch_scratch_bytes(matrix.num_pre, N))
+        self._patch_scratch = torch.zeros(nb // 4 + 1, dtype=torch.int32, device=dev)
         self.version = -1
+        self.patches = 0
 
     def rebuild(self, changed_flag: torch.Tensor | None = None) -> None:
         """Rebuild from the matrix; with a device ``changed_flag`` the kernels
@@ -42,12 +52,33 @@ class TransposeMap:
         _lib.call("sw_transpose_rebuild_coop", ctypes.byref(d), self.col_length.data_ptr(),
                   self.col_ptr.data_ptr(), self.src_pre.data_ptr(), self.src_slot.data_ptr(),
                   self._cursor.data_ptr(), self._max_len.data_ptr(), _lib.ptr(changed_flag),
-                  self._block_scratch.data_ptr(), _lib.stream_ptr())
+                  self._block_scratch.data_ptr(), self.slack, _lib.stream_ptr())
         self.version = self.matrix.version
+
+    def patch(self, patch_log: torch.Tensor, cap: int) -> None:
+        """Apply one update's changes in place (sw_transpose_patch): the
+        columns touched by the changed rows are re-merged; if a column runs
+        out of slack (or the log overflowed) a full rebuild follows on the
+        device.  Same result as rebuild(), bit for bit."""
+        if self.version < 0:
+            self.rebuild()
+            return
+        d = descriptor(self.matrix, None)
+        _lib.call("sw_transpose_patch", ctypes.byref(d), self.col_length.data_ptr(), self.col_ptr.data_ptr(),
+                  self.src_pre.data_ptr(), self.src_slot.data_ptr(), patch_log.data_ptr(), int(cap),
+                  self._need_rebuild.data_ptr(), self._patch_scratch.data_ptr(), _lib.stream_ptr())
+        # gated full rebuild: runs only if the patch flagged an overflow
+        _lib.call("sw_transpose_rebuild_coop", ctypes.byref(d), self.col_length.data_ptr(),
+                  self.col_ptr.data_ptr(), self.src_pre.data_ptr(), self.src_slot.data_ptr(),
+                  self._cursor.data_ptr(), self._max_len.data_ptr(), self._need_rebuild.data_ptr(),
+                  self._block_scratch.data_ptr(), self.slack, _lib.stream_ptr())
+        self._need_rebuild.zero_()
+        self.version = self.matrix.version
+        self.patches += 1
 
     @property
     def max_col_length(self) -> int:
-        return int(self._max_len.item())
+        return int(self.col_length.max().item()) if self.col_length.numel() else 0
 
     def is_stale(self) -> bool:
         return self.version != self.matrix.version
@@ -57,9 +88,13 @@ class TransposeMap:
             raise StaleTranspose("transpose map older than its matrix")
 
     def host_csr(self):
-        ptr = self.col_ptr.cpu().numpy()
-        E = int(ptr[-1])
-        return ptr, self.src_pre[:E].cpu().numpy(), self.src_slot[:E].cpu().numpy()
+        """Compact CSR (ptr[N+1], pre, slot) of the live entries (slack dropped)."""
+        start = self.col_ptr[:-1].cpu().numpy().astype(np.int64)
+        lens = self.col_length.cpu().numpy().astype(np.int64)
+        ptr = np.zeros(lens.size + 1, dtype=np.int64)
+        np.cumsum(lens, out=ptr[1:])
+        idx = np.repeat(start - ptr[:-1], lens) + np.arange(int(ptr[-1]))
+        return ptr, self.src_pre.cpu().numpy()[idx], self.src_slot.cpu().numpy()[idx]
 
     def column(self, j: int):
         ptr, pre, slot = self.host_csr()

@@ -117,10 +117,14 @@ class RuleBinding:
 class Model:
     """Registry of matrices, arrays, transposes and rule groups (updates.py:231-372)."""
 
-    def __init__(self, seed: int, workers: int = 1, always_remap: bool = False):
+    def __init__(self, seed: int, workers: int = 1, always_remap: bool = False,
+                 incremental_remap: bool = True):
         self.seed = seed
         self.workers = max(1, workers)   # accepted for API parity; the device is the worker pool
         self.always_remap = always_remap
+        # rules with a patch log (RewiringRule) remap incrementally
+        # (sw_transpose_patch); False: full rebuilds (updates.py:367-372)
+        self.incremental_remap = incremental_remap
         self.timers = PhaseTimers()
         self.matrices: dict[str, tuple[RaggedMatrix, SynVarMatrix]] = {}
         self.arrays: dict[str, torch.Tensor] = {}
@@ -212,5 +216,10 @@ class Model:
             tm = self.transposes.get(b.matrix_name)
             if tm is not None and (self.always_remap or b.matrix.version != v0):
                 self.timers.start("remap")
-                tm.rebuild(changed_flag=getattr(rule, "changed_flag", None) if not self.always_remap else None)
+                src = getattr(rule, "patch_source", None)
+                if src is not None and self.incremental_remap and not self.always_remap:
+                    # incremental: only the columns the update touched (sw_transpose_patch)
+                    tm.patch(src.patch_log, src.patch_cap)
+                else:
+                    tm.rebuild(changed_flag=getattr(rule, "changed_flag", None) if not self.always_remap else None)
                 self.timers.stop("remap")

@@ -332,3 +332,52 @@ def test_rows_with_more_than_64_attempts_are_exact(dev_lib):
         assert st["attempts"] == int(att.sum())
         assert [d for _, d in rule.elim_events] == [d for _, k, d in r.events if k == 1]
         assert [d for _, d in rule.form_events] == [d for _, k, d in r.events if k == 2]
+
+
+def test_incremental_transpose_patch_equals_rebuild(dev_lib):
+    """sw_transpose_patch (the rewiring update's changed rows re-merged into
+    the columns they touch) leaves every column exactly as a full rebuild
+    (connectivity.py:173-192 order) after every update of a 1 s run; the
+    whole model state is bit-identical to a run with full rebuilds."""
+    from paper_2510_19764_b200.topomap import TopomapModel
+    from paper_2510_19764_b200.transpose import TransposeMap
+    inc = TopomapModel(1, seed=8, use_graph=False, record_events=False)
+    full = TopomapModel(1, seed=8, use_graph=False, record_events=False, incremental_remap=False)
+    checked = [0, 0]
+    orig = inc.net.run_update_group
+
+    def wrapped(group):
+        orig(group)
+        checked[0] += 1
+        if checked[0] % 5:
+            return
+        for name, tm in (("ff", inc.ff_tmap), ("lat", inc.lat_tmap)):
+            ref = TransposeMap(inc.net.matrices[name][0])
+            ref.rebuild()
+            a, b = tm.host_csr(), ref.host_csr()
+            for x, y in zip(a, b):
+                assert np.array_equal(x, y), (name, checked[0])
+        checked[1] += 1
+    inc.net.run_update_group = wrapped
+    inc.run(1000.0)
+    full.run(1000.0)
+    assert checked[1] >= 150
+    assert inc.ff_tmap.patches > 0
+    si, sf = inc.state_arrays(), full.state_arrays()
+    for k in si:
+        assert np.array_equal(si[k], sf[k]), k
+    # the run rewired: some updates changed the structure
+    assert sum(int(x) for x in inc._update_log[:, :].sum(dim=1).cpu().numpy()) > 0
+
+
+def test_incremental_transpose_patch_in_graph(dev_lib):
+    """The patch path inside the captured rewiring-period graph gives the
+    same state as eager full rebuilds."""
+    from paper_2510_19764_b200.topomap import TopomapModel
+    g = TopomapModel(2, seed=9, use_graph=True, record_events=False)
+    e = TopomapModel(2, seed=9, use_graph=False, record_events=False, incremental_remap=False)
+    g.run(300.0)
+    e.run(300.0)
+    sg, se = g.state_arrays(), e.state_arrays()
+    for k in sg:
+        assert np.array_equal(sg[k], se[k]), k
