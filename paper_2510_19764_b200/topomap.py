@@ -339,6 +339,8 @@ class TopomapModel:
         if world > 1:
             # target spikes live in the all-gather buffer (world * words-per-rank words)
             self.target.spike_bits = self.shard.bits
+            # one eager collective: the communicator exists before any graph capture
+            self.shard.gather()
         self.ff_stdp = StdpSynapses(ff_m, ff_syn, self.h, self.stdp_params)
         self.lat_stdp = StdpSynapses(lat_m, lat_syn, self.h, self.stdp_params)
         self.ff_tmap = self.net.register_transpose("ff")
@@ -426,6 +428,12 @@ class TopomapModel:
         _lib.call("sw_topomap_synapses", ctypes.byref(s), self.spike_counts.data_ptr(),
                   _lib.stream_ptr())
 
+    def _nccl(self) -> bool:
+        if self.pg is None:
+            return False
+        import torch.distributed as dist
+        return dist.get_backend(self.pg) == "nccl"
+
     def _period(self, rewire_steps: int) -> None:
         """rewire_steps model steps + the rewiring group (device only).
         Unsharded sheets of up to PERSISTENT_MAX_NODES: the steps run in one
@@ -459,7 +467,9 @@ class TopomapModel:
         if recorder is not None and self.step_index == 0:
             recorder.snapshot(0.0, self, tag="initial")
         spikes_each_step = recorder is not None and recorder.record_spikes
-        graph_ok = (self.use_graph and self.shard.world == 1 and not self.ff_rule.record_events
+        # sharded runs capture the period too when the collective can be
+        # captured (NCCL: the spike all-gather becomes a graph node)
+        graph_ok = (self.use_graph and (self.shard.world == 1 or self._nccl()) and not self.ff_rule.record_events
                     and not self.lat_rule.record_events and stim_steps % rewire_steps == 0
                     and not spikes_each_step
                     and (not snap_steps or snap_steps % rewire_steps == 0))

@@ -314,3 +314,41 @@ def form_hist_sharded(rank, world, port, out):
         out.put((rank, res))
     finally:
         dist.destroy_process_group()
+
+
+def _init_nccl(rank, world, port):
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+
+
+def nccl_batch_dp(rank, world, port, out):
+    """Batch-DP over NCCL (one GPU per rank): gradients all-reduced on the
+    device; the ranks must end bit-identical."""
+    from paper_2510_19764_b200.classifier import EpropClassifierTrainer, SyntheticTask
+    from paper_2510_19764_b200.sharding import shard_batch
+    _init_nccl(rank, world, port)
+    try:
+        task = SyntheticTask(num_classes=3, num_inputs=20, example_steps=40, seed=4)
+        B = 8
+        tr = EpropClassifierTrainer(task, hidden=24, batch_size=B, seed=4, deep_r=True,
+                                    input_density=0.3, recurrent_density=0.2,
+                                    process_group=dist.group.WORLD, local_batch=shard_batch(B, rank, world))
+        hist = [tr.train_batch(k) for k in range(2)]
+        out.put((rank, [(h["loss"], h["removed"]) for h in hist], tr.s_in.planes["w"].cpu().numpy(),
+                 hashlib.sha256(tr.connectivity_fingerprint()).hexdigest()))
+    finally:
+        dist.destroy_process_group()
+
+
+def nccl_topomap(rank, world, port, out):
+    """Postsynaptically sharded topomap over NCCL with the rewiring period
+    captured in a CUDA graph (spike all-gather as a graph node)."""
+    from paper_2510_19764_b200.topomap import TopomapModel
+    _init_nccl(rank, world, port)
+    try:
+        m = TopomapModel(1, seed=4, record_events=False, use_graph=True, process_group=dist.group.WORLD)
+        m.run(50.0)
+        st = m.state_arrays()
+        out.put((rank, {k: st[k] for k in st if k != "V"}, st["V"], (m.post_lo, m.post_hi), len(m._graphs)))
+    finally:
+        dist.destroy_process_group()
