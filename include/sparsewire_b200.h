@@ -396,7 +396,23 @@ typedef struct sw_clf_step {
    * kernel stages a spiking row with one bulk copy.  NULL: k_clf_step. */
   const int32_t* in_tw; const int32_t* rec_tw;
   int32_t in_tw_stride; int32_t rec_tw_stride;
+  /* precomputed input spikes (sw_clf_inputs), grouped launches only:
+   * in_bits[t][batch][in_words]; NULL = the kernel draws them itself */
+  const uint32_t* in_bits; int32_t in_words;
 } sw_clf_step_t;
+/* The trial's input side at once (classifier.py:63-67, 210-213): every input
+ * spike of steps 0..steps-1 from the examples' counter streams, as words
+ * in_bits[t][batch][words] (words = ceil(num_inputs/32)), and the input
+ * traces xbar_t[t][num_inputs][ldb] (replica-minor, zero past the batch). */
+typedef struct sw_clf_inputs {
+  int32_t steps, batch, ldb, num_inputs, words;
+  const double* p_in;        /* [batch, num_inputs] */
+  const uint64_t* ex_key;    /* [batch] */
+  float alpha;
+  float* xbar_t;
+  uint32_t* in_bits;
+} sw_clf_inputs_t;
+SW_API int sw_clf_inputs(const sw_clf_inputs_t* p, void* stream);
 /* tw[i][s] = (target[i][s], f32(w[i][s])) for s < row_length[i], (0, 0)
  * after; tw_stride >= stride, even. */
 SW_API int sw_clf_pack_rows(const int32_t* row_length, const int32_t* target, const double* w,

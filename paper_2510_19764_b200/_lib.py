@@ -117,7 +117,14 @@ class ClfStep(C.Structure):
                 ("y", P), ("pi_sum", P), ("loss", P), ("d", P), ("psi", P), ("lsig", P),
                 ("alpha", F32), ("rho", F32), ("beta", F32), ("v_thr", F32), ("alpha64", F64),
                 ("zbar_in", P), ("xbar_in", P), ("n_steps", I32), ("slot_count", I32),
-                ("in_tw", P), ("rec_tw", P), ("in_tw_stride", I32), ("rec_tw_stride", I32)]
+                ("in_tw", P), ("rec_tw", P), ("in_tw_stride", I32), ("rec_tw_stride", I32),
+                ("in_bits", P), ("in_words", I32)]
+
+
+class ClfInputs(C.Structure):
+    """sw_clf_inputs_t"""
+    _fields_ = [("steps", I32), ("batch", I32), ("ldb", I32), ("num_inputs", I32), ("words", I32),
+                ("p_in", P), ("ex_key", P), ("alpha", F32), ("xbar_t", P), ("in_bits", P)]
 BP = C.POINTER(BitfieldDesc)
 
 # name -> argtypes (restype is int status for all but sw_last_error)
@@ -168,6 +175,7 @@ SIGNATURES: dict[str, list] = {
     "sw_poisson_rates": [I32, P, I32, F64, F64, F64, F64, P, P, P],
     "sw_clf_step": [C.c_void_p, P],
     "sw_clf_pack_rows": [P, P, P, I32, I32, I32, P, P],
+    "sw_clf_inputs": [P, P],
     "sw_clf_batch_stats": [P, P, P, I32, I32, P, P],
     "sw_f64_to_f32": [P, P, I64, P],
     "sw_scale_f64": [P, I64, F64, P],

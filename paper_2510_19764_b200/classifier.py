@@ -306,11 +306,16 @@ class EpropClassifierTrainer:
         # replica-minor copies of one group's e-prop inputs (sw_eprop_prep):
         # [K][rows][ldb], and the pass kernel's split partials / tickets
         K, L = EPROP_BLOCK_STEPS, self.plan_in.ldb
-        self.xbar_t = torch.zeros((K, NI, L), **f32)
         self.zbar_t = torch.zeros((K, H, L), **f32)
         self.psi_t = torch.zeros((K, H, L), **f32)
         self.lsig_t = torch.zeros((K, H, L), **f32)
         self._tsegs = (_lib.EpropTSeg * 2)()
+        # the trial's input side (sw_clf_inputs, once per batch): spike words
+        # for the forward pass and the input traces in the e-prop layout
+        T = self.task.example_steps
+        self._in_words = (NI + 31) // 32
+        self.in_bits = torch.zeros((T, B, self._in_words), dtype=torch.int32, device="cuda")
+        self.xbar_all = torch.zeros((T, NI, L), **f32)
         nb = int(_lib.lib().sw_eprop_prep_scratch_bytes(K, B, H, C))
         self._ro_partial = torch.zeros(nb // 8 + 1, **f64)
         self._pass_scratch = None
@@ -357,8 +362,10 @@ class EpropClassifierTrainer:
         s.zbar_in = s.xbar_in = 0
         s.n_steps, s.slot_count = k, 2 * EPROP_BLOCK_STEPS
         # the learning signal is computed by sw_eprop_prep, directly in the
-        # e-prop pass's layout (the forward pass never reads it)
+        # e-prop pass's layout (the forward pass never reads it); the input
+        # spikes and traces come from sw_clf_inputs
         s.lsig = 0
+        s.in_bits, s.in_words = self.in_bits.data_ptr(), self._in_words
         return s
 
     def _slot(self, t: int) -> dict:
@@ -388,16 +395,16 @@ class EpropClassifierTrainer:
         tp.k = k
         for j in range(k):
             sl = self._slot(t0 + j)
-            pr.xbar[j], pr.zbar[j] = sl["xbar"].data_ptr(), sl["zbar"].data_ptr()
+            pr.xbar[j], pr.zbar[j] = 0, sl["zbar"].data_ptr()   # xbar_t: precomputed
             pr.psi[j], pr.d[j] = sl["psi"].data_ptr(), sl["d"].data_ptr()
             tp.psi_t[j], tp.lsig_t[j] = self.psi_t[j].data_ptr(), self.lsig_t[j].data_ptr()
         pr.w_out = self.w_out.data_ptr()
-        pr.xbar_t, pr.zbar_t = self.xbar_t.data_ptr(), self.zbar_t.data_ptr()
+        pr.xbar_t, pr.zbar_t = 0, self.zbar_t.data_ptr()
         pr.psi_t, pr.lsig_t = self.psi_t.data_ptr(), self.lsig_t.data_ptr()
         pr.g_w_out, pr.g_b_out = self.g_w_out.data_ptr(), self.g_b_out.data_ptr()
         pr.ro_partial = self._ro_partial.data_ptr()
         _lib.call("sw_eprop_prep", ctypes.byref(pr), st)
-        self._tsegs[0] = self.plan_in.tseg([self.xbar_t[j] for j in range(k)])
+        self._tsegs[0] = self.plan_in.tseg([self.xbar_all[t0 + j] for j in range(k)])
         self._tsegs[1] = self.plan_rec.tseg([self.zbar_t[j] for j in range(k)])
         tp.scratch = self._pass_scratch_ptr()
         _lib.call("sw_eprop_pass", ctypes.cast(self._tsegs, ctypes.c_void_p), 2, ctypes.byref(tp),
@@ -557,6 +564,13 @@ class EpropClassifierTrainer:
                       syn.planes["w"].data_ptr(), m.num_pre, m.stride, self._tw_stride[key], tw.data_ptr(), st)
         for x in [self.v, self.a, self.z, self.y, self.pi_sum, self.loss_b] + self._slot_zbar + self._slot_xbar:
             x.zero_()
+        ip = _lib.ClfInputs()
+        ip.steps, ip.batch, ip.ldb = self.task.example_steps, self.local_b, self.plan_in.ldb
+        ip.num_inputs, ip.words = self.task.num_inputs, self._in_words
+        ip.p_in, ip.ex_key = self.p_in.data_ptr(), self.keys.data_ptr()
+        ip.alpha = float(np.float32(self.params.alpha))
+        ip.xbar_t, ip.in_bits = self.xbar_all.data_ptr(), self.in_bits.data_ptr()
+        _lib.call("sw_clf_inputs", ctypes.byref(ip), st)
         if learn:
             for plan, syn in ((self.plan_in, self.s_in), (self.plan_rec, self.s_rec)):
                 plan.ensure(plan.m.edge_count())

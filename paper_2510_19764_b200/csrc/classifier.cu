@@ -537,7 +537,8 @@ size_t clf_smem_bytes(int H, int NI, int C, int scap, int rcap, bool compact) {
   return o + (size_t)(compact ? 2 : 5) * C * 8 + 16;   // yv, dv (+ ypre, pipre, bpre)
 }
 
-int clf_fwd_launch(const sw_clf_step_t* p, void* stream);   // classifier_fwd.cu
+int clf_fwd_launch(const sw_clf_step_t* p, void* stream);    // classifier_fwd.cu
+int clf_fwd2_launch(const sw_clf_step_t* p, void* stream);   // classifier_fwd2.cu
 
 extern "C" int sw_clf_step(const sw_clf_step_t* p, void* stream) {
   const int H = p->hidden, NI = p->num_inputs, C = p->num_classes;
@@ -552,6 +553,10 @@ extern "C" int sw_clf_step(const sw_clf_step_t* p, void* stream) {
     const char* e = getenv("SW_CLF_KERNEL");
     return e && e[0] == 's';
   }();
+  if (!legacy && p->in_bits && clf_fwd2_launch(p, stream) == SW_OK) {
+    SW_CHECK_LAUNCH("sw_clf_step");
+    return SW_OK;
+  }
   if (!legacy && clf_fwd_launch(p, stream) == SW_OK) {
     SW_CHECK_LAUNCH("sw_clf_step");
     return SW_OK;

@@ -29,8 +29,12 @@ namespace {
 // phase timestamps of block 7, step 3 (tools/fwd_phases.py); armed by sw_debug_fwd_prof
 __device__ long long g_fwd_prof[16];
 __device__ int g_fwd_prof_on;
+#ifdef SW_FWD_PROF
 #define FWD_PROF(i) do { if (g_fwd_prof_on && blockIdx.x == 7 && s == 3 && (threadIdx.x & 31) == 0) \
     g_fwd_prof[(i) + 8 * (threadIdx.x >= 32)] = clock64(); } while (0)
+#else
+#define FWD_PROF(i) do { } while (0)
+#endif
 
 constexpr int kT = 256;          // threads per replica block
 constexpr int kW = kT / 32;
@@ -45,8 +49,7 @@ __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.syn
 
 // row groups of the event-driven current sums (see P2b)
 __host__ __device__ inline int fwd_groups(int H) {
-  const int g = 4096 / H;
-  return g < 1 ? 1 : (g > kW ? kW : g);
+  return H <= 256 ? 8 : (H <= 512 ? 4 : 2);   // classifier_fwd2.cu fwd2_groups: the same groups
 }
 
 // bytes of the dynamic shared-memory layout
@@ -288,7 +291,7 @@ __global__ void __launch_bounds__(kT, 4) k_clf_fwd(sw_clf_step_t P) {
       const int rb = half == 0 ? 0 : nx, n = half == 0 ? nx : nz;
       if (warp < G) {
         float* pg = part + warp * H;
-        const int g0 = rb + (int)((int64_t)n * warp / G), g1 = rb + (int)((int64_t)n * (warp + 1) / G);
+        const int g0 = rb + n * warp / G, g1 = rb + n * (warp + 1) / G;
         for (int r = g0; r < g1; ++r) {
           const int x = list[r];
           const int len = rlen[x];

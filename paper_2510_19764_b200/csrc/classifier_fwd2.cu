@@ -1,0 +1,497 @@
+// The classifier's trial with the input side precomputed
+// (sparsewire/classifier.py:63-67, 196-234).
+//
+// The input spikes and the input traces xbar do not depend on the network
+// state, so one launch per batch (k_clf_inputs) draws every input spike of
+// the trial from the examples' counter streams (u = uniform01 #(t*NI + k) <
+// p_k, as the exact integer compare (h >> 11) < ceil(p_k * 2^53)) and runs
+// the xbar recursion: spike words in_bits[t][b][k/32] for the forward pass,
+// and xbar_t[t][k][b] already in the replica-minor layout the e-prop pass
+// reads (no transpose).
+//
+// The forward kernel (k_clf_fwd2, block per replica, a group of steps per
+// launch, state in registers) then only builds its spiking-row lists from
+// those words and the hidden spikes:
+//   A  hidden spikes -> ascending list (warp ballots, one barrier);
+//   B  warp 6 builds step t+1's input-row list from its spike words and
+//      issues its rows' bulk copies into the other staging buffer, so the
+//      copies of the next step land while this step computes;
+//   C  the ascending input rows and hidden rows are split into G ordered
+//      groups each (warp g sums group g of both into its partial rows: input
+//      rows from the staged copies, hidden rows straight from the packed
+//      rows); warp 7 then computes the readout and softmax;
+//   D  per post the group partials are added in group order, the ALIF step
+//      and the surrogate (neurons.py:60-73).
+// Every output is bit-identical to k_clf_fwd's (classifier_fwd.cu): the same
+// per-post current sums (groups of the ascending rows, group order), the same
+// readout / softmax / ALIF arithmetic.
+#include "common.cuh"
+#include "sm100_async.cuh"
+
+#include <cmath>
+#include <cstdlib>
+
+namespace {
+
+// phase timestamps of block 7, step 3 (tools/fwd_phases.py; sw_debug_fwd2_prof)
+// (compiled in with -DSW_FWD_PROF only)
+__device__ long long g_fwd2_prof[64];
+__device__ int g_fwd2_prof_on;
+#ifdef SW_FWD_PROF
+#define FWD2_PROF(i) do { if (g_fwd2_prof_on && blockIdx.x == 7 && s == 3 && (threadIdx.x & 31) == 0) \
+    g_fwd2_prof[(i) * 8 + (threadIdx.x >> 5)] = clock64(); } while (0)
+#else
+#define FWD2_PROF(i) do { } while (0)
+#endif
+
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// ------------------------------------------------------------- inputs ----
+// block = 32 replicas (lane) x 64 inputs (8 per warp), all T steps
+__global__ void __launch_bounds__(256) k_clf_inputs(const sw_clf_inputs_t P) {
+  __shared__ uint32_t s_bits[32][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = blockIdx.y * 32 + lane;
+  const int xb0 = blockIdx.x * 64, x0 = xb0 + warp * 8;
+  const int NI = P.num_inputs;
+  const bool bok = b < P.batch;
+  uint64_t thr[8];
+  float xb[8];
+  const uint64_t key = bok ? P.ex_key[b] : 0ull;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int x = x0 + j;
+    thr[j] = (bok && x < NI) ? (uint64_t)ceil(P.p_in[(int64_t)b * NI + x] * 0x1p53) : 0ull;
+    xb[j] = 0.0f;
+  }
+  const int64_t plane = (int64_t)NI * P.ldb;
+  for (int t = 0; t < P.steps; ++t) {
+    if (threadIdx.x < 64) s_bits[threadIdx.x >> 1][threadIdx.x & 1] = 0u;
+    __syncthreads();
+    unsigned f = 0;
+    const uint64_t c0 = (uint64_t)t * (uint64_t)NI + (uint64_t)x0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int x = x0 + j;
+      if (x < NI) {
+        const bool sp = bok && (sw::draw(key, c0 + j) >> 11) < thr[j];
+        xb[j] = __fadd_rn(__fmul_rn(xb[j], P.alpha), sp ? 1.0f : 0.0f);
+        if (b < P.ldb) P.xbar_t[t * plane + (int64_t)x * P.ldb + b] = bok ? xb[j] : 0.0f;
+        if (sp) f |= 1u << j;
+      }
+    }
+    if (f) atomicOr(&s_bits[lane][warp >> 2], f << ((warp & 3) * 8));
+    __syncthreads();
+    if (threadIdx.x < 64) {
+      const int bl = threadIdx.x >> 1, wd = threadIdx.x & 1;
+      const int bb = blockIdx.y * 32 + bl, word = xb0 / 32 + wd;
+      if (bb < P.batch && word < P.words)
+        P.in_bits[((int64_t)t * P.batch + bb) * P.words + word] = s_bits[bl][wd];
+    }
+  }
+}
+
+// ------------------------------------------------------------ forward ----
+// row groups of the current sums: 8 / (hidden units per thread)
+__host__ __device__ inline int fwd2_groups(int H) { return H <= 256 ? 8 : (H <= 512 ? 4 : 2); }
+
+__host__ __device__ inline size_t fwd2_fixed_bytes(int H, int NI, int C) {
+  const size_t NT = (size_t)NI + H;
+  size_t o = (size_t)2 * fwd2_groups(H) * H * 4;   // input / hidden partial rows
+  o += NT * 4;                                      // rlen
+  o += (size_t)2 * NI * 4 + (size_t)2 * (NI + 1) * 4;   // input lists, offsets (2 buffers)
+  o += (size_t)H * 4 + (size_t)(H + 1) * 4;         // hidden list, offsets (unused slots)
+  o = (o + 15) & ~(size_t)15;
+  o += (size_t)4 * C * 8;                           // y, pi_sum, d, b_out
+  o += 32;                                          // 2 mbarriers
+  o += (size_t)SW_EPROP_MAX_BLOCK * 2 * ((NI + 31) / 32) * 4;   // the launch's input spike words
+  return o;
+}
+
+// NTH threads per replica block (256, or 128 to leave room on the SM for a
+// concurrent e-prop pass); GT row groups (== fwd2_groups(H)), warp w sums
+// groups w, w + NTH/32, ... (the same numbers for any NTH)
+template <int NTH, int HPT, int GT>
+__global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, int stage) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int kT2 = NTH, kW2 = NTH / 32;
+  constexpr int G = GT;
+  const int H = P.hidden, NI = P.num_inputs, C = P.num_classes;
+  const int NT = NI + H;
+  size_t o = 0;
+  float* pin = (float*)(smem_raw + o);   o += (size_t)G * H * 4;
+  float* prc = (float*)(smem_raw + o);   o += (size_t)G * H * 4;
+  int* rlen = (int*)(smem_raw + o);      o += (size_t)NT * 4;
+  int* lin = (int*)(smem_raw + o);       o += (size_t)2 * NI * 4;        // [2][NI]
+  int* soin = (int*)(smem_raw + o);      o += (size_t)2 * (NI + 1) * 4;  // [2][NI + 1]
+  int* lh = (int*)(smem_raw + o);        o += (size_t)H * 4;
+  o += (size_t)(H + 1) * 4;
+  o = (o + 15) & ~(size_t)15;
+  double* yv = (double*)(smem_raw + o);
+  double* pis = yv + C;
+  double* dv = pis + C;
+  double* bo = dv + C;
+  o += (size_t)4 * C * 8;
+  uint64_t* sbar = (uint64_t*)(smem_raw + o); o += 32;
+  uint32_t* wsm = (uint32_t*)(smem_raw + o);   // [n_steps][in_words] spike words
+  o += (size_t)SW_EPROP_MAX_BLOCK * 2 * ((NI + 31) / 32) * 4;
+  int2* st = (int2*)(smem_raw + o);      // [2][stage]
+  __shared__ int s_wcnt[kW2];
+  __shared__ int s_nin[2], s_staged[2];
+  __shared__ double s_loss;
+
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bH = b * H, bC = b * C;
+  const int B = P.batch;
+  const int nslot = P.slot_count;
+  const int nsteps = P.n_steps;
+
+  for (int x = tid; x < NT; x += kT2)
+    rlen[x] = (x < NI) ? __ldg(P.in_row_length + x) : __ldg(P.rec_row_length + (x - NI));
+  for (int c = tid; c < C; c += kT2) {
+    yv[c] = P.y[bC + c];
+    pis[c] = P.pi_sum[bC + c];
+    bo[c] = P.b_out[c];
+  }
+  for (int x = tid; x < G * H; x += kT2) { pin[x] = 0.0f; prc[x] = 0.0f; }
+  if (tid == 0) {
+    s_loss = P.loss[b];
+    sw::mbar_init(&sbar[0], 1);
+    sw::mbar_init(&sbar[1], 1);
+    sw::fence_mbar_init();
+  }
+  const int prev = ((P.t - 1) % nslot + nslot) % nslot;
+  const float* zin0 = P.zbar + prev * B * H;
+  float v[HPT], a[HPT], z[HPT], zb[HPT];
+  const int h0 = tid * HPT;
+#pragma unroll
+  for (int j = 0; j < HPT; ++j) {
+    const int h = h0 + j;
+    const bool ok = h < H;
+    v[j] = ok ? P.v[bH + h] : 0.f;
+    a[j] = ok ? P.a[bH + h] : 0.f;
+    z[j] = ok ? P.z[bH + h] : 0.f;
+    zb[j] = ok ? zin0[bH + h] : 0.f;
+  }
+  const int label = P.labels[b];
+  const float alpha = P.alpha, rho = P.rho, beta = P.beta, v_thr = P.v_thr;
+  // the launch's input spike words (all its steps) into shared memory
+  for (int x = tid; x < nsteps * P.in_words; x += kT2) {
+    const int q = x / P.in_words, w = x - q * P.in_words;
+    wsm[x] = __ldg(P.in_bits + ((int64_t)(P.t + q) * B + b) * P.in_words + w);
+  }
+  __syncthreads();
+
+  // warp 6 (or the last warp): step t's input-row list from its spike words,
+  // staging offsets, bulk copies into buffer buf
+  const int pw = kW2 - 2;
+  auto build_inputs = [&](int t, int buf) {
+    const uint32_t* wds = wsm + (t - P.t) * P.in_words;
+    int* L = lin + buf * NI;
+    int* O = soin + buf * (NI + 1);
+    int n = 0;
+    for (int w0 = 0; w0 < P.in_words; w0 += 32) {
+      const uint32_t wd = (w0 + lane < P.in_words) ? wds[w0 + lane] : 0u;
+      const int c = __popc(wd);
+      int inc = c;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int u = __shfl_up_sync(SW_FULL_MASK, inc, d);
+        if (lane >= d) inc += u;
+      }
+      int p = n + inc - c;
+      for (uint32_t m = wd; m; m &= m - 1) L[p++] = (w0 + lane) * 32 + __ffs(m) - 1;
+      n += __shfl_sync(SW_FULL_MASK, inc, 31);
+    }
+    __syncwarp();
+    // staging offsets: padded row lengths, ascending
+    int off = 0;
+    for (int q0 = 0; q0 < n; q0 += 32) {
+      const int q = q0 + lane;
+      const int len = q < n ? ((rlen[L[q]] + 1) & ~1) : 0;
+      int inc = len;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int u = __shfl_up_sync(SW_FULL_MASK, inc, d);
+        if (lane >= d) inc += u;
+      }
+      if (q < n) O[q] = off + inc - len;
+      off += __shfl_sync(SW_FULL_MASK, inc, 31);
+    }
+    const bool staged = off <= stage;
+    if (lane == 0) {
+      O[n] = off;
+      s_nin[buf] = n;
+      s_staged[buf] = staged ? 1 : 0;
+    }
+    __syncwarp();
+    if (lane == 0 && staged) sw::mbar_arrive_expect_tx(&sbar[buf], (uint32_t)off * 8u);
+    __syncwarp();
+    if (staged) {
+      // one bulk copy per row (16-byte multiples: rows padded to even entries)
+      int2* S = st + buf * stage;
+      for (int q = lane; q < n; q += 32) {
+        const int x = L[q];
+        const uint32_t bytes = (uint32_t)((rlen[x] + 1) & ~1) * 8u;
+        if (bytes) sw::bulk_g2s(S + O[q], P.in_tw + (int64_t)x * P.in_tw_stride * 2, bytes, &sbar[buf]);
+      }
+    }
+  };
+  if (warp == pw) build_inputs(P.t, 0);
+  __syncthreads();
+  uint32_t phase = 0;   // bit buf: completed-phase parity of sbar[buf]
+
+  for (int s = 0; s < nsteps; ++s) {
+    const int t = P.t + s;
+    const int cb = s & 1;
+    const int cur = t % nslot;
+    float* zbar_o = P.zbar + cur * B * H;
+    float* psi_o = P.psi + cur * B * H;
+    double* d_o = P.d + cur * B * C;
+
+    FWD2_PROF(0);
+    // ---- A: hidden spikes -> ascending list ----
+    unsigned hm[HPT];
+    int hc = 0;
+#pragma unroll
+    for (int j = 0; j < HPT; ++j) {
+      hm[j] = __ballot_sync(SW_FULL_MASK, (h0 + j < H) && z[j] != 0.0f);
+      hc += __popc(hm[j]);
+    }
+    if (lane == 0) s_wcnt[warp] = hc;
+    __syncthreads();   // B1
+    FWD2_PROF(1);
+    int hbase = 0, nh = 0;
+#pragma unroll
+    for (int w = 0; w < kW2; ++w) {
+      const int c = s_wcnt[w];
+      if (w < warp) hbase += c;
+      nh += c;
+    }
+    {
+      // this thread's units in ascending order: lanes before it contribute
+      // all their units, earlier j of this lane come first
+      int p = hbase;
+#pragma unroll
+      for (int j = 0; j < HPT; ++j) p += __popc(hm[j] & sw::lanemask_lt());
+#pragma unroll
+      for (int j = 0; j < HPT; ++j)
+        if ((hm[j] >> lane) & 1u) lh[p++] = h0 + j;
+    }
+    // ---- B: next step's input rows, staged while this step computes ----
+    if (warp == pw && s + 1 < nsteps) build_inputs(t + 1, cb ^ 1);
+    // zbar (old z) for the e-prop traces and the readout gradient
+#pragma unroll
+    for (int j = 0; j < HPT; ++j) {
+      const int h = h0 + j;
+      if (h < H) {
+        zb[j] = __fadd_rn(__fmul_rn(zb[j], alpha), z[j]);
+        zbar_o[bH + h] = zb[j];
+      }
+    }
+    FWD2_PROF(2);
+    __syncthreads();   // B2: hidden list (and the next buffer's list) written
+    FWD2_PROF(3);
+
+    // ---- C: ordered group sums of the input rows and the hidden rows ----
+    const int nin = s_nin[cb];
+    const bool staged = s_staged[cb] != 0;
+    if (staged) {
+      sw::mbar_wait(&sbar[cb], (phase >> cb) & 1u);
+      phase ^= 1u << cb;
+    }
+    FWD2_PROF(4);
+    for (int grp = warp; grp < G; grp += kW2) {
+      const int* L = lin + cb * NI;
+      const int* O = soin + cb * (NI + 1);
+      const int2* S = st + cb * stage;
+      float* pg = pin + grp * H;
+      const int g0 = nin * grp / G, g1 = nin * (grp + 1) / G;
+      for (int r = g0; r < g1; ++r) {
+        const int x = L[r];
+        const int len = rlen[x];
+        const int2* e = staged ? S + O[r] : reinterpret_cast<const int2*>(P.in_tw + (int64_t)x * P.in_tw_stride * 2);
+        for (int q = lane; q < len; q += 32) {
+          const int2 tw = staged ? e[q] : __ldg(e + q);
+          pg[tw.x] = __fadd_rn(pg[tw.x], __int_as_float(tw.y));
+        }
+        __syncwarp();
+      }
+      float* pr = prc + grp * H;
+      const int k0 = nh * grp / G, k1 = nh * (grp + 1) / G;
+      for (int r = k0; r < k1; ++r) {
+        const int h = lh[r];
+        const int len = rlen[NI + h];
+        const int2* e = reinterpret_cast<const int2*>(P.rec_tw + (int64_t)h * P.rec_tw_stride * 2);
+        for (int q = lane; q < len; q += 32) {
+          const int2 tw = __ldg(e + q);
+          pr[tw.x] = __fadd_rn(pr[tw.x], __int_as_float(tw.y));
+        }
+        __syncwarp();
+      }
+    }
+    if (warp == kW2 - 1) {
+      // readout y = alpha*y + z @ W_out^T + b (classifier.py:215), lane = class,
+      // spiking units ascending; softmax / cross-entropy / d (plasticity.py:156-165)
+      for (int c0 = 0; c0 < C; c0 += 32) {
+        const int c = c0 + lane;
+        if (c < C) {
+          double sacc = 0.0;
+          const double* wr = P.w_out + (int64_t)c * H;
+          // 8 independent loads in flight, then the ordered adds
+          for (int q0 = 0; q0 < nh; q0 += 8) {
+            double wv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) wv[u] = q0 + u < nh ? __ldg(wr + lh[q0 + u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (q0 + u < nh) sacc = __dadd_rn(sacc, wv[u]);
+          }
+          yv[c] = __dadd_rn(__dadd_rn(__dmul_rn(P.alpha64, yv[c]), sacc), bo[c]);
+        }
+      }
+      __syncwarp();
+      double mx = -INFINITY;
+      for (int c = lane; c < C; c += 32) mx = fmax(mx, yv[c]);
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) mx = fmax(mx, __shfl_xor_sync(SW_FULL_MASK, mx, o2));
+      double se = 0.0;
+      double ex[2] = {0.0, 0.0};
+      for (int c = lane, u = 0; c < C; c += 32, ++u) {
+        const double e = exp(yv[c] - mx);
+        if (u < 2) ex[u] = e;
+        se += e;
+      }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) se += __shfl_xor_sync(SW_FULL_MASK, se, o2);
+      for (int c = lane, u = 0; c < C; c += 32, ++u) {
+        const double pi = (u < 2 ? ex[u] : exp(yv[c] - mx)) / se;
+        pis[c] = pis[c] + pi;
+        const double dd = pi - (c == label ? 1.0 : 0.0);
+        dv[c] = dd;
+        d_o[bC + c] = dd;
+        if (c == label) s_loss = s_loss + -log(pi);
+      }
+    }
+    FWD2_PROF(5);
+    __syncthreads();   // B3: partial rows complete
+    FWD2_PROF(6);
+
+    // ---- D: group partials in order, ALIF step, surrogate ----
+#pragma unroll
+    for (int j = 0; j < HPT; ++j) {
+      const int h = h0 + j;
+      if (h >= H) continue;
+      float ae = pin[h], ar = prc[h];
+      pin[h] = 0.0f;
+      prc[h] = 0.0f;
+      for (int g = 1; g < G; ++g) {
+        ae = __fadd_rn(ae, pin[g * H + h]);
+        ar = __fadd_rn(ar, prc[g * H + h]);
+        pin[g * H + h] = 0.0f;
+        prc[g * H + h] = 0.0f;
+      }
+      const float thr_o = __fadd_rn(v_thr, __fmul_rn(beta, a[j]));
+      const float cc = __fdiv_rn(__fsub_rn(v[j], thr_o), v_thr);
+      const float r = __fsub_rn(1.0f, fabsf(cc));
+      psi_o[bH + h] = __fmul_rn(0.5f, (r > 0.0f || r != r) ? r : 0.0f);
+      float vv = __fmul_rn(alpha, __fsub_rn(v[j], __fmul_rn(z[j], v_thr)));
+      vv = __fadd_rn(__fadd_rn(vv, ar), ae);
+      const float aa = __fadd_rn(__fmul_rn(rho, a[j]), z[j]);
+      v[j] = vv;
+      a[j] = aa;
+      z[j] = (vv >= __fadd_rn(v_thr, __fmul_rn(beta, aa))) ? 1.0f : 0.0f;
+    }
+    FWD2_PROF(7);
+    // the next step's list writes happen after its B1, which every thread
+    // reaches only after finishing this step
+  }
+
+#pragma unroll
+  for (int j = 0; j < HPT; ++j) {
+    const int h = h0 + j;
+    if (h < H) {
+      P.v[bH + h] = v[j];
+      P.a[bH + h] = a[j];
+      P.z[bH + h] = z[j];
+    }
+  }
+  __syncthreads();
+  for (int c = tid; c < C; c += kT2) {
+    P.y[bC + c] = yv[c];
+    P.pi_sum[bC + c] = pis[c];
+  }
+  if (tid == 0) P.loss[b] = s_loss;
+}
+
+template <int NTH, int HPT, int GT>
+int launch_fwd2(const sw_clf_step_t* p, size_t smem, int stage, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute((const void*)k_clf_fwd2<NTH, HPT, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr = true;
+  }
+  k_clf_fwd2<NTH, HPT, GT><<<p->batch, NTH, smem, st>>>(*p, stage);
+  sw::count_launch();
+  return SW_OK;
+}
+
+}  // namespace
+
+extern "C" __attribute__((visibility("default"))) int sw_debug_fwd2_prof(int enable, long long* out16) {
+  if (out16 && cudaMemcpyFromSymbol(out16, g_fwd2_prof, 64 * sizeof(long long)) != cudaSuccess) return SW_ERR_CUDA;
+  return cudaMemcpyToSymbol(g_fwd2_prof_on, &enable, sizeof(int)) == cudaSuccess ? 0 : SW_ERR_CUDA;
+}
+
+extern "C" int sw_clf_inputs(const sw_clf_inputs_t* p, void* stream) {
+  if (!p || p->batch < 1 || p->ldb < p->batch || p->num_inputs < 1 || p->steps < 0 ||
+      p->words != (p->num_inputs + 31) / 32) {
+    sw::set_last_error("sw_clf_inputs: bad shapes (ldb >= batch, words = ceil(num_inputs / 32))");
+    return SW_ERR_INVALID_ARG;
+  }
+  if (p->steps == 0) return SW_OK;
+  dim3 grid((p->num_inputs + 63) / 64, (p->ldb + 31) / 32);
+  k_clf_inputs<<<grid, 256, 0, (cudaStream_t)stream>>>(*p);
+  sw::count_launch();
+  SW_CHECK_LAUNCH("sw_clf_inputs");
+  return SW_OK;
+}
+
+// the grouped forward with precomputed inputs (sw_clf_step with in_bits);
+// SW_ERR_INVALID_ARG when the shapes are outside its layout
+int clf_fwd2_launch(const sw_clf_step_t* p, void* stream) {
+  const int H = p->hidden, NI = p->num_inputs, C = p->num_classes;
+  if (p->n_steps < 1 || p->n_steps > 2 * SW_EPROP_MAX_BLOCK || !p->in_bits || !p->in_tw || !p->rec_tw || H < 1 || H > 1024 || NI < 1 || C < 1 ||
+      p->in_words != (NI + 31) / 32)
+    return SW_ERR_INVALID_ARG;
+  const size_t fixed = fwd2_fixed_bytes(H, NI, C);
+  // threads per replica block: 256, or 128 (SW_FWD_THREADS=128) to leave
+  // registers and shared memory for a concurrent e-prop pass
+  static const int nth = [] {
+    const char* e = getenv("SW_FWD_THREADS");
+    return (e && atoi(e) == 128) ? 128 : 256;
+  }();
+  const int per_sm = 1024 / nth;
+  // staged input entries per buffer: what keeps per_sm blocks per SM
+  const size_t budget = (size_t)(nth == 128 ? 50 : 56) * 1024;
+  int stage = 2048;
+  while (stage > 256 && fixed + (size_t)stage * 16 > budget) stage -= 128;
+  const size_t smem = fixed + (size_t)stage * 16;
+  if (smem > 200 * 1024) return SW_ERR_INVALID_ARG;
+  (void)per_sm;
+  const int G = fwd2_groups(H);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (nth == 128 && H <= 256) return launch_fwd2<128, 2, 8>(p, smem, stage, st);
+  if (nth == 128 && H <= 512) return launch_fwd2<128, 4, 4>(p, smem, stage, st);
+  if (G == 8) return launch_fwd2<256, 1, 8>(p, smem, stage, st);
+  if (G == 4) return launch_fwd2<256, 2, 4>(p, smem, stage, st);
+  return launch_fwd2<256, 4, 2>(p, smem, stage, st);
+}

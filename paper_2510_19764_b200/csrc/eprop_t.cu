@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(256) k_prep(const sw_eprop_prep_t P) {
   };
   const int nht = gridDim.x;
   const int xper = (NI + nht - 1) / nht, x0 = min(NI, ht * xper), x1 = min(NI, x0 + xper);
-  for (int r0 = x0; r0 < x1; r0 += kHT) {
+  for (int r0 = x0; P.xbar[k] && r0 < x1; r0 += kHT) {   // NULL: xbar_t precomputed (sw_clf_inputs)
     load_tile(P.xbar[k], NI, r0, min(kHT, x1 - r0));
     __syncthreads();
     store_tile(r0, min(kHT, x1 - r0), P.xbar_t + (int64_t)k * NI * L);

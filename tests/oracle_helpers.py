@@ -64,10 +64,10 @@ def check_topomap_post(fx, k, name, row_length, target, g):
     assert valid_equal(rl, g, fx[f"u{k}_post_{name}_g"]), (k, name)
 
 
-def fwd_groups(H: int, warps: int = 8) -> int:
-    """Row groups of the forward kernel's event-driven current sums
-    (classifier_fwd.cu fwd_groups)."""
-    return max(1, min(warps, 4096 // H))
+def fwd_groups(H: int) -> int:
+    """Row groups of the forward kernels' event-driven current sums
+    (classifier_fwd.cu fwd_groups, classifier_fwd2.cu fwd2_groups)."""
+    return 8 if H <= 256 else (4 if H <= 512 else 2)
 
 
 def grouped_currents(rl, tg, w32, spiking, H):

@@ -166,8 +166,10 @@ def test_trainer_at_bench_config_matches_oracle(dev_lib, cfg):
     for t in range(T):
         sl = {k: v.cpu().numpy() for k, v in tr._slot(t).items()}
         for k in sl:
-            if k != "lsig":   # the grouped path computes it in sw_eprop_prep (below)
+            if k not in ("lsig", "xbar"):   # grouped path: sw_eprop_prep / sw_clf_inputs (below)
                 assert np.array_equal(sl[k], snaps[t][k]), (t, k)
+        # the precomputed input traces (sw_clf_inputs), replica-minor
+        assert np.array_equal(tr.xbar_all[t, :, :B].cpu().numpy().T, snaps[t]["xbar"]), t
     # the last group's replica-minor e-prop inputs (sw_eprop_prep) == the
     # single-step forward's own slots, learning signal included
     K = EPROP_BLOCK_STEPS
@@ -176,7 +178,7 @@ def test_trainer_at_bench_config_matches_oracle(dev_lib, cfg):
         assert np.array_equal(tr.lsig_t[j, :, :B].cpu().numpy().T, s["lsig"]), j
         assert np.array_equal(tr.psi_t[j, :, :B].cpu().numpy().T, s["psi"]), j
         assert np.array_equal(tr.zbar_t[j, :, :B].cpu().numpy().T, s["zbar"]), j
-        assert np.array_equal(tr.xbar_t[j, :, :B].cpu().numpy().T, s["xbar"]), j
+
     assert np.array_equal(tr.v.cpu().numpy(), prev["v"]) and np.array_equal(tr.z.cpu().numpy(), prev["z"])
     assert float(tr.loss_b.sum()) == loss_d
 

@@ -282,9 +282,13 @@ def test_grouped_forward_equals_single_steps(dev_lib):
     a, b = tr
     for name in ("v", "a", "z", "y", "pi_sum", "loss_b"):
         assert torch.equal(getattr(a, name), getattr(b, name)), name
-    # (the grouped launch leaves the learning signal to sw_eprop_prep)
-    for name in ("_slots_zbar", "_slots_xbar", "_slots_psi", "_slots_d"):
+    # (the grouped launch leaves the learning signal to sw_eprop_prep and
+    # takes its input spikes / traces from sw_clf_inputs)
+    for name in ("_slots_zbar", "_slots_psi", "_slots_d"):
         assert torch.equal(getattr(a, name), getattr(b, name)), name
+    K2 = 2 * EPROP_BLOCK_STEPS
+    for t in range(T):
+        assert torch.equal(a._slots_xbar[t % K2].T, b.xbar_all[t, :, :a.local_b]) or t < T - K2, t
 
 
 @pytest.mark.parametrize("NI,H,din,drec,p_spk,z_spk", [

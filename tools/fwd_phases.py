@@ -1,4 +1,4 @@
-"""Phase timestamps (clock64) of one forward block (block 7, step 3 of a
+"""(Build with SW_NVCC_EXTRA=-DSW_FWD_PROF.)  Phase timestamps (clock64) of one forward block (block 7, step 3 of a
 launch) mid-trial: warp 0 (lane 0) and warp 1.  Usage: python tools/fwd_phases.py [c1|c2]"""
 import ctypes
 import os
@@ -19,21 +19,25 @@ tr._upload_batch(task.train_ids(0, 512))
 tr._prepare(False)
 L = _lib.lib()
 L.sw_debug_fwd_prof.argtypes = [ctypes.c_int, ctypes.c_void_p]
+L.sw_debug_fwd2_prof.argtypes = [ctypes.c_int, ctypes.c_void_p]
+# grouped launches with precomputed inputs run k_clf_fwd2
+prof = L.sw_debug_fwd2_prof
+tr._prepare(False)
 st = _lib.stream_ptr()
 for t0 in range(0, 400, 8):
     _lib.call("sw_clf_step", ctypes.byref(tr._group_params(t0, 8)), st)
 torch.cuda.synchronize()
-names = ["step start", "lists ready (B1b)", "staging landed", "input currents", "recurrent currents", "step end"]
+names = ["start", "B1", "work>B2", "B2", "landed", "work>B3", "B3", "end"]
 acc = {}
 for rep in range(10):
-    L.sw_debug_fwd_prof(1, None)
+    prof(1, None)
     _lib.call("sw_clf_step", ctypes.byref(tr._group_params(400 + 8 * rep, 8)), st)
     torch.cuda.synchronize()
-    out = (ctypes.c_longlong * 16)()
-    L.sw_debug_fwd_prof(0, out)
-    for w in range(2):
-        t = [out[i + 8 * w] for i in range(6)]
-        for i in range(1, 6):
-            acc.setdefault((w, i), []).append(t[i] - t[0])
-for w in range(2):
-    print(f"warp {w}: " + ", ".join(f"{names[i]} {sum(acc[(w, i)]) / len(acc[(w, i)]):.0f}" for i in range(1, 6)))
+    out = (ctypes.c_longlong * 64)()
+    prof(0, out)
+    t0 = min(out[w] for w in range(8))
+    for i in range(8):
+        for w in range(8):
+            acc.setdefault((i, w), []).append(out[i * 8 + w] - t0)
+for i in range(8):
+    print(f"{names[i]:9s} " + " ".join(f"{sum(acc[(i, w)]) / len(acc[(i, w)]):7.0f}" for w in range(8)))
