@@ -227,6 +227,8 @@ struct TPass {
   double* partial;       // [tiles][splits][8]
   int ldb, splits, chunks_per_split;
   float beta, rho, alpha;
+  unsigned long long nz;   // (-0.0f, -0.0f)
+  int dbg;   // measurement only (SW_EPT_DBG): 1 = every synapse reads pre/post 0 (L1-resident inputs), 2 = no state traffic
 };
 
 // packed float32x2 helpers (add/sub/mul .rn.f32x2, sm_100)
@@ -252,6 +254,25 @@ __device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigne
   unsigned long long r;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
+}
+
+// products as fma(a, b, nz) with nz = (-0, -0) from a kernel argument: the
+// exact product rounded once (fma with a -0 addend), which ptxas cannot
+// contract into a following packed add (it does contract mul.rn.f32x2)
+__device__ __forceinline__ unsigned long long pmul2(unsigned long long a, unsigned long long b, unsigned long long nz) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(nz));
+  return r;
+}
+__device__ __forceinline__ void ld256p(unsigned long long (&v)[4], const float* p) {
+  asm("ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%4];" : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void ld256p_cs(unsigned long long (&v)[4], const float* p) {
+  asm("ld.global.cs.v4.b64 {%0,%1,%2,%3}, [%4];" : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void st256p_cs(float* p, const unsigned long long (&v)[4]) {
+  asm volatile("st.global.cs.v4.b64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(v[0]), "l"(v[1]), "l"(v[2]), "l"(v[3])
+               : "memory");
 }
 
 __device__ __forceinline__ void ld256(float (&v)[8], const float* p) {
@@ -295,76 +316,84 @@ __global__ void __launch_bounds__(kTW * 32, MB) k_eprop_t(const TPass T) {
   const int items = tiles * T.splits;
   const int nchunk = T.ldb / 32;
   const int64_t L = T.ldb;
-  // static round-robin over the uniform work items (no ticket atomics)
-  const int nwarps = gridDim.x * (blockDim.x >> 5);
-  for (int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < items; item += nwarps) {
+  // static assignment of the uniform work items (no ticket atomics): block b
+  // owns the contiguous item range [b*items/nb, (b+1)*items/nb) and its warps
+  // stride through it, so the warps of a block work on neighbouring tiles of
+  // one replica split at a time (their trace / psi / lsig lines are shared
+  // in L1 when the plan orders tiles by pre block)
+  const int nwb = blockDim.x >> 5;
+  const int i0 = (int)((int64_t)items * blockIdx.x / gridDim.x), i1 = (int)((int64_t)items * (blockIdx.x + 1) / gridDim.x);
+  for (int item = i0 + (threadIdx.x >> 5); item < i1; item += nwb) {
     // split-major item order: the warps working at any moment share replica ranges
     const int split = item / tiles, tile = item - split * tiles;
     const bool first = tile < tiles0;
     const TSeg& S = first ? T.s[0] : T.s[1];
     const int lt = first ? tile : tile - tiles0;
     const int e = lt * 8 + sl;
-    const int pre = __ldg(S.pre + e), post = __ldg(S.post + e);
+    int pre = __ldg(S.pre + e), post = __ldg(S.post + e);
+    if (T.dbg == 1) pre = post = 0;
     const int c0 = split * T.chunks_per_split, c1 = min(nchunk, c0 + T.chunks_per_split);
     const int64_t tofs = (int64_t)pre * L + g * 8, pofs = (int64_t)post * L + g * 8;
+    const unsigned long long B2 = pk2(T.beta, T.beta), A2 = pk2(T.alpha, T.alpha), R2 = pk2(T.rho, T.rho);
+    const unsigned long long NZ = T.nz;
     double acc = 0.0;
-    float ep[8], eb[8];
+    // state and inputs as packed replica pairs (4 x f32x2 per lane)
+    unsigned long long ep[4], eb[4];
     const int64_t so0 = (((int64_t)lt * nchunk + c0) * 32 + lane) * 8;
-    ld256_cs(ep, S.eps + so0);
-    ld256_cs(eb, S.ebar + so0);
+    if (T.dbg == 2) {
+      for (int r = 0; r < 4; ++r) ep[r] = eb[r] = 0ull;
+    } else {
+      ld256p_cs(ep, S.eps + so0);
+      ld256p_cs(eb, S.ebar + so0);
+    }
     for (int c = c0; c < c1; ++c) {
       const int b0 = c * 32;
       const int64_t so = (((int64_t)lt * nchunk + c) * 32 + lane) * 8;
-      float zin[K][8], pin[K][8], lin[K][8];
+      unsigned long long zin[K][4], pin[K][4], lin[K][4];
 #pragma unroll
       for (int k = 0; k < PD && k < K; ++k) {
-        ld256(zin[k], S.trace[k] + tofs + b0);
-        ld256(pin[k], T.psi[k] + pofs + b0);
-        ld256(lin[k], T.lsig[k] + pofs + b0);
+        ld256p(zin[k], S.trace[k] + tofs + b0);
+        ld256p(pin[k], T.psi[k] + pofs + b0);
+        ld256p(lin[k], T.lsig[k] + pofs + b0);
       }
-      float nep[8], neb[8];
+      unsigned long long nep[4], neb[4];
       if (SP && c + 1 < c1) {
-        ld256_cs(nep, S.eps + so + 32 * 8);
-        ld256_cs(neb, S.ebar + so + 32 * 8);
+        ld256p_cs(nep, S.eps + so + 32 * 8);
+        ld256p_cs(neb, S.ebar + so + 32 * 8);
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         if (k + PD < K) {
-          ld256(zin[k + PD], S.trace[k + PD] + tofs + b0);
-          ld256(pin[k + PD], T.psi[k + PD] + pofs + b0);
-          ld256(lin[k + PD], T.lsig[k + PD] + pofs + b0);
+          ld256p(zin[k + PD], S.trace[k + PD] + tofs + b0);
+          ld256p(pin[k + PD], T.psi[k + PD] + pofs + b0);
+          ld256p(lin[k + PD], T.lsig[k + PD] + pofs + b0);
         }
-        // replicas in pairs: the subtract, the two adds and the gradient-term
-        // product as packed f32x2 ops (FADD2 / FMUL2: two separately rounded
-        // IEEE ops); the products that feed an add stay scalar (ptxas would
-        // contract a packed multiply feeding a packed add into FFMA2)
+        // _kernels.py:33-38 on replica pairs, every op a separately rounded
+        // packed f32x2 op: e = psi*(zb - beta*eps); ebar = alpha*ebar + e;
+        // grad += f64(lsig*ebar); eps = rho*eps + e
 #pragma unroll
-        for (int r = 0; r < 8; r += 2) {
-          const unsigned long long x =
-              sub2(pk2(zin[k][r], zin[k][r + 1]), pk2(__fmul_rn(T.beta, ep[r]), __fmul_rn(T.beta, ep[r + 1])));
-          float x0, x1;
-          up2(x, x0, x1);
-          const float e0 = __fmul_rn(pin[k][r], x0), e1 = __fmul_rn(pin[k][r + 1], x1);
-          const unsigned long long ee = pk2(e0, e1);
-          const unsigned long long ebn = add2(pk2(__fmul_rn(T.alpha, eb[r]), __fmul_rn(T.alpha, eb[r + 1])), ee);
-          const unsigned long long epn = add2(pk2(__fmul_rn(T.rho, ep[r]), __fmul_rn(T.rho, ep[r + 1])), ee);
+        for (int r = 0; r < 4; ++r) {
+          const unsigned long long x = sub2(zin[k][r], pmul2(B2, ep[r], NZ));
+          const unsigned long long ee = pmul2(pin[k][r], x, NZ);
+          eb[r] = add2(pmul2(A2, eb[r], NZ), ee);
           float t0, t1;
-          up2(mul2(pk2(lin[k][r], lin[k][r + 1]), ebn), t0, t1);
+          up2(mul2(lin[k][r], eb[r]), t0, t1);
           acc = __dadd_rn(acc, (double)t0);
           acc = __dadd_rn(acc, (double)t1);
-          up2(ebn, eb[r], eb[r + 1]);
-          up2(epn, ep[r], ep[r + 1]);
+          ep[r] = add2(pmul2(R2, ep[r], NZ), ee);
         }
       }
-      st256_cs(S.eps + so, ep);
-      st256_cs(S.ebar + so, eb);
-      if (c + 1 < c1) {
+      if (T.dbg != 2) {
+        st256p_cs(S.eps + so, ep);
+        st256p_cs(S.ebar + so, eb);
+      }
+      if (c + 1 < c1 && T.dbg != 2) {
         if (SP) {
 #pragma unroll
-          for (int r = 0; r < 8; ++r) { ep[r] = nep[r]; eb[r] = neb[r]; }
+          for (int r = 0; r < 4; ++r) { ep[r] = nep[r]; eb[r] = neb[r]; }
         } else {
-          ld256_cs(ep, S.eps + so + 32 * 8);
-          ld256_cs(eb, S.ebar + so + 32 * 8);
+          ld256p_cs(ep, S.eps + so + 32 * 8);
+          ld256p_cs(eb, S.ebar + so + 32 * 8);
         }
       }
     }
@@ -598,6 +627,11 @@ extern "C" int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const 
   T.beta = beta;
   T.rho = rho;
   T.alpha = alpha;
+  T.nz = 0x8000000080000000ull;
+  {
+    static const int dbg = [] { const char* e = getenv("SW_EPT_DBG"); return e ? atoi(e) : 0; }();
+    T.dbg = dbg;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   // variant (SW_EPT_CFG = "PD,SP,MB" for measurement): inputs PD steps
   // ahead, next-chunk state prefetch SP, MB blocks per SM
