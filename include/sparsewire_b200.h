@@ -444,6 +444,12 @@ SW_API int sw_transpose_rebuild_coop(const sw_ragged_t* m, int32_t* col_length, 
                                      int32_t* src_pre, int32_t* src_slot, int32_t* cursor,
                                      int32_t* max_len, const int32_t* changed,
                                      int32_t* block_scratch, int32_t slack, void* stream);
+/* sw_transpose_rebuild_coop gated by a flag the call also resets
+ * (clear_changed != 0): the patch path's "overflowed, rebuild" flag. */
+SW_API int sw_transpose_rebuild_gated(const sw_ragged_t* m, int32_t* col_length, int32_t* col_ptr,
+                                      int32_t* src_pre, int32_t* src_slot, int32_t* cursor,
+                                      int32_t* max_len, int32_t* changed, int32_t* block_scratch,
+                                      int32_t slack, int32_t clear_changed, void* stream);
 /* Incremental remap (connectivity.py:173-192 applied to one update's
  * changes instead of the whole matrix).  patch_log (device int32, written by
  * the mutating kernel, e.g. sw_rewire_update with prm->patch_log):

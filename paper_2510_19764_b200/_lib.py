@@ -182,6 +182,7 @@ SIGNATURES: dict[str, list] = {
     "sw_transpose_rebuild": [RP, P, P, P, P, P, P, P, I32, P],
     "sw_transpose_rebuild_coop": [RP, P, P, P, P, P, P, P, P, I32, P],
     "sw_transpose_patch": [RP, P, P, P, P, P, I32, P, P, P],
+    "sw_transpose_rebuild_gated": [RP, P, P, P, P, P, P, P, P, I32, I32, P],
     "sw_transpose_patch_scratch_bytes": [I32, I32],
     "sw_propagate_atomic": [P, P, P, I32, I32, I32, P, P, I32, P, P, I64, P],
     "sw_propagate_ordered": [P, I32, I32, P, I32, P],

@@ -24,6 +24,13 @@
 namespace cg = cooperative_groups;
 
 namespace {
+// grid barrier; a single-block launch (small sheets: no cooperative launch,
+// whose set-up costs more than the work) uses the block barrier
+__device__ __forceinline__ void gsync(cg::grid_group& grid) {
+  if (gridDim.x == 1) __syncthreads();
+  else grid.sync();
+}
+
 
 constexpr int kKMax = 64;   // attempts per row handled by one thread
 constexpr int kTotals = 16;  // totals[] words: see sw_rewire_update
@@ -349,7 +356,7 @@ k_rw_fused(RwArgs A, uint64_t host_prefix, uint64_t row_prefix, int32_t rule_id,
     *A.changed = 0;
     *rej = 0;
   }
-  grid.sync();
+  gsync(grid);
   if (gt == 0) *update_count = (int64_t)u + 1;
   const uint64_t rem = sw::reject_rem(P);
   const bool pow2 = (P & (P - 1)) == 0;
@@ -360,7 +367,7 @@ k_rw_fused(RwArgs A, uint64_t host_prefix, uint64_t row_prefix, int32_t rule_id,
     else ++r;
   }
   if (r) atomicAdd((unsigned long long*)rej, (unsigned long long)r);
-  grid.sync();
+  gsync(grid);
   if (gt == 0 && *rej) {
     // rejected draws (probability < P / 2^64): continue the stream serially
     int64_t need = *rej;
@@ -370,7 +377,7 @@ k_rw_fused(RwArgs A, uint64_t host_prefix, uint64_t row_prefix, int32_t rule_id,
       if (sw::draw_valid(h, rem)) { attempts[h % P] += 1; --need; }
     }
   }
-  if (rem != 0) grid.sync();
+  if (rem != 0) gsync(grid);
   rw_rows(A, gt, gn);
   rw_heavy_tail(A);
 }
@@ -423,7 +430,12 @@ extern "C" int sw_rewire_update(const sw_ragged_t* m, int32_t weight_plane, cons
     int64_t ta = prm->total_attempts;
     void* args[] = {(void*)&A, (void*)&hp, (void*)&rp, (void*)&rid, (void*)&update_count, (void*)&keys,
                     (void*)&attempts, (void*)&ta, (void*)&rej};
-    cudaLaunchCooperativeKernel((const void*)k_rw_fused, dim3(blocks), dim3(256), args, 0, st);
+    if (P <= 256) {
+      // small sheets: one block, block barriers, an ordinary launch
+      k_rw_fused<<<1, 256, 0, st>>>(A, hp, rp, rid, update_count, keys, attempts, ta, rej);
+    } else {
+      cudaLaunchCooperativeKernel((const void*)k_rw_fused, dim3(blocks), dim3(256), args, 0, st);
+    }
     sw::count_launch();
     SW_CHECK_LAUNCH("sw_rewire_update");
     return SW_OK;

@@ -14,6 +14,13 @@
 namespace cg = cooperative_groups;
 
 namespace {
+// grid barrier; a single-block launch (small sheets: no cooperative launch,
+// whose set-up costs more than the work) uses the block barrier
+__device__ __forceinline__ void gsync(cg::grid_group& grid) {
+  if (gridDim.x == 1) __syncthreads();
+  else grid.sync();
+}
+
 
 __device__ __forceinline__ bool skip(const int32_t* changed) { return changed && *changed == 0; }
 
@@ -123,7 +130,8 @@ __global__ void k_zero_i32_guard(int32_t* a, int n, const int32_t* changed) {
 // ---- the whole rebuild in one cooperative launch -------------------------------------
 __global__ void __launch_bounds__(512)
 k_tr_coop(sw_ragged_t m, int32_t* col_length, int32_t* col_ptr, int32_t* src_pre, int32_t* src_slot,
-          int32_t* cursor, int32_t* max_len, const int32_t* changed, int32_t* bsum, int slack) {
+          int32_t* cursor, int32_t* max_len, const int32_t* changed, int32_t* bsum, int slack,
+          int clear_changed) {
   if (skip(changed)) return;   // uniform: every block returns before any grid barrier
   cg::grid_group grid = cg::this_grid();
   const int N = m.num_post;
@@ -135,12 +143,12 @@ k_tr_coop(sw_ragged_t m, int32_t* col_length, int32_t* col_ptr, int32_t* src_pre
     cursor[j] = 0;
   }
   if (gt == 0) *max_len = 0;
-  grid.sync();
+  gsync(grid);
   for (int64_t x = gt; x < total; x += gn) {
     const int64_t i = x / m.stride;
     if ((int)(x - i * m.stride) < m.row_length[i]) atomicAdd(&col_length[m.target[x]], 1);
   }
-  grid.sync();
+  gsync(grid);
   // exclusive scan: block b owns the contiguous columns [c0, c1)
   __shared__ int32_t wsum[32];
   __shared__ int32_t carry, boff;
@@ -181,7 +189,7 @@ k_tr_coop(sw_ragged_t m, int32_t* col_length, int32_t* col_ptr, int32_t* src_pre
   if (threadIdx.x == 0) boff = 0;
   block_scan(false);
   if (threadIdx.x == 0) bsum[blockIdx.x] = carry;
-  grid.sync();
+  gsync(grid);
   if (threadIdx.x == 0) {
     int o = 0;
     for (int b = 0; b < (int)blockIdx.x; ++b) o += bsum[b];
@@ -190,7 +198,7 @@ k_tr_coop(sw_ragged_t m, int32_t* col_length, int32_t* col_ptr, int32_t* src_pre
   }
   __syncthreads();
   block_scan(true);
-  grid.sync();
+  gsync(grid);
   for (int64_t x = gt; x < total; x += gn) {
     const int64_t i = x / m.stride;
     const int s = (int)(x - i * m.stride);
@@ -201,7 +209,7 @@ k_tr_coop(sw_ragged_t m, int32_t* col_length, int32_t* col_ptr, int32_t* src_pre
       src_slot[pos] = s;
     }
   }
-  grid.sync();
+  gsync(grid);
   for (int64_t j = gt; j < N; j += gn) {
     const int a = col_ptr[j], e = a + col_length[j];
     for (int q = a + 1; q < e; ++q) {
@@ -217,6 +225,12 @@ k_tr_coop(sw_ragged_t m, int32_t* col_length, int32_t* col_ptr, int32_t* src_pre
     }
     atomicMax(max_len, e - a);
   }
+  if (clear_changed) {
+    // the gate flag is ours (the patch's overflow flag): reset it once every
+    // block has read it
+    gsync(grid);
+    if (gt == 0) *const_cast<int32_t*>(changed) = 0;
+  }
 }
 
 int grid1(int64_t n) {
@@ -226,6 +240,11 @@ int grid1(int64_t n) {
 }
 
 }  // namespace
+
+extern "C" int sw_transpose_rebuild_gated(const sw_ragged_t* m, int32_t* col_length, int32_t* col_ptr,
+                                          int32_t* src_pre, int32_t* src_slot, int32_t* cursor,
+                                          int32_t* max_len, int32_t* changed, int32_t* block_scratch,
+                                          int32_t slack, int32_t clear_changed, void* stream);
 
 extern "C" int sw_transpose_rebuild(const sw_ragged_t* m, int32_t* col_length, int32_t* col_ptr,
                                     int32_t* src_pre, int32_t* src_slot, int32_t* cursor,
@@ -250,6 +269,14 @@ extern "C" int sw_transpose_rebuild_coop(const sw_ragged_t* m, int32_t* col_leng
                                          int32_t* src_pre, int32_t* src_slot, int32_t* cursor,
                                          int32_t* max_len, const int32_t* changed,
                                          int32_t* block_scratch, int32_t slack, void* stream) {
+  return sw_transpose_rebuild_gated(m, col_length, col_ptr, src_pre, src_slot, cursor, max_len, const_cast<int32_t*>(changed),
+                                    block_scratch, slack, 0, stream);
+}
+
+extern "C" int sw_transpose_rebuild_gated(const sw_ragged_t* m, int32_t* col_length, int32_t* col_ptr,
+                                          int32_t* src_pre, int32_t* src_slot, int32_t* cursor,
+                                          int32_t* max_len, int32_t* changed, int32_t* block_scratch,
+                                          int32_t slack, int32_t clear_changed, void* stream) {
   if (!block_scratch) { sw::set_last_error("sw_transpose_rebuild_coop: block scratch required"); return SW_ERR_INVALID_ARG; }
   static int max_blocks = 0;
   if (max_blocks == 0) {
@@ -268,8 +295,15 @@ extern "C" int sw_transpose_rebuild_coop(const sw_ragged_t* m, int32_t* col_leng
   int blocks = (int)(want < 1 ? 1 : (want > max_blocks ? max_blocks : want));
   sw_ragged_t M = *m;
   void* args[] = {(void*)&M, (void*)&col_length, (void*)&col_ptr, (void*)&src_pre, (void*)&src_slot,
-                  (void*)&cursor, (void*)&max_len, (void*)&changed, (void*)&block_scratch, (void*)&slack};
-  cudaLaunchCooperativeKernel((const void*)k_tr_coop, dim3(blocks), dim3(512), args, 0, (cudaStream_t)stream);
+                  (void*)&cursor, (void*)&max_len, (void*)&changed, (void*)&block_scratch, (void*)&slack,
+                  (void*)&clear_changed};
+  if (total <= 65536) {
+    // small matrices: one block, block barriers, an ordinary launch
+    k_tr_coop<<<1, 512, 0, (cudaStream_t)stream>>>(M, col_length, col_ptr, src_pre, src_slot, cursor, max_len,
+                                                    changed, block_scratch, slack, clear_changed);
+  } else {
+    cudaLaunchCooperativeKernel((const void*)k_tr_coop, dim3(blocks), dim3(512), args, 0, (cudaStream_t)stream);
+  }
   sw::count_launch();
   SW_CHECK_LAUNCH("sw_transpose_rebuild_coop");
   return SW_OK;

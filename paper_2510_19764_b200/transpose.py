@@ -67,12 +67,12 @@ class TransposeMap:
         _lib.call("sw_transpose_patch", ctypes.byref(d), self.col_length.data_ptr(), self.col_ptr.data_ptr(),
                   self.src_pre.data_ptr(), self.src_slot.data_ptr(), patch_log.data_ptr(), int(cap),
                   self._need_rebuild.data_ptr(), self._patch_scratch.data_ptr(), _lib.stream_ptr())
-        # gated full rebuild: runs only if the patch flagged an overflow
-        _lib.call("sw_transpose_rebuild_coop", ctypes.byref(d), self.col_length.data_ptr(),
+        # gated full rebuild: runs only if the patch flagged an overflow, and
+        # resets the flag
+        _lib.call("sw_transpose_rebuild_gated", ctypes.byref(d), self.col_length.data_ptr(),
                   self.col_ptr.data_ptr(), self.src_pre.data_ptr(), self.src_slot.data_ptr(),
                   self._cursor.data_ptr(), self._max_len.data_ptr(), self._need_rebuild.data_ptr(),
-                  self._block_scratch.data_ptr(), self.slack, _lib.stream_ptr())
-        self._need_rebuild.zero_()
+                  self._block_scratch.data_ptr(), self.slack, 1, _lib.stream_ptr())
         self.version = self.matrix.version
         self.patches += 1
 
