@@ -19,7 +19,8 @@
 //   C  the ascending input rows and hidden rows are split into G ordered
 //      groups each (warp g sums group g of both into its partial rows: input
 //      rows from the staged copies, hidden rows straight from the packed
-//      rows); warp 7 then computes the readout and softmax;
+//      rows); the readout and softmax of a step run on the last warp during
+//      the next step's list building (nothing in a step reads them);
 //   D  per post the group partials are added in group order, the ALIF step
 //      and the surrogate (neurons.py:60-73).
 // Every output is bit-identical to k_clf_fwd's (classifier_fwd.cu): the same
@@ -130,8 +131,8 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
   int* rlen = (int*)(smem_raw + o);      o += (size_t)NT * 4;
   int* lin = (int*)(smem_raw + o);       o += (size_t)2 * NI * 4;        // [2][NI]
   int* soin = (int*)(smem_raw + o);      o += (size_t)2 * (NI + 1) * 4;  // [2][NI + 1]
-  int* lh = (int*)(smem_raw + o);        o += (size_t)H * 4;
-  o += (size_t)(H + 1) * 4;
+  int* lhb = (int*)(smem_raw + o);       o += (size_t)2 * H * 4;         // [2][H] hidden lists
+  o += 4;
   o = (o + 15) & ~(size_t)15;
   double* yv = (double*)(smem_raw + o);
   double* pis = yv + C;
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
   o += (size_t)SW_EPROP_MAX_BLOCK * 2 * ((NI + 31) / 32) * 4;
   int2* st = (int2*)(smem_raw + o);      // [2][stage]
   __shared__ int s_wcnt[kW2];
-  __shared__ int s_nin[2], s_staged[2];
+  __shared__ int s_nin[2], s_staged[2], s_nh[2];
   __shared__ double s_loss;
 
   const int b = blockIdx.x;
@@ -244,6 +245,51 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
       }
     }
   };
+  // warp kW2-1: readout y = alpha*y + z @ W_out^T + b (classifier.py:215) of
+  // one step from its hidden list (lane = class, spiking units ascending,
+  // 8 loads in flight), then softmax / cross-entropy / d (plasticity.py:156-165,
+  // classifier.py:216-219).  Nothing else in a step reads its result, so it
+  // runs one step late, beside the next step's list building.
+  auto readout = [&](const int* L, int n, double* d_out) {
+    for (int c0 = 0; c0 < C; c0 += 32) {
+      const int c = c0 + lane;
+      if (c < C) {
+        double sacc = 0.0;
+        const double* wr = P.w_out + (int64_t)c * H;
+        for (int q0 = 0; q0 < n; q0 += 8) {
+          double wv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) wv[u] = q0 + u < n ? __ldg(wr + L[q0 + u]) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (q0 + u < n) sacc = __dadd_rn(sacc, wv[u]);
+        }
+        yv[c] = __dadd_rn(__dadd_rn(__dmul_rn(P.alpha64, yv[c]), sacc), bo[c]);
+      }
+    }
+    __syncwarp();
+    double mx = -INFINITY;
+    for (int c = lane; c < C; c += 32) mx = fmax(mx, yv[c]);
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) mx = fmax(mx, __shfl_xor_sync(SW_FULL_MASK, mx, o2));
+    double se = 0.0;
+    double ex[2] = {0.0, 0.0};
+    for (int c = lane, u = 0; c < C; c += 32, ++u) {
+      const double e = exp(yv[c] - mx);
+      if (u < 2) ex[u] = e;
+      se += e;
+    }
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) se += __shfl_xor_sync(SW_FULL_MASK, se, o2);
+    for (int c = lane, u = 0; c < C; c += 32, ++u) {
+      const double pi = (u < 2 ? ex[u] : exp(yv[c] - mx)) / se;
+      pis[c] = pis[c] + pi;
+      const double dd = pi - (c == label ? 1.0 : 0.0);
+      dv[c] = dd;
+      d_out[bC + c] = dd;
+      if (c == label) s_loss = s_loss + -log(pi);
+    }
+  };
   if (warp == pw) build_inputs(P.t, 0);
   __syncthreads();
   uint32_t phase = 0;   // bit buf: completed-phase parity of sbar[buf]
@@ -254,7 +300,6 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
     const int cur = t % nslot;
     float* zbar_o = P.zbar + cur * B * H;
     float* psi_o = P.psi + cur * B * H;
-    double* d_o = P.d + cur * B * C;
 
     FWD2_PROF(0);
     // ---- A: hidden spikes -> ascending list ----
@@ -275,6 +320,7 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
       if (w < warp) hbase += c;
       nh += c;
     }
+    int* lh = lhb + cb * H;
     {
       // this thread's units in ascending order: lanes before it contribute
       // all their units, earlier j of this lane come first
@@ -285,8 +331,11 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
       for (int j = 0; j < HPT; ++j)
         if ((hm[j] >> lane) & 1u) lh[p++] = h0 + j;
     }
-    // ---- B: next step's input rows, staged while this step computes ----
+    if (tid == 0) s_nh[cb] = nh;
+    // ---- B: next step's input rows, staged while this step computes; the
+    // previous step's readout ----
     if (warp == pw && s + 1 < nsteps) build_inputs(t + 1, cb ^ 1);
+    if (warp == kW2 - 1 && s > 0) readout(lhb + (cb ^ 1) * H, s_nh[cb ^ 1], P.d + ((t - 1) % nslot) * B * C);
     // zbar (old z) for the e-prop traces and the readout gradient
 #pragma unroll
     for (int j = 0; j < HPT; ++j) {
@@ -337,49 +386,6 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
         __syncwarp();
       }
     }
-    if (warp == kW2 - 1) {
-      // readout y = alpha*y + z @ W_out^T + b (classifier.py:215), lane = class,
-      // spiking units ascending; softmax / cross-entropy / d (plasticity.py:156-165)
-      for (int c0 = 0; c0 < C; c0 += 32) {
-        const int c = c0 + lane;
-        if (c < C) {
-          double sacc = 0.0;
-          const double* wr = P.w_out + (int64_t)c * H;
-          // 8 independent loads in flight, then the ordered adds
-          for (int q0 = 0; q0 < nh; q0 += 8) {
-            double wv[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) wv[u] = q0 + u < nh ? __ldg(wr + lh[q0 + u]) : 0.0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              if (q0 + u < nh) sacc = __dadd_rn(sacc, wv[u]);
-          }
-          yv[c] = __dadd_rn(__dadd_rn(__dmul_rn(P.alpha64, yv[c]), sacc), bo[c]);
-        }
-      }
-      __syncwarp();
-      double mx = -INFINITY;
-      for (int c = lane; c < C; c += 32) mx = fmax(mx, yv[c]);
-#pragma unroll
-      for (int o2 = 16; o2 > 0; o2 >>= 1) mx = fmax(mx, __shfl_xor_sync(SW_FULL_MASK, mx, o2));
-      double se = 0.0;
-      double ex[2] = {0.0, 0.0};
-      for (int c = lane, u = 0; c < C; c += 32, ++u) {
-        const double e = exp(yv[c] - mx);
-        if (u < 2) ex[u] = e;
-        se += e;
-      }
-#pragma unroll
-      for (int o2 = 16; o2 > 0; o2 >>= 1) se += __shfl_xor_sync(SW_FULL_MASK, se, o2);
-      for (int c = lane, u = 0; c < C; c += 32, ++u) {
-        const double pi = (u < 2 ? ex[u] : exp(yv[c] - mx)) / se;
-        pis[c] = pis[c] + pi;
-        const double dd = pi - (c == label ? 1.0 : 0.0);
-        dv[c] = dd;
-        d_o[bC + c] = dd;
-        if (c == label) s_loss = s_loss + -log(pi);
-      }
-    }
     FWD2_PROF(5);
     __syncthreads();   // B3: partial rows complete
     FWD2_PROF(6);
@@ -414,6 +420,11 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
     // reaches only after finishing this step
   }
 
+  // the last step's readout
+  if (warp == kW2 - 1) {
+    const int tl = P.t + nsteps - 1, bl = (nsteps - 1) & 1;
+    readout(lhb + bl * H, s_nh[bl], P.d + (tl % nslot) * B * C);
+  }
 #pragma unroll
   for (int j = 0; j < HPT; ++j) {
     const int h = h0 + j;

@@ -1,25 +1,25 @@
 #!/bin/bash
-# One GPU-box pass: gpu tests, smoke, bench, ncu launch list + full captures.
-# Usage (under gpurun): bash tools/gpu_round.sh [tag]
+# One GPU-box pass: gpu tests, smoke, bench (C1 + C2), ncu launch list and
+# full captures of the hot kernels.  Usage (under gpurun): bash tools/gpu_round.sh [tag]
 set -x
-TAG=${1:-r1}
+TAG=${1:-r2}
 O=gpurun_out/$TAG
 mkdir -p $O
 nvidia-smi > $O/nvidia-smi.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
-timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
-timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench exit $?" >> $O/bench.err
+timeout 1500 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench exit $?" >> $O/bench.err
+timeout 900 python bench.py --workload clf-c2 --no-micro > $O/bench_c2.json 2> $O/bench_c2.err
 timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > $O/bench_ref.json 2> $O/bench_ref.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2600 --csv --log-file $O/launches.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $O/launches.csv \
    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-micro > $O/ncu_launch_bench.log 2>&1
-timeout 600 env EAGER=1 ncu --set full --clock-control none --import-source on -k regex:k_eprop_block -s 5 -c 1 \
+timeout 600 env EAGER=1 REPS=2 ncu --set full --clock-control none --import-source on -k regex:"k_eprop_t|k_prep" -c 2 \
    -o $O/eprop_c1 -f python tools/profile_eprop.py c1 > $O/ncu_eprop.log 2>&1
-timeout 600 env ROWS=262144 ncu --set full --clock-control none --import-source on \
-   -k regex:"k_deepr_elim|k_deepr_form_rows|k_remove_marked" -c 6 \
-   -o $O/deepr -f python tools/mupdate_breakdown.py > $O/ncu_deepr.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_clf_step -s 3 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_clf_fwd2 -s 50 -c 1 \
    -o $O/forward_c1 -f python tools/profile_forward.py c1 > $O/ncu_forward.log 2>&1
-timeout 600 ncu --set full --clock-control none -k regex:k_prop_bucketed -s 1 -c 1 \
-   -o $O/prop_bucketed -f python tools/profile_prop.py > $O/ncu_prop.log 2>&1
+timeout 900 env ROWS=262144 ncu --set full --clock-control none --import-source on \
+   -k regex:"k_deepr_elim|k_deepr_form_rows" -c 6 -o $O/deepr -f python tools/mupdate_breakdown.py > $O/ncu_deepr.log 2>&1
+timeout 600 ncu --set full --clock-control none -k regex:"k_prop_bucketed|k_prop_atomic" -c 4 \
+   -o $O/prop -f python tools/profile_prop.py > $O/ncu_prop.log 2>&1
 ls -la $O
