@@ -299,9 +299,9 @@ SW_API int sw_eprop_fused_block(const sw_eprop_seg_t* segs, int32_t n_segs, cons
  * signal lsig_t[k][hidden][ldb] = f32(sum_c d[b][c] * w_out[c][h]) (classes
  * ascending: classifier.py:223).  Columns b in [batch, ldb) are zero.
  * sw_eprop_pass runs k recursion steps of _kernels.py:15-39 over both
- * projections on those copies: eps/ebar in [e_pad/8][ldb/32][32][8] order
- * (8-synapse tile, 32-replica chunk, lane = 4*synapse + replica group,
- * 8 replicas), ldb a multiple of 32, bit-identical to the
+ * projections on those copies: eps/ebar in [e_pad/SPW][ldb/32][32][SPW]
+ * order (SPW-synapse tile, 32-replica chunk, lane = (32/SPW)*synapse +
+ * replica group, SPW replicas), ldb a multiple of 32, bit-identical to the
  * reference's; the float64 gradient terms are summed per synapse in
  * 64-replica splits and the splits added in order (within float64 rounding
  * of the reference's replica-ordered sum).  scratch:
@@ -327,7 +327,7 @@ typedef struct sw_eprop_tseg {
   const int32_t* pre;                        /* [e_pad] plan order */
   const int32_t* post;
   const float* trace_t[SW_EPROP_MAX_BLOCK];  /* [num_pre, ldb] per step */
-  float* eps; float* ebar;                   /* [e_pad/8][ldb/32][32][8] */
+  float* eps; float* ebar;                   /* [e_pad/SPW][ldb/32][32][SPW] */
   double* grad;                              /* [e_pad] compact gradient */
   int32_t e_pad;
 } sw_eprop_tseg_t;
@@ -337,6 +337,10 @@ typedef struct sw_eprop_tpass {
   const float* lsig_t[SW_EPROP_MAX_BLOCK];
   void* scratch;
 } sw_eprop_tpass_t;
+/* synapses per warp tile of sw_eprop_pass (SPW): eps/ebar are laid out
+ * [e_pad/SPW][ldb/32][32 lanes][SPW replicas], lane = (32/SPW)*synapse + group */
+#define SW_EPROP_PASS_SPW 4
+SW_API int32_t sw_eprop_pass_synapses_per_warp(void);
 SW_API int64_t sw_eprop_pass_scratch_bytes(int32_t e_pad_total, int32_t ldb);
 SW_API int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const sw_eprop_tpass_t* p,
                            int32_t ldb, float beta, float rho, float alpha, void* stream);

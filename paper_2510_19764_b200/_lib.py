@@ -162,6 +162,7 @@ SIGNATURES: dict[str, list] = {
     "sw_eprop_prep_scratch_bytes": [I32, I32, I32, I32],
     "sw_eprop_pass": [C.c_void_p, I32, P, I32, F32, F32, F32, P],
     "sw_eprop_pass_scratch_bytes": [I32, I32],
+    "sw_eprop_pass_synapses_per_warp": [],
     "sw_prop_bucket_slabs": [I32],
     "sw_prop_buckets_build": [P, P, P, I32, I32, I32, P, P, P, P, P],
     "sw_prop_buckets_refresh": [P, P, I32, I32, P, P, P],

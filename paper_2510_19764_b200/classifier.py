@@ -117,7 +117,7 @@ class SyntheticTask:
 class _Plan:
     """Compact per-batch synapse order of one projection (sw_eprop_plan:
     bucketed by post >> shift, then pre, then slot) and its eligibility state.
-    layout "chunk" (the trainer's, sw_eprop_pass): [e_pad/8][ldb/32][32][8],
+    layout "chunk" (the trainer's, sw_eprop_pass): [e_pad/SPW][ldb/32][32][SPW],
     with shift 0 (synapses by post); layout "tile" (sw_eprop_fused_step /
     _block): [tile][batch][32]."""
 
@@ -143,9 +143,10 @@ class _Plan:
         self.off = torch.zeros(e_pad, dtype=torch.int32, device=dev)
         self.grad = torch.zeros(e_pad, dtype=torch.float64, device=dev)
         if self.layout == "chunk":
-            # [8-synapse tile, 32-replica chunk, lane = 4 * synapse + group,
-            # 8 replicas of the group] (sw_eprop_pass)
-            self.eps = torch.zeros((e_pad // 8, self.ldb // 32, 32, 8), dtype=torch.float32, device=dev)
+            # [SPW-synapse tile, 32-replica chunk, lane = (32/SPW) * synapse +
+            # group, SPW replicas of the group] (sw_eprop_pass)
+            spw = self.spw = int(_lib.lib().sw_eprop_pass_synapses_per_warp())
+            self.eps = torch.zeros((e_pad // spw, self.ldb // 32, 32, spw), dtype=torch.float32, device=dev)
         else:
             # [tile, replica, lane] (sw_eprop_fused_step / sw_eprop_fused_block)
             self.eps = torch.zeros((e_pad // 32, self.batch, 32), dtype=torch.float32, device=dev)
@@ -154,7 +155,8 @@ class _Plan:
     def replica_major(self, state: torch.Tensor) -> torch.Tensor:
         """[batch, e_pad] copy of eps or ebar (tests, inspection)."""
         if self.layout == "chunk":
-            t = state.view(self.e_pad // 8, self.ldb // 32, 8, 4, 8)      # [t8, c, s, g, r]
+            spw = self.spw
+            t = state.view(self.e_pad // spw, self.ldb // 32, spw, 32 // spw, spw)   # [tile, c, s, g, r]
             return t.permute(1, 3, 4, 0, 2).reshape(self.ldb, self.e_pad)[:self.batch]
         return state.permute(1, 0, 2).reshape(self.batch, self.e_pad)
 

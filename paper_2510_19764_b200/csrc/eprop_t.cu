@@ -275,42 +275,57 @@ __device__ __forceinline__ void st256p_cs(float* p, const unsigned long long (&v
                : "memory");
 }
 
-__device__ __forceinline__ void ld256(float (&v)[8], const float* p) {
-  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
-               : "l"(p));
-}
-__device__ __forceinline__ void ld256_cs(float (&v)[8], const float* p) {
-  asm("ld.global.cs.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
-               : "l"(p));
-}
-__device__ __forceinline__ void st256_cs(float* p, const float (&v)[8]) {
-  asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
-               "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
-               : "memory");
-}
-
 // grad[e] += the splits' partials, split order
+template <int SPW>
 __global__ void k_grad_reduce(const TPass T) {
   const int tiles0 = T.s[0].tiles, tiles = tiles0 + T.s[1].tiles;
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < tiles * 8; x += gridDim.x * blockDim.x) {
-    const int tile = x >> 3, sl = x & 7;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < tiles * SPW; x += gridDim.x * blockDim.x) {
+    const int tile = x / SPW, sl = x % SPW;
     const bool first = tile < tiles0;
     double* grad = first ? T.s[0].grad : T.s[1].grad;
-    const int e = (first ? tile : tile - tiles0) * 8 + sl;
+    const int e = (first ? tile : tile - tiles0) * SPW + sl;
     double gr = grad[e];
-    for (int q = 0; q < T.splits; ++q) gr = __dadd_rn(gr, __ldcg(T.partial + ((int64_t)tile * T.splits + q) * 8 + sl));
+    for (int q = 0; q < T.splits; ++q)
+      gr = __dadd_rn(gr, __ldcg(T.partial + ((int64_t)tile * T.splits + q) * SPW + sl));
     grad[e] = gr;
   }
 }
 
-// PD: steps of inputs loaded ahead of the recursion; SP: the next chunk's
-// eligibility state is loaded during the current chunk
-template <int K, int PD, bool SP, int MB>
+// RPL replicas per lane as RPL/2 packed pairs: one 128- or 256-bit access
+template <int RPL>
+__device__ __forceinline__ void ldp(unsigned long long (&v)[RPL / 2], const float* p) {
+  if constexpr (RPL == 8) {
+    asm("ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%4];" : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p));
+  } else {
+    asm("ld.global.nc.v2.b64 {%0,%1}, [%2];" : "=l"(v[0]), "=l"(v[1]) : "l"(p));
+  }
+}
+template <int RPL>
+__device__ __forceinline__ void ldp_cs(unsigned long long (&v)[RPL / 2], const float* p) {
+  if constexpr (RPL == 8) {
+    asm("ld.global.cs.v4.b64 {%0,%1,%2,%3}, [%4];" : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p));
+  } else {
+    asm("ld.global.cs.v2.b64 {%0,%1}, [%2];" : "=l"(v[0]), "=l"(v[1]) : "l"(p));
+  }
+}
+template <int RPL>
+__device__ __forceinline__ void stp_cs(float* p, const unsigned long long (&v)[RPL / 2]) {
+  if constexpr (RPL == 8) {
+    asm volatile("st.global.cs.v4.b64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(v[0]), "l"(v[1]), "l"(v[2]), "l"(v[3])
+                 : "memory");
+  } else {
+    asm volatile("st.global.cs.v2.b64 [%0], {%1,%2};" ::"l"(p), "l"(v[0]), "l"(v[1]) : "memory");
+  }
+}
+
+// SPW synapses per warp (tile), LPS = 32/SPW lanes per synapse, each lane
+// RPL = 32/LPS consecutive replicas of the 32-replica chunk; PD: steps of
+// inputs loaded ahead of the recursion
+template <int K, int PD, int SPW, int MB>
 __global__ void __launch_bounds__(kTW * 32, MB) k_eprop_t(const TPass T) {
+  constexpr int LPS = 32 / SPW, RPL = 32 / LPS, NP = RPL / 2;
   const int lane = threadIdx.x & 31;
-  const int sl = lane >> 2, g = lane & 3;
+  const int sl = lane / LPS, g = lane % LPS;
   const int tiles0 = T.s[0].tiles;
   const int tiles = tiles0 + T.s[1].tiles;
   const int items = tiles * T.splits;
@@ -319,8 +334,7 @@ __global__ void __launch_bounds__(kTW * 32, MB) k_eprop_t(const TPass T) {
   // static assignment of the uniform work items (no ticket atomics): block b
   // owns the contiguous item range [b*items/nb, (b+1)*items/nb) and its warps
   // stride through it, so the warps of a block work on neighbouring tiles of
-  // one replica split at a time (their trace / psi / lsig lines are shared
-  // in L1 when the plan orders tiles by pre block)
+  // one replica split at a time
   const int nwb = blockDim.x >> 5;
   const int i0 = (int)((int64_t)items * blockIdx.x / gridDim.x), i1 = (int)((int64_t)items * (blockIdx.x + 1) / gridDim.x);
   for (int item = i0 + (threadIdx.x >> 5); item < i1; item += nwb) {
@@ -329,50 +343,45 @@ __global__ void __launch_bounds__(kTW * 32, MB) k_eprop_t(const TPass T) {
     const bool first = tile < tiles0;
     const TSeg& S = first ? T.s[0] : T.s[1];
     const int lt = first ? tile : tile - tiles0;
-    const int e = lt * 8 + sl;
+    const int e = lt * SPW + sl;
     int pre = __ldg(S.pre + e), post = __ldg(S.post + e);
     if (T.dbg == 1) pre = post = 0;
     const int c0 = split * T.chunks_per_split, c1 = min(nchunk, c0 + T.chunks_per_split);
-    const int64_t tofs = (int64_t)pre * L + g * 8, pofs = (int64_t)post * L + g * 8;
+    const int64_t tofs = (int64_t)pre * L + g * RPL, pofs = (int64_t)post * L + g * RPL;
     const unsigned long long B2 = pk2(T.beta, T.beta), A2 = pk2(T.alpha, T.alpha), R2 = pk2(T.rho, T.rho);
     const unsigned long long NZ = T.nz;
     double acc = 0.0;
-    // state and inputs as packed replica pairs (4 x f32x2 per lane)
-    unsigned long long ep[4], eb[4];
-    const int64_t so0 = (((int64_t)lt * nchunk + c0) * 32 + lane) * 8;
+    // state and inputs as packed replica pairs
+    unsigned long long ep[NP], eb[NP];
+    const int64_t so0 = (((int64_t)lt * nchunk + c0) * 32 + lane) * RPL;
     if (T.dbg == 2) {
-      for (int r = 0; r < 4; ++r) ep[r] = eb[r] = 0ull;
+      for (int r = 0; r < NP; ++r) ep[r] = eb[r] = 0ull;
     } else {
-      ld256p_cs(ep, S.eps + so0);
-      ld256p_cs(eb, S.ebar + so0);
+      ldp_cs<RPL>(ep, S.eps + so0);
+      ldp_cs<RPL>(eb, S.ebar + so0);
     }
     for (int c = c0; c < c1; ++c) {
       const int b0 = c * 32;
-      const int64_t so = (((int64_t)lt * nchunk + c) * 32 + lane) * 8;
-      unsigned long long zin[K][4], pin[K][4], lin[K][4];
+      const int64_t so = (((int64_t)lt * nchunk + c) * 32 + lane) * RPL;
+      unsigned long long zin[K][NP], pin[K][NP], lin[K][NP];
 #pragma unroll
       for (int k = 0; k < PD && k < K; ++k) {
-        ld256p(zin[k], S.trace[k] + tofs + b0);
-        ld256p(pin[k], T.psi[k] + pofs + b0);
-        ld256p(lin[k], T.lsig[k] + pofs + b0);
-      }
-      unsigned long long nep[4], neb[4];
-      if (SP && c + 1 < c1) {
-        ld256p_cs(nep, S.eps + so + 32 * 8);
-        ld256p_cs(neb, S.ebar + so + 32 * 8);
+        ldp<RPL>(zin[k], S.trace[k] + tofs + b0);
+        ldp<RPL>(pin[k], T.psi[k] + pofs + b0);
+        ldp<RPL>(lin[k], T.lsig[k] + pofs + b0);
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         if (k + PD < K) {
-          ld256p(zin[k + PD], S.trace[k + PD] + tofs + b0);
-          ld256p(pin[k + PD], T.psi[k + PD] + pofs + b0);
-          ld256p(lin[k + PD], T.lsig[k + PD] + pofs + b0);
+          ldp<RPL>(zin[k + PD], S.trace[k + PD] + tofs + b0);
+          ldp<RPL>(pin[k + PD], T.psi[k + PD] + pofs + b0);
+          ldp<RPL>(lin[k + PD], T.lsig[k + PD] + pofs + b0);
         }
         // _kernels.py:33-38 on replica pairs, every op a separately rounded
         // packed f32x2 op: e = psi*(zb - beta*eps); ebar = alpha*ebar + e;
         // grad += f64(lsig*ebar); eps = rho*eps + e
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < NP; ++r) {
           const unsigned long long x = sub2(zin[k][r], pmul2(B2, ep[r], NZ));
           const unsigned long long ee = pmul2(pin[k][r], x, NZ);
           eb[r] = add2(pmul2(A2, eb[r], NZ), ee);
@@ -384,157 +393,19 @@ __global__ void __launch_bounds__(kTW * 32, MB) k_eprop_t(const TPass T) {
         }
       }
       if (T.dbg != 2) {
-        st256p_cs(S.eps + so, ep);
-        st256p_cs(S.ebar + so, eb);
+        stp_cs<RPL>(S.eps + so, ep);
+        stp_cs<RPL>(S.ebar + so, eb);
       }
       if (c + 1 < c1 && T.dbg != 2) {
-        if (SP) {
-#pragma unroll
-          for (int r = 0; r < 4; ++r) { ep[r] = nep[r]; eb[r] = neb[r]; }
-        } else {
-          ld256p_cs(ep, S.eps + so + 32 * 8);
-          ld256p_cs(eb, S.ebar + so + 32 * 8);
-        }
+        ldp_cs<RPL>(ep, S.eps + so + 32 * RPL);
+        ldp_cs<RPL>(eb, S.ebar + so + 32 * RPL);
       }
     }
-    // the synapse's 4 replica groups: (g0 + g1) + (g2 + g3)
-    acc = __dadd_rn(acc, __shfl_xor_sync(SW_FULL_MASK, acc, 1));
-    acc = __dadd_rn(acc, __shfl_xor_sync(SW_FULL_MASK, acc, 2));
+    // the synapse's LPS replica groups, added pairwise: (g0 + g1) + (g2 + g3) ...
+#pragma unroll
+    for (int o = 1; o < LPS; o <<= 1) acc = __dadd_rn(acc, __shfl_xor_sync(SW_FULL_MASK, acc, o));
     // this split's partial; k_grad_reduce adds the splits in order
-    if (g == 0) T.partial[((int64_t)tile * T.splits + split) * 8 + sl] = acc;
-  }
-}
-
-// The same recursion with the eligibility state streamed through a per-warp
-// ring of NST shared-memory stages by bulk copies (cp.async.bulk, one lane
-// issues them, an mbarrier per stage): the state of the chunk NST-1 ahead is
-// in flight while the current chunk computes, so its DRAM latency is off the
-// critical path without holding it in registers.  Inputs as in k_eprop_t.
-template <int K, int NST, int MB>
-__global__ void __launch_bounds__(kTW * 32, MB) k_eprop_tma(const TPass T) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int sl = lane >> 2, g = lane & 3;
-  float* ring = reinterpret_cast<float*>(smem_raw) + (size_t)wib * NST * 512;   // [NST][eps 256 | ebar 256]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kTW * NST * 2048) + wib * NST;
-  const int tiles0 = T.s[0].tiles;
-  const int tiles = tiles0 + T.s[1].tiles;
-  const int items = tiles * T.splits;
-  const int nchunk = T.ldb / 32;
-  const int64_t L = T.ldb;
-  const int nwarps = gridDim.x * kTW;
-  const int gw = blockIdx.x * kTW + wib;
-  if (lane == 0)
-    for (int q = 0; q < NST; ++q) sw::mbar_init(&bars[q], 1);
-  sw::fence_mbar_init();
-  __syncwarp();
-  // chunk cursor over this warp's (item, chunk) sequence
-  struct Cur { int item, c, c1; };
-  auto first_chunk = [&](int item) {
-    Cur u{item, 0, 0};
-    if (item < items) {
-      const int split = item / tiles;
-      u.c = split * T.chunks_per_split;
-      u.c1 = min(nchunk, u.c + T.chunks_per_split);
-    }
-    return u;
-  };
-  auto advance = [&](Cur& u) {
-    if (++u.c >= u.c1) u = first_chunk(u.item + nwarps);
-  };
-  auto state_ptrs = [&](const Cur& u, const float*& pe, const float*& pb) {
-    const int tile = u.item % tiles;
-    const bool first = tile < tiles0;
-    const TSeg& S = first ? T.s[0] : T.s[1];
-    const int lt = first ? tile : tile - tiles0;
-    const int64_t so = ((int64_t)lt * nchunk + u.c) * 32 * 8;
-    pe = S.eps + so;
-    pb = S.ebar + so;
-  };
-  Cur prod = first_chunk(gw);
-  for (int q = 0; q < NST; ++q) {
-    if (prod.item < items && lane == 0) {
-      const float *pe, *pb;
-      state_ptrs(prod, pe, pb);
-      sw::mbar_arrive_expect_tx(&bars[q], 2048);
-      sw::bulk_g2s(ring + q * 512, pe, 1024, &bars[q]);
-      sw::bulk_g2s(ring + q * 512 + 256, pb, 1024, &bars[q]);
-    }
-    if (prod.item < items) advance(prod);
-  }
-  Cur cons = first_chunk(gw);
-  double acc = 0.0;
-  for (uint32_t n = 0; cons.item < items; ++n) {
-    const int split = cons.item / tiles, tile = cons.item - split * tiles;
-    const bool first = tile < tiles0;
-    const TSeg& S = first ? T.s[0] : T.s[1];
-    const int lt = first ? tile : tile - tiles0;
-    const int e = lt * 8 + sl;
-    const int pre = __ldg(S.pre + e), post = __ldg(S.post + e);
-    const int64_t tofs = (int64_t)pre * L + g * 8, pofs = (int64_t)post * L + g * 8;
-    const int b0 = cons.c * 32;
-    float zin[K][8], pin[K][8], lin[K][8];
-    ld256(zin[0], S.trace[0] + tofs + b0);
-    ld256(pin[0], T.psi[0] + pofs + b0);
-    ld256(lin[0], T.lsig[0] + pofs + b0);
-    const int q = n % NST;
-    sw::mbar_wait(&bars[q], (n / NST) & 1);
-    float ep[8], eb[8];
-    {
-      const float4* se = reinterpret_cast<const float4*>(ring + q * 512 + lane * 8);
-      const float4* sb = reinterpret_cast<const float4*>(ring + q * 512 + 256 + lane * 8);
-      const float4 a0 = se[0], a1 = se[1], c0 = sb[0], c1 = sb[1];
-      ep[0] = a0.x; ep[1] = a0.y; ep[2] = a0.z; ep[3] = a0.w; ep[4] = a1.x; ep[5] = a1.y; ep[6] = a1.z; ep[7] = a1.w;
-      eb[0] = c0.x; eb[1] = c0.y; eb[2] = c0.z; eb[3] = c0.w; eb[4] = c1.x; eb[5] = c1.y; eb[6] = c1.z; eb[7] = c1.w;
-    }
-    __syncwarp();
-    // refill this stage with the chunk NST ahead
-    if (prod.item < items) {
-      if (lane == 0) {
-        sw::fence_proxy_async_smem();
-        const float *pe, *pb;
-        state_ptrs(prod, pe, pb);
-        sw::mbar_arrive_expect_tx(&bars[q], 2048);
-        sw::bulk_g2s(ring + q * 512, pe, 1024, &bars[q]);
-        sw::bulk_g2s(ring + q * 512 + 256, pb, 1024, &bars[q]);
-      }
-      advance(prod);
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if (k + 1 < K) {
-        ld256(zin[k + 1], S.trace[k + 1] + tofs + b0);
-        ld256(pin[k + 1], T.psi[k + 1] + pofs + b0);
-        ld256(lin[k + 1], T.lsig[k + 1] + pofs + b0);
-      }
-#pragma unroll
-      for (int r = 0; r < 8; r += 2) {
-        const unsigned long long x =
-            sub2(pk2(zin[k][r], zin[k][r + 1]), pk2(__fmul_rn(T.beta, ep[r]), __fmul_rn(T.beta, ep[r + 1])));
-        float x0, x1;
-        up2(x, x0, x1);
-        const unsigned long long ee = pk2(__fmul_rn(pin[k][r], x0), __fmul_rn(pin[k][r + 1], x1));
-        const unsigned long long ebn = add2(pk2(__fmul_rn(T.alpha, eb[r]), __fmul_rn(T.alpha, eb[r + 1])), ee);
-        const unsigned long long epn = add2(pk2(__fmul_rn(T.rho, ep[r]), __fmul_rn(T.rho, ep[r + 1])), ee);
-        float t0, t1;
-        up2(mul2(pk2(lin[k][r], lin[k][r + 1]), ebn), t0, t1);
-        acc = __dadd_rn(acc, (double)t0);
-        acc = __dadd_rn(acc, (double)t1);
-        up2(ebn, eb[r], eb[r + 1]);
-        up2(epn, ep[r], ep[r + 1]);
-      }
-    }
-    const int64_t so = (((int64_t)lt * nchunk + cons.c) * 32 + lane) * 8;
-    st256_cs(S.eps + so, ep);
-    st256_cs(S.ebar + so, eb);
-    if (cons.c + 1 >= cons.c1) {
-      // item done: the synapse's 4 replica groups (g0 + g1) + (g2 + g3), then the split partial
-      acc = __dadd_rn(acc, __shfl_xor_sync(SW_FULL_MASK, acc, 1));
-      acc = __dadd_rn(acc, __shfl_xor_sync(SW_FULL_MASK, acc, 2));
-      if (g == 0) T.partial[((int64_t)tile * T.splits + split) * 8 + sl] = acc;
-      acc = 0.0;
-    }
-    advance(cons);
+    if (g == 0) T.partial[((int64_t)tile * T.splits + split) * SPW + sl] = acc;
   }
 }
 
@@ -577,11 +448,16 @@ extern "C" int sw_eprop_prep(const sw_eprop_prep_t* p, void* stream) {
   return SW_OK;
 }
 
+// synapses per warp of the pass (the plan's state layout, [e_pad/SPW][ldb/32][32][32/(32/SPW)])
+constexpr int kSPW = SW_EPROP_PASS_SPW;
+
+extern "C" int32_t sw_eprop_pass_synapses_per_warp(void) { return kSPW; }
+
 extern "C" int64_t sw_eprop_pass_scratch_bytes(int32_t e_pad_total, int32_t ldb) {
   if (e_pad_total <= 0 || ldb <= 0) return 0;
-  const int64_t tiles = e_pad_total / 8;
+  const int64_t tiles = e_pad_total / kSPW;
   const int64_t splits = (ldb + 63) / 64;
-  return tiles * splits * 8 * 8;
+  return tiles * splits * kSPW * 8;
 }
 
 extern "C" int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const sw_eprop_tpass_t* p,
@@ -595,7 +471,7 @@ extern "C" int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const 
     return SW_ERR_INVALID_ARG;
   }
   if (!p->scratch) {
-    sw::set_last_error("sw_eprop_pass: scratch of sw_eprop_pass_scratch_bytes() bytes (zeroed once) required");
+    sw::set_last_error("sw_eprop_pass: scratch of sw_eprop_pass_scratch_bytes() bytes required");
     return SW_ERR_INVALID_ARG;
   }
   TPass T{};
@@ -609,21 +485,20 @@ extern "C" int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const 
     T.s[i].eps = q.eps;
     T.s[i].ebar = q.ebar;
     T.s[i].grad = q.grad;
-    T.s[i].tiles = q.e_pad / 8;
+    T.s[i].tiles = q.e_pad / kSPW;
     etot += q.e_pad;
   }
   for (int k = 0; k < SW_EPROP_MAX_BLOCK; ++k) {
     T.psi[k] = p->psi_t[k < p->k ? k : 0];
     T.lsig[k] = p->lsig_t[k < p->k ? k : 0];
   }
-  const int tiles = etot / 8;
+  const int tiles = etot / kSPW;
   if (tiles == 0) return SW_OK;
   const int nchunk = ldb / 32;
   T.ldb = ldb;
   T.splits = (ldb + 63) / 64;
   T.chunks_per_split = (nchunk + T.splits - 1) / T.splits;
-  unsigned char* sc = (unsigned char*)p->scratch;
-  T.partial = (double*)sc;
+  T.partial = (double*)p->scratch;
   T.beta = beta;
   T.rho = rho;
   T.alpha = alpha;
@@ -633,71 +508,43 @@ extern "C" int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const 
     T.dbg = dbg;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  // variant (SW_EPT_CFG = "PD,SP,MB" for measurement): inputs PD steps
-  // ahead, next-chunk state prefetch SP, MB blocks per SM
+  // variant (SW_EPT_CFG = "PD,MB": inputs PD steps ahead, MB blocks per SM)
   static int cfg = -1;
   if (cfg < 0) {
     cfg = 0;
     if (const char* ev = getenv("SW_EPT_CFG")) {
-      int pd = 0, sp = 0, mb = 0;
-      if (sscanf(ev, "%d,%d,%d", &pd, &sp, &mb) == 3) cfg = pd * 100 + sp * 10 + mb;
+      int pd = 0, mb = 0;
+      if (sscanf(ev, "%d,%d", &pd, &mb) == 2) cfg = pd * 10 + mb;
     }
   }
   const int items = tiles * T.splits;
-  const void* fn = nullptr;
-  int kern = 0;
-#define SW_EPT_VARIANTS(X) X(1, false, 3) X(2, false, 2) X(2, true, 2) X(1, true, 3) X(2, false, 3) X(1, true, 2)
-  const int want = cfg ? cfg : 202;
-  if (want / 100 == 9) {
-    const int nst = (want / 10) % 10, mb = want % 10;
-    auto launch_tma = [&](auto kfn, int NST) {
-      const int smem = kTW * NST * 2048 + kTW * NST * 8;
-      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kTW * 32, smem);
-      if (per_sm < 1) per_sm = 1;
-      int blocks = 148 * per_sm;
-      if (blocks * kTW > items) blocks = (items + kTW - 1) / kTW;
-      kfn<<<blocks, kTW * 32, smem, st>>>(T);
-    };
-    if (p->k != 8) { sw::set_last_error("sw_eprop_pass: TMA variant is k = 8 only"); return SW_ERR_INVALID_ARG; }
-    if (nst == 3 && mb == 3) launch_tma(k_eprop_tma<8, 3, 3>, 3);
-    else if (nst == 4 && mb == 3) launch_tma(k_eprop_tma<8, 4, 3>, 4);
-    else if (nst == 2 && mb == 3) launch_tma(k_eprop_tma<8, 2, 3>, 2);
-    else launch_tma(k_eprop_tma<8, 4, 2>, 4);
-    sw::count_launch();
-    const int n = tiles * 8;
-    k_grad_reduce<<<(n + 255) / 256, 256, 0, st>>>(T);
-    sw::count_launch();
-    SW_CHECK_LAUNCH("sw_eprop_pass");
-    return SW_OK;
-  }
-  auto launch = [&](auto kfn, int mb) {
+  auto launch = [&](auto kfn) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kTW * 32, 0);
     if (per_sm < 1) per_sm = 1;
     int blocks = 148 * per_sm;
     if (blocks * kTW > items) blocks = (items + kTW - 1) / kTW;
     kfn<<<blocks, kTW * 32, 0, st>>>(T);
-    (void)mb;
   };
-  (void)fn; (void)kern;
-  bool done = false;
+  const int want = cfg ? cfg : (kSPW == 8 ? 22 : 24);
   switch (p->k) {
-#define SW_EPT_CASE(PD, SP, MB) \
-    if (!done && want == PD * 100 + (SP ? 1 : 0) * 10 + MB) { launch(k_eprop_t<KK, PD, SP, MB>, MB); done = true; }
-#define SW_K(KK_) case KK_: { constexpr int KK = KK_; SW_EPT_VARIANTS(SW_EPT_CASE) \
-    if (!done) { launch(k_eprop_t<KK, 1, false, 3>, 3); done = true; } break; }
+#define SW_K(KK)                                                                 \
+  case KK:                                                                       \
+    if (want == 13) launch(k_eprop_t<KK, 1, kSPW, 3>);                           \
+    else if (want == 14) launch(k_eprop_t<KK, 1, kSPW, 4>);                      \
+    else if (want == 23) launch(k_eprop_t<KK, 2, kSPW, 3>);                      \
+    else if (want == 24) launch(k_eprop_t<KK, 2, kSPW, 4>);                      \
+    else if (want == 16) launch(k_eprop_t<KK, 1, kSPW, 6>);                      \
+    else launch(k_eprop_t<KK, 2, kSPW, 2>);                                      \
+    break;
     SW_K(1) SW_K(2) SW_K(3) SW_K(4) SW_K(5) SW_K(6) SW_K(7) SW_K(8)
 #undef SW_K
-#undef SW_EPT_CASE
-#undef SW_EPT_VARIANTS
     default: sw::set_last_error("sw_eprop_pass: k"); return SW_ERR_INVALID_ARG;
   }
   sw::count_launch();
   {
-    const int n = tiles * 8;
-    k_grad_reduce<<<(n + 255) / 256, 256, 0, st>>>(T);
+    const int n = tiles * kSPW;
+    k_grad_reduce<kSPW><<<(n + 255) / 256, 256, 0, st>>>(T);
   }
   sw::count_launch();
   SW_CHECK_LAUNCH("sw_eprop_pass");
