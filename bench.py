@@ -804,6 +804,8 @@ def run_device(args, w):
         return e0.elapsed_time(e1) * 1e3 / reps
     k_us = graph_us("pass")
     prep_us = graph_us("prep")
+    tr._pass_scratch.zero_()      # the replays accumulated deferred partials
+    tr._ro_partial.zero_()
     E = tr.m_in.edge_count() + tr.m_rec.edge_count()
     Bl = tr.local_b
     # eligibility state read + written once per pass, gradient r/w + plan,

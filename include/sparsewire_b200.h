@@ -224,8 +224,8 @@ SW_API int sw_eprop_accumulate_batch(const int32_t* targets, const int32_t* row_
                                      int32_t num_post, float* eps, float* ebar, double* grad,
                                      float beta, float rho, float alpha, void* stream);
 /* Per-batch compact synapse order for the fused step: synapses bucketed by
- * (target >> shift, pre, slot).  scratch: 2*G*num_pre int32 with
- * G = ((num_post-1) >> shift) + 1.  out_* have e_pad entries (multiple of
+ * (target >> shift, pre, slot).  scratch: 2*n + ceil(n/4096) + 1 int32
+ * with n = G*num_pre, G = ((num_post-1) >> shift) + 1.  out_* have e_pad entries (multiple of
  * 32); entries past *total are padding (out_off = -1). */
 SW_API int sw_eprop_plan(const int32_t* row_length, const int32_t* target, int32_t num_pre,
                          int32_t stride, int32_t num_post, int32_t shift, int32_t* scratch,
@@ -319,7 +319,12 @@ typedef struct sw_eprop_prep {
    * g_w_out[C, H] += sum d^T zbar, g_b_out[C] += sum d, through ro_partial
    * (sw_eprop_prep_scratch_bytes); g_w_out NULL = none */
   double* g_w_out; double* g_b_out; double* ro_partial;
+  /* defer_reduce != 0: the readout partials accumulate in ro_partial over
+   * the batch's groups (zeroed before the first, e.g. by the previous
+   * sw_eprop_prep_reduce) and sw_eprop_prep_reduce adds them once */
+  int32_t defer_reduce;
 } sw_eprop_prep_t;
+SW_API int sw_eprop_prep_reduce(const sw_eprop_prep_t* p, void* stream);
 SW_API int64_t sw_eprop_prep_scratch_bytes(int32_t k, int32_t batch, int32_t hidden, int32_t num_classes);
 SW_API int sw_eprop_prep(const sw_eprop_prep_t* p, void* stream);
 
@@ -336,7 +341,13 @@ typedef struct sw_eprop_tpass {
   const float* psi_t[SW_EPROP_MAX_BLOCK];    /* [hidden, ldb] per step */
   const float* lsig_t[SW_EPROP_MAX_BLOCK];
   void* scratch;
+  /* defer_reduce != 0: the split partials accumulate in scratch over the
+   * batch's passes (zeroed before the first) and sw_eprop_pass_reduce adds
+   * them to the gradients once (zeroing them again) */
+  int32_t defer_reduce;
 } sw_eprop_tpass_t;
+SW_API int sw_eprop_pass_reduce(const sw_eprop_tseg_t* segs, int32_t n_segs, int32_t ldb, void* scratch,
+                                void* stream);
 /* synapses per warp tile of sw_eprop_pass (SPW): eps/ebar are laid out
  * [e_pad/SPW][ldb/32][32 lanes][SPW replicas], lane = (32/SPW)*synapse + group */
 #define SW_EPROP_PASS_SPW 4
@@ -407,7 +418,8 @@ typedef struct sw_clf_step {
 /* The trial's input side at once (classifier.py:63-67, 210-213): every input
  * spike of steps 0..steps-1 from the examples' counter streams, as words
  * in_bits[t][batch][words] (words = ceil(num_inputs/32)), and the input
- * traces xbar_t[t][num_inputs][ldb] (replica-minor, zero past the batch). */
+ * traces xbar_t[t][num_inputs][ldb] (replica-minor, zero past the batch).
+ * num_inputs <= 25600. */
 typedef struct sw_clf_inputs {
   int32_t steps, batch, ldb, num_inputs, words;
   const double* p_in;        /* [batch, num_inputs] */

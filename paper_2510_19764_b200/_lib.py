@@ -93,7 +93,7 @@ class EpropPrep(C.Structure):
                 ("num_classes", I32), ("xbar", P * MAX_BLOCK), ("zbar", P * MAX_BLOCK),
                 ("psi", P * MAX_BLOCK), ("d", P * MAX_BLOCK), ("w_out", P), ("xbar_t", P),
                 ("zbar_t", P), ("psi_t", P), ("lsig_t", P), ("g_w_out", P), ("g_b_out", P),
-                ("ro_partial", P)]
+                ("ro_partial", P), ("defer_reduce", I32)]
 
 
 class EpropTSeg(C.Structure):
@@ -104,7 +104,8 @@ class EpropTSeg(C.Structure):
 
 class EpropTPass(C.Structure):
     """sw_eprop_tpass_t"""
-    _fields_ = [("k", I32), ("psi_t", P * MAX_BLOCK), ("lsig_t", P * MAX_BLOCK), ("scratch", P)]
+    _fields_ = [("k", I32), ("psi_t", P * MAX_BLOCK), ("lsig_t", P * MAX_BLOCK), ("scratch", P),
+                ("defer_reduce", I32)]
 
 
 class ClfStep(C.Structure):
@@ -159,6 +160,8 @@ SIGNATURES: dict[str, list] = {
     "sw_eprop_fused_block": [C.c_void_p, I32, P, I32, I32, F32, F32, F32, P, P, I32, P, P],
     "sw_eprop_readout_scratch_bytes": [I32, I32, I32],
     "sw_eprop_prep": [P, P],
+    "sw_eprop_prep_reduce": [P, P],
+    "sw_eprop_pass_reduce": [C.c_void_p, I32, I32, P, P],
     "sw_eprop_prep_scratch_bytes": [I32, I32, I32, I32],
     "sw_eprop_pass": [C.c_void_p, I32, P, I32, F32, F32, F32, P],
     "sw_eprop_pass_scratch_bytes": [I32, I32],

@@ -129,7 +129,8 @@ class _Plan:
         self.batch = batch
         self.ldb = -(-batch // 32) * 32
         G = ((m.num_post - 1) >> shift) + 1
-        self.scratch = torch.zeros(2 * G * m.num_pre, dtype=torch.int32, device="cuda")
+        n = G * m.num_pre   # counts, cursor, then one sum per 4096-count scan tile
+        self.scratch = torch.zeros(2 * n + (n + 4095) // 4096 + 1, dtype=torch.int32, device="cuda")
         self.total = torch.zeros(1, dtype=torch.int32, device="cuda")
 
     def ensure(self, edges: int) -> None:
@@ -414,10 +415,12 @@ class EpropClassifierTrainer:
         pr.psi_t, pr.lsig_t = self.psi_t.data_ptr(), self.lsig_t.data_ptr()
         pr.g_w_out, pr.g_b_out = self.g_w_out.data_ptr(), self.g_b_out.data_ptr()
         pr.ro_partial = self._ro_partial.data_ptr()
+        pr.defer_reduce = 1   # readout partials summed once per batch (_finish)
         _lib.call("sw_eprop_prep", ctypes.byref(pr), st)
         self._tsegs[0] = self.plan_in.tseg([self.xbar_all[t0 + j] for j in range(k)])
         self._tsegs[1] = self.plan_rec.tseg([self.zbar_t[j] for j in range(k)])
         tp.scratch = self._pass_scratch_ptr()
+        tp.defer_reduce = 1   # split partials summed into the gradients once per batch (_finish)
         _lib.call("sw_eprop_pass", ctypes.cast(self._tsegs, ctypes.c_void_p), 2, ctypes.byref(tp),
                   L, b32, r32, a32, st)
 
@@ -573,7 +576,7 @@ class EpropClassifierTrainer:
         for m, syn, tw, key in ((self.m_in, self.s_in, self.tw_in, "in"), (self.m_rec, self.s_rec, self.tw_rec, "rec")):
             _lib.call("sw_clf_pack_rows", m.row_length.data_ptr(), m.target.data_ptr(),
                       syn.planes["w"].data_ptr(), m.num_pre, m.stride, self._tw_stride[key], tw.data_ptr(), st)
-        for x in [self.v, self.a, self.z, self.y, self.pi_sum, self.loss_b] + self._slot_zbar + self._slot_xbar:
+        for x in (self.v, self.a, self.z, self.y, self.pi_sum, self.loss_b, self._slots_zbar, self._slots_xbar):
             x.zero_()
         ip = _lib.ClfInputs()
         ip.steps, ip.batch, ip.ldb = self.task.example_steps, self.local_b, self.plan_in.ldb
@@ -591,9 +594,27 @@ class EpropClassifierTrainer:
                 _lib.call("sw_gather_f64", syn.planes["grad"].data_ptr(), plan.off.data_ptr(),
                           plan.e_pad, plan.grad.data_ptr(), st)
 
+    def reduce_partials(self) -> None:
+        """Add the batch's deferred e-prop split partials and readout partials
+        to the gradients (sw_eprop_pass_reduce / sw_eprop_prep_reduce; both
+        zero the partials for the next batch)."""
+        st = _lib.stream_ptr()
+        if self._pass_scratch is not None:
+            self._tsegs[0] = self.plan_in.tseg([])
+            self._tsegs[1] = self.plan_rec.tseg([])
+            _lib.call("sw_eprop_pass_reduce", ctypes.cast(self._tsegs, ctypes.c_void_p), 2, self.plan_in.ldb,
+                      self._pass_scratch.data_ptr(), st)
+        pr = _lib.EpropPrep()
+        pr.k, pr.batch, pr.ldb = EPROP_BLOCK_STEPS, self.local_b, self.plan_in.ldb
+        pr.num_inputs, pr.hidden, pr.num_classes = self.task.num_inputs, self.hidden, self.task.num_classes
+        pr.g_w_out, pr.g_b_out = self.g_w_out.data_ptr(), self.g_b_out.data_ptr()
+        pr.ro_partial = self._ro_partial.data_ptr()
+        _lib.call("sw_eprop_prep_reduce", ctypes.byref(pr), st)
+
     def _finish(self, learn: bool):
         st = _lib.stream_ptr()
         if learn:
+            self.reduce_partials()
             for plan, syn in ((self.plan_in, self.s_in), (self.plan_rec, self.s_rec)):
                 _lib.call("sw_scatter_f64", syn.planes["grad"].data_ptr(), plan.off.data_ptr(),
                           plan.e_pad, plan.grad.data_ptr(), st)

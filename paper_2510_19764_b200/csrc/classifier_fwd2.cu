@@ -2,7 +2,7 @@
 // (sparsewire/classifier.py:63-67, 196-234).
 //
 // The input spikes and the input traces xbar do not depend on the network
-// state, so one launch per batch (k_clf_inputs) draws every input spike of
+// state, so two launches per batch (sw_clf_inputs) draw every input spike of
 // the trial from the examples' counter streams (u = uniform01 #(t*NI + k) <
 // p_k, as the exact integer compare (h >> 11) < ceil(p_k * 2^53)) and runs
 // the xbar recursion: spike words in_bits[t][b][k/32] for the forward pass,
@@ -54,46 +54,63 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // ------------------------------------------------------------- inputs ----
-// block = 32 replicas (lane) x 64 inputs (8 per warp), all T steps
-__global__ void __launch_bounds__(256) k_clf_inputs(const sw_clf_inputs_t P) {
-  __shared__ uint32_t s_bits[32][2];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int b = blockIdx.y * 32 + lane;
-  const int xb0 = blockIdx.x * 64, x0 = xb0 + warp * 8;
-  const int NI = P.num_inputs;
-  const bool bok = b < P.batch;
-  uint64_t thr[8];
-  float xb[8];
-  const uint64_t key = bok ? P.ex_key[b] : 0ull;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int x = x0 + j;
-    thr[j] = (bok && x < NI) ? (uint64_t)ceil(P.p_in[(int64_t)b * NI + x] * 0x1p53) : 0ull;
-    xb[j] = 0.0f;
+// (1) spike words: block = (replica, kSpkSteps steps), thread = (step, word of
+//     32 inputs) flattened so every lane has a word; the replica's spike
+//     thresholds ceil(p * 2^53) in shared memory
+//     (u01(h) < p  <=>  (h >> 11) < ceil(p * 2^53), both sides exact)
+constexpr int kSpkSteps = 32;
+__global__ void __launch_bounds__(256) k_clf_spikes(const sw_clf_inputs_t P) {
+  extern __shared__ uint64_t s_thr[];
+  const int NI = P.num_inputs, W = P.words;
+  const int b = blockIdx.x;
+  const uint64_t key = __ldg(P.ex_key + b);
+  for (int x = threadIdx.x; x < NI; x += blockDim.x) s_thr[x] = (uint64_t)ceil(__ldg(P.p_in + (int64_t)b * NI + x) * 0x1p53);
+  __syncthreads();
+  const int t0 = blockIdx.y * kSpkSteps;
+  const int items = min(kSpkSteps, P.steps - t0) * W;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int tt = it / W, w = it - tt * W, t = t0 + tt;
+    const int n = min(32, NI - w * 32);
+    const uint64_t* thr = s_thr + w * 32;
+    const uint64_t c0 = (uint64_t)t * (uint64_t)NI + (uint64_t)(w * 32);
+    uint32_t bits = 0;
+#pragma unroll 4
+    for (int j = 0; j < n; ++j)
+      if ((sw::draw(key, c0 + j) >> 11) < thr[j]) bits |= 1u << j;
+    P.in_bits[((int64_t)t * P.batch + b) * W + w] = bits;
   }
+}
+
+// (2) the xbar recursion (classifier.py:212-213): block = (word of 32 inputs,
+//     32 replicas), warp = input, lane = replica, steps in order; the
+//     block's spike words staged through shared memory kXbSteps steps at a
+//     time (one load per (step, replica) instead of one per input), xbar
+//     written replica-minor
+constexpr int kXbSteps = 32;
+__global__ void __launch_bounds__(1024) k_clf_xbar(const sw_clf_inputs_t P) {
+  __shared__ uint32_t s_w[kXbSteps][33];
+  const int NI = P.num_inputs;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int w = blockIdx.x;
+  const int b = blockIdx.y * 32 + lane;
+  const int x = w * 32 + warp;
+  const bool bok = b < P.batch;
   const int64_t plane = (int64_t)NI * P.ldb;
-  for (int t = 0; t < P.steps; ++t) {
-    if (threadIdx.x < 64) s_bits[threadIdx.x >> 1][threadIdx.x & 1] = 0u;
+  const int64_t tstride = (int64_t)P.batch * P.words;
+  const uint32_t* wp = P.in_bits + (int64_t)(bok ? b : 0) * P.words + w;
+  float* out = P.xbar_t + (int64_t)x * P.ldb + b;
+  float xb = 0.0f;
+  for (int t0 = 0; t0 < P.steps; t0 += kXbSteps) {
+    const int nt = min(kXbSteps, P.steps - t0);
     __syncthreads();
-    unsigned f = 0;
-    const uint64_t c0 = (uint64_t)t * (uint64_t)NI + (uint64_t)x0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int x = x0 + j;
-      if (x < NI) {
-        const bool sp = bok && (sw::draw(key, c0 + j) >> 11) < thr[j];
-        xb[j] = __fadd_rn(__fmul_rn(xb[j], P.alpha), sp ? 1.0f : 0.0f);
-        if (b < P.ldb) P.xbar_t[t * plane + (int64_t)x * P.ldb + b] = bok ? xb[j] : 0.0f;
-        if (sp) f |= 1u << j;
+    if (warp < nt) s_w[warp][lane] = bok ? __ldg(wp + (int64_t)(t0 + warp) * tstride) : 0u;
+    __syncthreads();
+    if (x < NI) {
+      for (int tt = 0; tt < nt; ++tt) {
+        const bool sp = (s_w[tt][lane] >> warp) & 1u;
+        xb = __fadd_rn(__fmul_rn(xb, P.alpha), sp ? 1.0f : 0.0f);
+        out[(int64_t)(t0 + tt) * plane] = bok ? xb : 0.0f;
       }
-    }
-    if (f) atomicOr(&s_bits[lane][warp >> 2], f << ((warp & 3) * 8));
-    __syncthreads();
-    if (threadIdx.x < 64) {
-      const int bl = threadIdx.x >> 1, wd = threadIdx.x & 1;
-      const int bb = blockIdx.y * 32 + bl, word = xb0 / 32 + wd;
-      if (bb < P.batch && word < P.words)
-        P.in_bits[((int64_t)t * P.batch + bb) * P.words + word] = s_bits[bl][wd];
     }
   }
 }
@@ -469,8 +486,18 @@ extern "C" int sw_clf_inputs(const sw_clf_inputs_t* p, void* stream) {
     return SW_ERR_INVALID_ARG;
   }
   if (p->steps == 0) return SW_OK;
-  dim3 grid((p->num_inputs + 63) / 64, (p->ldb + 31) / 32);
-  k_clf_inputs<<<grid, 256, 0, (cudaStream_t)stream>>>(*p);
+  const size_t thr_bytes = (size_t)p->num_inputs * 8;
+  if (thr_bytes > 200 * 1024) {
+    sw::set_last_error("sw_clf_inputs: num_inputs > 25600 (spike thresholds are staged in shared memory)");
+    return SW_ERR_INVALID_ARG;
+  }
+  if (thr_bytes > 48 * 1024)
+    cudaFuncSetAttribute(k_clf_spikes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)thr_bytes);
+  dim3 grid1(p->batch, (p->steps + kSpkSteps - 1) / kSpkSteps);
+  k_clf_spikes<<<grid1, 256, thr_bytes, (cudaStream_t)stream>>>(*p);
+  sw::count_launch();
+  dim3 grid2(p->words, (p->ldb + 31) / 32);
+  k_clf_xbar<<<grid2, 1024, 0, (cudaStream_t)stream>>>(*p);
   sw::count_launch();
   SW_CHECK_LAUNCH("sw_clf_inputs");
   return SW_OK;

@@ -58,41 +58,73 @@ __global__ void k_bucket_count(const int32_t* row_length, const int32_t* target,
   }
 }
 
-// single-block exclusive scan (in place), n up to a few million
-__global__ void k_scan_excl(int32_t* a, int n, int32_t* total) {
-  __shared__ int32_t warp_sums[32];
-  __shared__ int32_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
+// exclusive scan of the bucket counts in three launches: per-tile scan
+// (kScanTile elements per 1024-thread block) with tile sums, a one-block scan
+// of the tile sums (+ the total), then tile offsets added while the cursor
+// copy is written
+constexpr int kScanTile = 4096;
+__device__ __forceinline__ int block_scan_1024(int v, int* warp_sums, int* block_total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int base = 0; base < n; base += blockDim.x) {
-    const int x = base + threadIdx.x;
-    const int v = x < n ? a[x] : 0;
-    int inc = v;
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(SW_FULL_MASK, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) warp_sums[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < (blockDim.x >> 5) ? warp_sums[lane] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(SW_FULL_MASK, inc, o);
-      if (lane >= o) inc += t;
+      const int t = __shfl_up_sync(SW_FULL_MASK, w, o);
+      if (lane >= o) w += t;
     }
-    if (lane == 31) warp_sums[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-      int w = lane < (blockDim.x >> 5) ? warp_sums[lane] : 0;
+    warp_sums[lane] = w;   // inclusive
+  }
+  __syncthreads();
+  const int before = warp ? warp_sums[warp - 1] : 0;
+  *block_total = warp_sums[31];
+  __syncthreads();
+  return before + inc - v;   // exclusive
+}
+
+__global__ void __launch_bounds__(1024) k_scan_tiles(int32_t* a, int n, int32_t* tile_sum) {
+  __shared__ int warp_sums[32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 4;
+  int v[4], s = 0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(SW_FULL_MASK, w, o);
-        if (lane >= o) w += t;
-      }
-      warp_sums[lane] = w;   // inclusive
-    }
-    __syncthreads();
-    const int before = carry + (warp ? warp_sums[warp - 1] : 0);
-    if (x < n) a[x] = before + inc - v;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = before + inc;
-    __syncthreads();
+  for (int u = 0; u < 4; ++u) { v[u] = base + u < n ? a[base + u] : 0; s += v[u]; }
+  int tot;
+  int ex = block_scan_1024(s, warp_sums, &tot);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (base + u < n) a[base + u] = ex;
+    ex += v[u];
+  }
+  if (threadIdx.x == 0) tile_sum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_sums(int32_t* tile_sum, int nt, int32_t* total) {
+  __shared__ int warp_sums[32];
+  int carry = 0;
+  for (int b0 = 0; b0 < nt; b0 += 1024) {
+    const int x = b0 + threadIdx.x;
+    const int v = x < nt ? tile_sum[x] : 0;
+    int tot;
+    const int ex = block_scan_1024(v, warp_sums, &tot);
+    if (x < nt) tile_sum[x] = carry + ex;
+    carry += tot;
   }
   if (threadIdx.x == 0 && total) *total = carry;
+}
+
+__global__ void k_scan_add(int32_t* a, int n, const int32_t* tile_sum, int32_t* copy) {
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+    const int v = a[x] + tile_sum[x / kScanTile];
+    a[x] = v;
+    copy[x] = v;
+  }
 }
 
 __global__ void k_bucket_fill(const int32_t* row_length, const int32_t* target, int P, int S,
@@ -155,7 +187,7 @@ extern "C" int sw_eprop_plan(const int32_t* row_length, const int32_t* target, i
                              int32_t stride, int32_t num_post, int32_t shift, int32_t* scratch,
                              int32_t* out_pre, int32_t* out_post, int32_t* out_off,
                              int32_t e_pad, int32_t* total, void* stream) {
-  // scratch: 2 * G * num_pre int32 (counts/offsets, cursor)
+  // scratch: counts/offsets [n], cursor [n], scan tile sums [ceil(n/4096)]
   cudaStream_t st = (cudaStream_t)stream;
   const int G = ((num_post - 1) >> shift) + 1;
   const int n = G * num_pre;
@@ -164,8 +196,11 @@ extern "C" int sw_eprop_plan(const int32_t* row_length, const int32_t* target, i
   cudaMemsetAsync(counts, 0, (size_t)n * 4, st);
   if (num_pre > 0) {
     k_bucket_count<<<grid1(num_pre), 256, 0, st>>>(row_length, target, num_pre, stride, shift, counts); sw::count_launch();
-    k_scan_excl<<<1, 1024, 0, st>>>(counts, n, total); sw::count_launch();
-    cudaMemcpyAsync(cursor, counts, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
+    const int nt = (n + kScanTile - 1) / kScanTile;
+    int32_t* tile_sum = cursor + n;
+    k_scan_tiles<<<nt, 1024, 0, st>>>(counts, n, tile_sum); sw::count_launch();
+    k_scan_sums<<<1, 1024, 0, st>>>(tile_sum, nt, total); sw::count_launch();
+    k_scan_add<<<grid1(n), 256, 0, st>>>(counts, n, tile_sum, cursor); sw::count_launch();
     k_bucket_fill<<<grid1(num_pre), 256, 0, st>>>(row_length, target, num_pre, stride, shift, cursor,
                                                   out_pre, out_post, out_off); sw::count_launch();
   } else {

@@ -151,20 +151,25 @@ __global__ void __launch_bounds__(256) k_prep(const sw_eprop_prep_t P) {
           for (int u = 0; u < CP; ++u) acc[u] = __dadd_rn(acc[u], __dmul_rn(dg[u * kBT + b], z));
         }
 #pragma unroll
-        for (int u = 0; u < CP; ++u) part[(int64_t)(cg * CP + u) * H + h0 + r] = acc[u];
+        for (int u = 0; u < CP; ++u) {
+          double* pp = part + (int64_t)(cg * CP + u) * H + h0 + r;
+          *pp = P.defer_reduce ? __dadd_rn(*pp, acc[u]) : acc[u];
+        }
       } else {
         const int cper = (C + 3) / 4, ca = cg * cper, cb = min(C, ca + cper);
         for (int c = ca; c < cb; ++c) {
           double acc = 0.0;
           for (int b = 0; b < kBT; ++b) acc = __dadd_rn(acc, __dmul_rn(dt[c * kBT + b], (double)tile[b][r]));
-          part[(int64_t)c * H + h0 + r] = acc;
+          double* pp = part + (int64_t)c * H + h0 + r;
+          *pp = P.defer_reduce ? __dadd_rn(*pp, acc) : acc;
         }
       }
     }
     if (ht == 0 && tid < C) {
       double sb = 0.0;
       for (int b = 0; b < kBT; ++b) sb = __dadd_rn(sb, dt[tid * kBT + b]);
-      part[(int64_t)C * H + tid] = sb;
+      double* pp = part + (int64_t)C * H + tid;
+      *pp = P.defer_reduce ? __dadd_rn(*pp, sb) : sb;
     }
   }
 }
@@ -187,9 +192,15 @@ __global__ void __launch_bounds__(256) k_readout_reduce(const sw_eprop_prep_t P,
 #pragma unroll
       for (int u = 0; u < 8; ++u) v[u] = __ldcg(P.ro_partial + (q + u) * stride + x);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+      for (int u = 0; u < 8; ++u) {
+        s = __dadd_rn(s, v[u]);
+        P.ro_partial[(q + u) * stride + x] = 0.0;
+      }
     }
-    for (; q < q1; ++q) s = __dadd_rn(s, __ldcg(P.ro_partial + q * stride + x));
+    for (; q < q1; ++q) {
+      s = __dadd_rn(s, __ldcg(P.ro_partial + q * stride + x));
+      P.ro_partial[q * stride + x] = 0.0;
+    }
   }
   ws8[warp][lane] = s;
   __syncthreads();
@@ -228,6 +239,7 @@ struct TPass {
   int ldb, splits, chunks_per_split;
   float beta, rho, alpha;
   unsigned long long nz;   // (-0.0f, -0.0f)
+  int defer;               // partials accumulate over passes; sw_eprop_pass_reduce adds them
   int dbg;   // measurement only (SW_EPT_DBG): 1 = every synapse reads pre/post 0 (L1-resident inputs), 2 = no state traffic
 };
 
@@ -285,8 +297,11 @@ __global__ void k_grad_reduce(const TPass T) {
     double* grad = first ? T.s[0].grad : T.s[1].grad;
     const int e = (first ? tile : tile - tiles0) * SPW + sl;
     double gr = grad[e];
-    for (int q = 0; q < T.splits; ++q)
-      gr = __dadd_rn(gr, __ldcg(T.partial + ((int64_t)tile * T.splits + q) * SPW + sl));
+    for (int q = 0; q < T.splits; ++q) {
+      double* pp = T.partial + ((int64_t)tile * T.splits + q) * SPW + sl;
+      gr = __dadd_rn(gr, __ldcg(pp));
+      *pp = 0.0;
+    }
     grad[e] = gr;
   }
 }
@@ -405,7 +420,10 @@ __global__ void __launch_bounds__(kTW * 32, MB) k_eprop_t(const TPass T) {
 #pragma unroll
     for (int o = 1; o < LPS; o <<= 1) acc = __dadd_rn(acc, __shfl_xor_sync(SW_FULL_MASK, acc, o));
     // this split's partial; k_grad_reduce adds the splits in order
-    if (g == 0) T.partial[((int64_t)tile * T.splits + split) * SPW + sl] = acc;
+    if (g == 0) {
+      double* pp = T.partial + ((int64_t)tile * T.splits + split) * SPW + sl;
+      *pp = T.defer ? __dadd_rn(*pp, acc) : acc;   // deferred: the batch's passes in order
+    }
   }
 }
 
@@ -439,12 +457,24 @@ extern "C" int sw_eprop_prep(const sw_eprop_prep_t* p, void* stream) {
   if (p->num_classes == 20) k_prep<20><<<grid, 256, smem, st>>>(*p);   // the SHD-shaped task
   else k_prep<0><<<grid, 256, smem, st>>>(*p);
   sw::count_launch();
-  if (p->g_w_out) {
+  if (p->g_w_out && !p->defer_reduce) {
     const int n = p->num_classes * p->hidden + p->num_classes;
     k_readout_reduce<<<(n + 31) / 32, 256, 0, st>>>(*p, p->k * (int)grid.y);
     sw::count_launch();
   }
   SW_CHECK_LAUNCH("sw_eprop_prep");
+  return SW_OK;
+}
+
+extern "C" int sw_eprop_prep_reduce(const sw_eprop_prep_t* p, void* stream) {
+  if (!p || !p->g_w_out || !p->g_b_out || !p->ro_partial || p->k < 1 || p->ldb < 32) {
+    sw::set_last_error("sw_eprop_prep_reduce: readout gradients, partials and the group's k / ldb required");
+    return SW_ERR_INVALID_ARG;
+  }
+  const int n = p->num_classes * p->hidden + p->num_classes;
+  k_readout_reduce<<<(n + 31) / 32, 256, 0, (cudaStream_t)stream>>>(*p, p->k * ((p->ldb + kBT - 1) / kBT));
+  sw::count_launch();
+  SW_CHECK_LAUNCH("sw_eprop_prep_reduce");
   return SW_OK;
 }
 
@@ -503,6 +533,7 @@ extern "C" int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const 
   T.rho = rho;
   T.alpha = alpha;
   T.nz = 0x8000000080000000ull;
+  T.defer = p->defer_reduce != 0;
   {
     static const int dbg = [] { const char* e = getenv("SW_EPT_DBG"); return e ? atoi(e) : 0; }();
     T.dbg = dbg;
@@ -542,11 +573,34 @@ extern "C" int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const 
     default: sw::set_last_error("sw_eprop_pass: k"); return SW_ERR_INVALID_ARG;
   }
   sw::count_launch();
-  {
+  if (!T.defer) {
     const int n = tiles * kSPW;
     k_grad_reduce<kSPW><<<(n + 255) / 256, 256, 0, st>>>(T);
+    sw::count_launch();
   }
-  sw::count_launch();
   SW_CHECK_LAUNCH("sw_eprop_pass");
+  return SW_OK;
+}
+
+extern "C" int sw_eprop_pass_reduce(const sw_eprop_tseg_t* segs, int32_t n_segs, int32_t ldb, void* scratch,
+                                    void* stream) {
+  if (n_segs < 1 || n_segs > 2 || ldb < 32 || ldb % 32 || !scratch) {
+    sw::set_last_error("sw_eprop_pass_reduce: 1 or 2 segments, ldb a multiple of 32, scratch");
+    return SW_ERR_INVALID_ARG;
+  }
+  TPass T{};
+  int etot = 0;
+  for (int i = 0; i < n_segs; ++i) {
+    T.s[i].grad = segs[i].grad;
+    T.s[i].tiles = segs[i].e_pad / kSPW;
+    etot += segs[i].e_pad;
+  }
+  T.splits = (ldb + 63) / 64;
+  T.partial = (double*)scratch;
+  const int n = etot;
+  if (n == 0) return SW_OK;
+  k_grad_reduce<kSPW><<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(T);
+  sw::count_launch();
+  SW_CHECK_LAUNCH("sw_eprop_pass_reduce");
   return SW_OK;
 }
