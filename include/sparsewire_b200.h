@@ -414,6 +414,10 @@ typedef struct sw_clf_step {
   /* precomputed input spikes (sw_clf_inputs), grouped launches only:
    * in_bits[t][batch][in_words]; NULL = the kernel draws them itself */
   const uint32_t* in_bits; int32_t in_words;
+  /* with in_bits: [n_steps][batch][ceil(hidden/32)] scratch for the hidden
+   * spike words of the launch's steps; the readout / softmax of those steps
+   * then runs as a second launch (k_clf_readout) over all of them at once */
+  uint32_t* z_bits;
 } sw_clf_step_t;
 /* The trial's input side at once (classifier.py:63-67, 210-213): every input
  * spike of steps 0..steps-1 from the examples' counter streams, as words

@@ -119,7 +119,7 @@ class ClfStep(C.Structure):
                 ("alpha", F32), ("rho", F32), ("beta", F32), ("v_thr", F32), ("alpha64", F64),
                 ("zbar_in", P), ("xbar_in", P), ("n_steps", I32), ("slot_count", I32),
                 ("in_tw", P), ("rec_tw", P), ("in_tw_stride", I32), ("rec_tw_stride", I32),
-                ("in_bits", P), ("in_words", I32)]
+                ("in_bits", P), ("in_words", I32), ("z_bits", P)]
 
 
 class ClfInputs(C.Structure):

@@ -327,6 +327,9 @@ class EpropClassifierTrainer:
         T = self.task.example_steps
         self._in_words = (NI + 31) // 32
         self.in_bits = torch.zeros((T, B, self._in_words), dtype=torch.int32, device="cuda")
+        # hidden spike words of one grouped launch (its readout runs after it)
+        self.z_bits = torch.zeros((2 * EPROP_BLOCK_STEPS, B, (self.hidden + 31) // 32), dtype=torch.int32,
+                                  device="cuda")
         self.xbar_all = torch.zeros((T, NI, L), **f32)
         nb = int(_lib.lib().sw_eprop_prep_scratch_bytes(K, B, H, C))
         self._ro_partial = torch.zeros(nb // 8 + 1, **f64)
@@ -378,6 +381,7 @@ class EpropClassifierTrainer:
         # spikes and traces come from sw_clf_inputs
         s.lsig = 0
         s.in_bits, s.in_words = self.in_bits.data_ptr(), self._in_words
+        s.z_bits = self.z_bits.data_ptr()
         return s
 
     def _slot(self, t: int) -> dict:
@@ -507,12 +511,12 @@ class EpropClassifierTrainer:
         self.steps_launched += T
 
     def kernels_per_trial(self, learn: bool = True) -> int:
-        """One grouped forward launch and (learning) one e-prop pass per
-        EPROP_BLOCK_STEPS timesteps."""
+        """Per EPROP_BLOCK_STEPS timesteps: the grouped forward launch and its
+        readout launch, and (learning) the e-prop prep and pass (their
+        reductions run once per batch)."""
         T = self.task.example_steps
         groups = -(-T // EPROP_BLOCK_STEPS)
-        # learning: forward + prep (+ readout reduction) + pass
-        return groups * (4 if learn else 1)
+        return groups * (4 if learn else 2)
 
     def _run_trial(self, learn: bool) -> None:
         if not self.use_graph:

@@ -49,7 +49,7 @@ __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.syn
 
 // row groups of the event-driven current sums (see P2b)
 __host__ __device__ inline int fwd_groups(int H) {
-  return H <= 256 ? 8 : (H <= 512 ? 4 : 2);   // classifier_fwd2.cu fwd2_groups: the same groups
+  return H <= 256 ? 8 : 4;   // classifier_fwd2.cu fwd2_groups: the same groups
 }
 
 // bytes of the dynamic shared-memory layout

@@ -12,17 +12,19 @@
 // The forward kernel (k_clf_fwd2, block per replica, a group of steps per
 // launch, state in registers) then only builds its spiking-row lists from
 // those words and the hidden spikes:
-//   A  hidden spikes -> ascending list (warp ballots, one barrier);
-//   B  warp 6 builds step t+1's input-row list from its spike words and
-//      issues its rows' bulk copies into the other staging buffer, so the
-//      copies of the next step land while this step computes;
+//   A  hidden spikes -> ascending list (warp ballots, one barrier); the
+//      spike words also go to z_bits for the readout launch;
+//   B  warp 6 builds step t+1's ascending input-row list from its spike
+//      words while this step computes (two list buffers);
 //   C  the ascending input rows and hidden rows are split into G ordered
-//      groups each (warp g sums group g of both into its partial rows: input
-//      rows from the staged copies, hidden rows straight from the packed
-//      rows); the readout and softmax of a step run on the last warp during
-//      the next step's list building (nothing in a step reads them);
+//      groups each (warp g sums group g of both into its partial rows, rows
+//      read from the packed (target, weight) rows, kRowsAhead rows' entries
+//      loaded before any is added);
 //   D  per post the group partials are added in group order, the ALIF step
 //      and the surrogate (neurons.py:60-73).
+// The readout / softmax of all the launch's steps then runs as one launch
+// (k_clf_readout): the steps' weight sums are independent, so their load
+// latencies overlap instead of sitting on the forward pass's step chain.
 // Every output is bit-identical to k_clf_fwd's (classifier_fwd.cu): the same
 // per-post current sums (groups of the ascending rows, group order), the same
 // readout / softmax / ALIF arithmetic.
@@ -46,12 +48,7 @@ __device__ int g_fwd2_prof_on;
 #endif
 
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 
 // ------------------------------------------------------------- inputs ----
 // (1) spike words: block = (replica, kSpkSteps steps), thread = (step, word of
@@ -117,74 +114,85 @@ __global__ void __launch_bounds__(1024) k_clf_xbar(const sw_clf_inputs_t P) {
 
 // ------------------------------------------------------------ forward ----
 // row groups of the current sums: 8 / (hidden units per thread)
-__host__ __device__ inline int fwd2_groups(int H) { return H <= 256 ? 8 : (H <= 512 ? 4 : 2); }
+__host__ __device__ inline int fwd2_groups(int H) { return H <= 256 ? 8 : 4; }
+static_assert(SW_EPROP_MAX_BLOCK * 2 <= 16, "spike-word slots");
 
 __host__ __device__ inline size_t fwd2_fixed_bytes(int H, int NI, int C) {
   const size_t NT = (size_t)NI + H;
   size_t o = (size_t)2 * fwd2_groups(H) * H * 4;   // input / hidden partial rows
   o += NT * 4;                                      // rlen
-  o += (size_t)2 * NI * 4 + (size_t)2 * (NI + 1) * 4;   // input lists, offsets (2 buffers)
-  o += (size_t)H * 4 + (size_t)(H + 1) * 4;         // hidden list, offsets (unused slots)
+  o += (size_t)2 * NI * 4;                          // input lists (2 buffers)
+  o += (size_t)2 * H * 4;                           // hidden lists (2 buffers)
   o = (o + 15) & ~(size_t)15;
-  o += (size_t)4 * C * 8;                           // y, pi_sum, d, b_out
-  o += 32;                                          // 2 mbarriers
   o += (size_t)SW_EPROP_MAX_BLOCK * 2 * ((NI + 31) / 32) * 4;   // the launch's input spike words
   return o;
 }
 
-// NTH threads per replica block (256, or 128 to leave room on the SM for a
-// concurrent e-prop pass); GT row groups (== fwd2_groups(H)), warp w sums
-// groups w, w + NTH/32, ... (the same numbers for any NTH)
+// dst[target] += weight over the packed rows list[r0..r1) in order, one
+// warp: the entries of kRowsAhead rows loaded before any is added (lane =
+// entry), so their L2 latencies overlap
+constexpr int kRowsAhead = 4;
+__device__ __forceinline__ void sum_rows(const int* list, int r0, int r1, const int* rl, const int2* base,
+                                         int stride, float* dst, int lane) {
+  for (int r = r0; r < r1; r += kRowsAhead) {
+    int2 tw[kRowsAhead];
+    int len[kRowsAhead];
+    const int2* e[kRowsAhead];
+#pragma unroll
+    for (int u = 0; u < kRowsAhead; ++u) {
+      len[u] = 0;
+      e[u] = base;
+      if (r + u < r1) {
+        const int x = list[r + u];
+        len[u] = rl[x];
+        e[u] = base + (int64_t)x * stride;
+      }
+      tw[u] = make_int2(0, 0);
+      if (lane < len[u]) tw[u] = __ldg(e[u] + lane);
+    }
+#pragma unroll
+    for (int u = 0; u < kRowsAhead; ++u) {
+      if (lane < len[u]) dst[tw[u].x] = __fadd_rn(dst[tw[u].x], __int_as_float(tw[u].y));
+      for (int q = lane + 32; q < len[u]; q += 32) {
+        const int2 t2 = __ldg(e[u] + q);
+        dst[t2.x] = __fadd_rn(dst[t2.x], __int_as_float(t2.y));
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// NTH threads per replica block, HPT hidden units per thread; GT row groups
+// (== fwd2_groups(H)), warp w sums group w
 template <int NTH, int HPT, int GT>
-__global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, int stage) {
+__global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int kT2 = NTH, kW2 = NTH / 32;
   constexpr int G = GT;
-  const int H = P.hidden, NI = P.num_inputs, C = P.num_classes;
+  const int H = P.hidden, NI = P.num_inputs;
   const int NT = NI + H;
   size_t o = 0;
   float* pin = (float*)(smem_raw + o);   o += (size_t)G * H * 4;
   float* prc = (float*)(smem_raw + o);   o += (size_t)G * H * 4;
   int* rlen = (int*)(smem_raw + o);      o += (size_t)NT * 4;
-  int* lin = (int*)(smem_raw + o);       o += (size_t)2 * NI * 4;        // [2][NI]
-  int* soin = (int*)(smem_raw + o);      o += (size_t)2 * (NI + 1) * 4;  // [2][NI + 1]
+  int* lin = (int*)(smem_raw + o);       o += (size_t)2 * NI * 4;        // [2][NI] input lists
   int* lhb = (int*)(smem_raw + o);       o += (size_t)2 * H * 4;         // [2][H] hidden lists
-  o += 4;
   o = (o + 15) & ~(size_t)15;
-  double* yv = (double*)(smem_raw + o);
-  double* pis = yv + C;
-  double* dv = pis + C;
-  double* bo = dv + C;
-  o += (size_t)4 * C * 8;
-  uint64_t* sbar = (uint64_t*)(smem_raw + o); o += 32;
   uint32_t* wsm = (uint32_t*)(smem_raw + o);   // [n_steps][in_words] spike words
-  o += (size_t)SW_EPROP_MAX_BLOCK * 2 * ((NI + 31) / 32) * 4;
-  int2* st = (int2*)(smem_raw + o);      // [2][stage]
   __shared__ int s_wcnt[kW2];
-  __shared__ int s_nin[2], s_staged[2], s_nh[2];
-  __shared__ double s_loss;
+  __shared__ int s_nin[2];
 
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int bH = b * H, bC = b * C;
+  const int bH = b * H;
+  const int HW = (H + 31) / 32;
   const int B = P.batch;
   const int nslot = P.slot_count;
   const int nsteps = P.n_steps;
 
   for (int x = tid; x < NT; x += kT2)
     rlen[x] = (x < NI) ? __ldg(P.in_row_length + x) : __ldg(P.rec_row_length + (x - NI));
-  for (int c = tid; c < C; c += kT2) {
-    yv[c] = P.y[bC + c];
-    pis[c] = P.pi_sum[bC + c];
-    bo[c] = P.b_out[c];
-  }
   for (int x = tid; x < G * H; x += kT2) { pin[x] = 0.0f; prc[x] = 0.0f; }
-  if (tid == 0) {
-    s_loss = P.loss[b];
-    sw::mbar_init(&sbar[0], 1);
-    sw::mbar_init(&sbar[1], 1);
-    sw::fence_mbar_init();
-  }
   const int prev = ((P.t - 1) % nslot + nslot) % nslot;
   const float* zin0 = P.zbar + prev * B * H;
   float v[HPT], a[HPT], z[HPT], zb[HPT];
@@ -198,7 +206,6 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
     z[j] = ok ? P.z[bH + h] : 0.f;
     zb[j] = ok ? zin0[bH + h] : 0.f;
   }
-  const int label = P.labels[b];
   const float alpha = P.alpha, rho = P.rho, beta = P.beta, v_thr = P.v_thr;
   // the launch's input spike words (all its steps) into shared memory
   for (int x = tid; x < nsteps * P.in_words; x += kT2) {
@@ -207,13 +214,12 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
   }
   __syncthreads();
 
-  // warp 6 (or the last warp): step t's input-row list from its spike words,
-  // staging offsets, bulk copies into buffer buf
+  // warp 6 (or the last warp): step t's ascending input-row list from its
+  // spike words, into list buffer buf
   const int pw = kW2 - 2;
   auto build_inputs = [&](int t, int buf) {
     const uint32_t* wds = wsm + (t - P.t) * P.in_words;
     int* L = lin + buf * NI;
-    int* O = soin + buf * (NI + 1);
     int n = 0;
     for (int w0 = 0; w0 < P.in_words; w0 += 32) {
       const uint32_t wd = (w0 + lane < P.in_words) ? wds[w0 + lane] : 0u;
@@ -228,88 +234,10 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
       for (uint32_t m = wd; m; m &= m - 1) L[p++] = (w0 + lane) * 32 + __ffs(m) - 1;
       n += __shfl_sync(SW_FULL_MASK, inc, 31);
     }
-    __syncwarp();
-    // staging offsets: padded row lengths, ascending
-    int off = 0;
-    for (int q0 = 0; q0 < n; q0 += 32) {
-      const int q = q0 + lane;
-      const int len = q < n ? ((rlen[L[q]] + 1) & ~1) : 0;
-      int inc = len;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int u = __shfl_up_sync(SW_FULL_MASK, inc, d);
-        if (lane >= d) inc += u;
-      }
-      if (q < n) O[q] = off + inc - len;
-      off += __shfl_sync(SW_FULL_MASK, inc, 31);
-    }
-    const bool staged = off <= stage;
-    if (lane == 0) {
-      O[n] = off;
-      s_nin[buf] = n;
-      s_staged[buf] = staged ? 1 : 0;
-    }
-    __syncwarp();
-    if (lane == 0 && staged) sw::mbar_arrive_expect_tx(&sbar[buf], (uint32_t)off * 8u);
-    __syncwarp();
-    if (staged) {
-      // one bulk copy per row (16-byte multiples: rows padded to even entries)
-      int2* S = st + buf * stage;
-      for (int q = lane; q < n; q += 32) {
-        const int x = L[q];
-        const uint32_t bytes = (uint32_t)((rlen[x] + 1) & ~1) * 8u;
-        if (bytes) sw::bulk_g2s(S + O[q], P.in_tw + (int64_t)x * P.in_tw_stride * 2, bytes, &sbar[buf]);
-      }
-    }
-  };
-  // warp kW2-1: readout y = alpha*y + z @ W_out^T + b (classifier.py:215) of
-  // one step from its hidden list (lane = class, spiking units ascending,
-  // 8 loads in flight), then softmax / cross-entropy / d (plasticity.py:156-165,
-  // classifier.py:216-219).  Nothing else in a step reads its result, so it
-  // runs one step late, beside the next step's list building.
-  auto readout = [&](const int* L, int n, double* d_out) {
-    for (int c0 = 0; c0 < C; c0 += 32) {
-      const int c = c0 + lane;
-      if (c < C) {
-        double sacc = 0.0;
-        const double* wr = P.w_out + (int64_t)c * H;
-        for (int q0 = 0; q0 < n; q0 += 8) {
-          double wv[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) wv[u] = q0 + u < n ? __ldg(wr + L[q0 + u]) : 0.0;
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (q0 + u < n) sacc = __dadd_rn(sacc, wv[u]);
-        }
-        yv[c] = __dadd_rn(__dadd_rn(__dmul_rn(P.alpha64, yv[c]), sacc), bo[c]);
-      }
-    }
-    __syncwarp();
-    double mx = -INFINITY;
-    for (int c = lane; c < C; c += 32) mx = fmax(mx, yv[c]);
-#pragma unroll
-    for (int o2 = 16; o2 > 0; o2 >>= 1) mx = fmax(mx, __shfl_xor_sync(SW_FULL_MASK, mx, o2));
-    double se = 0.0;
-    double ex[2] = {0.0, 0.0};
-    for (int c = lane, u = 0; c < C; c += 32, ++u) {
-      const double e = exp(yv[c] - mx);
-      if (u < 2) ex[u] = e;
-      se += e;
-    }
-#pragma unroll
-    for (int o2 = 16; o2 > 0; o2 >>= 1) se += __shfl_xor_sync(SW_FULL_MASK, se, o2);
-    for (int c = lane, u = 0; c < C; c += 32, ++u) {
-      const double pi = (u < 2 ? ex[u] : exp(yv[c] - mx)) / se;
-      pis[c] = pis[c] + pi;
-      const double dd = pi - (c == label ? 1.0 : 0.0);
-      dv[c] = dd;
-      d_out[bC + c] = dd;
-      if (c == label) s_loss = s_loss + -log(pi);
-    }
+    if (lane == 0) s_nin[buf] = n;
   };
   if (warp == pw) build_inputs(P.t, 0);
   __syncthreads();
-  uint32_t phase = 0;   // bit buf: completed-phase parity of sbar[buf]
 
   for (int s = 0; s < nsteps; ++s) {
     const int t = P.t + s;
@@ -328,6 +256,22 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
       hc += __popc(hm[j]);
     }
     if (lane == 0) s_wcnt[warp] = hc;
+    {
+      // hidden spike words in unit order for the readout launch: warp w holds
+      // units w*32*HPT + HPT*lane + j, so word q of the warp takes bit i*HPT+j
+      // from ballot j's bit q*(32/HPT)+i
+      uint32_t* zw = P.z_bits + ((int64_t)s * B + b) * HW;
+      if (HPT == 1) {
+        if (lane == 0 && warp < HW) zw[warp] = hm[0];
+      } else if (lane < HPT && warp * HPT + lane < HW) {
+        uint32_t wd = 0;
+#pragma unroll
+        for (int j = 0; j < HPT; ++j)
+#pragma unroll
+          for (int i = 0; i < 32 / HPT; ++i) wd |= ((hm[j] >> (lane * (32 / HPT) + i)) & 1u) << (i * HPT + j);
+        zw[warp * HPT + lane] = wd;
+      }
+    }
     __syncthreads();   // B1
     FWD2_PROF(1);
     int hbase = 0, nh = 0;
@@ -348,11 +292,8 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
       for (int j = 0; j < HPT; ++j)
         if ((hm[j] >> lane) & 1u) lh[p++] = h0 + j;
     }
-    if (tid == 0) s_nh[cb] = nh;
-    // ---- B: next step's input rows, staged while this step computes; the
-    // previous step's readout ----
+    // ---- B: next step's input-row list ----
     if (warp == pw && s + 1 < nsteps) build_inputs(t + 1, cb ^ 1);
-    if (warp == kW2 - 1 && s > 0) readout(lhb + (cb ^ 1) * H, s_nh[cb ^ 1], P.d + ((t - 1) % nslot) * B * C);
     // zbar (old z) for the e-prop traces and the readout gradient
 #pragma unroll
     for (int j = 0; j < HPT; ++j) {
@@ -368,40 +309,14 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
 
     // ---- C: ordered group sums of the input rows and the hidden rows ----
     const int nin = s_nin[cb];
-    const bool staged = s_staged[cb] != 0;
-    if (staged) {
-      sw::mbar_wait(&sbar[cb], (phase >> cb) & 1u);
-      phase ^= 1u << cb;
-    }
     FWD2_PROF(4);
     for (int grp = warp; grp < G; grp += kW2) {
-      const int* L = lin + cb * NI;
-      const int* O = soin + cb * (NI + 1);
-      const int2* S = st + cb * stage;
-      float* pg = pin + grp * H;
       const int g0 = nin * grp / G, g1 = nin * (grp + 1) / G;
-      for (int r = g0; r < g1; ++r) {
-        const int x = L[r];
-        const int len = rlen[x];
-        const int2* e = staged ? S + O[r] : reinterpret_cast<const int2*>(P.in_tw + (int64_t)x * P.in_tw_stride * 2);
-        for (int q = lane; q < len; q += 32) {
-          const int2 tw = staged ? e[q] : __ldg(e + q);
-          pg[tw.x] = __fadd_rn(pg[tw.x], __int_as_float(tw.y));
-        }
-        __syncwarp();
-      }
-      float* pr = prc + grp * H;
+      sum_rows(lin + cb * NI, g0, g1, rlen, reinterpret_cast<const int2*>(P.in_tw), P.in_tw_stride,
+               pin + grp * H, lane);
       const int k0 = nh * grp / G, k1 = nh * (grp + 1) / G;
-      for (int r = k0; r < k1; ++r) {
-        const int h = lh[r];
-        const int len = rlen[NI + h];
-        const int2* e = reinterpret_cast<const int2*>(P.rec_tw + (int64_t)h * P.rec_tw_stride * 2);
-        for (int q = lane; q < len; q += 32) {
-          const int2 tw = __ldg(e + q);
-          pr[tw.x] = __fadd_rn(pr[tw.x], __int_as_float(tw.y));
-        }
-        __syncwarp();
-      }
+      sum_rows(lh, k0, k1, rlen + NI, reinterpret_cast<const int2*>(P.rec_tw), P.rec_tw_stride, prc + grp * H,
+               lane);
     }
     FWD2_PROF(5);
     __syncthreads();   // B3: partial rows complete
@@ -437,11 +352,6 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
     // reaches only after finishing this step
   }
 
-  // the last step's readout
-  if (warp == kW2 - 1) {
-    const int tl = P.t + nsteps - 1, bl = (nsteps - 1) & 1;
-    readout(lhb + bl * H, s_nh[bl], P.d + (tl % nslot) * B * C);
-  }
 #pragma unroll
   for (int j = 0; j < HPT; ++j) {
     const int h = h0 + j;
@@ -451,23 +361,146 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P, i
       P.z[bH + h] = z[j];
     }
   }
-  __syncthreads();
-  for (int c = tid; c < C; c += kT2) {
-    P.y[bC + c] = yv[c];
-    P.pi_sum[bC + c] = pis[c];
+}
+
+// ------------------------------------------------------------ readout ----
+// The readout of a grouped launch's steps (classifier.py:215-219,
+// plasticity.py:156-165), block per replica, from the hidden spike words the
+// forward launch wrote:
+//   1  per step, the ascending list of spiking units (warp per step);
+//   2  thread per (step, class): s = sum of w_out[c][h] over the list in
+//      order (f64, from +0.0, 8 loads in flight) -- the steps are
+//      independent here, so their load latencies overlap;
+//   3  warp 0: y = alpha*y + s + b per class, steps in order;
+//   4  warp per step: softmax, d = pi - onehot (written to the step's slot);
+//   5  warp 0: pi_sum and the loss accumulated in step order.
+__host__ __device__ inline size_t readout_smem(int n_steps, int H, int C) {
+  return (size_t)n_steps * H * 4 + (size_t)n_steps * 4 + (size_t)n_steps * C * 8 * 3 + (size_t)C * 8;
+}
+
+__global__ void __launch_bounds__(256) k_clf_readout(const sw_clf_step_t P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int H = P.hidden, C = P.num_classes, B = P.batch, n = P.n_steps;
+  const int HW = (H + 31) / 32;
+  double* s_sum = reinterpret_cast<double*>(smem_raw);      // [n][C]
+  double* s_y = s_sum + (size_t)n * C;                      // [n][C]
+  double* s_pi = s_y + (size_t)n * C;                       // [n][C]
+  double* s_bo = s_pi + (size_t)n * C;                      // [C]
+  int* s_cnt = reinterpret_cast<int*>(s_bo + C);            // [n]
+  int* s_list = s_cnt + n;                                  // [n][H]
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kW = 8;
+  const int bC = b * C;
+  for (int c = tid; c < C; c += blockDim.x) s_bo[c] = P.b_out[c];
+  // 1
+  for (int t = warp; t < n; t += kW) {
+    const uint32_t* zw = P.z_bits + ((int64_t)t * B + b) * HW;
+    int* L = s_list + (size_t)t * H;
+    int cnt = 0;
+    for (int w0 = 0; w0 < HW; w0 += 32) {
+      const uint32_t wd = w0 + lane < HW ? zw[w0 + lane] : 0u;
+      const int c = __popc(wd);
+      int inc = c;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int u = __shfl_up_sync(SW_FULL_MASK, inc, d);
+        if (lane >= d) inc += u;
+      }
+      int p = cnt + inc - c;
+      for (uint32_t m = wd; m; m &= m - 1) L[p++] = (w0 + lane) * 32 + __ffs(m) - 1;
+      cnt += __shfl_sync(SW_FULL_MASK, inc, 31);
+    }
+    if (lane == 0) s_cnt[t] = cnt;
   }
-  if (tid == 0) P.loss[b] = s_loss;
+  __syncthreads();
+  // 2
+  for (int i = tid; i < n * C; i += blockDim.x) {
+    const int t = i / C, c = i - t * C;
+    const int* L = s_list + (size_t)t * H;
+    const int cnt = s_cnt[t];
+    const double* wr = P.w_out + (int64_t)c * H;
+    double sacc = 0.0;
+    for (int q0 = 0; q0 < cnt; q0 += 8) {
+      double wv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) wv[u] = q0 + u < cnt ? __ldg(wr + L[q0 + u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q0 + u < cnt) sacc = __dadd_rn(sacc, wv[u]);
+    }
+    s_sum[i] = sacc;
+  }
+  __syncthreads();
+  // 3
+  if (warp == 0) {
+    for (int c = lane; c < C; c += 32) {
+      double y = P.y[bC + c];
+      for (int t = 0; t < n; ++t) {
+        y = __dadd_rn(__dadd_rn(__dmul_rn(P.alpha64, y), s_sum[t * C + c]), s_bo[c]);
+        s_y[t * C + c] = y;
+      }
+      P.y[bC + c] = y;
+    }
+  }
+  __syncthreads();
+  // 4
+  const int label = P.labels[b];
+  const int nslot = P.slot_count;
+  for (int t = warp; t < n; t += kW) {
+    const double* yv = s_y + (size_t)t * C;
+    double* d_out = P.d + (size_t)((P.t + t) % nslot) * B * C;
+    double mx = -INFINITY;
+    for (int c = lane; c < C; c += 32) mx = fmax(mx, yv[c]);
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) mx = fmax(mx, __shfl_xor_sync(SW_FULL_MASK, mx, o2));
+    double se = 0.0;
+    double ex[2] = {0.0, 0.0};
+    for (int c = lane, u = 0; c < C; c += 32, ++u) {
+      const double e = exp(yv[c] - mx);
+      if (u < 2) ex[u] = e;
+      se += e;
+    }
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) se += __shfl_xor_sync(SW_FULL_MASK, se, o2);
+    for (int c = lane, u = 0; c < C; c += 32, ++u) {
+      const double pi = (u < 2 ? ex[u] : exp(yv[c] - mx)) / se;
+      s_pi[t * C + c] = pi;
+      d_out[bC + c] = pi - (c == label ? 1.0 : 0.0);
+    }
+  }
+  __syncthreads();
+  // 5
+  if (warp == 0) {
+    for (int c = lane; c < C; c += 32) {
+      double ps = P.pi_sum[bC + c];
+      for (int t = 0; t < n; ++t) ps = ps + s_pi[t * C + c];
+      P.pi_sum[bC + c] = ps;
+      if (c == label) {
+        double ls = P.loss[b];
+        for (int t = 0; t < n; ++t) ls = ls + -log(s_pi[t * C + c]);
+        P.loss[b] = ls;
+      }
+    }
+  }
 }
 
 template <int NTH, int HPT, int GT>
-int launch_fwd2(const sw_clf_step_t* p, size_t smem, int stage, cudaStream_t st) {
+int launch_fwd2(const sw_clf_step_t* p, size_t smem, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute((const void*)k_clf_fwd2<NTH, HPT, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     attr = true;
   }
-  k_clf_fwd2<NTH, HPT, GT><<<p->batch, NTH, smem, st>>>(*p, stage);
+  k_clf_fwd2<NTH, HPT, GT><<<p->batch, NTH, smem, st>>>(*p);
+  sw::count_launch();
+  const size_t rsm = readout_smem(p->n_steps, p->hidden, p->num_classes);
+  static size_t rsm_attr = 48 * 1024;
+  if (rsm > rsm_attr) {
+    cudaFuncSetAttribute(k_clf_readout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+    rsm_attr = rsm;
+  }
+  k_clf_readout<<<p->batch, 256, rsm, st>>>(*p);
   sw::count_launch();
   return SW_OK;
 }
@@ -507,29 +540,15 @@ extern "C" int sw_clf_inputs(const sw_clf_inputs_t* p, void* stream) {
 // SW_ERR_INVALID_ARG when the shapes are outside its layout
 int clf_fwd2_launch(const sw_clf_step_t* p, void* stream) {
   const int H = p->hidden, NI = p->num_inputs, C = p->num_classes;
-  if (p->n_steps < 1 || p->n_steps > 2 * SW_EPROP_MAX_BLOCK || !p->in_bits || !p->in_tw || !p->rec_tw || H < 1 || H > 1024 || NI < 1 || C < 1 ||
+  if (p->n_steps < 1 || p->n_steps > 2 * SW_EPROP_MAX_BLOCK || !p->in_bits || !p->z_bits || !p->in_tw || !p->rec_tw || H < 1 || H > 1024 || NI < 1 || C < 1 ||
+      readout_smem(p->n_steps, H, C) > 200 * 1024 ||
       p->in_words != (NI + 31) / 32)
     return SW_ERR_INVALID_ARG;
-  const size_t fixed = fwd2_fixed_bytes(H, NI, C);
-  // threads per replica block: 256, or 128 (SW_FWD_THREADS=128) to leave
-  // registers and shared memory for a concurrent e-prop pass
-  static const int nth = [] {
-    const char* e = getenv("SW_FWD_THREADS");
-    return (e && atoi(e) == 128) ? 128 : 256;
-  }();
-  const int per_sm = 1024 / nth;
-  // staged input entries per buffer: what keeps per_sm blocks per SM
-  const size_t budget = (size_t)(nth == 128 ? 50 : 56) * 1024;
-  int stage = 2048;
-  while (stage > 256 && fixed + (size_t)stage * 16 > budget) stage -= 128;
-  const size_t smem = fixed + (size_t)stage * 16;
-  if (smem > 200 * 1024) return SW_ERR_INVALID_ARG;
-  (void)per_sm;
-  const int G = fwd2_groups(H);
+  // 4 replica blocks per SM (512 replicas in one wave): <= 56 KB each
+  const size_t smem = fwd2_fixed_bytes(H, NI, C);
+  if (smem > 56 * 1024) return SW_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
-  if (nth == 128 && H <= 256) return launch_fwd2<128, 2, 8>(p, smem, stage, st);
-  if (nth == 128 && H <= 512) return launch_fwd2<128, 4, 4>(p, smem, stage, st);
-  if (G == 8) return launch_fwd2<256, 1, 8>(p, smem, stage, st);
-  if (G == 4) return launch_fwd2<256, 2, 4>(p, smem, stage, st);
-  return launch_fwd2<256, 4, 2>(p, smem, stage, st);
+  if (H <= 256) return launch_fwd2<256, 1, 8>(p, smem, st);
+  if (H <= 512) return launch_fwd2<256, 2, 4>(p, smem, st);
+  return launch_fwd2<256, 4, 4>(p, smem, st);
 }

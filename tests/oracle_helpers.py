@@ -67,7 +67,7 @@ def check_topomap_post(fx, k, name, row_length, target, g):
 def fwd_groups(H: int) -> int:
     """Row groups of the forward kernels' event-driven current sums
     (classifier_fwd.cu fwd_groups, classifier_fwd2.cu fwd2_groups)."""
-    return 8 if H <= 256 else (4 if H <= 512 else 2)
+    return 8 if H <= 256 else 4
 
 
 def grouped_currents(rl, tg, w32, spiking, H):
