@@ -262,7 +262,7 @@ SW_API int sw_eprop_fused_step(const sw_eprop_seg_t* segs, int32_t n_segs, const
                                double* g_w_out, double* g_b_out, int32_t num_classes,
                                int32_t max_blocks_per_sm, uint32_t* workspace, void* stream);
 
-#define SW_EPROP_MAX_BLOCK 8
+#define SW_EPROP_MAX_BLOCK 16
 /* k consecutive timesteps (1 <= k <= SW_EPROP_MAX_BLOCK) of the fused step in one pass over
  * the eligibility state (temporal blocking: the forward pass of the k steps
  * runs first, it never reads eps/ebar/grad).  Per step s < k: psi[s],

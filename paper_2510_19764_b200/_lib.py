@@ -37,7 +37,7 @@ P = C.c_void_p
 I32 = C.c_int32
 I64 = C.c_int64
 # SW_EPROP_MAX_BLOCK (include/sparsewire_b200.h): timesteps per blocked e-prop pass
-MAX_BLOCK = 8
+MAX_BLOCK = 16
 U64 = C.c_uint64
 F64 = C.c_double
 F32 = C.c_float

@@ -37,7 +37,7 @@ from .updates import Model
 # timesteps per e-prop pass over the eligibility state (temporal blocking,
 # sw_eprop_fused_block): K forward steps run first, then one pass applies K
 # recursion steps to every (replica, synapse) element
-EPROP_BLOCK_STEPS = int(os.environ.get("SW_EPROP_BLOCK_STEPS", "8"))
+EPROP_BLOCK_STEPS = int(os.environ.get("SW_EPROP_BLOCK_STEPS", "16"))
 if not 1 <= EPROP_BLOCK_STEPS <= _lib.MAX_BLOCK:
     raise ValueError(f"SW_EPROP_BLOCK_STEPS={EPROP_BLOCK_STEPS}: must be in 1..{_lib.MAX_BLOCK} "
                      "(SW_EPROP_MAX_BLOCK in include/sparsewire_b200.h)")

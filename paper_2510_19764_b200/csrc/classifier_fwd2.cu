@@ -115,16 +115,15 @@ __global__ void __launch_bounds__(1024) k_clf_xbar(const sw_clf_inputs_t P) {
 // ------------------------------------------------------------ forward ----
 // row groups of the current sums: 8 / (hidden units per thread)
 __host__ __device__ inline int fwd2_groups(int H) { return H <= 256 ? 8 : 4; }
-static_assert(SW_EPROP_MAX_BLOCK * 2 <= 16, "spike-word slots");
 
-__host__ __device__ inline size_t fwd2_fixed_bytes(int H, int NI, int C) {
+__host__ __device__ inline size_t fwd2_fixed_bytes(int H, int NI, int n_steps) {
   const size_t NT = (size_t)NI + H;
   size_t o = (size_t)2 * fwd2_groups(H) * H * 4;   // input / hidden partial rows
   o += NT * 4;                                      // rlen
   o += (size_t)2 * NI * 4;                          // input lists (2 buffers)
   o += (size_t)2 * H * 4;                           // hidden lists (2 buffers)
   o = (o + 15) & ~(size_t)15;
-  o += (size_t)SW_EPROP_MAX_BLOCK * 2 * ((NI + 31) / 32) * 4;   // the launch's input spike words
+  o += (size_t)n_steps * ((NI + 31) / 32) * 4;      // the launch's input spike words
   return o;
 }
 
@@ -545,7 +544,7 @@ int clf_fwd2_launch(const sw_clf_step_t* p, void* stream) {
       p->in_words != (NI + 31) / 32)
     return SW_ERR_INVALID_ARG;
   // 4 replica blocks per SM (512 replicas in one wave): <= 56 KB each
-  const size_t smem = fwd2_fixed_bytes(H, NI, C);
+  const size_t smem = fwd2_fixed_bytes(H, NI, p->n_steps);
   if (smem > 56 * 1024) return SW_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   if (H <= 256) return launch_fwd2<256, 1, 8>(p, smem, st);

@@ -539,7 +539,7 @@ extern "C" int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const 
     T.dbg = dbg;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  // variant (SW_EPT_CFG = "PD,MB": inputs PD steps ahead, MB blocks per SM)
+  // variant (SW_EPT_CFG = "1,4": inputs 1 step ahead instead of 2)
   static int cfg = -1;
   if (cfg < 0) {
     cfg = 0;
@@ -557,18 +557,15 @@ extern "C" int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const 
     if (blocks * kTW > items) blocks = (items + kTW - 1) / kTW;
     kfn<<<blocks, kTW * 32, 0, st>>>(T);
   };
-  const int want = cfg ? cfg : (kSPW == 8 ? 22 : 24);
+  const int want = cfg ? cfg : 24;
   switch (p->k) {
 #define SW_K(KK)                                                                 \
   case KK:                                                                       \
-    if (want == 13) launch(k_eprop_t<KK, 1, kSPW, 3>);                           \
-    else if (want == 14) launch(k_eprop_t<KK, 1, kSPW, 4>);                      \
-    else if (want == 23) launch(k_eprop_t<KK, 2, kSPW, 3>);                      \
-    else if (want == 24) launch(k_eprop_t<KK, 2, kSPW, 4>);                      \
-    else if (want == 16) launch(k_eprop_t<KK, 1, kSPW, 6>);                      \
-    else launch(k_eprop_t<KK, 2, kSPW, 2>);                                      \
+    if (want == 14) launch(k_eprop_t<KK, 1, kSPW, 4>);                           \
+    else launch(k_eprop_t<KK, 2, kSPW, 4>);                                      \
     break;
     SW_K(1) SW_K(2) SW_K(3) SW_K(4) SW_K(5) SW_K(6) SW_K(7) SW_K(8)
+    SW_K(9) SW_K(10) SW_K(11) SW_K(12) SW_K(13) SW_K(14) SW_K(15) SW_K(16)
 #undef SW_K
     default: sw::set_last_error("sw_eprop_pass: k"); return SW_ERR_INVALID_ARG;
   }
