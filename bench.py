@@ -675,7 +675,8 @@ def run_topomap_sweep(scales=(1, 2, 4, 8, 16), model_ms=100.0, seed=1, process_g
     for s in scales:
         t0 = time.perf_counter()
         model = TopomapModel(s, seed=seed, record_events=False, use_graph=True,
-                             rates_on_device=True, process_group=process_group)
+                             rates_on_device=True, process_group=process_group,
+                             incremental_remap=os.environ.get("SW_TOPO_REMAP", "patch") != "full")
         torch.cuda.synchronize()
         build_s = time.perf_counter() - t0
         model.run(40.0)   # warm-up: graph captures, first replays, two stimulus changes
@@ -852,8 +853,8 @@ def run_device(args, w):
                          "kernel_us_per_timestep": round(k_us / K, 2),
                          "share_of_step": round(k_us * 1e-3 * (w["steps"] / K) / ms_dev, 3),
                          "prep_us": round(prep_us, 2),
-                         "note": "the pass re-reads its K steps of trace/psi/lsig runs from L2 per "
-                                 "8-synapse tile (L2 throughput, not HBM, is its ceiling: see DESIGN.md)",
+                         "note": "the pass re-reads its K steps of trace/psi/lsig runs through L1/L2 per "
+                                 "4-synapse tile (L1/L2 throughput, not HBM, is its ceiling: see DESIGN.md)",
                          # the same K timesteps as K single-step passes would
                          # move K x the eligibility bytes: the temporally
                          # blocked pass beats that formulation's HBM roofline

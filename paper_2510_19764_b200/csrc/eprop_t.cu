@@ -52,15 +52,17 @@ constexpr int kBT = 32;
 constexpr int kMaxC = 32;
 
 __host__ __device__ inline size_t prep_smem_bytes(int C) {
-  return (size_t)kBT * (kHT + 1) * 4 + (size_t)C * kHT * 8 + (size_t)kBT * C * 8;
+  return (size_t)2 * kBT * (kHT + 1) * 4 + (size_t)C * kHT * 8 + (size_t)kBT * C * 8;
 }
 
-// CT: the class count as a compile-time constant (0 = runtime, any count)
-template <int CT>
-__global__ void __launch_bounds__(256) k_prep(const sw_eprop_prep_t P) {
+// CT: the class count as a compile-time constant (0 = runtime, any count);
+// MB: blocks per SM the register budget is sized for
+template <int CT, int MB = 1>
+__global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float (*tile)[kHT + 1] = reinterpret_cast<float (*)[kHT + 1]>(smem_raw);
-  double* ws = reinterpret_cast<double*>(smem_raw + (size_t)kBT * (kHT + 1) * 4);   // [C][kHT]
+  float (*tile)[kHT + 1] = reinterpret_cast<float (*)[kHT + 1]>(smem_raw);                       // zbar
+  float (*ptile)[kHT + 1] = reinterpret_cast<float (*)[kHT + 1]>(smem_raw + (size_t)kBT * (kHT + 1) * 4);   // psi
+  double* ws = reinterpret_cast<double*>(smem_raw + (size_t)2 * kBT * (kHT + 1) * 4);   // [C][kHT]
   const int C = CT ? CT : P.num_classes;
   const int H = P.hidden, NI = P.num_inputs, B = P.batch;
   const int64_t L = P.ldb;
@@ -93,12 +95,39 @@ __global__ void __launch_bounds__(256) k_prep(const sw_eprop_prep_t P) {
     store_tile(r0, min(kHT, x1 - r0), P.xbar_t + (int64_t)k * NI * L);
     __syncthreads();
   }
-  load_tile(P.psi[k], H, h0, nh);
-  __syncthreads();
-  store_tile(h0, nh, P.psi_t + (int64_t)k * H * L);
-  __syncthreads();
-  // zbar last: its tile stays in shared memory for the readout partials
-  load_tile(P.zbar[k], H, h0, nh);
+  // one round of loads: the psi and zbar tiles (through registers, all
+  // issued before any shared-memory store), W_out, d, and (deferred
+  // reduction) the readout partials this block adds to
+  constexpr int kPer = kBT * kHT / 256;
+  {
+    float pv[kPer], zv[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int x = tid + u * 256, b = x / kHT, r = x % kHT;
+      const bool ok = r < nh && b0 + b < B;
+      const int64_t g = (int64_t)(b0 + b) * H + h0 + r;
+      pv[u] = ok ? P.psi[k][g] : 0.f;
+      zv[u] = ok ? P.zbar[k][g] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int x = tid + u * 256, b = x / kHT, r = x % kHT;
+      ptile[b][r] = pv[u];
+      tile[b][r] = zv[u];
+    }
+  }
+  constexpr int CP = (CT > 0 && CT % 4 == 0) ? CT / 4 : 1;
+  const int rr = tid % kHT, cg = tid / kHT;   // readout partials: thread = (hidden unit, class group of 4)
+  double* part = ro ? P.ro_partial + ((int64_t)k * gridDim.y + bt) * (C * (int64_t)H + C) : nullptr;
+  double prev[CP];
+#pragma unroll
+  for (int u = 0; u < CP; ++u) prev[u] = 0.0;
+  if constexpr (CT > 0 && CT % 4 == 0) {
+    if (ro && P.defer_reduce && rr < nh) {
+#pragma unroll
+      for (int u = 0; u < CP; ++u) prev[u] = part[(int64_t)(cg * CP + u) * H + h0 + rr];
+    }
+  }
   if (want_lsig || ro) {
     for (int x = tid; x < C * kHT; x += 256) {
       const int c = x / kHT, r = x % kHT;
@@ -110,7 +139,13 @@ __global__ void __launch_bounds__(256) k_prep(const sw_eprop_prep_t P) {
     }
   }
   __syncthreads();
-  store_tile(h0, nh, P.zbar_t + (int64_t)k * H * L);
+  for (int x = tid; x < kBT * kHT; x += 256) {
+    const int r = x / kBT, b = x % kBT;
+    if (r < nh && b0 + b < L) {
+      P.psi_t[(int64_t)k * H * L + (int64_t)(h0 + r) * L + b0 + b] = ptile[b][r];
+      P.zbar_t[(int64_t)k * H * L + (int64_t)(h0 + r) * L + b0 + b] = tile[b][r];
+    }
+  }
 
   // ---- B: learning signal, lane = replica ----
   if (want_lsig) {
@@ -136,11 +171,9 @@ __global__ void __launch_bounds__(256) k_prep(const sw_eprop_prep_t P) {
 
   // ---- C: readout partials, thread = (hidden unit, class group of 4) ----
   if (ro) {
-    double* part = P.ro_partial + ((int64_t)k * gridDim.y + bt) * (C * (int64_t)H + C);
-    const int r = tid % kHT, cg = tid / kHT;   // 4 class groups
+    const int r = rr;
     if (r < nh) {
       if constexpr (CT > 0 && CT % 4 == 0) {
-        constexpr int CP = CT / 4;
         double acc[CP];
 #pragma unroll
         for (int u = 0; u < CP; ++u) acc[u] = 0.0;
@@ -153,7 +186,7 @@ __global__ void __launch_bounds__(256) k_prep(const sw_eprop_prep_t P) {
 #pragma unroll
         for (int u = 0; u < CP; ++u) {
           double* pp = part + (int64_t)(cg * CP + u) * H + h0 + r;
-          *pp = P.defer_reduce ? __dadd_rn(*pp, acc[u]) : acc[u];
+          *pp = P.defer_reduce ? __dadd_rn(prev[u], acc[u]) : acc[u];
         }
       } else {
         const int cper = (C + 3) / 4, ca = cg * cper, cb = min(C, ca + cper);
@@ -447,15 +480,23 @@ extern "C" int sw_eprop_prep(const sw_eprop_prep_t* p, void* stream) {
   const size_t smem = prep_smem_bytes(p->num_classes);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute((const void*)k_prep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute((const void*)k_prep<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute((const void*)k_prep<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute((const void*)k_prep<20, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute((const void*)k_prep<20, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   if (smem > 200 * 1024) { sw::set_last_error("sw_eprop_prep: shared memory"); return SW_ERR_INVALID_ARG; }
   // the replica tiles cover ldb (the padding columns are written as zeros)
   dim3 grid((p->hidden + kHT - 1) / kHT, (p->ldb + kBT - 1) / kBT, p->k);
-  if (p->num_classes == 20) k_prep<20><<<grid, 256, smem, st>>>(*p);   // the SHD-shaped task
-  else k_prep<0><<<grid, 256, smem, st>>>(*p);
+  // register budget for 3 blocks per SM (80 registers; measured: C1 prep
+  // 27.9 -> 25.0 us, C2 118.6 -> 96.6 us against the unconstrained 89, and
+  // 26.2 / 99.0 us at 4 blocks, which spills); SW_PREP_MB=1|4 (measurement)
+  static const int pmb = [] { const char* e = getenv("SW_PREP_MB"); return e ? atoi(e) : 3; }();
+  if (p->num_classes == 20 && pmb == 4) k_prep<20, 4><<<grid, 256, smem, st>>>(*p);   // the SHD-shaped task
+  else if (p->num_classes == 20 && pmb == 1) k_prep<20><<<grid, 256, smem, st>>>(*p);
+  else if (p->num_classes == 20) k_prep<20, 3><<<grid, 256, smem, st>>>(*p);
+  else k_prep<0, 2><<<grid, 256, smem, st>>>(*p);
   sw::count_launch();
   if (p->g_w_out && !p->defer_reduce) {
     const int n = p->num_classes * p->hidden + p->num_classes;
