@@ -167,15 +167,6 @@ class _Plan:
                   m.stride, m.num_post, self.shift, self.scratch.data_ptr(), self.pre.data_ptr(),
                   self.post.data_ptr(), self.off.data_ptr(), self.e_pad, self.total.data_ptr(),
                   _lib.stream_ptr())
-        pb = int(os.environ.get("SW_PLAN_PREBLOCK", "0"))
-        if pb > 0 and self.layout == "chunk":
-            # experiment: order by (pre block, post, pre)
-            E = m.edge_count()
-            pre, post = self.pre[:E].long(), self.post[:E].long()
-            key = ((pre // pb) * m.num_post + post) * m.num_pre + pre
-            order = torch.argsort(key)
-            for t in (self.pre, self.post, self.off):
-                t[:E] = t[:E][order]
 
     def tseg(self, trace_t: list) -> _lib.EpropTSeg:
         s = _lib.EpropTSeg()
