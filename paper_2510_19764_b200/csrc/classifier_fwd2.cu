@@ -12,14 +12,13 @@
 // The forward kernel (k_clf_fwd2, block per replica, a group of steps per
 // launch, state in registers) then only builds its spiking-row lists from
 // those words and the hidden spikes:
-//   A  hidden spikes -> ascending list (warp ballots, one barrier); the
-//      spike words also go to z_bits for the readout launch;
-//   B  warp 6 builds step t+1's ascending input-row list from its spike
-//      words while this step computes (two list buffers);
-//   C  the ascending input rows and hidden rows are split into G ordered
-//      groups each (warp g sums group g of both into its partial rows, rows
-//      read from the packed (target, weight) rows, kRowsAhead rows' entries
-//      loaded before any is added);
+//   A  hidden spikes -> spike words in unit order (warp ballots), to shared
+//      memory and to z_bits for the readout launch; one barrier;
+//   C  warp g selects group g of the ascending input rows and group g of
+//      the ascending hidden rows straight from the spike words (a popcount
+//      scan per warp; G ordered groups by count, no list-building warp and
+//      no second barrier) and sums them into its partial rows, reading the
+//      packed (target, weight) rows with kRowsAhead rows' loads in flight;
 //   D  per post the group partials are added in group order, the ALIF step
 //      and the surrogate (neurons.py:60-73).
 // The readout / softmax of all the launch's steps then runs as one launch
@@ -116,45 +115,85 @@ __global__ void __launch_bounds__(1024) k_clf_xbar(const sw_clf_inputs_t P) {
 // row groups of the current sums: 8 / (hidden units per thread)
 __host__ __device__ inline int fwd2_groups(int H) { return H <= 256 ? 8 : 4; }
 
+// per-group row-list capacity: a group holds at most ceil(n / G) rows
+__host__ __device__ inline int fwd2_list_cap(int H, int NI) {
+  const int G = fwd2_groups(H);
+  return (NI + G - 1) / G + (H + G - 1) / G + 2;
+}
+
 __host__ __device__ inline size_t fwd2_fixed_bytes(int H, int NI, int n_steps) {
   const size_t NT = (size_t)NI + H;
   size_t o = (size_t)2 * fwd2_groups(H) * H * 4;   // input / hidden partial rows
   o += NT * 4;                                      // rlen
-  o += (size_t)2 * NI * 4;                          // input lists (2 buffers)
-  o += (size_t)2 * H * 4;                           // hidden lists (2 buffers)
+  o += (size_t)fwd2_groups(H) * fwd2_list_cap(H, NI) * 4;   // per-group row lists
+  o += (size_t)((H + 31) / 32) * 4;                 // hidden spike words
   o = (o + 15) & ~(size_t)15;
   o += (size_t)n_steps * ((NI + 31) / 32) * 4;      // the launch's input spike words
   return o;
 }
 
-// dst[target] += weight over the packed rows list[r0..r1) in order, one
-// warp: the entries of kRowsAhead rows loaded before any is added (lane =
-// entry), so their L2 latencies overlap
+// rows [n*grp/G, n*(grp+1)/G) of the ascending set-bit list of words[0..nw)
+// (n = the total set bits) into out[0..), one warp; returns their count
+__device__ __forceinline__ int group_rows(const uint32_t* words, int nw, int grp, int G, int* out, int lane) {
+  int n = 0;
+  for (int w0 = 0; w0 < nw; w0 += 32) {
+    const uint32_t wd = w0 + lane < nw ? words[w0 + lane] : 0u;
+    n += __reduce_add_sync(SW_FULL_MASK, __popc(wd));
+  }
+  const int g0 = n * grp / G, g1 = n * (grp + 1) / G;
+  int base = 0;
+  for (int w0 = 0; w0 < nw && base < g1; w0 += 32) {
+    const uint32_t wd = w0 + lane < nw ? words[w0 + lane] : 0u;
+    const int c = __popc(wd);
+    int inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int u = __shfl_up_sync(SW_FULL_MASK, inc, d);
+      if (lane >= d) inc += u;
+    }
+    int rank = base + inc - c;
+    if (rank < g1 && rank + c > g0)
+      for (uint32_t m = wd; m; m &= m - 1, ++rank)
+        if (rank >= g0 && rank < g1) out[rank - g0] = (w0 + lane) * 32 + __ffs(m) - 1;
+    base += __shfl_sync(SW_FULL_MASK, inc, 31);
+  }
+  __syncwarp();
+  return g1 - g0;
+}
+
+// dst[target] += weight over the packed rows list[0..nr) in order, one
+// warp: lanes 0..kRowsAhead-1 look up a row each (index, length, offset),
+// the rows' entries are loaded before any is added (lane = entry), so their
+// L2 latencies overlap; per row two shuffles, one load and one shared-memory
+// read-modify-write per lane
 constexpr int kRowsAhead = 4;
-__device__ __forceinline__ void sum_rows(const int* list, int r0, int r1, const int* rl, const int2* base,
-                                         int stride, float* dst, int lane) {
-  for (int r = r0; r < r1; r += kRowsAhead) {
+template <typename IDX>
+__device__ __forceinline__ void sum_rows(const IDX* list, int nr, const int* rl, const int2* base, int stride,
+                                         float* dst, int lane) {
+  for (int r = 0; r < nr; r += kRowsAhead) {
+    int my_len = 0, my_off = 0;
+    if (lane < kRowsAhead && r + lane < nr) {
+      const int x = list[r + lane];
+      my_len = rl[x];
+      my_off = x * stride;
+    }
     int2 tw[kRowsAhead];
-    int len[kRowsAhead];
-    const int2* e[kRowsAhead];
+    int len[kRowsAhead], off[kRowsAhead];
 #pragma unroll
     for (int u = 0; u < kRowsAhead; ++u) {
-      len[u] = 0;
-      e[u] = base;
-      if (r + u < r1) {
-        const int x = list[r + u];
-        len[u] = rl[x];
-        e[u] = base + (int64_t)x * stride;
-      }
+      len[u] = __shfl_sync(SW_FULL_MASK, my_len, u);
+      off[u] = __shfl_sync(SW_FULL_MASK, my_off, u);
       tw[u] = make_int2(0, 0);
-      if (lane < len[u]) tw[u] = __ldg(e[u] + lane);
+      if (lane < len[u]) tw[u] = __ldg(base + off[u] + lane);
     }
 #pragma unroll
     for (int u = 0; u < kRowsAhead; ++u) {
       if (lane < len[u]) dst[tw[u].x] = __fadd_rn(dst[tw[u].x], __int_as_float(tw[u].y));
-      for (int q = lane + 32; q < len[u]; q += 32) {
-        const int2 t2 = __ldg(e[u] + q);
-        dst[t2.x] = __fadd_rn(dst[t2.x], __int_as_float(t2.y));
+      if (len[u] > 32) {   // warp-uniform: long rows only
+        for (int q = lane + 32; q < len[u]; q += 32) {
+          const int2 t2 = __ldg(base + off[u] + q);
+          dst[t2.x] = __fadd_rn(dst[t2.x], __int_as_float(t2.y));
+        }
       }
       __syncwarp();
     }
@@ -166,25 +205,24 @@ __device__ __forceinline__ void sum_rows(const int* list, int r0, int r1, const 
 template <int NTH, int HPT, int GT>
 __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int kT2 = NTH, kW2 = NTH / 32;
+  constexpr int kT2 = NTH;
   constexpr int G = GT;
   const int H = P.hidden, NI = P.num_inputs;
   const int NT = NI + H;
+  const int HW = (H + 31) / 32;
+  const int cap = fwd2_list_cap(H, NI);
   size_t o = 0;
   float* pin = (float*)(smem_raw + o);   o += (size_t)G * H * 4;
   float* prc = (float*)(smem_raw + o);   o += (size_t)G * H * 4;
   int* rlen = (int*)(smem_raw + o);      o += (size_t)NT * 4;
-  int* lin = (int*)(smem_raw + o);       o += (size_t)2 * NI * 4;        // [2][NI] input lists
-  int* lhb = (int*)(smem_raw + o);       o += (size_t)2 * H * 4;         // [2][H] hidden lists
+  int* lists = (int*)(smem_raw + o);     o += (size_t)G * cap * 4;      // [G][cap] this step's rows
+  uint32_t* zws = (uint32_t*)(smem_raw + o); o += (size_t)HW * 4;       // hidden spike words
   o = (o + 15) & ~(size_t)15;
   uint32_t* wsm = (uint32_t*)(smem_raw + o);   // [n_steps][in_words] spike words
-  __shared__ int s_wcnt[kW2];
-  __shared__ int s_nin[2];
 
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int bH = b * H;
-  const int HW = (H + 31) / 32;
   const int B = P.batch;
   const int nslot = P.slot_count;
   const int nsteps = P.n_steps;
@@ -211,88 +249,36 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
     const int q = x / P.in_words, w = x - q * P.in_words;
     wsm[x] = __ldg(P.in_bits + ((int64_t)(P.t + q) * B + b) * P.in_words + w);
   }
-  __syncthreads();
 
-  // warp 6 (or the last warp): step t's ascending input-row list from its
-  // spike words, into list buffer buf
-  const int pw = kW2 - 2;
-  auto build_inputs = [&](int t, int buf) {
-    const uint32_t* wds = wsm + (t - P.t) * P.in_words;
-    int* L = lin + buf * NI;
-    int n = 0;
-    for (int w0 = 0; w0 < P.in_words; w0 += 32) {
-      const uint32_t wd = (w0 + lane < P.in_words) ? wds[w0 + lane] : 0u;
-      const int c = __popc(wd);
-      int inc = c;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int u = __shfl_up_sync(SW_FULL_MASK, inc, d);
-        if (lane >= d) inc += u;
-      }
-      int p = n + inc - c;
-      for (uint32_t m = wd; m; m &= m - 1) L[p++] = (w0 + lane) * 32 + __ffs(m) - 1;
-      n += __shfl_sync(SW_FULL_MASK, inc, 31);
-    }
-    if (lane == 0) s_nin[buf] = n;
-  };
-  if (warp == pw) build_inputs(P.t, 0);
-  __syncthreads();
-
-  for (int s = 0; s < nsteps; ++s) {
-    const int t = P.t + s;
-    const int cb = s & 1;
-    const int cur = t % nslot;
+  int cur = P.t % nslot;
+  for (int s = 0; s < nsteps; ++s, cur = (cur + 1 == nslot) ? 0 : cur + 1) {
     float* zbar_o = P.zbar + cur * B * H;
     float* psi_o = P.psi + cur * B * H;
 
     FWD2_PROF(0);
-    // ---- A: hidden spikes -> ascending list ----
+    // ---- A: hidden spike words (unit order) to shared memory and to z_bits
+    // for the readout launch: warp w holds units w*32*HPT + HPT*lane + j, so
+    // word q of the warp takes bit i*HPT+j from ballot j's bit q*(32/HPT)+i ----
     unsigned hm[HPT];
-    int hc = 0;
 #pragma unroll
-    for (int j = 0; j < HPT; ++j) {
-      hm[j] = __ballot_sync(SW_FULL_MASK, (h0 + j < H) && z[j] != 0.0f);
-      hc += __popc(hm[j]);
-    }
-    if (lane == 0) s_wcnt[warp] = hc;
+    for (int j = 0; j < HPT; ++j) hm[j] = __ballot_sync(SW_FULL_MASK, (h0 + j < H) && z[j] != 0.0f);
     {
-      // hidden spike words in unit order for the readout launch: warp w holds
-      // units w*32*HPT + HPT*lane + j, so word q of the warp takes bit i*HPT+j
-      // from ballot j's bit q*(32/HPT)+i
       uint32_t* zw = P.z_bits + ((int64_t)s * B + b) * HW;
       if (HPT == 1) {
-        if (lane == 0 && warp < HW) zw[warp] = hm[0];
+        if (lane == 0 && warp < HW) {
+          zws[warp] = hm[0];
+          zw[warp] = hm[0];
+        }
       } else if (lane < HPT && warp * HPT + lane < HW) {
         uint32_t wd = 0;
 #pragma unroll
         for (int j = 0; j < HPT; ++j)
 #pragma unroll
           for (int i = 0; i < 32 / HPT; ++i) wd |= ((hm[j] >> (lane * (32 / HPT) + i)) & 1u) << (i * HPT + j);
+        zws[warp * HPT + lane] = wd;
         zw[warp * HPT + lane] = wd;
       }
     }
-    __syncthreads();   // B1
-    FWD2_PROF(1);
-    int hbase = 0, nh = 0;
-#pragma unroll
-    for (int w = 0; w < kW2; ++w) {
-      const int c = s_wcnt[w];
-      if (w < warp) hbase += c;
-      nh += c;
-    }
-    int* lh = lhb + cb * H;
-    {
-      // this thread's units in ascending order: lanes before it contribute
-      // all their units, earlier j of this lane come first
-      int p = hbase;
-#pragma unroll
-      for (int j = 0; j < HPT; ++j) p += __popc(hm[j] & sw::lanemask_lt());
-#pragma unroll
-      for (int j = 0; j < HPT; ++j)
-        if ((hm[j] >> lane) & 1u) lh[p++] = h0 + j;
-    }
-    // ---- B: next step's input-row list ----
-    if (warp == pw && s + 1 < nsteps) build_inputs(t + 1, cb ^ 1);
     // zbar (old z) for the e-prop traces and the readout gradient
 #pragma unroll
     for (int j = 0; j < HPT; ++j) {
@@ -302,19 +288,19 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
         zbar_o[bH + h] = zb[j];
       }
     }
-    FWD2_PROF(2);
-    __syncthreads();   // B2: hidden list (and the next buffer's list) written
-    FWD2_PROF(3);
+    __syncthreads();   // B1: hidden spike words (and, at s = 0, the setup) visible
+    FWD2_PROF(1);
 
-    // ---- C: ordered group sums of the input rows and the hidden rows ----
-    const int nin = s_nin[cb];
-    FWD2_PROF(4);
-    for (int grp = warp; grp < G; grp += kW2) {
-      const int g0 = nin * grp / G, g1 = nin * (grp + 1) / G;
-      sum_rows(lin + cb * NI, g0, g1, rlen, reinterpret_cast<const int2*>(P.in_tw), P.in_tw_stride,
-               pin + grp * H, lane);
-      const int k0 = nh * grp / G, k1 = nh * (grp + 1) / G;
-      sum_rows(lh, k0, k1, rlen + NI, reinterpret_cast<const int2*>(P.rec_tw), P.rec_tw_stride, prc + grp * H,
+    // ---- C: warp g selects its group of the ascending input rows and of the
+    // ascending hidden rows straight from the spike words, then sums them ----
+    if (warp < G) {
+      int* L = lists + warp * cap;
+      const int nin = group_rows(wsm + s * P.in_words, P.in_words, warp, G, L, lane);
+      int* Lh = L + nin;
+      const int nhd = group_rows(zws, HW, warp, G, Lh, lane);
+      FWD2_PROF(4);
+      sum_rows(L, nin, rlen, reinterpret_cast<const int2*>(P.in_tw), P.in_tw_stride, pin + warp * H, lane);
+      sum_rows(Lh, nhd, rlen + NI, reinterpret_cast<const int2*>(P.rec_tw), P.rec_tw_stride, prc + warp * H,
                lane);
     }
     FWD2_PROF(5);
@@ -347,8 +333,8 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
       z[j] = (vv >= __fadd_rn(v_thr, __fmul_rn(beta, aa))) ? 1.0f : 0.0f;
     }
     FWD2_PROF(7);
-    // the next step's list writes happen after its B1, which every thread
-    // reaches only after finishing this step
+    // the next step's word writes (A) race with nothing: every warp finished
+    // this step's C before B3
   }
 
 #pragma unroll
