@@ -133,8 +133,27 @@ __host__ __device__ inline size_t fwd2_fixed_bytes(int H, int NI, int n_steps) {
 }
 
 // rows [n*grp/G, n*(grp+1)/G) of the ascending set-bit list of words[0..nw)
-// (n = the total set bits) into out[0..), one warp; returns their count
+// (n = the total set bits) into out[0..), one warp; returns their count.
+// Up to 32 words: one load, one scan; more: a counting pass first.
 __device__ __forceinline__ int group_rows(const uint32_t* words, int nw, int grp, int G, int* out, int lane) {
+  if (nw <= 32) {
+    const uint32_t wd = lane < nw ? words[lane] : 0u;
+    const int c = __popc(wd);
+    int inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int u = __shfl_up_sync(SW_FULL_MASK, inc, d);
+      if (lane >= d) inc += u;
+    }
+    const int n = __shfl_sync(SW_FULL_MASK, inc, 31);
+    const int g0 = n * grp / G, g1 = n * (grp + 1) / G;
+    int rank = inc - c;
+    if (rank < g1 && rank + c > g0)
+      for (uint32_t m = wd; m; m &= m - 1, ++rank)
+        if (rank >= g0 && rank < g1) out[rank - g0] = lane * 32 + __ffs(m) - 1;
+    __syncwarp();
+    return g1 - g0;
+  }
   int n = 0;
   for (int w0 = 0; w0 < nw; w0 += 32) {
     const uint32_t wd = w0 + lane < nw ? words[w0 + lane] : 0u;
@@ -159,6 +178,37 @@ __device__ __forceinline__ int group_rows(const uint32_t* words, int nw, int grp
   }
   __syncwarp();
   return g1 - g0;
+}
+
+// both selections at once when the input and the hidden words fit one warp
+// (lanes [0, nwi) input words, [nwi, nwi + nwh) hidden words): one scan
+__device__ __forceinline__ void group_rows2(const uint32_t* wi, int nwi, const uint32_t* wh, int nwh, int grp,
+                                            int G, int* out_in, int& nin, int*& out_h, int& nh, int lane) {
+  const bool is_in = lane < nwi;
+  const uint32_t wd = is_in ? wi[lane] : (lane < nwi + nwh ? wh[lane - nwi] : 0u);
+  const int c = __popc(wd);
+  int inc = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int u = __shfl_up_sync(SW_FULL_MASK, inc, d);
+    if (lane >= d) inc += u;
+  }
+  const int n_in = __shfl_sync(SW_FULL_MASK, inc, nwi - 1);
+  const int n_h = __shfl_sync(SW_FULL_MASK, inc, 31) - n_in;
+  const int a0 = n_in * grp / G, a1 = n_in * (grp + 1) / G;
+  const int h0 = n_h * grp / G, h1 = n_h * (grp + 1) / G;
+  out_h = out_in + (a1 - a0);
+  // this lane's word: ranks within its own list, its group's range
+  const int r0 = is_in ? a0 : h0, r1 = is_in ? a1 : h1;
+  int rank = inc - c - (is_in ? 0 : n_in);
+  int* out = is_in ? out_in - a0 : out_h - h0;
+  const int wbase = (is_in ? lane : lane - nwi) * 32;
+  if (rank < r1 && rank + c > r0)
+    for (uint32_t m = wd; m; m &= m - 1, ++rank)
+      if (rank >= r0 && rank < r1) out[rank] = wbase + __ffs(m) - 1;
+  __syncwarp();
+  nin = a1 - a0;
+  nh = h1 - h0;
 }
 
 // dst[target] += weight over the packed rows list[0..nr) in order, one
@@ -295,9 +345,15 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
     // ascending hidden rows straight from the spike words, then sums them ----
     if (warp < G) {
       int* L = lists + warp * cap;
-      const int nin = group_rows(wsm + s * P.in_words, P.in_words, warp, G, L, lane);
-      int* Lh = L + nin;
-      const int nhd = group_rows(zws, HW, warp, G, Lh, lane);
+      int nin, nhd;
+      int* Lh;
+      if (P.in_words + HW <= 32) {
+        group_rows2(wsm + s * P.in_words, P.in_words, zws, HW, warp, G, L, nin, Lh, nhd, lane);
+      } else {
+        nin = group_rows(wsm + s * P.in_words, P.in_words, warp, G, L, lane);
+        Lh = L + nin;
+        nhd = group_rows(zws, HW, warp, G, Lh, lane);
+      }
       FWD2_PROF(4);
       sum_rows(L, nin, rlen, reinterpret_cast<const int2*>(P.in_tw), P.in_tw_stride, pin + warp * H, lane);
       sum_rows(Lh, nhd, rlen + NI, reinterpret_cast<const int2*>(P.rec_tw), P.rec_tw_stride, prc + warp * H,
