@@ -148,9 +148,11 @@ __device__ __forceinline__ int group_rows(const uint32_t* words, int nw, int grp
     const int n = __shfl_sync(SW_FULL_MASK, inc, 31);
     const int g0 = n * grp / G, g1 = n * (grp + 1) / G;
     int rank = inc - c;
-    if (rank < g1 && rank + c > g0)
-      for (uint32_t m = wd; m; m &= m - 1, ++rank)
-        if (rank >= g0 && rank < g1) out[rank - g0] = lane * 32 + __ffs(m) - 1;
+    if (rank < g1 && rank + c > g0) {
+      uint32_t m = wd;
+      for (; rank < g0; ++rank) m &= m - 1;   // set bits below the group
+      for (; m && rank < g1; m &= m - 1, ++rank) out[rank - g0] = lane * 32 + __ffs(m) - 1;
+    }
     __syncwarp();
     return g1 - g0;
   }
@@ -203,9 +205,11 @@ __device__ __forceinline__ void group_rows2(const uint32_t* wi, int nwi, const u
   int rank = inc - c - (is_in ? 0 : n_in);
   int* out = is_in ? out_in - a0 : out_h - h0;
   const int wbase = (is_in ? lane : lane - nwi) * 32;
-  if (rank < r1 && rank + c > r0)
-    for (uint32_t m = wd; m; m &= m - 1, ++rank)
-      if (rank >= r0 && rank < r1) out[rank] = wbase + __ffs(m) - 1;
+  if (rank < r1 && rank + c > r0) {
+    uint32_t m = wd;
+    for (; rank < r0; ++rank) m &= m - 1;   // set bits below the group
+    for (; m && rank < r1; m &= m - 1, ++rank) out[rank] = wbase + __ffs(m) - 1;
+  }
   __syncwarp();
   nin = a1 - a0;
   nh = h1 - h0;
@@ -214,38 +218,51 @@ __device__ __forceinline__ void group_rows2(const uint32_t* wi, int nwi, const u
 // dst[target] += weight over the packed rows list[0..nr) in order, one
 // warp: lanes 0..kRowsAhead-1 look up a row each (index, length, offset),
 // the rows' entries are loaded before any is added (lane = entry), so their
-// L2 latencies overlap; per row two shuffles, one load and one shared-memory
-// read-modify-write per lane
+// L2 latencies overlap.  Warp-uniform branches skip the empty row slots of a
+// batch and, unless a row of the batch is longer than 32, the long-row code.
 constexpr int kRowsAhead = 4;
 template <typename IDX>
 __device__ __forceinline__ void sum_rows(const IDX* list, int nr, const int* rl, const int2* base, int stride,
                                          float* dst, int lane) {
   for (int r = 0; r < nr; r += kRowsAhead) {
+    const int cnt = min(kRowsAhead, nr - r);
     int my_len = 0, my_off = 0;
-    if (lane < kRowsAhead && r + lane < nr) {
+    if (lane < cnt) {
       const int x = list[r + lane];
       my_len = rl[x];
       my_off = x * stride;
     }
+    const bool longrows = __reduce_max_sync(SW_FULL_MASK, my_len) > 32;
     int2 tw[kRowsAhead];
-    int len[kRowsAhead], off[kRowsAhead];
+    int len[kRowsAhead];
 #pragma unroll
     for (int u = 0; u < kRowsAhead; ++u) {
       len[u] = __shfl_sync(SW_FULL_MASK, my_len, u);
-      off[u] = __shfl_sync(SW_FULL_MASK, my_off, u);
+      const int off = __shfl_sync(SW_FULL_MASK, my_off, u);
       tw[u] = make_int2(0, 0);
-      if (lane < len[u]) tw[u] = __ldg(base + off[u] + lane);
+      if (lane < len[u]) tw[u] = __ldg(base + off + lane);
     }
+    if (!longrows) {
 #pragma unroll
-    for (int u = 0; u < kRowsAhead; ++u) {
-      if (lane < len[u]) dst[tw[u].x] = __fadd_rn(dst[tw[u].x], __int_as_float(tw[u].y));
-      if (len[u] > 32) {   // warp-uniform: long rows only
-        for (int q = lane + 32; q < len[u]; q += 32) {
-          const int2 t2 = __ldg(base + off[u] + q);
-          dst[t2.x] = __fadd_rn(dst[t2.x], __int_as_float(t2.y));
+      for (int u = 0; u < kRowsAhead; ++u) {
+        if (u < cnt) {
+          if (lane < len[u]) dst[tw[u].x] = __fadd_rn(dst[tw[u].x], __int_as_float(tw[u].y));
+          __syncwarp();
         }
       }
-      __syncwarp();
+    } else {
+#pragma unroll
+      for (int u = 0; u < kRowsAhead; ++u) {
+        if (u < cnt) {
+          if (lane < len[u]) dst[tw[u].x] = __fadd_rn(dst[tw[u].x], __int_as_float(tw[u].y));
+          const int off = __shfl_sync(SW_FULL_MASK, my_off, u);
+          for (int q = lane + 32; q < len[u]; q += 32) {
+            const int2 t2 = __ldg(base + off + q);
+            dst[t2.x] = __fadd_rn(dst[t2.x], __int_as_float(t2.y));
+          }
+          __syncwarp();
+        }
+      }
     }
   }
 }
