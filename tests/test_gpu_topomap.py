@@ -117,8 +117,11 @@ def test_rewiring_state_injected_bit_exact(dev_lib, tag):
 
 def test_free_run_spikes_match_reference(dev_lib):
     """300 steps of TopomapModel(1, seed=11): source spikes are counter-exact;
-    target spikes and propagated conductances match the reference run (LIF
-    uses exp: float tolerance on V, spikes identical in practice)."""
+    target spikes match the reference run at every step and V to 1e-6 (F8:
+    the conductance LIF uses CUDA exp against numpy's, so V may differ in
+    the last bits; a spike could flip only if V landed within that error of
+    the threshold at a crossing, which this fixed-seed run does not do --
+    the comparison is deterministic, so any flip is a real change)."""
     from paper_2510_19764_b200.neurons import unpack_spike_bits
     from paper_2510_19764_b200.topomap import TopomapModel
     g = golden("topomap_run.npz")
@@ -132,7 +135,7 @@ def test_free_run_spikes_match_reference(dev_lib):
         src_ok += np.array_equal(src, np.flatnonzero(g["src"][t]))
         tgt_ok += np.array_equal(tgt, np.flatnonzero(g["tgt"][t]))
     assert src_ok == T
-    assert tgt_ok >= T - 2
+    assert tgt_ok == T
     st = model.state_arrays()
     assert np.allclose(st["V"], g["state_V"], rtol=0, atol=1e-6)
     for key in ("ff.row_length", "lat.row_length"):
