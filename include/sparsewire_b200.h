@@ -345,6 +345,9 @@ typedef struct sw_eprop_tpass {
    * batch's passes (zeroed before the first) and sw_eprop_pass_reduce adds
    * them to the gradients once (zeroing them again) */
   int32_t defer_reduce;
+  /* state_zero != 0: eps and ebar start from zero (the first pass of a
+   * batch): they are written, not read */
+  int32_t state_zero;
 } sw_eprop_tpass_t;
 SW_API int sw_eprop_pass_reduce(const sw_eprop_tseg_t* segs, int32_t n_segs, int32_t ldb, void* scratch,
                                 void* stream);
@@ -443,6 +446,10 @@ SW_API int sw_clf_step(const sw_clf_step_t* params, void* stream);
 SW_API int sw_clf_batch_stats(const double* loss, const double* pi_sum, const int32_t* labels,
                               int32_t batch, int32_t num_classes, double* out2, void* stream);
 SW_API int sw_f64_to_f32(const double* in, float* out, int64_t n, void* stream);
+/* zero n <= 16 device ranges (bytes[i] bytes at ptrs[i]) in one launch: the
+ * per-batch state resets of the trainer */
+#define SW_ZERO_MAX_RANGES 16
+SW_API int sw_zero_ranges(void* const* ptrs, const int64_t* bytes, int32_t n, void* stream);
 SW_API int sw_scale_f64(double* x, int64_t n, double s, void* stream);
 
 /* ---- transpose (connectivity.py:151-203) ----------------------------------- */

@@ -105,7 +105,7 @@ class EpropTSeg(C.Structure):
 class EpropTPass(C.Structure):
     """sw_eprop_tpass_t"""
     _fields_ = [("k", I32), ("psi_t", P * MAX_BLOCK), ("lsig_t", P * MAX_BLOCK), ("scratch", P),
-                ("defer_reduce", I32)]
+                ("defer_reduce", I32), ("state_zero", I32)]
 
 
 class ClfStep(C.Structure):
@@ -182,6 +182,7 @@ SIGNATURES: dict[str, list] = {
     "sw_clf_inputs": [P, P],
     "sw_clf_batch_stats": [P, P, P, I32, I32, P, P],
     "sw_f64_to_f32": [P, P, I64, P],
+    "sw_zero_ranges": [P, P, I32, P],
     "sw_scale_f64": [P, I64, F64, P],
     "sw_transpose_rebuild": [RP, P, P, P, P, P, P, P, I32, P],
     "sw_transpose_rebuild_coop": [RP, P, P, P, P, P, P, P, P, I32, P],

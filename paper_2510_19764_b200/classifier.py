@@ -388,10 +388,12 @@ class EpropClassifierTrainer:
             self._pass_scratch_key = key
         return self._pass_scratch.data_ptr()
 
-    def _eprop_block(self, t0: int, k: int, st: int) -> None:
+    def _eprop_block(self, t0: int, k: int, st: int, state_zero: bool | None = None) -> None:
         """e-prop of steps t0 .. t0+k-1: sw_eprop_prep (replica-minor copies,
         the learning signal and the readout gradients, classifier.py:221-223)
-        and one sw_eprop_pass over both projections."""
+        and one sw_eprop_pass over both projections.  The trial's first pass
+        (t0 = 0 unless state_zero says otherwise) starts eps/ebar from zero
+        without reading them."""
         p = self.params
         a32, r32, b32 = float(np.float32(p.alpha)), float(np.float32(p.rho)), float(np.float32(p.beta))
         B, L = self.local_b, self.plan_in.ldb
@@ -416,6 +418,7 @@ class EpropClassifierTrainer:
         self._tsegs[1] = self.plan_rec.tseg([self.zbar_t[j] for j in range(k)])
         tp.scratch = self._pass_scratch_ptr()
         tp.defer_reduce = 1   # split partials summed into the gradients once per batch (_finish)
+        tp.state_zero = int(t0 == 0 if state_zero is None else state_zero)
         _lib.call("sw_eprop_pass", ctypes.cast(self._tsegs, ctypes.c_void_p), 2, ctypes.byref(tp),
                   L, b32, r32, a32, st)
 
@@ -430,7 +433,7 @@ class EpropClassifierTrainer:
             with torch.cuda.graph(g, stream=side):
                 st = torch.cuda.current_stream().cuda_stream
                 for _ in range(reps):
-                    self._eprop_block(0, EPROP_BLOCK_STEPS, st)
+                    self._eprop_block(0, EPROP_BLOCK_STEPS, st, state_zero=False)
         torch.cuda.current_stream().wait_stream(side)
         return g
 
@@ -446,7 +449,7 @@ class EpropClassifierTrainer:
             return orig(name, *args)
         _lib.call = rec
         try:
-            self._eprop_block(0, EPROP_BLOCK_STEPS, _lib.stream_ptr())
+            self._eprop_block(0, EPROP_BLOCK_STEPS, _lib.stream_ptr(), state_zero=False)
         finally:
             _lib.call = orig
         want = "sw_eprop_pass" if part == "pass" else "sw_eprop_prep"
@@ -571,8 +574,12 @@ class EpropClassifierTrainer:
         for m, syn, tw, key in ((self.m_in, self.s_in, self.tw_in, "in"), (self.m_rec, self.s_rec, self.tw_rec, "rec")):
             _lib.call("sw_clf_pack_rows", m.row_length.data_ptr(), m.target.data_ptr(),
                       syn.planes["w"].data_ptr(), m.num_pre, m.stride, self._tw_stride[key], tw.data_ptr(), st)
-        for x in (self.v, self.a, self.z, self.y, self.pi_sum, self.loss_b, self._slots_zbar, self._slots_xbar):
-            x.zero_()
+        # per-batch state resets in one launch (eps/ebar: the trial's first
+        # e-prop pass starts them from zero)
+        resets = (self.v, self.a, self.z, self.y, self.pi_sum, self.loss_b, self._slots_zbar, self._slots_xbar)
+        ptrs = (ctypes.c_void_p * len(resets))(*[x.data_ptr() for x in resets])
+        nbytes = (ctypes.c_int64 * len(resets))(*[x.numel() * x.element_size() for x in resets])
+        _lib.call("sw_zero_ranges", ptrs, nbytes, len(resets), st)
         ip = _lib.ClfInputs()
         ip.steps, ip.batch, ip.ldb = self.task.example_steps, self.local_b, self.plan_in.ldb
         ip.num_inputs, ip.words = self.task.num_inputs, self._in_words
@@ -584,8 +591,6 @@ class EpropClassifierTrainer:
             for plan, syn in ((self.plan_in, self.s_in), (self.plan_rec, self.s_rec)):
                 plan.ensure(plan.m.edge_count())
                 plan.build()
-                plan.eps.zero_()
-                plan.ebar.zero_()
                 _lib.call("sw_gather_f64", syn.planes["grad"].data_ptr(), plan.off.data_ptr(),
                           plan.e_pad, plan.grad.data_ptr(), st)
 

@@ -617,6 +617,55 @@ extern "C" int sw_clf_batch_stats(const double* loss, const double* pi_sum, cons
   return SW_OK;
 }
 
+namespace {
+struct ZeroArgs {
+  char* p[SW_ZERO_MAX_RANGES];
+  int64_t n[SW_ZERO_MAX_RANGES];
+  int count;
+};
+// 16-byte stores over each range's aligned body, bytes at its ends
+__global__ void k_zero_ranges(const ZeroArgs A) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  for (int r = 0; r < A.count; ++r) {
+    char* p = A.p[r];
+    const int64_t n = A.n[r];
+    const int64_t head = min(n, (int64_t)((16 - ((uintptr_t)p & 15)) & 15));
+    const int64_t body = (n - head) >> 4;
+    uint4* q = reinterpret_cast<uint4*>(p + head);
+    for (int64_t x = tid; x < body; x += nt) q[x] = make_uint4(0u, 0u, 0u, 0u);
+    const int64_t tail0 = head + body * 16;
+    for (int64_t x = tid; x < head; x += nt) p[x] = 0;
+    for (int64_t x = tail0 + tid; x < n; x += nt) p[x] = 0;
+  }
+}
+}  // namespace
+
+extern "C" int sw_zero_ranges(void* const* ptrs, const int64_t* bytes, int32_t n, void* stream) {
+  if (n < 0 || n > SW_ZERO_MAX_RANGES || (n > 0 && (!ptrs || !bytes))) {
+    sw::set_last_error("sw_zero_ranges: 0 <= n <= SW_ZERO_MAX_RANGES");
+    return SW_ERR_INVALID_ARG;
+  }
+  ZeroArgs A{};
+  int64_t total = 0;
+  for (int i = 0; i < n; ++i) {
+    if (bytes[i] < 0 || (bytes[i] > 0 && !ptrs[i])) {
+      sw::set_last_error("sw_zero_ranges: negative size or null range");
+      return SW_ERR_INVALID_ARG;
+    }
+    A.p[A.count] = (char*)ptrs[i];
+    A.n[A.count] = bytes[i];
+    A.count += bytes[i] > 0;
+    total += bytes[i];
+  }
+  if (total == 0) return SW_OK;
+  int64_t g = (total / 16 + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  k_zero_ranges<<<(int)(g < 1 ? 1 : g), 256, 0, (cudaStream_t)stream>>>(A);
+  sw::count_launch();
+  SW_CHECK_LAUNCH("sw_zero_ranges");
+  return SW_OK;
+}
+
 extern "C" int sw_f64_to_f32(const double* in, float* out, int64_t n, void* stream) {
   if (n <= 0) return SW_OK;
   k_f64_to_f32<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(in, out, n); sw::count_launch();

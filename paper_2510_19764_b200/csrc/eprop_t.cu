@@ -273,6 +273,7 @@ struct TPass {
   float beta, rho, alpha;
   unsigned long long nz;   // (-0.0f, -0.0f)
   int defer;               // partials accumulate over passes; sw_eprop_pass_reduce adds them
+  int zero;                // eps/ebar start from zero (not read)
   int dbg;   // measurement only (SW_EPT_DBG): 1 = every synapse reads pre/post 0 (L1-resident inputs), 2 = no state traffic
 };
 
@@ -402,7 +403,7 @@ __global__ void __launch_bounds__(kTW * 32, MB) k_eprop_t(const TPass T) {
     // state and inputs as packed replica pairs
     unsigned long long ep[NP], eb[NP];
     const int64_t so0 = (((int64_t)lt * nchunk + c0) * 32 + lane) * RPL;
-    if (T.dbg == 2) {
+    if (T.dbg == 2 || T.zero) {
       for (int r = 0; r < NP; ++r) ep[r] = eb[r] = 0ull;
     } else {
       ldp_cs<RPL>(ep, S.eps + so0);
@@ -445,8 +446,13 @@ __global__ void __launch_bounds__(kTW * 32, MB) k_eprop_t(const TPass T) {
         stp_cs<RPL>(S.ebar + so, eb);
       }
       if (c + 1 < c1 && T.dbg != 2) {
-        ldp_cs<RPL>(ep, S.eps + so + 32 * RPL);
-        ldp_cs<RPL>(eb, S.ebar + so + 32 * RPL);
+        if (T.zero) {
+#pragma unroll
+          for (int r = 0; r < NP; ++r) ep[r] = eb[r] = 0ull;
+        } else {
+          ldp_cs<RPL>(ep, S.eps + so + 32 * RPL);
+          ldp_cs<RPL>(eb, S.ebar + so + 32 * RPL);
+        }
       }
     }
     // the synapse's LPS replica groups, added pairwise: (g0 + g1) + (g2 + g3) ...
@@ -575,6 +581,7 @@ extern "C" int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const 
   T.alpha = alpha;
   T.nz = 0x8000000080000000ull;
   T.defer = p->defer_reduce != 0;
+  T.zero = p->state_zero != 0;
   {
     static const int dbg = [] { const char* e = getenv("SW_EPT_DBG"); return e ? atoi(e) : 0; }();
     T.dbg = dbg;

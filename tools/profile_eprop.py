@@ -23,7 +23,7 @@ reps = int(os.environ.get("REPS", "3"))
 if os.environ.get("EAGER"):
     st = _lib.stream_ptr()
     for _ in range(reps):
-        tr._eprop_block(0, EPROP_BLOCK_STEPS, st)
+        tr._eprop_block(0, EPROP_BLOCK_STEPS, st, state_zero=False)
     torch.cuda.synchronize()
     print("eager launches done")
     sys.exit(0)
