@@ -323,6 +323,11 @@ typedef struct sw_eprop_prep {
    * the batch's groups (zeroed before the first, e.g. by the previous
    * sw_eprop_prep_reduce) and sw_eprop_prep_reduce adds them once */
   int32_t defer_reduce;
+  /* psl_t != NULL: psi and lsig are written interleaved instead of to
+   * psi_t / lsig_t: psl_t[k][h][ldb/4][8] holds, per group of 4 replicas,
+   * their 4 psi then their 4 lsig values (the pass reads both with one
+   * 32-byte load; sw_eprop_tpass_t.psl) */
+  float* psl_t;
 } sw_eprop_prep_t;
 SW_API int sw_eprop_prep_reduce(const sw_eprop_prep_t* p, void* stream);
 SW_API int64_t sw_eprop_prep_scratch_bytes(int32_t k, int32_t batch, int32_t hidden, int32_t num_classes);
@@ -348,6 +353,9 @@ typedef struct sw_eprop_tpass {
   /* state_zero != 0: eps and ebar start from zero (the first pass of a
    * batch): they are written, not read */
   int32_t state_zero;
+  /* psl != 0: psi_t[k] is the interleaved psi/lsig array of
+   * sw_eprop_prep_t.psl_t (step k), lsig_t ignored */
+  int32_t psl;
 } sw_eprop_tpass_t;
 SW_API int sw_eprop_pass_reduce(const sw_eprop_tseg_t* segs, int32_t n_segs, int32_t ldb, void* scratch,
                                 void* stream);

@@ -93,7 +93,7 @@ class EpropPrep(C.Structure):
                 ("num_classes", I32), ("xbar", P * MAX_BLOCK), ("zbar", P * MAX_BLOCK),
                 ("psi", P * MAX_BLOCK), ("d", P * MAX_BLOCK), ("w_out", P), ("xbar_t", P),
                 ("zbar_t", P), ("psi_t", P), ("lsig_t", P), ("g_w_out", P), ("g_b_out", P),
-                ("ro_partial", P), ("defer_reduce", I32)]
+                ("ro_partial", P), ("defer_reduce", I32), ("psl_t", P)]
 
 
 class EpropTSeg(C.Structure):
@@ -105,7 +105,7 @@ class EpropTSeg(C.Structure):
 class EpropTPass(C.Structure):
     """sw_eprop_tpass_t"""
     _fields_ = [("k", I32), ("psi_t", P * MAX_BLOCK), ("lsig_t", P * MAX_BLOCK), ("scratch", P),
-                ("defer_reduce", I32), ("state_zero", I32)]
+                ("defer_reduce", I32), ("state_zero", I32), ("psl", I32)]
 
 
 class ClfStep(C.Structure):

@@ -310,8 +310,9 @@ class EpropClassifierTrainer:
         # [K][rows][ldb], and the pass kernel's split partials / tickets
         K, L = EPROP_BLOCK_STEPS, self.plan_in.ldb
         self.zbar_t = torch.zeros((K, H, L), **f32)
-        self.psi_t = torch.zeros((K, H, L), **f32)
-        self.lsig_t = torch.zeros((K, H, L), **f32)
+        # psi and lsig interleaved per 4-replica group ([K][H][L/4][2][4]):
+        # the pass reads both with one 32-byte load (sw_eprop_tpass_t.psl)
+        self.psl_t = torch.zeros((K, H, 2 * L), **f32)
         self._tsegs = (_lib.EpropTSeg * 2)()
         # the trial's input side (sw_clf_inputs, once per batch): spike words
         # for the forward pass and the input traces in the e-prop layout
@@ -388,6 +389,20 @@ class EpropClassifierTrainer:
             self._pass_scratch_key = key
         return self._pass_scratch.data_ptr()
 
+    @property
+    def psi_t(self) -> torch.Tensor:
+        """[K, H, ldb] replica-minor psi of the last e-prop group (a copy out
+        of the interleaved psl_t)."""
+        K, H, L2 = self.psl_t.shape
+        return self.psl_t.view(K, H, L2 // 8, 2, 4)[:, :, :, 0, :].reshape(K, H, L2 // 2)
+
+    @property
+    def lsig_t(self) -> torch.Tensor:
+        """[K, H, ldb] replica-minor learning signal of the last e-prop group
+        (a copy out of the interleaved psl_t)."""
+        K, H, L2 = self.psl_t.shape
+        return self.psl_t.view(K, H, L2 // 8, 2, 4)[:, :, :, 1, :].reshape(K, H, L2 // 2)
+
     def _eprop_block(self, t0: int, k: int, st: int, state_zero: bool | None = None) -> None:
         """e-prop of steps t0 .. t0+k-1: sw_eprop_prep (replica-minor copies,
         the learning signal and the readout gradients, classifier.py:221-223)
@@ -406,10 +421,11 @@ class EpropClassifierTrainer:
             sl = self._slot(t0 + j)
             pr.xbar[j], pr.zbar[j] = 0, sl["zbar"].data_ptr()   # xbar_t: precomputed
             pr.psi[j], pr.d[j] = sl["psi"].data_ptr(), sl["d"].data_ptr()
-            tp.psi_t[j], tp.lsig_t[j] = self.psi_t[j].data_ptr(), self.lsig_t[j].data_ptr()
+            tp.psi_t[j], tp.lsig_t[j] = self.psl_t[j].data_ptr(), 0
         pr.w_out = self.w_out.data_ptr()
         pr.xbar_t, pr.zbar_t = 0, self.zbar_t.data_ptr()
-        pr.psi_t, pr.lsig_t = self.psi_t.data_ptr(), self.lsig_t.data_ptr()
+        pr.psi_t, pr.lsig_t, pr.psl_t = 0, 0, self.psl_t.data_ptr()
+        tp.psl = 1
         pr.g_w_out, pr.g_b_out = self.g_w_out.data_ptr(), self.g_b_out.data_ptr()
         pr.ro_partial = self._ro_partial.data_ptr()
         pr.defer_reduce = 1   # readout partials summed once per batch (_finish)

@@ -49,6 +49,12 @@ constexpr int kTW = 8;          // warps per pass block
 //      regrouping of the reference's float64 sums).
 constexpr int kHT = 64;
 constexpr int kBT = 32;
+
+// the interleaved psi/lsig layout: per group of 4 replicas, 4 psi then 4
+// lsig floats; psi of (row, b) at psl_index, its lsig 4 floats later
+__host__ __device__ __forceinline__ int64_t psl_index(int64_t row, int64_t L, int b) {
+  return (row * L + (b & ~3)) * 2 + (b & 3);
+}
 constexpr int kMaxC = 32;
 
 __host__ __device__ inline size_t prep_smem_bytes(int C) {
@@ -72,7 +78,7 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
   const int nh = min(kHT, H - h0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool ro = P.g_w_out != nullptr;
-  const bool want_lsig = P.lsig_t != nullptr && P.d[0] != nullptr;
+  const bool want_lsig = (P.lsig_t != nullptr || P.psl_t != nullptr) && P.d[0] != nullptr;
 
   // ---- A: transposes (psi, zbar of the tile; xbar rows split over the h tiles) ----
   auto load_tile = [&](const float* in, int n, int r0, int nr) {
@@ -142,14 +148,21 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
   for (int x = tid; x < kBT * kHT; x += 256) {
     const int r = x / kBT, b = x % kBT;
     if (r < nh && b0 + b < L) {
-      P.psi_t[(int64_t)k * H * L + (int64_t)(h0 + r) * L + b0 + b] = ptile[b][r];
-      P.zbar_t[(int64_t)k * H * L + (int64_t)(h0 + r) * L + b0 + b] = tile[b][r];
+      const int64_t row = (int64_t)k * H + h0 + r;
+      if (P.psl_t) P.psl_t[psl_index(row, L, b0 + b)] = ptile[b][r];
+      else P.psi_t[row * L + b0 + b] = ptile[b][r];
+      P.zbar_t[row * L + b0 + b] = tile[b][r];
     }
   }
 
   // ---- B: learning signal, lane = replica ----
   if (want_lsig) {
-    float* out = P.lsig_t + (int64_t)k * H * L + b0 + lane;
+    // lsig of (row, replica b0 + lane): lsig_t[row][b], or the lsig half of
+    // the interleaved group
+    auto lsig_at = [&](int r) -> float* {
+      const int64_t row = (int64_t)k * H + h0 + r;
+      return P.psl_t ? P.psl_t + psl_index(row, L, b0 + lane) + 4 : P.lsig_t + row * L + b0 + lane;
+    };
     if constexpr (CT > 0) {
       double dr[CT];
 #pragma unroll
@@ -158,13 +171,13 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
         double ls = 0.0;
 #pragma unroll
         for (int c = 0; c < CT; ++c) ls = __dadd_rn(ls, __dmul_rn(dr[c], ws[c * kHT + r]));
-        if (b0 + lane < L) out[(int64_t)(h0 + r) * L] = b0 + lane < B ? __double2float_rn(ls) : 0.f;
+        if (b0 + lane < L) *lsig_at(r) = b0 + lane < B ? __double2float_rn(ls) : 0.f;
       }
     } else {
       for (int r = warp; r < nh; r += 8) {
         double ls = 0.0;
         for (int c = 0; c < C; ++c) ls = __dadd_rn(ls, __dmul_rn(dt[c * kBT + lane], ws[c * kHT + r]));
-        if (b0 + lane < L) out[(int64_t)(h0 + r) * L] = b0 + lane < B ? __double2float_rn(ls) : 0.f;
+        if (b0 + lane < L) *lsig_at(r) = b0 + lane < B ? __double2float_rn(ls) : 0.f;
       }
     }
   }
@@ -367,12 +380,34 @@ __device__ __forceinline__ void stp_cs(float* p, const unsigned long long (&v)[R
   }
 }
 
+// psi and lsig runs of a lane (RPL replicas from replica-minor offset off):
+// two loads, or one 32-byte load of the interleaved group (PSL)
+template <int RPL, bool PSL>
+__device__ __forceinline__ void load_pl(unsigned long long (&pv)[RPL / 2], unsigned long long (&lv)[RPL / 2],
+                                        const float* psi, const float* lsig, int64_t off) {
+  if constexpr (PSL) {
+    unsigned long long v[4];
+    asm("ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%4];" : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3])
+        : "l"(psi + 2 * off));
+    pv[0] = v[0];
+    pv[1] = v[1];
+    lv[0] = v[2];
+    lv[1] = v[3];
+  } else {
+    ldp<RPL>(pv, psi + off);
+    ldp<RPL>(lv, lsig + off);
+  }
+}
+
 // SPW synapses per warp (tile), LPS = 32/SPW lanes per synapse, each lane
 // RPL = 32/LPS consecutive replicas of the 32-replica chunk; PD: steps of
 // inputs loaded ahead of the recursion
-template <int K, int PD, int SPW, int MB>
+// PSL: psi and lsig interleaved per 4-replica group (one 32-byte load per
+// step instead of two 16-byte loads; RPL = 4 only)
+template <int K, int PD, int SPW, int MB, bool PSL>
 __global__ void __launch_bounds__(kTW * 32, MB) k_eprop_t(const TPass T) {
   constexpr int LPS = 32 / SPW, RPL = 32 / LPS, NP = RPL / 2;
+  static_assert(!PSL || RPL == 4, "interleaved psi/lsig: 4 replicas per lane");
   const int lane = threadIdx.x & 31;
   const int sl = lane / LPS, g = lane % LPS;
   const int tiles0 = T.s[0].tiles;
@@ -416,15 +451,13 @@ __global__ void __launch_bounds__(kTW * 32, MB) k_eprop_t(const TPass T) {
 #pragma unroll
       for (int k = 0; k < PD && k < K; ++k) {
         ldp<RPL>(zin[k], S.trace[k] + tofs + b0);
-        ldp<RPL>(pin[k], T.psi[k] + pofs + b0);
-        ldp<RPL>(lin[k], T.lsig[k] + pofs + b0);
+        load_pl<RPL, PSL>(pin[k], lin[k], T.psi[k], T.lsig[k], pofs + b0);
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         if (k + PD < K) {
           ldp<RPL>(zin[k + PD], S.trace[k + PD] + tofs + b0);
-          ldp<RPL>(pin[k + PD], T.psi[k + PD] + pofs + b0);
-          ldp<RPL>(lin[k + PD], T.lsig[k + PD] + pofs + b0);
+          load_pl<RPL, PSL>(pin[k + PD], lin[k + PD], T.psi[k + PD], T.lsig[k + PD], pofs + b0);
         }
         // _kernels.py:33-38 on replica pairs, every op a separately rounded
         // packed f32x2 op: e = psi*(zb - beta*eps); ebar = alpha*ebar + e;
@@ -609,8 +642,9 @@ extern "C" int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const 
   switch (p->k) {
 #define SW_K(KK)                                                                 \
   case KK:                                                                       \
-    if (want == 14) launch(k_eprop_t<KK, 1, kSPW, 4>);                           \
-    else launch(k_eprop_t<KK, 2, kSPW, 4>);                                      \
+    if (want == 14) launch(k_eprop_t<KK, 1, kSPW, 4, false>);                    \
+    else if (p->psl) launch(k_eprop_t<KK, 2, kSPW, 4, true>);                    \
+    else launch(k_eprop_t<KK, 2, kSPW, 4, false>);                               \
     break;
     SW_K(1) SW_K(2) SW_K(3) SW_K(4) SW_K(5) SW_K(6) SW_K(7) SW_K(8)
     SW_K(9) SW_K(10) SW_K(11) SW_K(12) SW_K(13) SW_K(14) SW_K(15) SW_K(16)
