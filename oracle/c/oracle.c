@@ -3,6 +3,7 @@
  * Compiled with -O2 -ffp-contract=off: every float32 op is separately
  * rounded, grad accumulates float64(float32 product) in (b, i, s) order,
  * exactly the numba loop (per synapse; the rows of a replica run in parallel). */
+#include <math.h>
 #include <stdint.h>
 #ifdef _OPENMP
 #include <omp.h>
@@ -43,4 +44,17 @@ int oracle_threads(void) {
 #else
   return 1;
 #endif
+}
+
+/* The learning signal lsig[b][h] = f32(sum_c d[b][c] * w[c][h]) as the
+ * device computes it (classifier.py:223, the device's stated order): classes
+ * ascending from +0.0, one correctly rounded fused multiply-add per class
+ * (C99 fma). */
+void oracle_lsig_fma(const double* d, const double* w, int64_t B, int64_t C, int64_t H, float* out) {
+  for (int64_t b = 0; b < B; ++b)
+    for (int64_t h = 0; h < H; ++h) {
+      double ls = 0.0;
+      for (int64_t c = 0; c < C; ++c) ls = fma(d[b * C + c], w[c * H + h], ls);
+      out[b * H + h] = (float)ls;
+    }
 }

@@ -18,7 +18,7 @@ def build() -> str:
     if os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(s) for s in srcs):
         return OUT
     cmd = ["gcc", "-O3", "-mavx2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC",
-           "-o", OUT] + srcs
+           "-o", OUT] + srcs + ["-lm"]
     subprocess.run(cmd, check=True)
     return OUT
 
@@ -34,6 +34,8 @@ def lib():
         L.oracle_eprop_accumulate_batch.argtypes = [P, P, I64, I64, P, P, P, I64, I64, P, P, P,
                                                     F32, F32, F32]
         L.oracle_eprop_accumulate_batch.restype = None
+        L.oracle_lsig_fma.argtypes = [P, P, I64, I64, I64, P]
+        L.oracle_lsig_fma.restype = None
         L.oracle_threads.argtypes = []
         L.oracle_threads.restype = ctypes.c_int
         _lib = L
@@ -53,6 +55,19 @@ def eprop_accumulate_c(targets, row_length, pre_trace, psi, lsig, eps, ebar, gra
                                         pre_trace.ctypes.data, psi.ctypes.data, lsig.ctypes.data,
                                         B, H, eps.ctypes.data, ebar.ctypes.data, grad.ctypes.data,
                                         float(beta), float(rho), float(alpha))
+
+
+def lsig_fma_c(d, w):
+    """[B, H] float32 learning signal f32(sum_c d[:, c] * w[c]) with one fma
+    per class, classes ascending (the device's order)."""
+    import numpy as np
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    B, C = d.shape
+    H = w.shape[1]
+    out = np.empty((B, H), np.float32)
+    lib().oracle_lsig_fma(d.ctypes.data, w.ctypes.data, B, C, H, out.ctypes.data)
+    return out
 
 
 def threads() -> int:

@@ -424,7 +424,7 @@ __device__ __forceinline__ void clf_step_body(const sw_clf_step_t& P, int scap_a
       for (int u = 0; u < 8; ++u) wv[u] = (c0 + u < C) ? __ldg(P.w_out + (int64_t)(c0 + u) * H + h) : 0.0;
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (c0 + u < C) ls = __dadd_rn(ls, __dmul_rn(dv[c0 + u], wv[u]));
+        if (c0 + u < C) ls = __fma_rn(dv[c0 + u], wv[u], ls);
     }
     if (P.lsig) P.lsig[bH + h] = __double2float_rn(ls);
     float vv = __fmul_rn(P.alpha, __fsub_rn(vo, __fmul_rn(zo, P.v_thr)));

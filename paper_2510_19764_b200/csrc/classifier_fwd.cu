@@ -345,12 +345,12 @@ __global__ void __launch_bounds__(kT, 4) k_clf_fwd(sw_clf_step_t P) {
         for (; c + 4 <= C; c += 4) {
           const double w0 = __ldg(wc), w1 = __ldg(wc + H), w2 = __ldg(wc + 2 * H), w3 = __ldg(wc + 3 * H);
           wc += 4 * H;
-          ls = __dadd_rn(ls, __dmul_rn(dv[c], w0));
-          ls = __dadd_rn(ls, __dmul_rn(dv[c + 1], w1));
-          ls = __dadd_rn(ls, __dmul_rn(dv[c + 2], w2));
-          ls = __dadd_rn(ls, __dmul_rn(dv[c + 3], w3));
+          ls = __fma_rn(dv[c], w0, ls);
+          ls = __fma_rn(dv[c + 1], w1, ls);
+          ls = __fma_rn(dv[c + 2], w2, ls);
+          ls = __fma_rn(dv[c + 3], w3, ls);
         }
-        for (; c < C; ++c, wc += H) ls = __dadd_rn(ls, __dmul_rn(dv[c], __ldg(wc)));
+        for (; c < C; ++c, wc += H) ls = __fma_rn(dv[c], __ldg(wc), ls);
         lsig_o[bH + h] = __double2float_rn(ls);
       }
       float vv = __fmul_rn(alpha, __fsub_rn(v[j], __fmul_rn(z[j], v_thr)));

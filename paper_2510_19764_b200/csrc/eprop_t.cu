@@ -38,7 +38,7 @@ constexpr int kTW = 8;          // warps per pass block
 //   A  replica-minor copies: zbar and psi of the tile, and a share of the
 //      xbar rows, through a [kBT][kHT + 1] shared tile (coalesced both ways);
 //   B  lsig_t[k][h][b] = f32(sum_c d[b][c] * W_out[c][h]), c ascending, one
-//      unfused multiply-add pair per class (the forward pass's arithmetic):
+//      fused multiply-add per class from +0.0 (the forward pass's arithmetic):
 //      lane = replica with its d row in registers, W_out[:, tile] in shared
 //      memory, each warp kHT/8 hidden units;
 //   C  readout-gradient partials over the tile's replicas, b ascending:
@@ -170,13 +170,13 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
       for (int r = warp; r < nh; r += 8) {
         double ls = 0.0;
 #pragma unroll
-        for (int c = 0; c < CT; ++c) ls = __dadd_rn(ls, __dmul_rn(dr[c], ws[c * kHT + r]));
+        for (int c = 0; c < CT; ++c) ls = __fma_rn(dr[c], ws[c * kHT + r], ls);
         if (b0 + lane < L) *lsig_at(r) = b0 + lane < B ? __double2float_rn(ls) : 0.f;
       }
     } else {
       for (int r = warp; r < nh; r += 8) {
         double ls = 0.0;
-        for (int c = 0; c < C; ++c) ls = __dadd_rn(ls, __dmul_rn(dt[c * kBT + lane], ws[c * kHT + r]));
+        for (int c = 0; c < C; ++c) ls = __fma_rn(dt[c * kBT + lane], ws[c * kHT + r], ls);
         if (b0 + lane < L) *lsig_at(r) = b0 + lane < B ? __double2float_rn(ls) : 0.f;
       }
     }
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
         for (int b = 0; b < kBT; ++b) {
           const double z = (double)tile[b][r];
 #pragma unroll
-          for (int u = 0; u < CP; ++u) acc[u] = __dadd_rn(acc[u], __dmul_rn(dg[u * kBT + b], z));
+          for (int u = 0; u < CP; ++u) acc[u] = __fma_rn(dg[u * kBT + b], z, acc[u]);
         }
 #pragma unroll
         for (int u = 0; u < CP; ++u) {
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
         const int cper = (C + 3) / 4, ca = cg * cper, cb = min(C, ca + cper);
         for (int c = ca; c < cb; ++c) {
           double acc = 0.0;
-          for (int b = 0; b < kBT; ++b) acc = __dadd_rn(acc, __dmul_rn(dt[c * kBT + b], (double)tile[b][r]));
+          for (int b = 0; b < kBT; ++b) acc = __fma_rn(dt[c * kBT + b], (double)tile[b][r], acc);
           double* pp = part + (int64_t)c * H + h0 + r;
           *pp = P.defer_reduce ? __dadd_rn(*pp, acc) : acc;
         }

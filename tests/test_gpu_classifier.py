@@ -361,8 +361,10 @@ def test_eprop_pass_replica_minor(dev_lib, P, H, cap, R, B, k):
     reference-layout kernel (sw_eprop_accumulate_batch, _kernels.py:15-39
     semantics) over k steps: eps and ebar bit-identical, the gradient within
     1e-13 relative (float64 regrouping of the replica sum); the learning
-    signal lsig_t bit-identical to the forward pass's f32(d @ W_out) in class
-    order; ragged batches (B not a multiple of 32) padded with zeros."""
+    signal lsig_t bit-identical to the forward pass's f32(d @ W_out) (one fma
+    per class, class order; oracle/c lsig_fma); ragged batches (B not a
+    multiple of 32) padded with zeros."""
+    from oracle.cbuild import lsig_fma_c
     import ctypes
     from paper_2510_19764_b200 import _lib
     from paper_2510_19764_b200.classifier import _Plan
@@ -416,11 +418,7 @@ def test_eprop_pass_replica_minor(dev_lib, P, H, cap, R, B, k):
         assert np.allclose(gw.cpu().numpy(), gw_o, rtol=1e-12, atol=1e-12)
         assert np.allclose(gb.cpu().numpy(), gb_o, rtol=1e-12, atol=1e-12)
         for j, s in enumerate(steps):
-            dn, wn = s["d"].cpu().numpy(), w_out.cpu().numpy()
-            ls = np.zeros((B, H))
-            for c in range(C):
-                ls = ls + dn[:, c:c + 1] * wn[c][None, :]
-            s["lsig"] = torch.from_numpy(ls.astype(np.float32)).cuda()
+            s["lsig"] = torch.from_numpy(lsig_fma_c(s["d"].cpu().numpy(), w_out.cpu().numpy())).cuda()
             assert torch.equal(lt[j, :, :B].T, s["lsig"]), j
             assert torch.equal(xt[j, :, :B].T, s["trace"]) and torch.equal(zt[j, :, :B].T, s["zbar"])
             assert torch.equal(pt[j, :, :B].T, s["psi"])
