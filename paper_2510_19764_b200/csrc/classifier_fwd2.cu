@@ -360,7 +360,21 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
 
     // ---- C: warp g selects its group of the ascending input rows and of the
     // ascending hidden rows straight from the spike words, then sums them ----
-    if (warp < G) {
+    if constexpr (2 * G <= NTH / 32) {
+      // spare warps (H > 256: G = 4): the input groups on warps 0..G-1, the
+      // hidden groups on warps G..2G-1 (separate partial rows, so the same sums)
+      if (warp < G) {
+        int* L = lists + warp * cap;
+        const int nin = group_rows(wsm + s * P.in_words, P.in_words, warp, G, L, lane);
+        sum_rows(L, nin, rlen, reinterpret_cast<const int2*>(P.in_tw), P.in_tw_stride, pin + warp * H, lane);
+      } else if (warp < 2 * G) {
+        const int g = warp - G;
+        int* Lh = lists + g * cap + (NI + G - 1) / G + 1;
+        const int nhd = group_rows(zws, HW, g, G, Lh, lane);
+        sum_rows(Lh, nhd, rlen + NI, reinterpret_cast<const int2*>(P.rec_tw), P.rec_tw_stride, prc + g * H,
+                 lane);
+      }
+    } else if (warp < G) {
       int* L = lists + warp * cap;
       int nin, nhd;
       int* Lh;
