@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
   }
 
   int cur = P.t % nslot;
+  uint32_t* zw_step = P.z_bits + (int64_t)b * HW;   // this replica's spike words of step s
   for (int s = 0; s < nsteps; ++s, cur = (cur + 1 == nslot) ? 0 : cur + 1) {
     float* zbar_o = P.zbar + cur * B * H;
     float* psi_o = P.psi + cur * B * H;
@@ -330,7 +331,8 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
 #pragma unroll
     for (int j = 0; j < HPT; ++j) hm[j] = __ballot_sync(SW_FULL_MASK, (h0 + j < H) && z[j] != 0.0f);
     {
-      uint32_t* zw = P.z_bits + ((int64_t)s * B + b) * HW;
+      uint32_t* zw = zw_step;
+      zw_step += (int64_t)B * HW;
       if (HPT == 1) {
         if (lane == 0 && warp < HW) {
           zws[warp] = hm[0];
