@@ -418,8 +418,9 @@ typedef struct sw_clf_step {
    * (zbar_in/xbar_in ignored).  n_steps = 0: one step, fields as above. */
   int32_t n_steps; int32_t slot_count;
   /* packed (target, f32 weight) rows, [num_pre][tw_stride] int32 pairs with
-   * an even tw_stride (sw_clf_pack_rows): the register-resident forward
-   * kernel stages a spiking row with one bulk copy.  NULL: k_clf_step. */
+   * an even tw_stride (sw_clf_pack_rows): read entry by entry by the
+   * grouped forward (in_bits), staged with one bulk copy per spiking row by
+   * the single-step register-resident forward.  NULL: k_clf_step. */
   const int32_t* in_tw; const int32_t* rec_tw;
   int32_t in_tw_stride; int32_t rec_tw_stride;
   /* precomputed input spikes (sw_clf_inputs), grouped launches only:
