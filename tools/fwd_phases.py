@@ -25,9 +25,11 @@ prof = L.sw_debug_fwd2_prof
 tr._prepare(False)
 st = _lib.stream_ptr()
 for t0 in range(0, 400, 8):
-    _lib.call("sw_clf_step", ctypes.byref(tr._group_params(t0, 8)), st)
+    _lib.call("sw_clf_step", ctypes.byref(tr._group_params(t0, 8)), st)   # steady state
 torch.cuda.synchronize()
-names = ["start", "B1", "work>B2", "B2", "landed", "work>B3", "B3", "end"]
+# markers of k_clf_fwd2 (FWD2_PROF): 0 step start, 1 after B1, 4 rows
+# selected, 5 row sums done, 6 after B3, 7 step end (2, 3 unused)
+names = ["start", "B1", "-", "-", "selected", "summed", "B3", "end"]
 acc = {}
 for rep in range(10):
     prof(1, None)
@@ -40,4 +42,5 @@ for rep in range(10):
         for w in range(8):
             acc.setdefault((i, w), []).append(out[i * 8 + w] - t0)
 for i in range(8):
-    print(f"{names[i]:9s} " + " ".join(f"{sum(acc[(i, w)]) / len(acc[(i, w)]):7.0f}" for w in range(8)))
+    if names[i] != "-":
+        print(f"{names[i]:9s} " + " ".join(f"{sum(acc[(i, w)]) / len(acc[(i, w)]):7.0f}" for w in range(8)))
