@@ -450,3 +450,97 @@ def test_eprop_pass_replica_minor(dev_lib, P, H, cap, R, B, k):
         gr = ref_grad.cpu().numpy()
         mask = np.arange(cap)[None, :] < rl[:, None]
         assert np.allclose(g.cpu().numpy()[mask], gr[mask], rtol=1e-13, atol=1e-13 * np.abs(gr).max())
+
+
+def test_eprop_interleaved_psl_and_zero_state(dev_lib):
+    """The trainer's e-prop options against the plain layout: sw_eprop_prep
+    writing psi / lsig interleaved (psl_t) and sw_eprop_pass reading them
+    (psl = 1), with the first pass starting eps / ebar from zero without
+    reading them (state_zero = 1; the state buffers hold garbage) -- eps,
+    ebar, gradient and the de-interleaved psi / lsig bit-identical to separate
+    arrays and explicitly zeroed state."""
+    import ctypes
+    from paper_2510_19764_b200 import _lib
+    from paper_2510_19764_b200.classifier import _Plan
+    from paper_2510_19764_b200.connectivity import RaggedMatrix
+    P, H, cap, B, C, k = 300, 96, 30, 70, 20, 6
+    rs = np.random.default_rng(7)
+    tg = np.zeros((P, cap), np.int32)
+    rl = np.zeros(P, np.int32)
+    for i in range(P):
+        n = int(min(cap, rs.poisson(10.0)))
+        tg[i, :n] = rs.choice(H, size=n, replace=False)
+        rl[i] = n
+    m = RaggedMatrix(P, H, cap)
+    m.load_state(rl, tg)
+    plans = []
+    for _ in range(2):
+        pl = _Plan(m, B, shift=0, layout="chunk")
+        pl.ensure(int(rl.sum()))
+        pl.build()
+        plans.append(pl)
+    L = plans[0].ldb
+    plans[0].eps.fill_(7.0)        # garbage: state_zero must not read it
+    plans[0].ebar.fill_(-3.0)
+    plans[1].eps.zero_()
+    plans[1].ebar.zero_()
+    f = lambda *s: torch.from_numpy(rs.random(s).astype(np.float32)).cuda()  # noqa: E731
+    w_out = torch.from_numpy(rs.standard_normal((C, H))).cuda()
+    beta, rho, alpha = (float(np.float32(x)) for x in (0.0174, 0.9995, 0.95))
+    psl = torch.zeros((k, H, 2 * L), dtype=torch.float32, device="cuda")
+    xt = torch.zeros((k, P, L), dtype=torch.float32, device="cuda")
+    zt = [torch.zeros((k, H, L), dtype=torch.float32, device="cuda") for _ in range(2)]
+    pt, lt = (torch.zeros((k, H, L), dtype=torch.float32, device="cuda") for _ in range(2))
+    scr = [torch.zeros(int(_lib.lib().sw_eprop_pass_scratch_bytes(pl.e_pad, L)) // 8 + 1,
+                       dtype=torch.float64, device="cuda") for pl in plans]
+    for rep in range(2):
+        steps = [dict(trace=f(B, P) * 2, psi=f(B, H) * 0.5, zbar=f(B, H),
+                      d=torch.from_numpy(rs.standard_normal((B, C))).cuda()) for _ in range(k)]
+        for j, s in enumerate(steps):
+            xt[j, :, :B] = s["trace"].T
+        for v, pl in enumerate(plans):
+            pr = _lib.EpropPrep()
+            pr.k, pr.batch, pr.ldb, pr.num_inputs, pr.hidden, pr.num_classes = k, B, L, P, H, C
+            for j, s in enumerate(steps):
+                pr.zbar[j], pr.psi[j], pr.d[j] = s["zbar"].data_ptr(), s["psi"].data_ptr(), s["d"].data_ptr()
+            pr.w_out, pr.zbar_t = w_out.data_ptr(), zt[v].data_ptr()
+            if v == 0:
+                pr.psl_t = psl.data_ptr()
+            else:
+                pr.psi_t, pr.lsig_t = pt.data_ptr(), lt.data_ptr()
+            _lib.call("sw_eprop_prep", ctypes.byref(pr), _lib.stream_ptr())
+            segs = (_lib.EpropTSeg * 1)()
+            segs[0] = pl.tseg([xt[j] for j in range(k)])
+            tp = _lib.EpropTPass()
+            tp.k, tp.scratch = k, scr[v].data_ptr()
+            for j in range(k):
+                tp.psi_t[j], tp.lsig_t[j] = ((psl[j].data_ptr(), 0) if v == 0
+                                             else (pt[j].data_ptr(), lt[j].data_ptr()))
+            tp.psl = 1 if v == 0 else 0
+            tp.state_zero = 1 if (v == 0 and rep == 0) else 0
+            _lib.call("sw_eprop_pass", ctypes.cast(segs, ctypes.c_void_p), 1, ctypes.byref(tp), L, beta, rho,
+                      alpha, _lib.stream_ptr())
+        torch.cuda.synchronize()
+        q = psl.view(k, H, L // 4, 2, 4)
+        assert torch.equal(q[:, :, :, 0, :].reshape(k, H, L), pt)
+        assert torch.equal(q[:, :, :, 1, :].reshape(k, H, L), lt)
+        assert torch.equal(plans[0].eps, plans[1].eps) and torch.equal(plans[0].ebar, plans[1].ebar)
+        assert torch.equal(plans[0].grad, plans[1].grad)
+
+
+def test_zero_ranges(dev_lib):
+    """sw_zero_ranges zeroes exactly its ranges (unaligned starts and odd
+    byte counts included) and nothing around them."""
+    import ctypes
+    from paper_2510_19764_b200 import _lib
+    buf = torch.full((1 << 16,), 0xAB, dtype=torch.uint8, device="cuda")
+    ranges = [(3, 1), (17, 45), (256, 4096), (5000, 3), (8191, 20001)]
+    base = buf.data_ptr()
+    ptrs = (ctypes.c_void_p * len(ranges))(*[base + a for a, _ in ranges])
+    nbytes = (ctypes.c_int64 * len(ranges))(*[n for _, n in ranges])
+    _lib.call("sw_zero_ranges", ptrs, nbytes, len(ranges), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    want = np.full(1 << 16, 0xAB, np.uint8)
+    for a, n in ranges:
+        want[a:a + n] = 0
+    assert np.array_equal(buf.cpu().numpy(), want)
