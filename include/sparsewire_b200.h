@@ -361,7 +361,9 @@ SW_API int sw_eprop_pass_reduce(const sw_eprop_tseg_t* segs, int32_t n_segs, int
                                 void* stream);
 /* synapses per warp tile of sw_eprop_pass (SPW): eps/ebar are laid out
  * [e_pad/SPW][ldb/32][32 lanes][SPW replicas], lane = (32/SPW)*synapse + group */
+#ifndef SW_EPROP_PASS_SPW
 #define SW_EPROP_PASS_SPW 4
+#endif
 SW_API int32_t sw_eprop_pass_synapses_per_warp(void);
 SW_API int64_t sw_eprop_pass_scratch_bytes(int32_t e_pad_total, int32_t ldb);
 SW_API int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const sw_eprop_tpass_t* p,

@@ -358,6 +358,8 @@ template <int RPL>
 __device__ __forceinline__ void ldp(unsigned long long (&v)[RPL / 2], const float* p) {
   if constexpr (RPL == 8) {
     asm("ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%4];" : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p));
+  } else if constexpr (RPL == 2) {
+    asm("ld.global.nc.b64 %0, [%1];" : "=l"(v[0]) : "l"(p));
   } else {
     asm("ld.global.nc.v2.b64 {%0,%1}, [%2];" : "=l"(v[0]), "=l"(v[1]) : "l"(p));
   }
@@ -366,6 +368,8 @@ template <int RPL>
 __device__ __forceinline__ void ldp_cs(unsigned long long (&v)[RPL / 2], const float* p) {
   if constexpr (RPL == 8) {
     asm("ld.global.cs.v4.b64 {%0,%1,%2,%3}, [%4];" : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p));
+  } else if constexpr (RPL == 2) {
+    asm("ld.global.cs.b64 %0, [%1];" : "=l"(v[0]) : "l"(p));
   } else {
     asm("ld.global.cs.v2.b64 {%0,%1}, [%2];" : "=l"(v[0]), "=l"(v[1]) : "l"(p));
   }
@@ -375,6 +379,8 @@ __device__ __forceinline__ void stp_cs(float* p, const unsigned long long (&v)[R
   if constexpr (RPL == 8) {
     asm volatile("st.global.cs.v4.b64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(v[0]), "l"(v[1]), "l"(v[2]), "l"(v[3])
                  : "memory");
+  } else if constexpr (RPL == 2) {
+    asm volatile("st.global.cs.b64 [%0], %1;" ::"l"(p), "l"(v[0]) : "memory");
   } else {
     asm volatile("st.global.cs.v2.b64 [%0], {%1,%2};" ::"l"(p), "l"(v[0]), "l"(v[1]) : "memory");
   }
@@ -385,7 +391,13 @@ __device__ __forceinline__ void stp_cs(float* p, const unsigned long long (&v)[R
 template <int RPL, bool PSL>
 __device__ __forceinline__ void load_pl(unsigned long long (&pv)[RPL / 2], unsigned long long (&lv)[RPL / 2],
                                         const float* psi, const float* lsig, int64_t off) {
-  if constexpr (PSL) {
+  if constexpr (PSL && RPL == 2) {
+    // two replicas (an aligned pair) of a 4-replica group: psi pair, then
+    // the lsig pair 4 floats later
+    const float* q = psi + ((off & ~3ll) * 2 + (off & 3));
+    asm("ld.global.nc.b64 %0, [%1];" : "=l"(pv[0]) : "l"(q));
+    asm("ld.global.nc.b64 %0, [%1];" : "=l"(lv[0]) : "l"(q + 4));
+  } else if constexpr (PSL) {
     unsigned long long v[4];
     asm("ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%4];" : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3])
         : "l"(psi + 2 * off));
@@ -407,7 +419,7 @@ __device__ __forceinline__ void load_pl(unsigned long long (&pv)[RPL / 2], unsig
 template <int K, int PD, int SPW, int MB, bool PSL>
 __global__ void __launch_bounds__(kTW * 32, MB) k_eprop_t(const TPass T) {
   constexpr int LPS = 32 / SPW, RPL = 32 / LPS, NP = RPL / 2;
-  static_assert(!PSL || RPL == 4, "interleaved psi/lsig: 4 replicas per lane");
+  static_assert(!PSL || RPL == 4 || RPL == 2, "interleaved psi/lsig: 2 or 4 replicas per lane");
   const int lane = threadIdx.x & 31;
   const int sl = lane / LPS, g = lane % LPS;
   const int tiles0 = T.s[0].tiles;
@@ -634,6 +646,8 @@ extern "C" int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const 
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kTW * 32, 0);
     if (per_sm < 1) per_sm = 1;
+    static const int cap_sm = [] { const char* e = getenv("SW_EPT_PER_SM"); return e ? atoi(e) : 0; }();
+    if (cap_sm > 0 && cap_sm < per_sm) per_sm = cap_sm;   // measurement: leave room on the SMs
     int blocks = 148 * per_sm;
     if (blocks * kTW > items) blocks = (items + kTW - 1) / kTW;
     kfn<<<blocks, kTW * 32, 0, st>>>(T);
