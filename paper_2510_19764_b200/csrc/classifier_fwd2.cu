@@ -60,19 +60,22 @@ __global__ void __launch_bounds__(256) k_clf_spikes(const sw_clf_inputs_t P) {
   const int NI = P.num_inputs, W = P.words;
   const int b = blockIdx.x;
   const uint64_t key = __ldg(P.ex_key + b);
-  for (int x = threadIdx.x; x < NI; x += blockDim.x) s_thr[x] = (uint64_t)ceil(__ldg(P.p_in + (int64_t)b * NI + x) * 0x1p53);
+  // thresholds as [bit j][word w]: the lanes of a warp (consecutive words)
+  // read consecutive entries (a [w][j] layout puts all 32 lanes in one bank)
+  for (int x = threadIdx.x; x < NI; x += blockDim.x)
+    s_thr[(x & 31) * W + (x >> 5)] = (uint64_t)ceil(__ldg(P.p_in + (int64_t)b * NI + x) * 0x1p53);
   __syncthreads();
   const int t0 = blockIdx.y * kSpkSteps;
   const int items = min(kSpkSteps, P.steps - t0) * W;
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int tt = it / W, w = it - tt * W, t = t0 + tt;
     const int n = min(32, NI - w * 32);
-    const uint64_t* thr = s_thr + w * 32;
+    const uint64_t* thr = s_thr + w;
     const uint64_t c0 = (uint64_t)t * (uint64_t)NI + (uint64_t)(w * 32);
     uint32_t bits = 0;
 #pragma unroll 4
     for (int j = 0; j < n; ++j)
-      if ((sw::draw(key, c0 + j) >> 11) < thr[j]) bits |= 1u << j;
+      if ((sw::draw(key, c0 + j) >> 11) < thr[j * W]) bits |= 1u << j;
     P.in_bits[((int64_t)t * P.batch + b) * W + w] = bits;
   }
 }
@@ -593,7 +596,7 @@ extern "C" int sw_clf_inputs(const sw_clf_inputs_t* p, void* stream) {
     return SW_ERR_INVALID_ARG;
   }
   if (p->steps == 0) return SW_OK;
-  const size_t thr_bytes = (size_t)p->num_inputs * 8;
+  const size_t thr_bytes = (size_t)p->words * 32 * 8;
   if (thr_bytes > 200 * 1024) {
     sw::set_last_error("sw_clf_inputs: num_inputs > 25600 (spike thresholds are staged in shared memory)");
     return SW_ERR_INVALID_ARG;
