@@ -56,9 +56,12 @@ __host__ __device__ __forceinline__ int64_t psl_index(int64_t row, int64_t L, in
   return (row * L + (b & ~3)) * 2 + (b & 3);
 }
 constexpr int kMaxC = 32;
+// d of the replica tile, class-major with one pad double per class row: the
+// class-fastest stores of the coalesced d read then hit distinct banks
+constexpr int kDT = kBT + 1;
 
 __host__ __device__ inline size_t prep_smem_bytes(int C) {
-  return (size_t)2 * kBT * (kHT + 1) * 4 + (size_t)C * kHT * 8 + (size_t)kBT * C * 8;
+  return (size_t)2 * kBT * (kHT + 1) * 4 + (size_t)C * kHT * 8 + (size_t)kDT * C * 8;
 }
 
 // CT: the class count as a compile-time constant (0 = runtime, any count);
@@ -72,7 +75,7 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
   const int C = CT ? CT : P.num_classes;
   const int H = P.hidden, NI = P.num_inputs, B = P.batch;
   const int64_t L = P.ldb;
-  double* dt = ws + (size_t)C * kHT;                                                  // [C][kBT]
+  double* dt = ws + (size_t)C * kHT;                                                  // [C][kDT]
   const int ht = blockIdx.x, bt = blockIdx.y, k = blockIdx.z;
   const int h0 = ht * kHT, b0 = bt * kBT;
   const int nh = min(kHT, H - h0);
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
     }
     for (int x = tid; x < kBT * C; x += 256) {   // coalesced read of d, class-major store
       const int b = x / C, c = x - b * C;
-      dt[c * kBT + b] = b0 + b < B ? P.d[k][(int64_t)(b0 + b) * C + c] : 0.0;
+      dt[c * kDT + b] = b0 + b < B ? P.d[k][(int64_t)(b0 + b) * C + c] : 0.0;
     }
   }
   __syncthreads();
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
     if constexpr (CT > 0) {
       double dr[CT];
 #pragma unroll
-      for (int c = 0; c < CT; ++c) dr[c] = dt[c * kBT + lane];
+      for (int c = 0; c < CT; ++c) dr[c] = dt[c * kDT + lane];
       for (int r = warp; r < nh; r += 8) {
         double ls = 0.0;
 #pragma unroll
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
     } else {
       for (int r = warp; r < nh; r += 8) {
         double ls = 0.0;
-        for (int c = 0; c < C; ++c) ls = __fma_rn(dt[c * kBT + lane], ws[c * kHT + r], ls);
+        for (int c = 0; c < C; ++c) ls = __fma_rn(dt[c * kDT + lane], ws[c * kHT + r], ls);
         if (b0 + lane < L) *lsig_at(r) = b0 + lane < B ? __double2float_rn(ls) : 0.f;
       }
     }
@@ -190,11 +193,11 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
         double acc[CP];
 #pragma unroll
         for (int u = 0; u < CP; ++u) acc[u] = 0.0;
-        const double* dg = dt + cg * CP * kBT;
+        const double* dg = dt + cg * CP * kDT;
         for (int b = 0; b < kBT; ++b) {
           const double z = (double)tile[b][r];
 #pragma unroll
-          for (int u = 0; u < CP; ++u) acc[u] = __fma_rn(dg[u * kBT + b], z, acc[u]);
+          for (int u = 0; u < CP; ++u) acc[u] = __fma_rn(dg[u * kDT + b], z, acc[u]);
         }
 #pragma unroll
         for (int u = 0; u < CP; ++u) {
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
         const int cper = (C + 3) / 4, ca = cg * cper, cb = min(C, ca + cper);
         for (int c = ca; c < cb; ++c) {
           double acc = 0.0;
-          for (int b = 0; b < kBT; ++b) acc = __fma_rn(dt[c * kBT + b], (double)tile[b][r], acc);
+          for (int b = 0; b < kBT; ++b) acc = __fma_rn(dt[c * kDT + b], (double)tile[b][r], acc);
           double* pp = part + (int64_t)c * H + h0 + r;
           *pp = P.defer_reduce ? __dadd_rn(*pp, acc) : acc;
         }
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
     }
     if (ht == 0 && tid < C) {
       double sb = 0.0;
-      for (int b = 0; b < kBT; ++b) sb = __dadd_rn(sb, dt[tid * kBT + b]);
+      for (int b = 0; b < kBT; ++b) sb = __dadd_rn(sb, dt[tid * kDT + b]);
       double* pp = part + (int64_t)C * H + tid;
       *pp = P.defer_reduce ? __dadd_rn(*pp, sb) : sb;
     }
