@@ -83,11 +83,14 @@ __global__ void __launch_bounds__(256) k_clf_spikes(const sw_clf_inputs_t P) {
 // (2) the xbar recursion (classifier.py:212-213): block = (word of 32 inputs,
 //     32 replicas), warp = input, lane = replica, steps in order; the
 //     block's spike words staged through shared memory kXbSteps steps at a
-//     time (one load per (step, replica) instead of one per input), xbar
-//     written replica-minor
+//     time (one load per (step, replica) instead of one per input), double
+//     buffered: a chunk's words are loaded into registers before the
+//     previous chunk is computed and stored to shared memory after it, so
+//     one barrier per chunk and no exposed load latency; xbar written
+//     replica-minor
 constexpr int kXbSteps = 32;
 __global__ void __launch_bounds__(1024) k_clf_xbar(const sw_clf_inputs_t P) {
-  __shared__ uint32_t s_w[kXbSteps][33];
+  __shared__ uint32_t s_w[2][kXbSteps][33];
   const int NI = P.num_inputs;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int w = blockIdx.x;
@@ -99,18 +102,23 @@ __global__ void __launch_bounds__(1024) k_clf_xbar(const sw_clf_inputs_t P) {
   const uint32_t* wp = P.in_bits + (int64_t)(bok ? b : 0) * P.words + w;
   float* out = P.xbar_t + (int64_t)x * P.ldb + b;
   float xb = 0.0f;
-  for (int t0 = 0; t0 < P.steps; t0 += kXbSteps) {
+  // chunk 0's words
+  if (warp < min(kXbSteps, P.steps)) s_w[0][warp][lane] = bok ? __ldg(wp + (int64_t)warp * tstride) : 0u;
+  __syncthreads();
+  for (int t0 = 0, cb = 0; t0 < P.steps; t0 += kXbSteps, cb ^= 1) {
     const int nt = min(kXbSteps, P.steps - t0);
-    __syncthreads();
-    if (warp < nt) s_w[warp][lane] = bok ? __ldg(wp + (int64_t)(t0 + warp) * tstride) : 0u;
-    __syncthreads();
+    // the next chunk's word of this thread, in flight during this chunk
+    const int tn = t0 + kXbSteps + warp;
+    const uint32_t nxt = (tn < P.steps && bok) ? __ldg(wp + (int64_t)tn * tstride) : 0u;
     if (x < NI) {
       for (int tt = 0; tt < nt; ++tt) {
-        const bool sp = (s_w[tt][lane] >> warp) & 1u;
+        const bool sp = (s_w[cb][tt][lane] >> warp) & 1u;
         xb = __fadd_rn(__fmul_rn(xb, P.alpha), sp ? 1.0f : 0.0f);
         out[(int64_t)(t0 + tt) * plane] = bok ? xb : 0.0f;
       }
     }
+    if (t0 + kXbSteps < P.steps && warp < kXbSteps) s_w[cb ^ 1][warp][lane] = nxt;
+    __syncthreads();
   }
 }
 
