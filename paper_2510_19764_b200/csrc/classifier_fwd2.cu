@@ -476,6 +476,7 @@ __global__ void __launch_bounds__(256) k_clf_readout(const sw_clf_step_t P) {
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int kW = 8;
   const int bC = b * C;
+  const int label = P.labels[b];   // loaded early: read after the sums
   for (int c = tid; c < C; c += blockDim.x) s_bo[c] = P.b_out[c];
   // 1
   for (int t = warp; t < n; t += kW) {
@@ -529,7 +530,6 @@ __global__ void __launch_bounds__(256) k_clf_readout(const sw_clf_step_t P) {
   }
   __syncthreads();
   // 4
-  const int label = P.labels[b];
   const int nslot = P.slot_count;
   for (int t = warp; t < n; t += kW) {
     const double* yv = s_y + (size_t)t * C;
@@ -560,12 +560,16 @@ __global__ void __launch_bounds__(256) k_clf_readout(const sw_clf_step_t P) {
       double ps = P.pi_sum[bC + c];
       for (int t = 0; t < n; ++t) ps = ps + s_pi[t * C + c];
       P.pi_sum[bC + c] = ps;
-      if (c == label) {
-        double ls = P.loss[b];
-        for (int t = 0; t < n; ++t) ls = ls + -log(s_pi[t * C + c]);
-        P.loss[b] = ls;
-      }
     }
+  } else if (warp == 1) {
+    // the loss terms -log(pi[t][label]) of the steps in parallel (lane =
+    // step), then added in step order by lane 0
+    double ls = P.loss[b];
+    for (int t0 = 0; t0 < n; t0 += 32) {
+      const double term = t0 + lane < n ? -log(s_pi[(t0 + lane) * C + label]) : 0.0;
+      for (int u = 0; u < 32 && t0 + u < n; ++u) ls = ls + __shfl_sync(SW_FULL_MASK, term, u);
+    }
+    if (lane == 0) P.loss[b] = ls;
   }
 }
 
