@@ -81,6 +81,36 @@ __device__ __forceinline__ void col_sum(double& acc, int a, int e, const int32_t
   }
 }
 
+// the first kColU entries of both columns (ff, then lat) loaded together —
+// their pre ids, spike words and (spiking entries) weights — so the two
+// columns' round trips overlap; the sums still run ff entries ascending,
+// then lat entries ascending (the order col_sum gives)
+struct ColBatch {
+  double v[kColU];
+  unsigned hit;
+};
+__device__ __forceinline__ void col_load(ColBatch& cb, int a, int e, const int32_t* src_pre, const int32_t* src_slot,
+                                         const uint32_t* bits, const double* g, int stride) {
+  int pre[kColU];
+  uint32_t wd[kColU];
+#pragma unroll
+  for (int u = 0; u < kColU; ++u) pre[u] = (a + u < e) ? src_pre[a + u] : -1;
+#pragma unroll
+  for (int u = 0; u < kColU; ++u) wd[u] = pre[u] >= 0 ? bits[pre[u] >> 5] : 0u;
+  cb.hit = 0u;
+#pragma unroll
+  for (int u = 0; u < kColU; ++u) {
+    const bool h = (wd[u] >> (pre[u] & 31)) & 1u;
+    cb.v[u] = h ? g[(int64_t)pre[u] * stride + src_slot[a + u]] : 0.0;
+    cb.hit |= (h ? 1u : 0u) << u;
+  }
+}
+__device__ __forceinline__ void col_add(double& acc, const ColBatch& cb) {
+#pragma unroll
+  for (int u = 0; u < kColU; ++u)
+    if ((cb.hit >> u) & 1u) acc = __dadd_rn(acc, cb.v[u]);
+}
+
 __device__ __forceinline__ void tm_prop(const sw_topomap_step_t& S, int t0, int dt) {
   for (int j = t0; j < S.n; j += dt) {
     // trace decays (x per pre, y per post; square model: n pres and n posts)
@@ -90,10 +120,15 @@ __device__ __forceinline__ void tm_prop(const sw_topomap_step_t& S, int t0, int 
     S.lat_y[j] = __dmul_rn(S.lat_y[j], S.decay_y);
     if (j < S.post_lo || j >= S.post_hi) continue;
     double acc = 0.0;
-    col_sum(acc, S.ff_col_ptr[j], S.ff_col_ptr[j] + S.ff_col_len[j], S.ff_src_pre, S.ff_src_slot, S.src_bits, S.ff_g,
-            S.ff_stride);
-    col_sum(acc, S.lat_col_ptr[j], S.lat_col_ptr[j] + S.lat_col_len[j], S.lat_src_pre, S.lat_src_slot, S.tgt_bits,
-            S.lat_g, S.lat_stride);
+    const int fa = S.ff_col_ptr[j], fe = fa + S.ff_col_len[j];
+    const int la = S.lat_col_ptr[j], le = la + S.lat_col_len[j];
+    ColBatch fb, lb;
+    col_load(fb, fa, fe, S.ff_src_pre, S.ff_src_slot, S.src_bits, S.ff_g, S.ff_stride);
+    col_load(lb, la, le, S.lat_src_pre, S.lat_src_slot, S.tgt_bits, S.lat_g, S.lat_stride);
+    col_add(acc, fb);
+    col_sum(acc, fa + kColU, fe, S.ff_src_pre, S.ff_src_slot, S.src_bits, S.ff_g, S.ff_stride);
+    col_add(acc, lb);
+    col_sum(acc, la + kColU, le, S.lat_src_pre, S.lat_src_slot, S.tgt_bits, S.lat_g, S.lat_stride);
     S.pending[j] = acc;
   }
 }
