@@ -222,21 +222,35 @@ __device__ __forceinline__ void tm_count(const sw_topomap_step_t& S, int w0, int
 }
 
 // ---- one phase per launch (the sharded path splits the step around an all-gather) --
+// programmatic dependent launch (the per-step kernels are launched with the
+// PDL attribute): a kernel lets the next one be scheduled as soon as all its
+// blocks run, and waits for the previous kernel's completion (and memory)
+// before its first access — the launch latency of a phase overlaps the tail
+// of the one before.  Without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __global__ void k_tm_neurons(sw_topomap_step_t S) {
+  pdl_enter();
   tm_neurons(S, *S.step, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 __global__ void k_tm_prop(sw_topomap_step_t S, int64_t* spike_counts) {
+  pdl_enter();
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, gn = gridDim.x * blockDim.x;
   tm_prop(S, gt, gn);
   if (spike_counts) tm_count(S, gt, gn, spike_counts);
 }
 
 __global__ void k_tm_pre(sw_topomap_step_t S) {
+  pdl_enter();
   tm_pre(S, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gridDim.x * (blockDim.x >> 5));
 }
 
 __global__ void k_tm_post(sw_topomap_step_t S) {
+  pdl_enter();
   tm_post(S, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gridDim.x * (blockDim.x >> 5));
   // the step counter is read only by the next step's neuron phase
   if (blockIdx.x == 0 && threadIdx.x == 0) *S.step += 1;
@@ -370,6 +384,28 @@ int grid1(int64_t n) {
   return (int)(g < 1 ? 1 : g);
 }
 
+// launch with the programmatic-stream-serialization attribute (PDL; kernels
+// start with pdl_enter) for sheets of up to 16 384 nodes (s <= 8: 2.5-4 %
+// faster per step; at 65 536 nodes the early-resident dependent blocks cost
+// more than the launch latency they hide, -4.5 %); SW_TM_PDL=0 launches
+// plainly (measurement)
+template <typename... KArgs, typename... Args>
+void launch_pdl(int n, void (*kern)(KArgs...), int grid, int block, cudaStream_t st, Args... args) {
+  static const bool env_on = [] { const char* e = getenv("SW_TM_PDL"); return !(e && e[0] == '0'); }();
+  const bool on = env_on && n <= 16384;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = on ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 }  // namespace
 
 static int check_step(const sw_topomap_step_t* s) {
@@ -385,7 +421,7 @@ extern "C" int sw_topomap_neurons(const sw_topomap_step_t* s, void* stream) {
   if (int e = check_step(s)) return e;
   const int n = s->n;
   if (n <= 0) return SW_OK;
-  k_tm_neurons<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(*s); sw::count_launch();
+  launch_pdl(n, k_tm_neurons, grid1(n), 256, (cudaStream_t)stream, *s); sw::count_launch();
   SW_CHECK_LAUNCH("sw_topomap_neurons");
   return SW_OK;
 }
@@ -395,14 +431,14 @@ extern "C" int sw_topomap_synapses(const sw_topomap_step_t* s, int64_t* spike_co
   cudaStream_t st = (cudaStream_t)stream;
   const int n = s->n;
   if (n <= 0) return SW_OK;
-  k_tm_prop<<<grid1(n), 256, 0, st>>>(*s, spike_counts); sw::count_launch();
+  launch_pdl(n, k_tm_prop, grid1(n), 256, st, *s, spike_counts); sw::count_launch();
   int groups = (n + 31) / 32;
   int blocks = (2 * groups + 7) / 8;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_tm_pre<<<blocks, 256, 0, st>>>(*s); sw::count_launch();
+  launch_pdl(n, k_tm_pre, blocks, 256, st, *s); sw::count_launch();
   int pblocks = (groups + 7) / 8;
   if (pblocks > 148 * 8) pblocks = 148 * 8;
-  k_tm_post<<<pblocks, 256, 0, st>>>(*s); sw::count_launch();
+  launch_pdl(n, k_tm_post, pblocks, 256, st, *s); sw::count_launch();
   SW_CHECK_LAUNCH("sw_topomap_synapses");
   return SW_OK;
 }
