@@ -283,6 +283,7 @@ __device__ __forceinline__ void sum_rows(const IDX* list, int nr, const int* rl,
 template <int NTH, int HPT, int GT>
 __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  sw::pdl_enter();
   constexpr int kT2 = NTH;
   constexpr int G = GT;
   const int H = P.hidden, NI = P.num_inputs;
@@ -465,6 +466,7 @@ __host__ __device__ inline size_t readout_smem(int n_steps, int H, int C) {
 
 __global__ void __launch_bounds__(256) k_clf_readout(const sw_clf_step_t P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  sw::pdl_enter();
   const int H = P.hidden, C = P.num_classes, B = P.batch, n = P.n_steps;
   const int HW = (H + 31) / 32;
   double* s_sum = reinterpret_cast<double*>(smem_raw);      // [n][C]
@@ -573,6 +575,12 @@ __global__ void __launch_bounds__(256) k_clf_readout(const sw_clf_step_t P) {
   }
 }
 
+// SW_CLF_PDL=1: the trial's per-group kernels with programmatic dependent launch
+inline bool clf_pdl() {
+  static const bool on = [] { const char* e = getenv("SW_CLF_PDL"); return e && e[0] == '1'; }();
+  return on;
+}
+
 template <int NTH, int HPT, int GT>
 int launch_fwd2(const sw_clf_step_t* p, size_t smem, cudaStream_t st) {
   static bool attr = false;
@@ -581,7 +589,7 @@ int launch_fwd2(const sw_clf_step_t* p, size_t smem, cudaStream_t st) {
                          200 * 1024);
     attr = true;
   }
-  k_clf_fwd2<NTH, HPT, GT><<<p->batch, NTH, smem, st>>>(*p);
+  sw::pdl_launch(clf_pdl(), k_clf_fwd2<NTH, HPT, GT>, dim3(p->batch), dim3(NTH), smem, st, *p);
   sw::count_launch();
   const size_t rsm = readout_smem(p->n_steps, p->hidden, p->num_classes);
   static size_t rsm_attr = 48 * 1024;
@@ -589,7 +597,7 @@ int launch_fwd2(const sw_clf_step_t* p, size_t smem, cudaStream_t st) {
     cudaFuncSetAttribute(k_clf_readout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
     rsm_attr = rsm;
   }
-  k_clf_readout<<<p->batch, 256, rsm, st>>>(*p);
+  sw::pdl_launch(clf_pdl(), k_clf_readout, dim3(p->batch), dim3(256), rsm, st, *p);
   sw::count_launch();
   return SW_OK;
 }

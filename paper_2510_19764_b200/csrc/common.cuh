@@ -77,3 +77,31 @@ void count_launch();
 }  // namespace sw
 
 #define SW_CHECK_LAUNCH(name) do { int _s = sw::check_launch(name); if (_s) return _s; } while (0)
+
+// ---- programmatic dependent launch -----------------------------------------
+// A kernel launched with pdl_launch may be scheduled while the previous
+// kernel in the stream drains; it must call pdl_enter() before touching
+// anything that kernel writes (griddepcontrol.wait: the previous grid has
+// completed and its memory is visible), and lets its own successor be
+// scheduled (launch_dependents).  Without the attribute both are no-ops.
+namespace sw {
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(bool on, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = on ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+}  // namespace sw

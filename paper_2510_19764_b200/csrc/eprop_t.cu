@@ -69,6 +69,7 @@ __host__ __device__ inline size_t prep_smem_bytes(int C) {
 template <int CT, int MB = 1>
 __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  sw::pdl_enter();
   float (*tile)[kHT + 1] = reinterpret_cast<float (*)[kHT + 1]>(smem_raw);                       // zbar
   float (*ptile)[kHT + 1] = reinterpret_cast<float (*)[kHT + 1]>(smem_raw + (size_t)kBT * (kHT + 1) * 4);   // psi
   double* ws = reinterpret_cast<double*>(smem_raw + (size_t)2 * kBT * (kHT + 1) * 4);   // [C][kHT]
@@ -423,6 +424,7 @@ template <int K, int PD, int SPW, int MB, bool PSL>
 __global__ void __launch_bounds__(kTW * 32, MB) k_eprop_t(const TPass T) {
   constexpr int LPS = 32 / SPW, RPL = 32 / LPS, NP = RPL / 2;
   static_assert(!PSL || RPL == 4 || RPL == 2, "interleaved psi/lsig: 2 or 4 replicas per lane");
+  sw::pdl_enter();
   const int lane = threadIdx.x & 31;
   const int sl = lane / LPS, g = lane % LPS;
   const int tiles0 = T.s[0].tiles;
@@ -547,10 +549,11 @@ extern "C" int sw_eprop_prep(const sw_eprop_prep_t* p, void* stream) {
   // 27.9 -> 25.0 us, C2 118.6 -> 96.6 us against the unconstrained 89, and
   // 26.2 / 99.0 us at 4 blocks, which spills); SW_PREP_MB=1|4 (measurement)
   static const int pmb = [] { const char* e = getenv("SW_PREP_MB"); return e ? atoi(e) : 3; }();
-  if (p->num_classes == 20 && pmb == 4) k_prep<20, 4><<<grid, 256, smem, st>>>(*p);   // the SHD-shaped task
-  else if (p->num_classes == 20 && pmb == 1) k_prep<20><<<grid, 256, smem, st>>>(*p);
-  else if (p->num_classes == 20) k_prep<20, 3><<<grid, 256, smem, st>>>(*p);
-  else k_prep<0, 2><<<grid, 256, smem, st>>>(*p);
+  static const bool pdl = [] { const char* e = getenv("SW_CLF_PDL"); return e && e[0] == '1'; }();
+  if (p->num_classes == 20 && pmb == 4) sw::pdl_launch(pdl, k_prep<20, 4>, grid, dim3(256), smem, st, *p);
+  else if (p->num_classes == 20 && pmb == 1) sw::pdl_launch(pdl, k_prep<20>, grid, dim3(256), smem, st, *p);
+  else if (p->num_classes == 20) sw::pdl_launch(pdl, k_prep<20, 3>, grid, dim3(256), smem, st, *p);   // the SHD-shaped task
+  else sw::pdl_launch(pdl, k_prep<0, 2>, grid, dim3(256), smem, st, *p);
   sw::count_launch();
   if (p->g_w_out && !p->defer_reduce) {
     const int n = p->num_classes * p->hidden + p->num_classes;
@@ -653,7 +656,8 @@ extern "C" int sw_eprop_pass(const sw_eprop_tseg_t* segs, int32_t n_segs, const 
     if (cap_sm > 0 && cap_sm < per_sm) per_sm = cap_sm;   // measurement: leave room on the SMs
     int blocks = 148 * per_sm;
     if (blocks * kTW > items) blocks = (items + kTW - 1) / kTW;
-    kfn<<<blocks, kTW * 32, 0, st>>>(T);
+    static const bool pdl = [] { const char* e = getenv("SW_CLF_PDL"); return e && e[0] == '1'; }();
+    sw::pdl_launch(pdl, kfn, dim3(blocks), dim3(kTW * 32), 0, st, T);
   };
   const int want = cfg ? cfg : 24;
   switch (p->k) {

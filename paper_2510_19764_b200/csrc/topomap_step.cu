@@ -222,15 +222,10 @@ __device__ __forceinline__ void tm_count(const sw_topomap_step_t& S, int w0, int
 }
 
 // ---- one phase per launch (the sharded path splits the step around an all-gather) --
-// programmatic dependent launch (the per-step kernels are launched with the
-// PDL attribute): a kernel lets the next one be scheduled as soon as all its
-// blocks run, and waits for the previous kernel's completion (and memory)
-// before its first access — the launch latency of a phase overlaps the tail
-// of the one before.  Without the attribute both are no-ops.
-__device__ __forceinline__ void pdl_enter() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
+// the per-step kernels start with sw::pdl_enter (common.cuh): launched with
+// the PDL attribute, a phase's blocks are scheduled while the previous phase
+// drains and wait for its completion before their first access
+using sw::pdl_enter;
 
 __global__ void k_tm_neurons(sw_topomap_step_t S) {
   pdl_enter();
@@ -392,18 +387,7 @@ int grid1(int64_t n) {
 template <typename... KArgs, typename... Args>
 void launch_pdl(int n, void (*kern)(KArgs...), int grid, int block, cudaStream_t st, Args... args) {
   static const bool env_on = [] { const char* e = getenv("SW_TM_PDL"); return !(e && e[0] == '0'); }();
-  const bool on = env_on && n <= 16384;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = on ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kern, args...);
+  sw::pdl_launch(env_on && n <= 16384, kern, dim3(grid), dim3(block), 0, st, args...);
 }
 
 }  // namespace
