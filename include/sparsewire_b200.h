@@ -661,6 +661,13 @@ SW_API int sw_topomap_neurons(const sw_topomap_step_t* s, void* stream);
 SW_API int sw_topomap_run_steps(const sw_topomap_step_t* s, int32_t n_steps, int64_t* spike_counts,
                                 uint32_t* barrier_words, void* stream);
 SW_API int sw_topomap_synapses(const sw_topomap_step_t* s, int64_t* spike_counts, void* stream);
+/* n_steps whole steps (unsharded sheet) as 3 launches per step: step t's
+ * STDP post phase and step t+1's neuron phase share one launch, the target
+ * spike words alternating between s->tgt_bits and tgt_bits_alt (same size);
+ * the last step's words end in s->tgt_bits.  Same results as n_steps calls
+ * of sw_topomap_step. */
+SW_API int sw_topomap_steps_fused(const sw_topomap_step_t* s, uint32_t* tgt_bits_alt, int32_t n_steps,
+                                  int64_t* spike_counts, void* stream);
 
 #ifdef __cplusplus
 }

@@ -251,6 +251,35 @@ __global__ void k_tm_post(sw_topomap_step_t S) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *S.step += 1;
 }
 
+// ---- fused period (unsharded sheets): step t's STDP post phase and step
+// t+1's neuron phase in one launch.  They share no data once the target
+// spike words alternate between two buffers (post(t) reads step t's words,
+// neurons(t+1) writes step t+1's) and the step counter is advanced by the
+// propagation phase instead of the post phase: 3 launches per step instead
+// of 4, and the two latency-bound phases overlap.
+__global__ void k_tm_prop_inc(sw_topomap_step_t S, int64_t* spike_counts) {
+  pdl_enter();
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gn = gridDim.x * blockDim.x;
+  tm_prop(S, gt, gn);
+  if (spike_counts) tm_count(S, gt, gn, spike_counts);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *S.step += 1;   // read by the next neuron phase only
+}
+
+__global__ void k_tm_post_neurons(sw_topomap_step_t Sp, sw_topomap_step_t Sn, int post_blocks) {
+  pdl_enter();
+  if ((int)blockIdx.x < post_blocks) {
+    tm_post(Sp, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), post_blocks * (blockDim.x >> 5));
+  } else {
+    const int b = blockIdx.x - post_blocks;
+    tm_neurons(Sn, *Sn.step, b * blockDim.x + threadIdx.x, (gridDim.x - post_blocks) * blockDim.x);
+  }
+}
+
+__global__ void k_tm_post_only(sw_topomap_step_t S) {
+  pdl_enter();
+  tm_post(S, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gridDim.x * (blockDim.x >> 5));
+}
+
 // ---- persistent multi-step kernel ------------------------------------------------------
 // n_steps whole steps in one launch: the phases of a step are separated by
 // grid-wide barriers (cooperative launch: every CTA resident) — or by
@@ -469,6 +498,43 @@ extern "C" int sw_topomap_run_steps(const sw_topomap_step_t* s, int32_t n_steps,
   cudaLaunchCooperativeKernel((const void*)k_tm_run, dim3(ctas), dim3(512), args, 0, (cudaStream_t)stream);
   sw::count_launch();
   SW_CHECK_LAUNCH("sw_topomap_run_steps");
+  return SW_OK;
+}
+
+extern "C" int sw_topomap_steps_fused(const sw_topomap_step_t* s, uint32_t* tgt_bits_alt, int32_t n_steps,
+                                      int64_t* spike_counts, void* stream) {
+  if (int e = check_step(s)) return e;
+  if (s->post_lo != 0 || s->post_hi != s->n || !tgt_bits_alt) {
+    sw::set_last_error("sw_topomap_steps_fused: unsharded sheets and a second target-spike buffer");
+    return SW_ERR_INVALID_ARG;
+  }
+  const int n = s->n;
+  if (n <= 0 || n_steps <= 0) return SW_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  sw_topomap_step_t S[2] = {*s, *s};
+  S[1].tgt_bits = tgt_bits_alt;
+  const int groups = (n + 31) / 32;
+  int blocks = (2 * groups + 7) / 8;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  int pblocks = (groups + 7) / 8;
+  if (pblocks > 148 * 8) pblocks = 148 * 8;
+  const int nblocks = grid1(n);
+  launch_pdl(n, k_tm_neurons, nblocks, 256, st, S[0]); sw::count_launch();
+  for (int t = 0; t < n_steps; ++t) {
+    const sw_topomap_step_t& Sc = S[t & 1];
+    launch_pdl(n, k_tm_prop_inc, nblocks, 256, st, Sc, spike_counts); sw::count_launch();
+    launch_pdl(n, k_tm_pre, blocks, 256, st, Sc); sw::count_launch();
+    if (t + 1 < n_steps) {
+      launch_pdl(n, k_tm_post_neurons, pblocks + nblocks, 256, st, Sc, S[(t + 1) & 1], pblocks);
+    } else {
+      launch_pdl(n, k_tm_post_only, pblocks, 256, st, Sc);
+    }
+    sw::count_launch();
+  }
+  // the last step's target spikes back into the model's buffer
+  if ((n_steps - 1) & 1)
+    cudaMemcpyAsync(s->tgt_bits, tgt_bits_alt, (size_t)groups * 4, cudaMemcpyDeviceToDevice, st);
+  SW_CHECK_LAUNCH("sw_topomap_steps_fused");
   return SW_OK;
 }
 

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -35,6 +36,9 @@ BASE_SIDE = 16
 
 # sheets up to this size step in one single-CTA persistent launch per period
 PERSISTENT_MAX_NODES = 2048
+# larger unsharded sheets: sw_topomap_steps_fused (SW_TM_FUSE=0: one
+# sw_topomap_step per step, for comparison)
+FUSED_STEPS = os.environ.get("SW_TM_FUSE", "1") != "0"
 # rewiring periods captured per CUDA graph (a divisor of the periods per
 # stimulus interval is used): one replay per 10 ms of model time keeps the
 # host loop off the critical path for small sheets
@@ -358,6 +362,7 @@ class TopomapModel:
         self._step = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.spike_counts = torch.zeros(2, dtype=torch.int64, device="cuda")
         self._barrier = torch.zeros(2, dtype=torch.int32, device="cuda")
+        self._tgt_alt = None     # second target-spike buffer of sw_topomap_steps_fused
         self.step_index = 0
         self._graphs = {}        # periods per graph -> captured CUDA graph
         self._update_log = None
@@ -443,6 +448,14 @@ class TopomapModel:
             s = self._step_struct()
             _lib.call("sw_topomap_run_steps", ctypes.byref(s), rewire_steps,
                       self.spike_counts.data_ptr(), self._barrier.data_ptr(), _lib.stream_ptr())
+        elif self.shard.world == 1 and FUSED_STEPS:
+            # 3 launches per step: STDP post of step t with the neuron phase
+            # of step t+1 (alternating target-spike buffers)
+            if self._tgt_alt is None:
+                self._tgt_alt = torch.zeros_like(self.target.spike_bits)
+            s = self._step_struct()
+            _lib.call("sw_topomap_steps_fused", ctypes.byref(s), self._tgt_alt.data_ptr(), rewire_steps,
+                      self.spike_counts.data_ptr(), _lib.stream_ptr())
         else:
             for _ in range(rewire_steps):
                 self._launch_step()

@@ -384,3 +384,24 @@ def test_incremental_transpose_patch_in_graph(dev_lib):
     sg, se = g.state_arrays(), e.state_arrays()
     for k in sg:
         assert np.array_equal(sg[k], se[k]), k
+
+
+def test_fused_period_equals_per_step_launches(dev_lib, monkeypatch):
+    """s = 4 (4096 nodes, above the single-CTA path): the fused period
+    (sw_topomap_steps_fused: STDP post of step t with the neuron phase of
+    step t+1, alternating target-spike buffers) leaves exactly the state of
+    one sw_topomap_step per step, rewiring included."""
+    import paper_2510_19764_b200.topomap as tmod
+    from paper_2510_19764_b200.neurons import unpack_spike_bits
+    res = []
+    for fused in (True, False):
+        monkeypatch.setattr(tmod, "FUSED_STEPS", fused)
+        m = tmod.TopomapModel(4, seed=5, record_events=False, use_graph=True)
+        m.run(30.0)
+        st = m.state_arrays()
+        st["tgt"] = unpack_spike_bits(m.target.spike_bits, m.geometry.n).cpu().numpy()
+        res.append(st)
+    a, b = res
+    assert a.keys() == b.keys()
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
