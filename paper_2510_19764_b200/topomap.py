@@ -459,7 +459,10 @@ class TopomapModel:
         else:
             for _ in range(rewire_steps):
                 self._launch_step()
-        self.net.run_update_group("rewiring")
+        # small sheets (single-block rewiring and remap kernels): the two
+        # projections' updates on two streams (their kernels are too small to
+        # fill the GPU; cooperative launches of larger sheets stay serial)
+        self.net.run_update_group("rewiring", concurrent=self.geometry.n <= 256 and self.shard.world == 1)
         self._log_update()
 
     def _log_update(self) -> None:

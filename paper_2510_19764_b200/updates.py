@@ -197,29 +197,55 @@ class Model:
         return (fold_key(self.seed, "host", binding.rule_id, binding.update_count, pass_index),
                 fold_key(self.seed, "row", binding.rule_id, binding.update_count, pass_index))
 
-    def run_update_group(self, group: str) -> None:
-        for b in self.groups[group]:
-            rule = b.rule
-            v0 = b.matrix.version
-            p = 0
-            while True:
-                hk, rk = self.keys(b, p)
-                self.timers.start("row_update")
-                again = rule.device_pass(self, b, p, hk, rk)
-                self.timers.stop("row_update")
-                p += 1
-                if not again:
-                    break
-                if p > 2 * b.matrix.num_pre + 16:
-                    raise RuntimeError(f"rule {rule.name!r} did not converge after {p} passes")
-            b.update_count += 1
-            tm = self.transposes.get(b.matrix_name)
-            if tm is not None and (self.always_remap or b.matrix.version != v0):
-                self.timers.start("remap")
-                src = getattr(rule, "patch_source", None)
-                if src is not None and self.incremental_remap and not self.always_remap:
-                    # incremental: only the columns the update touched (sw_transpose_patch)
-                    tm.patch(src.patch_log, src.patch_cap)
-                else:
-                    tm.rebuild(changed_flag=getattr(rule, "changed_flag", None) if not self.always_remap else None)
-                self.timers.stop("remap")
+    def run_update_group(self, group: str, concurrent: bool = False) -> None:
+        """Run every binding of the group (updates.py:323-372).  concurrent:
+        the bindings (distinct matrices, their own keys and counters) are
+        enqueued on separate streams joined at the end, so their device
+        passes and remaps overlap (timers off: the phase events would mix)."""
+        bindings = self.groups[group]
+        if not concurrent or len(bindings) < 2 or self.timers.enabled:
+            for b in bindings:
+                self._run_binding(b)
+            return
+        main = torch.cuda.current_stream()
+        sides = self._side_streams(len(bindings) - 1)
+        for st in sides:
+            st.wait_stream(main)
+        for b, st in zip(bindings, [main] + sides):
+            with torch.cuda.stream(st):
+                self._run_binding(b)
+        for st in sides:
+            main.wait_stream(st)
+
+    def _side_streams(self, n: int) -> list:
+        if not hasattr(self, "_sides"):
+            self._sides = []
+        while len(self._sides) < n:
+            self._sides.append(torch.cuda.Stream())
+        return self._sides[:n]
+
+    def _run_binding(self, b) -> None:
+        rule = b.rule
+        v0 = b.matrix.version
+        p = 0
+        while True:
+            hk, rk = self.keys(b, p)
+            self.timers.start("row_update")
+            again = rule.device_pass(self, b, p, hk, rk)
+            self.timers.stop("row_update")
+            p += 1
+            if not again:
+                break
+            if p > 2 * b.matrix.num_pre + 16:
+                raise RuntimeError(f"rule {rule.name!r} did not converge after {p} passes")
+        b.update_count += 1
+        tm = self.transposes.get(b.matrix_name)
+        if tm is not None and (self.always_remap or b.matrix.version != v0):
+            self.timers.start("remap")
+            src = getattr(rule, "patch_source", None)
+            if src is not None and self.incremental_remap and not self.always_remap:
+                # incremental: only the columns the update touched (sw_transpose_patch)
+                tm.patch(src.patch_log, src.patch_cap)
+            else:
+                tm.rebuild(changed_flag=getattr(rule, "changed_flag", None) if not self.always_remap else None)
+            self.timers.stop("remap")
