@@ -661,13 +661,16 @@ SW_API int sw_topomap_neurons(const sw_topomap_step_t* s, void* stream);
 SW_API int sw_topomap_run_steps(const sw_topomap_step_t* s, int32_t n_steps, int64_t* spike_counts,
                                 uint32_t* barrier_words, void* stream);
 SW_API int sw_topomap_synapses(const sw_topomap_step_t* s, int64_t* spike_counts, void* stream);
-/* n_steps whole steps (unsharded sheet) as 3 launches per step: step t's
- * STDP post phase and step t+1's neuron phase share one launch, the target
- * spike words alternating between s->tgt_bits and tgt_bits_alt (same size);
- * the last step's words end in s->tgt_bits.  Same results as n_steps calls
- * of sw_topomap_step. */
-SW_API int sw_topomap_steps_fused(const sw_topomap_step_t* s, uint32_t* tgt_bits_alt, int32_t n_steps,
-                                  int64_t* spike_counts, void* stream);
+/* n_steps whole steps (unsharded sheet) as 2 launches per step: the
+ * propagation of step t, then step t's STDP pre and post phases together
+ * with step t+1's neuron phase (trace increments deferred to the next
+ * propagation; synapses whose pre and post both spiked updated once, in
+ * order, by the pre phase); the spike words alternate between s->src_bits /
+ * s->tgt_bits and src_bits_alt / tgt_bits_alt (same sizes) and the last
+ * step's words end in s's buffers.  Same results as n_steps calls of
+ * sw_topomap_step. */
+SW_API int sw_topomap_steps_fused(const sw_topomap_step_t* s, uint32_t* src_bits_alt, uint32_t* tgt_bits_alt,
+                                  int32_t n_steps, int64_t* spike_counts, void* stream);
 
 #ifdef __cplusplus
 }

@@ -201,7 +201,7 @@ SIGNATURES: dict[str, list] = {
     "sw_topomap_log": [P, P, P, P, I64, P],
     "sw_topomap_neurons": [P, P],
     "sw_topomap_run_steps": [P, I32, P, P, P],
-    "sw_topomap_steps_fused": [P, P, I32, P, P],
+    "sw_topomap_steps_fused": [P, P, P, I32, P, P],
     "sw_topomap_synapses": [P, P, P],
     "sw_flip_signs": [RP, I32, U64, F64, P],
     "sw_adam_f64": [P, P, P, P, I64, F64, F64, F64, F64, F64, F64, F64, F64, P],

@@ -111,13 +111,27 @@ __device__ __forceinline__ void col_add(double& acc, const ColBatch& cb) {
     if ((cb.hit >> u) & 1u) acc = __dadd_rn(acc, cb.v[u]);
 }
 
-__device__ __forceinline__ void tm_prop(const sw_topomap_step_t& S, int t0, int dt) {
+__device__ __forceinline__ bool bit_of(const uint32_t* w, int i) { return (w[i >> 5] >> (i & 31)) & 1u; }
+
+// psrc / ptgt (fused period, else null): the previous step's spike words,
+// whose trace increments (x of spiking pres, y of spiking posts, += 1) were
+// deferred to here, applied before the decay — the same two roundings as the
+// increment in that step's STDP phases followed by this step's decay
+__device__ __forceinline__ void tm_prop(const sw_topomap_step_t& S, int t0, int dt,
+                                        const uint32_t* psrc = nullptr, const uint32_t* ptgt = nullptr) {
   for (int j = t0; j < S.n; j += dt) {
     // trace decays (x per pre, y per post; square model: n pres and n posts)
-    S.ff_x[j] = __dmul_rn(S.ff_x[j], S.decay_x);
-    S.ff_y[j] = __dmul_rn(S.ff_y[j], S.decay_y);
-    S.lat_x[j] = __dmul_rn(S.lat_x[j], S.decay_x);
-    S.lat_y[j] = __dmul_rn(S.lat_y[j], S.decay_y);
+    double fx = S.ff_x[j], fy = S.ff_y[j], lx = S.lat_x[j], ly = S.lat_y[j];
+    if (psrc && bit_of(psrc, j)) fx = __dadd_rn(fx, 1.0);
+    if (ptgt && bit_of(ptgt, j)) {
+      lx = __dadd_rn(lx, 1.0);
+      fy = __dadd_rn(fy, 1.0);
+      ly = __dadd_rn(ly, 1.0);
+    }
+    S.ff_x[j] = __dmul_rn(fx, S.decay_x);
+    S.ff_y[j] = __dmul_rn(fy, S.decay_y);
+    S.lat_x[j] = __dmul_rn(lx, S.decay_x);
+    S.lat_y[j] = __dmul_rn(ly, S.decay_y);
     if (j < S.post_lo || j >= S.post_hi) continue;
     double acc = 0.0;
     const int fa = S.ff_col_ptr[j], fe = fa + S.ff_col_len[j];
@@ -202,6 +216,80 @@ __device__ __forceinline__ void tm_post(const sw_topomap_step_t& S, int w0, int 
   }
 }
 
+// ---- STDP pre and post of one step in one launch (fused period) ----------
+// The sequential order is: pre (depress rows of spiking pres with the posts'
+// y, then x[pre] += 1), post (potentiate columns of spiking posts with the
+// pres' x, then y[post] += 1).  In one launch: the trace increments are
+// deferred to the next step's propagation phase (tm_prop psrc / ptgt), the
+// pre phase uses y as it is (= before the increment) and, for a synapse
+// whose post also spiked, applies the potentiation right after the
+// depression with x + 1 of its (spiking) pre; the post phase skips synapses
+// whose pre spiked and otherwise uses x as it is (the pre did not spike).
+// Every synapse is written by one phase, in the sequential order.
+__device__ __forceinline__ void depress_row_fused(const int32_t* rl, const int32_t* tg, double* w, int stride,
+                                                  int i, const double* y, const double* x,
+                                                  const uint32_t* post_bits, const sw_topomap_step_t& S, int lane) {
+  const int len = rl[i];
+  const int64_t off = (int64_t)i * stride;
+  const double xa = __dadd_rn(x[i], 1.0);
+  for (int s = lane; s < len; s += 32) {
+    const int j = tg[off + s];
+    double v = __dsub_rn(w[off + s], __dmul_rn(S.a_minus, y[j]));
+    v = fmin(fmax(v, S.w_min), S.w_max);
+    if (bit_of(post_bits, j)) {
+      v = __dadd_rn(v, __dmul_rn(S.a_plus, xa));
+      v = fmin(fmax(v, S.w_min), S.w_max);
+    }
+    w[off + s] = v;
+  }
+}
+
+__device__ __forceinline__ void tm_pre_fused(const sw_topomap_step_t& S, int w0, int dw) {
+  const int lane = threadIdx.x & 31;
+  const int groups = (S.n + 31) / 32;
+  for (int g = w0; g < 2 * groups; g += dw) {
+    const bool ff = g < groups;
+    const int grp = ff ? g : g - groups;
+    unsigned m = ff ? S.src_bits[grp] : S.tgt_bits[grp];
+    while (m) {
+      const int i = grp * 32 + __ffs(m) - 1;
+      m &= m - 1;
+      if (ff) depress_row_fused(S.ff_row_length, S.ff_target, S.ff_g, S.ff_stride, i, S.ff_y, S.ff_x, S.tgt_bits, S, lane);
+      else depress_row_fused(S.lat_row_length, S.lat_target, S.lat_g, S.lat_stride, i, S.lat_y, S.lat_x, S.tgt_bits, S, lane);
+    }
+  }
+}
+
+__device__ __forceinline__ void potentiate_col_fused(int a, int e, const int32_t* src_pre, const int32_t* src_slot,
+                                                     double* g, int stride, const double* x,
+                                                     const uint32_t* pre_bits, const sw_topomap_step_t& S,
+                                                     int lane) {
+  for (int q = a + lane; q < e; q += 32) {
+    const int i = src_pre[q];
+    if (bit_of(pre_bits, i)) continue;   // done by the pre phase
+    const int64_t o = (int64_t)i * stride + src_slot[q];
+    double v = __dadd_rn(g[o], __dmul_rn(S.a_plus, x[i]));
+    v = fmax(v, S.w_min);
+    g[o] = fmin(v, S.w_max);
+  }
+}
+
+__device__ __forceinline__ void tm_post_fused(const sw_topomap_step_t& S, int w0, int dw) {
+  const int lane = threadIdx.x & 31;
+  const int words = (S.n + 31) / 32;
+  for (int gw = w0; gw < words; gw += dw) {
+    unsigned m = S.tgt_bits[gw];
+    while (m) {
+      const int j = gw * 32 + __ffs(m) - 1;
+      m &= m - 1;
+      potentiate_col_fused(S.ff_col_ptr[j], S.ff_col_ptr[j] + S.ff_col_len[j], S.ff_src_pre, S.ff_src_slot, S.ff_g,
+                           S.ff_stride, S.ff_x, S.src_bits, S, lane);
+      potentiate_col_fused(S.lat_col_ptr[j], S.lat_col_ptr[j] + S.lat_col_len[j], S.lat_src_pre, S.lat_src_slot,
+                           S.lat_g, S.lat_stride, S.lat_x, S.tgt_bits, S, lane);
+    }
+  }
+}
+
 // per-step spike counts of words [w0, words) step dw, added to cnt[2]
 __device__ __forceinline__ void tm_count(const sw_topomap_step_t& S, int w0, int dw, int64_t* cnt) {
   const int words = (S.n + 31) / 32;
@@ -251,34 +339,49 @@ __global__ void k_tm_post(sw_topomap_step_t S) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *S.step += 1;
 }
 
-// ---- fused period (unsharded sheets): step t's STDP post phase and step
-// t+1's neuron phase in one launch.  They share no data once the target
-// spike words alternate between two buffers (post(t) reads step t's words,
-// neurons(t+1) writes step t+1's) and the step counter is advanced by the
-// propagation phase instead of the post phase: 3 launches per step instead
-// of 4, and the two latency-bound phases overlap.
-__global__ void k_tm_prop_inc(sw_topomap_step_t S, int64_t* spike_counts) {
+// ---- fused period (unsharded sheets): 2 launches per step ----------------
+// (1) propagation of step t, with the previous step's deferred trace
+//     increments and the step counter advanced for the next neuron phase;
+// (2) STDP pre and post of step t (tm_pre_fused / tm_post_fused) together
+//     with the neuron phase of step t+1 — disjoint data once the spike words
+//     alternate between two buffer pairs.
+__global__ void k_tm_prop_fused(sw_topomap_step_t S, const uint32_t* psrc, const uint32_t* ptgt,
+                                int64_t* spike_counts) {
   pdl_enter();
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, gn = gridDim.x * blockDim.x;
-  tm_prop(S, gt, gn);
+  tm_prop(S, gt, gn, psrc, ptgt);
   if (spike_counts) tm_count(S, gt, gn, spike_counts);
   if (blockIdx.x == 0 && threadIdx.x == 0) *S.step += 1;   // read by the next neuron phase only
 }
 
-__global__ void k_tm_post_neurons(sw_topomap_step_t Sp, sw_topomap_step_t Sn, int post_blocks) {
+__global__ void k_tm_stdp_neurons(sw_topomap_step_t S, sw_topomap_step_t Sn, int pre_blocks, int post_blocks,
+                                  int with_neurons) {
   pdl_enter();
-  if ((int)blockIdx.x < post_blocks) {
-    tm_post(Sp, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), post_blocks * (blockDim.x >> 5));
-  } else {
-    const int b = blockIdx.x - post_blocks;
-    tm_neurons(Sn, *Sn.step, b * blockDim.x + threadIdx.x, (gridDim.x - post_blocks) * blockDim.x);
+  const int wpb = blockDim.x >> 5, warp = threadIdx.x >> 5;
+  if ((int)blockIdx.x < pre_blocks) {
+    tm_pre_fused(S, blockIdx.x * wpb + warp, pre_blocks * wpb);
+  } else if ((int)blockIdx.x < pre_blocks + post_blocks) {
+    tm_post_fused(S, (blockIdx.x - pre_blocks) * wpb + warp, post_blocks * wpb);
+  } else if (with_neurons) {
+    const int b = blockIdx.x - pre_blocks - post_blocks;
+    const int nb = gridDim.x - pre_blocks - post_blocks;
+    tm_neurons(Sn, *Sn.step, b * blockDim.x + threadIdx.x, nb * blockDim.x);
   }
 }
 
-__global__ void k_tm_post_only(sw_topomap_step_t S) {
+// the period's last deferred trace increments (no decay)
+__global__ void k_tm_trace_flush(sw_topomap_step_t S) {
   pdl_enter();
-  tm_post(S, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gridDim.x * (blockDim.x >> 5));
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < S.n; j += gridDim.x * blockDim.x) {
+    if (bit_of(S.src_bits, j)) S.ff_x[j] = __dadd_rn(S.ff_x[j], 1.0);
+    if (bit_of(S.tgt_bits, j)) {
+      S.lat_x[j] = __dadd_rn(S.lat_x[j], 1.0);
+      S.ff_y[j] = __dadd_rn(S.ff_y[j], 1.0);
+      S.lat_y[j] = __dadd_rn(S.lat_y[j], 1.0);
+    }
+  }
 }
+
 
 // ---- persistent multi-step kernel ------------------------------------------------------
 // n_steps whole steps in one launch: the phases of a step are separated by
@@ -501,39 +604,43 @@ extern "C" int sw_topomap_run_steps(const sw_topomap_step_t* s, int32_t n_steps,
   return SW_OK;
 }
 
-extern "C" int sw_topomap_steps_fused(const sw_topomap_step_t* s, uint32_t* tgt_bits_alt, int32_t n_steps,
-                                      int64_t* spike_counts, void* stream) {
+extern "C" int sw_topomap_steps_fused(const sw_topomap_step_t* s, uint32_t* src_bits_alt, uint32_t* tgt_bits_alt,
+                                      int32_t n_steps, int64_t* spike_counts, void* stream) {
   if (int e = check_step(s)) return e;
-  if (s->post_lo != 0 || s->post_hi != s->n || !tgt_bits_alt) {
-    sw::set_last_error("sw_topomap_steps_fused: unsharded sheets and a second target-spike buffer");
+  if (s->post_lo != 0 || s->post_hi != s->n || !src_bits_alt || !tgt_bits_alt) {
+    sw::set_last_error("sw_topomap_steps_fused: unsharded sheets and second spike-word buffers");
     return SW_ERR_INVALID_ARG;
   }
   const int n = s->n;
   if (n <= 0 || n_steps <= 0) return SW_OK;
   cudaStream_t st = (cudaStream_t)stream;
   sw_topomap_step_t S[2] = {*s, *s};
+  S[1].src_bits = src_bits_alt;
   S[1].tgt_bits = tgt_bits_alt;
   const int groups = (n + 31) / 32;
-  int blocks = (2 * groups + 7) / 8;
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  int pblocks = (groups + 7) / 8;
-  if (pblocks > 148 * 8) pblocks = 148 * 8;
+  int pre_blocks = (2 * groups + 7) / 8;
+  if (pre_blocks > 148 * 8) pre_blocks = 148 * 8;
+  int post_blocks = (groups + 7) / 8;
+  if (post_blocks > 148 * 8) post_blocks = 148 * 8;
   const int nblocks = grid1(n);
   launch_pdl(n, k_tm_neurons, nblocks, 256, st, S[0]); sw::count_launch();
   for (int t = 0; t < n_steps; ++t) {
     const sw_topomap_step_t& Sc = S[t & 1];
-    launch_pdl(n, k_tm_prop_inc, nblocks, 256, st, Sc, spike_counts); sw::count_launch();
-    launch_pdl(n, k_tm_pre, blocks, 256, st, Sc); sw::count_launch();
-    if (t + 1 < n_steps) {
-      launch_pdl(n, k_tm_post_neurons, pblocks + nblocks, 256, st, Sc, S[(t + 1) & 1], pblocks);
-    } else {
-      launch_pdl(n, k_tm_post_only, pblocks, 256, st, Sc);
-    }
+    const uint32_t* psrc = t > 0 ? S[(t - 1) & 1].src_bits : nullptr;
+    const uint32_t* ptgt = t > 0 ? S[(t - 1) & 1].tgt_bits : nullptr;
+    launch_pdl(n, k_tm_prop_fused, nblocks, 256, st, Sc, psrc, ptgt, spike_counts); sw::count_launch();
+    const int with_neurons = t + 1 < n_steps ? 1 : 0;
+    launch_pdl(n, k_tm_stdp_neurons, pre_blocks + post_blocks + (with_neurons ? nblocks : 0), 256, st, Sc,
+               S[(t + 1) & 1], pre_blocks, post_blocks, with_neurons);
     sw::count_launch();
   }
-  // the last step's target spikes back into the model's buffer
-  if ((n_steps - 1) & 1)
+  const sw_topomap_step_t& Sl = S[(n_steps - 1) & 1];
+  launch_pdl(n, k_tm_trace_flush, nblocks, 256, st, Sl); sw::count_launch();
+  // the last step's spike words back into the model's buffers
+  if ((n_steps - 1) & 1) {
+    cudaMemcpyAsync(s->src_bits, src_bits_alt, (size_t)groups * 4, cudaMemcpyDeviceToDevice, st);
     cudaMemcpyAsync(s->tgt_bits, tgt_bits_alt, (size_t)groups * 4, cudaMemcpyDeviceToDevice, st);
+  }
   SW_CHECK_LAUNCH("sw_topomap_steps_fused");
   return SW_OK;
 }

@@ -362,7 +362,7 @@ class TopomapModel:
         self._step = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.spike_counts = torch.zeros(2, dtype=torch.int64, device="cuda")
         self._barrier = torch.zeros(2, dtype=torch.int32, device="cuda")
-        self._tgt_alt = None     # second target-spike buffer of sw_topomap_steps_fused
+        self._src_alt = self._tgt_alt = None     # second spike buffers of sw_topomap_steps_fused
         self.step_index = 0
         self._graphs = {}        # periods per graph -> captured CUDA graph
         self._update_log = None
@@ -449,13 +449,14 @@ class TopomapModel:
             _lib.call("sw_topomap_run_steps", ctypes.byref(s), rewire_steps,
                       self.spike_counts.data_ptr(), self._barrier.data_ptr(), _lib.stream_ptr())
         elif self.shard.world == 1 and FUSED_STEPS:
-            # 3 launches per step: STDP post of step t with the neuron phase
-            # of step t+1 (alternating target-spike buffers)
+            # 2 launches per step: propagation, then the STDP phases of step
+            # t with the neuron phase of step t+1 (alternating spike buffers)
             if self._tgt_alt is None:
+                self._src_alt = torch.zeros_like(self.source.spike_bits)
                 self._tgt_alt = torch.zeros_like(self.target.spike_bits)
             s = self._step_struct()
-            _lib.call("sw_topomap_steps_fused", ctypes.byref(s), self._tgt_alt.data_ptr(), rewire_steps,
-                      self.spike_counts.data_ptr(), _lib.stream_ptr())
+            _lib.call("sw_topomap_steps_fused", ctypes.byref(s), self._src_alt.data_ptr(), self._tgt_alt.data_ptr(),
+                      rewire_steps, self.spike_counts.data_ptr(), _lib.stream_ptr())
         else:
             for _ in range(rewire_steps):
                 self._launch_step()
