@@ -446,7 +446,7 @@ k_tm_run(sw_topomap_step_t S, int n_steps, int64_t* spike_counts, unsigned* bar)
 struct TmSmem {
   static size_t bytes(int n) {
     const int words = (n + 31) / 32;
-    return (size_t)n * 8 * 9 + (size_t)(n + 1) * 4 * 2 + (size_t)n * 4 * 4 + (size_t)words * 4 * 2 + 64;
+    return (size_t)n * 8 * 9 + (size_t)(n + 1) * 4 * 2 + (size_t)n * 4 * 4 + (size_t)words * 4 * 4 + 64;
   }
 };
 
@@ -461,7 +461,9 @@ k_tm_run_staged(sw_topomap_step_t G, int n_steps, int64_t* spike_counts) {
   int32_t* ip = reinterpret_cast<int32_t*>(d + 9 * n);
   int32_t *fcp = ip, *lcp = ip + (n + 1), *frl = ip + 2 * (n + 1), *lrl = frl + n;
   int32_t *fcl = lrl + n, *lcl = fcl + n;
-  uint32_t *sb = reinterpret_cast<uint32_t*>(lcl + n), *tb = sb + words;
+  // two spike-word buffer pairs: step t's words stay readable while step
+  // t+1's neuron phase writes the other pair
+  uint32_t *sb = reinterpret_cast<uint32_t*>(lcl + n), *tb = sb + words, *sb1 = tb + words, *tb1 = sb1 + words;
   for (int x = threadIdx.x; x < n; x += blockDim.x) {
     V[x] = G.V[x]; gt[x] = G.g_tot[x]; pend[x] = G.pending[x];
     fx[x] = G.ff_x[x]; fy[x] = G.ff_y[x]; lx[x] = G.lat_x[x]; ly[x] = G.lat_y[x];
@@ -479,18 +481,43 @@ k_tm_run_staged(sw_topomap_step_t G, int n_steps, int64_t* spike_counts) {
   S.p_src = ps; S.ref_until = ref; S.ff_row_length = frl; S.lat_row_length = lrl;
   S.ff_col_ptr = fcp; S.lat_col_ptr = lcp; S.ff_col_len = fcl; S.lat_col_len = lcl;
   S.src_bits = sb; S.tgt_bits = tb;
+  sw_topomap_step_t S1 = S;
+  S1.src_bits = sb1; S1.tgt_bits = tb1;
   __syncthreads();
   const int t = threadIdx.x, nt = blockDim.x;
   const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // two phases per step (the fused-period order of sw_topomap_steps_fused):
+  // propagation with the previous step's deferred trace increments, then
+  // STDP pre + post of this step and the neuron phase of the next
+  tm_neurons(S, k0, w * 32, nw * 32);
+  __syncthreads();
   for (int st = 0; st < n_steps; ++st) {
-    tm_neurons(S, k0 + st, w * 32, nw * 32);
+    const sw_topomap_step_t& Sc = (st & 1) ? S1 : S;
+    const sw_topomap_step_t& Sp = (st & 1) ? S : S1;
+    tm_prop(Sc, t, nt, st > 0 ? Sp.src_bits : nullptr, st > 0 ? Sp.tgt_bits : nullptr);
+    if (spike_counts) tm_count(Sc, t, nt, spike_counts);
     __syncthreads();
-    tm_prop(S, t, nt);
-    if (spike_counts) tm_count(S, t, nt, spike_counts);
+    tm_pre_fused(Sc, w, nw);
+    tm_post_fused(Sc, w, nw);
+    if (st + 1 < n_steps) tm_neurons(Sp, k0 + st + 1, w * 32, nw * 32);
     __syncthreads();
-    tm_pre(S, w, nw);
-    __syncthreads();
-    tm_post(S, w, nw);
+  }
+  {
+    // the last step's deferred trace increments, its words in the first pair
+    const sw_topomap_step_t& Sl = ((n_steps - 1) & 1) ? S1 : S;
+    for (int j = t; j < n; j += nt) {
+      if (bit_of(Sl.src_bits, j)) fx[j] = __dadd_rn(fx[j], 1.0);
+      if (bit_of(Sl.tgt_bits, j)) {
+        lx[j] = __dadd_rn(lx[j], 1.0);
+        fy[j] = __dadd_rn(fy[j], 1.0);
+        ly[j] = __dadd_rn(ly[j], 1.0);
+      }
+    }
+    if ((n_steps - 1) & 1)
+      for (int x = t; x < words; x += nt) {
+        sb[x] = sb1[x];
+        tb[x] = tb1[x];
+      }
     __syncthreads();
   }
   for (int x = threadIdx.x; x < n; x += blockDim.x) {

@@ -35,7 +35,7 @@ BASE_SIDE = 16
 
 
 # sheets up to this size step in one single-CTA persistent launch per period
-PERSISTENT_MAX_NODES = 2048
+PERSISTENT_MAX_NODES = 512   # single-CTA periods up to here; s = 2 (1024 nodes): 2-launch steps 12.2 vs 13.0 us
 # larger unsharded sheets: sw_topomap_steps_fused (SW_TM_FUSE=0: one
 # sw_topomap_step per step, for comparison)
 FUSED_STEPS = os.environ.get("SW_TM_FUSE", "1") != "0"
