@@ -545,8 +545,8 @@ int grid1(int64_t n) {
 // plainly (measurement)
 template <typename... KArgs, typename... Args>
 void launch_pdl(int n, void (*kern)(KArgs...), int grid, int block, cudaStream_t st, Args... args) {
-  static const bool env_on = [] { const char* e = getenv("SW_TM_PDL"); return !(e && e[0] == '0'); }();
-  sw::pdl_launch(env_on && n <= 16384, kern, dim3(grid), dim3(block), 0, st, args...);
+  static const int mode = [] { const char* e = getenv("SW_TM_PDL"); return e ? atoi(e) : 1; }();   // 0 off, 2 all sizes
+  sw::pdl_launch(mode == 2 || (mode == 1 && n <= 16384), kern, dim3(grid), dim3(block), 0, st, args...);
 }
 
 }  // namespace
