@@ -340,6 +340,51 @@ def test_forward_currents_are_grouped_ordered_sums(dev_lib, NI, H, din, drec, p_
             assert v[b, h] == vv, (b, h)
 
 
+@pytest.mark.parametrize("NI,H,din,drec,p_spk,z_spk", [
+    (333, 200, 0.3, 0.25, 0.5, 0.3),     # 8 groups, ragged input words
+    (300, 200, 0.3, 0.25, 1.0, 1.0),     # every row spikes: the group lists full
+    (700, 512, 0.1, 0.05, 0.5, 0.3),     # 4 groups, 2 hidden units per thread
+    (300, 1024, 0.05, 0.02, 1.0, 1.0),   # 4 groups, 4 hidden units per thread, all rows
+])
+def test_grouped_forward_currents_forced_spikes(dev_lib, NI, H, din, drec, p_spk, z_spk):
+    """The trainer's grouped forward (k_clf_fwd2: input spikes from
+    sw_clf_inputs' words, hidden rows from the previous step's z) computes
+    each current as the grouped ordered sum of oracle_helpers.grouped_currents.
+    Spikes are forced (p_in in {0, 1}, chosen z; v = a = 0), so after the
+    first step v = f32(alpha * (0 - z*v_thr)) + rec + ext exactly."""
+    from oracle_helpers import grouped_currents
+    import ctypes
+    from paper_2510_19764_b200 import _lib
+    from paper_2510_19764_b200.classifier import EpropClassifierTrainer, SyntheticTask
+    task = SyntheticTask(num_classes=5, num_inputs=NI, example_steps=10, seed=11)
+    tr = EpropClassifierTrainer(task, hidden=H, batch_size=6, seed=11, deep_r=False,
+                                input_density=din, recurrent_density=drec, use_graph=False)
+    ids = task.train_ids(0, tr.batch_size)
+    tr._upload_batch(ids)
+    rs = np.random.default_rng(11)
+    B = tr.batch_size
+    pin = (rs.random((B, NI)) < p_spk).astype(np.float64)
+    z = (rs.random((B, H)) < z_spk).astype(np.float32)
+    tr.p_in.copy_(torch.from_numpy(pin).to(tr.p_in.dtype).reshape(tr.p_in.shape))
+    tr._prepare(False)
+    tr.z.copy_(torch.from_numpy(z))
+    prm = tr._group_params(0, 1)
+    _lib.call("sw_clf_step", ctypes.byref(prm), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    v = tr.v.cpu().numpy()
+    f32 = np.float32
+    alpha, vthr = f32(tr.params.alpha), f32(tr.params.v_thr)
+    w_in, w_rec = tr.w32_in.cpu().numpy(), tr.w32_rec.cpu().numpy()
+    mi, mr = tr.m_in, tr.m_rec
+    ext_all = grouped_currents(mi.row_length.cpu().numpy(), mi.target.cpu().numpy(), w_in, pin == 1.0, H)
+    rec_all = grouped_currents(mr.row_length.cpu().numpy(), mr.target.cpu().numpy(), w_rec, z != 0, H)
+    for b in range(B):
+        vv = (alpha * (f32(0) - z[b] * vthr)).astype(f32)
+        vv = ((vv + rec_all[b]).astype(f32) + ext_all[b]).astype(f32)
+        bad = np.flatnonzero(v[b] != vv)
+        assert bad.size == 0, (b, bad[:8], v[b, bad[:4]], vv[bad[:4]])
+
+
 def test_pinned_host_inputs_equal_numpy_inputs(dev_lib):
     """train_batch from host inputs already in pinned memory (direct async
     copies) == from numpy arrays (staged through the trainer's pinned buffers)."""
