@@ -109,6 +109,11 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
   // issued before any shared-memory store), W_out, d, and (deferred
   // reduction) the readout partials this block adds to
   constexpr int kPer = kBT * kHT / 256;
+  // with the class count known, W_out's tile columns and the replicas' d
+  // rows join the same round (registers, stored after the tiles)
+  constexpr int kWPer = CT > 0 ? (CT * kHT + 255) / 256 : 1;
+  constexpr int kDPer = CT > 0 ? (kBT * CT + 255) / 256 : 1;
+  double wv[kWPer], dv[kDPer];
   {
     float pv[kPer], zv[kPer];
 #pragma unroll
@@ -118,6 +123,20 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
       const int64_t g = (int64_t)(b0 + b) * H + h0 + r;
       pv[u] = ok ? P.psi[k][g] : 0.f;
       zv[u] = ok ? P.zbar[k][g] : 0.f;
+    }
+    if constexpr (CT > 0) {
+      if (want_lsig || ro) {
+#pragma unroll
+        for (int u = 0; u < kWPer; ++u) {
+          const int x = tid + u * 256, c = x / kHT, r = x % kHT;
+          wv[u] = (x < CT * kHT && r < nh) ? P.w_out[(int64_t)c * H + h0 + r] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kDPer; ++u) {
+          const int x = tid + u * 256, b = x / CT, c = x - b * CT;
+          dv[u] = (x < kBT * CT && b0 + b < B) ? P.d[k][(int64_t)(b0 + b) * CT + c] : 0.0;
+        }
+      }
     }
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
@@ -138,7 +157,20 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
       for (int u = 0; u < CP; ++u) prev[u] = part[(int64_t)(cg * CP + u) * H + h0 + rr];
     }
   }
-  if (want_lsig || ro) {
+  if constexpr (CT > 0) {
+    if (want_lsig || ro) {
+#pragma unroll
+      for (int u = 0; u < kWPer; ++u) {
+        const int x = tid + u * 256;
+        if (x < CT * kHT) ws[x] = wv[u];
+      }
+#pragma unroll
+      for (int u = 0; u < kDPer; ++u) {
+        const int x = tid + u * 256, b = x / CT, c = x - b * CT;
+        if (x < kBT * CT) dt[c * kDT + b] = dv[u];
+      }
+    }
+  } else if (want_lsig || ro) {
     for (int x = tid; x < C * kHT; x += 256) {
       const int c = x / kHT, r = x % kHT;
       ws[x] = r < nh ? P.w_out[(int64_t)c * H + h0 + r] : 0.0;
@@ -171,11 +203,17 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
       double dr[CT];
 #pragma unroll
       for (int c = 0; c < CT; ++c) dr[c] = dt[c * kDT + lane];
-      for (int r = warp; r < nh; r += 8) {
-        double ls = 0.0;
+      // rows r0, r0 + 8, r0 + 16, r0 + 24: four independent class chains
+      // interleaved (W_out's columns past nh are zero in shared memory)
+      for (int r0 = warp; r0 < nh; r0 += 32) {
+        double ls[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int c = 0; c < CT; ++c) ls = __fma_rn(dr[c], ws[c * kHT + r], ls);
-        if (b0 + lane < L) *lsig_at(r) = b0 + lane < B ? __double2float_rn(ls) : 0.f;
+        for (int c = 0; c < CT; ++c)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) ls[q] = __fma_rn(dr[c], ws[c * kHT + r0 + 8 * q], ls[q]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (r0 + 8 * q < nh && b0 + lane < L) *lsig_at(r0 + 8 * q) = b0 + lane < B ? __double2float_rn(ls[q]) : 0.f;
       }
     } else {
       for (int r = warp; r < nh; r += 8) {
