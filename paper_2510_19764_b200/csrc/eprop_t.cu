@@ -56,9 +56,10 @@ __host__ __device__ __forceinline__ int64_t psl_index(int64_t row, int64_t L, in
   return (row * L + (b & ~3)) * 2 + (b & 3);
 }
 constexpr int kMaxC = 32;
-// d of the replica tile, class-major with one pad double per class row: the
-// class-fastest stores of the coalesced d read then hit distinct banks
-constexpr int kDT = kBT + 1;
+// d of the replica tile, class-major with two pad doubles per class row: the
+// class-fastest stores of the coalesced d read spread over the banks, and a
+// class's replicas b, b+1 (b even) are one 16-byte load
+constexpr int kDT = kBT + 2;
 
 __host__ __device__ inline size_t prep_smem_bytes(int C) {
   return (size_t)2 * kBT * (kHT + 1) * 4 + (size_t)C * kHT * 8 + (size_t)kDT * C * 8;
@@ -203,17 +204,26 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
       double dr[CT];
 #pragma unroll
       for (int c = 0; c < CT; ++c) dr[c] = dt[c * kDT + lane];
-      // rows r0, r0 + 8, r0 + 16, r0 + 24: four independent class chains
-      // interleaved (W_out's columns past nh are zero in shared memory)
-      for (int r0 = warp; r0 < nh; r0 += 32) {
+      // warp w: rows 8w .. 8w+7, four consecutive rows at a time (their
+      // W_out values one 32-byte shared load per class), four independent
+      // class chains interleaved (W_out's columns past nh are zero)
+#pragma unroll 1
+      for (int i = 0; i < 2; ++i) {
+        const int r0 = warp * 8 + i * 4;
+        if (r0 >= nh) break;
         double ls[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int c = 0; c < CT; ++c)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) ls[q] = __fma_rn(dr[c], ws[c * kHT + r0 + 8 * q], ls[q]);
+        for (int c = 0; c < CT; ++c) {
+          const double2* w2 = reinterpret_cast<const double2*>(ws + c * kHT + r0);
+          const double2 wa = w2[0], wb = w2[1];
+          ls[0] = __fma_rn(dr[c], wa.x, ls[0]);
+          ls[1] = __fma_rn(dr[c], wa.y, ls[1]);
+          ls[2] = __fma_rn(dr[c], wb.x, ls[2]);
+          ls[3] = __fma_rn(dr[c], wb.y, ls[3]);
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (r0 + 8 * q < nh && b0 + lane < L) *lsig_at(r0 + 8 * q) = b0 + lane < B ? __double2float_rn(ls[q]) : 0.f;
+          if (r0 + q < nh && b0 + lane < L) *lsig_at(r0 + q) = b0 + lane < B ? __double2float_rn(ls[q]) : 0.f;
       }
     } else {
       for (int r = warp; r < nh; r += 8) {
@@ -233,10 +243,13 @@ __global__ void __launch_bounds__(256, MB) k_prep(const sw_eprop_prep_t P) {
 #pragma unroll
         for (int u = 0; u < CP; ++u) acc[u] = 0.0;
         const double* dg = dt + cg * CP * kDT;
-        for (int b = 0; b < kBT; ++b) {
-          const double z = (double)tile[b][r];
+        for (int b = 0; b < kBT; b += 2) {
+          const double z0 = (double)tile[b][r], z1 = (double)tile[b + 1][r];
 #pragma unroll
-          for (int u = 0; u < CP; ++u) acc[u] = __fma_rn(dg[u * kDT + b], z, acc[u]);
+          for (int u = 0; u < CP; ++u) {
+            const double2 dd = *reinterpret_cast<const double2*>(dg + u * kDT + b);
+            acc[u] = __fma_rn(dd.y, z1, __fma_rn(dd.x, z0, acc[u]));
+          }
         }
 #pragma unroll
         for (int u = 0; u < CP; ++u) {
