@@ -453,15 +453,21 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
 // The readout of a grouped launch's steps (classifier.py:215-219,
 // plasticity.py:156-165), block per replica, from the hidden spike words the
 // forward launch wrote:
-//   1  per step, the ascending list of spiking units (warp per step);
-//   2  thread per (step, class): s = sum of w_out[c][h] over the list in
-//      order (f64, from +0.0, 8 loads in flight) -- the steps are
-//      independent here, so their load latencies overlap;
+//   1  per step (warp per step), the hidden spike words and the ascending
+//      list of spiking units, the list capped at kRoList entries;
+//   2  thread per (step, class): s = sum of w_out[c][h] over the step's
+//      spiking units in ascending order -- from the list, or for steps with
+//      more spikes straight from the words -- (f64, from +0.0, 8 loads in
+//      flight); the steps are independent here, so their load latencies
+//      overlap; the block's shared memory stays small (no H-sized lists), so
+//      more replica blocks per SM and W_out's rows stay in L1;
 //   3  warp 0: y = alpha*y + s + b per class, steps in order;
 //   4  warp per step: softmax, d = pi - onehot (written to the step's slot);
 //   5  warp 0: pi_sum and the loss accumulated in step order.
+constexpr int kRoList = 64;
 __host__ __device__ inline size_t readout_smem(int n_steps, int H, int C) {
-  return (size_t)n_steps * H * 4 + (size_t)n_steps * 4 + (size_t)n_steps * C * 8 * 3 + (size_t)C * 8;
+  return (size_t)n_steps * ((H + 31) / 32) * 4 + (size_t)n_steps * (4 + kRoList * 2) + (size_t)n_steps * C * 8 * 3 +
+         (size_t)C * 8;
 }
 
 __global__ void __launch_bounds__(256) k_clf_readout(const sw_clf_step_t P) {
@@ -473,8 +479,9 @@ __global__ void __launch_bounds__(256) k_clf_readout(const sw_clf_step_t P) {
   double* s_y = s_sum + (size_t)n * C;                      // [n][C]
   double* s_pi = s_y + (size_t)n * C;                       // [n][C]
   double* s_bo = s_pi + (size_t)n * C;                      // [C]
-  int* s_cnt = reinterpret_cast<int*>(s_bo + C);            // [n]
-  int* s_list = s_cnt + n;                                  // [n][H]
+  uint32_t* s_zw = reinterpret_cast<uint32_t*>(s_bo + C);  // [n][HW]
+  int* s_cnt = reinterpret_cast<int*>(s_zw + (size_t)n * HW);   // [n]
+  uint16_t* s_list = reinterpret_cast<uint16_t*>(s_cnt + n);      // [n][kRoList]
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int kW = 8;
   const int bC = b * C;
@@ -483,10 +490,11 @@ __global__ void __launch_bounds__(256) k_clf_readout(const sw_clf_step_t P) {
   // 1
   for (int t = warp; t < n; t += kW) {
     const uint32_t* zw = P.z_bits + ((int64_t)t * B + b) * HW;
-    int* L = s_list + (size_t)t * H;
+    uint16_t* L = s_list + (size_t)t * kRoList;
     int cnt = 0;
     for (int w0 = 0; w0 < HW; w0 += 32) {
       const uint32_t wd = w0 + lane < HW ? zw[w0 + lane] : 0u;
+      if (w0 + lane < HW) s_zw[(size_t)t * HW + w0 + lane] = wd;
       const int c = __popc(wd);
       int inc = c;
 #pragma unroll
@@ -495,7 +503,7 @@ __global__ void __launch_bounds__(256) k_clf_readout(const sw_clf_step_t P) {
         if (lane >= d) inc += u;
       }
       int p = cnt + inc - c;
-      for (uint32_t m = wd; m; m &= m - 1) L[p++] = (w0 + lane) * 32 + __ffs(m) - 1;
+      for (uint32_t m = wd; m && p < kRoList; m &= m - 1) L[p++] = (uint16_t)((w0 + lane) * 32 + __ffs(m) - 1);
       cnt += __shfl_sync(SW_FULL_MASK, inc, 31);
     }
     if (lane == 0) s_cnt[t] = cnt;
@@ -504,17 +512,41 @@ __global__ void __launch_bounds__(256) k_clf_readout(const sw_clf_step_t P) {
   // 2
   for (int i = tid; i < n * C; i += blockDim.x) {
     const int t = i / C, c = i - t * C;
-    const int* L = s_list + (size_t)t * H;
-    const int cnt = s_cnt[t];
     const double* wr = P.w_out + (int64_t)c * H;
     double sacc = 0.0;
-    for (int q0 = 0; q0 < cnt; q0 += 8) {
+    const int cnt = s_cnt[t];
+    if (cnt <= kRoList) {
+      const uint16_t* L = s_list + (size_t)t * kRoList;
+      for (int q0 = 0; q0 < cnt; q0 += 8) {
+        double wv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) wv[u] = q0 + u < cnt ? __ldg(wr + L[q0 + u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (q0 + u < cnt) sacc = __dadd_rn(sacc, wv[u]);
+      }
+      s_sum[i] = sacc;
+      continue;
+    }
+    const uint32_t* zw = s_zw + (size_t)t * HW;
+    int w = 0;
+    uint32_t m = zw[0];
+    for (;;) {
+      // the next 8 spiking units (ascending; -1 past the last)
+      int idx[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        while (m == 0u && w + 1 < HW) m = zw[++w];
+        idx[u] = m ? w * 32 + __ffs(m) - 1 : -1;
+        m &= m - 1;
+      }
       double wv[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) wv[u] = q0 + u < cnt ? __ldg(wr + L[q0 + u]) : 0.0;
+      for (int u = 0; u < 8; ++u) wv[u] = idx[u] >= 0 ? __ldg(wr + idx[u]) : 0.0;
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (q0 + u < cnt) sacc = __dadd_rn(sacc, wv[u]);
+        if (idx[u] >= 0) sacc = __dadd_rn(sacc, wv[u]);
+      if (idx[7] < 0) break;
     }
     s_sum[i] = sacc;
   }

@@ -385,6 +385,48 @@ def test_grouped_forward_currents_forced_spikes(dev_lib, NI, H, din, drec, p_spk
         assert bad.size == 0, (b, bad[:8], v[b, bad[:4]], vv[bad[:4]])
 
 
+@pytest.mark.parametrize("H,v0", [(200, 0.0), (200, 50.0), (1024, 50.0)])
+def test_grouped_readout_sums_from_spike_words(dev_lib, H, v0):
+    """The readout launch after the grouped forward: per step and class the
+    f64 sum of w_out[c][h] over the step's spiking units (the spike words the
+    forward wrote) in ascending order from +0.0, then y = (alpha*y + s) + b,
+    steps in order -- bit-exact against numpy.  v0 > threshold drives every
+    hidden unit to spike, so steps with more spiking units than the readout's
+    list capacity take the word-walk path."""
+    import ctypes
+    from paper_2510_19764_b200 import _lib
+    from paper_2510_19764_b200.classifier import EPROP_BLOCK_STEPS as K
+    from paper_2510_19764_b200.classifier import EpropClassifierTrainer, SyntheticTask
+    task = SyntheticTask(num_classes=7, num_inputs=150, example_steps=2 * K, seed=3)
+    tr = EpropClassifierTrainer(task, hidden=H, batch_size=5, seed=3, deep_r=False,
+                                input_density=0.2, recurrent_density=0.1, use_graph=False)
+    tr._upload_batch(task.train_ids(0, tr.batch_size))
+    tr._prepare(False)
+    tr.v.fill_(v0)
+    y = tr.y.cpu().numpy().copy()
+    w_out, b_out = tr.w_out.cpu().numpy(), tr.b_out.cpu().numpy()
+    alpha = float(tr.params.alpha)
+    B, C, HW = tr.batch_size, task.num_classes, (H + 31) // 32
+    dense = 0
+    for t0 in (0, K):
+        _lib.call("sw_clf_step", ctypes.byref(tr._group_params(t0, K)), _lib.stream_ptr())
+        torch.cuda.synchronize()
+        words = tr.z_bits.cpu().numpy().view(np.uint32)
+        for s in range(K):
+            for b in range(B):
+                bits = np.unpackbits(words[s, b].view(np.uint8), bitorder="little")[:H]
+                units = np.flatnonzero(bits)
+                dense += units.size > 64
+                for c in range(C):
+                    acc = 0.0
+                    for h in units:
+                        acc = acc + float(w_out[c, h])
+                    y[b, c] = (alpha * y[b, c] + acc) + float(b_out[c])
+    assert np.array_equal(tr.y.cpu().numpy(), y)
+    if v0 > 0:
+        assert dense > 0
+
+
 def test_pinned_host_inputs_equal_numpy_inputs(dev_lib):
     """train_batch from host inputs already in pinned memory (direct async
     copies) == from numpy arrays (staged through the trainer's pinned buffers)."""
