@@ -337,27 +337,31 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
 
     FWD2_PROF(0);
     // ---- A: hidden spike words (unit order) to shared memory and to z_bits
-    // for the readout launch: warp w holds units w*32*HPT + HPT*lane + j, so
-    // word q of the warp takes bit i*HPT+j from ballot j's bit q*(32/HPT)+i ----
-    unsigned hm[HPT];
-#pragma unroll
-    for (int j = 0; j < HPT; ++j) hm[j] = __ballot_sync(SW_FULL_MASK, (h0 + j < H) && z[j] != 0.0f);
+    // for the readout launch: thread t holds units HPT*t + j, i.e. bits
+    // HPT*(t % (32/HPT)) + j of word t / (32/HPT); the 32/HPT threads of a
+    // word OR their bit groups together (butterfly) ----
     {
       uint32_t* zw = zw_step;
       zw_step += (int64_t)B * HW;
       if (HPT == 1) {
+        const unsigned hm = __ballot_sync(SW_FULL_MASK, h0 < H && z[0] != 0.0f);
         if (lane == 0 && warp < HW) {
-          zws[warp] = hm[0];
-          zw[warp] = hm[0];
+          zws[warp] = hm;
+          zw[warp] = hm;
         }
-      } else if (lane < HPT && warp * HPT + lane < HW) {
+      } else {
+        constexpr int TPW = 32 / HPT;   // threads per word
         uint32_t wd = 0;
 #pragma unroll
-        for (int j = 0; j < HPT; ++j)
+        for (int j = 0; j < HPT; ++j) wd |= (h0 + j < H && z[j] != 0.0f) ? 1u << j : 0u;
+        wd <<= HPT * (lane % TPW);
 #pragma unroll
-          for (int i = 0; i < 32 / HPT; ++i) wd |= ((hm[j] >> (lane * (32 / HPT) + i)) & 1u) << (i * HPT + j);
-        zws[warp * HPT + lane] = wd;
-        zw[warp * HPT + lane] = wd;
+        for (int o = 1; o < TPW; o <<= 1) wd |= __shfl_xor_sync(SW_FULL_MASK, wd, o);
+        const int q = tid / TPW;
+        if (lane % TPW == 0 && q < HW) {
+          zws[q] = wd;
+          zw[q] = wd;
+        }
       }
     }
     // zbar (old z) for the e-prop traces and the readout gradient
@@ -409,19 +413,59 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
     FWD2_PROF(6);
 
     // ---- D: group partials in order, ALIF step, surrogate ----
+    float aes[HPT], ars[HPT];
+    if (HPT > 1 && (H % HPT) == 0) {
+      // the thread's HPT consecutive units: one vector load / store per row
+      using VecT = typename std::conditional<HPT == 4, float4, float2>::type;
+      if (h0 < H) {
+        VecT e = *reinterpret_cast<const VecT*>(pin + h0), r = *reinterpret_cast<const VecT*>(prc + h0);
+        const VecT zero{};
+        *reinterpret_cast<VecT*>(pin + h0) = zero;
+        *reinterpret_cast<VecT*>(prc + h0) = zero;
+        float* ef = reinterpret_cast<float*>(&e);
+        float* rf = reinterpret_cast<float*>(&r);
+        for (int g = 1; g < G; ++g) {
+          VecT pe = *reinterpret_cast<const VecT*>(pin + g * H + h0);
+          VecT pr = *reinterpret_cast<const VecT*>(prc + g * H + h0);
+          *reinterpret_cast<VecT*>(pin + g * H + h0) = zero;
+          *reinterpret_cast<VecT*>(prc + g * H + h0) = zero;
+          const float* pef = reinterpret_cast<const float*>(&pe);
+          const float* prf = reinterpret_cast<const float*>(&pr);
+#pragma unroll
+          for (int j = 0; j < HPT; ++j) {
+            ef[j] = __fadd_rn(ef[j], pef[j]);
+            rf[j] = __fadd_rn(rf[j], prf[j]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < HPT; ++j) {
+          aes[j] = ef[j];
+          ars[j] = rf[j];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < HPT; ++j) {
+        const int h = h0 + j;
+        if (h >= H) continue;
+        float ae = pin[h], ar = prc[h];
+        pin[h] = 0.0f;
+        prc[h] = 0.0f;
+        for (int g = 1; g < G; ++g) {
+          ae = __fadd_rn(ae, pin[g * H + h]);
+          ar = __fadd_rn(ar, prc[g * H + h]);
+          pin[g * H + h] = 0.0f;
+          prc[g * H + h] = 0.0f;
+        }
+        aes[j] = ae;
+        ars[j] = ar;
+      }
+    }
 #pragma unroll
     for (int j = 0; j < HPT; ++j) {
       const int h = h0 + j;
       if (h >= H) continue;
-      float ae = pin[h], ar = prc[h];
-      pin[h] = 0.0f;
-      prc[h] = 0.0f;
-      for (int g = 1; g < G; ++g) {
-        ae = __fadd_rn(ae, pin[g * H + h]);
-        ar = __fadd_rn(ar, prc[g * H + h]);
-        pin[g * H + h] = 0.0f;
-        prc[g * H + h] = 0.0f;
-      }
+      const float ae = aes[j], ar = ars[j];
       const float thr_o = __fadd_rn(v_thr, __fmul_rn(beta, a[j]));
       const float cc = __fdiv_rn(__fsub_rn(v[j], thr_o), v_thr);
       const float r = __fsub_rn(1.0f, fabsf(cc));
