@@ -427,6 +427,35 @@ def test_grouped_readout_sums_from_spike_words(dev_lib, H, v0):
         assert dense > 0
 
 
+@pytest.mark.parametrize("H,p_spk", [(512, 0.05), (512, 1.0), (1024, 0.05), (1024, 1.0)])
+def test_grouped_forward_wide_layers_equal_single_steps(dev_lib, H, p_spk):
+    """Wide layers (2 / 4 units per thread, input and hidden groups on
+    separate warps): the grouped launch over 16 steps -- with the launch's
+    input-row lists prebuilt (sparse inputs) or, past their capacity (every
+    input spiking every step), selected per step -- equals 16 single-step
+    launches bit for bit (v, a, z)."""
+    import ctypes
+    from paper_2510_19764_b200 import _lib
+    from paper_2510_19764_b200.classifier import EPROP_BLOCK_STEPS as K
+    from paper_2510_19764_b200.classifier import EpropClassifierTrainer, SyntheticTask
+    task = SyntheticTask(num_classes=4, num_inputs=300, example_steps=K, seed=5)
+    trs = [EpropClassifierTrainer(task, hidden=H, batch_size=3, seed=5, deep_r=False, input_density=0.05,
+                                  recurrent_density=0.02, use_graph=False) for _ in range(2)]
+    rs = np.random.default_rng(5)
+    pin = (rs.random((3, task.num_inputs)) < p_spk).astype(np.float64)
+    for tr in trs:
+        tr._upload_batch(task.train_ids(0, tr.batch_size))
+        tr.p_in.copy_(torch.from_numpy(pin))
+        tr._prepare(False)
+    st = _lib.stream_ptr()
+    for t in range(K):
+        _lib.call("sw_clf_step", ctypes.byref(trs[0]._step_params(t)), st)
+    _lib.call("sw_clf_step", ctypes.byref(trs[1]._group_params(0, K)), st)
+    torch.cuda.synchronize()
+    for name in ("v", "a", "z"):
+        assert torch.equal(getattr(trs[0], name), getattr(trs[1], name)), name
+
+
 def test_pinned_host_inputs_equal_numpy_inputs(dev_lib):
     """train_batch from host inputs already in pinned memory (direct async
     copies) == from numpy arrays (staged through the trainer's pinned buffers)."""
