@@ -143,21 +143,6 @@ __host__ __device__ inline size_t fwd2_fixed_bytes(int H, int NI, int n_steps) {
   return o;
 }
 
-// the launch's ascending input-row lists, built once at the start (per step
-// a count, an offset and the 16-bit row ids, kPreList ids in all), when the
-// input words fit one warp: the per-step group selection then only scans the
-// hidden words (a launch with more input spikes keeps the per-step selection);
-// C2 forward+readout 109.7 -> 104.6 us per 16 steps
-constexpr int kPreList = 2048;
-__host__ __device__ inline size_t fwd2_prelist_bytes(int NI, int n_steps) {
-  return (((size_t)n_steps * 8 + (size_t)kPreList * 2) + 15) & ~(size_t)15;
-}
-__host__ __device__ inline bool fwd2_prelist(int H, int NI, int n_steps) {
-  // (layers up to 256 units select input and hidden rows in one scan of at
-  // most 32 words already: measured 1 us per 16 steps slower with the lists)
-  return H > 256 && (NI + 31) / 32 <= 32 && fwd2_fixed_bytes(H, NI, n_steps) + fwd2_prelist_bytes(NI, n_steps) <= 56 * 1024;
-}
-
 // rows [n*grp/G, n*(grp+1)/G) of the ascending set-bit list of words[0..nw)
 // (n = the total set bits) into out[0..), one warp; returns their count.
 // Up to 32 words: one load, one scan; more: a counting pass first.
@@ -313,11 +298,6 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
   uint32_t* zws = (uint32_t*)(smem_raw + o); o += (size_t)HW * 4;       // hidden spike words
   o = (o + 15) & ~(size_t)15;
   uint32_t* wsm = (uint32_t*)(smem_raw + o);   // [n_steps][in_words] spike words
-  o += (size_t)P.n_steps * P.in_words * 4;
-  bool pre = HPT > 1 && fwd2_prelist(H, NI, P.n_steps);   // (compiled out for H <= 256)
-  int* s_inn = (int*)(smem_raw + o);                       // [n_steps] input rows spiking
-  int* s_ino = s_inn + P.n_steps;                          // [n_steps] their offsets in s_inl
-  uint16_t* s_inl = (uint16_t*)(s_ino + P.n_steps);        // [kPreList] ascending ids, step by step
 
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -347,37 +327,6 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
   for (int x = tid; x < nsteps * P.in_words; x += kT2) {
     const int q = x / P.in_words, w = x - q * P.in_words;
     wsm[x] = __ldg(P.in_bits + ((int64_t)(P.t + q) * B + b) * P.in_words + w);
-  }
-  if (pre) {
-    // warp per step: the step's count, then (all counts known) its offset
-    // and its ascending ids
-    __syncthreads();
-    for (int q = warp; q < nsteps; q += NTH / 32) {
-      const uint32_t wd = lane < P.in_words ? wsm[q * P.in_words + lane] : 0u;
-      const int n = __reduce_add_sync(SW_FULL_MASK, __popc(wd));
-      if (lane == 0) s_inn[q] = n;
-    }
-    __syncthreads();
-    int total = 0;
-    for (int q = 0; q < nsteps; ++q) total += s_inn[q];
-    pre = total <= kPreList;   // block-uniform
-    if (pre) {
-      for (int q = warp; q < nsteps; q += NTH / 32) {
-        int off = 0;
-        for (int q2 = 0; q2 < q; ++q2) off += s_inn[q2];
-        const uint32_t wd = lane < P.in_words ? wsm[q * P.in_words + lane] : 0u;
-        const int c = __popc(wd);
-        int inc = c;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const int u = __shfl_up_sync(SW_FULL_MASK, inc, d);
-          if (lane >= d) inc += u;
-        }
-        uint16_t* out = s_inl + off + (inc - c);
-        for (uint32_t m = wd; m; m &= m - 1) *out++ = (uint16_t)(lane * 32 + __ffs(m) - 1);
-        if (lane == 0) s_ino[q] = off;
-      }
-    }
   }
 
   int cur = P.t % nslot;
@@ -433,15 +382,9 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
       // spare warps (H > 256: G = 4): the input groups on warps 0..G-1, the
       // hidden groups on warps G..2G-1 (separate partial rows, so the same sums)
       if (warp < G) {
-        if (pre) {
-          const int n = s_inn[s], a0 = n * warp / G, a1 = n * (warp + 1) / G;
-          sum_rows(s_inl + s_ino[s] + a0, a1 - a0, rlen, reinterpret_cast<const int2*>(P.in_tw),
-                   P.in_tw_stride, pin + warp * H, lane);
-        } else {
-          int* L = lists + warp * cap;
-          const int nin = group_rows(wsm + s * P.in_words, P.in_words, warp, G, L, lane);
-          sum_rows(L, nin, rlen, reinterpret_cast<const int2*>(P.in_tw), P.in_tw_stride, pin + warp * H, lane);
-        }
+        int* L = lists + warp * cap;
+        const int nin = group_rows(wsm + s * P.in_words, P.in_words, warp, G, L, lane);
+        sum_rows(L, nin, rlen, reinterpret_cast<const int2*>(P.in_tw), P.in_tw_stride, pin + warp * H, lane);
       } else if (warp < 2 * G) {
         const int g = warp - G;
         int* Lh = lists + g * cap + (NI + G - 1) / G + 1;
@@ -449,13 +392,6 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
         sum_rows(Lh, nhd, rlen + NI, reinterpret_cast<const int2*>(P.rec_tw), P.rec_tw_stride, prc + g * H,
                  lane);
       }
-    } else if (warp < G && pre) {
-      const int n = s_inn[s], a0 = n * warp / G, a1 = n * (warp + 1) / G;
-      int* Lh = lists + warp * cap;
-      const int nhd = group_rows(zws, HW, warp, G, Lh, lane);
-      sum_rows(s_inl + s_ino[s] + a0, a1 - a0, rlen, reinterpret_cast<const int2*>(P.in_tw), P.in_tw_stride,
-               pin + warp * H, lane);
-      sum_rows(Lh, nhd, rlen + NI, reinterpret_cast<const int2*>(P.rec_tw), P.rec_tw_stride, prc + warp * H, lane);
     } else if (warp < G) {
       int* L = lists + warp * cap;
       int nin, nhd;
@@ -782,9 +718,8 @@ int clf_fwd2_launch(const sw_clf_step_t* p, void* stream) {
       p->in_words != (NI + 31) / 32)
     return SW_ERR_INVALID_ARG;
   // 4 replica blocks per SM (512 replicas in one wave): <= 56 KB each
-  size_t smem = fwd2_fixed_bytes(H, NI, p->n_steps);
+  const size_t smem = fwd2_fixed_bytes(H, NI, p->n_steps);
   if (smem > 56 * 1024) return SW_ERR_INVALID_ARG;
-  if (fwd2_prelist(H, NI, p->n_steps)) smem += fwd2_prelist_bytes(NI, p->n_steps);
   cudaStream_t st = (cudaStream_t)stream;
   if (H <= 256) return launch_fwd2<256, 1, 8>(p, smem, st);
   if (H <= 512) return launch_fwd2<256, 2, 4>(p, smem, st);

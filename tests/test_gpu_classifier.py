@@ -430,9 +430,8 @@ def test_grouped_readout_sums_from_spike_words(dev_lib, H, v0):
 @pytest.mark.parametrize("H,p_spk", [(512, 0.05), (512, 1.0), (1024, 0.05), (1024, 1.0)])
 def test_grouped_forward_wide_layers_equal_single_steps(dev_lib, H, p_spk):
     """Wide layers (2 / 4 units per thread, input and hidden groups on
-    separate warps): the grouped launch over 16 steps -- with the launch's
-    input-row lists prebuilt (sparse inputs) or, past their capacity (every
-    input spiking every step), selected per step -- equals 16 single-step
+    separate warps): the grouped launch over 16 steps, with sparse and with
+    saturated inputs (every input spiking every step), equals 16 single-step
     launches bit for bit (v, a, z)."""
     import ctypes
     from paper_2510_19764_b200 import _lib
