@@ -135,8 +135,9 @@ __host__ __device__ inline int fwd2_list_cap(int H, int NI) {
 __host__ __device__ inline size_t fwd2_fixed_bytes(int H, int NI, int n_steps) {
   const size_t NT = (size_t)NI + H;
   size_t o = (size_t)2 * fwd2_groups(H) * H * 4;   // input / hidden partial rows
-  o += NT * 4;                                      // rlen
-  o += (size_t)fwd2_groups(H) * fwd2_list_cap(H, NI) * 4;   // per-group row lists
+  o += NT * 2;                                      // rlen (16-bit)
+  o += (size_t)fwd2_groups(H) * fwd2_list_cap(H, NI) * 2;   // per-group row lists (16-bit ids)
+  o = (o + 3) & ~(size_t)3;
   o += (size_t)((H + 31) / 32) * 4;                 // hidden spike words
   o = (o + 15) & ~(size_t)15;
   o += (size_t)n_steps * ((NI + 31) / 32) * 4;      // the launch's input spike words
@@ -146,7 +147,7 @@ __host__ __device__ inline size_t fwd2_fixed_bytes(int H, int NI, int n_steps) {
 // rows [n*grp/G, n*(grp+1)/G) of the ascending set-bit list of words[0..nw)
 // (n = the total set bits) into out[0..), one warp; returns their count.
 // Up to 32 words: one load, one scan; more: a counting pass first.
-__device__ __forceinline__ int group_rows(const uint32_t* words, int nw, int grp, int G, int* out, int lane) {
+__device__ __forceinline__ int group_rows(const uint32_t* words, int nw, int grp, int G, uint16_t* out, int lane) {
   if (nw <= 32) {
     const uint32_t wd = lane < nw ? words[lane] : 0u;
     const int c = __popc(wd);
@@ -196,7 +197,7 @@ __device__ __forceinline__ int group_rows(const uint32_t* words, int nw, int grp
 // both selections at once when the input and the hidden words fit one warp
 // (lanes [0, nwi) input words, [nwi, nwi + nwh) hidden words): one scan
 __device__ __forceinline__ void group_rows2(const uint32_t* wi, int nwi, const uint32_t* wh, int nwh, int grp,
-                                            int G, int* out_in, int& nin, int*& out_h, int& nh, int lane) {
+                                            int G, uint16_t* out_in, int& nin, uint16_t*& out_h, int& nh, int lane) {
   const bool is_in = lane < nwi;
   const uint32_t wd = is_in ? wi[lane] : (lane < nwi + nwh ? wh[lane - nwi] : 0u);
   const int c = __popc(wd);
@@ -214,7 +215,7 @@ __device__ __forceinline__ void group_rows2(const uint32_t* wi, int nwi, const u
   // this lane's word: ranks within its own list, its group's range
   const int r0 = is_in ? a0 : h0, r1 = is_in ? a1 : h1;
   int rank = inc - c - (is_in ? 0 : n_in);
-  int* out = is_in ? out_in - a0 : out_h - h0;
+  uint16_t* out = is_in ? out_in - a0 : out_h - h0;
   const int wbase = (is_in ? lane : lane - nwi) * 32;
   if (rank < r1 && rank + c > r0) {
     uint32_t m = wd;
@@ -233,7 +234,7 @@ __device__ __forceinline__ void group_rows2(const uint32_t* wi, int nwi, const u
 // batch and, unless a row of the batch is longer than 32, the long-row code.
 constexpr int kRowsAhead = 4;
 template <typename IDX>
-__device__ __forceinline__ void sum_rows(const IDX* list, int nr, const int* rl, const int2* base, int stride,
+__device__ __forceinline__ void sum_rows(const IDX* list, int nr, const uint16_t* rl, const int2* base, int stride,
                                          float* dst, int lane) {
   for (int r = 0; r < nr; r += kRowsAhead) {
     const int cnt = min(kRowsAhead, nr - r);
@@ -293,8 +294,11 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
   size_t o = 0;
   float* pin = (float*)(smem_raw + o);   o += (size_t)G * H * 4;
   float* prc = (float*)(smem_raw + o);   o += (size_t)G * H * 4;
-  int* rlen = (int*)(smem_raw + o);      o += (size_t)NT * 4;
-  int* lists = (int*)(smem_raw + o);     o += (size_t)G * cap * 4;      // [G][cap] this step's rows
+  // 16-bit row lengths and ids: a smaller block leaves more L1 to the e-prop
+  // pass running next to it
+  uint16_t* rlen = (uint16_t*)(smem_raw + o);   o += (size_t)NT * 2;
+  uint16_t* lists = (uint16_t*)(smem_raw + o);  o += (size_t)G * cap * 2;   // [G][cap] this step's rows
+  o = (o + 3) & ~(size_t)3;
   uint32_t* zws = (uint32_t*)(smem_raw + o); o += (size_t)HW * 4;       // hidden spike words
   o = (o + 15) & ~(size_t)15;
   uint32_t* wsm = (uint32_t*)(smem_raw + o);   // [n_steps][in_words] spike words
@@ -307,7 +311,7 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
   const int nsteps = P.n_steps;
 
   for (int x = tid; x < NT; x += kT2)
-    rlen[x] = (x < NI) ? __ldg(P.in_row_length + x) : __ldg(P.rec_row_length + (x - NI));
+    rlen[x] = (uint16_t)((x < NI) ? __ldg(P.in_row_length + x) : __ldg(P.rec_row_length + (x - NI)));
   for (int x = tid; x < G * H; x += kT2) { pin[x] = 0.0f; prc[x] = 0.0f; }
   const int prev = ((P.t - 1) % nslot + nslot) % nslot;
   const float* zin0 = P.zbar + prev * B * H;
@@ -382,20 +386,20 @@ __global__ void __launch_bounds__(NTH, 1024 / NTH) k_clf_fwd2(sw_clf_step_t P) {
       // spare warps (H > 256: G = 4): the input groups on warps 0..G-1, the
       // hidden groups on warps G..2G-1 (separate partial rows, so the same sums)
       if (warp < G) {
-        int* L = lists + warp * cap;
+        uint16_t* L = lists + warp * cap;
         const int nin = group_rows(wsm + s * P.in_words, P.in_words, warp, G, L, lane);
         sum_rows(L, nin, rlen, reinterpret_cast<const int2*>(P.in_tw), P.in_tw_stride, pin + warp * H, lane);
       } else if (warp < 2 * G) {
         const int g = warp - G;
-        int* Lh = lists + g * cap + (NI + G - 1) / G + 1;
+        uint16_t* Lh = lists + g * cap + (NI + G - 1) / G + 1;
         const int nhd = group_rows(zws, HW, g, G, Lh, lane);
         sum_rows(Lh, nhd, rlen + NI, reinterpret_cast<const int2*>(P.rec_tw), P.rec_tw_stride, prc + g * H,
                  lane);
       }
     } else if (warp < G) {
-      int* L = lists + warp * cap;
+      uint16_t* L = lists + warp * cap;
       int nin, nhd;
-      int* Lh;
+      uint16_t* Lh;
       if (P.in_words + HW <= 32) {
         group_rows2(wsm + s * P.in_words, P.in_words, zws, HW, warp, G, L, nin, Lh, nhd, lane);
       } else {
@@ -714,6 +718,7 @@ extern "C" int sw_clf_inputs(const sw_clf_inputs_t* p, void* stream) {
 int clf_fwd2_launch(const sw_clf_step_t* p, void* stream) {
   const int H = p->hidden, NI = p->num_inputs, C = p->num_classes;
   if (p->n_steps < 1 || p->n_steps > 2 * SW_EPROP_MAX_BLOCK || !p->in_bits || !p->z_bits || !p->in_tw || !p->rec_tw || H < 1 || H > 1024 || NI < 1 || C < 1 ||
+      NI + H > 65535 || p->in_tw_stride > 65535 || p->rec_tw_stride > 65535 ||   // 16-bit ids and lengths
       readout_smem(p->n_steps, H, C) > 200 * 1024 ||
       p->in_words != (NI + 31) / 32)
     return SW_ERR_INVALID_ARG;
