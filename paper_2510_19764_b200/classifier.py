@@ -204,8 +204,9 @@ class EpropClassifierTrainer:
         self.deep_r_enabled = deep_r
         self.params = AlifParams()
         self.use_graph = use_graph
-        # graph replays overlap group g's e-prop pass with group g+1's forward launch
-        self.overlap = True
+        # graph replays overlap group g's e-prop pass with group g+1's forward
+        # launch (SW_CLF_OVERLAP=0: one stream, measurement)
+        self.overlap = os.environ.get("SW_CLF_OVERLAP", "1") != "0"
         self.pg = process_group
         # replicas handled by this rank (batch-DP); default: all of them
         self.local = local_batch if local_batch is not None else slice(0, batch_size)
